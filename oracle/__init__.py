@@ -1,0 +1,169 @@
+"""CPU oracle for the Spira SpC hot path (arXiv 2511.20834) -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (its ``cpu_baseline``
+leg and ``--impl reference``) may import this package.  The product path
+(``paper_2511_20834_b200``) never imports it and shares no code with it.
+
+The arithmetic lives in plain C (``spc_oracle.c``); this module only marshals numpy
+arrays through ctypes.  Every function follows a definition in PAPER.md:
+
+=====================  =============================================================
+``sort_coords``        canonical lexicographic order (§5.2)
+``pack``               A1 biased-field key (§5.3 + DESIGN.md readings A3/A5)
+``downsample``         Eq. (1) V_q = floor(V_p/s_q)*s_q, unique (§2.1)
+``offsets``            Delta(K, s_p) lexicographic, dz fastest
+``kmap``               M[i,k] = j iff p_j = q_i + delta_k, hash-set lookup
+``conv``               Eq. (2) in fp64, OS or WS loop order
+``conv_rows``          Eq. (2) for sampled output rows (full-size sampled parity)
+=====================  =============================================================
+
+Parity pins: tests/test_oracle_pins.py (brute force, closed forms, paper examples,
+torch conv3d in float64).  No function here is "parity unpinned".
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "spc_oracle.c")
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc (plain C11, -O2, no OpenMP)."""
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < max(
+            os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "spc_oracle.h"))):
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", _SRC, "-o", _LIB_PATH])
+    return _LIB_PATH
+
+
+def _L():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_LIB_PATH)
+        P = ctypes.c_void_p
+        I64 = ctypes.c_int64
+        I = ctypes.c_int
+        lib.orc_sort_coords.argtypes = [P, I64, P, P]
+        lib.orc_sort_coords.restype = I64
+        lib.orc_pack.argtypes = [P, I64, I, I, I, I, P]
+        lib.orc_pack.restype = I64
+        lib.orc_round_down.argtypes = [ctypes.c_int32, ctypes.c_int32]
+        lib.orc_round_down.restype = ctypes.c_int32
+        lib.orc_downsample.argtypes = [P, I64, ctypes.c_int32, P]
+        lib.orc_downsample.restype = I64
+        lib.orc_offsets.argtypes = [I, I, P, P]
+        lib.orc_offsets.restype = I
+        lib.orc_kmap.argtypes = [P, I64, P, I64, I, I, I, P, I64]
+        lib.orc_kmap.restype = I64
+        lib.orc_conv.argtypes = [P, I64, P, I64, I, I, I, P, I, P, I, P, I]
+        lib.orc_conv.restype = I64
+        lib.orc_conv_rows.argtypes = [P, I64, P, P, I64, I, I, I, P, I, P, I, P]
+        lib.orc_conv_rows.restype = I64
+        _lib = lib
+    return _lib
+
+
+def _c(a, dtype):
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+def _p(a):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def sort_coords(coords):
+    """-> (sorted int32 [n,4], perm int32 [n] with sorted[p] = coords[perm[p]], n_dups)."""
+    c = _c(coords, np.int32).reshape(-1, 4)
+    n = c.shape[0]
+    s = np.empty_like(c)
+    perm = np.empty(n, np.int32)
+    d = _L().orc_sort_coords(_p(c), n, _p(s), _p(perm))
+    return s, perm, int(d)
+
+
+def pack(coords, bits):
+    """bits = (Bb, Bx, By, Bz) -> (uint64 keys [n], n_out_of_range)."""
+    c = _c(coords, np.int32).reshape(-1, 4)
+    keys = np.empty(c.shape[0], np.uint64)
+    bad = _L().orc_pack(_p(c), c.shape[0], int(bits[0]), int(bits[1]), int(bits[2]), int(bits[3]),
+                        _p(keys))
+    return keys, int(bad)
+
+
+def round_down(v: int, s: int) -> int:
+    return int(_L().orc_round_down(int(v), int(s)))
+
+
+def downsample(coords, s: int):
+    """Eq. (1): sorted unique int32 [m, 4]."""
+    c = _c(coords, np.int32).reshape(-1, 4)
+    out = np.empty_like(c)
+    m = _L().orc_downsample(_p(c), c.shape[0], int(s), _p(out))
+    if m < 0:
+        raise ValueError("orc_downsample failed")
+    return out[:m].copy()
+
+
+def offsets(K: int, spacing: int = 1):
+    """-> (int32 [K^3, 3] offsets, int32 [K^3] L1 norm in units of ``spacing``)."""
+    kv = K ** 3
+    off = np.empty((kv, 3), np.int32)
+    l1 = np.empty(kv, np.int32)
+    r = _L().orc_offsets(int(K), int(spacing), _p(off), _p(l1))
+    if r < 0:
+        raise ValueError("even or non-positive K")
+    return off, l1
+
+
+def kmap(in_coords, out_coords, K: int, spacing: int, transposed: bool = False):
+    """-> int32 [nnz, 3] triples (k, out_index, in_index), lexicographically sorted."""
+    a = _c(in_coords, np.int32).reshape(-1, 4)
+    b = _c(out_coords, np.int32).reshape(-1, 4)
+    L = _L()
+    nnz = L.orc_kmap(_p(a), a.shape[0], _p(b), b.shape[0], int(K), int(spacing), int(transposed),
+                     None, 0)
+    if nnz < 0:
+        raise ValueError("orc_kmap failed")
+    t = np.empty((nnz, 3), np.int32)
+    L.orc_kmap(_p(a), a.shape[0], _p(b), b.shape[0], int(K), int(spacing), int(transposed), _p(t), nnz)
+    return t
+
+
+def conv(in_coords, out_coords, K: int, spacing: int, F_in, W, transposed: bool = False,
+         order: str = "os"):
+    """Eq. (2) in fp64.  F_in [n_in, c_in], W [K^3, c_in, c_out] -> F_out [n_out, c_out]."""
+    a = _c(in_coords, np.int32).reshape(-1, 4)
+    b = _c(out_coords, np.int32).reshape(-1, 4)
+    F = _c(F_in, np.float64)
+    Wd = _c(W, np.float64)
+    c_in, c_out = Wd.shape[1], Wd.shape[2]
+    assert F.shape == (a.shape[0], c_in) and Wd.shape[0] == K ** 3
+    out = np.empty((b.shape[0], c_out), np.float64)
+    r = _L().orc_conv(_p(a), a.shape[0], _p(b), b.shape[0], int(K), int(spacing), int(transposed),
+                      _p(F), c_in, _p(Wd), c_out, _p(out), 0 if order == "os" else 1)
+    if r < 0:
+        raise ValueError("orc_conv failed")
+    return out
+
+
+def conv_rows(in_coords, out_coords, rows, K: int, spacing: int, F_in, W, transposed: bool = False):
+    """Eq. (2) for output rows ``rows`` only -> [len(rows), c_out] fp64."""
+    a = _c(in_coords, np.int32).reshape(-1, 4)
+    b = _c(out_coords, np.int32).reshape(-1, 4)
+    rr = _c(rows, np.int64)
+    F = _c(F_in, np.float64)
+    Wd = _c(W, np.float64)
+    c_in, c_out = Wd.shape[1], Wd.shape[2]
+    out = np.empty((rr.shape[0], c_out), np.float64)
+    r = _L().orc_conv_rows(_p(a), a.shape[0], _p(b), _p(rr), rr.shape[0], int(K), int(spacing),
+                           int(transposed), _p(F), c_in, _p(Wd), c_out, _p(out))
+    if r < 0:
+        raise ValueError("orc_conv_rows failed")
+    return out

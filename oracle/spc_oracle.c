@@ -1,0 +1,292 @@
+/*
+ * spc_oracle.c -- plain, slow, obviously-correct CPU oracle for the Spira SpC hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY (see spc_oracle.h).  Nothing here is shared with, or
+ * reachable from, the CUDA product path.  Each function cites the passage of
+ * /root/reference/PAPER.md (P:line) it writes out.
+ *
+ * Build: gcc -O2 -std=c11 -fPIC -shared spc_oracle.c -o liboracle.so
+ */
+#include "spc_oracle.h"
+
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------------------------
+ * canonical order (§5.2 "lexicographically sorted")
+ * ---------------------------------------------------------------------------------- */
+
+typedef struct {
+    int32_t c[4];
+    int32_t row;
+} orc_row;
+
+static int cmp_tuple(const int32_t *a, const int32_t *b) {
+    for (int d = 0; d < 4; ++d) {
+        if (a[d] < b[d]) return -1;
+        if (a[d] > b[d]) return 1;
+    }
+    return 0;
+}
+
+static int cmp_row(const void *pa, const void *pb) {
+    const orc_row *a = (const orc_row *)pa, *b = (const orc_row *)pb;
+    int c = cmp_tuple(a->c, b->c);
+    if (c) return c;
+    return (a->row > b->row) - (a->row < b->row); /* stable */
+}
+
+int64_t orc_sort_coords(const int32_t *coords, int64_t n, int32_t *sorted_out, int32_t *perm_out) {
+    if (n < 0) return -1;
+    orc_row *r = (orc_row *)malloc(sizeof(orc_row) * (size_t)(n ? n : 1));
+    if (!r) return -1;
+    for (int64_t i = 0; i < n; ++i) {
+        memcpy(r[i].c, coords + 4 * i, 16);
+        r[i].row = (int32_t)i;
+    }
+    qsort(r, (size_t)n, sizeof(orc_row), cmp_row);
+    int64_t dups = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        if (sorted_out) memcpy(sorted_out + 4 * i, r[i].c, 16);
+        if (perm_out) perm_out[i] = r[i].row;
+        if (i > 0 && cmp_tuple(r[i - 1].c, r[i].c) == 0) ++dups;
+    }
+    free(r);
+    return dups;
+}
+
+/* ------------------------------------------------------------------------------------
+ * packed key (§5.3: x in the most significant bits, then y, then z; the
+ * batch field above x and the 2^(b-1) bias per field are DESIGN.md readings A3/A5)
+ * ---------------------------------------------------------------------------------- */
+
+int64_t orc_pack(const int32_t *coords, int64_t n, int bits_b, int bits_x, int bits_y, int bits_z,
+                 uint64_t *keys_out) {
+    int64_t bad = 0;
+    const int bits[4] = {bits_b, bits_x, bits_y, bits_z};
+    for (int64_t i = 0; i < n; ++i) {
+        uint64_t key = 0;
+        int ok = 1;
+        for (int d = 0; d < 4; ++d) {
+            int64_t v = coords[4 * i + d];
+            int64_t field = (d == 0) ? v : v + ((int64_t)1 << (bits[d] - 1));
+            if (field < 0 || field >= ((int64_t)1 << bits[d])) ok = 0;
+            key = (key << bits[d]) | (uint64_t)field;   /* b first => b ends up highest */
+        }
+        if (!ok) { key = 0; ++bad; }
+        keys_out[i] = key;
+    }
+    return bad;
+}
+
+/* ------------------------------------------------------------------------------------
+ * Eq. (1) downsampling (§2.1), floor toward -infinity
+ * ---------------------------------------------------------------------------------- */
+
+int32_t orc_round_down(int32_t v, int32_t s) {
+    int32_t q = v / s;                  /* C division truncates toward zero */
+    if ((v % s != 0) && (v < 0)) q -= 1; /* ... so step down for negative non-multiples */
+    return q * s;
+}
+
+int64_t orc_downsample(const int32_t *coords, int64_t n, int32_t s, int32_t *out) {
+    if (s <= 0) return -1;
+    int32_t *tmp = (int32_t *)malloc(16 * (size_t)(n ? n : 1));
+    if (!tmp) return -1;
+    for (int64_t i = 0; i < n; ++i) {
+        tmp[4 * i + 0] = coords[4 * i + 0];
+        for (int d = 1; d < 4; ++d) tmp[4 * i + d] = orc_round_down(coords[4 * i + d], s);
+    }
+    int32_t *sorted = (int32_t *)malloc(16 * (size_t)(n ? n : 1));
+    if (!sorted) { free(tmp); return -1; }
+    orc_sort_coords(tmp, n, sorted, NULL);
+    int64_t m = 0;
+    for (int64_t i = 0; i < n; ++i) {       /* keep only the unique values */
+        if (i > 0 && cmp_tuple(sorted + 4 * (i - 1), sorted + 4 * i) == 0) continue;
+        memcpy(out + 4 * m, sorted + 4 * i, 16);
+        ++m;
+    }
+    free(tmp);
+    free(sorted);
+    return m;
+}
+
+/* ------------------------------------------------------------------------------------
+ * Delta(K, s_p) (§2.1) in the order of P:266 (group 0 = (-1,-1,-1),(-1,-1,0),(-1,-1,1))
+ * ---------------------------------------------------------------------------------- */
+
+int orc_offsets(int K, int spacing, int32_t *off_out, int32_t *l1_units_out) {
+    if (K <= 0 || (K % 2) == 0) return -1;
+    int r = (K - 1) / 2, k = 0;
+    for (int ex = -r; ex <= r; ++ex)
+        for (int ey = -r; ey <= r; ++ey)
+            for (int ez = -r; ez <= r; ++ez, ++k) {
+                if (off_out) {
+                    off_out[3 * k + 0] = ex * spacing;
+                    off_out[3 * k + 1] = ey * spacing;
+                    off_out[3 * k + 2] = ez * spacing;
+                }
+                if (l1_units_out) l1_units_out[k] = abs(ex) + abs(ey) + abs(ez);
+            }
+    return k;
+}
+
+/* ------------------------------------------------------------------------------------
+ * hash set over (b,x,y,z) tuples -> canonical index (open addressing, linear probing)
+ * ---------------------------------------------------------------------------------- */
+
+typedef struct {
+    const int32_t *coords;
+    int64_t *slot; /* index+1, 0 = empty */
+    uint64_t mask;
+} orc_hash;
+
+static uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+static uint64_t hash_tuple(const int32_t *t) {
+    uint64_t h = 0x9e3779b97f4a7c15ULL;
+    for (int d = 0; d < 4; ++d) h = mix64(h ^ (uint64_t)(uint32_t)t[d]);
+    return h;
+}
+
+static int hash_build(orc_hash *h, const int32_t *coords, int64_t n) {
+    uint64_t cap = 16;
+    while (cap < (uint64_t)(2 * n + 1)) cap <<= 1;
+    h->slot = (int64_t *)calloc(cap, sizeof(int64_t));
+    if (!h->slot) return -1;
+    h->mask = cap - 1;
+    h->coords = coords;
+    for (int64_t i = 0; i < n; ++i) {
+        uint64_t p = hash_tuple(coords + 4 * i) & h->mask;
+        while (h->slot[p]) p = (p + 1) & h->mask;
+        h->slot[p] = i + 1;
+    }
+    return 0;
+}
+
+static int64_t hash_find(const orc_hash *h, const int32_t *t) {
+    uint64_t p = hash_tuple(t) & h->mask;
+    while (h->slot[p]) {
+        int64_t j = h->slot[p] - 1;
+        if (cmp_tuple(h->coords + 4 * j, t) == 0) return j;
+        p = (p + 1) & h->mask;
+    }
+    return -1;
+}
+
+/* the query of Eq. (2)'s indicator: p = q + delta_k (normal) or p = q - delta_k (transposed) */
+static void make_query(const int32_t *q, const int32_t *off, int transposed, int32_t *t) {
+    t[0] = q[0];
+    for (int d = 0; d < 3; ++d) t[d + 1] = transposed ? q[d + 1] - off[d] : q[d + 1] + off[d];
+}
+
+/* ------------------------------------------------------------------------------------
+ * kernel map (§2.2): M[i,k] = j if q_i + delta_k matches p_j, else -1
+ * ---------------------------------------------------------------------------------- */
+
+int64_t orc_kmap(const int32_t *in_coords, int64_t n_in, const int32_t *out_coords, int64_t n_out,
+                 int K, int spacing, int transposed, int32_t *triples, int64_t cap) {
+    int kv = orc_offsets(K, 1, NULL, NULL);
+    if (kv < 0) return -1;
+    int32_t *off = (int32_t *)malloc(sizeof(int32_t) * 3 * (size_t)kv);
+    orc_offsets(K, spacing, off, NULL);
+    orc_hash h;
+    if (hash_build(&h, in_coords, n_in)) { free(off); return -1; }
+    int64_t nnz = 0;
+    int32_t t[4];
+    for (int k = 0; k < kv; ++k)
+        for (int64_t i = 0; i < n_out; ++i) {
+            make_query(out_coords + 4 * i, off + 3 * k, transposed, t);
+            int64_t j = hash_find(&h, t);
+            if (j < 0) continue;
+            if (triples && nnz < cap) {
+                triples[3 * nnz + 0] = k;
+                triples[3 * nnz + 1] = (int32_t)i;
+                triples[3 * nnz + 2] = (int32_t)j;
+            }
+            ++nnz;
+        }
+    free(h.slot);
+    free(off);
+    return nnz;
+}
+
+/* ------------------------------------------------------------------------------------
+ * Eq. (2) in fp64 (§2.1), two loop orders (§2.2 dataflows)
+ * ---------------------------------------------------------------------------------- */
+
+static void axpy_row(const double *f, int c_in, const double *Wk, int c_out, double *acc) {
+    for (int ci = 0; ci < c_in; ++ci) {
+        double a = f[ci];
+        const double *w = Wk + (size_t)ci * c_out;
+        for (int co = 0; co < c_out; ++co) acc[co] += a * w[co];
+    }
+}
+
+int64_t orc_conv(const int32_t *in_coords, int64_t n_in, const int32_t *out_coords, int64_t n_out,
+                 int K, int spacing, int transposed, const double *F_in, int c_in,
+                 const double *W, int c_out, double *F_out, int order) {
+    int kv = orc_offsets(K, 1, NULL, NULL);
+    if (kv < 0 || c_in <= 0 || c_out <= 0) return -1;
+    int32_t *off = (int32_t *)malloc(sizeof(int32_t) * 3 * (size_t)kv);
+    orc_offsets(K, spacing, off, NULL);
+    orc_hash h;
+    if (hash_build(&h, in_coords, n_in)) { free(off); return -1; }
+    memset(F_out, 0, sizeof(double) * (size_t)n_out * (size_t)c_out);
+    int64_t nnz = 0;
+    int32_t t[4];
+    if (order == 0) { /* output-stationary: each output row finished before the next */
+        for (int64_t i = 0; i < n_out; ++i)
+            for (int k = 0; k < kv; ++k) {
+                make_query(out_coords + 4 * i, off + 3 * k, transposed, t);
+                int64_t j = hash_find(&h, t);
+                if (j < 0) continue;
+                axpy_row(F_in + (size_t)j * c_in, c_in, W + (size_t)k * c_in * c_out, c_out,
+                         F_out + (size_t)i * c_out);
+                ++nnz;
+            }
+    } else {          /* weight-stationary: one offset at a time, partial sums merged */
+        for (int k = 0; k < kv; ++k)
+            for (int64_t i = 0; i < n_out; ++i) {
+                make_query(out_coords + 4 * i, off + 3 * k, transposed, t);
+                int64_t j = hash_find(&h, t);
+                if (j < 0) continue;
+                axpy_row(F_in + (size_t)j * c_in, c_in, W + (size_t)k * c_in * c_out, c_out,
+                         F_out + (size_t)i * c_out);
+                ++nnz;
+            }
+    }
+    free(h.slot);
+    free(off);
+    return nnz;
+}
+
+int64_t orc_conv_rows(const int32_t *in_coords, int64_t n_in, const int32_t *out_coords,
+                      const int64_t *rows, int64_t n_rows, int K, int spacing, int transposed,
+                      const double *F_in, int c_in, const double *W, int c_out, double *F_out) {
+    int kv = orc_offsets(K, 1, NULL, NULL);
+    if (kv < 0) return -1;
+    int32_t *off = (int32_t *)malloc(sizeof(int32_t) * 3 * (size_t)kv);
+    orc_offsets(K, spacing, off, NULL);
+    orc_hash h;
+    if (hash_build(&h, in_coords, n_in)) { free(off); return -1; }
+    memset(F_out, 0, sizeof(double) * (size_t)n_rows * (size_t)c_out);
+    int64_t nnz = 0;
+    int32_t t[4];
+    for (int64_t r = 0; r < n_rows; ++r)
+        for (int k = 0; k < kv; ++k) {
+            make_query(out_coords + 4 * rows[r], off + 3 * k, transposed, t);
+            int64_t j = hash_find(&h, t);
+            if (j < 0) continue;
+            axpy_row(F_in + (size_t)j * c_in, c_in, W + (size_t)k * c_in * c_out, c_out,
+                     F_out + (size_t)r * c_out);
+            ++nnz;
+        }
+    free(h.slot);
+    free(off);
+    return nnz;
+}
