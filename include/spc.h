@@ -1,0 +1,268 @@
+/*
+ * spc.h -- C ABI of libspc, the B200 (sm_100a) sparse-convolution hot path of
+ * "Accelerating Sparse Convolutions in Voxel-Based Point Cloud Networks" (Spira,
+ * arXiv 2511.20834).  Citations "P:N" are lines of that paper's PAPER.md.
+ *
+ * Conventions (all entry points)
+ * ------------------------------
+ * - Pointers are DEVICE pointers unless the name ends in _host.  No torch types.
+ * - `stream` is a cudaStream_t passed as void*.  Every call only ENQUEUES work on it
+ *   and returns without a device synchronisation; none of them allocates device
+ *   memory: persistent buffers and scratch ("ws") come from the caller.
+ * - Host-detectable errors return a status != SPC_OK immediately (nothing enqueued);
+ *   spc_last_error_detail() names the offending argument.  Data-dependent errors are
+ *   OR-ed by the kernels into a caller-owned device uint32 status word (SPC_FLAG_*),
+ *   readable after the caller synchronises the stream.
+ * - Sizes: every function that consumes a data-dependent count takes the host
+ *   CAPACITY (n_*) and an optional device pointer to the actual count (n_*_dev, may be
+ *   NULL = the capacity is the count).  This keeps whole network passes free of host
+ *   syncs and CUDA-graph capturable.
+ * - Index spaces: voxel i of a coordinate set is its position in the SORTED key array
+ *   (canonical lexicographic order).
+ * - Weights: user layout [K^3][C_in][C_out], offset index k in lexicographic (dx,dy,dz)
+ *   order with dz fastest (k of -delta = K^3-1-k).
+ * - Kernels are compiled for sm_100a only.  There is no CPU fallback.
+ */
+#ifndef SPC_H
+#define SPC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPC_VERSION 1
+
+typedef enum {
+    SPC_OK = 0,
+    SPC_ERR_INVALID_ARG = 1,   /* null pointer, negative size, bad dtype/shape/alignment */
+    SPC_ERR_UNSUPPORTED = 2,   /* even K, channels not a multiple of 16, ...            */
+    SPC_ERR_RANGE = 3,         /* coordinate extent does not fit the key fields          */
+    SPC_ERR_DUPLICATE = 4,
+    SPC_ERR_UNSORTED = 5,
+    SPC_ERR_CAPACITY = 6,
+    SPC_ERR_WORKSPACE = 7,     /* ws smaller than *_workspace_size()                     */
+    SPC_ERR_CUDA = 8           /* a CUDA runtime call failed (detail has the message)    */
+} spc_status;
+
+/* device status word bits (set by kernels with atomicOr) */
+#define SPC_FLAG_RANGE 0x1u      /* pack: coordinate outside its key field            */
+#define SPC_FLAG_DUPLICATE 0x2u  /* pack_sort: two equal keys                         */
+#define SPC_FLAG_UNSORTED 0x4u   /* build_kmap (SPC_KMAP_CHECK_SORTED): input unsorted */
+#define SPC_FLAG_CAPACITY 0x8u   /* a device count exceeded its host capacity          */
+
+typedef enum { SPC_F32 = 0, SPC_F16 = 1, SPC_BF16 = 2 } spc_dtype;
+
+const char *spc_status_string(int status);
+const char *spc_last_error_detail(void);   /* thread-local, last failing call */
+int spc_version(void);
+size_t spc_kmap_struct_bytes(void);        /* sizeof(spc_kmap), for binding layout checks */
+
+/* ================================================================================
+ * A1  Packed keys (§5.3)
+ *
+ * key = b << (Bx+By+Bz) | (x + 2^(Bx-1)) << (By+Bz) | (y + 2^(By-1)) << Bz | (z + 2^(Bz-1))
+ *
+ * z is least significant, x most significant among the spatial fields; the
+ * batch index b (unsigned, never offset or masked) sits above x (reading A5).
+ * Each spatial field is biased by 2^(B-1), a multiple of every stride 2^m with
+ * m <= B-1, so AND-masking the biased field equals floor rounding of the signed
+ * coordinate (reading A3) and packed(q) + packed(delta) = packed(q + delta)
+ * as long as q + delta stays inside the field (headroom, reading A4).
+ * Bb + Bx + By + Bz <= 62 (two bits are reserved for the level tag of spc_downsample).
+ * ================================================================================ */
+typedef struct {
+    int32_t bits_b, bits_x, bits_y, bits_z;
+} spc_pack_spec;
+
+/* Smallest field widths such that every coordinate in [lo_host, hi_host] (per axis),
+ * every output of downsampling up to stride max_out_stride (rounding moves a
+ * coordinate down by at most max_out_stride-1) and every query q +- delta with
+ * |delta| <= max_reach stays inside its biased field (reading A4/A6).
+ * Returns SPC_ERR_RANGE (detail names the axis and the bits required) if the total
+ * exceeds 62 bits. */
+spc_status spc_plan_pack(const int32_t lo_host[3], const int32_t hi_host[3], int32_t n_batch,
+                         int32_t max_out_stride, int32_t max_reach, spc_pack_spec *out_host);
+
+/* packed(delta) = dx*2^(By+Bz) + dy*2^Bz + dz as a signed 64-bit word. */
+int64_t spc_pack_offset(spc_pack_spec spec, int32_t dx, int32_t dy, int32_t dz);
+
+/* The downsample mask of P:327-336 for s_q = 2^m: per spatial field B-m ones then m
+ * zeros; the batch field all ones (read as bitwise AND, reading A1). */
+uint64_t spc_downsample_mask(spc_pack_spec spec, int32_t m);
+
+/* ================================================================================
+ * A1+A2  spc_pack_sort -- pack int32 coordinates and sort them once
+ *
+ * coords   : int32 [n][4] rows (b, x, y, z), any row order.
+ * keys_out : uint64 [n], ascending (stable LSD radix sort over the used key bits).
+ * perm_out : int32 [n] (nullable): keys_out[p] = key(coords[perm_out[p]]).  The caller
+ *            gathers feature rows with it (spc_gather_rows).
+ * status   : device uint32, OR-ed with SPC_FLAG_RANGE (a coordinate does not fit; its
+ *            key is undefined) and SPC_FLAG_DUPLICATE (two rows with equal coordinates).
+ * ws       : >= spc_pack_sort_workspace_size(n) bytes.
+ * ================================================================================ */
+size_t spc_pack_sort_workspace_size(int64_t n);
+spc_status spc_pack_sort(const int32_t *coords, int64_t n, spc_pack_spec spec, uint64_t *keys_out,
+                         int32_t *perm_out, uint32_t *status, void *ws, size_t ws_bytes, void *stream);
+
+/* dst row r = src row perm[r] (row_bytes each, 16-byte aligned rows).  n_dev nullable. */
+spc_status spc_gather_rows(const void *src, int64_t ld_src_bytes, const int32_t *perm, int64_t n,
+                           const int64_t *n_dev, int32_t row_bytes, void *dst, int64_t ld_dst_bytes,
+                           void *stream);
+
+/* ================================================================================
+ * A3  spc_downsample -- Eq. (1) for several output strides at once, each computed
+ *     directly from V_0 (Eq. (3)):  V_m = unique(sort(V_0 & mask_m)).
+ *
+ * The AND mask is not monotone across fields, so every level is re-sorted (reading A2).
+ * All levels go through ONE radix sort of n_levels*n tagged keys and one unique
+ * compaction (the grouped phase 1 of network-wide indexing).
+ *
+ * keys      : sorted unique V_0 keys, capacity n (n_dev: actual count, nullable).
+ * log2_stride_host[l] : m_l in 1..min(B)-1 (output stride 2^m_l).  n_levels <= 4.
+ * level_keys: device buffer [n_levels][n]; level l's sorted unique keys are written at
+ *             level_keys + l*n.
+ * level_n_dev: device int64 [n_levels], the unique counts.
+ * ================================================================================ */
+size_t spc_downsample_workspace_size(int64_t n, int32_t n_levels);
+spc_status spc_downsample(const uint64_t *keys, int64_t n, const int64_t *n_dev, spc_pack_spec spec,
+                          int32_t n_levels, const int32_t *log2_stride_host, uint64_t *level_keys,
+                          int64_t *level_n_dev, void *ws, size_t ws_bytes, void *stream);
+
+/* ================================================================================
+ * A4-A8  Kernel maps (§2.2, z-delta search P:253-301 §5.2, layouts P:393-421)
+ * ================================================================================ */
+typedef struct {
+    int32_t kernel_size;   /* K, odd                                            */
+    int32_t stride;        /* layer stride s_l: 1 = submanifold (V_q = V_p), 2 = down/up */
+    int32_t dilation;      /* d >= 1 (offsets delta * d; not in the paper, reading A11)  */
+    int32_t tensor_stride; /* stride of the FINE coordinate set (s_p of a normal layer,  */
+                           /* s_q of a transposed one); offsets are spaced by           */
+                           /* tensor_stride * dilation (Delta(K, s_p))           */
+    int32_t transposed;    /* 0: out = V_{ts*stride} (coarse) or V_ts (submanifold), in = V_ts */
+                           /* 1: out = V_ts (fine), in = V_{ts*stride} (coarse); triple  */
+                           /*    (k,i,j) iff in_j = out_i - delta_k  (reading A8)        */
+} spc_geom;
+
+/* dataflow threshold t: offset k is dense (output-stationary) iff
+ * L1(e_k) < t, where e_k in {-r..r}^3 is the offset in units of tensor_stride*dilation
+ * (reading A15).  t = 0: all weight-stationary; t >= 3r+1 (SPC_T_ALL_OS): all OS. */
+#define SPC_T_ALL_OS (-1)
+#define SPC_T_ALL_WS 0
+
+#define SPC_KMAP_HALVE_SYMMETRIC 0x1u /* submanifold: store WS pairs of k < centre only */
+#define SPC_KMAP_CHECK_SORTED 0x2u    /* debug: flag unsorted / duplicate input keys          */
+#define SPC_KMAP_COUNT_SEARCHES 0x4u  /* debug: count binary searches and scan probes        */
+
+#define SPC_MAX_KVOL 125
+
+/* A built kernel map: plain struct of device pointers into one caller buffer.
+ * OS part : os_table[i*k_dense + c] = input index of output i at dense offset
+ *           dense_k[c], or -1 (unfiltered |V_q| x K_dense layout).
+ * WS part : list l (offset list_k[l]) holds counts_dev[list_k[l]] pairs
+ *           ws_pairs[(l*n_out + p)*2 + {0,1}] = (in j, out i), no sentinels, in no
+ *           particular order (reading A16).  With halving, list_mirror[l] != 0 means
+ *           the pair also stands for (in i, out j) at offset K^3-1-list_k[l].
+ * counts_dev: int32 [2*SPC_MAX_KVOL].  counts_dev[k] = matches found for offset k (the
+ *           K^3 auxiliary buffer; offsets skipped by halving read 0 -- their count
+ *           equals that of K^3-1-k by symmetry); counts_dev[SPC_MAX_KVOL + l] = pairs
+ *           stored in WS list l.
+ * tile_mask_dev (OS): bit c of word [tile*words + c/32] set iff some output of the
+ *           128-row tile has a match at dense offset c (empty chunks are skipped). */
+typedef struct {
+    spc_geom geom;
+    int32_t t;            /* effective threshold (SPC_T_ALL_OS resolved)            */
+    int32_t k_vol;        /* K^3                                                    */
+    int32_t k_dense;      /* number of dense offsets (OS part)                      */
+    int32_t n_lists;      /* number of stored WS lists                              */
+    int32_t halved;       /* 1 if SPC_KMAP_HALVE_SYMMETRIC was applied              */
+    int32_t tile_words;   /* 32-bit words per OS tile in tile_mask_dev              */
+    int64_t n_in;         /* capacities (host)                                      */
+    int64_t n_out;
+    const int64_t *n_in_dev;   /* actual counts (device, nullable)                  */
+    const int64_t *n_out_dev;
+    const uint64_t *in_keys;
+    const uint64_t *out_keys;
+    int32_t *os_table;
+    int32_t *ws_pairs;
+    int32_t *counts_dev;
+    uint32_t *tile_mask_dev;
+    unsigned long long *search_stats_dev; /* [2]: binary searches, scan probes (or NULL) */
+    int16_t dense_k[SPC_MAX_KVOL];
+    int16_t list_k[SPC_MAX_KVOL];
+    int8_t list_mirror[SPC_MAX_KVOL];
+} spc_kmap;
+
+/* bytes of the caller buffer spc_build_kmap needs for this geometry/t/capacities */
+size_t spc_kmap_bytes(spc_geom geom, int32_t t, uint32_t flags, int64_t n_in, int64_t n_out);
+
+/* Build the kernel map of one layer with the one-shot z-delta search:
+ * per (output i, offset group g) one lower_bound of q_i + packed(delta_anchor(g)) in
+ * the sorted input keys, then a forward cursor scan for the group's other members in
+ * ascending query order.  Both layouts are written straight from the search (OS block
+ * staged per 128-output tile, WS pairs compacted with warp-aggregated atomics): there
+ * is no separate transpose / filter post-processing pass.
+ * in_keys/out_keys: sorted unique keys of the input/output coordinate sets (the same
+ * array for a submanifold layer).  buf: >= spc_kmap_bytes() bytes, 256-byte aligned.
+ * status: device uint32 (nullable) for SPC_FLAG_UNSORTED / SPC_FLAG_CAPACITY.
+ * kmap_out_host: filled with pointers into buf. */
+spc_status spc_build_kmap(const uint64_t *in_keys, int64_t n_in, const int64_t *n_in_dev,
+                          const uint64_t *out_keys, int64_t n_out, const int64_t *n_out_dev,
+                          spc_pack_spec spec, spc_geom geom, int32_t t, uint32_t flags, void *buf,
+                          size_t buf_bytes, uint32_t *status, spc_kmap *kmap_out_host, void *stream);
+
+/* Export the map as (k, out, in) int32 triples sorted lexicographically (parity
+ * tooling; [sync]: synchronises `stream`).  Returns the nnz in *nnz_host; writes at
+ * most cap triples to triples_host (host memory). */
+spc_status spc_kmap_export(const spc_kmap *kmap, int32_t *triples_host, int64_t cap, int64_t *nnz_host,
+                           void *stream);
+
+/* ================================================================================
+ * A9-A12  spc_conv_forward -- Eq. (2) with the output-stationary part (dense offsets)
+ * and the weight-stationary part (sparse offsets) of the map.
+ *
+ * f_in   : [n_in][ld_in] elements of in_dtype, first c_in used.  Rows 16-byte aligned.
+ * weight : prepared weights (spc_prepare_weight) for this (K^3, c_in, c_out, in_dtype).
+ * f_out  : [n_out][ld_out] elements of out_dtype, first c_out written.
+ * residual: nullable, [n_out][ld_res] elements of out_dtype, added to the result.
+ * Arithmetic: f16/bf16 inputs -> tcgen05.mma kind::f16 with fp32 accumulation in TMEM;
+ * f32 inputs -> FFMA (fp32).  c_in, c_out multiples of 16 (f16/bf16) or 4 (f32),
+ * c_out <= 256 per weight tile (larger c_out is tiled).
+ * ws     : >= spc_conv_workspace_size() bytes (fp32 accumulator of the WS part).
+ * ================================================================================ */
+size_t spc_prepared_weight_bytes(int32_t k_vol, int32_t c_in, int32_t c_out, int32_t in_dtype);
+spc_status spc_prepare_weight(const void *weight, int32_t k_vol, int32_t c_in, int32_t c_out,
+                              int32_t in_dtype, void *prepared, void *stream);
+size_t spc_conv_workspace_size(const spc_kmap *kmap, int32_t c_out, int32_t out_dtype);
+spc_status spc_conv_forward(const spc_kmap *kmap, const void *f_in, int64_t ld_in, int32_t in_dtype,
+                            int32_t c_in, const void *weight, int32_t c_out, void *f_out,
+                            int64_t ld_out, int32_t out_dtype, const void *residual, int64_t ld_res,
+                            void *ws, size_t ws_bytes, void *stream);
+
+/* ================================================================================
+ * A13  spc_network_kmaps -- network-wide voxel indexing (§5.5)
+ *
+ * Phase 1: every coordinate level V_m = floor(V_0/2^m)2^m, m = 1..n_levels-1, from V_0
+ * directly (Eq. (3)) in one grouped spc_downsample.  Phase 2: every map of `geoms`
+ * (identical (geom, t, flags) entries are built once and shared).  No host sync:
+ * level counts stay on the device.
+ * level_keys_out: device buffer [n_levels][n0]; level 0 = a copy of v0_keys.
+ * level_n_dev   : device int64 [n_levels].
+ * maps_out_host : [n_maps] kmap structs (pointers into ws).
+ * ws            : >= spc_network_workspace_size(...).
+ * ================================================================================ */
+size_t spc_network_workspace_size(int64_t n0, int32_t n_levels, const spc_geom *geoms_host,
+                                  const int32_t *t_host, const uint32_t *flags_host, int32_t n_maps);
+spc_status spc_network_kmaps(const uint64_t *v0_keys, int64_t n0, const int64_t *n0_dev,
+                             spc_pack_spec spec, int32_t n_levels, const spc_geom *geoms_host,
+                             const int32_t *t_host, const uint32_t *flags_host, int32_t n_maps,
+                             uint64_t *level_keys_out, int64_t *level_n_dev, spc_kmap *maps_out_host,
+                             uint32_t *status, void *ws, size_t ws_bytes, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPC_H */

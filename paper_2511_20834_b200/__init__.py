@@ -1,0 +1,365 @@
+"""paper_2511_20834_b200 -- B200 (sm_100a) sparse-convolution hot path of Spira
+(arXiv 2511.20834), behind the C ABI declared in include/spc.h.
+
+This module is the thin Python binding: it only marshals torch tensors (device memory,
+streams) into the C entry points of ``libspc.so`` -- every step of the hot path runs in
+the library's CUDA kernels.  Function names follow the C ABI.  There is no CPU fallback:
+if ``libspc.so`` is missing or no CUDA device is present the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libspc.so")
+
+SPC_OK = 0
+SPC_F32, SPC_F16, SPC_BF16 = 0, 1, 2
+SPC_T_ALL_OS = -1
+SPC_T_ALL_WS = 0
+SPC_KMAP_HALVE_SYMMETRIC = 0x1
+SPC_KMAP_CHECK_SORTED = 0x2
+SPC_KMAP_COUNT_SEARCHES = 0x4
+SPC_FLAG_RANGE, SPC_FLAG_DUPLICATE, SPC_FLAG_UNSORTED, SPC_FLAG_CAPACITY = 1, 2, 4, 8
+SPC_MAX_KVOL = 125
+
+_DT = {torch.float32: SPC_F32, torch.float16: SPC_F16, torch.bfloat16: SPC_BF16}
+_TORCH_DT = {v: k for k, v in _DT.items()}
+
+
+class SpcError(RuntimeError):
+    pass
+
+
+class PackSpec(ctypes.Structure):
+    _fields_ = [("bits_b", ctypes.c_int32), ("bits_x", ctypes.c_int32), ("bits_y", ctypes.c_int32),
+                ("bits_z", ctypes.c_int32)]
+
+    def used_bits(self) -> int:
+        return self.bits_b + self.bits_x + self.bits_y + self.bits_z
+
+    def astuple(self):
+        return (self.bits_b, self.bits_x, self.bits_y, self.bits_z)
+
+    def __repr__(self):
+        return f"PackSpec{self.astuple()}"
+
+
+class Geom(ctypes.Structure):
+    _fields_ = [("kernel_size", ctypes.c_int32), ("stride", ctypes.c_int32), ("dilation", ctypes.c_int32),
+                ("tensor_stride", ctypes.c_int32), ("transposed", ctypes.c_int32)]
+
+    def __init__(self, kernel_size=3, stride=1, dilation=1, tensor_stride=1, transposed=0):
+        super().__init__(kernel_size, stride, dilation, tensor_stride, int(transposed))
+
+    def key(self):
+        return (self.kernel_size, self.stride, self.dilation, self.tensor_stride, self.transposed)
+
+    def __repr__(self):
+        return "Geom(K=%d, s=%d, d=%d, ts=%d, tr=%d)" % self.key()
+
+
+class _Kmap(ctypes.Structure):
+    _fields_ = [("geom", Geom), ("t", ctypes.c_int32), ("k_vol", ctypes.c_int32), ("k_dense", ctypes.c_int32),
+                ("n_lists", ctypes.c_int32), ("halved", ctypes.c_int32), ("tile_words", ctypes.c_int32),
+                ("n_in", ctypes.c_int64), ("n_out", ctypes.c_int64),
+                ("n_in_dev", ctypes.c_void_p), ("n_out_dev", ctypes.c_void_p),
+                ("in_keys", ctypes.c_void_p), ("out_keys", ctypes.c_void_p),
+                ("os_table", ctypes.c_void_p), ("ws_pairs", ctypes.c_void_p), ("counts_dev", ctypes.c_void_p),
+                ("tile_mask_dev", ctypes.c_void_p), ("search_stats_dev", ctypes.c_void_p),
+                ("dense_k", ctypes.c_int16 * SPC_MAX_KVOL), ("list_k", ctypes.c_int16 * SPC_MAX_KVOL),
+                ("list_mirror", ctypes.c_int8 * SPC_MAX_KVOL)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libspc.so (built by __graft_entry__.build() / paper_2511_20834_b200.build)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise SpcError(f"{LIB_PATH} not built: run python -m paper_2511_20834_b200.build")
+        L = ctypes.CDLL(LIB_PATH)
+        P, I32, I64, U32, SZ = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_size_t
+        sig = {
+            "spc_status_string": ([ctypes.c_int], ctypes.c_char_p),
+            "spc_last_error_detail": ([], ctypes.c_char_p),
+            "spc_version": ([], ctypes.c_int),
+            "spc_kmap_struct_bytes": ([], SZ),
+            "spc_plan_pack": ([P, P, I32, I32, I32, ctypes.POINTER(PackSpec)], ctypes.c_int),
+            "spc_pack_offset": ([PackSpec, I32, I32, I32], I64),
+            "spc_downsample_mask": ([PackSpec, I32], ctypes.c_uint64),
+            "spc_pack_sort_workspace_size": ([I64], SZ),
+            "spc_pack_sort": ([P, I64, PackSpec, P, P, P, P, SZ, P], ctypes.c_int),
+            "spc_gather_rows": ([P, I64, P, I64, P, I32, P, I64, P], ctypes.c_int),
+            "spc_downsample_workspace_size": ([I64, I32], SZ),
+            "spc_downsample": ([P, I64, P, PackSpec, I32, P, P, P, P, SZ, P], ctypes.c_int),
+            "spc_kmap_bytes": ([Geom, I32, U32, I64, I64], SZ),
+            "spc_build_kmap": ([P, I64, P, P, I64, P, PackSpec, Geom, I32, U32, P, SZ, P,
+                                ctypes.POINTER(_Kmap), P], ctypes.c_int),
+            "spc_kmap_export": ([ctypes.POINTER(_Kmap), P, I64, ctypes.POINTER(I64), P], ctypes.c_int),
+            "spc_prepared_weight_bytes": ([I32, I32, I32, I32], SZ),
+            "spc_prepare_weight": ([P, I32, I32, I32, I32, P, P], ctypes.c_int),
+            "spc_conv_workspace_size": ([ctypes.POINTER(_Kmap), I32, I32], SZ),
+            "spc_conv_forward": ([ctypes.POINTER(_Kmap), P, I64, I32, I32, P, I32, P, I64, I32, P, I64, P, SZ, P],
+                                 ctypes.c_int),
+            "spc_network_workspace_size": ([I64, I32, P, P, P, I32], SZ),
+            "spc_network_kmaps": ([P, I64, P, PackSpec, I32, P, P, P, I32, P, P, P, P, P, SZ, P], ctypes.c_int),
+        }
+        for name, (args, res) in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = L
+    return _lib
+
+
+def _check(status: int, what: str):
+    if status != SPC_OK:
+        L = lib()
+        raise SpcError(f"{what}: {L.spc_status_string(status).decode()}: {L.spc_last_error_detail().decode()}")
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ws(nbytes: int, device) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+
+
+# ---------------------------------------------------------------------------------------
+# A1/A2
+# ---------------------------------------------------------------------------------------
+
+def spc_plan_pack(lo, hi, n_batch: int = 1, max_out_stride: int = 1, max_reach: int = 0) -> PackSpec:
+    spec = PackSpec()
+    lo_a = (ctypes.c_int32 * 3)(*[int(v) for v in lo])
+    hi_a = (ctypes.c_int32 * 3)(*[int(v) for v in hi])
+    _check(lib().spc_plan_pack(lo_a, hi_a, int(n_batch), int(max_out_stride), int(max_reach), ctypes.byref(spec)),
+           "spc_plan_pack")
+    return spec
+
+
+def spc_pack_offset(spec: PackSpec, dx: int, dy: int, dz: int) -> int:
+    return int(lib().spc_pack_offset(spec, int(dx), int(dy), int(dz)))
+
+
+def spc_downsample_mask(spec: PackSpec, m: int) -> int:
+    return int(lib().spc_downsample_mask(spec, int(m)))
+
+
+def spc_pack_sort(coords: torch.Tensor, spec: PackSpec, status: torch.Tensor | None = None, stream=None,
+                  keys_out=None, perm_out=None, ws=None):
+    """coords int32 [n,4] (b,x,y,z) on the GPU -> (keys uint64-as-int64 [n], perm int32 [n], status uint32[1])."""
+    assert coords.is_cuda and coords.dtype == torch.int32 and coords.is_contiguous() and coords.shape[-1] == 4
+    n = coords.shape[0]
+    dev = coords.device
+    keys = keys_out if keys_out is not None else torch.empty(n, dtype=torch.int64, device=dev)
+    perm = perm_out if perm_out is not None else torch.empty(n, dtype=torch.int32, device=dev)
+    if status is None:
+        status = torch.zeros(1, dtype=torch.int32, device=dev)
+    L = lib()
+    wsb = int(L.spc_pack_sort_workspace_size(n))
+    if ws is None or ws.numel() < wsb:
+        ws = _ws(wsb, dev)
+    _check(L.spc_pack_sort(_ptr(coords), n, spec, _ptr(keys), _ptr(perm), _ptr(status), _ptr(ws), ws.numel(),
+                           _stream(stream)), "spc_pack_sort")
+    return keys, perm, status
+
+
+def spc_gather_rows(src: torch.Tensor, perm: torch.Tensor, out: torch.Tensor | None = None, n_dev=None,
+                    stream=None) -> torch.Tensor:
+    """out[r] = src[perm[r]] (rows of a 2-D tensor; row bytes multiple of 16)."""
+    n = perm.shape[0]
+    if out is None:
+        out = torch.empty((n,) + tuple(src.shape[1:]), dtype=src.dtype, device=src.device)
+    row_bytes = src[0].numel() * src.element_size() if src.shape[0] else out[0].numel() * out.element_size()
+    _check(lib().spc_gather_rows(_ptr(src), src.stride(0) * src.element_size(), _ptr(perm), n, _ptr(n_dev),
+                                 row_bytes, _ptr(out), out.stride(0) * out.element_size(), _stream(stream)),
+           "spc_gather_rows")
+    return out
+
+
+# ---------------------------------------------------------------------------------------
+# A3
+# ---------------------------------------------------------------------------------------
+
+def spc_downsample(keys: torch.Tensor, spec: PackSpec, log2_strides, n_dev=None, stream=None):
+    """Sorted unique keys -> (level_keys int64 [L, n] (row l valid up to level_n[l]), level_n int64 [L])."""
+    n = keys.shape[0]
+    L_ = len(log2_strides)
+    dev = keys.device
+    out = torch.empty((L_, n), dtype=torch.int64, device=dev)
+    level_n = torch.empty(L_, dtype=torch.int64, device=dev)
+    m = (ctypes.c_int32 * L_)(*[int(v) for v in log2_strides])
+    L = lib()
+    ws = _ws(L.spc_downsample_workspace_size(n, L_), dev)
+    _check(L.spc_downsample(_ptr(keys), n, _ptr(n_dev), spec, L_, m, _ptr(out), _ptr(level_n), _ptr(ws), ws.numel(),
+                            _stream(stream)), "spc_downsample")
+    return out, level_n
+
+
+# ---------------------------------------------------------------------------------------
+# A4-A8
+# ---------------------------------------------------------------------------------------
+
+class KernelMap:
+    """A built kernel map: the C struct plus the torch buffer that owns its memory."""
+
+    def __init__(self, struct: _Kmap, buf: torch.Tensor, keepalive=()):
+        self.c = struct
+        self.buf = buf
+        self._keep = keepalive
+
+    @property
+    def k_dense(self):
+        return self.c.k_dense
+
+    @property
+    def n_lists(self):
+        return self.c.n_lists
+
+    @property
+    def k_vol(self):
+        return self.c.k_vol
+
+    @property
+    def n_out(self):
+        return self.c.n_out
+
+    @property
+    def dense_k(self):
+        return [self.c.dense_k[i] for i in range(self.c.k_dense)]
+
+    @property
+    def list_k(self):
+        return [self.c.list_k[i] for i in range(self.c.n_lists)]
+
+    def _view(self, ptr, count, dtype):
+        off = ptr - self.buf.data_ptr()
+        es = torch.empty((), dtype=dtype).element_size()
+        return self.buf[off:off + count * es].view(dtype)
+
+    def os_table(self) -> torch.Tensor:
+        return self._view(self.c.os_table, self.c.n_out * self.c.k_dense, torch.int32).view(self.c.n_out,
+                                                                                              self.c.k_dense)
+
+    def counts(self) -> torch.Tensor:
+        return self._view(self.c.counts_dev, 2 * SPC_MAX_KVOL, torch.int32)
+
+    def search_stats(self) -> torch.Tensor | None:
+        if not self.c.search_stats_dev:
+            return None
+        return self._view(self.c.search_stats_dev, 2, torch.int64)
+
+    def ws_pairs(self, l: int) -> torch.Tensor:
+        cnt = int(self.counts()[SPC_MAX_KVOL + l].item())
+        base = self.c.ws_pairs + l * self.c.n_out * 8
+        return self._view(base, 2 * cnt, torch.int32).view(cnt, 2)
+
+
+def spc_kmap_bytes(geom: Geom, t: int, flags: int, n_in: int, n_out: int) -> int:
+    return int(lib().spc_kmap_bytes(geom, int(t), int(flags), int(n_in), int(n_out)))
+
+
+def spc_build_kmap(in_keys: torch.Tensor, out_keys: torch.Tensor, spec: PackSpec, geom: Geom,
+                   t: int = SPC_T_ALL_OS, flags: int = 0, n_in_dev=None, n_out_dev=None, status=None,
+                   stream=None) -> KernelMap:
+    n_in, n_out = in_keys.shape[0], out_keys.shape[0]
+    nbytes = spc_kmap_bytes(geom, t, flags, n_in, n_out)
+    if nbytes == 0:
+        raise SpcError(f"spc_kmap_bytes: unsupported geometry {geom!r}")
+    buf = torch.empty(nbytes + 256, dtype=torch.uint8, device=in_keys.device)
+    off = (-buf.data_ptr()) % 256
+    buf = buf[off:off + nbytes]
+    km = _Kmap()
+    _check(lib().spc_build_kmap(_ptr(in_keys), n_in, _ptr(n_in_dev), _ptr(out_keys), n_out, _ptr(n_out_dev), spec,
+                                geom, int(t), int(flags), _ptr(buf), nbytes, _ptr(status), ctypes.byref(km),
+                                _stream(stream)), "spc_build_kmap")
+    return KernelMap(km, buf, (in_keys, out_keys, n_in_dev, n_out_dev))
+
+
+def spc_kmap_export(km: KernelMap, stream=None) -> np.ndarray:
+    """[sync] -> int32 [nnz, 3] (k, out, in) triples, lexicographically sorted."""
+    L = lib()
+    nnz = ctypes.c_int64(0)
+    _check(L.spc_kmap_export(ctypes.byref(km.c), None, 0, ctypes.byref(nnz), _stream(stream)), "spc_kmap_export")
+    out = np.empty((nnz.value, 3), dtype=np.int32)
+    _check(L.spc_kmap_export(ctypes.byref(km.c), out.ctypes.data_as(ctypes.c_void_p), nnz.value, ctypes.byref(nnz),
+                             _stream(stream)), "spc_kmap_export")
+    return out
+
+
+# ---------------------------------------------------------------------------------------
+# A9-A12
+# ---------------------------------------------------------------------------------------
+
+def spc_prepare_weight(weight: torch.Tensor, stream=None) -> torch.Tensor:
+    """weight [K^3, C_in, C_out] (f32/f16/bf16, on the GPU) -> prepared weight for spc_conv_forward."""
+    kv, ci, co = weight.shape
+    w = weight.contiguous()
+    dt = _DT[w.dtype]
+    out = torch.empty(w.numel(), dtype=w.dtype, device=w.device)
+    _check(lib().spc_prepare_weight(_ptr(w), kv, ci, co, dt, _ptr(out), _stream(stream)), "spc_prepare_weight")
+    return out
+
+
+def spc_conv_workspace_size(km: KernelMap, c_out: int, out_dtype=torch.float32) -> int:
+    return int(lib().spc_conv_workspace_size(ctypes.byref(km.c), int(c_out), _DT[out_dtype]))
+
+
+def spc_conv_forward(km: KernelMap, f_in: torch.Tensor, weight_prepared: torch.Tensor, c_in: int, c_out: int,
+                     out: torch.Tensor | None = None, out_dtype=None, residual: torch.Tensor | None = None,
+                     ws: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Eq. (2) for the map ``km``: f_in [n_in, >=c_in] (row stride = f_in.stride(0)) -> out [n_out, c_out]."""
+    out_dtype = out_dtype or (out.dtype if out is not None else f_in.dtype)
+    if out is None:
+        out = torch.empty((km.n_out, c_out), dtype=out_dtype, device=f_in.device)
+    need = spc_conv_workspace_size(km, c_out, out_dtype)
+    if ws is None or ws.numel() < need:
+        ws = _ws(need, f_in.device)
+    _check(lib().spc_conv_forward(ctypes.byref(km.c), _ptr(f_in), f_in.stride(0), _DT[f_in.dtype], int(c_in),
+                                  _ptr(weight_prepared), int(c_out), _ptr(out), out.stride(0), _DT[out.dtype],
+                                  _ptr(residual), residual.stride(0) if residual is not None else 0, _ptr(ws),
+                                  ws.numel(), _stream(stream)), "spc_conv_forward")
+    return out
+
+
+# ---------------------------------------------------------------------------------------
+# A13
+# ---------------------------------------------------------------------------------------
+
+def spc_network_kmaps(v0_keys: torch.Tensor, spec: PackSpec, n_levels: int, geoms, ts, flags=None, n0_dev=None,
+                      status=None, ws=None, stream=None):
+    """Network-wide indexing -> (level_keys [n_levels, n0], level_n [n_levels], [KernelMap per entry], ws)."""
+    n0 = v0_keys.shape[0]
+    dev = v0_keys.device
+    n = len(geoms)
+    G = (Geom * max(n, 1))(*geoms)
+    T = (ctypes.c_int32 * max(n, 1))(*[int(t) for t in ts])
+    F = (ctypes.c_uint32 * max(n, 1))(*[int(f) for f in (flags or [0] * n)])
+    L = lib()
+    need = int(L.spc_network_workspace_size(n0, n_levels, G, T, F, n))
+    if ws is None or ws.numel() < need + 256:
+        ws = torch.empty(need + 256, dtype=torch.uint8, device=dev)
+    off = (-ws.data_ptr()) % 256
+    wsa = ws[off:]
+    level_keys = torch.empty((n_levels, n0), dtype=torch.int64, device=dev)
+    level_n = torch.empty(n_levels, dtype=torch.int64, device=dev)
+    maps = (_Kmap * max(n, 1))()
+    _check(L.spc_network_kmaps(_ptr(v0_keys), n0, _ptr(n0_dev), spec, int(n_levels), G, T, F, n, _ptr(level_keys),
+                               _ptr(level_n), maps, _ptr(status), _ptr(wsa), wsa.numel(), _stream(stream)),
+           "spc_network_kmaps")
+    kms = [KernelMap(maps[i], wsa, (v0_keys, level_keys, level_n)) for i in range(n)]
+    return level_keys, level_n, kms, ws

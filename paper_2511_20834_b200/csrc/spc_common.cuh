@@ -1,0 +1,99 @@
+// spc_common.cuh -- internal helpers of libspc (not part of the C ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "spc.h"
+
+namespace spc {
+
+// ------------------------------------------------------------------------------------
+// host-side error plumbing
+// ------------------------------------------------------------------------------------
+void set_detail(const std::string &s);
+spc_status fail(spc_status st, const std::string &detail);
+spc_status cuda_fail(cudaError_t e, const char *what);
+
+#define SPC_CHECK_ARG(cond, msg)                                                         \
+    do {                                                                                 \
+        if (!(cond)) return ::spc::fail(SPC_ERR_INVALID_ARG, std::string(__func__) + ": " + (msg)); \
+    } while (0)
+
+#define SPC_CUDA(call)                                                                   \
+    do {                                                                                 \
+        cudaError_t _e = (call);                                                         \
+        if (_e != cudaSuccess) return ::spc::cuda_fail(_e, #call);                       \
+    } while (0)
+
+#define SPC_LAUNCH_CHECK(name)                                                           \
+    do {                                                                                 \
+        cudaError_t _e = cudaGetLastError();                                             \
+        if (_e != cudaSuccess) return ::spc::cuda_fail(_e, name);                        \
+    } while (0)
+
+__host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// simple bump allocator over a caller workspace
+struct Bump {
+    char *base;
+    size_t cap, used;
+    Bump(void *b, size_t c) : base(static_cast<char *>(b)), cap(c), used(0) {}
+    template <class T>
+    T *take(size_t count) {
+        used = align_up(used, 256);
+        T *p = reinterpret_cast<T *>(base + used);
+        used += count * sizeof(T);
+        return p;
+    }
+    bool ok() const { return used <= cap; }
+};
+// size-only twin of Bump
+struct Sizer {
+    size_t used = 0;
+    template <class T>
+    void take(size_t count) {
+        used = align_up(used, 256);
+        used += count * sizeof(T);
+    }
+};
+
+int num_sms();
+
+// ------------------------------------------------------------------------------------
+// device helpers
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ int64_t dev_count(int64_t cap, const int64_t *n_dev) {
+    if (!n_dev) return cap;
+    int64_t n = *n_dev;
+    return n < cap ? n : cap;
+}
+
+__device__ __forceinline__ unsigned lane_id() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%laneid;" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+    return r;
+}
+
+}  // namespace spc
+
+// internal entry points shared between translation units
+namespace spc {
+// radix sort of (keys, optional int32 values) over bits [0, n_bits); result in keys_out / vals_out
+size_t radix_sort_workspace(int64_t n, bool with_vals);
+spc_status radix_sort(const uint64_t *keys_in, const int32_t *vals_in /*nullable: identity*/, int64_t n,
+                      const int64_t *n_dev, int n_bits, uint64_t *keys_out, int32_t *vals_out /*nullable*/,
+                      void *ws, size_t ws_bytes, cudaStream_t st);
+}  // namespace spc

@@ -1,0 +1,763 @@
+// spc_conv.cu -- A9-A12 feature computation (Eq. 2) with the output-stationary
+// and weight-stationary dataflows and the hybrid split.
+//
+// f16/bf16 path: one persistent, warp-specialised tcgen05 kernel (k_conv_tc), launched
+// once for the OS part and once for the WS part of a map:
+//   warps 0-3  gather producers: one thread per tile row, cp.async 16-byte row segments
+//              (src-size 0 zero-fill for sentinel rows) into the UMMA K-major canonical
+//              layout, then fence.proxy.async + mbarrier arrive
+//   warp 8     weight producer: one 1-D bulk copy (TMA engine) per stage of the
+//              pre-tiled weight blob W_k[c-chunk] (spc_prepare_weight)
+//   warp 9     MMA issuer: tcgen05.mma kind::f16, M=128, N=C_out tile, K=16, fp32
+//              accumulator in TMEM (double-buffered across tiles), tcgen05.commit
+//   warps 4-7  epilogue: tcgen05.ld -> OS: plain stores (final dtype, fused residual, or
+//              fp32 accumulator); WS: red.global.add.v4.f32 scatter (P:132 atomics)
+// A tile of the OS part is 128 outputs x all dense offsets whose (tile, offset) chunk is
+// non-empty (tile mask from the map build); a tile of the WS part is 128 pairs of one
+// offset list (plus, for halved submanifold maps, the mirrored product).
+//
+// f32 path: FFMA kernel with the same tiling semantics (1e-5 accuracy bar; 1xTF32 cannot
+// meet it, reading A19).
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include "spc_common.cuh"
+#include "spc_ptx.cuh"
+
+namespace spc {
+
+constexpr int TC_THREADS = 320;
+constexpr int TC_BM = 128;
+constexpr int TC_SMEM_BUDGET = 225 * 1024;
+
+enum OutKind : int { OUT_FINAL = 0, OUT_F32_STORE = 1, OUT_F32_RED = 2 };
+
+struct ConvParams {
+    int mode;   // 0 = OS part, 1 = WS part
+    // map
+    const int32_t *os;
+    int k_dense;
+    const uint32_t *tile_mask;
+    int tile_words;
+    const int2 *pairs;
+    int64_t list_stride;
+    const int32_t *counts;   // [2*SPC_MAX_KVOL]
+    int n_lists;
+    int k_vol;
+    int64_t n_out_cap;
+    const int64_t *n_out_dev;
+    // operands
+    const char *f_in;
+    int64_t ld_in_bytes;
+    const char *wblob;
+    int n_chunks, n_ntiles, BK, BN;
+    uint32_t a_bytes, b_bytes;
+    int stages;
+    uint32_t tmem_cols;   // per accumulator stage (power of two >= 32)
+    uint32_t idesc;
+    // output
+    void *out;
+    int64_t ld_out;       // elements
+    int out_kind;
+    int out_dtype;        // for OUT_FINAL
+    const void *residual;
+    int64_t ld_res;
+    int16_t dense_k[SPC_MAX_KVOL];
+    int16_t list_k[SPC_MAX_KVOL];
+    int8_t list_mirror[SPC_MAX_KVOL];
+};
+
+struct TileInfo {
+    int64_t row0;   // first output (OS) or first pair (WS)
+    int rows;
+    int nt;         // C_out tile
+    int list, dir, k;
+    uint32_t mask[4];
+};
+
+// virtual tile v -> TileInfo; identical in every role (deterministic)
+__device__ __forceinline__ void decode_tile(const ConvParams &p, int64_t v, const int *list_prefix, int64_t n_out,
+                                            TileInfo &t) {
+    t.nt = (int)(v % p.n_ntiles);
+    const int64_t tv = v / p.n_ntiles;
+    if (p.mode == 0) {
+        t.row0 = tv * TC_BM;
+        t.rows = (int)imin64(TC_BM, n_out - t.row0);
+        t.list = t.dir = 0;
+        t.k = -1;
+        bool any = false;
+        for (int w = 0; w < 4; ++w) {
+            t.mask[w] = w < p.tile_words ? p.tile_mask[tv * p.tile_words + w] : 0u;
+            any |= t.mask[w] != 0;
+        }
+        if (!any) t.mask[0] = 1u;   // keep one (all-sentinel) step so the tile is written
+    } else {
+        int l = 0;
+        while (l + 1 < p.n_lists && list_prefix[l + 1] <= tv) ++l;
+        const int local = (int)(tv - list_prefix[l]);
+        const int cnt = p.counts[SPC_MAX_KVOL + l];
+        const int per = (cnt + TC_BM - 1) / TC_BM;
+        t.list = l;
+        t.dir = local / per;
+        const int tl = local - t.dir * per;
+        t.row0 = (int64_t)tl * TC_BM;
+        t.rows = min(TC_BM, cnt - tl * TC_BM);
+        t.k = t.dir ? p.k_vol - 1 - p.list_k[l] : p.list_k[l];
+        t.mask[0] = 1u;
+        t.mask[1] = t.mask[2] = t.mask[3] = 0u;
+    }
+}
+
+__device__ __forceinline__ int next_bit(const uint32_t (&m)[4], int from) {
+    for (int c = from; c < 128; ++c)
+        if (m[c >> 5] >> (c & 31) & 1u) return c;
+    return -1;
+}
+
+__device__ __forceinline__ float to_f(uint32_t u) { return __uint_as_float(u); }
+
+__device__ __forceinline__ uint32_t pack2(float a, float b, int dt) {
+    if (dt == SPC_BF16) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+        return *reinterpret_cast<uint32_t *>(&h);
+    }
+    __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t *>(&h);
+}
+__device__ __forceinline__ float2 unpack2(uint32_t u, int dt) {
+    if (dt == SPC_BF16) return __bfloat1622float2(*reinterpret_cast<__nv_bfloat162 *>(&u));
+    return __half22float2(*reinterpret_cast<__half2 *>(&u));
+}
+
+// store 'n' (16 or 32) fp32 values of one row to the output
+__device__ __forceinline__ void store_row(const ConvParams &p, int64_t row, int col, const uint32_t (&v)[32], int n) {
+    if (p.out_kind == OUT_FINAL && p.out_dtype != SPC_F32) {
+        uint32_t packed[16];
+        float res[32];
+        if (p.residual) {
+            const uint4 *rp = reinterpret_cast<const uint4 *>(static_cast<const uint16_t *>(p.residual) + row * p.ld_res + col);
+            for (int q = 0; q < n / 8; ++q) {
+                uint4 u = rp[q];
+                uint32_t w[4] = {u.x, u.y, u.z, u.w};
+                for (int e = 0; e < 4; ++e) {
+                    float2 f = unpack2(w[e], p.out_dtype);
+                    res[q * 8 + 2 * e] = f.x;
+                    res[q * 8 + 2 * e + 1] = f.y;
+                }
+            }
+        } else {
+            for (int e = 0; e < 32; ++e) res[e] = 0.f;
+        }
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+            if (2 * e < n) packed[e] = pack2(to_f(v[2 * e]) + res[2 * e], to_f(v[2 * e + 1]) + res[2 * e + 1], p.out_dtype);
+        uint4 *op = reinterpret_cast<uint4 *>(static_cast<uint16_t *>(p.out) + row * p.ld_out + col);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (q * 8 < n) op[q] = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+    } else {
+        float *op = static_cast<float *>(p.out) + row * p.ld_out + col;
+        const float *rp = (p.out_kind == OUT_FINAL && p.residual)
+                              ? static_cast<const float *>(p.residual) + row * p.ld_res + col
+                              : nullptr;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            if (q * 4 >= n) break;
+            float4 o = make_float4(to_f(v[4 * q]), to_f(v[4 * q + 1]), to_f(v[4 * q + 2]), to_f(v[4 * q + 3]));
+            if (rp) {
+                float4 r = reinterpret_cast<const float4 *>(rp)[q];
+                o.x += r.x; o.y += r.y; o.z += r.z; o.w += r.w;
+            }
+            reinterpret_cast<float4 *>(op)[q] = o;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant__ ConvParams p) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int S = p.stages;
+    uint8_t *sa = smem;
+    uint8_t *sb = smem + (size_t)S * p.a_bytes;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sb + (size_t)S * p.b_bytes);
+    uint64_t *full = bars, *empty = bars + S, *tfull = bars + 2 * S, *tempty = bars + 2 * S + 2;
+    uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 2 * S + 4);
+    int *list_prefix = reinterpret_cast<int *>(tmem_holder + 4);   // [SPC_MAX_KVOL + 1]
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t n_out = dev_count(p.n_out_cap, p.n_out_dev);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            ptx::mbar_init(ptx::smem_u32(&full[s]), TC_BM + 1);
+            ptx::mbar_init(ptx::smem_u32(&empty[s]), 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(ptx::smem_u32(&tfull[a]), 1);
+            ptx::mbar_init(ptx::smem_u32(&tempty[a]), 4);
+        }
+        ptx::fence_mbar_init();
+        ptx::fence_proxy_async();
+    }
+    if (warp == 9) ptx::tmem_alloc(ptx::smem_u32(tmem_holder), 2 * p.tmem_cols);
+    if (p.mode == 1 && warp == 0) {
+        // virtual-tile prefix over the WS lists (device-side counts, no host sync)
+        int carry = 0;
+        for (int base = 0; base < p.n_lists; base += 32) {
+            const int l = base + lane;
+            int v = 0;
+            if (l < p.n_lists) {
+                const int cnt = p.counts[SPC_MAX_KVOL + l];
+                v = ((cnt + TC_BM - 1) / TC_BM) * (p.list_mirror[l] ? 2 : 1);
+            }
+            int x = v;
+            for (int o = 1; o < 32; o <<= 1) {
+                int y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (l < p.n_lists) list_prefix[l] = carry + x - v;
+            carry += __shfl_sync(0xffffffffu, x, 31);
+        }
+        if (lane == 0) list_prefix[p.n_lists] = carry;
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder;
+
+    int64_t n_tiles;
+    if (p.mode == 0) n_tiles = ((n_out + TC_BM - 1) / TC_BM) * p.n_ntiles;
+    else n_tiles = (int64_t)list_prefix[p.n_lists] * p.n_ntiles;
+
+    const uint32_t lbo = 128, sbo = (uint32_t)p.BK * 16;
+
+    if (warp < 4) {
+        // ===================== gather producers (one thread per tile row) ==============
+        const int r = threadIdx.x;   // 0..127
+        const uint32_t a_row_off = (uint32_t)((r >> 3) * (p.BK * 16) + (r & 7) * 16);
+        const int nq = p.BK / 8;     // 16-byte pieces per row segment
+        uint32_t it = 0;             // global step counter
+        uint32_t pend_first = 0, pend = 0;   // un-arrived steps [pend_first, pend_first+pend)
+        const int LAG = S - 1 < 3 ? S - 1 : 3;
+        for (int64_t v = blockIdx.x; v < n_tiles; v += gridDim.x) {
+            TileInfo t;
+            decode_tile(p, v, list_prefix, n_out, t);
+            for (int c = next_bit(t.mask, 0); c >= 0; c = next_bit(t.mask, c + 1)) {
+                int32_t idx = -1;
+                if (r < t.rows) {
+                    if (p.mode == 0) idx = p.os[(t.row0 + r) * p.k_dense + c];
+                    else {
+                        const int2 pr = p.pairs[t.list * p.list_stride + t.row0 + r];
+                        idx = t.dir ? pr.y : pr.x;
+                    }
+                }
+                const char *src_row = idx >= 0 ? p.f_in + (int64_t)idx * p.ld_in_bytes : p.f_in;
+                const uint32_t sz = idx >= 0 ? 16u : 0u;
+                for (int cc = 0; cc < p.n_chunks; ++cc, ++it) {
+                    const int s = it % S;
+                    const uint32_t round = it / S;
+                    ptx::mbar_wait(ptx::smem_u32(&empty[s]), (round & 1) ^ 1);
+                    const uint32_t dst = ptx::smem_u32(sa + (size_t)s * p.a_bytes) + a_row_off;
+                    const char *src = src_row + (idx >= 0 ? cc * p.BK * 2 : 0);
+                    for (int q = 0; q < nq; ++q) ptx::cp_async_16(dst + q * 128, src + q * 16, sz);
+                    ptx::cp_async_commit();
+                    ++pend;
+                    if ((int)pend > LAG) {
+                        // the oldest pending step has landed once at most LAG groups are in flight
+                        if (LAG >= 3) ptx::cp_async_wait<3>();
+                        else if (LAG == 2) ptx::cp_async_wait<2>();
+                        else if (LAG == 1) ptx::cp_async_wait<1>();
+                        else ptx::cp_async_wait<0>();
+                        ptx::fence_proxy_async();
+                        ptx::mbar_arrive(ptx::smem_u32(&full[pend_first % S]));
+                        ++pend_first;
+                        --pend;
+                    }
+                }
+            }
+        }
+        ptx::cp_async_wait<0>();
+        ptx::fence_proxy_async();
+        while (pend) {
+            ptx::mbar_arrive(ptx::smem_u32(&full[pend_first % S]));
+            ++pend_first;
+            --pend;
+        }
+    } else if (warp == 8) {
+        // ===================== weight producer (1-D bulk copies) =======================
+        if (lane == 0) {
+            uint32_t it = 0;
+            for (int64_t v = blockIdx.x; v < n_tiles; v += gridDim.x) {
+                TileInfo t;
+                decode_tile(p, v, list_prefix, n_out, t);
+                for (int c = next_bit(t.mask, 0); c >= 0; c = next_bit(t.mask, c + 1)) {
+                    const int k = p.mode == 0 ? p.dense_k[c] : t.k;
+                    for (int cc = 0; cc < p.n_chunks; ++cc, ++it) {
+                        const int s = it % S;
+                        const uint32_t round = it / S;
+                        ptx::mbar_wait(ptx::smem_u32(&empty[s]), (round & 1) ^ 1);
+                        const uint32_t fb = ptx::smem_u32(&full[s]);
+                        ptx::mbar_arrive_expect_tx(fb, p.b_bytes);
+                        const int64_t blob = ((int64_t)k * p.n_ntiles + t.nt) * p.n_chunks + cc;
+                        ptx::bulk_g2s(ptx::smem_u32(sb + (size_t)s * p.b_bytes), p.wblob + blob * p.b_bytes, p.b_bytes,
+                                      fb);
+                    }
+                }
+            }
+        }
+    } else if (warp == 9) {
+        // ===================== MMA issuer ===============================================
+        if (lane == 0) {
+            uint32_t it = 0, tt = 0;
+            for (int64_t v = blockIdx.x; v < n_tiles; v += gridDim.x, ++tt) {
+                TileInfo t;
+                decode_tile(p, v, list_prefix, n_out, t);
+                const uint32_t a = tt & 1, ar = tt >> 1;
+                ptx::mbar_wait(ptx::smem_u32(&tempty[a]), (ar & 1) ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d_tmem = tmem_base + a * p.tmem_cols;
+                uint32_t acc = 0;
+                for (int c = next_bit(t.mask, 0); c >= 0; c = next_bit(t.mask, c + 1)) {
+                    for (int cc = 0; cc < p.n_chunks; ++cc, ++it) {
+                        const int s = it % S;
+                        const uint32_t round = it / S;
+                        ptx::mbar_wait(ptx::smem_u32(&full[s]), round & 1);
+                        ptx::tc_fence_after();
+                        const uint32_t a_base = ptx::smem_u32(sa + (size_t)s * p.a_bytes);
+                        const uint32_t b_base = ptx::smem_u32(sb + (size_t)s * p.b_bytes);
+                        for (int kk = 0; kk < p.BK / 16; ++kk) {
+                            const uint64_t ad = ptx::umma_desc_kmajor(a_base + kk * 256, lbo, sbo);
+                            const uint64_t bd = ptx::umma_desc_kmajor(b_base + kk * 256, lbo, sbo);
+                            ptx::mma_f16_ss(d_tmem, ad, bd, p.idesc, acc);
+                            acc = 1;
+                        }
+                        ptx::mma_commit(ptx::smem_u32(&empty[s]));
+                    }
+                }
+                ptx::mma_commit(ptx::smem_u32(&tfull[a]));
+            }
+        }
+        __syncwarp();
+    } else {
+        // ===================== epilogue (warps 4-7, thread = TMEM lane = tile row) =====
+        const int e = warp - 4;
+        const int r = e * 32 + lane;
+        uint32_t tt = 0;
+        for (int64_t v = blockIdx.x; v < n_tiles; v += gridDim.x, ++tt) {
+            TileInfo t;
+            decode_tile(p, v, list_prefix, n_out, t);
+            const uint32_t a = tt & 1, ar = tt >> 1;
+            ptx::mbar_wait(ptx::smem_u32(&tfull[a]), ar & 1);
+            ptx::tc_fence_after();
+            int64_t orow = -1;
+            if (r < t.rows) {
+                if (p.mode == 0) orow = t.row0 + r;
+                else {
+                    const int2 pr = p.pairs[t.list * p.list_stride + t.row0 + r];
+                    orow = t.dir ? pr.x : pr.y;
+                }
+            }
+            const uint32_t tbase = tmem_base + a * p.tmem_cols + ((uint32_t)(e * 32) << 16);
+            for (int col = 0; col < p.BN; col += 32) {
+                uint32_t vals[32];
+                const int n = min(32, p.BN - col);
+                if (n == 32) ptx::tmem_ld32(tbase + col, vals);
+                else ptx::tmem_ld16(tbase + col, vals);
+                ptx::tmem_ld_wait();
+                if (orow >= 0) {
+                    const int gcol = t.nt * p.BN + col;
+                    if (p.out_kind == OUT_F32_RED) {
+                        float *op = static_cast<float *>(p.out) + orow * p.ld_out + gcol;
+                        for (int q = 0; q < n / 4; ++q)
+                            ptx::red_add_v4(op + 4 * q, to_f(vals[4 * q]), to_f(vals[4 * q + 1]), to_f(vals[4 * q + 2]),
+                                            to_f(vals[4 * q + 3]));
+                    } else {
+                        store_row(p, orow, gcol, vals, n);
+                    }
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&tempty[a]));
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 9) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem_base, 2 * p.tmem_cols);
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// fp32 FFMA path (same OS / WS semantics)
+// ------------------------------------------------------------------------------------
+constexpr int SM_TM = 64, SM_TN = 64, SM_TK = 16;
+
+__global__ void __launch_bounds__(256) k_conv_simt(const __grid_constant__ ConvParams p, const float *__restrict__ W,
+                                                   int c_in, int c_out) {
+    __shared__ float As[SM_TK][SM_TM + 4];
+    __shared__ float Bs[SM_TK][SM_TN];
+    __shared__ int32_t gidx[SM_TM];
+    __shared__ int64_t sidx[SM_TM];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int64_t n_out = dev_count(p.n_out_cap, p.n_out_dev);
+    const int col0 = blockIdx.y * SM_TN;
+    int64_t row0;
+    int rows, list = 0, dir = 0;
+    int kfix = -1;
+    if (p.mode == 0) {
+        row0 = (int64_t)blockIdx.x * SM_TM;
+        if (row0 >= n_out) return;
+        rows = (int)imin64(SM_TM, n_out - row0);
+    } else {
+        // blockIdx.x -> (list, dir, tile) with a fixed per-list tile budget
+        const int64_t tiles_per = (p.n_out_cap + SM_TM - 1) / SM_TM;
+        const int64_t v = blockIdx.x;
+        list = (int)(v / (2 * tiles_per));
+        const int64_t rem = v - (int64_t)list * 2 * tiles_per;
+        dir = (int)(rem / tiles_per);
+        const int64_t tl = rem - (int64_t)dir * tiles_per;
+        if (list >= p.n_lists) return;
+        if (dir == 1 && !p.list_mirror[list]) return;
+        const int cnt = p.counts[SPC_MAX_KVOL + list];
+        row0 = tl * SM_TM;
+        if (row0 >= cnt) return;
+        rows = (int)imin64(SM_TM, cnt - row0);
+        kfix = dir ? p.k_vol - 1 - p.list_k[list] : p.list_k[list];
+    }
+    float acc[4][4] = {};
+    const int n_steps = p.mode == 0 ? p.k_dense : 1;
+    for (int st = 0; st < n_steps; ++st) {
+        const int k = p.mode == 0 ? p.dense_k[st] : kfix;
+        __syncthreads();
+        if (threadIdx.x < SM_TM) {
+            const int r = threadIdx.x;
+            int32_t g = -1;
+            int64_t so = -1;
+            if (r < rows) {
+                if (p.mode == 0) {
+                    g = p.os[(row0 + r) * p.k_dense + st];
+                    so = row0 + r;
+                } else {
+                    const int2 pr = p.pairs[list * p.list_stride + row0 + r];
+                    g = dir ? pr.y : pr.x;
+                    so = dir ? pr.x : pr.y;
+                }
+            }
+            gidx[r] = g;
+            sidx[r] = so;
+        }
+        __syncthreads();
+        for (int k0 = 0; k0 < c_in; k0 += SM_TK) {
+            for (int e = threadIdx.x; e < SM_TM * SM_TK; e += 256) {
+                const int r = e / SM_TK, kk = e % SM_TK;
+                const int32_t g = gidx[r];
+                As[kk][r] = (g >= 0 && k0 + kk < c_in)
+                                ? reinterpret_cast<const float *>(p.f_in + (int64_t)g * p.ld_in_bytes)[k0 + kk]
+                                : 0.f;
+            }
+            for (int e = threadIdx.x; e < SM_TK * SM_TN; e += 256) {
+                const int kk = e / SM_TN, cc = e % SM_TN;
+                Bs[kk][cc] = (k0 + kk < c_in && col0 + cc < c_out)
+                                 ? W[((int64_t)k * c_in + k0 + kk) * c_out + col0 + cc]
+                                 : 0.f;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int kk = 0; kk < SM_TK; ++kk) {
+                float a[4], b[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+            }
+            __syncthreads();
+        }
+    }
+    for (int i = 0; i < 4; ++i) {
+        const int r = ty * 4 + i;
+        if (r >= rows) continue;
+        const int64_t orow = sidx[r];
+        for (int j = 0; j < 4; ++j) {
+            const int col = col0 + tx * 4 + j;
+            if (col >= c_out) continue;
+            float v = acc[i][j];
+            if (p.out_kind == OUT_F32_RED) {
+                atomicAdd(static_cast<float *>(p.out) + orow * p.ld_out + col, v);
+            } else if (p.out_kind == OUT_F32_STORE || p.out_dtype == SPC_F32) {
+                if (p.out_kind == OUT_FINAL && p.residual) v += static_cast<const float *>(p.residual)[orow * p.ld_res + col];
+                static_cast<float *>(p.out)[orow * p.ld_out + col] = v;
+            } else {
+                if (p.residual) {
+                    const uint16_t h = static_cast<const uint16_t *>(p.residual)[orow * p.ld_res + col];
+                    v += p.out_dtype == SPC_BF16 ? __bfloat162float(__ushort_as_bfloat16(h))
+                                                 : __half2float(__ushort_as_half(h));
+                }
+                static_cast<uint16_t *>(p.out)[orow * p.ld_out + col] =
+                    p.out_dtype == SPC_BF16 ? __bfloat16_as_ushort(__float2bfloat16_rn(v))
+                                            : __half_as_ushort(__float2half_rn(v));
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// weight preparation, accumulator conversion, zero fill
+// ------------------------------------------------------------------------------------
+__global__ void k_prepare_weight_tc(const uint16_t *__restrict__ w, int k_vol, int c_in, int c_out, int BK, int BN,
+                                    uint16_t *__restrict__ out) {
+    const int64_t total = (int64_t)k_vol * c_in * c_out;
+    const int n_nt = c_out / BN, n_ch = c_in / BK;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int co = (int)(e % c_out);
+        const int64_t t = e / c_out;
+        const int ci = (int)(t % c_in);
+        const int k = (int)(t / c_in);
+        const int nt = co / BN, n = co % BN, cc = ci / BK, c = ci % BK;
+        const int64_t blob = ((int64_t)k * n_nt + nt) * n_ch + cc;
+        const int64_t off = blob * BN * BK + ((n >> 3) * (BK >> 3) + (c >> 3)) * 64 + (n & 7) * 8 + (c & 7);
+        out[off] = w[e];
+    }
+}
+
+__global__ void k_convert(const float *__restrict__ acc, int64_t ld_acc, int64_t n_cap, const int64_t *n_dev, int c_out,
+                          int out_dtype, void *__restrict__ out, int64_t ld_out, const void *__restrict__ res,
+                          int64_t ld_res) {
+    const int64_t n = dev_count(n_cap, n_dev);
+    const int64_t total = n * c_out;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = e / c_out;
+        const int c = (int)(e - r * c_out);
+        float v = acc[r * ld_acc + c];
+        if (out_dtype == SPC_F32) {
+            if (res) v += static_cast<const float *>(res)[r * ld_res + c];
+            static_cast<float *>(out)[r * ld_out + c] = v;
+        } else {
+            if (res) {
+                const uint16_t h = static_cast<const uint16_t *>(res)[r * ld_res + c];
+                v += out_dtype == SPC_BF16 ? __bfloat162float(__ushort_as_bfloat16(h)) : __half2float(__ushort_as_half(h));
+            }
+            static_cast<uint16_t *>(out)[r * ld_out + c] = out_dtype == SPC_BF16
+                                                               ? __bfloat16_as_ushort(__float2bfloat16_rn(v))
+                                                               : __half_as_ushort(__float2half_rn(v));
+        }
+    }
+}
+
+__global__ void k_zero_rows(float *__restrict__ acc, int64_t ld, int64_t n_cap, const int64_t *n_dev, int c) {
+    const int64_t n = dev_count(n_cap, n_dev);
+    const int64_t total = n * c;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = e / c;
+        acc[r * ld + (e - r * c)] = 0.f;
+    }
+}
+
+static int pick_bk(int c_in) { return c_in % 64 == 0 ? 64 : (c_in % 32 == 0 ? 32 : 16); }
+static int pick_bn(int c_out) {
+    if (c_out <= 256) return c_out;
+    for (int bn = 256; bn >= 16; bn -= 16)
+        if (c_out % bn == 0) return bn;
+    return 16;
+}
+static uint32_t pow2_cols(int n) {
+    uint32_t c = 32;
+    while ((int)c < n) c <<= 1;
+    return c;
+}
+
+static size_t elem_size(int dt) { return dt == SPC_F32 ? 4 : 2; }
+
+}  // namespace spc
+
+using namespace spc;
+
+extern "C" size_t spc_prepared_weight_bytes(int32_t k_vol, int32_t c_in, int32_t c_out, int32_t in_dtype) {
+    if (k_vol <= 0 || c_in <= 0 || c_out <= 0) return 0;
+    return (size_t)k_vol * c_in * c_out * elem_size(in_dtype);
+}
+
+extern "C" spc_status spc_prepare_weight(const void *weight, int32_t k_vol, int32_t c_in, int32_t c_out,
+                                         int32_t in_dtype, void *prepared, void *stream) {
+    SPC_CHECK_ARG(weight && prepared, "null pointer");
+    SPC_CHECK_ARG(k_vol >= 1 && k_vol <= SPC_MAX_KVOL && c_in > 0 && c_out > 0, "bad shape");
+    cudaStream_t st = as_stream(stream);
+    if (in_dtype == SPC_F32) {
+        SPC_CUDA(cudaMemcpyAsync(prepared, weight, (size_t)k_vol * c_in * c_out * 4, cudaMemcpyDeviceToDevice, st));
+        return SPC_OK;
+    }
+    SPC_CHECK_ARG(in_dtype == SPC_F16 || in_dtype == SPC_BF16, "bad dtype");
+    if (c_in % 16 || c_out % 16)
+        return fail(SPC_ERR_UNSUPPORTED, "spc_prepare_weight: f16/bf16 needs c_in and c_out multiples of 16");
+    const int64_t total = (int64_t)k_vol * c_in * c_out;
+    k_prepare_weight_tc<<<(unsigned)std::min<int64_t>((total + 255) / 256, 4096), 256, 0, st>>>(
+        static_cast<const uint16_t *>(weight), k_vol, c_in, c_out, pick_bk(c_in), pick_bn(c_out),
+        static_cast<uint16_t *>(prepared));
+    SPC_LAUNCH_CHECK("k_prepare_weight_tc");
+    return SPC_OK;
+}
+
+extern "C" size_t spc_conv_workspace_size(const spc_kmap *km, int32_t c_out, int32_t out_dtype) {
+    if (!km || c_out <= 0) return 0;
+    (void)out_dtype;
+    return align_up((size_t)km->n_out * c_out * 4, 256) + 256;
+}
+
+static void fill_map_params(ConvParams &p, const spc_kmap *km) {
+    p.os = km->os_table;
+    p.k_dense = km->k_dense;
+    p.tile_mask = km->tile_mask_dev;
+    p.tile_words = km->tile_words;
+    p.pairs = reinterpret_cast<const int2 *>(km->ws_pairs);
+    p.list_stride = km->n_out;
+    p.counts = km->counts_dev;
+    p.n_lists = km->n_lists;
+    p.k_vol = km->k_vol;
+    p.n_out_cap = km->n_out;
+    p.n_out_dev = km->n_out_dev;
+    for (int c = 0; c < km->k_dense; ++c) p.dense_k[c] = km->dense_k[c];
+    for (int l = 0; l < km->n_lists; ++l) {
+        p.list_k[l] = km->list_k[l];
+        p.list_mirror[l] = km->list_mirror[l];
+    }
+}
+
+static spc_status launch_tc(const ConvParams &p0, int mode, int out_kind, void *out, int64_t ld_out, cudaStream_t st) {
+    ConvParams p = p0;
+    p.mode = mode;
+    p.out_kind = out_kind;
+    p.out = out;
+    p.ld_out = ld_out;
+    const size_t stage = (size_t)p.a_bytes + p.b_bytes;
+    const size_t extra = 64 * 8 + 16 + (SPC_MAX_KVOL + 1) * 4 + 64;
+    int S = (int)((TC_SMEM_BUDGET - extra) / stage);
+    if (S > 8) S = 8;
+    if (S < 2) return fail(SPC_ERR_UNSUPPORTED, "spc_conv_forward: tile does not fit shared memory");
+    p.stages = S;
+    const size_t smem = stage * S + extra;
+    static bool configured = false;
+    if (!configured) {
+        SPC_CUDA(cudaFuncSetAttribute(k_conv_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BUDGET));
+        configured = true;
+    }
+    // persistent: one CTA per SM (the WS tile count lives on the device)
+    int64_t tiles_cap = mode == 0 ? ((p.n_out_cap + TC_BM - 1) / TC_BM) * p.n_ntiles : (int64_t)num_sms();
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles_cap, num_sms()));
+    k_conv_tc<<<grid, TC_THREADS, smem, st>>>(p);
+    SPC_LAUNCH_CHECK("k_conv_tc");
+    return SPC_OK;
+}
+
+extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int64_t ld_in, int32_t in_dtype,
+                                       int32_t c_in, const void *weight, int32_t c_out, void *f_out, int64_t ld_out,
+                                       int32_t out_dtype, const void *residual, int64_t ld_res, void *ws,
+                                       size_t ws_bytes, void *stream) {
+    SPC_CHECK_ARG(km && weight && f_out, "null pointer");
+    SPC_CHECK_ARG(in_dtype >= SPC_F32 && in_dtype <= SPC_BF16 && out_dtype >= SPC_F32 && out_dtype <= SPC_BF16,
+                  "bad dtype");
+    SPC_CHECK_ARG(c_in > 0 && c_out > 0 && ld_in >= c_in && ld_out >= c_out, "bad channel counts / leading dims");
+    SPC_CHECK_ARG(f_in || km->n_in == 0, "null f_in");
+    SPC_CHECK_ARG(!residual || ld_res >= c_out, "bad ld_res");
+    const size_t ein = elem_size(in_dtype), eout = elem_size(out_dtype);
+    SPC_CHECK_ARG(((uintptr_t)f_in % 16) == 0 && (ld_in * ein) % 16 == 0, "f_in rows must be 16-byte aligned");
+    SPC_CHECK_ARG(((uintptr_t)f_out % 16) == 0 && (ld_out * eout) % 16 == 0, "f_out rows must be 16-byte aligned");
+    SPC_CHECK_ARG(!residual || (((uintptr_t)residual % 16) == 0 && (ld_res * eout) % 16 == 0),
+                  "residual rows must be 16-byte aligned");
+    cudaStream_t st = as_stream(stream);
+    if (km->n_out == 0) return SPC_OK;
+    const bool has_os = km->k_dense > 0, has_ws = km->n_lists > 0;
+
+    ConvParams p;
+    memset(&p, 0, sizeof(p));
+    fill_map_params(p, km);
+    p.f_in = static_cast<const char *>(f_in);
+    p.ld_in_bytes = ld_in * (int64_t)ein;
+    p.out_dtype = out_dtype;
+    p.residual = residual;
+    p.ld_res = ld_res;
+
+    // accumulator of the WS part (fp32)
+    float *acc = nullptr;
+    int64_t ld_acc = 0;
+    if (has_ws) {
+        if (out_dtype == SPC_F32 && !residual) {
+            acc = static_cast<float *>(f_out);
+            ld_acc = ld_out;
+        } else {
+            if (!ws || ws_bytes < spc_conv_workspace_size(km, c_out, out_dtype))
+                return fail(SPC_ERR_WORKSPACE, "spc_conv_forward: ws too small");
+            acc = static_cast<float *>(ws);
+            ld_acc = c_out;
+        }
+    }
+
+    if (in_dtype == SPC_F32) {
+        SPC_CHECK_ARG(c_in % 4 == 0 && c_out % 4 == 0, "f32 path needs channels multiple of 4");
+        const dim3 block(256);
+        const unsigned gy = (unsigned)((c_out + SM_TN - 1) / SM_TN);
+        if (has_os) {
+            ConvParams q = p;
+            q.mode = 0;
+            q.out_kind = has_ws ? OUT_F32_STORE : OUT_FINAL;
+            q.out = has_ws ? (void *)acc : f_out;
+            q.ld_out = has_ws ? ld_acc : ld_out;
+            k_conv_simt<<<dim3((unsigned)((km->n_out + SM_TM - 1) / SM_TM), gy), block, 0, st>>>(
+                q, static_cast<const float *>(weight), c_in, c_out);
+            SPC_LAUNCH_CHECK("k_conv_simt os");
+        } else if (has_ws) {
+            k_zero_rows<<<1024, 256, 0, st>>>(acc, ld_acc, km->n_out, km->n_out_dev, c_out);
+        }
+        if (has_ws) {
+            ConvParams q = p;
+            q.mode = 1;
+            q.out_kind = OUT_F32_RED;
+            q.out = acc;
+            q.ld_out = ld_acc;
+            const int64_t tiles_per = (km->n_out + SM_TM - 1) / SM_TM;
+            k_conv_simt<<<dim3((unsigned)(tiles_per * 2 * km->n_lists), gy), block, 0, st>>>(
+                q, static_cast<const float *>(weight), c_in, c_out);
+            SPC_LAUNCH_CHECK("k_conv_simt ws");
+            if (acc != f_out) {
+                k_convert<<<2048, 256, 0, st>>>(acc, ld_acc, km->n_out, km->n_out_dev, c_out, out_dtype, f_out, ld_out,
+                                                residual, ld_res);
+                SPC_LAUNCH_CHECK("k_convert");
+            }
+        }
+        return SPC_OK;
+    }
+
+    // ---- tcgen05 path ------------------------------------------------------------------
+    if (c_in % 16 || c_out % 16)
+        return fail(SPC_ERR_UNSUPPORTED, "spc_conv_forward: f16/bf16 needs c_in and c_out multiples of 16");
+    p.BK = pick_bk(c_in);
+    p.BN = pick_bn(c_out);
+    p.n_chunks = c_in / p.BK;
+    p.n_ntiles = c_out / p.BN;
+    p.a_bytes = (uint32_t)(TC_BM * p.BK * 2);
+    p.b_bytes = (uint32_t)(p.BN * p.BK * 2);
+    p.tmem_cols = pow2_cols(p.BN);
+    p.idesc = ptx::umma_idesc_f16(in_dtype == SPC_BF16, TC_BM, p.BN);
+    p.wblob = static_cast<const char *>(weight);
+    if (has_os) {
+        spc_status s = has_ws ? launch_tc(p, 0, OUT_F32_STORE, acc, ld_acc, st) : launch_tc(p, 0, OUT_FINAL, f_out, ld_out, st);
+        if (s != SPC_OK) return s;
+    } else if (has_ws) {
+        k_zero_rows<<<1024, 256, 0, st>>>(acc, ld_acc, km->n_out, km->n_out_dev, c_out);
+        SPC_LAUNCH_CHECK("k_zero_rows");
+    }
+    if (has_ws) {
+        spc_status s = launch_tc(p, 1, OUT_F32_RED, acc, ld_acc, st);
+        if (s != SPC_OK) return s;
+        if (acc != f_out) {
+            k_convert<<<2048, 256, 0, st>>>(acc, ld_acc, km->n_out, km->n_out_dev, c_out, out_dtype, f_out, ld_out,
+                                            residual, ld_res);
+            SPC_LAUNCH_CHECK("k_convert");
+        }
+    }
+    return SPC_OK;
+}

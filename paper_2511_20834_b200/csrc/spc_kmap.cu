@@ -1,0 +1,445 @@
+// spc_kmap.cu -- A4-A8: one-shot z-delta kernel-map build on packed keys (§5.2,
+// P:341 packed queries, P:393-421 layouts and symmetric halving).
+//
+// CTA = tile of KM_BM sorted outputs.  For a fixed offset group the queries of a tile are
+// sorted, so every match of (tile, group g) lies in ONE contiguous window of the sorted
+// input keys: [lb(q_first + d_anchor(g)), lb(q_last + d_last(g) + 1)).  Phase A finds the
+// 2*K^2 window bounds (parallel global lower_bounds), phase A' stages the windows in
+// shared memory (coalesced), phase B runs the paper's z-delta search per (output, group)
+// inside the window: one lower_bound for the anchor query, then a forward cursor for the
+// other K-1 members.  Both layouts are written straight from phase B:
+//   OS (dense offsets): staged as a [KM_BM x K_dense] int32 block in smem, flushed with
+//       coalesced 16-byte stores (no transpose pass);
+//   WS (sparse offsets): (in, out) pairs appended with one warp-aggregated atomicAdd per
+//       (warp, offset) (no filter pass); halved for submanifold layers.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "spc_common.cuh"
+
+namespace spc {
+
+constexpr int KM_BM = 128;          // outputs per tile
+constexpr int KM_THREADS = 256;
+constexpr int KM_WIN_CAP = 4096;    // staged window keys per tile (32 KB)
+
+struct KmapParams {
+    const uint64_t *in;
+    int64_t n_in_cap;
+    const int64_t *n_in_dev;
+    const uint64_t *out;
+    int64_t n_out_cap;
+    const int64_t *n_out_dev;
+    int32_t *os;
+    int2 *pairs;
+    int32_t *counts;
+    uint32_t *tile_mask;
+    unsigned long long *stats;
+    int64_t list_stride;
+    int K, n_groups, k_dense, tile_words;
+    int64_t delta[SPC_MAX_KVOL];      // [g*K + m]: packed query delta, ascending in m
+    int16_t kslot[SPC_MAX_KVOL];      // [g*K + m] -> weight offset index k
+    int16_t dense_col[SPC_MAX_KVOL];  // [k] -> OS column or -1
+    int16_t list_id[SPC_MAX_KVOL];    // [k] -> WS list or -1
+    uint8_t group_needed[25];
+};
+
+__device__ __forceinline__ int64_t lower_bound_g(const uint64_t *__restrict__ a, int64_t n, uint64_t q) {
+    int64_t lo = 0, len = n;
+    while (len > 0) {
+        int64_t half = len >> 1;
+        if (__ldg(a + lo + half) < q) {
+            lo += half + 1;
+            len -= half + 1;
+        } else {
+            len = half;
+        }
+    }
+    return lo;
+}
+
+__device__ __forceinline__ int lower_bound_s(const uint64_t *a, int n, uint64_t q) {
+    int lo = 0, len = n;
+    while (len > 0) {
+        int half = len >> 1;
+        if (a[lo + half] < q) {
+            lo += half + 1;
+            len -= half + 1;
+        } else {
+            len = half;
+        }
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(KM_THREADS) k_kmap_zdelta(const __grid_constant__ KmapParams p) {
+    extern __shared__ __align__(16) unsigned char km_smem[];
+    __shared__ int64_t win_lo[25];
+    __shared__ int win_len[25];
+    __shared__ int win_base[25];   // -1: window not staged, use global search
+    __shared__ uint32_t smask[4];  // tile bit mask over dense columns (<= 125)
+
+    const int64_t n_out = dev_count(p.n_out_cap, p.n_out_dev);
+    const int64_t n_in = dev_count(p.n_in_cap, p.n_in_dev);
+    const int64_t row0 = (int64_t)blockIdx.x * KM_BM;
+    if (row0 >= n_out) return;
+    const int rows = (int)imin64(KM_BM, n_out - row0);
+    const int K = p.K, G = p.n_groups, KD = p.k_dense;
+    int32_t *os_tile = reinterpret_cast<int32_t *>(km_smem);
+    uint64_t *win = reinterpret_cast<uint64_t *>(km_smem + KM_BM * KD * 4);   // KM_BM*4 = 512 B multiple
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid < 4) smask[tid] = 0;
+
+    // ---- phase A: window bounds of every (tile, group) ------------------------------
+    const uint64_t q_first = p.out[row0];
+    const uint64_t q_last = p.out[row0 + rows - 1];
+    if (tid < 2 * G) {
+        const int g = tid >> 1;
+        if (p.group_needed[g]) {
+            uint64_t q = (tid & 1) ? q_last + (uint64_t)p.delta[g * K + K - 1] + 1ull
+                                   : q_first + (uint64_t)p.delta[g * K];
+            int64_t b = lower_bound_g(p.in, n_in, q);
+            if (tid & 1) win_len[g] = (int)imin64(b, INT32_MAX);   // hi for now
+            else win_lo[g] = b;
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int base = 0;
+        for (int g = 0; g < G; ++g) {
+            if (!p.group_needed[g]) { win_base[g] = -1; win_len[g] = 0; continue; }
+            int64_t len = (int64_t)win_len[g] - win_lo[g];
+            if (len < 0) len = 0;
+            win_len[g] = (int)len;
+            if (base + len <= KM_WIN_CAP) { win_base[g] = base; base += (int)len; }
+            else win_base[g] = -1;
+        }
+    }
+    __syncthreads();
+    // ---- phase A': stage windows (one warp per group, coalesced) ---------------------
+    for (int g = warp; g < G; g += KM_THREADS / 32) {
+        if (win_base[g] < 0) continue;
+        const uint64_t *src = p.in + win_lo[g];
+        uint64_t *dst = win + win_base[g];
+        for (int e = lane; e < win_len[g]; e += 32) dst[e] = __ldg(src + e);
+    }
+    __syncthreads();
+
+    // ---- phase B: z-delta search per (output, group) ---------------------------------
+    unsigned long long n_search = 0, n_probe = 0;
+    const int chunks = KM_BM / 32;
+    for (int item = warp; item < G * chunks; item += KM_THREADS / 32) {
+        const int g = item / chunks, ch = item - g * chunks;
+        if (!p.group_needed[g]) continue;
+        const int lr = ch * 32 + lane;               // local row
+        const bool valid = lr < rows;
+        const int64_t i = row0 + lr;
+        const uint64_t q = valid ? p.out[i] : 0;
+        const bool staged = win_base[g] >= 0;
+        const uint64_t *wk = staged ? win + win_base[g] : p.in + win_lo[g];
+        const int wl = win_len[g];
+        int pos = 0;
+        if (valid) {
+            pos = lower_bound_s(wk, wl, q + (uint64_t)p.delta[g * K]);
+            ++n_search;
+        }
+        for (int m = 0; m < K; ++m) {
+            const uint64_t query = q + (uint64_t)p.delta[g * K + m];
+            bool match = false;
+            if (valid) {
+                while (pos < wl && wk[pos] < query) { ++pos; ++n_probe; }
+                match = pos < wl && wk[pos] == query;
+            }
+            const int k = p.kslot[g * K + m];
+            const int32_t j = match ? (int32_t)(win_lo[g] + pos) : -1;
+            const unsigned bal = __ballot_sync(0xffffffffu, match);
+            if (lane == 0 && bal) atomicAdd(&p.counts[k], __popc(bal));
+            const int col = p.dense_col[k];
+            if (col >= 0) {
+                if (valid) os_tile[lr * KD + col] = j;
+                if (lane == 0 && bal) atomicOr(&smask[col >> 5], 1u << (col & 31));
+            } else {
+                const int l = p.list_id[k];
+                if (l >= 0 && bal) {
+                    int base = 0;
+                    if (lane == 0) base = atomicAdd(&p.counts[SPC_MAX_KVOL + l], __popc(bal));
+                    base = __shfl_sync(0xffffffffu, base, 0);
+                    if (match) {
+                        int2 pr = make_int2(j, (int32_t)i);
+                        p.pairs[(int64_t)l * p.list_stride + base + __popc(bal & lanemask_lt())] = pr;
+                    }
+                }
+            }
+        }
+    }
+    if (p.stats) {
+        for (int o = 16; o > 0; o >>= 1) {
+            n_search += __shfl_xor_sync(0xffffffffu, n_search, o);
+            n_probe += __shfl_xor_sync(0xffffffffu, n_probe, o);
+        }
+        if (lane == 0) {
+            atomicAdd(&p.stats[0], n_search);
+            atomicAdd(&p.stats[1], n_probe);
+        }
+    }
+    __syncthreads();
+    // ---- phase C: flush the OS block (contiguous rows*KD int32) -----------------------
+    if (KD > 0) {
+        int32_t *dst = p.os + row0 * KD;
+        const int total = rows * KD;
+        // row0*KD*4 is 16-byte aligned when KD % 4 == 0 or row0 % 4 == 0 (KM_BM = 128)
+        const int nvec = total / 4;
+        int4 *d4 = reinterpret_cast<int4 *>(dst);
+        const int4 *s4 = reinterpret_cast<const int4 *>(os_tile);
+        for (int e = tid; e < nvec; e += KM_THREADS) d4[e] = s4[e];
+        for (int e = nvec * 4 + tid; e < total; e += KM_THREADS) dst[e] = os_tile[e];
+        if (tid < p.tile_words) p.tile_mask[blockIdx.x * (int64_t)p.tile_words + tid] = smask[tid];
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// host: plan (offset tables, dense/sparse split, lists) and entry points
+// ------------------------------------------------------------------------------------
+struct KmapPlan {
+    int K = 0, r = 0, k_vol = 0, k_dense = 0, n_lists = 0, halved = 0, t_eff = 0, spacing = 1;
+    int16_t dense_k[SPC_MAX_KVOL], list_k[SPC_MAX_KVOL];
+    int8_t list_mirror[SPC_MAX_KVOL];
+    int16_t dense_col[SPC_MAX_KVOL], list_id[SPC_MAX_KVOL];
+    uint8_t group_needed[25];
+};
+
+static spc_status make_plan(const spc_geom &g, int32_t t, uint32_t flags, KmapPlan &pl) {
+    if (g.kernel_size < 1 || g.kernel_size % 2 == 0 || g.kernel_size > 5)
+        return fail(SPC_ERR_UNSUPPORTED, "kernel_size must be odd and <= 5 (P:111), got " +
+                                             std::to_string(g.kernel_size));
+    if (g.stride < 1 || g.dilation < 1 || g.tensor_stride < 1)
+        return fail(SPC_ERR_INVALID_ARG, "stride, dilation and tensor_stride must be >= 1");
+    if (g.transposed && g.stride == 1)
+        return fail(SPC_ERR_INVALID_ARG, "a transposed map needs stride > 1");
+    pl.K = g.kernel_size;
+    pl.r = (pl.K - 1) / 2;
+    pl.k_vol = pl.K * pl.K * pl.K;
+    pl.spacing = g.tensor_stride * g.dilation;
+    const int l1max = 3 * pl.r;
+    pl.t_eff = (t < 0 || t > l1max + 1) ? l1max + 1 : t;
+    const bool subm = g.stride == 1 && !g.transposed;
+    pl.halved = (flags & SPC_KMAP_HALVE_SYMMETRIC) && subm ? 1 : 0;
+    const int centre = (pl.k_vol - 1) / 2;
+    pl.k_dense = pl.n_lists = 0;
+    for (int k = 0; k < pl.k_vol; ++k) {
+        int ex = k / (pl.K * pl.K) - pl.r, ey = (k / pl.K) % pl.K - pl.r, ez = k % pl.K - pl.r;
+        int l1 = abs(ex) + abs(ey) + abs(ez);
+        pl.dense_col[k] = -1;
+        pl.list_id[k] = -1;
+        if (l1 < pl.t_eff) {
+            pl.dense_col[k] = (int16_t)pl.k_dense;
+            pl.dense_k[pl.k_dense++] = (int16_t)k;
+        } else if (!pl.halved || k <= centre) {
+            pl.list_id[k] = (int16_t)pl.n_lists;
+            pl.list_mirror[pl.n_lists] = (pl.halved && k < centre) ? 1 : 0;
+            pl.list_k[pl.n_lists++] = (int16_t)k;
+        }
+    }
+    for (int gi = 0; gi < pl.K * pl.K; ++gi) {
+        bool need = false;
+        for (int m = 0; m < pl.K; ++m) {
+            int k = gi * pl.K + m;
+            need |= pl.dense_col[k] >= 0 || pl.list_id[k] >= 0;
+        }
+        pl.group_needed[gi] = need;
+    }
+    return SPC_OK;
+}
+
+struct KmapLayout {
+    size_t os, pairs, counts, mask, stats, total;
+    int64_t tiles;
+    int words;
+};
+
+static KmapLayout layout_of(const KmapPlan &pl, int64_t n_out) {
+    KmapLayout L{};
+    L.tiles = (n_out + KM_BM - 1) / KM_BM;
+    L.words = (pl.k_dense + 31) / 32;
+    size_t off = 0;
+    auto take = [&](size_t bytes) { off = align_up(off, 256); size_t at = off; off += bytes; return at; };
+    L.os = take(sizeof(int32_t) * (size_t)n_out * pl.k_dense);
+    L.pairs = take(sizeof(int2) * (size_t)n_out * pl.n_lists);
+    L.counts = take(sizeof(int32_t) * 2 * SPC_MAX_KVOL);
+    L.mask = take(sizeof(uint32_t) * (size_t)(L.tiles * L.words));
+    L.stats = take(sizeof(unsigned long long) * 2);
+    L.total = align_up(off, 256);
+    return L;
+}
+
+size_t kmap_smem_bytes(int k_dense) { return (size_t)KM_BM * k_dense * 4 + (size_t)KM_WIN_CAP * 8; }
+
+}  // namespace spc
+
+using namespace spc;
+
+extern "C" size_t spc_kmap_bytes(spc_geom geom, int32_t t, uint32_t flags, int64_t n_in, int64_t n_out) {
+    KmapPlan pl;
+    if (make_plan(geom, t, flags, pl) != SPC_OK || n_out < 0) return 0;
+    (void)n_in;
+    return layout_of(pl, n_out).total;
+}
+
+namespace spc {
+__global__ void k_flag_dups(const uint64_t *keys, int64_t n_cap, const int64_t *n_dev, uint32_t *status,
+                            uint32_t flag);
+}
+
+extern "C" spc_status spc_build_kmap(const uint64_t *in_keys, int64_t n_in, const int64_t *n_in_dev,
+                                     const uint64_t *out_keys, int64_t n_out, const int64_t *n_out_dev,
+                                     spc_pack_spec spec, spc_geom geom, int32_t t, uint32_t flags, void *buf,
+                                     size_t buf_bytes, uint32_t *status, spc_kmap *kmap_out, void *stream) {
+    SPC_CHECK_ARG(kmap_out, "null kmap_out");
+    SPC_CHECK_ARG(n_in >= 0 && n_out >= 0, "negative size");
+    SPC_CHECK_ARG(n_in < INT32_MAX && n_out < INT32_MAX, "sizes must fit int32 indices");
+    SPC_CHECK_ARG((in_keys || n_in == 0) && (out_keys || n_out == 0), "null keys");
+    KmapPlan pl;
+    spc_status s = make_plan(geom, t, flags, pl);
+    if (s != SPC_OK) return s;
+    const KmapLayout L = layout_of(pl, n_out);
+    SPC_CHECK_ARG(buf && ((uintptr_t)buf % 256) == 0, "buf must be non-null and 256-byte aligned");
+    if (buf_bytes < L.total) return fail(SPC_ERR_WORKSPACE, "spc_build_kmap: buffer too small");
+    // reach check (reading A4): the planner guarantees headroom; here we only refuse
+    // offsets that cannot be represented in the z field at all
+    const int reach = pl.r * pl.spacing;
+    if (reach >= (1 << (spec.bits_z - 1)) || reach >= (1 << (spec.bits_y - 1)) || reach >= (1 << (spec.bits_x - 1)))
+        return fail(SPC_ERR_RANGE, "spc_build_kmap: kernel reach " + std::to_string(reach) +
+                                       " does not fit the key fields");
+    cudaStream_t st = as_stream(stream);
+    char *base = static_cast<char *>(buf);
+
+    spc_kmap &km = *kmap_out;
+    memset(&km, 0, sizeof(km));
+    km.geom = geom;
+    km.t = pl.t_eff;
+    km.k_vol = pl.k_vol;
+    km.k_dense = pl.k_dense;
+    km.n_lists = pl.n_lists;
+    km.halved = pl.halved;
+    km.tile_words = L.words;
+    km.n_in = n_in;
+    km.n_out = n_out;
+    km.n_in_dev = n_in_dev;
+    km.n_out_dev = n_out_dev;
+    km.in_keys = in_keys;
+    km.out_keys = out_keys;
+    km.os_table = reinterpret_cast<int32_t *>(base + L.os);
+    km.ws_pairs = reinterpret_cast<int32_t *>(base + L.pairs);
+    km.counts_dev = reinterpret_cast<int32_t *>(base + L.counts);
+    km.tile_mask_dev = reinterpret_cast<uint32_t *>(base + L.mask);
+    km.search_stats_dev = (flags & SPC_KMAP_COUNT_SEARCHES) ? reinterpret_cast<unsigned long long *>(base + L.stats)
+                                                             : nullptr;
+    for (int c = 0; c < pl.k_dense; ++c) km.dense_k[c] = pl.dense_k[c];
+    for (int l = 0; l < pl.n_lists; ++l) {
+        km.list_k[l] = pl.list_k[l];
+        km.list_mirror[l] = pl.list_mirror[l];
+    }
+    SPC_CUDA(cudaMemsetAsync(base + L.counts, 0, L.stats + 2 * sizeof(unsigned long long) - L.counts, st));
+    if (n_out == 0) return SPC_OK;
+    if ((flags & SPC_KMAP_CHECK_SORTED) && status) {
+        k_flag_dups<<<64, 256, 0, st>>>(in_keys, n_in, n_in_dev, status, SPC_FLAG_UNSORTED);
+        k_flag_dups<<<64, 256, 0, st>>>(out_keys, n_out, n_out_dev, status, SPC_FLAG_UNSORTED);
+    }
+
+    KmapParams p;
+    memset(&p, 0, sizeof(p));
+    p.in = in_keys;
+    p.n_in_cap = n_in;
+    p.n_in_dev = n_in_dev;
+    p.out = out_keys;
+    p.n_out_cap = n_out;
+    p.n_out_dev = n_out_dev;
+    p.os = km.os_table;
+    p.pairs = reinterpret_cast<int2 *>(km.ws_pairs);
+    p.counts = km.counts_dev;
+    p.tile_mask = km.tile_mask_dev;
+    p.stats = km.search_stats_dev;
+    p.list_stride = n_out;
+    p.K = pl.K;
+    p.n_groups = pl.K * pl.K;
+    p.k_dense = pl.k_dense;
+    p.tile_words = L.words;
+    const int sp = pl.spacing;
+    for (int gi = 0; gi < pl.K * pl.K; ++gi) {
+        const int ex = gi / pl.K - pl.r, ey = gi % pl.K - pl.r;
+        for (int m = 0; m < pl.K; ++m) {
+            // members in ascending QUERY order: +delta (ez ascending) or -delta (ez descending)
+            const int ez = geom.transposed ? pl.r - m : m - pl.r;
+            const int k = ((ex + pl.r) * pl.K + (ey + pl.r)) * pl.K + (ez + pl.r);
+            int64_t d = spc_pack_offset(spec, ex * sp, ey * sp, ez * sp);
+            p.delta[gi * pl.K + m] = geom.transposed ? -d : d;
+            p.kslot[gi * pl.K + m] = (int16_t)k;
+        }
+        p.group_needed[gi] = pl.group_needed[gi];
+    }
+    for (int k = 0; k < pl.k_vol; ++k) {
+        p.dense_col[k] = pl.dense_col[k];
+        p.list_id[k] = pl.list_id[k];
+    }
+    const size_t smem = kmap_smem_bytes(pl.k_dense);
+    static int configured = 0;
+    if (!configured) {
+        SPC_CUDA(cudaFuncSetAttribute(k_kmap_zdelta, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)kmap_smem_bytes(SPC_MAX_KVOL)));
+        configured = 1;
+    }
+    k_kmap_zdelta<<<(unsigned)L.tiles, KM_THREADS, smem, st>>>(p);
+    SPC_LAUNCH_CHECK("k_kmap_zdelta");
+    return SPC_OK;
+}
+
+extern "C" spc_status spc_kmap_export(const spc_kmap *km, int32_t *triples_host, int64_t cap, int64_t *nnz_host,
+                                      void *stream) {
+    SPC_CHECK_ARG(km && nnz_host, "null pointer");
+    cudaStream_t st = as_stream(stream);
+    SPC_CUDA(cudaStreamSynchronize(st));
+    int64_t n_out = km->n_out;
+    if (km->n_out_dev) {
+        int64_t v;
+        SPC_CUDA(cudaMemcpy(&v, km->n_out_dev, sizeof(v), cudaMemcpyDeviceToHost));
+        n_out = std::min(v, n_out);
+    }
+    std::vector<int32_t> counts(2 * SPC_MAX_KVOL);
+    SPC_CUDA(cudaMemcpy(counts.data(), km->counts_dev, counts.size() * 4, cudaMemcpyDeviceToHost));
+    std::vector<int32_t> os((size_t)n_out * km->k_dense);
+    if (!os.empty()) SPC_CUDA(cudaMemcpy(os.data(), km->os_table, os.size() * 4, cudaMemcpyDeviceToHost));
+    struct Tr { int32_t k, i, j; };
+    std::vector<Tr> tr;
+    for (int64_t i = 0; i < n_out; ++i)
+        for (int c = 0; c < km->k_dense; ++c) {
+            int32_t j = os[(size_t)i * km->k_dense + c];
+            if (j >= 0) tr.push_back({km->dense_k[c], (int32_t)i, j});
+        }
+    for (int l = 0; l < km->n_lists; ++l) {
+        int32_t cnt = counts[SPC_MAX_KVOL + l];
+        std::vector<int32_t> pr((size_t)cnt * 2);
+        if (cnt) SPC_CUDA(cudaMemcpy(pr.data(), km->ws_pairs + (size_t)l * km->n_out * 2, pr.size() * 4,
+                                     cudaMemcpyDeviceToHost));
+        const int k = km->list_k[l];
+        for (int32_t q = 0; q < cnt; ++q) {
+            tr.push_back({k, pr[2 * q + 1], pr[2 * q]});
+            if (km->list_mirror[l]) tr.push_back({km->k_vol - 1 - k, pr[2 * q], pr[2 * q + 1]});
+        }
+    }
+    std::sort(tr.begin(), tr.end(), [](const Tr &a, const Tr &b) {
+        if (a.k != b.k) return a.k < b.k;
+        if (a.i != b.i) return a.i < b.i;
+        return a.j < b.j;
+    });
+    *nnz_host = (int64_t)tr.size();
+    if (triples_host)
+        for (int64_t q = 0; q < (int64_t)tr.size() && q < cap; ++q) {
+            triples_host[3 * q] = tr[q].k;
+            triples_host[3 * q + 1] = tr[q].i;
+            triples_host[3 * q + 2] = tr[q].j;
+        }
+    return SPC_OK;
+}

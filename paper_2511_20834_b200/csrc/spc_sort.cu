@@ -1,0 +1,544 @@
+// spc_sort.cu -- A1 pack, A2 sort-once, A3 grouped downsampling (Eq. 1 / Eq. 3).
+//
+// LSD radix sort over the USED key bits only (8-bit digits).  One pass = three kernels:
+//   k_radix_hist   : per-tile digit histograms (warp-aggregated smem atomics)
+//   k_radix_scan   : per-digit exclusive scan over tiles (digit-major, one CTA per digit)
+//   k_radix_scatter: stable in-tile ranking with __match_any_sync, tile staged in smem,
+//                    then written out digit-run by digit-run (coalesced runs).
+// Every kernel reads the element count from device memory (n_dev), so the whole
+// indexing phase runs without host syncs.
+#include <cuda_runtime.h>
+
+#include "spc_common.cuh"
+
+namespace spc {
+
+constexpr int SORT_THREADS = 256;
+constexpr int SORT_ITEMS = 4;
+constexpr int SORT_TILE = SORT_THREADS * SORT_ITEMS;   // 1024 keys per tile
+constexpr int SORT_WARPS = SORT_THREADS / 32;
+
+// exclusive block scan of one int per thread (256 threads); returns the block total
+__device__ __forceinline__ int block_excl_scan_256(int v, int *warp_sums, int &total) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sums[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        int s = lane < SORT_WARPS ? warp_sums[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s += y;
+        }
+        if (lane < SORT_WARPS) warp_sums[lane] = s;   // inclusive
+    }
+    __syncthreads();
+    int before = (w > 0 ? warp_sums[w - 1] : 0) + x - v;
+    total = warp_sums[SORT_WARPS - 1];
+    __syncthreads();
+    return before;
+}
+
+__global__ void __launch_bounds__(SORT_THREADS) k_radix_hist(const uint64_t *__restrict__ keys,
+                                                             int64_t n_cap, const int64_t *n_dev,
+                                                             int shift, int *__restrict__ hist,
+                                                             int n_tiles) {
+    __shared__ int cnt[256];
+    const int tile = blockIdx.x;
+    cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t n = dev_count(n_cap, n_dev);
+    const int64_t base = (int64_t)tile * SORT_TILE;
+#pragma unroll
+    for (int it = 0; it < SORT_ITEMS; ++it) {
+        int64_t idx = base + it * SORT_THREADS + threadIdx.x;
+        bool valid = idx < n;
+        unsigned d = valid ? (unsigned)((keys[idx] >> shift) & 255u) : 256u + (threadIdx.x & 31);
+        unsigned peers = __match_any_sync(0xffffffffu, d);
+        if (valid && (lanemask_lt() & peers) == 0) atomicAdd(&cnt[d], __popc(peers));
+    }
+    __syncthreads();
+    hist[threadIdx.x * n_tiles + tile] = cnt[threadIdx.x];
+}
+
+// one CTA per digit: exclusive scan of hist[d][0..n_tiles) in place, total -> totals[d]
+__global__ void __launch_bounds__(1024) k_radix_scan(int *__restrict__ hist, int n_tiles,
+                                                     int *__restrict__ totals) {
+    __shared__ int wsum[32];
+    __shared__ int carry_s;
+    int *row = hist + (int64_t)blockIdx.x * n_tiles;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (threadIdx.x == 0) carry_s = 0;
+    __syncthreads();
+    for (int base = 0; base < n_tiles; base += 1024) {
+        int i = base + threadIdx.x;
+        int v = i < n_tiles ? row[i] : 0;
+        int x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[w] = x;
+        __syncthreads();
+        if (w == 0) {
+            int s = wsum[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int y = __shfl_up_sync(0xffffffffu, s, o);
+                if (lane >= o) s += y;
+            }
+            wsum[lane] = s;
+        }
+        __syncthreads();
+        int carry = carry_s;
+        int excl = carry + (w > 0 ? wsum[w - 1] : 0) + x - v;
+        if (i < n_tiles) row[i] = excl;
+        __syncthreads();
+        if (threadIdx.x == 0) carry_s = carry + wsum[31];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) totals[blockIdx.x] = carry_s;
+}
+
+template <bool VALS>
+__global__ void __launch_bounds__(SORT_THREADS) k_radix_scatter(
+    const uint64_t *__restrict__ keys_in, const int32_t *__restrict__ vals_in, int64_t n_cap,
+    const int64_t *n_dev, int shift, const int *__restrict__ hist, const int *__restrict__ totals,
+    int n_tiles, uint64_t *__restrict__ keys_out, int32_t *__restrict__ vals_out) {
+    __shared__ int digit_base[256];
+    __shared__ int tile_off[256];
+    __shared__ int local_start[256];
+    __shared__ int cnt[SORT_WARPS][256];
+    __shared__ int warp_sums[SORT_WARPS];
+    __shared__ uint64_t skeys[SORT_TILE];
+    __shared__ int32_t svals[VALS ? SORT_TILE : 1];
+
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int tile = blockIdx.x;
+    const int64_t n = dev_count(n_cap, n_dev);
+    const int64_t base = (int64_t)tile * SORT_TILE;
+    if (base >= n) return;
+    const int tile_valid = (int)imin64(SORT_TILE, n - base);
+
+    {
+        int tot;
+        int b = block_excl_scan_256(totals[tid], warp_sums, tot);
+        digit_base[tid] = b;
+        tile_off[tid] = hist[tid * n_tiles + tile];
+#pragma unroll
+        for (int ww = 0; ww < SORT_WARPS; ++ww) cnt[ww][tid] = 0;
+    }
+    __syncthreads();
+
+    uint64_t key[SORT_ITEMS];
+    int32_t val[SORT_ITEMS];
+    int rank[SORT_ITEMS];
+    unsigned dig[SORT_ITEMS];
+#pragma unroll
+    for (int r = 0; r < SORT_ITEMS; ++r) {
+        const int li = w * (32 * SORT_ITEMS) + r * 32 + lane;   // warp-contiguous chunk
+        const int64_t idx = base + li;
+        const bool valid = li < tile_valid;
+        key[r] = valid ? keys_in[idx] : ~0ull;
+        if (VALS) val[r] = valid ? (vals_in ? vals_in[idx] : (int32_t)idx) : 0;
+        dig[r] = valid ? (unsigned)((key[r] >> shift) & 255u) : 256u + lane;
+        unsigned peers = __match_any_sync(0xffffffffu, dig[r]);
+        int before = __popc(peers & lanemask_lt());
+        int c = valid ? cnt[w][dig[r]] : 0;
+        rank[r] = c + before;
+        __syncwarp();
+        if (valid && before == 0) cnt[w][dig[r]] = c + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    {
+        int s = 0;
+#pragma unroll
+        for (int ww = 0; ww < SORT_WARPS; ++ww) {
+            int c = cnt[ww][tid];
+            cnt[ww][tid] = s;
+            s += c;
+        }
+        int tot;
+        local_start[tid] = block_excl_scan_256(s, warp_sums, tot);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < SORT_ITEMS; ++r) {
+        if (dig[r] < 256u) {
+            int lp = local_start[dig[r]] + cnt[w][dig[r]] + rank[r];
+            skeys[lp] = key[r];
+            if (VALS) svals[lp] = val[r];
+        }
+    }
+    __syncthreads();
+    for (int s = tid; s < tile_valid; s += SORT_THREADS) {
+        uint64_t k = skeys[s];
+        int d = (int)((k >> shift) & 255u);
+        int64_t g = (int64_t)digit_base[d] + tile_off[d] + (s - local_start[d]);
+        keys_out[g] = k;
+        if (VALS) vals_out[g] = svals[s];
+    }
+}
+
+__global__ void k_copy_keys(const uint64_t *__restrict__ a, int64_t n_cap, const int64_t *n_dev,
+                            uint64_t *__restrict__ b, const int32_t *vals_in, int32_t *vals_out) {
+    const int64_t n = dev_count(n_cap, n_dev);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        b[i] = a[i];
+        if (vals_out) vals_out[i] = vals_in ? vals_in[i] : (int32_t)i;
+    }
+}
+
+static int n_tiles_of(int64_t n) { return (int)((n + SORT_TILE - 1) / SORT_TILE); }
+
+size_t radix_sort_workspace(int64_t n, bool with_vals) {
+    Sizer s;
+    const int nt = n_tiles_of(n > 0 ? n : 1);
+    s.take<int>((size_t)nt * 256);
+    s.take<int>(256);
+    s.take<uint64_t>((size_t)n);
+    if (with_vals) s.take<int32_t>((size_t)n);
+    return s.used + 256;
+}
+
+spc_status radix_sort(const uint64_t *keys_in, const int32_t *vals_in, int64_t n, const int64_t *n_dev,
+                      int n_bits, uint64_t *keys_out, int32_t *vals_out, void *ws, size_t ws_bytes,
+                      cudaStream_t st) {
+    if (n <= 0) return SPC_OK;
+    const bool with_vals = vals_out != nullptr;
+    Bump b(ws, ws_bytes);
+    const int nt = n_tiles_of(n);
+    int *hist = b.take<int>((size_t)nt * 256);
+    int *totals = b.take<int>(256);
+    uint64_t *ktmp = b.take<uint64_t>((size_t)n);
+    int32_t *vtmp = with_vals ? b.take<int32_t>((size_t)n) : nullptr;
+    if (!b.ok()) return fail(SPC_ERR_WORKSPACE, "radix_sort: workspace too small");
+    const int passes = (n_bits + 7) / 8;
+    if (passes == 0) {
+        k_copy_keys<<<256, 256, 0, st>>>(keys_in, n, n_dev, keys_out, vals_in, vals_out);
+        SPC_LAUNCH_CHECK("k_copy_keys");
+        return SPC_OK;
+    }
+    const uint64_t *src_k = keys_in;
+    const int32_t *src_v = vals_in;
+    for (int p = 0; p < passes; ++p) {
+        const bool to_out = ((passes - 1 - p) % 2) == 0;
+        uint64_t *dst_k = to_out ? keys_out : ktmp;
+        int32_t *dst_v = with_vals ? (to_out ? vals_out : vtmp) : nullptr;
+        const int shift = 8 * p;
+        k_radix_hist<<<nt, SORT_THREADS, 0, st>>>(src_k, n, n_dev, shift, hist, nt);
+        k_radix_scan<<<256, 1024, 0, st>>>(hist, nt, totals);
+        if (with_vals)
+            k_radix_scatter<true><<<nt, SORT_THREADS, 0, st>>>(src_k, src_v, n, n_dev, shift, hist, totals, nt,
+                                                              dst_k, dst_v);
+        else
+            k_radix_scatter<false><<<nt, SORT_THREADS, 0, st>>>(src_k, nullptr, n, n_dev, shift, hist, totals,
+                                                               nt, dst_k, nullptr);
+        SPC_LAUNCH_CHECK("radix pass");
+        src_k = dst_k;
+        src_v = dst_v;
+    }
+    return SPC_OK;
+}
+
+// ------------------------------------------------------------------------------------
+// A1 pack + duplicate flag
+// ------------------------------------------------------------------------------------
+struct PackDev {
+    int bb, bx, by, bz;
+};
+
+__global__ void k_pack(const int4 *__restrict__ coords, int64_t n, PackDev s, uint64_t *__restrict__ keys,
+                       uint32_t *status) {
+    bool bad = false;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        int4 c = coords[i];
+        int64_t fb = c.x;
+        int64_t fx = (int64_t)c.y + (1ll << (s.bx - 1));
+        int64_t fy = (int64_t)c.z + (1ll << (s.by - 1));
+        int64_t fz = (int64_t)c.w + (1ll << (s.bz - 1));
+        bool ok = fb >= 0 && fb < (1ll << s.bb) && fx >= 0 && fx < (1ll << s.bx) && fy >= 0 &&
+                  fy < (1ll << s.by) && fz >= 0 && fz < (1ll << s.bz);
+        bad |= !ok;
+        uint64_t k = ((uint64_t)fb << (s.bx + s.by + s.bz)) | ((uint64_t)fx << (s.by + s.bz)) |
+                     ((uint64_t)fy << s.bz) | (uint64_t)fz;
+        keys[i] = k;
+    }
+    if (__any_sync(0xffffffffu, bad) && status && (threadIdx.x & 31) == 0) atomicOr(status, SPC_FLAG_RANGE);
+}
+
+__global__ void k_flag_dups(const uint64_t *__restrict__ keys, int64_t n_cap, const int64_t *n_dev,
+                            uint32_t *status, uint32_t flag) {
+    const int64_t n = dev_count(n_cap, n_dev);
+    bool dup = false;
+    for (int64_t i = 1 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dup |= keys[i] <= keys[i - 1];
+    if (__any_sync(0xffffffffu, dup) && (threadIdx.x & 31) == 0) atomicOr(status, flag);
+}
+
+__global__ void k_gather_rows(const char *__restrict__ src, int64_t ld_src, const int32_t *__restrict__ perm,
+                              int64_t n_cap, const int64_t *n_dev, int row_bytes, char *__restrict__ dst,
+                              int64_t ld_dst) {
+    const int64_t n = dev_count(n_cap, n_dev);
+    const int vec = row_bytes / 16;
+    const int64_t total = n * vec;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t r = t / vec;
+        int v = (int)(t - r * vec);
+        const int4 *s = reinterpret_cast<const int4 *>(src + (int64_t)perm[r] * ld_src) + v;
+        int4 *d = reinterpret_cast<int4 *>(dst + r * ld_dst) + v;
+        *d = __ldg(s);
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// A3 grouped downsampling: tagged keys (level << used_bits) | (v0 & mask_level)
+// ------------------------------------------------------------------------------------
+struct LevelMasks {
+    uint64_t mask[4];
+};
+
+__global__ void k_build_tagged(const uint64_t *__restrict__ v0, int64_t n_cap, const int64_t *n_dev, int L,
+                               LevelMasks m, int used_bits, uint64_t *__restrict__ tagged,
+                               int64_t *__restrict__ total_dev) {
+    const int64_t n = dev_count(n_cap, n_dev);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *total_dev = n * L;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * L; i += (int64_t)gridDim.x * blockDim.x) {
+        int l = (int)(i / n);
+        int64_t r = i - (int64_t)l * n;
+        tagged[i] = ((uint64_t)l << used_bits) | (v0[r] & m.mask[l]);
+    }
+}
+
+__global__ void __launch_bounds__(SORT_THREADS) k_unique_count(const uint64_t *__restrict__ k, const int64_t *total_dev,
+                                                               int *__restrict__ tile_cnt) {
+    __shared__ int ws[SORT_WARPS];
+    const int64_t total = *total_dev;
+    const int64_t base = (int64_t)blockIdx.x * SORT_TILE;
+    int c = 0;
+#pragma unroll
+    for (int it = 0; it < SORT_ITEMS; ++it) {
+        int64_t i = base + threadIdx.x * SORT_ITEMS + it;
+        if (i < total) c += (i == 0 || k[i] != k[i - 1]);
+    }
+    int tot;
+    block_excl_scan_256(c, ws, tot);
+    if (threadIdx.x == 0) tile_cnt[blockIdx.x] = tot;
+}
+
+// single CTA: scan tile counts, then the unique-prefix at each level boundary l*n
+__global__ void __launch_bounds__(1024) k_unique_scan(int *__restrict__ tile_cnt, int n_tiles,
+                                                      const uint64_t *__restrict__ k, const int64_t *total_dev,
+                                                      int64_t n_cap, const int64_t *n_dev, int L,
+                                                      int64_t *__restrict__ level_base, int64_t *__restrict__ level_n) {
+    __shared__ int wsum[32];
+    __shared__ int carry_s;
+    __shared__ int red[32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (threadIdx.x == 0) carry_s = 0;
+    __syncthreads();
+    for (int base = 0; base < n_tiles; base += 1024) {
+        int i = base + threadIdx.x;
+        int v = i < n_tiles ? tile_cnt[i] : 0;
+        int x = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[w] = x;
+        __syncthreads();
+        if (w == 0) {
+            int s = wsum[lane];
+            for (int o = 1; o < 32; o <<= 1) {
+                int y = __shfl_up_sync(0xffffffffu, s, o);
+                if (lane >= o) s += y;
+            }
+            wsum[lane] = s;
+        }
+        __syncthreads();
+        int carry = carry_s;
+        if (i < n_tiles) tile_cnt[i] = carry + (w > 0 ? wsum[w - 1] : 0) + x - v;
+        __syncthreads();
+        if (threadIdx.x == 0) carry_s = carry + wsum[31];
+        __syncthreads();
+    }
+    const int64_t total_unique = carry_s;
+    const int64_t n = dev_count(n_cap, n_dev);
+    const int64_t total = *total_dev;
+    for (int l = 0; l <= L; ++l) {
+        int64_t b = (int64_t)l * n;
+        int64_t pref;
+        if (b >= total) {
+            pref = total_unique;
+        } else {
+            int64_t tb = b / SORT_TILE;
+            int c = 0;
+            for (int64_t i = tb * SORT_TILE + threadIdx.x; i < b; i += 1024) c += (i == 0 || k[i] != k[i - 1]);
+            for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+            if (lane == 0) red[w] = c;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                int s = 0;
+                for (int q = 0; q < 32; ++q) s += red[q];
+                red[0] = s;
+            }
+            __syncthreads();
+            pref = (int64_t)tile_cnt[tb] + red[0];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) level_base[l] = pref;
+    }
+    __syncthreads();
+    if (threadIdx.x < L) level_n[threadIdx.x] = level_base[threadIdx.x + 1] - level_base[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(SORT_THREADS) k_unique_write(const uint64_t *__restrict__ k, const int64_t *total_dev,
+                                                               int64_t n_cap, const int64_t *n_dev,
+                                                               const int *__restrict__ tile_scan,
+                                                               const int64_t *__restrict__ level_base,
+                                                               uint64_t strip_mask, uint64_t *__restrict__ out,
+                                                               int64_t out_stride) {
+    __shared__ int ws[SORT_WARPS];
+    const int64_t total = *total_dev;
+    const int64_t n = dev_count(n_cap, n_dev);
+    const int64_t base = (int64_t)blockIdx.x * SORT_TILE;
+    if (base >= total) return;
+    int f[SORT_ITEMS];
+    int c = 0;
+#pragma unroll
+    for (int it = 0; it < SORT_ITEMS; ++it) {
+        int64_t i = base + threadIdx.x * SORT_ITEMS + it;
+        f[it] = (i < total) && (i == 0 || k[i] != k[i - 1]);
+        c += f[it];
+    }
+    int tot;
+    int pos = block_excl_scan_256(c, ws, tot) + tile_scan[blockIdx.x];
+#pragma unroll
+    for (int it = 0; it < SORT_ITEMS; ++it) {
+        int64_t i = base + threadIdx.x * SORT_ITEMS + it;
+        if (f[it]) {
+            int l = (int)(i / n);
+            out[(int64_t)l * out_stride + (pos - level_base[l])] = k[i] & strip_mask;
+            ++pos;
+        }
+    }
+}
+
+}  // namespace spc
+
+using namespace spc;
+
+extern "C" size_t spc_pack_sort_workspace_size(int64_t n) {
+    if (n < 0) n = 0;
+    return align_up(sizeof(uint64_t) * (size_t)n, 256) + radix_sort_workspace(n, true) + 256;
+}
+
+extern "C" spc_status spc_pack_sort(const int32_t *coords, int64_t n, spc_pack_spec spec, uint64_t *keys_out,
+                                    int32_t *perm_out, uint32_t *status, void *ws, size_t ws_bytes,
+                                    void *stream) {
+    SPC_CHECK_ARG(n >= 0, "n < 0");
+    if (n == 0) return SPC_OK;
+    SPC_CHECK_ARG(coords && keys_out, "null coords/keys_out");
+    SPC_CHECK_ARG(n < (int64_t)INT32_MAX, "n too large for int32 indices");
+    const int used = spec.bits_b + spec.bits_x + spec.bits_y + spec.bits_z;
+    SPC_CHECK_ARG(spec.bits_b >= 0 && spec.bits_x >= 2 && spec.bits_y >= 2 && spec.bits_z >= 2 && used <= 62,
+                  "bad pack spec");
+    if (ws_bytes < spc_pack_sort_workspace_size(n)) return fail(SPC_ERR_WORKSPACE, "spc_pack_sort: ws too small");
+    cudaStream_t st = as_stream(stream);
+    Bump b(ws, ws_bytes);
+    uint64_t *raw = b.take<uint64_t>((size_t)n);
+    void *rws = b.base + align_up(b.used, 256);
+    size_t rws_bytes = ws_bytes - align_up(b.used, 256);
+    PackDev pd{spec.bits_b, spec.bits_x, spec.bits_y, spec.bits_z};
+    int grid = (int)imin64((n + 255) / 256, 4 * 148);
+    k_pack<<<grid, 256, 0, st>>>(reinterpret_cast<const int4 *>(coords), n, pd, raw, status);
+    SPC_LAUNCH_CHECK("k_pack");
+    int32_t *perm = perm_out;
+    spc_status s = radix_sort(raw, nullptr, n, nullptr, used, keys_out, perm, rws, rws_bytes, st);
+    if (s != SPC_OK) return s;
+    if (status) {
+        k_flag_dups<<<grid, 256, 0, st>>>(keys_out, n, nullptr, status, SPC_FLAG_DUPLICATE);
+        SPC_LAUNCH_CHECK("k_flag_dups");
+    }
+    return SPC_OK;
+}
+
+extern "C" spc_status spc_gather_rows(const void *src, int64_t ld_src_bytes, const int32_t *perm, int64_t n,
+                                      const int64_t *n_dev, int32_t row_bytes, void *dst, int64_t ld_dst_bytes,
+                                      void *stream) {
+    SPC_CHECK_ARG(n >= 0, "n < 0");
+    if (n == 0) return SPC_OK;
+    SPC_CHECK_ARG(src && perm && dst, "null pointer");
+    SPC_CHECK_ARG(row_bytes > 0 && row_bytes % 16 == 0 && ld_src_bytes % 16 == 0 && ld_dst_bytes % 16 == 0 &&
+                      ((uintptr_t)src % 16) == 0 && ((uintptr_t)dst % 16) == 0,
+                  "rows must be 16-byte aligned multiples of 16 bytes");
+    int64_t work = n * (row_bytes / 16);
+    int grid = (int)imin64((work + 255) / 256, 8 * 148);
+    k_gather_rows<<<grid, 256, 0, as_stream(stream)>>>((const char *)src, ld_src_bytes, perm, n, n_dev, row_bytes,
+                                                      (char *)dst, ld_dst_bytes);
+    SPC_LAUNCH_CHECK("k_gather_rows");
+    return SPC_OK;
+}
+
+extern "C" size_t spc_downsample_workspace_size(int64_t n, int32_t n_levels) {
+    if (n < 0) n = 0;
+    int64_t tot = n * (n_levels > 0 ? n_levels : 1);
+    Sizer s;
+    s.take<uint64_t>((size_t)tot);       // tagged
+    s.take<uint64_t>((size_t)tot);       // sorted tagged
+    s.take<int64_t>(8);                  // total, level_base
+    s.take<int>((size_t)(tot / SORT_TILE + 2));
+    return s.used + radix_sort_workspace(tot, false) + 512;
+}
+
+extern "C" spc_status spc_downsample(const uint64_t *keys, int64_t n, const int64_t *n_dev, spc_pack_spec spec,
+                                     int32_t n_levels, const int32_t *log2_stride_host, uint64_t *level_keys,
+                                     int64_t *level_n_dev, void *ws, size_t ws_bytes, void *stream) {
+    SPC_CHECK_ARG(n >= 0 && n_levels >= 1 && n_levels <= 4, "n < 0 or n_levels not in 1..4");
+    SPC_CHECK_ARG(log2_stride_host && level_keys && level_n_dev && (keys || n == 0), "null pointer");
+    const int minb = min(spec.bits_x, min(spec.bits_y, spec.bits_z));
+    LevelMasks lm{};
+    for (int l = 0; l < n_levels; ++l) {
+        int m = log2_stride_host[l];
+        if (m < 0 || m > minb - 1)
+            return fail(SPC_ERR_INVALID_ARG, "spc_downsample: log2 stride " + std::to_string(m) + " out of range");
+        lm.mask[l] = spc_downsample_mask(spec, m);
+    }
+    if (ws_bytes < spc_downsample_workspace_size(n, n_levels))
+        return fail(SPC_ERR_WORKSPACE, "spc_downsample: ws too small");
+    cudaStream_t st = as_stream(stream);
+    if (n == 0) {
+        SPC_CUDA(cudaMemsetAsync(level_n_dev, 0, sizeof(int64_t) * n_levels, st));
+        return SPC_OK;
+    }
+    const int used = spec.bits_b + spec.bits_x + spec.bits_y + spec.bits_z;
+    const int64_t tot = n * n_levels;
+    Bump b(ws, ws_bytes);
+    uint64_t *tagged = b.take<uint64_t>((size_t)tot);
+    uint64_t *sorted = b.take<uint64_t>((size_t)tot);
+    int64_t *scal = b.take<int64_t>(8);   // [0] total, [1..5] level_base
+    const int nt = (int)((tot + SORT_TILE - 1) / SORT_TILE);
+    int *tile_cnt = b.take<int>((size_t)(tot / SORT_TILE + 2));
+    void *rws = b.base + align_up(b.used, 256);
+    size_t rws_bytes = ws_bytes - align_up(b.used, 256);
+    int grid = (int)imin64((tot + 255) / 256, 8 * 148);
+    k_build_tagged<<<grid, 256, 0, st>>>(keys, n, n_dev, n_levels, lm, used, tagged, scal);
+    SPC_LAUNCH_CHECK("k_build_tagged");
+    const int tag_bits = n_levels > 2 ? 2 : (n_levels > 1 ? 1 : 0);
+    spc_status s = radix_sort(tagged, nullptr, tot, scal, used + tag_bits, sorted, nullptr, rws, rws_bytes, st);
+    if (s != SPC_OK) return s;
+    k_unique_count<<<nt, SORT_THREADS, 0, st>>>(sorted, scal, tile_cnt);
+    k_unique_scan<<<1, 1024, 0, st>>>(tile_cnt, nt, sorted, scal, n, n_dev, n_levels, scal + 1, level_n_dev);
+    const uint64_t strip = used >= 64 ? ~0ull : ((1ull << used) - 1);
+    k_unique_write<<<nt, SORT_THREADS, 0, st>>>(sorted, scal, n, n_dev, tile_cnt, scal + 1, strip, level_keys, n);
+    SPC_LAUNCH_CHECK("unique");
+    return SPC_OK;
+}

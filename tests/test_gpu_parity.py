@@ -1,0 +1,311 @@
+"""GPU parity: every step of the CUDA hot path (through the C ABI) against the CPU oracle.
+
+Integer work (keys, permutation, downsampled sets, kernel maps) must be bit-exact;
+features within north_star's tolerance: max|gpu - ref| <= 2e-3 * max|ref| for f16/bf16
+inputs (fp32 output), <= 1e-5 * max|ref| for the fp32 path; bf16/f16-stored outputs are
+checked against round(ref) to within one unit in the last place (reading A18).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+import paper_2511_20834_b200 as spc
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def _spec_for(coords, max_stride=16, reach=16):
+    lo = coords[:, 1:].min(0)
+    hi = coords[:, 1:].max(0)
+    nb = int(coords[:, 0].max()) + 1
+    return spc.spc_plan_pack(lo, hi, nb, max_stride, reach)
+
+
+def _pack_sort(coords, spec):
+    c = torch.from_numpy(np.ascontiguousarray(coords, dtype=np.int32)).to(DEV)
+    keys, perm, status = spc.spc_pack_sort(c, spec)
+    torch.cuda.synchronize()
+    return keys, perm, int(status.item())
+
+
+def _keys_of(coords_sorted, spec):
+    k, bad = oracle.pack(coords_sorted, spec.astuple())
+    assert bad == 0
+    return k.view(np.int64)
+
+
+# ---------------------------------------------------------------------------------------
+# A1 + A2
+# ---------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("case", ["c1", "random_batched", "tiny", "one"])
+def test_pack_sort_bit_exact(case):
+    if case == "c1":
+        coords = synth.make_scan(1, 0)
+    elif case == "random_batched":
+        coords = synth.random_cloud(50_000, 600, seed=3, n_batch=5)
+    elif case == "tiny":
+        coords = synth.random_cloud(37, 20, seed=4)
+    else:
+        coords = np.array([[0, 5, -3, 2]], np.int32)
+    spec = _spec_for(coords)
+    keys, perm, status = _pack_sort(coords, spec)
+    s, p, dups = oracle.sort_coords(coords)
+    assert dups == 0 and status == 0
+    np.testing.assert_array_equal(keys.cpu().numpy(), _keys_of(s, spec))
+    np.testing.assert_array_equal(perm.cpu().numpy(), p)
+
+
+def test_pack_sort_flags_duplicates_and_range():
+    coords = synth.random_cloud(3000, 100, seed=9)
+    dup = np.concatenate([coords, coords[:5]])
+    spec = _spec_for(coords)
+    _, _, status = _pack_sort(dup, spec)
+    assert status & spc.SPC_FLAG_DUPLICATE
+    bad = coords.copy()
+    bad[7, 1] = 1 << (spec.bits_x - 1)          # one past the top of the x field
+    _, _, status = _pack_sort(bad, spec)
+    assert status & spc.SPC_FLAG_RANGE
+
+
+def test_gather_rows():
+    coords = synth.random_cloud(5000, 200, seed=1)
+    spec = _spec_for(coords)
+    keys, perm, _ = _pack_sort(coords, spec)
+    F = torch.randn(5000, 48, device=DEV).to(torch.bfloat16)
+    out = spc.spc_gather_rows(F, perm)
+    torch.testing.assert_close(out, F[perm.long()], rtol=0, atol=0)
+
+
+# ---------------------------------------------------------------------------------------
+# A3
+# ---------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("config", [1, 2])
+def test_downsample_levels_bit_exact(config):
+    coords = synth.make_scan(config, 0)
+    spec = _spec_for(coords)
+    keys, _, _ = _pack_sort(coords, spec)
+    lv, ln = spc.spc_downsample(keys, spec, [1, 2, 3, 4])
+    torch.cuda.synchronize()
+    ln = ln.cpu().numpy()
+    for l, m in enumerate([1, 2, 3, 4]):
+        ref = oracle.downsample(coords, 2 ** m)
+        assert ln[l] == len(ref)
+        np.testing.assert_array_equal(lv[l, :ln[l]].cpu().numpy(), _keys_of(ref, spec))
+
+
+# ---------------------------------------------------------------------------------------
+# A4-A8 kernel maps
+# ---------------------------------------------------------------------------------------
+
+def _levels(coords, spec, strides):
+    keys, _, _ = _pack_sort(coords, spec)
+    out = {1: (keys, oracle.sort_coords(coords)[0])}
+    for s in strides:
+        c = oracle.downsample(coords, s)
+        k = torch.from_numpy(_keys_of(c, spec)).to(DEV)
+        out[s] = (k, c)
+    return out
+
+
+MAP_CASES = [
+    # (K, dilation, kind, t, flags)
+    (3, 1, "subm", -1, 0), (3, 1, "subm", 0, 0), (3, 1, "subm", 2, 0), (3, 1, "subm", 0, 1), (3, 1, "subm", 2, 1),
+    (5, 1, "subm", -1, 0), (5, 1, "subm", 3, 0), (5, 1, "subm", 3, 1), (5, 1, "subm", 0, 1),
+    (1, 1, "subm", -1, 0), (3, 2, "subm", 2, 1),
+    (3, 1, "strided", -1, 0), (3, 1, "strided", 0, 0), (3, 1, "strided", 2, 0), (5, 1, "strided", 3, 0),
+    (3, 1, "transposed", -1, 0), (3, 1, "transposed", 2, 0),
+]
+
+
+@pytest.mark.parametrize("K,d,kind,t,flags", MAP_CASES)
+def test_kmap_bit_exact(K, d, kind, t, flags):
+    coords = synth.make_scan(1, 1)
+    spec = _spec_for(coords)
+    lv = _levels(coords, spec, [2])
+    fine_k, fine_c = lv[1]
+    coarse_k, coarse_c = lv[2]
+    if kind == "subm":
+        g = spc.Geom(K, 1, d, 1, 0)
+        km = spc.spc_build_kmap(fine_k, fine_k, spec, g, t, flags | spc.SPC_KMAP_COUNT_SEARCHES)
+        ref = oracle.kmap(fine_c, fine_c, K, d)
+        n_out = len(fine_c)
+    elif kind == "strided":
+        g = spc.Geom(K, 2, d, 1, 0)
+        km = spc.spc_build_kmap(fine_k, coarse_k, spec, g, t, flags)
+        ref = oracle.kmap(fine_c, coarse_c, K, d)
+        n_out = len(coarse_c)
+    else:
+        g = spc.Geom(K, 2, d, 1, 1)
+        km = spc.spc_build_kmap(coarse_k, fine_k, spec, g, t, flags)
+        ref = oracle.kmap(coarse_c, fine_c, K, d, transposed=True)
+        n_out = len(fine_c)
+    got = spc.spc_kmap_export(km)
+    np.testing.assert_array_equal(got, ref)
+    if kind == "subm":
+        st = km.search_stats().cpu().numpy()
+        if not (flags & 1):
+            assert st[0] == n_out * K * K                              # P:297 |V_q| K^2 searches
+            assert st[1] <= n_out * K * K * (K - 1) * d                # <= (K-1)d advances each
+        else:
+            assert st[0] <= n_out * K * K                              # halving skips groups
+
+
+def test_kmap_os_table_exact_and_centre():
+    coords = synth.make_scan(1, 0)
+    spec = _spec_for(coords)
+    keys, _, _ = _pack_sort(coords, spec)
+    c = oracle.sort_coords(coords)[0]
+    km = spc.spc_build_kmap(keys, keys, spec, spc.Geom(3, 1, 1, 1, 0), -1, 0)
+    tab = km.os_table().cpu().numpy()
+    ref = np.full((len(c), 27), -1, np.int32)
+    tr = oracle.kmap(c, c, 3, 1)
+    ref[tr[:, 1], tr[:, 0]] = tr[:, 2]
+    np.testing.assert_array_equal(tab, ref)
+    assert (tab[:, 13] == np.arange(len(c))).all()          # centre maps i -> i
+
+
+def test_kmap_edge_cases():
+    spec = spc.PackSpec(0, 8, 8, 8)
+    one = torch.tensor([(128 << 16) | (128 << 8) | 128], dtype=torch.int64, device=DEV)
+    km = spc.spc_build_kmap(one, one, spec, spc.Geom(3, 1, 1, 1, 0), -1, 0)
+    assert spc.spc_kmap_export(km).tolist() == [[13, 0, 0]]
+    empty = torch.empty(0, dtype=torch.int64, device=DEV)
+    km = spc.spc_build_kmap(one, empty, spec, spc.Geom(3, 1, 1, 1, 0), -1, 0)
+    assert spc.spc_kmap_export(km).shape == (0, 3)
+    km = spc.spc_build_kmap(empty, one, spec, spc.Geom(3, 1, 1, 1, 0), 0, 0)
+    assert spc.spc_kmap_export(km).shape == (0, 3)
+    with pytest.raises(spc.SpcError):
+        spc.spc_build_kmap(one, one, spec, spc.Geom(4, 1, 1, 1, 0), -1, 0)
+
+
+def test_network_kmaps_equal_sequential():
+    coords = synth.make_scan(1, 0)
+    spec = _spec_for(coords)
+    keys, _, _ = _pack_sort(coords, spec)
+    geoms = [spc.Geom(3, 1, 1, 1, 0), spc.Geom(3, 2, 1, 1, 0), spc.Geom(3, 1, 1, 2, 0), spc.Geom(3, 2, 1, 2, 0),
+             spc.Geom(3, 1, 1, 4, 0), spc.Geom(3, 2, 1, 2, 1), spc.Geom(3, 2, 1, 1, 1), spc.Geom(3, 1, 1, 1, 0)]
+    ts = [-1, 0, 2, -1, 0, -1, 2, -1]
+    lk, ln, maps, _ = spc.spc_network_kmaps(keys, spec, 4, geoms, ts)
+    c = oracle.sort_coords(coords)[0]
+    lv = {1: c, 2: oracle.downsample(c, 2), 4: oracle.downsample(c, 4), 8: oracle.downsample(c, 8)}
+    assert ln.cpu().tolist() == [len(lv[1]), len(lv[2]), len(lv[4]), len(lv[8])]
+    for g, km in zip(geoms, maps):
+        fine, coarse = lv[g.tensor_stride], lv[g.tensor_stride * g.stride]
+        if g.transposed:
+            ref = oracle.kmap(coarse, fine, 3, g.tensor_stride, transposed=True)
+        else:
+            ref = oracle.kmap(fine, coarse, 3, g.tensor_stride)
+        np.testing.assert_array_equal(spc.spc_kmap_export(km), ref)
+
+
+# ---------------------------------------------------------------------------------------
+# A9-A12 features
+# ---------------------------------------------------------------------------------------
+
+def _rel_err(got, ref):
+    m = np.abs(ref).max()
+    return np.abs(got - ref).max() / (m if m > 0 else 1.0)
+
+
+CONV_CASES = [
+    # (K, kind, t, flags, c_in, c_out, dtype)
+    (3, "subm", -1, 0, 16, 16, "bf16"), (3, "subm", 0, 1, 32, 32, "bf16"), (3, "subm", 2, 1, 64, 96, "bf16"),
+    (3, "subm", 2, 0, 32, 64, "f16"), (5, "subm", 3, 1, 32, 32, "bf16"), (5, "subm", -1, 0, 16, 16, "bf16"),
+    (3, "subm", -1, 0, 128, 128, "bf16"), (3, "subm", 0, 1, 256, 256, "bf16"), (1, "subm", -1, 0, 96, 32, "bf16"),
+    (3, "strided", -1, 0, 32, 64, "bf16"), (3, "strided", 0, 0, 64, 64, "bf16"),
+    (3, "transposed", -1, 0, 64, 32, "bf16"), (3, "transposed", 2, 0, 48, 384, "bf16"),
+    (3, "subm", 2, 1, 16, 32, "f32"), (3, "strided", 0, 0, 32, 16, "f32"),
+]
+
+
+@pytest.mark.parametrize("K,kind,t,flags,c_in,c_out,dt", CONV_CASES)
+def test_conv_forward_matches_eq2(K, kind, t, flags, c_in, c_out, dt):
+    coords = synth.make_scan(1, 0)[:6000]
+    spec = _spec_for(coords)
+    lv = _levels(coords, spec, [2])
+    fine_k, fine_c = lv[1]
+    coarse_k, coarse_c = lv[2]
+    if kind == "subm":
+        inp_k, inp_c, out_k, out_c, g = fine_k, fine_c, fine_k, fine_c, spc.Geom(K, 1, 1, 1, 0)
+    elif kind == "strided":
+        inp_k, inp_c, out_k, out_c, g = fine_k, fine_c, coarse_k, coarse_c, spc.Geom(K, 2, 1, 1, 0)
+    else:
+        inp_k, inp_c, out_k, out_c, g = coarse_k, coarse_c, fine_k, fine_c, spc.Geom(K, 2, 1, 1, 1)
+    km = spc.spc_build_kmap(inp_k, out_k, spec, g, t, flags)
+    F = synth.make_features(len(inp_c), c_in, seed=c_in + K, dtype=dt)
+    W = synth.make_weights(K ** 3, c_in, c_out, seed=c_out + K, nnz_per_out=10, dtype=dt)
+    tdt = {"bf16": torch.bfloat16, "f16": torch.float16, "f32": torch.float32}[dt]
+    Fg = torch.from_numpy(F).to(DEV).to(tdt)
+    Wg = spc.spc_prepare_weight(torch.from_numpy(W).to(DEV).to(tdt))
+    out = spc.spc_conv_forward(km, Fg, Wg, c_in, c_out, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    ref = oracle.conv(inp_c, out_c, K, 1, F.astype(np.float64), W.astype(np.float64),
+                      transposed=(kind == "transposed"))
+    err = _rel_err(out.cpu().numpy().astype(np.float64), ref)
+    tol = 1e-5 if dt == "f32" else 2e-3
+    assert err <= tol, err
+
+
+def test_conv_bf16_output_and_residual():
+    coords = synth.make_scan(1, 0)[:5000]
+    spec = _spec_for(coords)
+    keys, _, _ = _pack_sort(coords, spec)
+    c = oracle.sort_coords(coords)[0]
+    for t, flags in ((-1, 0), (1, 1)):
+        km = spc.spc_build_kmap(keys, keys, spec, spc.Geom(3, 1, 1, 1, 0), t, flags)
+        F = synth.make_features(len(c), 32, seed=1)
+        W = synth.make_weights(27, 32, 32, seed=2, nnz_per_out=10)
+        R = synth.make_features(len(c), 32, seed=3)
+        Fg = torch.from_numpy(F).to(DEV).bfloat16()
+        Rg = torch.from_numpy(R).to(DEV).bfloat16()
+        Wg = spc.spc_prepare_weight(torch.from_numpy(W).to(DEV).bfloat16())
+        out = spc.spc_conv_forward(km, Fg, Wg, 32, 32, out_dtype=torch.bfloat16, residual=Rg)
+        ref = oracle.conv(c, c, 3, 1, F, W) + R.astype(np.float64)
+        got = out.float().cpu().numpy().astype(np.float64)
+        # one bf16 ulp of the reference value (2^-7 relative to its binade) + fp32 slack
+        ulp = np.exp2(np.floor(np.log2(np.maximum(np.abs(ref), 1e-30))) - 7)
+        assert (np.abs(got - ref) <= ulp + 1e-6 * np.abs(ref).max()).all()
+
+
+def test_conv_channel_slices():
+    """ld_in / ld_out > c: read from and write into column slices (free skip concat)."""
+    coords = synth.make_scan(1, 0)[:4000]
+    spec = _spec_for(coords)
+    keys, _, _ = _pack_sort(coords, spec)
+    c = oracle.sort_coords(coords)[0]
+    km = spc.spc_build_kmap(keys, keys, spec, spc.Geom(3, 1, 1, 1, 0), 2, 1)
+    F = synth.make_features(len(c), 64, seed=5)
+    W = synth.make_weights(27, 32, 48, seed=6, nnz_per_out=10)
+    Fg = torch.from_numpy(F).to(DEV).bfloat16()
+    big = torch.zeros(len(c), 96, dtype=torch.float32, device=DEV)
+    Wg = spc.spc_prepare_weight(torch.from_numpy(W).to(DEV).bfloat16())
+    spc.spc_conv_forward(km, Fg[:, 32:], Wg, 32, 48, out=big[:, 16:64])
+    ref = oracle.conv(c, c, 3, 1, F[:, 32:], W)
+    got = big.cpu().numpy()
+    assert _rel_err(got[:, 16:64].astype(np.float64), ref) <= 2e-3
+    assert not got[:, :16].any() and not got[:, 64:].any()
+
+
+@pytest.mark.slow
+def test_full_size_c2_sampled_parity():
+    """Config C2 (~100k voxels) in the launch configuration bench.py uses: full kernel
+    map bit-exact, features on 2048 sampled output rows."""
+    coords = synth.make_scan(2, 0)
+    spec = _spec_for(coords)
+    keys, perm, st = _pack_sort(coords, spec)
+    c = oracle.sort_coords(coords)[0]
+    km = spc.spc_build_kmap(keys, keys, spec, spc.Geom(3, 1, 1, 1, 0), 2, 1)
+    np.testing.assert_array_equal(spc.spc_kmap_export(km), oracle.kmap(c, c, 3, 1))
+    F = synth.make_features(len(c), 64, seed=7)
+    W = synth.make_weights(27, 64, 64, seed=8, nnz_per_out=10)
+    out = spc.spc_conv_forward(km, torch.from_numpy(F).to(DEV).bfloat16(),
+                               spc.spc_prepare_weight(torch.from_numpy(W).to(DEV).bfloat16()), 64, 64,
+                               out_dtype=torch.float32)
+    rows = np.random.default_rng(0).choice(len(c), 2048, replace=False)
+    ref = oracle.conv_rows(c, c, rows, 3, 1, F, W)
+    assert _rel_err(out.cpu().numpy()[rows].astype(np.float64), ref) <= 2e-3
