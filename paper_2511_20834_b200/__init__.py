@@ -15,7 +15,7 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libspc.so")
+LIB_PATH = os.environ.get("SPC_LIB_OVERRIDE") or os.path.join(_HERE, "libspc.so")   # override: experiments only
 
 SPC_OK = 0
 SPC_F32, SPC_F16, SPC_BF16 = 0, 1, 2
@@ -340,26 +340,44 @@ def spc_conv_forward(km: KernelMap, f_in: torch.Tensor, weight_prepared: torch.T
 # A13
 # ---------------------------------------------------------------------------------------
 
+class NetworkIndex:
+    """Pre-allocated state of spc_network_kmaps for one (n0, n_levels, map list): the
+    workspace, the level key / count buffers and the C kmap structs.  ``run()`` only
+    enqueues work (no allocation), so it can be captured in a CUDA graph."""
+
+    def __init__(self, n0: int, spec: PackSpec, n_levels: int, geoms, ts, flags=None, device="cuda"):
+        self.n0, self.spec, self.n_levels = int(n0), spec, int(n_levels)
+        n = len(geoms)
+        self.n = n
+        self.G = (Geom * max(n, 1))(*geoms)
+        self.T = (ctypes.c_int32 * max(n, 1))(*[int(t) for t in ts])
+        self.F = (ctypes.c_uint32 * max(n, 1))(*[int(f) for f in (flags or [0] * n)])
+        need = int(lib().spc_network_workspace_size(self.n0, self.n_levels, self.G, self.T, self.F, n))
+        ws = torch.empty(need + 256, dtype=torch.uint8, device=device)
+        off = (-ws.data_ptr()) % 256
+        self._ws_full = ws
+        self.ws = ws[off:off + need]
+        self.level_keys = torch.empty((self.n_levels, self.n0), dtype=torch.int64, device=device)
+        self.level_n = torch.empty(self.n_levels, dtype=torch.int64, device=device)
+        self.structs = (_Kmap * max(n, 1))()
+        self.maps = [None] * n
+
+    def run(self, v0_keys: torch.Tensor, n0_dev=None, status=None, stream=None):
+        _check(lib().spc_network_kmaps(_ptr(v0_keys), self.n0, _ptr(n0_dev), self.spec, self.n_levels, self.G, self.T,
+                                       self.F, self.n, _ptr(self.level_keys), _ptr(self.level_n), self.structs,
+                                       _ptr(status), _ptr(self.ws), self.ws.numel(), _stream(stream)),
+               "spc_network_kmaps")
+        if self.maps[0] is None or self.n == 0:
+            self.maps = [KernelMap(self.structs[i], self.ws, (v0_keys, self.level_keys, self.level_n))
+                         for i in range(self.n)]
+        return self.maps
+
+
 def spc_network_kmaps(v0_keys: torch.Tensor, spec: PackSpec, n_levels: int, geoms, ts, flags=None, n0_dev=None,
-                      status=None, ws=None, stream=None):
-    """Network-wide indexing -> (level_keys [n_levels, n0], level_n [n_levels], [KernelMap per entry], ws)."""
-    n0 = v0_keys.shape[0]
-    dev = v0_keys.device
-    n = len(geoms)
-    G = (Geom * max(n, 1))(*geoms)
-    T = (ctypes.c_int32 * max(n, 1))(*[int(t) for t in ts])
-    F = (ctypes.c_uint32 * max(n, 1))(*[int(f) for f in (flags or [0] * n)])
-    L = lib()
-    need = int(L.spc_network_workspace_size(n0, n_levels, G, T, F, n))
-    if ws is None or ws.numel() < need + 256:
-        ws = torch.empty(need + 256, dtype=torch.uint8, device=dev)
-    off = (-ws.data_ptr()) % 256
-    wsa = ws[off:]
-    level_keys = torch.empty((n_levels, n0), dtype=torch.int64, device=dev)
-    level_n = torch.empty(n_levels, dtype=torch.int64, device=dev)
-    maps = (_Kmap * max(n, 1))()
-    _check(L.spc_network_kmaps(_ptr(v0_keys), n0, _ptr(n0_dev), spec, int(n_levels), G, T, F, n, _ptr(level_keys),
-                               _ptr(level_n), maps, _ptr(status), _ptr(wsa), wsa.numel(), _stream(stream)),
-           "spc_network_kmaps")
-    kms = [KernelMap(maps[i], wsa, (v0_keys, level_keys, level_n)) for i in range(n)]
-    return level_keys, level_n, kms, ws
+                      status=None, stream=None):
+    """Network-wide indexing -> (level_keys [n_levels, n0], level_n [n_levels], [KernelMap per entry])."""
+    ni = NetworkIndex(v0_keys.shape[0], spec, n_levels, geoms, ts, flags, device=v0_keys.device)
+    maps = ni.run(v0_keys, n0_dev=n0_dev, status=status, stream=stream)
+    for m in maps:
+        m._keep = m._keep + (ni,)
+    return ni.level_keys, ni.level_n, maps

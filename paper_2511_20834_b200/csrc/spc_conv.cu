@@ -20,6 +20,8 @@
 // meet it, reading A19).
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include "spc_common.cuh"
@@ -27,13 +29,14 @@
 
 namespace spc {
 
-constexpr int TC_THREADS = 320;
+constexpr int TC_THREADS = 352;   // 11 warps: 4 gather, 4 epilogue, MMA, weight loader, scheduler
 constexpr int TC_BM = 128;
 constexpr int TC_SMEM_BUDGET = 225 * 1024;
 
 enum OutKind : int { OUT_FINAL = 0, OUT_F32_STORE = 1, OUT_F32_RED = 2 };
 
 struct ConvParams {
+    CUtensorMap tmap_a;   // f_in rows: 2-D {c_in, n_in}, box {BK, 1}, swizzle rb = 2*BK bytes
     int mode;   // 0 = OS part, 1 = WS part
     // map
     const int32_t *os;
@@ -110,8 +113,14 @@ __device__ __forceinline__ void decode_tile(const ConvParams &p, int64_t v, cons
 }
 
 __device__ __forceinline__ int next_bit(const uint32_t (&m)[4], int from) {
-    for (int c = from; c < 128; ++c)
-        if (m[c >> 5] >> (c & 31) & 1u) return c;
+    if (from >= 128) return -1;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+        if (w < (from >> 5)) continue;
+        uint32_t word = m[w];
+        if (w == (from >> 5)) word &= ~0u << (from & 31);
+        if (word) return w * 32 + __ffs(word) - 1;
+    }
     return -1;
 }
 
@@ -130,32 +139,33 @@ __device__ __forceinline__ float2 unpack2(uint32_t u, int dt) {
     return __half22float2(*reinterpret_cast<__half2 *>(&u));
 }
 
-// store 'n' (16 or 32) fp32 values of one row to the output
+// store 'n' (16 or 32) fp32 values of one row to the output (fully unrolled: registers only)
 __device__ __forceinline__ void store_row(const ConvParams &p, int64_t row, int col, const uint32_t (&v)[32], int n) {
     if (p.out_kind == OUT_FINAL && p.out_dtype != SPC_F32) {
-        uint32_t packed[16];
-        float res[32];
-        if (p.residual) {
-            const uint4 *rp = reinterpret_cast<const uint4 *>(static_cast<const uint16_t *>(p.residual) + row * p.ld_res + col);
-            for (int q = 0; q < n / 8; ++q) {
-                uint4 u = rp[q];
-                uint32_t w[4] = {u.x, u.y, u.z, u.w};
-                for (int e = 0; e < 4; ++e) {
-                    float2 f = unpack2(w[e], p.out_dtype);
-                    res[q * 8 + 2 * e] = f.x;
-                    res[q * 8 + 2 * e + 1] = f.y;
-                }
-            }
-        } else {
-            for (int e = 0; e < 32; ++e) res[e] = 0.f;
-        }
-#pragma unroll
-        for (int e = 0; e < 16; ++e)
-            if (2 * e < n) packed[e] = pack2(to_f(v[2 * e]) + res[2 * e], to_f(v[2 * e + 1]) + res[2 * e + 1], p.out_dtype);
+        const uint4 *rp = p.residual
+                              ? reinterpret_cast<const uint4 *>(static_cast<const uint16_t *>(p.residual) + row * p.ld_res + col)
+                              : nullptr;
         uint4 *op = reinterpret_cast<uint4 *>(static_cast<uint16_t *>(p.out) + row * p.ld_out + col);
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-            if (q * 8 < n) op[q] = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+        for (int q = 0; q < 4; ++q) {
+            if (q * 8 < n) {
+                float f[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) f[e] = to_f(v[q * 8 + e]);
+                if (rp) {
+                    const uint4 u = rp[q];
+                    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float2 r2 = unpack2(w[e], p.out_dtype);
+                        f[2 * e] += r2.x;
+                        f[2 * e + 1] += r2.y;
+                    }
+                }
+                op[q] = make_uint4(pack2(f[0], f[1], p.out_dtype), pack2(f[2], f[3], p.out_dtype),
+                                   pack2(f[4], f[5], p.out_dtype), pack2(f[6], f[7], p.out_dtype));
+            }
+        }
     } else {
         float *op = static_cast<float *>(p.out) + row * p.ld_out + col;
         const float *rp = (p.out_kind == OUT_FINAL && p.residual)
@@ -163,44 +173,84 @@ __device__ __forceinline__ void store_row(const ConvParams &p, int64_t row, int 
                               : nullptr;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-            if (q * 4 >= n) break;
-            float4 o = make_float4(to_f(v[4 * q]), to_f(v[4 * q + 1]), to_f(v[4 * q + 2]), to_f(v[4 * q + 3]));
-            if (rp) {
-                float4 r = reinterpret_cast<const float4 *>(rp)[q];
-                o.x += r.x; o.y += r.y; o.z += r.z; o.w += r.w;
+            if (q * 4 < n) {
+                float4 o = make_float4(to_f(v[4 * q]), to_f(v[4 * q + 1]), to_f(v[4 * q + 2]), to_f(v[4 * q + 3]));
+                if (rp) {
+                    const float4 r = reinterpret_cast<const float4 *>(rp)[q];
+                    o.x += r.x; o.y += r.y; o.z += r.z; o.w += r.w;
+                }
+                reinterpret_cast<float4 *>(op)[q] = o;
             }
-            reinterpret_cast<float4 *>(op)[q] = o;
         }
     }
 }
 
+
+// ---- shared-memory records produced by the scheduler warp ------------------------------
+constexpr int TREC_SLOTS = 4;      // tile records in flight
+constexpr int IDX_SLOTS = 16;      // per-(tile, offset) gather-index slots in flight
+constexpr int TREC_CONSUMERS = 10; // gather warps 4 + epilogue warps 4 + MMA 1 + weight loader 1
+constexpr int W_MMA = 8, W_BLOAD = 9, W_SCHED = 10;
+
+struct TileRec {
+    int64_t row0;
+    int rows, nt, list, dir, k, end;
+    uint32_t mask[4];
+    int32_t scatter[TC_BM];   // WS: output row of each pair row (OS: unused)
+};
+
+struct ConvSmem {
+    uint64_t full[8], empty[8], tfull[2], tempty[2];
+    uint64_t trec_full[TREC_SLOTS], trec_empty[TREC_SLOTS];
+    uint64_t idx_full[IDX_SLOTS], idx_empty[IDX_SLOTS];
+    uint32_t tmem_holder[4];
+    int list_prefix[SPC_MAX_KVOL + 1];
+    TileRec trec[TREC_SLOTS];
+    alignas(16) int32_t idx[IDX_SLOTS][TC_BM];
+};
+
+#ifdef SPC_EXP_TRACE
+__device__ long long g_tr[8][4096];
+#define TR(slot, i) do { if (blockIdx.x == 0 && (i) < 4096) g_tr[slot][(i)] = clock64(); } while (0)
+#else
+#define TR(slot, i) do {} while (0)
+#endif
+
+template <int BK>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant__ ConvParams p) {
-    extern __shared__ __align__(1024) uint8_t smem[];
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // stage buffers need 1024-byte alignment (swizzle atoms)
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int S = p.stages;
     uint8_t *sa = smem;
     uint8_t *sb = smem + (size_t)S * p.a_bytes;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(sb + (size_t)S * p.b_bytes);
-    uint64_t *full = bars, *empty = bars + S, *tfull = bars + 2 * S, *tempty = bars + 2 * S + 2;
-    uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 2 * S + 4);
-    int *list_prefix = reinterpret_cast<int *>(tmem_holder + 4);   // [SPC_MAX_KVOL + 1]
+    ConvSmem &cs = *reinterpret_cast<ConvSmem *>(sb + (size_t)S * p.b_bytes);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t n_out = dev_count(p.n_out_cap, p.n_out_dev);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
-            ptx::mbar_init(ptx::smem_u32(&full[s]), TC_BM + 1);
-            ptx::mbar_init(ptx::smem_u32(&empty[s]), 1);
+            ptx::mbar_init(ptx::smem_u32(&cs.full[s]), TC_BM + 1);   // 128 gather threads + weight expect_tx
+            ptx::mbar_init(ptx::smem_u32(&cs.empty[s]), 1);
         }
         for (int a = 0; a < 2; ++a) {
-            ptx::mbar_init(ptx::smem_u32(&tfull[a]), 1);
-            ptx::mbar_init(ptx::smem_u32(&tempty[a]), 4);
+            ptx::mbar_init(ptx::smem_u32(&cs.tfull[a]), 1);
+            ptx::mbar_init(ptx::smem_u32(&cs.tempty[a]), 4);
+        }
+        for (int i = 0; i < TREC_SLOTS; ++i) {
+            ptx::mbar_init(ptx::smem_u32(&cs.trec_full[i]), 32);
+            ptx::mbar_init(ptx::smem_u32(&cs.trec_empty[i]), TREC_CONSUMERS);
+        }
+        for (int i = 0; i < IDX_SLOTS; ++i) {
+            ptx::mbar_init(ptx::smem_u32(&cs.idx_full[i]), 32);
+            ptx::mbar_init(ptx::smem_u32(&cs.idx_empty[i]), 4);
         }
         ptx::fence_mbar_init();
         ptx::fence_proxy_async();
     }
-    if (warp == 9) ptx::tmem_alloc(ptx::smem_u32(tmem_holder), 2 * p.tmem_cols);
-    if (p.mode == 1 && warp == 0) {
+    if (warp == W_MMA) ptx::tmem_alloc(ptx::smem_u32(cs.tmem_holder), 2 * p.tmem_cols);
+    if (p.mode == 1 && warp == W_SCHED) {
         // virtual-tile prefix over the WS lists (device-side counts, no host sync)
         int carry = 0;
         for (int base = 0; base < p.n_lists; base += 32) {
@@ -215,148 +265,201 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                 int y = __shfl_up_sync(0xffffffffu, x, o);
                 if (lane >= o) x += y;
             }
-            if (l < p.n_lists) list_prefix[l] = carry + x - v;
+            if (l < p.n_lists) cs.list_prefix[l] = carry + x - v;
             carry += __shfl_sync(0xffffffffu, x, 31);
         }
-        if (lane == 0) list_prefix[p.n_lists] = carry;
+        if (lane == 0) cs.list_prefix[p.n_lists] = carry;
+        __syncwarp();
     }
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
-    const uint32_t tmem_base = *tmem_holder;
+    const uint32_t tmem_base = cs.tmem_holder[0];
+    constexpr uint32_t rb = BK * 2;           // bytes per operand row (= swizzle span)
 
-    int64_t n_tiles;
-    if (p.mode == 0) n_tiles = ((n_out + TC_BM - 1) / TC_BM) * p.n_ntiles;
-    else n_tiles = (int64_t)list_prefix[p.n_lists] * p.n_ntiles;
-
-    const uint32_t lbo = 128, sbo = (uint32_t)p.BK * 16;
-
-    if (warp < 4) {
-        // ===================== gather producers (one thread per tile row) ==============
-        const int r = threadIdx.x;   // 0..127
-        const uint32_t a_row_off = (uint32_t)((r >> 3) * (p.BK * 16) + (r & 7) * 16);
-        const int nq = p.BK / 8;     // 16-byte pieces per row segment
-        uint32_t it = 0;             // global step counter
-        uint32_t pend_first = 0, pend = 0;   // un-arrived steps [pend_first, pend_first+pend)
-        const int LAG = S - 1 < 3 ? S - 1 : 3;
-        for (int64_t v = blockIdx.x; v < n_tiles; v += gridDim.x) {
+    if (warp == W_SCHED) {
+        // ===================== scheduler: tile records + gather indices ==================
+        int64_t n_tiles;
+        if (p.mode == 0) n_tiles = ((n_out + TC_BM - 1) / TC_BM) * p.n_ntiles;
+        else n_tiles = (int64_t)cs.list_prefix[p.n_lists] * p.n_ntiles;
+        uint32_t ti = 0, ii = 0;
+        for (int64_t v = blockIdx.x;; v += gridDim.x, ++ti) {
+            const int st = ti % TREC_SLOTS;
+            ptx::mbar_wait(ptx::smem_u32(&cs.trec_empty[st]), ((ti / TREC_SLOTS) & 1) ^ 1);
+            TileRec &R = cs.trec[st];
+            if (v >= n_tiles) {
+                if (lane == 0) R.end = 1;
+                ptx::mbar_arrive(ptx::smem_u32(&cs.trec_full[st]));
+                break;
+            }
             TileInfo t;
-            decode_tile(p, v, list_prefix, n_out, t);
-            for (int c = next_bit(t.mask, 0); c >= 0; c = next_bit(t.mask, c + 1)) {
-                int32_t idx = -1;
-                if (r < t.rows) {
-                    if (p.mode == 0) idx = p.os[(t.row0 + r) * p.k_dense + c];
-                    else {
-                        const int2 pr = p.pairs[t.list * p.list_stride + t.row0 + r];
-                        idx = t.dir ? pr.y : pr.x;
-                    }
+            decode_tile(p, v, cs.list_prefix, n_out, t);
+            if (lane == 0) {
+                R.row0 = t.row0; R.rows = t.rows; R.nt = t.nt; R.list = t.list; R.dir = t.dir; R.k = t.k; R.end = 0;
+                for (int w = 0; w < 4; ++w) R.mask[w] = t.mask[w];
+            }
+            if (p.mode == 1) {
+                const int32_t *pr = reinterpret_cast<const int32_t *>(p.pairs + t.list * p.list_stride + t.row0);
+                for (int r = lane; r < TC_BM; r += 32) R.scatter[r] = r < t.rows ? pr[2 * r + (t.dir ? 0 : 1)] : -1;
+            }
+            ptx::mbar_arrive(ptx::smem_u32(&cs.trec_full[st]));
+            // gather indices of every step column of the tile, asynchronously (cp.async 4 B)
+            for (int c = next_bit(t.mask, 0); c >= 0; c = next_bit(t.mask, c + 1), ++ii) {
+                const int si = ii % IDX_SLOTS;
+                ptx::mbar_wait(ptx::smem_u32(&cs.idx_empty[si]), ((ii / IDX_SLOTS) & 1) ^ 1);
+                TR(4, ii);
+                const uint32_t dst = ptx::smem_u32(&cs.idx[si][0]);
+                for (int r = lane; r < TC_BM; r += 32) {
+                    const int rr = r < t.rows ? r : 0;
+                    const int32_t *src;
+                    if (p.mode == 0) src = p.os + (t.row0 + rr) * p.k_dense + c;
+                    else src = reinterpret_cast<const int32_t *>(p.pairs + t.list * p.list_stride + t.row0 + rr) +
+                               (t.dir ? 1 : 0);
+                    ptx::cp_async_4(dst + 4 * r, src, 4u);
                 }
-                const char *src_row = idx >= 0 ? p.f_in + (int64_t)idx * p.ld_in_bytes : p.f_in;
-                const uint32_t sz = idx >= 0 ? 16u : 0u;
-                for (int cc = 0; cc < p.n_chunks; ++cc, ++it) {
-                    const int s = it % S;
-                    const uint32_t round = it / S;
-                    ptx::mbar_wait(ptx::smem_u32(&empty[s]), (round & 1) ^ 1);
-                    const uint32_t dst = ptx::smem_u32(sa + (size_t)s * p.a_bytes) + a_row_off;
-                    const char *src = src_row + (idx >= 0 ? cc * p.BK * 2 : 0);
-                    for (int q = 0; q < nq; ++q) ptx::cp_async_16(dst + q * 128, src + q * 16, sz);
-                    ptx::cp_async_commit();
-                    ++pend;
-                    if ((int)pend > LAG) {
-                        // the oldest pending step has landed once at most LAG groups are in flight
-                        if (LAG >= 3) ptx::cp_async_wait<3>();
-                        else if (LAG == 2) ptx::cp_async_wait<2>();
-                        else if (LAG == 1) ptx::cp_async_wait<1>();
-                        else ptx::cp_async_wait<0>();
-                        ptx::fence_proxy_async();
-                        ptx::mbar_arrive(ptx::smem_u32(&full[pend_first % S]));
-                        ++pend_first;
-                        --pend;
-                    }
-                }
+                ptx::cp_async_mbar_arrive(ptx::smem_u32(&cs.idx_full[si]));
             }
         }
         ptx::cp_async_wait<0>();
-        ptx::fence_proxy_async();
-        while (pend) {
-            ptx::mbar_arrive(ptx::smem_u32(&full[pend_first % S]));
-            ++pend_first;
-            --pend;
+    } else if (warp < 4) {
+        // ===================== gather producers (cp.async, 4 warps x 32 rows) ============
+        // lane -> (row r_in of a rows_pi-row block, 16-byte chunk q_lane); every warp
+        // instruction stores whole sectors of rows_pi rows into the swizzled K-major tile
+        // (chunk j of row r lands at j ^ f(r)), 4 shared wavefronts per 512 bytes.
+        constexpr int NQ = BK / 8;                 // 16-byte chunks per row segment
+        constexpr int Q = NQ < 4 ? NQ : 4;         // chunks per warp instruction
+        constexpr int RPI = 32 / Q;                // rows per warp instruction
+        constexpr int NB = 32 / RPI;               // row blocks per warp (== Q)
+        constexpr int NT = NQ / Q;                 // instructions per row block
+        const int r_in = lane % RPI, q_lane = lane / RPI;
+        uint32_t it = 0, ii = 0;
+        for (uint32_t ti = 0;; ++ti) {
+            const int st = ti % TREC_SLOTS;
+            ptx::mbar_wait(ptx::smem_u32(&cs.trec_full[st]), (ti / TREC_SLOTS) & 1);
+            const TileRec &R = cs.trec[st];
+            if (R.end) break;
+            const int rows = R.rows;
+            uint32_t mask[4] = {R.mask[0], R.mask[1], R.mask[2], R.mask[3]};
+            for (int c = next_bit(mask, 0); c >= 0; c = next_bit(mask, c + 1), ++ii) {
+                const int si = ii % IDX_SLOTS;
+                ptx::mbar_wait(ptx::smem_u32(&cs.idx_full[si]), (ii / IDX_SLOTS) & 1);
+                const char *gp[NB];
+                uint32_t sz[NB], so[NB];
+#pragma unroll
+                for (int b = 0; b < NB; ++b) {
+                    const int r = warp * 32 + b * RPI + r_in;
+                    const int32_t g = r < rows ? cs.idx[si][r] : -1;
+                    const uint32_t f = rb == 128 ? (r & 7) : (rb == 64 ? ((r >> 1) & 3) : ((r >> 2) & 1));
+                    gp[b] = g >= 0 ? p.f_in + (int64_t)g * p.ld_in_bytes + q_lane * 16 : p.f_in;
+                    sz[b] = g >= 0 ? 16u : 0u;
+                    so[b] = (uint32_t)r * rb + ((q_lane ^ f) * 16);
+                }
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&cs.idx_empty[si]));
+                for (int cc = 0; cc < p.n_chunks; ++cc, ++it) {
+                    const int s = it % S;
+                    ptx::mbar_wait(ptx::smem_u32(&cs.empty[s]), ((it / S) & 1) ^ 1);
+                    if (threadIdx.x == 0) TR(0, it);
+                    const uint32_t abase = ptx::smem_u32(sa + (size_t)s * p.a_bytes);
+#pragma unroll
+                    for (int b = 0; b < NB; ++b)
+#pragma unroll
+                        for (int t = 0; t < NT; ++t)
+                            ptx::cp_async_16(abase + (so[b] ^ (uint32_t)(t * Q * 16)), gp[b] + t * Q * 16, sz[b]);
+                    ptx::cp_async_mbar_arrive(ptx::smem_u32(&cs.full[s]));
+#pragma unroll
+                    for (int b = 0; b < NB; ++b) gp[b] += sz[b] ? rb : 0;
+                }
+            }
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&cs.trec_empty[st]));
         }
-    } else if (warp == 8) {
-        // ===================== weight producer (1-D bulk copies) =======================
-        if (lane == 0) {
-            uint32_t it = 0;
-            for (int64_t v = blockIdx.x; v < n_tiles; v += gridDim.x) {
-                TileInfo t;
-                decode_tile(p, v, list_prefix, n_out, t);
-                for (int c = next_bit(t.mask, 0); c >= 0; c = next_bit(t.mask, c + 1)) {
-                    const int k = p.mode == 0 ? p.dense_k[c] : t.k;
+        ptx::cp_async_wait<0>();
+    } else if (warp == W_BLOAD) {
+        // ===================== weight loader (1-D bulk copies, TMA engine) ===============
+        uint32_t it = 0;
+        for (uint32_t ti = 0;; ++ti) {
+            const int st = ti % TREC_SLOTS;
+            ptx::mbar_wait(ptx::smem_u32(&cs.trec_full[st]), (ti / TREC_SLOTS) & 1);
+            const TileRec &R = cs.trec[st];
+            if (R.end) break;
+            if (lane == 0) {
+                uint32_t mask[4] = {R.mask[0], R.mask[1], R.mask[2], R.mask[3]};
+                const int nt = R.nt, kfix = R.k;
+                for (int c = next_bit(mask, 0); c >= 0; c = next_bit(mask, c + 1)) {
+                    const int k = p.mode == 0 ? p.dense_k[c] : kfix;
                     for (int cc = 0; cc < p.n_chunks; ++cc, ++it) {
                         const int s = it % S;
-                        const uint32_t round = it / S;
-                        ptx::mbar_wait(ptx::smem_u32(&empty[s]), (round & 1) ^ 1);
-                        const uint32_t fb = ptx::smem_u32(&full[s]);
+                        ptx::mbar_wait(ptx::smem_u32(&cs.empty[s]), ((it / S) & 1) ^ 1);
+                        const uint32_t fb = ptx::smem_u32(&cs.full[s]);
                         ptx::mbar_arrive_expect_tx(fb, p.b_bytes);
-                        const int64_t blob = ((int64_t)k * p.n_ntiles + t.nt) * p.n_chunks + cc;
+                        const int64_t blob = ((int64_t)k * p.n_ntiles + nt) * p.n_chunks + cc;
                         ptx::bulk_g2s(ptx::smem_u32(sb + (size_t)s * p.b_bytes), p.wblob + blob * p.b_bytes, p.b_bytes,
                                       fb);
                     }
                 }
+                ptx::mbar_arrive(ptx::smem_u32(&cs.trec_empty[st]));
             }
+            __syncwarp();
         }
-    } else if (warp == 9) {
+    } else if (warp == W_MMA) {
         // ===================== MMA issuer ===============================================
-        if (lane == 0) {
-            uint32_t it = 0, tt = 0;
-            for (int64_t v = blockIdx.x; v < n_tiles; v += gridDim.x, ++tt) {
-                TileInfo t;
-                decode_tile(p, v, list_prefix, n_out, t);
-                const uint32_t a = tt & 1, ar = tt >> 1;
-                ptx::mbar_wait(ptx::smem_u32(&tempty[a]), (ar & 1) ^ 1);
+        uint32_t it = 0;
+        for (uint32_t ti = 0;; ++ti) {
+            const int st = ti % TREC_SLOTS;
+            ptx::mbar_wait(ptx::smem_u32(&cs.trec_full[st]), (ti / TREC_SLOTS) & 1);
+            const TileRec &R = cs.trec[st];
+            if (R.end) break;
+            if (lane == 0) {
+                uint32_t mask[4] = {R.mask[0], R.mask[1], R.mask[2], R.mask[3]};
+                const uint32_t a = ti & 1;
+                ptx::mbar_wait(ptx::smem_u32(&cs.tempty[a]), ((ti >> 1) & 1) ^ 1);
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + a * p.tmem_cols;
                 uint32_t acc = 0;
-                for (int c = next_bit(t.mask, 0); c >= 0; c = next_bit(t.mask, c + 1)) {
+                for (int c = next_bit(mask, 0); c >= 0; c = next_bit(mask, c + 1)) {
                     for (int cc = 0; cc < p.n_chunks; ++cc, ++it) {
                         const int s = it % S;
-                        const uint32_t round = it / S;
-                        ptx::mbar_wait(ptx::smem_u32(&full[s]), round & 1);
+                        ptx::mbar_wait(ptx::smem_u32(&cs.full[s]), (it / S) & 1);
+                        TR(2, it);
+                        // the A tile was written by cp.async (generic proxy): order it before
+                        // the tensor core's async-proxy reads
+                        ptx::fence_proxy_async();
                         ptx::tc_fence_after();
                         const uint32_t a_base = ptx::smem_u32(sa + (size_t)s * p.a_bytes);
                         const uint32_t b_base = ptx::smem_u32(sb + (size_t)s * p.b_bytes);
-                        for (int kk = 0; kk < p.BK / 16; ++kk) {
-                            const uint64_t ad = ptx::umma_desc_kmajor(a_base + kk * 256, lbo, sbo);
-                            const uint64_t bd = ptx::umma_desc_kmajor(b_base + kk * 256, lbo, sbo);
+#pragma unroll
+                        for (int kk = 0; kk < BK / 16; ++kk) {
+                            const uint64_t ad = ptx::umma_desc_kmajor_sw(a_base + kk * 32, rb);
+                            const uint64_t bd = ptx::umma_desc_kmajor_sw(b_base + kk * 32, rb);
                             ptx::mma_f16_ss(d_tmem, ad, bd, p.idesc, acc);
                             acc = 1;
                         }
-                        ptx::mma_commit(ptx::smem_u32(&empty[s]));
+                        ptx::mma_commit(ptx::smem_u32(&cs.empty[s]));
+                        TR(3, it);
                     }
                 }
-                ptx::mma_commit(ptx::smem_u32(&tfull[a]));
+                ptx::mma_commit(ptx::smem_u32(&cs.tfull[a]));
+                ptx::mbar_arrive(ptx::smem_u32(&cs.trec_empty[st]));
             }
+            __syncwarp();
         }
-        __syncwarp();
-    } else {
+    } else if (warp >= 4 && warp < 8) {
         // ===================== epilogue (warps 4-7, thread = TMEM lane = tile row) =====
         const int e = warp - 4;
         const int r = e * 32 + lane;
-        uint32_t tt = 0;
-        for (int64_t v = blockIdx.x; v < n_tiles; v += gridDim.x, ++tt) {
-            TileInfo t;
-            decode_tile(p, v, list_prefix, n_out, t);
-            const uint32_t a = tt & 1, ar = tt >> 1;
-            ptx::mbar_wait(ptx::smem_u32(&tfull[a]), ar & 1);
-            ptx::tc_fence_after();
+        for (uint32_t ti = 0;; ++ti) {
+            const int st = ti % TREC_SLOTS;
+            ptx::mbar_wait(ptx::smem_u32(&cs.trec_full[st]), (ti / TREC_SLOTS) & 1);
+            const TileRec &R = cs.trec[st];
+            if (R.end) break;
+            const uint32_t a = ti & 1;
             int64_t orow = -1;
-            if (r < t.rows) {
-                if (p.mode == 0) orow = t.row0 + r;
-                else {
-                    const int2 pr = p.pairs[t.list * p.list_stride + t.row0 + r];
-                    orow = t.dir ? pr.x : pr.y;
-                }
-            }
+            if (r < R.rows) orow = p.mode == 0 ? R.row0 + r : (int64_t)R.scatter[r];
+            const int nt = R.nt;
+            ptx::mbar_wait(ptx::smem_u32(&cs.tfull[a]), (ti >> 1) & 1);
+            if (threadIdx.x == 128) TR(6, ti);
+            ptx::tc_fence_after();
             const uint32_t tbase = tmem_base + a * p.tmem_cols + ((uint32_t)(e * 32) << 16);
             for (int col = 0; col < p.BN; col += 32) {
                 uint32_t vals[32];
@@ -365,12 +468,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                 else ptx::tmem_ld16(tbase + col, vals);
                 ptx::tmem_ld_wait();
                 if (orow >= 0) {
-                    const int gcol = t.nt * p.BN + col;
+                    const int gcol = nt * p.BN + col;
                     if (p.out_kind == OUT_F32_RED) {
                         float *op = static_cast<float *>(p.out) + orow * p.ld_out + gcol;
-                        for (int q = 0; q < n / 4; ++q)
-                            ptx::red_add_v4(op + 4 * q, to_f(vals[4 * q]), to_f(vals[4 * q + 1]), to_f(vals[4 * q + 2]),
-                                            to_f(vals[4 * q + 3]));
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            if (q * 4 < n)
+                                ptx::red_add_v4(op + 4 * q, to_f(vals[4 * q]), to_f(vals[4 * q + 1]),
+                                                to_f(vals[4 * q + 2]), to_f(vals[4 * q + 3]));
                     } else {
                         store_row(p, orow, gcol, vals, n);
                     }
@@ -378,12 +483,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             }
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&tempty[a]));
+            if (threadIdx.x == 128) TR(7, ti);
+            if (lane == 0) {
+                ptx::mbar_arrive(ptx::smem_u32(&cs.tempty[a]));
+                ptx::mbar_arrive(ptx::smem_u32(&cs.trec_empty[st]));
+            }
         }
     }
     ptx::tc_fence_before();
     __syncthreads();
-    if (warp == 9) {
+    if (warp == W_MMA) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem_base, 2 * p.tmem_cols);
     }
@@ -509,10 +618,13 @@ __global__ void __launch_bounds__(256) k_conv_simt(const __grid_constant__ ConvP
 // ------------------------------------------------------------------------------------
 // weight preparation, accumulator conversion, zero fill
 // ------------------------------------------------------------------------------------
+// weights -> per (k, N-tile, C-chunk) blobs laid out exactly as the swizzled K-major smem
+// tile the MMA reads: row n (BK elements = rb bytes), 16-byte chunk j stored at j ^ f(n)
 __global__ void k_prepare_weight_tc(const uint16_t *__restrict__ w, int k_vol, int c_in, int c_out, int BK, int BN,
                                     uint16_t *__restrict__ out) {
     const int64_t total = (int64_t)k_vol * c_in * c_out;
     const int n_nt = c_out / BN, n_ch = c_in / BK;
+    const int rb = BK * 2;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         const int co = (int)(e % c_out);
         const int64_t t = e / c_out;
@@ -520,8 +632,10 @@ __global__ void k_prepare_weight_tc(const uint16_t *__restrict__ w, int k_vol, i
         const int k = (int)(t / c_in);
         const int nt = co / BN, n = co % BN, cc = ci / BK, c = ci % BK;
         const int64_t blob = ((int64_t)k * n_nt + nt) * n_ch + cc;
-        const int64_t off = blob * BN * BK + ((n >> 3) * (BK >> 3) + (c >> 3)) * 64 + (n & 7) * 8 + (c & 7);
-        out[off] = w[e];
+        const int f = rb == 128 ? (n & 7) : (rb == 64 ? ((n >> 1) & 3) : ((n >> 2) & 1));
+        const int j = (c * 2) / 16, within = (c * 2) % 16;
+        const int64_t byte = (int64_t)n * rb + (int64_t)((j ^ f) * 16) + within;
+        out[blob * BN * BK + byte / 2] = w[e];
     }
 }
 
@@ -627,6 +741,36 @@ static void fill_map_params(ConvParams &p, const spc_kmap *km) {
     }
 }
 
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void *p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+[[maybe_unused]] static spc_status encode_rows_tmap(CUtensorMap *tm, const void *base, int64_t n_rows, int c_in, int64_t ld_bytes,
+                                   int BK, int dtype) {
+    auto enc = tmap_encoder();
+    if (!enc) return fail(SPC_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+    const int rb = BK * 2;
+    const CUtensorMapSwizzle sw = rb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                            : (rb == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+    cuuint64_t gdim[2] = {(cuuint64_t)c_in, (cuuint64_t)(n_rows > 0 ? n_rows : 1)};
+    cuuint64_t gstride[1] = {(cuuint64_t)ld_bytes};
+    cuuint32_t box[2] = {(cuuint32_t)BK, 1u};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(tm, dtype == SPC_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
+                     const_cast<void *>(base), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(SPC_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    return SPC_OK;
+}
+
 static spc_status launch_tc(const ConvParams &p0, int mode, int out_kind, void *out, int64_t ld_out, cudaStream_t st) {
     ConvParams p = p0;
     p.mode = mode;
@@ -634,7 +778,7 @@ static spc_status launch_tc(const ConvParams &p0, int mode, int out_kind, void *
     p.out = out;
     p.ld_out = ld_out;
     const size_t stage = (size_t)p.a_bytes + p.b_bytes;
-    const size_t extra = 64 * 8 + 16 + (SPC_MAX_KVOL + 1) * 4 + 64;
+    const size_t extra = sizeof(ConvSmem) + 1024 + 64;   // + alignment slack
     int S = (int)((TC_SMEM_BUDGET - extra) / stage);
     if (S > 8) S = 8;
     if (S < 2) return fail(SPC_ERR_UNSUPPORTED, "spc_conv_forward: tile does not fit shared memory");
@@ -642,13 +786,17 @@ static spc_status launch_tc(const ConvParams &p0, int mode, int out_kind, void *
     const size_t smem = stage * S + extra;
     static bool configured = false;
     if (!configured) {
-        SPC_CUDA(cudaFuncSetAttribute(k_conv_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BUDGET));
+        SPC_CUDA(cudaFuncSetAttribute(k_conv_tc<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BUDGET));
+        SPC_CUDA(cudaFuncSetAttribute(k_conv_tc<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BUDGET));
+        SPC_CUDA(cudaFuncSetAttribute(k_conv_tc<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BUDGET));
         configured = true;
     }
     // persistent: one CTA per SM (the WS tile count lives on the device)
     int64_t tiles_cap = mode == 0 ? ((p.n_out_cap + TC_BM - 1) / TC_BM) * p.n_ntiles : (int64_t)num_sms();
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles_cap, num_sms()));
-    k_conv_tc<<<grid, TC_THREADS, smem, st>>>(p);
+    if (p.BK == 64) k_conv_tc<64><<<grid, TC_THREADS, smem, st>>>(p);
+    else if (p.BK == 32) k_conv_tc<32><<<grid, TC_THREADS, smem, st>>>(p);
+    else k_conv_tc<16><<<grid, TC_THREADS, smem, st>>>(p);
     SPC_LAUNCH_CHECK("k_conv_tc");
     return SPC_OK;
 }
@@ -761,3 +909,9 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
     }
     return SPC_OK;
 }
+
+#ifdef SPC_EXP_TRACE
+extern "C" int spc_exp_trace_read(long long *host) {
+    return (int)cudaMemcpyFromSymbol(host, spc::g_tr, sizeof(spc::g_tr));
+}
+#endif

@@ -1,0 +1,208 @@
+"""MinkUNet-42 (C2/C4) and a SECOND/CenterPoint-style K=5 backbone (C3) over libspc.
+
+Orchestration only: every step of a forward pass is a C-ABI call of libspc (pack+sort,
+row gather, network-wide kernel maps, 49 sparse convolutions with fused residual adds).
+BN/ReLU are identity (out of scope); weights are seeded random bf16.
+Channel-concatenation skips are free: encoder outputs are written straight into a
+column slice of the decoder's concat buffer (ld_out > c_out).
+
+Layer list (public MinkowskiEngine/TorchSparse MinkUNet with K=3 down/up):
+cs = [32, 32, 64, 128, 256, 256, 128, 96, 96]; stem 2 x SubM K3; 4 encoder stages
+(Down K3 s2 + 2 ResBlocks); 4 decoder stages (Up K3 s2 transposed + concat + 2
+ResBlocks) = 42 layers with K = 3 plus 7 1x1 projections.
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+
+import numpy as np
+import torch
+
+import paper_2511_20834_b200 as spc
+
+CS = [32, 32, 64, 128, 256, 256, 128, 96, 96]
+C_IN_RAW = 4
+C_IN_PAD = 16   # tcgen05 kind::f16 needs K multiple of 16; the extra input channels are 0
+
+
+@dataclasses.dataclass
+class ConvSpec:
+    name: str
+    map_key: tuple          # (K, stride, tensor_stride, transposed)
+    c_in: int
+    c_out: int
+    src: str                # activation buffer read
+    src_col: int            # first column read
+    dst: str                # activation buffer written
+    dst_col: int
+    level_out: int
+    residual: tuple | None = None   # (buffer, first column) added to the output
+    c_in_flops: int = 0     # channels counted for algorithmic FLOPs (stem: 4 real channels)
+
+
+def minkunet42_layers():
+    L = []
+    lvl_buf = {}
+
+    def conv(name, mk, ci, co, src, sc, dst, dc, lo, res=None, ci_fl=None):
+        L.append(ConvSpec(name, mk, ci, co, src, sc, dst, dc, lo, res, ci_fl or ci))
+
+    def subm(l):
+        return (3, 1, 2 ** l, 0)
+
+    def one(l):
+        return (1, 1, 2 ** l, 0)
+
+    def resblock(tag, l, src, sc, ci, co, dst, dc):
+        conv(f"{tag}.conv1", subm(l), ci, co, src, sc, f"h{l}", 0, l)
+        if ci != co:
+            conv(f"{tag}.proj", one(l), ci, co, src, sc, f"p{l}", 0, l)
+            res = (f"p{l}", 0)
+        else:
+            res = (src, sc)
+        conv(f"{tag}.conv2", subm(l), co, co, f"h{l}", 0, dst, dc, l, res)
+
+    # decoder concat widths per level: up channels + skip channels
+    up_c = {3: CS[5], 2: CS[6], 1: CS[7], 0: CS[8]}
+    skip_c = {3: CS[3], 2: CS[2], 1: CS[1], 0: CS[0]}
+    cat_w = {l: up_c[l] + skip_c[l] for l in up_c}
+
+    # stem (level 0)
+    conv("stem.conv1", subm(0), C_IN_PAD, CS[0], "x0", 0, "h0", 0, 0, None, C_IN_RAW)
+    conv("stem.conv2", subm(0), CS[0], CS[0], "h0", 0, "cat0", up_c[0], 0)
+    src, sc, ch = "cat0", up_c[0], CS[0]
+    # encoder
+    for i in range(1, 5):
+        l = i
+        conv(f"enc{i}.down", (3, 2, 2 ** (l - 1), 0), ch, ch, src, sc, f"d{l}", 0, l)
+        dst, dc = (f"cat{l}", up_c[l]) if l < 4 else ("e4", 0)
+        resblock(f"enc{i}.rb1", l, f"d{l}", 0, ch, CS[i], f"y{l}", 0)
+        resblock(f"enc{i}.rb2", l, f"y{l}", 0, CS[i], CS[i], dst, dc)
+        src, sc, ch = dst, dc, CS[i]
+    # decoder
+    for j in range(1, 5):
+        l = 4 - j
+        co = CS[4 + j]
+        conv(f"dec{j}.up", (3, 2, 2 ** l, 1), ch, co, src, sc, f"cat{l}", 0, l)
+        resblock(f"dec{j}.rb1", l, f"cat{l}", 0, cat_w[l], co, f"y{l}", 0)
+        dst = "out" if l == 0 else f"z{l}"
+        resblock(f"dec{j}.rb2", l, f"y{l}", 0, co, co, dst, 0)
+        src, sc, ch = dst, 0, co
+    widths = {"x0": C_IN_PAD, "out": CS[8], "e4": CS[4]}
+    for l in range(4):
+        widths[f"cat{l}"] = cat_w[l]
+    for s in L:
+        widths[s.dst] = max(widths.get(s.dst, 0), s.dst_col + s.c_out)
+    return L, widths
+
+
+def default_t(map_key):
+    """Dataflow threshold per map before tuning (reading: the paper's UNet uses WS in most
+    layers).  K=1 maps are always dense."""
+    K, stride, ts, tr = map_key
+    if K == 1:
+        return spc.SPC_T_ALL_OS
+    if stride == 1:
+        return 2                       # hybrid: centre + 6 face neighbours dense
+    return spc.SPC_T_ALL_OS
+
+
+class SparseUNet:
+    """MinkUNet-42 forward over libspc with every buffer pre-allocated for capacity n0."""
+
+    def __init__(self, n0_cap: int, spec: spc.PackSpec, device="cuda", seed: int = 20834, t_override=None,
+                 nnz_per_out: float = 10.0):
+        self.dev = torch.device(device)
+        self.spec = spec
+        self.n0 = int(n0_cap)
+        self.layers, widths = minkunet42_layers()
+        self.n_levels = 5
+        self.map_keys = []
+        for s in self.layers:
+            if s.map_key not in self.map_keys:
+                self.map_keys.append(s.map_key)
+        self.t = {mk: (t_override or {}).get(mk, default_t(mk)) for mk in self.map_keys}
+        # weights: seeded, bf16, prepared for the tcgen05 layout
+        g = torch.Generator().manual_seed(seed)
+        self.weights = []
+        for s in self.layers:
+            kv = s.map_key[0] ** 3
+            a = math.sqrt(3.0 / (min(kv, nnz_per_out) * s.c_in_flops))
+            w = (torch.rand(kv, s.c_in, s.c_out, generator=g) * 2 - 1) * a
+            if s.c_in != s.c_in_flops:
+                w[:, s.c_in_flops:, :] = 0
+            self.weights.append(spc.spc_prepare_weight(w.to(self.dev, torch.bfloat16)))
+        # activations (capacity n0 rows for every level)
+        self.bufs = {name: torch.zeros(self.n0, w, dtype=torch.bfloat16, device=self.dev) for name, w in widths.items()}
+        self.coords_ws = None
+        self.keys = torch.empty(self.n0, dtype=torch.int64, device=self.dev)
+        self.perm = torch.empty(self.n0, dtype=torch.int32, device=self.dev)
+        self.status = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self.sort_ws = torch.empty(int(spc.lib().spc_pack_sort_workspace_size(self.n0)), dtype=torch.uint8,
+                                   device=self.dev)
+        self.conv_ws = torch.empty(self.n0 * 256 * 4 + 1024, dtype=torch.uint8, device=self.dev)
+        self.netidx = None
+        self.maps = None
+
+    # ---------------------------------------------------------------------------------
+    def _geoms(self):
+        geoms, ts, flags = [], [], []
+        for mk in self.map_keys:
+            K, stride, tsd, tr = mk
+            geoms.append(spc.Geom(K, stride, 1, tsd, tr))
+            t = self.t[mk]
+            ts.append(t)
+            flags.append(spc.SPC_KMAP_HALVE_SYMMETRIC if (stride == 1 and K > 1) else 0)
+        return geoms, ts, flags
+
+    def index(self, stream=None):
+        """Network-wide voxel indexing: all levels, then all maps."""
+        if self.netidx is None:
+            geoms, ts, flags = self._geoms()
+            self.netidx = spc.NetworkIndex(self.n0, self.spec, self.n_levels, geoms, ts, flags, device=self.dev)
+        kms = self.netidx.run(self.keys, status=self.status, stream=stream)
+        self.level_keys, self.level_n = self.netidx.level_keys, self.netidx.level_n
+        self.maps = dict(zip(self.map_keys, kms))
+
+    def set_t(self, t_map: dict):
+        self.t.update(t_map)
+        self.netidx = None
+
+    def conv(self, i, stream=None):
+        s = self.layers[i]
+        km = self.maps[s.map_key]
+        src = self.bufs[s.src][:, s.src_col:s.src_col + s.c_in]
+        dst = self.bufs[s.dst][:, s.dst_col:s.dst_col + s.c_out]
+        res = None
+        if s.residual is not None:
+            rb, rc = s.residual
+            res = self.bufs[rb][:, rc:rc + s.c_out]
+        spc.spc_conv_forward(km, src, self.weights[i], s.c_in, s.c_out, out=dst, residual=res, ws=self.conv_ws,
+                             stream=stream)
+
+    def forward(self, coords: torch.Tensor, feats: torch.Tensor, stream=None) -> torch.Tensor:
+        """coords int32 [n,4] (any order), feats bf16 [n, 16] (first 4 channels real) -> out [n, 96]
+        in sorted (canonical) voxel order."""
+        n = coords.shape[0]
+        assert n <= self.n0
+        spc.spc_pack_sort(coords, self.spec, status=self.status, keys_out=self.keys[:n], perm_out=self.perm[:n],
+                          ws=self.sort_ws, stream=stream)
+        spc.spc_gather_rows(feats, self.perm[:n], out=self.bufs["x0"][:n], stream=stream)
+        if n != self.n0:
+            raise ValueError("capacity must equal the scan size (allocate per scan)")
+        self.index(stream)
+        for i in range(len(self.layers)):
+            self.conv(i, stream)
+        return self.bufs["out"]
+
+    # ---------------------------------------------------------------------------------
+    def algorithmic_flops(self) -> dict:
+        """2 * nnz * C_in * C_out per layer (valid pairs only; OS sentinel rows not credited).
+        [sync] -- exports every map once."""
+        nnz = {mk: int(spc.spc_kmap_export(km).shape[0]) for mk, km in self.maps.items()}
+        out = {}
+        for s in self.layers:
+            out[s.name] = 2.0 * nnz[s.map_key] * s.c_in_flops * s.c_out
+        self.nnz = nnz
+        return out

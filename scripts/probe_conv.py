@@ -1,0 +1,48 @@
+"""Run one sparse-conv layer of config C2 repeatedly (for ncu / timing probes).
+
+python scripts/probe_conv.py --cin 96 --cout 96 --t -1 --level 0 --reps 5
+"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+import paper_2511_20834_b200 as spc  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--cin", type=int, default=96)
+ap.add_argument("--cout", type=int, default=96)
+ap.add_argument("--K", type=int, default=3)
+ap.add_argument("--t", type=int, default=-1)
+ap.add_argument("--halve", type=int, default=1)
+ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--config", type=int, default=2)
+a = ap.parse_args()
+
+coords = synth.make_scan(a.config, 0)
+spec = spc.spc_plan_pack(coords[:, 1:].min(0), coords[:, 1:].max(0), 1, 16, 16)
+keys, perm, _ = spc.spc_pack_sort(torch.from_numpy(coords).cuda(), spec)
+km = spc.spc_build_kmap(keys, keys, spec, spc.Geom(a.K, 1, 1, 1, 0), a.t, spc.SPC_KMAP_HALVE_SYMMETRIC if a.halve else 0)
+n = keys.shape[0]
+F = torch.randn(n, a.cin, device="cuda").bfloat16()
+W = spc.spc_prepare_weight((torch.randn(a.K ** 3, a.cin, a.cout, device="cuda") * 0.05).bfloat16())
+out = torch.empty(n, a.cout, device="cuda", dtype=torch.bfloat16)
+ws = torch.empty(n * a.cout * 4 + 1024, dtype=torch.uint8, device="cuda")
+nnz = spc.spc_kmap_export(km).shape[0]
+for _ in range(2):
+    spc.spc_conv_forward(km, F, W, a.cin, a.cout, out=out, ws=ws)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(a.reps):
+    spc.spc_conv_forward(km, F, W, a.cin, a.cout, out=out, ws=ws)
+e1.record()
+torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / a.reps
+fl = 2.0 * nnz * a.cin * a.cout
+print(f"n={n} nnz={nnz} k_dense={km.k_dense} lists={km.n_lists} cin={a.cin} cout={a.cout} t={a.t}: "
+      f"{ms * 1e3:.1f} us  {fl / ms / 1e9:.1f} TFLOP/s (algorithmic)")

@@ -190,7 +190,7 @@ def test_network_kmaps_equal_sequential():
     geoms = [spc.Geom(3, 1, 1, 1, 0), spc.Geom(3, 2, 1, 1, 0), spc.Geom(3, 1, 1, 2, 0), spc.Geom(3, 2, 1, 2, 0),
              spc.Geom(3, 1, 1, 4, 0), spc.Geom(3, 2, 1, 2, 1), spc.Geom(3, 2, 1, 1, 1), spc.Geom(3, 1, 1, 1, 0)]
     ts = [-1, 0, 2, -1, 0, -1, 2, -1]
-    lk, ln, maps, _ = spc.spc_network_kmaps(keys, spec, 4, geoms, ts)
+    lk, ln, maps = spc.spc_network_kmaps(keys, spec, 4, geoms, ts)
     c = oracle.sort_coords(coords)[0]
     lv = {1: c, 2: oracle.downsample(c, 2), 4: oracle.downsample(c, 4), 8: oracle.downsample(c, 8)}
     assert ln.cpu().tolist() == [len(lv[1]), len(lv[2]), len(lv[4]), len(lv[8])]
