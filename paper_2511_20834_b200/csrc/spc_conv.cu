@@ -29,7 +29,8 @@
 
 namespace spc {
 
-constexpr int TC_THREADS = 352;   // 11 warps: 4 gather, 4 epilogue, MMA, weight loader, scheduler
+constexpr int TC_THREADS = 480;   // 15 warps: 8 gather, 4 epilogue, MMA, weight loader, scheduler
+constexpr int N_GATHER = 8;        // gather warps (two per SM sub-partition)
 constexpr int TC_BM = 128;
 constexpr int TC_SMEM_BUDGET = 225 * 1024;
 
@@ -188,25 +189,25 @@ __device__ __forceinline__ void store_row(const ConvParams &p, int64_t row, int 
 
 // ---- shared-memory records produced by the scheduler warp ------------------------------
 constexpr int TREC_SLOTS = 4;      // tile records in flight
-constexpr int IDX_SLOTS = 16;      // per-(tile, offset) gather-index slots in flight
-constexpr int TREC_CONSUMERS = 10; // gather warps 4 + epilogue warps 4 + MMA 1 + weight loader 1
-constexpr int W_MMA = 8, W_BLOAD = 9, W_SCHED = 10;
+constexpr int BLK_SLOTS = 2;       // per-tile gather-index blocks in flight
+constexpr int TREC_CONSUMERS = N_GATHER + 4 + 2;  // gather warps + epilogue warps + MMA + weight loader
+constexpr int W_EPI0 = 8, W_MMA = 12, W_BLOAD = 13, W_SCHED = 14;
 
 struct TileRec {
     int64_t row0;
-    int rows, nt, list, dir, k, end;
+    int rows, nt, list, dir, k, end, ncols;
     uint32_t mask[4];
+    uint8_t cols[128];        // active step columns (OS: dense offsets with a match; WS: {0})
     int32_t scatter[TC_BM];   // WS: output row of each pair row (OS: unused)
 };
 
 struct ConvSmem {
-    uint64_t full[8], empty[8], tfull[2], tempty[2];
+    uint64_t full[16], empty[16], tfull[2], tempty[2];
     uint64_t trec_full[TREC_SLOTS], trec_empty[TREC_SLOTS];
-    uint64_t idx_full[IDX_SLOTS], idx_empty[IDX_SLOTS];
+    uint64_t blk_full[BLK_SLOTS], blk_empty[BLK_SLOTS];
     uint32_t tmem_holder[4];
     int list_prefix[SPC_MAX_KVOL + 1];
     TileRec trec[TREC_SLOTS];
-    alignas(16) int32_t idx[IDX_SLOTS][TC_BM];
 };
 
 #ifdef SPC_EXP_TRACE
@@ -225,13 +226,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     uint8_t *sa = smem;
     uint8_t *sb = smem + (size_t)S * p.a_bytes;
     ConvSmem &cs = *reinterpret_cast<ConvSmem *>(sb + (size_t)S * p.b_bytes);
+    // gather-index blocks: OS: the tile's [rows x k_dense] slice of the OS table (one bulk
+    // copy per tile); WS: the 128 gather indices of the tile's pairs
+    const int kd = p.mode == 0 ? p.k_dense : 1;
+    int32_t *blk = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(&cs) + ((sizeof(ConvSmem) + 127) & ~size_t(127)));
+    const int blk_stride = (TC_BM * kd + 3) & ~3;   // int32 per block (16-byte multiple)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t n_out = dev_count(p.n_out_cap, p.n_out_dev);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
-            ptx::mbar_init(ptx::smem_u32(&cs.full[s]), TC_BM + 1);   // 128 gather threads + weight expect_tx
+            ptx::mbar_init(ptx::smem_u32(&cs.full[s]), N_GATHER * 32 + 1);   // gather threads + weight expect_tx
             ptx::mbar_init(ptx::smem_u32(&cs.empty[s]), 1);
         }
         for (int a = 0; a < 2; ++a) {
@@ -242,9 +248,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             ptx::mbar_init(ptx::smem_u32(&cs.trec_full[i]), 32);
             ptx::mbar_init(ptx::smem_u32(&cs.trec_empty[i]), TREC_CONSUMERS);
         }
-        for (int i = 0; i < IDX_SLOTS; ++i) {
-            ptx::mbar_init(ptx::smem_u32(&cs.idx_full[i]), 32);
-            ptx::mbar_init(ptx::smem_u32(&cs.idx_empty[i]), 4);
+        for (int i = 0; i < BLK_SLOTS; ++i) {
+            ptx::mbar_init(ptx::smem_u32(&cs.blk_full[i]), 32);
+            ptx::mbar_init(ptx::smem_u32(&cs.blk_empty[i]), N_GATHER);
         }
         ptx::fence_mbar_init();
         ptx::fence_proxy_async();
@@ -285,7 +291,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         uint32_t ti = 0, ii = 0;
         for (int64_t v = blockIdx.x;; v += gridDim.x, ++ti) {
             const int st = ti % TREC_SLOTS;
-            ptx::mbar_wait(ptx::smem_u32(&cs.trec_empty[st]), ((ti / TREC_SLOTS) & 1) ^ 1);
+            ptx::mbar_wait_sleep(ptx::smem_u32(&cs.trec_empty[st]), ((ti / TREC_SLOTS) & 1) ^ 1);
             TileRec &R = cs.trec[st];
             if (v >= n_tiles) {
                 if (lane == 0) R.end = 1;
@@ -297,82 +303,102 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             if (lane == 0) {
                 R.row0 = t.row0; R.rows = t.rows; R.nt = t.nt; R.list = t.list; R.dir = t.dir; R.k = t.k; R.end = 0;
                 for (int w = 0; w < 4; ++w) R.mask[w] = t.mask[w];
+                int nc = 0;
+                for (int c = next_bit(t.mask, 0); c >= 0; c = next_bit(t.mask, c + 1)) R.cols[nc++] = (uint8_t)c;
+                R.ncols = nc;
             }
             if (p.mode == 1) {
                 const int32_t *pr = reinterpret_cast<const int32_t *>(p.pairs + t.list * p.list_stride + t.row0);
                 for (int r = lane; r < TC_BM; r += 32) R.scatter[r] = r < t.rows ? pr[2 * r + (t.dir ? 0 : 1)] : -1;
             }
             ptx::mbar_arrive(ptx::smem_u32(&cs.trec_full[st]));
-            // gather indices of every step column of the tile, asynchronously (cp.async 4 B)
-            for (int c = next_bit(t.mask, 0); c >= 0; c = next_bit(t.mask, c + 1), ++ii) {
-                const int si = ii % IDX_SLOTS;
-                ptx::mbar_wait(ptx::smem_u32(&cs.idx_empty[si]), ((ii / IDX_SLOTS) & 1) ^ 1);
-                TR(4, ii);
-                const uint32_t dst = ptx::smem_u32(&cs.idx[si][0]);
-                for (int r = lane; r < TC_BM; r += 32) {
-                    const int rr = r < t.rows ? r : 0;
-                    const int32_t *src;
-                    if (p.mode == 0) src = p.os + (t.row0 + rr) * p.k_dense + c;
-                    else src = reinterpret_cast<const int32_t *>(p.pairs + t.list * p.list_stride + t.row0 + rr) +
-                               (t.dir ? 1 : 0);
-                    ptx::cp_async_4(dst + 4 * r, src, 4u);
+            // the tile's gather indices: one contiguous block
+            const int bs = ti % BLK_SLOTS;
+            ptx::mbar_wait_sleep(ptx::smem_u32(&cs.blk_empty[bs]), ((ti / BLK_SLOTS) & 1) ^ 1);
+            int32_t *B = blk + bs * blk_stride;
+            const uint32_t fb = ptx::smem_u32(&cs.blk_full[bs]);
+            if (p.mode == 0) {
+                // OS: rows [row0, row0+rows) of the [n_out x k_dense] table are contiguous
+                const uint32_t bytes = (uint32_t)((t.rows * p.k_dense * 4 + 15) & ~15);
+                if (lane == 0) {
+                    ptx::mbar_arrive_expect_tx(fb, bytes);
+                    ptx::bulk_g2s(ptx::smem_u32(B), p.os + t.row0 * p.k_dense, bytes, fb);
                 }
-                ptx::cp_async_mbar_arrive(ptx::smem_u32(&cs.idx_full[si]));
+                if (lane != 0) ptx::mbar_arrive(fb);
+            } else {
+                const int32_t *pr = reinterpret_cast<const int32_t *>(p.pairs + t.list * p.list_stride + t.row0);
+                for (int r = lane; r < TC_BM; r += 32) B[r] = r < t.rows ? pr[2 * r + (t.dir ? 1 : 0)] : -1;
+                ptx::mbar_arrive(fb);
             }
         }
         ptx::cp_async_wait<0>();
-    } else if (warp < 4) {
-        // ===================== gather producers (cp.async, 4 warps x 32 rows) ============
-        // lane -> (row r_in of a rows_pi-row block, 16-byte chunk q_lane); every warp
-        // instruction stores whole sectors of rows_pi rows into the swizzled K-major tile
+    } else if (warp < N_GATHER) {
+        // ===================== gather producers (cp.async, 8 warps x 16 rows) ============
+        // lane -> (row r_in of an RPI-row block, 16-byte chunk q_lane); every warp
+        // instruction stores whole sectors of RPI rows into the swizzled K-major tile
         // (chunk j of row r lands at j ^ f(r)), 4 shared wavefronts per 512 bytes.
         constexpr int NQ = BK / 8;                 // 16-byte chunks per row segment
-        constexpr int Q = NQ < 4 ? NQ : 4;         // chunks per warp instruction
-        constexpr int RPI = 32 / Q;                // rows per warp instruction
-        constexpr int NB = 32 / RPI;               // row blocks per warp (== Q)
-        constexpr int NT = NQ / Q;                 // instructions per row block
+        constexpr int Q = NQ;                      // chunks per warp instruction (whole rows)
+        constexpr int RPI = 32 / Q;                // rows per warp instruction (4 / 8 / 16)
+        constexpr int ROWS_W = TC_BM / N_GATHER;   // rows per warp (16)
+        constexpr int NB = ROWS_W / RPI;           // row blocks per warp
         const int r_in = lane % RPI, q_lane = lane / RPI;
-        uint32_t it = 0, ii = 0;
+        int s = 0;
+        uint32_t ph = 0;   // stage ring position / phase
+#ifdef SPC_EXP_TRACE
+        uint32_t ptr_ctr = 0;
+#endif
         for (uint32_t ti = 0;; ++ti) {
             const int st = ti % TREC_SLOTS;
             ptx::mbar_wait(ptx::smem_u32(&cs.trec_full[st]), (ti / TREC_SLOTS) & 1);
             const TileRec &R = cs.trec[st];
             if (R.end) break;
-            const int rows = R.rows;
-            uint32_t mask[4] = {R.mask[0], R.mask[1], R.mask[2], R.mask[3]};
-            for (int c = next_bit(mask, 0); c >= 0; c = next_bit(mask, c + 1), ++ii) {
-                const int si = ii % IDX_SLOTS;
-                ptx::mbar_wait(ptx::smem_u32(&cs.idx_full[si]), (ii / IDX_SLOTS) & 1);
+            const int rows = R.rows, ncols = R.ncols;
+            const int bs = ti % BLK_SLOTS;
+            ptx::mbar_wait(ptx::smem_u32(&cs.blk_full[bs]), (ti / BLK_SLOTS) & 1);
+            const int32_t *B = blk + bs * blk_stride;
+            for (int ci = 0; ci < ncols; ++ci) {
+                const int c = p.mode == 0 ? R.cols[ci] : 0;
+                if (threadIdx.x == 0) TR(0, ptr_ctr);
                 const char *gp[NB];
-                uint32_t sz[NB], so[NB];
+                bool ok[NB];
+                uint32_t so[NB];
 #pragma unroll
                 for (int b = 0; b < NB; ++b) {
-                    const int r = warp * 32 + b * RPI + r_in;
-                    const int32_t g = r < rows ? cs.idx[si][r] : -1;
+                    const int r = warp * ROWS_W + b * RPI + r_in;
+                    const int32_t g = r < rows ? B[r * kd + c] : -1;
                     const uint32_t f = rb == 128 ? (r & 7) : (rb == 64 ? ((r >> 1) & 3) : ((r >> 2) & 1));
-                    gp[b] = g >= 0 ? p.f_in + (int64_t)g * p.ld_in_bytes + q_lane * 16 : p.f_in;
-                    sz[b] = g >= 0 ? 16u : 0u;
+                    ok[b] = g >= 0;
+                    gp[b] = p.f_in + (ok[b] ? (int64_t)g * p.ld_in_bytes + q_lane * 16 : 0);
                     so[b] = (uint32_t)r * rb + ((q_lane ^ f) * 16);
                 }
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&cs.idx_empty[si]));
-                for (int cc = 0; cc < p.n_chunks; ++cc, ++it) {
-                    const int s = it % S;
-                    ptx::mbar_wait(ptx::smem_u32(&cs.empty[s]), ((it / S) & 1) ^ 1);
-                    if (threadIdx.x == 0) TR(0, it);
+                for (int cc = 0; cc < p.n_chunks; ++cc) {
+                    if (threadIdx.x == 0) TR(4, ptr_ctr);
+                    ptx::mbar_wait(ptx::smem_u32(&cs.empty[s]), ph ^ 1);
+                    if (threadIdx.x == 0) TR(1, ptr_ctr);
                     const uint32_t abase = ptx::smem_u32(sa + (size_t)s * p.a_bytes);
 #pragma unroll
-                    for (int b = 0; b < NB; ++b)
-#pragma unroll
-                        for (int t = 0; t < NT; ++t)
-                            ptx::cp_async_16(abase + (so[b] ^ (uint32_t)(t * Q * 16)), gp[b] + t * Q * 16, sz[b]);
+                    for (int b = 0; b < NB; ++b) {
+                        // matched rows: one whole-line request per row; sentinel rows (no
+                        // input voxel) never touch L2: zero them with a shared store
+                        if (ok[b]) ptx::cp_async_16(abase + so[b], gp[b], 16u);
+                        else asm volatile("st.shared.v4.b32 [%0], {%1,%1,%1,%1};" ::"r"(abase + so[b]), "r"(0) : "memory");
+                    }
                     ptx::cp_async_mbar_arrive(ptx::smem_u32(&cs.full[s]));
+                    if (threadIdx.x == 0) TR(5, ptr_ctr);
+#ifdef SPC_EXP_TRACE
+                    ++ptr_ctr;
+#endif
 #pragma unroll
-                    for (int b = 0; b < NB; ++b) gp[b] += sz[b] ? rb : 0;
+                    for (int b = 0; b < NB; ++b) gp[b] += ok[b] ? rb : 0;
+                    if (++s == S) { s = 0; ph ^= 1; }
                 }
             }
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&cs.trec_empty[st]));
+            if (lane == 0) {
+                ptx::mbar_arrive(ptx::smem_u32(&cs.blk_empty[bs]));
+                ptx::mbar_arrive(ptx::smem_u32(&cs.trec_empty[st]));
+            }
         }
         ptx::cp_async_wait<0>();
     } else if (warp == W_BLOAD) {
@@ -392,6 +418,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                         const int s = it % S;
                         ptx::mbar_wait(ptx::smem_u32(&cs.empty[s]), ((it / S) & 1) ^ 1);
                         const uint32_t fb = ptx::smem_u32(&cs.full[s]);
+#ifdef SPC_EXP_NO_B
+                        if (it >= (uint32_t)S) { ptx::mbar_arrive(fb); continue; }
+#endif
                         ptx::mbar_arrive_expect_tx(fb, p.b_bytes);
                         const int64_t blob = ((int64_t)k * p.n_ntiles + nt) * p.n_chunks + cc;
                         ptx::bulk_g2s(ptx::smem_u32(sb + (size_t)s * p.b_bytes), p.wblob + blob * p.b_bytes, p.b_bytes,
@@ -424,7 +453,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                         TR(2, it);
                         // the A tile was written by cp.async (generic proxy): order it before
                         // the tensor core's async-proxy reads
+#ifndef SPC_EXP_NO_FENCE
                         ptx::fence_proxy_async();
+#endif
                         ptx::tc_fence_after();
                         const uint32_t a_base = ptx::smem_u32(sa + (size_t)s * p.a_bytes);
                         const uint32_t b_base = ptx::smem_u32(sb + (size_t)s * p.b_bytes);
@@ -432,7 +463,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                         for (int kk = 0; kk < BK / 16; ++kk) {
                             const uint64_t ad = ptx::umma_desc_kmajor_sw(a_base + kk * 32, rb);
                             const uint64_t bd = ptx::umma_desc_kmajor_sw(b_base + kk * 32, rb);
+#ifndef SPC_EXP_NO_MMA
                             ptx::mma_f16_ss(d_tmem, ad, bd, p.idesc, acc);
+#endif
                             acc = 1;
                         }
                         ptx::mma_commit(ptx::smem_u32(&cs.empty[s]));
@@ -444,21 +477,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             }
             __syncwarp();
         }
-    } else if (warp >= 4 && warp < 8) {
-        // ===================== epilogue (warps 4-7, thread = TMEM lane = tile row) =====
-        const int e = warp - 4;
+    } else if (warp >= W_EPI0 && warp < W_EPI0 + 4) {
+        // ===================== epilogue (warps 8-11, thread = TMEM lane = tile row) ====
+        const int e = warp - W_EPI0;   // == warp % 4: the TMEM lane quadrant this warp may access
         const int r = e * 32 + lane;
         for (uint32_t ti = 0;; ++ti) {
             const int st = ti % TREC_SLOTS;
-            ptx::mbar_wait(ptx::smem_u32(&cs.trec_full[st]), (ti / TREC_SLOTS) & 1);
+            ptx::mbar_wait_sleep(ptx::smem_u32(&cs.trec_full[st]), (ti / TREC_SLOTS) & 1);
             const TileRec &R = cs.trec[st];
             if (R.end) break;
             const uint32_t a = ti & 1;
             int64_t orow = -1;
             if (r < R.rows) orow = p.mode == 0 ? R.row0 + r : (int64_t)R.scatter[r];
             const int nt = R.nt;
-            ptx::mbar_wait(ptx::smem_u32(&cs.tfull[a]), (ti >> 1) & 1);
-            if (threadIdx.x == 128) TR(6, ti);
+            ptx::mbar_wait_sleep(ptx::smem_u32(&cs.tfull[a]), (ti >> 1) & 1);
+            if (threadIdx.x == 32 * W_EPI0) TR(6, ti);
             ptx::tc_fence_after();
             const uint32_t tbase = tmem_base + a * p.tmem_cols + ((uint32_t)(e * 32) << 16);
             for (int col = 0; col < p.BN; col += 32) {
@@ -483,7 +516,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             }
             ptx::tc_fence_before();
             __syncwarp();
-            if (threadIdx.x == 128) TR(7, ti);
+            if (threadIdx.x == 32 * W_EPI0) TR(7, ti);
             if (lane == 0) {
                 ptx::mbar_arrive(ptx::smem_u32(&cs.tempty[a]));
                 ptx::mbar_arrive(ptx::smem_u32(&cs.trec_empty[st]));
@@ -778,9 +811,14 @@ static spc_status launch_tc(const ConvParams &p0, int mode, int out_kind, void *
     p.out = out;
     p.ld_out = ld_out;
     const size_t stage = (size_t)p.a_bytes + p.b_bytes;
-    const size_t extra = sizeof(ConvSmem) + 1024 + 64;   // + alignment slack
+    const int kd = mode == 0 ? p.k_dense : 1;
+    const size_t extra = ((sizeof(ConvSmem) + 127) & ~size_t(127)) + (size_t)BLK_SLOTS * ((TC_BM * kd + 3) & ~3) * 4 +
+                         1024 + 64;   // + alignment slack
     int S = (int)((TC_SMEM_BUDGET - extra) / stage);
-    if (S > 8) S = 8;
+#ifndef SPC_MAX_STAGES
+#define SPC_MAX_STAGES 16
+#endif
+    if (S > SPC_MAX_STAGES) S = SPC_MAX_STAGES;
     if (S < 2) return fail(SPC_ERR_UNSUPPORTED, "spc_conv_forward: tile does not fit shared memory");
     p.stages = S;
     const size_t smem = stage * S + extra;

@@ -24,8 +24,31 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+__device__ __forceinline__ bool mbar_test_wait(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+#ifdef SPC_EXP_TESTWAIT
+    while (!mbar_test_wait(bar, parity)) {
+    }
+#else
     while (!mbar_try_wait(bar, parity)) {
+    }
+#endif
+}
+// wait with exponential back-off: for waiters off the critical path (epilogue, scheduler),
+// so their polling does not compete with the pipeline's own mbarrier traffic
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
+    uint32_t ns = 32;
+    while (!mbar_try_wait(bar, parity)) {
+        __nanosleep(ns);
+        if (ns < 1024) ns <<= 1;
     }
 }
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
