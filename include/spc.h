@@ -229,7 +229,8 @@ spc_status spc_kmap_export(const spc_kmap *kmap, int32_t *triples_host, int64_t 
  * f_out  : [n_out][ld_out] elements of out_dtype, first c_out written.
  * residual: nullable, [n_out][ld_res] elements of out_dtype, added to the result.
  * Arithmetic: f16/bf16 inputs -> tcgen05.mma kind::f16 with fp32 accumulation in TMEM;
- * f32 inputs -> FFMA (fp32).  c_in, c_out multiples of 16 (f16/bf16) or 4 (f32),
+ * f32 inputs -> FFMA (fp32).  c_in, c_out multiples of 16 (f16/bf16); f32: c_in % 4 == 0,
+ * c_out % 8 == 0;
  * c_out <= 256 per weight tile (larger c_out is tiled).
  * ws     : >= spc_conv_workspace_size() bytes (fp32 accumulator of the WS part).
  * ================================================================================ */

@@ -95,5 +95,5 @@ namespace spc {
 size_t radix_sort_workspace(int64_t n, bool with_vals);
 spc_status radix_sort(const uint64_t *keys_in, const int32_t *vals_in /*nullable: identity*/, int64_t n,
                       const int64_t *n_dev, int n_bits, uint64_t *keys_out, int32_t *vals_out /*nullable*/,
-                      void *ws, size_t ws_bytes, cudaStream_t st);
+                      void *ws, size_t ws_bytes, cudaStream_t st, bool hist_done);
 }  // namespace spc

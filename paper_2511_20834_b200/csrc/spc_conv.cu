@@ -58,7 +58,8 @@ struct ConvParams {
     int n_chunks, n_ntiles, BK, BN;
     uint32_t a_bytes, b_bytes;
     int stages;
-    uint32_t tmem_cols;   // per accumulator stage (power of two >= 32)
+    int bm;               // rows per tile: 128 or 256 (two M=128 MMAs sharing the weight tile)
+    uint32_t tmem_cols;   // per 128-row accumulator (power of two >= 32)
     uint32_t idesc;
     // output
     void *out;
@@ -86,13 +87,17 @@ __device__ __forceinline__ void decode_tile(const ConvParams &p, int64_t v, cons
     t.nt = (int)(v % p.n_ntiles);
     const int64_t tv = v / p.n_ntiles;
     if (p.mode == 0) {
-        t.row0 = tv * TC_BM;
-        t.rows = (int)imin64(TC_BM, n_out - t.row0);
+        t.row0 = tv * p.bm;
+        t.rows = (int)imin64(p.bm, n_out - t.row0);
         t.list = t.dir = 0;
         t.k = -1;
         bool any = false;
+        const int64_t mt0 = t.row0 / 128, mt1 = (t.row0 + t.rows - 1) / 128;   // kernel-map mask tiles
         for (int w = 0; w < 4; ++w) {
-            t.mask[w] = w < p.tile_words ? p.tile_mask[tv * p.tile_words + w] : 0u;
+            uint32_t m = 0;
+            if (w < p.tile_words)
+                for (int64_t mt = mt0; mt <= mt1; ++mt) m |= p.tile_mask[mt * p.tile_words + w];
+            t.mask[w] = m;
             any |= t.mask[w] != 0;
         }
         if (!any) t.mask[0] = 1u;   // keep one (all-sentinel) step so the tile is written
@@ -101,12 +106,12 @@ __device__ __forceinline__ void decode_tile(const ConvParams &p, int64_t v, cons
         while (l + 1 < p.n_lists && list_prefix[l + 1] <= tv) ++l;
         const int local = (int)(tv - list_prefix[l]);
         const int cnt = p.counts[SPC_MAX_KVOL + l];
-        const int per = (cnt + TC_BM - 1) / TC_BM;
+        const int per = (cnt + p.bm - 1) / p.bm;
         t.list = l;
         t.dir = local / per;
         const int tl = local - t.dir * per;
-        t.row0 = (int64_t)tl * TC_BM;
-        t.rows = min(TC_BM, cnt - tl * TC_BM);
+        t.row0 = (int64_t)tl * p.bm;
+        t.rows = min(p.bm, cnt - tl * p.bm);
         t.k = t.dir ? p.k_vol - 1 - p.list_k[l] : p.list_k[l];
         t.mask[0] = 1u;
         t.mask[1] = t.mask[2] = t.mask[3] = 0u;
@@ -198,7 +203,7 @@ struct TileRec {
     int rows, nt, list, dir, k, end, ncols;
     uint32_t mask[4];
     uint8_t cols[128];        // active step columns (OS: dense offsets with a match; WS: {0})
-    int32_t scatter[TC_BM];   // WS: output row of each pair row (OS: unused)
+    int32_t scatter[256];     // WS: output row of each pair row (OS: unused)
 };
 
 struct ConvSmem {
@@ -217,8 +222,9 @@ __device__ long long g_tr[8][4096];
 #define TR(slot, i) do {} while (0)
 #endif
 
-template <int BK>
+template <int BK, int BM>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant__ ConvParams p) {
+    constexpr int NH = BM / TC_BM;   // 128-row MMA halves per tile
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // stage buffers need 1024-byte alignment (swizzle atoms)
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -230,7 +236,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     // copy per tile); WS: the 128 gather indices of the tile's pairs
     const int kd = p.mode == 0 ? p.k_dense : 1;
     int32_t *blk = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(&cs) + ((sizeof(ConvSmem) + 127) & ~size_t(127)));
-    const int blk_stride = (TC_BM * kd + 3) & ~3;   // int32 per block (16-byte multiple)
+    const int blk_stride = (BM * kd + 3) & ~3;      // int32 per block (16-byte multiple)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t n_out = dev_count(p.n_out_cap, p.n_out_dev);
@@ -255,7 +261,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         ptx::fence_mbar_init();
         ptx::fence_proxy_async();
     }
-    if (warp == W_MMA) ptx::tmem_alloc(ptx::smem_u32(cs.tmem_holder), 2 * p.tmem_cols);
+    if (warp == W_MMA) ptx::tmem_alloc(ptx::smem_u32(cs.tmem_holder), 2 * NH * p.tmem_cols);
     if (p.mode == 1 && warp == W_SCHED) {
         // virtual-tile prefix over the WS lists (device-side counts, no host sync)
         int carry = 0;
@@ -264,7 +270,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             int v = 0;
             if (l < p.n_lists) {
                 const int cnt = p.counts[SPC_MAX_KVOL + l];
-                v = ((cnt + TC_BM - 1) / TC_BM) * (p.list_mirror[l] ? 2 : 1);
+                v = ((cnt + BM - 1) / BM) * (p.list_mirror[l] ? 2 : 1);
             }
             int x = v;
             for (int o = 1; o < 32; o <<= 1) {
@@ -286,9 +292,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     if (warp == W_SCHED) {
         // ===================== scheduler: tile records + gather indices ==================
         int64_t n_tiles;
-        if (p.mode == 0) n_tiles = ((n_out + TC_BM - 1) / TC_BM) * p.n_ntiles;
+        if (p.mode == 0) n_tiles = ((n_out + BM - 1) / BM) * p.n_ntiles;
         else n_tiles = (int64_t)cs.list_prefix[p.n_lists] * p.n_ntiles;
-        uint32_t ti = 0, ii = 0;
+        uint32_t ti = 0;
         for (int64_t v = blockIdx.x;; v += gridDim.x, ++ti) {
             const int st = ti % TREC_SLOTS;
             ptx::mbar_wait_sleep(ptx::smem_u32(&cs.trec_empty[st]), ((ti / TREC_SLOTS) & 1) ^ 1);
@@ -309,7 +315,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             }
             if (p.mode == 1) {
                 const int32_t *pr = reinterpret_cast<const int32_t *>(p.pairs + t.list * p.list_stride + t.row0);
-                for (int r = lane; r < TC_BM; r += 32) R.scatter[r] = r < t.rows ? pr[2 * r + (t.dir ? 0 : 1)] : -1;
+                for (int r = lane; r < BM; r += 32) R.scatter[r] = r < t.rows ? pr[2 * r + (t.dir ? 0 : 1)] : -1;
             }
             ptx::mbar_arrive(ptx::smem_u32(&cs.trec_full[st]));
             // the tile's gather indices: one contiguous block
@@ -327,7 +333,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                 if (lane != 0) ptx::mbar_arrive(fb);
             } else {
                 const int32_t *pr = reinterpret_cast<const int32_t *>(p.pairs + t.list * p.list_stride + t.row0);
-                for (int r = lane; r < TC_BM; r += 32) B[r] = r < t.rows ? pr[2 * r + (t.dir ? 1 : 0)] : -1;
+                for (int r = lane; r < BM; r += 32) B[r] = r < t.rows ? pr[2 * r + (t.dir ? 1 : 0)] : -1;
                 ptx::mbar_arrive(fb);
             }
         }
@@ -340,7 +346,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         constexpr int NQ = BK / 8;                 // 16-byte chunks per row segment
         constexpr int Q = NQ;                      // chunks per warp instruction (whole rows)
         constexpr int RPI = 32 / Q;                // rows per warp instruction (4 / 8 / 16)
-        constexpr int ROWS_W = TC_BM / N_GATHER;   // rows per warp (16)
+        constexpr int ROWS_W = BM / N_GATHER;      // rows per warp (16 or 32)
         constexpr int NB = ROWS_W / RPI;           // row blocks per warp
         const int r_in = lane % RPI, q_lane = lane / RPI;
         int s = 0;
@@ -444,7 +450,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                 const uint32_t a = ti & 1;
                 ptx::mbar_wait(ptx::smem_u32(&cs.tempty[a]), ((ti >> 1) & 1) ^ 1);
                 ptx::tc_fence_after();
-                const uint32_t d_tmem = tmem_base + a * p.tmem_cols;
+                const uint32_t d_tmem = tmem_base + a * NH * p.tmem_cols;
                 uint32_t acc = 0;
                 for (int c = next_bit(mask, 0); c >= 0; c = next_bit(mask, c + 1)) {
                     for (int cc = 0; cc < p.n_chunks; ++cc, ++it) {
@@ -461,11 +467,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                         const uint32_t b_base = ptx::smem_u32(sb + (size_t)s * p.b_bytes);
 #pragma unroll
                         for (int kk = 0; kk < BK / 16; ++kk) {
-                            const uint64_t ad = ptx::umma_desc_kmajor_sw(a_base + kk * 32, rb);
                             const uint64_t bd = ptx::umma_desc_kmajor_sw(b_base + kk * 32, rb);
-#ifndef SPC_EXP_NO_MMA
-                            ptx::mma_f16_ss(d_tmem, ad, bd, p.idesc, acc);
-#endif
+#pragma unroll
+                            for (int h = 0; h < NH; ++h) {
+                                const uint64_t ad = ptx::umma_desc_kmajor_sw(a_base + h * TC_BM * rb + kk * 32, rb);
+                                ptx::mma_f16_ss(d_tmem + h * p.tmem_cols, ad, bd, p.idesc, acc);
+                            }
                             acc = 1;
                         }
                         ptx::mma_commit(ptx::smem_u32(&cs.empty[s]));
@@ -480,37 +487,40 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     } else if (warp >= W_EPI0 && warp < W_EPI0 + 4) {
         // ===================== epilogue (warps 8-11, thread = TMEM lane = tile row) ====
         const int e = warp - W_EPI0;   // == warp % 4: the TMEM lane quadrant this warp may access
-        const int r = e * 32 + lane;
         for (uint32_t ti = 0;; ++ti) {
             const int st = ti % TREC_SLOTS;
             ptx::mbar_wait_sleep(ptx::smem_u32(&cs.trec_full[st]), (ti / TREC_SLOTS) & 1);
             const TileRec &R = cs.trec[st];
             if (R.end) break;
             const uint32_t a = ti & 1;
-            int64_t orow = -1;
-            if (r < R.rows) orow = p.mode == 0 ? R.row0 + r : (int64_t)R.scatter[r];
             const int nt = R.nt;
             ptx::mbar_wait_sleep(ptx::smem_u32(&cs.tfull[a]), (ti >> 1) & 1);
             if (threadIdx.x == 32 * W_EPI0) TR(6, ti);
             ptx::tc_fence_after();
-            const uint32_t tbase = tmem_base + a * p.tmem_cols + ((uint32_t)(e * 32) << 16);
-            for (int col = 0; col < p.BN; col += 32) {
-                uint32_t vals[32];
-                const int n = min(32, p.BN - col);
-                if (n == 32) ptx::tmem_ld32(tbase + col, vals);
-                else ptx::tmem_ld16(tbase + col, vals);
-                ptx::tmem_ld_wait();
-                if (orow >= 0) {
-                    const int gcol = nt * p.BN + col;
-                    if (p.out_kind == OUT_F32_RED) {
-                        float *op = static_cast<float *>(p.out) + orow * p.ld_out + gcol;
+#pragma unroll 1
+            for (int h = 0; h < NH; ++h) {
+                const int r = h * TC_BM + e * 32 + lane;
+                int64_t orow = -1;
+                if (r < R.rows) orow = p.mode == 0 ? R.row0 + r : (int64_t)R.scatter[r];
+                const uint32_t tbase = tmem_base + (a * NH + h) * p.tmem_cols + ((uint32_t)(e * 32) << 16);
+                for (int col = 0; col < p.BN; col += 32) {
+                    uint32_t vals[32];
+                    const int n = min(32, p.BN - col);
+                    if (n == 32) ptx::tmem_ld32(tbase + col, vals);
+                    else ptx::tmem_ld16(tbase + col, vals);
+                    ptx::tmem_ld_wait();
+                    if (orow >= 0) {
+                        const int gcol = nt * p.BN + col;
+                        if (p.out_kind == OUT_F32_RED) {
+                            float *op = static_cast<float *>(p.out) + orow * p.ld_out + gcol;
 #pragma unroll
-                        for (int q = 0; q < 8; ++q)
-                            if (q * 4 < n)
-                                ptx::red_add_v4(op + 4 * q, to_f(vals[4 * q]), to_f(vals[4 * q + 1]),
-                                                to_f(vals[4 * q + 2]), to_f(vals[4 * q + 3]));
-                    } else {
-                        store_row(p, orow, gcol, vals, n);
+                            for (int q = 0; q < 8; ++q)
+                                if (q * 4 < n)
+                                    ptx::red_add_v4(op + 4 * q, to_f(vals[4 * q]), to_f(vals[4 * q + 1]),
+                                                    to_f(vals[4 * q + 2]), to_f(vals[4 * q + 3]));
+                        } else {
+                            store_row(p, orow, gcol, vals, n);
+                        }
                     }
                 }
             }
@@ -527,7 +537,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     __syncthreads();
     if (warp == W_MMA) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc(tmem_base, 2 * p.tmem_cols);
+        ptx::tmem_dealloc(tmem_base, 2 * NH * p.tmem_cols);
     }
 }
 
@@ -672,26 +682,43 @@ __global__ void k_prepare_weight_tc(const uint16_t *__restrict__ w, int k_vol, i
     }
 }
 
+// fp32 accumulator -> output dtype (+ residual): 8 columns per thread, 16/32-byte accesses
 __global__ void k_convert(const float *__restrict__ acc, int64_t ld_acc, int64_t n_cap, const int64_t *n_dev, int c_out,
                           int out_dtype, void *__restrict__ out, int64_t ld_out, const void *__restrict__ res,
                           int64_t ld_res) {
     const int64_t n = dev_count(n_cap, n_dev);
-    const int64_t total = n * c_out;
+    const int g8 = c_out / 8;                 // c_out is a multiple of 16
+    const int64_t total = n * g8;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = e / c_out;
-        const int c = (int)(e - r * c_out);
-        float v = acc[r * ld_acc + c];
+        const int64_t r = e / g8;
+        const int c = (int)(e - r * g8) * 8;
+        const float4 a0 = *reinterpret_cast<const float4 *>(acc + r * ld_acc + c);
+        const float4 a1 = *reinterpret_cast<const float4 *>(acc + r * ld_acc + c + 4);
+        float v[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
         if (out_dtype == SPC_F32) {
-            if (res) v += static_cast<const float *>(res)[r * ld_res + c];
-            static_cast<float *>(out)[r * ld_out + c] = v;
+            if (res) {
+                const float4 b0 = *reinterpret_cast<const float4 *>(static_cast<const float *>(res) + r * ld_res + c);
+                const float4 b1 = *reinterpret_cast<const float4 *>(static_cast<const float *>(res) + r * ld_res + c + 4);
+                v[0] += b0.x; v[1] += b0.y; v[2] += b0.z; v[3] += b0.w;
+                v[4] += b1.x; v[5] += b1.y; v[6] += b1.z; v[7] += b1.w;
+            }
+            float *o = static_cast<float *>(out) + r * ld_out + c;
+            *reinterpret_cast<float4 *>(o) = make_float4(v[0], v[1], v[2], v[3]);
+            *reinterpret_cast<float4 *>(o + 4) = make_float4(v[4], v[5], v[6], v[7]);
         } else {
             if (res) {
-                const uint16_t h = static_cast<const uint16_t *>(res)[r * ld_res + c];
-                v += out_dtype == SPC_BF16 ? __bfloat162float(__ushort_as_bfloat16(h)) : __half2float(__ushort_as_half(h));
+                const uint4 u = *reinterpret_cast<const uint4 *>(static_cast<const uint16_t *>(res) + r * ld_res + c);
+                const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float2 f = unpack2(w[q], out_dtype);
+                    v[2 * q] += f.x;
+                    v[2 * q + 1] += f.y;
+                }
             }
-            static_cast<uint16_t *>(out)[r * ld_out + c] = out_dtype == SPC_BF16
-                                                               ? __bfloat16_as_ushort(__float2bfloat16_rn(v))
-                                                               : __half_as_ushort(__float2half_rn(v));
+            *reinterpret_cast<uint4 *>(static_cast<uint16_t *>(out) + r * ld_out + c) =
+                make_uint4(pack2(v[0], v[1], out_dtype), pack2(v[2], v[3], out_dtype), pack2(v[4], v[5], out_dtype),
+                           pack2(v[6], v[7], out_dtype));
         }
     }
 }
@@ -812,7 +839,7 @@ static spc_status launch_tc(const ConvParams &p0, int mode, int out_kind, void *
     p.ld_out = ld_out;
     const size_t stage = (size_t)p.a_bytes + p.b_bytes;
     const int kd = mode == 0 ? p.k_dense : 1;
-    const size_t extra = ((sizeof(ConvSmem) + 127) & ~size_t(127)) + (size_t)BLK_SLOTS * ((TC_BM * kd + 3) & ~3) * 4 +
+    const size_t extra = ((sizeof(ConvSmem) + 127) & ~size_t(127)) + (size_t)BLK_SLOTS * ((p.bm * kd + 3) & ~3) * 4 +
                          1024 + 64;   // + alignment slack
     int S = (int)((TC_SMEM_BUDGET - extra) / stage);
 #ifndef SPC_MAX_STAGES
@@ -824,17 +851,26 @@ static spc_status launch_tc(const ConvParams &p0, int mode, int out_kind, void *
     const size_t smem = stage * S + extra;
     static bool configured = false;
     if (!configured) {
-        SPC_CUDA(cudaFuncSetAttribute(k_conv_tc<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BUDGET));
-        SPC_CUDA(cudaFuncSetAttribute(k_conv_tc<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BUDGET));
-        SPC_CUDA(cudaFuncSetAttribute(k_conv_tc<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BUDGET));
+        SPC_CUDA(cudaFuncSetAttribute(k_conv_tc<16, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BUDGET));
+        SPC_CUDA(cudaFuncSetAttribute(k_conv_tc<32, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BUDGET));
+        SPC_CUDA(cudaFuncSetAttribute(k_conv_tc<64, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BUDGET));
+        SPC_CUDA(cudaFuncSetAttribute(k_conv_tc<16, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BUDGET));
+        SPC_CUDA(cudaFuncSetAttribute(k_conv_tc<32, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BUDGET));
+        SPC_CUDA(cudaFuncSetAttribute(k_conv_tc<64, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BUDGET));
         configured = true;
     }
     // persistent: one CTA per SM (the WS tile count lives on the device)
-    int64_t tiles_cap = mode == 0 ? ((p.n_out_cap + TC_BM - 1) / TC_BM) * p.n_ntiles : (int64_t)num_sms();
+    int64_t tiles_cap = mode == 0 ? ((p.n_out_cap + p.bm - 1) / p.bm) * p.n_ntiles : (int64_t)num_sms();
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles_cap, num_sms()));
-    if (p.BK == 64) k_conv_tc<64><<<grid, TC_THREADS, smem, st>>>(p);
-    else if (p.BK == 32) k_conv_tc<32><<<grid, TC_THREADS, smem, st>>>(p);
-    else k_conv_tc<16><<<grid, TC_THREADS, smem, st>>>(p);
+    if (p.bm == 256) {
+        if (p.BK == 64) k_conv_tc<64, 256><<<grid, TC_THREADS, smem, st>>>(p);
+        else if (p.BK == 32) k_conv_tc<32, 256><<<grid, TC_THREADS, smem, st>>>(p);
+        else k_conv_tc<16, 256><<<grid, TC_THREADS, smem, st>>>(p);
+    } else {
+        if (p.BK == 64) k_conv_tc<64, 128><<<grid, TC_THREADS, smem, st>>>(p);
+        else if (p.BK == 32) k_conv_tc<32, 128><<<grid, TC_THREADS, smem, st>>>(p);
+        else k_conv_tc<16, 128><<<grid, TC_THREADS, smem, st>>>(p);
+    }
     SPC_LAUNCH_CHECK("k_conv_tc");
     return SPC_OK;
 }
@@ -883,7 +919,7 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
     }
 
     if (in_dtype == SPC_F32) {
-        SPC_CHECK_ARG(c_in % 4 == 0 && c_out % 4 == 0, "f32 path needs channels multiple of 4");
+        SPC_CHECK_ARG(c_in % 4 == 0 && c_out % 8 == 0, "f32 path needs c_in % 4 == 0 and c_out % 8 == 0");
         const dim3 block(256);
         const unsigned gy = (unsigned)((c_out + SM_TN - 1) / SM_TN);
         if (has_os) {
@@ -909,8 +945,9 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
                 q, static_cast<const float *>(weight), c_in, c_out);
             SPC_LAUNCH_CHECK("k_conv_simt ws");
             if (acc != f_out) {
-                k_convert<<<2048, 256, 0, st>>>(acc, ld_acc, km->n_out, km->n_out_dev, c_out, out_dtype, f_out, ld_out,
-                                                residual, ld_res);
+                const int64_t work = km->n_out * (c_out / 8);
+                k_convert<<<(unsigned)std::min<int64_t>((work + 255) / 256, 8 * 148), 256, 0, st>>>(
+                    acc, ld_acc, km->n_out, km->n_out_dev, c_out, out_dtype, f_out, ld_out, residual, ld_res);
                 SPC_LAUNCH_CHECK("k_convert");
             }
         }
@@ -924,9 +961,12 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
     p.BN = pick_bn(c_out);
     p.n_chunks = c_in / p.BK;
     p.n_ntiles = c_out / p.BN;
-    p.a_bytes = (uint32_t)(TC_BM * p.BK * 2);
-    p.b_bytes = (uint32_t)(p.BN * p.BK * 2);
     p.tmem_cols = pow2_cols(p.BN);
+    // 256-row tiles (two MMAs per weight tile) whenever four accumulators fit TMEM
+    p.bm = (4 * p.tmem_cols <= 512 && !getenv("SPC_BM128")) ? 256 : 128;
+    if (has_os && (size_t)BLK_SLOTS * p.bm * km->k_dense * 4 > 96 * 1024) p.bm = 128;   // OS index blocks (K=5)
+    p.a_bytes = (uint32_t)(p.bm * p.BK * 2);
+    p.b_bytes = (uint32_t)(p.BN * p.BK * 2);
     p.idesc = ptx::umma_idesc_f16(in_dtype == SPC_BF16, TC_BM, p.BN);
     p.wblob = static_cast<const char *>(weight);
     if (has_os) {
@@ -940,8 +980,9 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
         spc_status s = launch_tc(p, 1, OUT_F32_RED, acc, ld_acc, st);
         if (s != SPC_OK) return s;
         if (acc != f_out) {
-            k_convert<<<2048, 256, 0, st>>>(acc, ld_acc, km->n_out, km->n_out_dev, c_out, out_dtype, f_out, ld_out,
-                                            residual, ld_res);
+            const int64_t work = km->n_out * (c_out / 8);
+            k_convert<<<(unsigned)std::min<int64_t>((work + 255) / 256, 8 * 148), 256, 0, st>>>(
+                acc, ld_acc, km->n_out, km->n_out_dev, c_out, out_dtype, f_out, ld_out, residual, ld_res);
             SPC_LAUNCH_CHECK("k_convert");
         }
     }

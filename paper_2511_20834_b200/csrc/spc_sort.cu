@@ -45,144 +45,146 @@ __device__ __forceinline__ int block_excl_scan_256(int v, int *warp_sums, int &t
     return before;
 }
 
-__global__ void __launch_bounds__(SORT_THREADS) k_radix_hist(const uint64_t *__restrict__ keys,
-                                                             int64_t n_cap, const int64_t *n_dev,
-                                                             int shift, int *__restrict__ hist,
-                                                             int n_tiles) {
-    __shared__ int cnt[256];
-    const int tile = blockIdx.x;
-    cnt[threadIdx.x] = 0;
+// ---- onesweep LSD radix sort --------------------------------------------------------------
+// k_hist_all   : digit histograms of EVERY pass in one read of the keys (smem, then global atomics)
+// k_hist_scan  : exclusive scan of each pass's 256-bin histogram -> global digit bases
+// k_onesweep   : one launch per pass; tiles are claimed in order from an atomic counter,
+//                ranked locally (__match_any_sync, stable), and get their global offsets by
+//                decoupled look-back over the per-tile digit counts of earlier tiles.
+constexpr int OS_ITEMS = 8;
+constexpr int OS_TILE = SORT_THREADS * OS_ITEMS;   // 2048 keys per tile
+constexpr int MAX_PASSES = 8;
+constexpr uint32_t ST_AGG = 1u << 30, ST_INC = 2u << 30, ST_VAL = (1u << 30) - 1;
+
+__global__ void __launch_bounds__(SORT_THREADS) k_hist_all(const uint64_t *__restrict__ keys, int64_t n_cap,
+                                                           const int64_t *n_dev, int passes,
+                                                           unsigned int *__restrict__ ghist) {
+    __shared__ unsigned int h[MAX_PASSES][256];
+    for (int i = threadIdx.x; i < passes * 256; i += SORT_THREADS) h[i / 256][i % 256] = 0;
     __syncthreads();
     const int64_t n = dev_count(n_cap, n_dev);
-    const int64_t base = (int64_t)tile * SORT_TILE;
-#pragma unroll
-    for (int it = 0; it < SORT_ITEMS; ++it) {
-        int64_t idx = base + it * SORT_THREADS + threadIdx.x;
-        bool valid = idx < n;
-        unsigned d = valid ? (unsigned)((keys[idx] >> shift) & 255u) : 256u + (threadIdx.x & 31);
-        unsigned peers = __match_any_sync(0xffffffffu, d);
-        if (valid && (lanemask_lt() & peers) == 0) atomicAdd(&cnt[d], __popc(peers));
+    for (int64_t i = blockIdx.x * (int64_t)SORT_THREADS + threadIdx.x; i < n; i += (int64_t)gridDim.x * SORT_THREADS) {
+        const uint64_t k = keys[i];
+        for (int p = 0; p < passes; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 255u], 1u);
     }
     __syncthreads();
-    hist[threadIdx.x * n_tiles + tile] = cnt[threadIdx.x];
+    for (int i = threadIdx.x; i < passes * 256; i += SORT_THREADS)
+        if (h[i / 256][i % 256]) atomicAdd(&ghist[i], h[i / 256][i % 256]);
 }
 
-// one CTA per digit: exclusive scan of hist[d][0..n_tiles) in place, total -> totals[d]
-__global__ void __launch_bounds__(1024) k_radix_scan(int *__restrict__ hist, int n_tiles,
-                                                     int *__restrict__ totals) {
-    __shared__ int wsum[32];
-    __shared__ int carry_s;
-    int *row = hist + (int64_t)blockIdx.x * n_tiles;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    if (threadIdx.x == 0) carry_s = 0;
-    __syncthreads();
-    for (int base = 0; base < n_tiles; base += 1024) {
-        int i = base + threadIdx.x;
-        int v = i < n_tiles ? row[i] : 0;
-        int x = v;
-#pragma unroll
+__global__ void k_hist_scan(unsigned int *__restrict__ ghist, int passes) {
+    // one warp per pass: exclusive scan of 256 counters in place
+    const int p = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (p >= passes) return;
+    unsigned int *h = ghist + p * 256;
+    unsigned int carry = 0;
+    for (int base = 0; base < 256; base += 32) {
+        const unsigned int v = h[base + lane];
+        unsigned int x = v;
         for (int o = 1; o < 32; o <<= 1) {
-            int y = __shfl_up_sync(0xffffffffu, x, o);
+            unsigned int y = __shfl_up_sync(0xffffffffu, x, o);
             if (lane >= o) x += y;
         }
-        if (lane == 31) wsum[w] = x;
-        __syncthreads();
-        if (w == 0) {
-            int s = wsum[lane];
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                int y = __shfl_up_sync(0xffffffffu, s, o);
-                if (lane >= o) s += y;
-            }
-            wsum[lane] = s;
-        }
-        __syncthreads();
-        int carry = carry_s;
-        int excl = carry + (w > 0 ? wsum[w - 1] : 0) + x - v;
-        if (i < n_tiles) row[i] = excl;
-        __syncthreads();
-        if (threadIdx.x == 0) carry_s = carry + wsum[31];
-        __syncthreads();
+        h[base + lane] = carry + x - v;
+        carry += __shfl_sync(0xffffffffu, x, 31);
     }
-    if (threadIdx.x == 0) totals[blockIdx.x] = carry_s;
 }
 
 template <bool VALS>
-__global__ void __launch_bounds__(SORT_THREADS) k_radix_scatter(
-    const uint64_t *__restrict__ keys_in, const int32_t *__restrict__ vals_in, int64_t n_cap,
-    const int64_t *n_dev, int shift, const int *__restrict__ hist, const int *__restrict__ totals,
-    int n_tiles, uint64_t *__restrict__ keys_out, int32_t *__restrict__ vals_out) {
-    __shared__ int digit_base[256];
-    __shared__ int tile_off[256];
+__global__ void __launch_bounds__(SORT_THREADS) k_onesweep(const uint64_t *__restrict__ keys_in,
+                                                           const int32_t *__restrict__ vals_in, int64_t n_cap,
+                                                           const int64_t *n_dev, int shift,
+                                                           const unsigned int *__restrict__ gbase,
+                                                           unsigned int *tile_status, unsigned int *tile_counter,
+                                                           uint64_t *__restrict__ keys_out,
+                                                           int32_t *__restrict__ vals_out) {
+    __shared__ int tile_s;
+    __shared__ unsigned int excl_s[256];
     __shared__ int local_start[256];
     __shared__ int cnt[SORT_WARPS][256];
     __shared__ int warp_sums[SORT_WARPS];
-    __shared__ uint64_t skeys[SORT_TILE];
-    __shared__ int32_t svals[VALS ? SORT_TILE : 1];
+    __shared__ uint64_t skeys[OS_TILE];
+    __shared__ int32_t svals[VALS ? OS_TILE : 1];
 
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const int tile = blockIdx.x;
     const int64_t n = dev_count(n_cap, n_dev);
-    const int64_t base = (int64_t)tile * SORT_TILE;
-    if (base >= n) return;
-    const int tile_valid = (int)imin64(SORT_TILE, n - base);
-
-    {
-        int tot;
-        int b = block_excl_scan_256(totals[tid], warp_sums, tot);
-        digit_base[tid] = b;
-        tile_off[tid] = hist[tid * n_tiles + tile];
+    if (tid == 0) tile_s = (int)atomicAdd(tile_counter, 1u);
 #pragma unroll
-        for (int ww = 0; ww < SORT_WARPS; ++ww) cnt[ww][tid] = 0;
-    }
+    for (int ww = 0; ww < SORT_WARPS; ++ww) cnt[ww][tid] = 0;
     __syncthreads();
+    const int tile = tile_s;
+    const int64_t base = (int64_t)tile * OS_TILE;
+    if (base >= n) return;
+    const int tile_valid = (int)imin64(OS_TILE, n - base);
 
-    uint64_t key[SORT_ITEMS];
-    int32_t val[SORT_ITEMS];
-    int rank[SORT_ITEMS];
-    unsigned dig[SORT_ITEMS];
+    uint64_t key[OS_ITEMS];
+    int32_t val[OS_ITEMS];
+    int rank[OS_ITEMS];
+    unsigned dig[OS_ITEMS];
 #pragma unroll
-    for (int r = 0; r < SORT_ITEMS; ++r) {
-        const int li = w * (32 * SORT_ITEMS) + r * 32 + lane;   // warp-contiguous chunk
+    for (int r = 0; r < OS_ITEMS; ++r) {
+        const int li = w * (32 * OS_ITEMS) + r * 32 + lane;   // warp-contiguous chunk: stable order
         const int64_t idx = base + li;
         const bool valid = li < tile_valid;
         key[r] = valid ? keys_in[idx] : ~0ull;
         if (VALS) val[r] = valid ? (vals_in ? vals_in[idx] : (int32_t)idx) : 0;
         dig[r] = valid ? (unsigned)((key[r] >> shift) & 255u) : 256u + lane;
-        unsigned peers = __match_any_sync(0xffffffffu, dig[r]);
-        int before = __popc(peers & lanemask_lt());
-        int c = valid ? cnt[w][dig[r]] : 0;
+        const unsigned peers = __match_any_sync(0xffffffffu, dig[r]);
+        const int before = __popc(peers & lanemask_lt());
+        const int c = valid ? cnt[w][dig[r]] : 0;
         rank[r] = c + before;
         __syncwarp();
         if (valid && before == 0) cnt[w][dig[r]] = c + __popc(peers);
         __syncwarp();
     }
     __syncthreads();
+    int tile_cnt;
     {
         int s = 0;
 #pragma unroll
         for (int ww = 0; ww < SORT_WARPS; ++ww) {
-            int c = cnt[ww][tid];
+            const int c = cnt[ww][tid];
             cnt[ww][tid] = s;
             s += c;
         }
+        tile_cnt = s;
         int tot;
         local_start[tid] = block_excl_scan_256(s, warp_sums, tot);
     }
+    // ---- decoupled look-back: thread tid owns digit tid --------------------------------
+    {
+        unsigned int *st = tile_status + (int64_t)tile * 256 + tid;
+        if (tile == 0) {
+            atomicExch(st, ST_INC | (unsigned)tile_cnt);
+            excl_s[tid] = 0;
+        } else {
+            atomicExch(st, ST_AGG | (unsigned)tile_cnt);
+            unsigned int excl = 0;
+            for (int j = tile - 1; j >= 0; --j) {
+                const volatile unsigned int *q = tile_status + (int64_t)j * 256 + tid;
+                unsigned int v;
+                do { v = *q; } while ((v & ~ST_VAL) == 0);
+                excl += v & ST_VAL;
+                if (v & ST_INC) break;
+            }
+            atomicExch(st, ST_INC | (excl + (unsigned)tile_cnt));
+            excl_s[tid] = excl;
+        }
+    }
     __syncthreads();
 #pragma unroll
-    for (int r = 0; r < SORT_ITEMS; ++r) {
+    for (int r = 0; r < OS_ITEMS; ++r) {
         if (dig[r] < 256u) {
-            int lp = local_start[dig[r]] + cnt[w][dig[r]] + rank[r];
+            const int lp = local_start[dig[r]] + cnt[w][dig[r]] + rank[r];
             skeys[lp] = key[r];
             if (VALS) svals[lp] = val[r];
         }
     }
     __syncthreads();
     for (int s = tid; s < tile_valid; s += SORT_THREADS) {
-        uint64_t k = skeys[s];
-        int d = (int)((k >> shift) & 255u);
-        int64_t g = (int64_t)digit_base[d] + tile_off[d] + (s - local_start[d]);
+        const uint64_t k = skeys[s];
+        const int d = (int)((k >> shift) & 255u);
+        const int64_t g = (int64_t)gbase[d] + excl_s[d] + (s - local_start[d]);
         keys_out[g] = k;
         if (VALS) vals_out[g] = svals[s];
     }
@@ -197,52 +199,61 @@ __global__ void k_copy_keys(const uint64_t *__restrict__ a, int64_t n_cap, const
     }
 }
 
-static int n_tiles_of(int64_t n) { return (int)((n + SORT_TILE - 1) / SORT_TILE); }
+static int os_tiles(int64_t n) { return (int)((n + OS_TILE - 1) / OS_TILE); }
 
 size_t radix_sort_workspace(int64_t n, bool with_vals) {
     Sizer s;
-    const int nt = n_tiles_of(n > 0 ? n : 1);
-    s.take<int>((size_t)nt * 256);
-    s.take<int>(256);
+    const int nt = os_tiles(n > 0 ? n : 1);
+    s.take<unsigned int>((size_t)MAX_PASSES * 256);                 // histograms / bases
+    s.take<unsigned int>((size_t)MAX_PASSES * (nt * 256 + 32));      // tile status + counters
     s.take<uint64_t>((size_t)n);
     if (with_vals) s.take<int32_t>((size_t)n);
     return s.used + 256;
 }
 
-spc_status radix_sort(const uint64_t *keys_in, const int32_t *vals_in, int64_t n, const int64_t *n_dev,
-                      int n_bits, uint64_t *keys_out, int32_t *vals_out, void *ws, size_t ws_bytes,
-                      cudaStream_t st) {
+spc_status radix_sort(const uint64_t *keys_in, const int32_t *vals_in, int64_t n, const int64_t *n_dev, int n_bits,
+                      uint64_t *keys_out, int32_t *vals_out, void *ws, size_t ws_bytes, cudaStream_t st,
+                      bool hist_done) {
     if (n <= 0) return SPC_OK;
     const bool with_vals = vals_out != nullptr;
+    const int passes = (n_bits + 7) / 8;
+    if (passes > MAX_PASSES) return fail(SPC_ERR_INVALID_ARG, "radix_sort: too many key bits");
     Bump b(ws, ws_bytes);
-    const int nt = n_tiles_of(n);
-    int *hist = b.take<int>((size_t)nt * 256);
-    int *totals = b.take<int>(256);
+    const int nt = os_tiles(n);
+    unsigned int *hist = b.take<unsigned int>((size_t)MAX_PASSES * 256);
+    const size_t stride = (size_t)nt * 256 + 32;
+    unsigned int *status = b.take<unsigned int>((size_t)MAX_PASSES * stride);
     uint64_t *ktmp = b.take<uint64_t>((size_t)n);
     int32_t *vtmp = with_vals ? b.take<int32_t>((size_t)n) : nullptr;
     if (!b.ok()) return fail(SPC_ERR_WORKSPACE, "radix_sort: workspace too small");
-    const int passes = (n_bits + 7) / 8;
     if (passes == 0) {
         k_copy_keys<<<256, 256, 0, st>>>(keys_in, n, n_dev, keys_out, vals_in, vals_out);
         SPC_LAUNCH_CHECK("k_copy_keys");
         return SPC_OK;
     }
+    SPC_CUDA(cudaMemsetAsync(status, 0, sizeof(unsigned int) * MAX_PASSES * stride, st));
+    if (!hist_done) {
+        SPC_CUDA(cudaMemsetAsync(hist, 0, sizeof(unsigned int) * MAX_PASSES * 256, st));
+        const int g = (int)std::max<int64_t>(1, std::min<int64_t>((n + 4095) / 4096, 2 * num_sms()));
+        k_hist_all<<<g, SORT_THREADS, 0, st>>>(keys_in, n, n_dev, passes, hist);
+    }
+    k_hist_scan<<<1, 32 * MAX_PASSES, 0, st>>>(hist, passes);
+    SPC_LAUNCH_CHECK("radix histograms");
     const uint64_t *src_k = keys_in;
     const int32_t *src_v = vals_in;
     for (int p = 0; p < passes; ++p) {
         const bool to_out = ((passes - 1 - p) % 2) == 0;
         uint64_t *dst_k = to_out ? keys_out : ktmp;
         int32_t *dst_v = with_vals ? (to_out ? vals_out : vtmp) : nullptr;
-        const int shift = 8 * p;
-        k_radix_hist<<<nt, SORT_THREADS, 0, st>>>(src_k, n, n_dev, shift, hist, nt);
-        k_radix_scan<<<256, 1024, 0, st>>>(hist, nt, totals);
+        unsigned int *stp = status + (size_t)p * stride;
+        unsigned int *ctr = stp + (size_t)nt * 256;
         if (with_vals)
-            k_radix_scatter<true><<<nt, SORT_THREADS, 0, st>>>(src_k, src_v, n, n_dev, shift, hist, totals, nt,
-                                                              dst_k, dst_v);
+            k_onesweep<true><<<nt, SORT_THREADS, 0, st>>>(src_k, src_v, n, n_dev, 8 * p, hist + p * 256, stp, ctr,
+                                                         dst_k, dst_v);
         else
-            k_radix_scatter<false><<<nt, SORT_THREADS, 0, st>>>(src_k, nullptr, n, n_dev, shift, hist, totals,
-                                                               nt, dst_k, nullptr);
-        SPC_LAUNCH_CHECK("radix pass");
+            k_onesweep<false><<<nt, SORT_THREADS, 0, st>>>(src_k, nullptr, n, n_dev, 8 * p, hist + p * 256, stp, ctr,
+                                                          dst_k, nullptr);
+        SPC_LAUNCH_CHECK("onesweep pass");
         src_k = dst_k;
         src_v = dst_v;
     }
@@ -256,8 +267,12 @@ struct PackDev {
     int bb, bx, by, bz;
 };
 
-__global__ void k_pack(const int4 *__restrict__ coords, int64_t n, PackDev s, uint64_t *__restrict__ keys,
-                       uint32_t *status) {
+__global__ void __launch_bounds__(256) k_pack(const int4 *__restrict__ coords, int64_t n, PackDev s,
+                                              uint64_t *__restrict__ keys, uint32_t *status, int passes,
+                                              unsigned int *__restrict__ ghist) {
+    __shared__ unsigned int h[MAX_PASSES][256];
+    for (int i = threadIdx.x; i < passes * 256; i += blockDim.x) h[i / 256][i % 256] = 0;
+    __syncthreads();
     bool bad = false;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         int4 c = coords[i];
@@ -271,8 +286,12 @@ __global__ void k_pack(const int4 *__restrict__ coords, int64_t n, PackDev s, ui
         uint64_t k = ((uint64_t)fb << (s.bx + s.by + s.bz)) | ((uint64_t)fx << (s.by + s.bz)) |
                      ((uint64_t)fy << s.bz) | (uint64_t)fz;
         keys[i] = k;
+        for (int p = 0; p < passes; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 255u], 1u);   // sort histograms
     }
     if (__any_sync(0xffffffffu, bad) && status && (threadIdx.x & 31) == 0) atomicOr(status, SPC_FLAG_RANGE);
+    __syncthreads();
+    for (int i = threadIdx.x; i < passes * 256; i += blockDim.x)
+        if (h[i / 256][i % 256]) atomicAdd(&ghist[i], h[i / 256][i % 256]);
 }
 
 __global__ void k_flag_dups(const uint64_t *__restrict__ keys, int64_t n_cap, const int64_t *n_dev,
@@ -458,11 +477,15 @@ extern "C" spc_status spc_pack_sort(const int32_t *coords, int64_t n, spc_pack_s
     void *rws = b.base + align_up(b.used, 256);
     size_t rws_bytes = ws_bytes - align_up(b.used, 256);
     PackDev pd{spec.bits_b, spec.bits_x, spec.bits_y, spec.bits_z};
-    int grid = (int)imin64((n + 255) / 256, 4 * 148);
-    k_pack<<<grid, 256, 0, st>>>(reinterpret_cast<const int4 *>(coords), n, pd, raw, status);
+    int grid = (int)imin64((n + 2047) / 2048, 2 * 148);
+    // pack + all radix histograms in one pass over the coordinates (the histogram block is
+    // the first region of the radix workspace)
+    unsigned int *hist = reinterpret_cast<unsigned int *>(rws);   // == radix_sort's first workspace block
+    SPC_CUDA(cudaMemsetAsync(hist, 0, sizeof(unsigned int) * MAX_PASSES * 256, st));
+    k_pack<<<grid, 256, 0, st>>>(reinterpret_cast<const int4 *>(coords), n, pd, raw, status, (used + 7) / 8, hist);
     SPC_LAUNCH_CHECK("k_pack");
     int32_t *perm = perm_out;
-    spc_status s = radix_sort(raw, nullptr, n, nullptr, used, keys_out, perm, rws, rws_bytes, st);
+    spc_status s = radix_sort(raw, nullptr, n, nullptr, used, keys_out, perm, rws, rws_bytes, st, true);
     if (s != SPC_OK) return s;
     if (status) {
         k_flag_dups<<<grid, 256, 0, st>>>(keys_out, n, nullptr, status, SPC_FLAG_DUPLICATE);
@@ -533,7 +556,7 @@ extern "C" spc_status spc_downsample(const uint64_t *keys, int64_t n, const int6
     k_build_tagged<<<grid, 256, 0, st>>>(keys, n, n_dev, n_levels, lm, used, tagged, scal);
     SPC_LAUNCH_CHECK("k_build_tagged");
     const int tag_bits = n_levels > 2 ? 2 : (n_levels > 1 ? 1 : 0);
-    spc_status s = radix_sort(tagged, nullptr, tot, scal, used + tag_bits, sorted, nullptr, rws, rws_bytes, st);
+    spc_status s = radix_sort(tagged, nullptr, tot, scal, used + tag_bits, sorted, nullptr, rws, rws_bytes, st, false);
     if (s != SPC_OK) return s;
     k_unique_count<<<nt, SORT_THREADS, 0, st>>>(sorted, scal, tile_cnt);
     k_unique_scan<<<1, 1024, 0, st>>>(tile_cnt, nt, sorted, scal, n, n_dev, n_levels, scal + 1, level_n_dev);
