@@ -289,9 +289,8 @@ def main():
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     t_total = float(np.sum(step_ms)) / 1e3
     if world > 1:
-        tt = torch.tensor([t_total], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        t_total = float(tt.item())
+        from paper_2511_20834_b200.distributed import max_over_ranks
+        t_total = max_over_ranks(t_total, device=dev)
     value = world * args.steps / t_total
     clocks = clk.summary()
 
