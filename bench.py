@@ -171,11 +171,11 @@ def run_reference(args):
     coords, _ = workload(0)
     import synth  # noqa: F401
     for _ in range(args.warmup):
-        oracle_scan_seconds(coords, rows_per_layer=16)
+        oracle_scan_seconds(coords, rows_per_layer=32)
     t0 = time.perf_counter()
     est = []
     for i in range(args.steps):
-        sec, sampled, nl = oracle_scan_seconds(coords, rows_per_layer=16, rng_seed=i)
+        sec, sampled, nl = oracle_scan_seconds(coords, rows_per_layer=32, rng_seed=i)
         est.append(sec)
     wall = time.perf_counter() - t0
     per_scan = float(np.mean(est))
@@ -187,7 +187,7 @@ def run_reference(args):
             "config": {"workload": "C2: MinkUNet-42 on one SemanticKITTI-shaped synthetic scan (~100k voxels, 0.05 m)",
                        "n_voxels": int(coords.shape[0]), "l2": "n/a (CPU)"},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
-                             "sample": f"per step: full sort + Eq.(1) levels + {nl} layers x 16 sampled output rows of "
+                             "sample": f"per step: full sort + Eq.(1) levels + {nl} layers x 32 sampled output rows of "
                                        f"Eq.(2) fp64 (hash-set kernel map), extrapolated linearly in rows to one scan; "
                                        f"wall {wall:.1f}s for {args.steps} steps"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

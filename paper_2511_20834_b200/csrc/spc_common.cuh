@@ -97,3 +97,11 @@ spc_status radix_sort(const uint64_t *keys_in, const int32_t *vals_in /*nullable
                       const int64_t *n_dev, int n_bits, uint64_t *keys_out, int32_t *vals_out /*nullable*/,
                       void *ws, size_t ws_bytes, cudaStream_t st, bool hist_done);
 }  // namespace spc
+
+namespace spc {
+// network-wide phase 2: spc_build_kmap calls between begin/end are collected and built by
+// one grouped launch (spc_kmap.cu)
+void kmap_defer_begin();
+void kmap_defer_abort();
+spc_status kmap_defer_end(cudaStream_t st);
+}  // namespace spc

@@ -56,6 +56,8 @@ struct ConvParams {
     int64_t ld_in_bytes;
     const char *wblob;
     int n_chunks, n_ntiles, BK, BN;
+    int nkb;              // K-blocks (of BK channels) per pipeline stage; n_chunks % nkb == 0
+    uint32_t kb_a, kb_b;  // bytes of one A / B K-block in a stage
     uint32_t a_bytes, b_bytes;
     int stages;
     int bm;               // rows per tile: 128 or 256 (two M=128 MMAs sharing the weight tile)
@@ -378,17 +380,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                     gp[b] = p.f_in + (ok[b] ? (int64_t)g * p.ld_in_bytes + q_lane * 16 : 0);
                     so[b] = (uint32_t)r * rb + ((q_lane ^ f) * 16);
                 }
-                for (int cc = 0; cc < p.n_chunks; ++cc) {
+                for (int cc = 0; cc < p.n_chunks; cc += p.nkb) {
                     if (threadIdx.x == 0) TR(4, ptr_ctr);
                     ptx::mbar_wait(ptx::smem_u32(&cs.empty[s]), ph ^ 1);
                     if (threadIdx.x == 0) TR(1, ptr_ctr);
                     const uint32_t abase = ptx::smem_u32(sa + (size_t)s * p.a_bytes);
+                    for (int kb = 0; kb < p.nkb; ++kb) {
+                        const uint32_t kbo = kb * p.kb_a;
 #pragma unroll
-                    for (int b = 0; b < NB; ++b) {
-                        // matched rows: one whole-line request per row; sentinel rows (no
-                        // input voxel) never touch L2: zero them with a shared store
-                        if (ok[b]) ptx::cp_async_16(abase + so[b], gp[b], 16u);
-                        else asm volatile("st.shared.v4.b32 [%0], {%1,%1,%1,%1};" ::"r"(abase + so[b]), "r"(0) : "memory");
+                        for (int b = 0; b < NB; ++b) {
+                            // matched rows: one whole-line request per row; sentinel rows (no
+                            // input voxel) never touch L2: zero them with a shared store
+                            if (ok[b]) ptx::cp_async_16(abase + kbo + so[b], gp[b] + kb * rb, 16u);
+                            else asm volatile("st.shared.v4.b32 [%0], {%1,%1,%1,%1};" ::"r"(abase + kbo + so[b]), "r"(0)
+                                              : "memory");
+                        }
                     }
                     ptx::cp_async_mbar_arrive(ptx::smem_u32(&cs.full[s]));
                     if (threadIdx.x == 0) TR(5, ptr_ctr);
@@ -396,7 +402,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                     ++ptr_ctr;
 #endif
 #pragma unroll
-                    for (int b = 0; b < NB; ++b) gp[b] += ok[b] ? rb : 0;
+                    for (int b = 0; b < NB; ++b) gp[b] += ok[b] ? rb * p.nkb : 0;
                     if (++s == S) { s = 0; ph ^= 1; }
                 }
             }
@@ -420,17 +426,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                 const int nt = R.nt, kfix = R.k;
                 for (int c = next_bit(mask, 0); c >= 0; c = next_bit(mask, c + 1)) {
                     const int k = p.mode == 0 ? p.dense_k[c] : kfix;
-                    for (int cc = 0; cc < p.n_chunks; ++cc, ++it) {
+                    for (int cc = 0; cc < p.n_chunks; cc += p.nkb, ++it) {
                         const int s = it % S;
                         ptx::mbar_wait(ptx::smem_u32(&cs.empty[s]), ((it / S) & 1) ^ 1);
                         const uint32_t fb = ptx::smem_u32(&cs.full[s]);
-#ifdef SPC_EXP_NO_B
-                        if (it >= (uint32_t)S) { ptx::mbar_arrive(fb); continue; }
-#endif
+                        // nkb consecutive chunk blobs are contiguous: one bulk copy per stage
                         ptx::mbar_arrive_expect_tx(fb, p.b_bytes);
                         const int64_t blob = ((int64_t)k * p.n_ntiles + nt) * p.n_chunks + cc;
-                        ptx::bulk_g2s(ptx::smem_u32(sb + (size_t)s * p.b_bytes), p.wblob + blob * p.b_bytes, p.b_bytes,
-                                      fb);
+                        ptx::bulk_g2s(ptx::smem_u32(sb + (size_t)s * p.b_bytes), p.wblob + blob * p.kb_b, p.b_bytes, fb);
                     }
                 }
                 ptx::mbar_arrive(ptx::smem_u32(&cs.trec_empty[st]));
@@ -453,7 +456,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                 const uint32_t d_tmem = tmem_base + a * NH * p.tmem_cols;
                 uint32_t acc = 0;
                 for (int c = next_bit(mask, 0); c >= 0; c = next_bit(mask, c + 1)) {
-                    for (int cc = 0; cc < p.n_chunks; ++cc, ++it) {
+                    for (int cc = 0; cc < p.n_chunks; cc += p.nkb, ++it) {
                         const int s = it % S;
                         ptx::mbar_wait(ptx::smem_u32(&cs.full[s]), (it / S) & 1);
                         TR(2, it);
@@ -465,15 +468,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                         ptx::tc_fence_after();
                         const uint32_t a_base = ptx::smem_u32(sa + (size_t)s * p.a_bytes);
                         const uint32_t b_base = ptx::smem_u32(sb + (size_t)s * p.b_bytes);
+                        for (int kb = 0; kb < p.nkb; ++kb) {
 #pragma unroll
-                        for (int kk = 0; kk < BK / 16; ++kk) {
-                            const uint64_t bd = ptx::umma_desc_kmajor_sw(b_base + kk * 32, rb);
+                            for (int kk = 0; kk < BK / 16; ++kk) {
+                                const uint64_t bd = ptx::umma_desc_kmajor_sw(b_base + kb * p.kb_b + kk * 32, rb);
 #pragma unroll
-                            for (int h = 0; h < NH; ++h) {
-                                const uint64_t ad = ptx::umma_desc_kmajor_sw(a_base + h * TC_BM * rb + kk * 32, rb);
-                                ptx::mma_f16_ss(d_tmem + h * p.tmem_cols, ad, bd, p.idesc, acc);
+                                for (int h = 0; h < NH; ++h) {
+                                    const uint64_t ad =
+                                        ptx::umma_desc_kmajor_sw(a_base + kb * p.kb_a + h * TC_BM * rb + kk * 32, rb);
+                                    ptx::mma_f16_ss(d_tmem + h * p.tmem_cols, ad, bd, p.idesc, acc);
+                                }
+                                acc = 1;
                             }
-                            acc = 1;
                         }
                         ptx::mma_commit(ptx::smem_u32(&cs.empty[s]));
                         TR(3, it);
@@ -965,8 +971,17 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
     // 256-row tiles (two MMAs per weight tile) whenever four accumulators fit TMEM
     p.bm = (4 * p.tmem_cols <= 512 && !getenv("SPC_BM128")) ? 256 : 128;
     if (has_os && (size_t)BLK_SLOTS * p.bm * km->k_dense * 4 > 96 * 1024) p.bm = 128;   // OS index blocks (K=5)
-    p.a_bytes = (uint32_t)(p.bm * p.BK * 2);
-    p.b_bytes = (uint32_t)(p.BN * p.BK * 2);
+    p.kb_a = (uint32_t)(p.bm * p.BK * 2);
+    p.kb_b = (uint32_t)(p.BN * p.BK * 2);
+    // several K-blocks per stage: whole input rows per stage when they fit (fewer steps; the
+    // per-stage cost is mostly fixed), keeping >= 3 stages in shared memory
+    p.nkb = 1;
+    static const size_t stage_cap = getenv("SPC_STAGE_KB") ? (size_t)atoi(getenv("SPC_STAGE_KB")) * 1024 : 72 * 1024;
+    for (int d = p.n_chunks; d >= 1; --d)
+        if (p.n_chunks % d == 0 && (size_t)d * (p.kb_a + p.kb_b) <= stage_cap) { p.nkb = d; break; }
+    if (getenv("SPC_NKB1")) p.nkb = 1;
+    p.a_bytes = p.nkb * p.kb_a;
+    p.b_bytes = p.nkb * p.kb_b;
     p.idesc = ptx::umma_idesc_f16(in_dtype == SPC_BF16, TC_BM, p.BN);
     p.wblob = static_cast<const char *>(weight);
     if (has_os) {

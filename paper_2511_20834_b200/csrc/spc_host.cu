@@ -186,7 +186,8 @@ extern "C" spc_status spc_network_kmaps(const uint64_t *v0_keys, int64_t n0, con
                                       base, ds_bytes, stream);
         if (s != SPC_OK) return s;
     }
-    // ---- phase 2: every distinct map -------------------------------------------------
+    // ---- phase 2: every distinct map, one grouped launch ---------------------------------
+    kmap_defer_begin();
     for (int i = 0; i < n_maps; ++i) {
         const uint32_t fi = flags ? flags[i] : 0;
         int dup = -1;
@@ -198,13 +199,19 @@ extern "C" spc_status spc_network_kmaps(const uint64_t *v0_keys, int64_t n0, con
         }
         int li, lo;
         spc_status s = map_levels(geoms[i], n_levels, li, lo);
-        if (s != SPC_OK) return s;
+        if (s != SPC_OK) {
+            kmap_defer_abort();
+            return s;
+        }
         const size_t bytes = spc_kmap_bytes(geoms[i], ts[i], fi, n0, n0);
         s = spc_build_kmap(level_keys + (size_t)li * n0, n0, level_n_dev + li, level_keys + (size_t)lo * n0, n0,
                            level_n_dev + lo, spec, geoms[i], ts[i], fi, base + off, bytes, status, &maps_out[i],
                            stream);
-        if (s != SPC_OK) return s;
+        if (s != SPC_OK) {
+            kmap_defer_abort();   // leaves no half-open batch behind
+            return s;
+        }
         off += align_up(bytes, 256);
     }
-    return SPC_OK;
+    return kmap_defer_end(st);
 }

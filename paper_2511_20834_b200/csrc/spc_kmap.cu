@@ -25,12 +25,15 @@ constexpr int KM_BM = 128;          // outputs per tile
 constexpr int KM_THREADS = 256;
 constexpr int KM_WIN_CAP = 4096;    // staged window keys per tile (32 KB)
 
-struct KmapParams {
+// Compact per-map descriptor; the offset tables (packed query deltas, weight slots,
+// dense columns, WS lists) are rebuilt in shared memory from it, so one launch can build
+// every map of a network (phase 2 of network-wide indexing) with the descriptors
+// passed as kernel parameters.
+struct KmapDesc {
     const uint64_t *in;
-    int64_t n_in_cap;
-    const int64_t *n_in_dev;
     const uint64_t *out;
-    int64_t n_out_cap;
+    int64_t n_in_cap, n_out_cap;
+    const int64_t *n_in_dev;
     const int64_t *n_out_dev;
     int32_t *os;
     int2 *pairs;
@@ -38,12 +41,18 @@ struct KmapParams {
     uint32_t *tile_mask;
     unsigned long long *stats;
     int64_t list_stride;
-    int K, n_groups, k_dense, tile_words;
-    int64_t delta[SPC_MAX_KVOL];      // [g*K + m]: packed query delta, ascending in m
-    int16_t kslot[SPC_MAX_KVOL];      // [g*K + m] -> weight offset index k
-    int16_t dense_col[SPC_MAX_KVOL];  // [k] -> OS column or -1
-    int16_t list_id[SPC_MAX_KVOL];    // [k] -> WS list or -1
-    uint8_t group_needed[25];
+    int32_t spacing;
+    int16_t K, k_dense, tile_words, t_eff;
+    int8_t transposed, halved;
+};
+
+constexpr int KM_MAX_MAPS = 24;
+
+struct KmapBatch {
+    int n_maps;
+    int bits_y, bits_z;
+    unsigned int *work_ctr;   // zeroed before the launch
+    KmapDesc d[KM_MAX_MAPS];
 };
 
 __device__ __forceinline__ int64_t lower_bound_g(const uint64_t *__restrict__ a, int64_t n, uint64_t q) {
@@ -74,129 +83,207 @@ __device__ __forceinline__ int lower_bound_s(const uint64_t *a, int n, uint64_t 
     return lo;
 }
 
-__global__ void __launch_bounds__(KM_THREADS) k_kmap_zdelta(const __grid_constant__ KmapParams p) {
+// zero the per-map counters / stats and the work counter
+__global__ void k_kmap_prep(const __grid_constant__ KmapBatch b) {
+    const int m = blockIdx.x;
+    if (m == 0 && threadIdx.x == 0) *b.work_ctr = 0;
+    if (m >= b.n_maps) return;
+    for (int i = threadIdx.x; i < 2 * SPC_MAX_KVOL; i += blockDim.x) b.d[m].counts[i] = 0;
+    if (b.d[m].stats && threadIdx.x < 2) b.d[m].stats[threadIdx.x] = 0;
+}
+
+__global__ void __launch_bounds__(KM_THREADS) k_kmap_zdelta(const __grid_constant__ KmapBatch B) {
     extern __shared__ __align__(16) unsigned char km_smem[];
     __shared__ int64_t win_lo[25];
     __shared__ int win_len[25];
-    __shared__ int win_base[25];   // -1: window not staged, use global search
-    __shared__ uint32_t smask[4];  // tile bit mask over dense columns (<= 125)
-
-    const int64_t n_out = dev_count(p.n_out_cap, p.n_out_dev);
-    const int64_t n_in = dev_count(p.n_in_cap, p.n_in_dev);
-    const int64_t row0 = (int64_t)blockIdx.x * KM_BM;
-    if (row0 >= n_out) return;
-    const int rows = (int)imin64(KM_BM, n_out - row0);
-    const int K = p.K, G = p.n_groups, KD = p.k_dense;
-    int32_t *os_tile = reinterpret_cast<int32_t *>(km_smem);
-    uint64_t *win = reinterpret_cast<uint64_t *>(km_smem + KM_BM * KD * 4);   // KM_BM*4 = 512 B multiple
+    __shared__ int win_base[25];    // -1: window not staged, use global search
+    __shared__ uint32_t smask[4];   // tile bit mask over dense columns (<= 125)
+    __shared__ int64_t s_delta[SPC_MAX_KVOL];
+    __shared__ int16_t s_kslot[SPC_MAX_KVOL], s_dcol[SPC_MAX_KVOL], s_list[SPC_MAX_KVOL];
+    __shared__ uint8_t s_need[25];
+    __shared__ int s_prefix[KM_MAX_MAPS + 1];
+    __shared__ int s_work, s_cur_map;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid < 4) smask[tid] = 0;
-
-    // ---- phase A: window bounds of every (tile, group) ------------------------------
-    const uint64_t q_first = p.out[row0];
-    const uint64_t q_last = p.out[row0 + rows - 1];
-    if (tid < 2 * G) {
-        const int g = tid >> 1;
-        if (p.group_needed[g]) {
-            uint64_t q = (tid & 1) ? q_last + (uint64_t)p.delta[g * K + K - 1] + 1ull
-                                   : q_first + (uint64_t)p.delta[g * K];
-            int64_t b = lower_bound_g(p.in, n_in, q);
-            if (tid & 1) win_len[g] = (int)imin64(b, INT32_MAX);   // hi for now
-            else win_lo[g] = b;
-        }
-    }
-    __syncthreads();
     if (tid == 0) {
-        int base = 0;
-        for (int g = 0; g < G; ++g) {
-            if (!p.group_needed[g]) { win_base[g] = -1; win_len[g] = 0; continue; }
-            int64_t len = (int64_t)win_len[g] - win_lo[g];
-            if (len < 0) len = 0;
-            win_len[g] = (int)len;
-            if (base + len <= KM_WIN_CAP) { win_base[g] = base; base += (int)len; }
-            else win_base[g] = -1;
+        int acc = 0;
+        for (int m = 0; m < B.n_maps; ++m) {
+            s_prefix[m] = acc;
+            const int64_t n_out = dev_count(B.d[m].n_out_cap, B.d[m].n_out_dev);
+            acc += (int)((n_out + KM_BM - 1) / KM_BM);
         }
+        s_prefix[B.n_maps] = acc;
+        s_cur_map = -1;
     }
     __syncthreads();
-    // ---- phase A': stage windows (one warp per group, coalesced) ---------------------
-    for (int g = warp; g < G; g += KM_THREADS / 32) {
-        if (win_base[g] < 0) continue;
-        const uint64_t *src = p.in + win_lo[g];
-        uint64_t *dst = win + win_base[g];
-        for (int e = lane; e < win_len[g]; e += 32) dst[e] = __ldg(src + e);
-    }
-    __syncthreads();
+    const int total = s_prefix[B.n_maps];
 
-    // ---- phase B: z-delta search per (output, group) ---------------------------------
-    unsigned long long n_search = 0, n_probe = 0;
-    const int chunks = KM_BM / 32;
-    for (int item = warp; item < G * chunks; item += KM_THREADS / 32) {
-        const int g = item / chunks, ch = item - g * chunks;
-        if (!p.group_needed[g]) continue;
-        const int lr = ch * 32 + lane;               // local row
-        const bool valid = lr < rows;
-        const int64_t i = row0 + lr;
-        const uint64_t q = valid ? p.out[i] : 0;
-        const bool staged = win_base[g] >= 0;
-        const uint64_t *wk = staged ? win + win_base[g] : p.in + win_lo[g];
-        const int wl = win_len[g];
-        int pos = 0;
-        if (valid) {
-            pos = lower_bound_s(wk, wl, q + (uint64_t)p.delta[g * K]);
-            ++n_search;
-        }
-        for (int m = 0; m < K; ++m) {
-            const uint64_t query = q + (uint64_t)p.delta[g * K + m];
-            bool match = false;
-            if (valid) {
-                while (pos < wl && wk[pos] < query) { ++pos; ++n_probe; }
-                match = pos < wl && wk[pos] == query;
+    for (;;) {
+        if (tid == 0) s_work = (int)atomicAdd(B.work_ctr, 1u);
+        __syncthreads();
+        const int v = s_work;
+        if (v >= total) break;
+        int m = 0;
+        while (s_prefix[m + 1] <= v) ++m;
+        const KmapDesc &p = B.d[m];
+        const int tile = v - s_prefix[m];
+        const int K = p.K, G = K * K, KD = p.k_dense, r = (K - 1) / 2, kv = K * K * K;
+        // ---- per-map tables (rebuilt only when the map changes) -------------------------
+        if (s_cur_map != m) {
+            if (tid < kv) {
+                const int g = tid / K, mm = tid % K;
+                const int ex = g / K - r, ey = g % K - r;
+                const int ez = p.transposed ? r - mm : mm - r;   // ascending query order
+                const int k = ((ex + r) * K + (ey + r)) * K + (ez + r);
+                int64_t d = (int64_t)ex * p.spacing * (1ll << (B.bits_y + B.bits_z)) +
+                            (int64_t)ey * p.spacing * (1ll << B.bits_z) + (int64_t)ez * p.spacing;
+                s_delta[tid] = p.transposed ? -d : d;
+                s_kslot[tid] = (int16_t)k;
+                // per weight offset k == tid: dense column / WS list (same rule as make_plan)
+                const int kx = tid / (K * K) - r, ky = (tid / K) % K - r, kz = tid % K - r;
+                const int centre = (kv - 1) / 2;
+                int dcol = -1, lst = -1, nd = 0, nl = 0;
+                for (int k2 = 0; k2 <= tid; ++k2) {
+                    const int l1 = abs(k2 / (K * K) - r) + abs((k2 / K) % K - r) + abs(k2 % K - r);
+                    const bool dense = l1 < p.t_eff;
+                    const bool stored = !dense && (!p.halved || k2 <= centre);
+                    if (k2 == tid) {
+                        dcol = dense ? nd : -1;
+                        lst = stored ? nl : -1;
+                    }
+                    nd += dense;
+                    nl += stored;
+                }
+                (void)kx; (void)ky; (void)kz;
+                s_dcol[tid] = (int16_t)dcol;
+                s_list[tid] = (int16_t)lst;
             }
-            const int k = p.kslot[g * K + m];
-            const int32_t j = match ? (int32_t)(win_lo[g] + pos) : -1;
-            const unsigned bal = __ballot_sync(0xffffffffu, match);
-            if (lane == 0 && bal) atomicAdd(&p.counts[k], __popc(bal));
-            const int col = p.dense_col[k];
-            if (col >= 0) {
-                if (valid) os_tile[lr * KD + col] = j;
-                if (lane == 0 && bal) atomicOr(&smask[col >> 5], 1u << (col & 31));
-            } else {
-                const int l = p.list_id[k];
-                if (l >= 0 && bal) {
-                    int base = 0;
-                    if (lane == 0) base = atomicAdd(&p.counts[SPC_MAX_KVOL + l], __popc(bal));
-                    base = __shfl_sync(0xffffffffu, base, 0);
-                    if (match) {
-                        int2 pr = make_int2(j, (int32_t)i);
-                        p.pairs[(int64_t)l * p.list_stride + base + __popc(bal & lanemask_lt())] = pr;
+            __syncthreads();
+            if (tid < G) {
+                bool need = false;
+                for (int mm = 0; mm < K; ++mm) {
+                    const int k = s_kslot[tid * K + mm];
+                    need |= s_dcol[k] >= 0 || s_list[k] >= 0;
+                }
+                s_need[tid] = need;
+            }
+            if (tid == 0) s_cur_map = m;
+        }
+        if (tid < 4) smask[tid] = 0;
+        __syncthreads();
+
+        const int64_t n_out = dev_count(p.n_out_cap, p.n_out_dev);
+        const int64_t n_in = dev_count(p.n_in_cap, p.n_in_dev);
+        const int64_t row0 = (int64_t)tile * KM_BM;
+        const int rows = (int)imin64(KM_BM, n_out - row0);
+        int32_t *os_tile = reinterpret_cast<int32_t *>(km_smem);
+        uint64_t *win = reinterpret_cast<uint64_t *>(km_smem + KM_BM * KD * 4);   // KM_BM*4 = 512 B multiple
+
+        // ---- phase A: window bounds of every (tile, group) ----------------------------
+        const uint64_t q_first = p.out[row0];
+        const uint64_t q_last = p.out[row0 + rows - 1];
+        if (tid < 2 * G) {
+            const int g = tid >> 1;
+            if (s_need[g]) {
+                const uint64_t q = (tid & 1) ? q_last + (uint64_t)s_delta[g * K + K - 1] + 1ull
+                                             : q_first + (uint64_t)s_delta[g * K];
+                const int64_t b = lower_bound_g(p.in, n_in, q);
+                if (tid & 1) win_len[g] = (int)imin64(b, INT32_MAX);   // hi for now
+                else win_lo[g] = b;
+            }
+        }
+        __syncthreads();
+        if (tid == 0) {
+            int base = 0;
+            for (int g = 0; g < G; ++g) {
+                if (!s_need[g]) { win_base[g] = -1; win_len[g] = 0; continue; }
+                int64_t len = (int64_t)win_len[g] - win_lo[g];
+                if (len < 0) len = 0;
+                win_len[g] = (int)len;
+                if (base + len <= KM_WIN_CAP) { win_base[g] = base; base += (int)len; }
+                else win_base[g] = -1;
+            }
+        }
+        __syncthreads();
+        // ---- phase A': stage windows (one warp per group, coalesced) -----------------------
+        for (int g = warp; g < G; g += KM_THREADS / 32) {
+            if (win_base[g] < 0) continue;
+            const uint64_t *src = p.in + win_lo[g];
+            uint64_t *dst = win + win_base[g];
+            for (int e = lane; e < win_len[g]; e += 32) dst[e] = __ldg(src + e);
+        }
+        __syncthreads();
+
+        // ---- phase B: z-delta search per (output, group) ---------------------------------
+        unsigned long long n_search = 0, n_probe = 0;
+        const int chunks = KM_BM / 32;
+        for (int item = warp; item < G * chunks; item += KM_THREADS / 32) {
+            const int g = item / chunks, ch = item - g * chunks;
+            if (!s_need[g]) continue;
+            const int lr = ch * 32 + lane;               // local row
+            const bool valid = lr < rows;
+            const int64_t i = row0 + lr;
+            const uint64_t q = valid ? p.out[i] : 0;
+            const bool staged = win_base[g] >= 0;
+            const uint64_t *wk = staged ? win + win_base[g] : p.in + win_lo[g];
+            const int wl = win_len[g];
+            int pos = 0;
+            if (valid) {
+                pos = lower_bound_s(wk, wl, q + (uint64_t)s_delta[g * K]);
+                ++n_search;
+            }
+            for (int mm = 0; mm < K; ++mm) {
+                const uint64_t query = q + (uint64_t)s_delta[g * K + mm];
+                bool match = false;
+                if (valid) {
+                    while (pos < wl && wk[pos] < query) { ++pos; ++n_probe; }
+                    match = pos < wl && wk[pos] == query;
+                }
+                const int k = s_kslot[g * K + mm];
+                const int32_t j = match ? (int32_t)(win_lo[g] + pos) : -1;
+                const unsigned bal = __ballot_sync(0xffffffffu, match);
+                if (lane == 0 && bal) atomicAdd(&p.counts[k], __popc(bal));
+                const int col = s_dcol[k];
+                if (col >= 0) {
+                    if (valid) os_tile[lr * KD + col] = j;
+                    if (lane == 0 && bal) atomicOr(&smask[col >> 5], 1u << (col & 31));
+                } else {
+                    const int l = s_list[k];
+                    if (l >= 0 && bal) {
+                        int base = 0;
+                        if (lane == 0) base = atomicAdd(&p.counts[SPC_MAX_KVOL + l], __popc(bal));
+                        base = __shfl_sync(0xffffffffu, base, 0);
+                        if (match) {
+                            int2 pr = make_int2(j, (int32_t)i);
+                            p.pairs[(int64_t)l * p.list_stride + base + __popc(bal & lanemask_lt())] = pr;
+                        }
                     }
                 }
             }
         }
-    }
-    if (p.stats) {
-        for (int o = 16; o > 0; o >>= 1) {
-            n_search += __shfl_xor_sync(0xffffffffu, n_search, o);
-            n_probe += __shfl_xor_sync(0xffffffffu, n_probe, o);
+        if (p.stats) {
+            for (int o = 16; o > 0; o >>= 1) {
+                n_search += __shfl_xor_sync(0xffffffffu, n_search, o);
+                n_probe += __shfl_xor_sync(0xffffffffu, n_probe, o);
+            }
+            if (lane == 0) {
+                atomicAdd(&p.stats[0], n_search);
+                atomicAdd(&p.stats[1], n_probe);
+            }
         }
-        if (lane == 0) {
-            atomicAdd(&p.stats[0], n_search);
-            atomicAdd(&p.stats[1], n_probe);
+        __syncthreads();
+        // ---- phase C: flush the OS block (contiguous rows*KD int32) -----------------------
+        if (KD > 0) {
+            int32_t *dst = p.os + row0 * KD;
+            const int totalv = rows * KD;
+            const int nvec = totalv / 4;   // row0*KD*4 is 16-byte aligned (KM_BM = 128)
+            int4 *d4 = reinterpret_cast<int4 *>(dst);
+            const int4 *s4 = reinterpret_cast<const int4 *>(os_tile);
+            for (int e = tid; e < nvec; e += KM_THREADS) d4[e] = s4[e];
+            for (int e = nvec * 4 + tid; e < totalv; e += KM_THREADS) dst[e] = os_tile[e];
+            if (tid < p.tile_words) p.tile_mask[(int64_t)tile * p.tile_words + tid] = smask[tid];
         }
-    }
-    __syncthreads();
-    // ---- phase C: flush the OS block (contiguous rows*KD int32) -----------------------
-    if (KD > 0) {
-        int32_t *dst = p.os + row0 * KD;
-        const int total = rows * KD;
-        // row0*KD*4 is 16-byte aligned when KD % 4 == 0 or row0 % 4 == 0 (KM_BM = 128)
-        const int nvec = total / 4;
-        int4 *d4 = reinterpret_cast<int4 *>(dst);
-        const int4 *s4 = reinterpret_cast<const int4 *>(os_tile);
-        for (int e = tid; e < nvec; e += KM_THREADS) d4[e] = s4[e];
-        for (int e = nvec * 4 + tid; e < total; e += KM_THREADS) dst[e] = os_tile[e];
-        if (tid < p.tile_words) p.tile_mask[blockIdx.x * (int64_t)p.tile_words + tid] = smask[tid];
+        __syncthreads();
     }
 }
 
@@ -270,12 +357,62 @@ static KmapLayout layout_of(const KmapPlan &pl, int64_t n_out) {
     L.pairs = take(sizeof(int2) * (size_t)n_out * pl.n_lists);
     L.counts = take(sizeof(int32_t) * 2 * SPC_MAX_KVOL);
     L.mask = take(sizeof(uint32_t) * (size_t)(L.tiles * L.words));
-    L.stats = take(sizeof(unsigned long long) * 2);
+    L.stats = take(sizeof(unsigned long long) * 2 + 64);   // + a launch work counter
     L.total = align_up(off, 256);
     return L;
 }
 
 size_t kmap_smem_bytes(int k_dense) { return (size_t)KM_BM * k_dense * 4 + (size_t)KM_WIN_CAP * 8; }
+
+struct DeferState {
+    bool active = false;
+    KmapBatch b;
+    int max_kd = 0;
+    int64_t tiles = 0;
+};
+static thread_local DeferState g_defer;
+
+static void fill_desc(KmapDesc &d, const spc_kmap &km, const KmapPlan &pl) {
+    memset(&d, 0, sizeof(d));
+    d.in = km.in_keys;
+    d.out = km.out_keys;
+    d.n_in_cap = km.n_in;
+    d.n_out_cap = km.n_out;
+    d.n_in_dev = km.n_in_dev;
+    d.n_out_dev = km.n_out_dev;
+    d.os = km.os_table;
+    d.pairs = reinterpret_cast<int2 *>(km.ws_pairs);
+    d.counts = km.counts_dev;
+    d.tile_mask = km.tile_mask_dev;
+    d.stats = km.search_stats_dev;
+    d.list_stride = km.n_out;
+    d.spacing = pl.spacing;
+    d.K = (int16_t)pl.K;
+    d.k_dense = (int16_t)pl.k_dense;
+    d.tile_words = (int16_t)km.tile_words;
+    d.t_eff = (int16_t)pl.t_eff;
+    d.transposed = (int8_t)km.geom.transposed;
+    d.halved = (int8_t)pl.halved;
+}
+
+static spc_status launch_kmaps(const KmapBatch &b, int max_k_dense, int64_t max_tiles, cudaStream_t st) {
+    static int configured = 0;
+    if (!configured) {
+        SPC_CUDA(cudaFuncSetAttribute(k_kmap_zdelta, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)kmap_smem_bytes(SPC_MAX_KVOL)));
+        configured = 1;
+    }
+    k_kmap_prep<<<b.n_maps > 0 ? b.n_maps : 1, 256, 0, st>>>(b);
+    SPC_LAUNCH_CHECK("k_kmap_prep");
+    const size_t smem = kmap_smem_bytes(max_k_dense);
+    int per_sm = (int)((228 * 1024) / (smem + 4096));
+    if (per_sm < 1) per_sm = 1;
+    if (per_sm > 8) per_sm = 8;
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(max_tiles, (int64_t)num_sms() * per_sm));
+    k_kmap_zdelta<<<(unsigned)grid, KM_THREADS, smem, st>>>(b);
+    SPC_LAUNCH_CHECK("k_kmap_zdelta");
+    return SPC_OK;
+}
 
 }  // namespace spc
 
@@ -342,59 +479,55 @@ extern "C" spc_status spc_build_kmap(const uint64_t *in_keys, int64_t n_in, cons
         km.list_k[l] = pl.list_k[l];
         km.list_mirror[l] = pl.list_mirror[l];
     }
-    SPC_CUDA(cudaMemsetAsync(base + L.counts, 0, L.stats + 2 * sizeof(unsigned long long) - L.counts, st));
-    if (n_out == 0) return SPC_OK;
+    if (n_out == 0) {
+        SPC_CUDA(cudaMemsetAsync(base + L.counts, 0, L.stats + 2 * sizeof(unsigned long long) - L.counts, st));
+        return SPC_OK;
+    }
     if ((flags & SPC_KMAP_CHECK_SORTED) && status) {
         k_flag_dups<<<64, 256, 0, st>>>(in_keys, n_in, n_in_dev, status, SPC_FLAG_UNSORTED);
         k_flag_dups<<<64, 256, 0, st>>>(out_keys, n_out, n_out_dev, status, SPC_FLAG_UNSORTED);
     }
 
-    KmapParams p;
-    memset(&p, 0, sizeof(p));
-    p.in = in_keys;
-    p.n_in_cap = n_in;
-    p.n_in_dev = n_in_dev;
-    p.out = out_keys;
-    p.n_out_cap = n_out;
-    p.n_out_dev = n_out_dev;
-    p.os = km.os_table;
-    p.pairs = reinterpret_cast<int2 *>(km.ws_pairs);
-    p.counts = km.counts_dev;
-    p.tile_mask = km.tile_mask_dev;
-    p.stats = km.search_stats_dev;
-    p.list_stride = n_out;
-    p.K = pl.K;
-    p.n_groups = pl.K * pl.K;
-    p.k_dense = pl.k_dense;
-    p.tile_words = L.words;
-    const int sp = pl.spacing;
-    for (int gi = 0; gi < pl.K * pl.K; ++gi) {
-        const int ex = gi / pl.K - pl.r, ey = gi % pl.K - pl.r;
-        for (int m = 0; m < pl.K; ++m) {
-            // members in ascending QUERY order: +delta (ez ascending) or -delta (ez descending)
-            const int ez = geom.transposed ? pl.r - m : m - pl.r;
-            const int k = ((ex + pl.r) * pl.K + (ey + pl.r)) * pl.K + (ez + pl.r);
-            int64_t d = spc_pack_offset(spec, ex * sp, ey * sp, ez * sp);
-            p.delta[gi * pl.K + m] = geom.transposed ? -d : d;
-            p.kslot[gi * pl.K + m] = (int16_t)k;
+    if (g_defer.active) {
+        // network-wide phase 2: collect, launch once in kmap_defer_end()
+        KmapBatch &b = g_defer.b;
+        if (b.n_maps >= KM_MAX_MAPS) return fail(SPC_ERR_CAPACITY, "too many distinct kernel maps in one batch");
+        if (b.n_maps == 0) {
+            b.bits_y = spec.bits_y;
+            b.bits_z = spec.bits_z;
+            b.work_ctr = reinterpret_cast<unsigned int *>(base + L.stats) + 4;
+        } else if (b.bits_y != spec.bits_y || b.bits_z != spec.bits_z) {
+            return fail(SPC_ERR_INVALID_ARG, "batched kernel maps must share one pack spec");
         }
-        p.group_needed[gi] = pl.group_needed[gi];
+        fill_desc(b.d[b.n_maps++], km, pl);
+        g_defer.max_kd = std::max(g_defer.max_kd, pl.k_dense);
+        g_defer.tiles += (int64_t)L.tiles;
+        return SPC_OK;
     }
-    for (int k = 0; k < pl.k_vol; ++k) {
-        p.dense_col[k] = pl.dense_col[k];
-        p.list_id[k] = pl.list_id[k];
-    }
-    const size_t smem = kmap_smem_bytes(pl.k_dense);
-    static int configured = 0;
-    if (!configured) {
-        SPC_CUDA(cudaFuncSetAttribute(k_kmap_zdelta, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)kmap_smem_bytes(SPC_MAX_KVOL)));
-        configured = 1;
-    }
-    k_kmap_zdelta<<<(unsigned)L.tiles, KM_THREADS, smem, st>>>(p);
-    SPC_LAUNCH_CHECK("k_kmap_zdelta");
-    return SPC_OK;
+    KmapBatch b;
+    memset(&b, 0, sizeof(b));
+    b.n_maps = 1;
+    b.bits_y = spec.bits_y;
+    b.bits_z = spec.bits_z;
+    b.work_ctr = reinterpret_cast<unsigned int *>(base + L.stats) + 4;   // scratch after the stats
+    fill_desc(b.d[0], km, pl);
+    return launch_kmaps(b, pl.k_dense, (int64_t)L.tiles, st);
 }
+
+namespace spc {
+void kmap_defer_begin() {
+    memset(&g_defer.b, 0, sizeof(g_defer.b));
+    g_defer.max_kd = 0;
+    g_defer.tiles = 0;
+    g_defer.active = true;
+}
+void kmap_defer_abort() { g_defer.active = false; }
+spc_status kmap_defer_end(cudaStream_t st) {
+    g_defer.active = false;
+    if (g_defer.b.n_maps == 0) return SPC_OK;
+    return launch_kmaps(g_defer.b, g_defer.max_kd, g_defer.tiles, st);
+}
+}  // namespace spc
 
 extern "C" spc_status spc_kmap_export(const spc_kmap *km, int32_t *triples_host, int64_t cap, int64_t *nnz_host,
                                       void *stream) {

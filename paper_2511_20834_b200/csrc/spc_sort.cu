@@ -159,13 +159,26 @@ __global__ void __launch_bounds__(SORT_THREADS) k_onesweep(const uint64_t *__res
             excl_s[tid] = 0;
         } else {
             atomicExch(st, ST_AGG | (unsigned)tile_cnt);
+            // look back 8 predecessors per round trip (independent loads), newest first
             unsigned int excl = 0;
-            for (int j = tile - 1; j >= 0; --j) {
-                const volatile unsigned int *q = tile_status + (int64_t)j * 256 + tid;
-                unsigned int v;
-                do { v = *q; } while ((v & ~ST_VAL) == 0);
-                excl += v & ST_VAL;
-                if (v & ST_INC) break;
+            int j = tile - 1;
+            while (j >= 0) {
+                unsigned int v[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    v[q] = (j - q >= 0) ? *((const volatile unsigned int *)(tile_status + (int64_t)(j - q) * 256 + tid))
+                                        : 0u;
+                int consumed = 0;
+                bool stop = false;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    if (j - q < 0 || (v[q] & ~ST_VAL) == 0) break;   // before tile 0 / not published yet
+                    excl += v[q] & ST_VAL;
+                    ++consumed;
+                    if (v[q] & ST_INC) { stop = true; break; }
+                }
+                if (stop) break;
+                j -= consumed;
             }
             atomicExch(st, ST_INC | (excl + (unsigned)tile_cnt));
             excl_s[tid] = excl;
