@@ -61,6 +61,7 @@ struct ConvParams {
     uint32_t a_bytes, b_bytes;
     int stages;
     int bm;               // rows per tile: 128 or 256 (two M=128 MMAs sharing the weight tile)
+    int os_split;         // OS part: active offsets of a tile split over this many CTAs (red.add)
     uint32_t tmem_cols;   // per 128-row accumulator (power of two >= 32)
     uint32_t idesc;
     // output
@@ -89,9 +90,11 @@ __device__ __forceinline__ void decode_tile(const ConvParams &p, int64_t v, cons
     t.nt = (int)(v % p.n_ntiles);
     const int64_t tv = v / p.n_ntiles;
     if (p.mode == 0) {
-        t.row0 = tv * p.bm;
+        t.list = (int)(tv % p.os_split);   // OS: split index of the tile's active offsets
+        const int64_t rt = tv / p.os_split;
+        t.row0 = rt * p.bm;
         t.rows = (int)imin64(p.bm, n_out - t.row0);
-        t.list = t.dir = 0;
+        t.dir = 0;
         t.k = -1;
         bool any = false;
         const int64_t mt0 = t.row0 / 128, mt1 = (t.row0 + t.rows - 1) / 128;   // kernel-map mask tiles
@@ -294,7 +297,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     if (warp == W_SCHED) {
         // ===================== scheduler: tile records + gather indices ==================
         int64_t n_tiles;
-        if (p.mode == 0) n_tiles = ((n_out + BM - 1) / BM) * p.n_ntiles;
+        if (p.mode == 0) n_tiles = ((n_out + BM - 1) / BM) * p.os_split * p.n_ntiles;
         else n_tiles = (int64_t)cs.list_prefix[p.n_lists] * p.n_ntiles;
         uint32_t ti = 0;
         for (int64_t v = blockIdx.x;; v += gridDim.x, ++ti) {
@@ -313,6 +316,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                 for (int w = 0; w < 4; ++w) R.mask[w] = t.mask[w];
                 int nc = 0;
                 for (int c = next_bit(t.mask, 0); c >= 0; c = next_bit(t.mask, c + 1)) R.cols[nc++] = (uint8_t)c;
+                if (p.mode == 0 && p.os_split > 1) {   // keep this split's contiguous share
+                    const int per = (nc + p.os_split - 1) / p.os_split;
+                    const int c0 = min(nc, t.list * per), c1 = min(nc, c0 + per);
+                    for (int q = c0; q < c1; ++q) R.cols[q - c0] = R.cols[q];
+                    nc = c1 - c0;
+                }
                 R.ncols = nc;
             }
             if (p.mode == 1) {
@@ -422,10 +431,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             const TileRec &R = cs.trec[st];
             if (R.end) break;
             if (lane == 0) {
-                uint32_t mask[4] = {R.mask[0], R.mask[1], R.mask[2], R.mask[3]};
-                const int nt = R.nt, kfix = R.k;
-                for (int c = next_bit(mask, 0); c >= 0; c = next_bit(mask, c + 1)) {
-                    const int k = p.mode == 0 ? p.dense_k[c] : kfix;
+                const int nt = R.nt, kfix = R.k, ncols = R.ncols;
+                for (int ci = 0; ci < ncols; ++ci) {
+                    const int k = p.mode == 0 ? p.dense_k[R.cols[ci]] : kfix;
                     for (int cc = 0; cc < p.n_chunks; cc += p.nkb, ++it) {
                         const int s = it % S;
                         ptx::mbar_wait(ptx::smem_u32(&cs.empty[s]), ((it / S) & 1) ^ 1);
@@ -449,13 +457,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             const TileRec &R = cs.trec[st];
             if (R.end) break;
             if (lane == 0) {
-                uint32_t mask[4] = {R.mask[0], R.mask[1], R.mask[2], R.mask[3]};
+                const int ncols = R.ncols;
                 const uint32_t a = ti & 1;
                 ptx::mbar_wait(ptx::smem_u32(&cs.tempty[a]), ((ti >> 1) & 1) ^ 1);
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + a * NH * p.tmem_cols;
                 uint32_t acc = 0;
-                for (int c = next_bit(mask, 0); c >= 0; c = next_bit(mask, c + 1)) {
+                for (int ci = 0; ci < ncols; ++ci) {
                     for (int cc = 0; cc < p.n_chunks; cc += p.nkb, ++it) {
                         const int s = it % S;
                         ptx::mbar_wait(ptx::smem_u32(&cs.full[s]), (it / S) & 1);
@@ -507,7 +515,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             for (int h = 0; h < NH; ++h) {
                 const int r = h * TC_BM + e * 32 + lane;
                 int64_t orow = -1;
-                if (r < R.rows) orow = p.mode == 0 ? R.row0 + r : (int64_t)R.scatter[r];
+                if (r < R.rows && R.ncols > 0) orow = p.mode == 0 ? R.row0 + r : (int64_t)R.scatter[r];
                 const uint32_t tbase = tmem_base + (a * NH + h) * p.tmem_cols + ((uint32_t)(e * 32) << 16);
                 for (int col = 0; col < p.BN; col += 32) {
                     uint32_t vals[32];
@@ -866,7 +874,7 @@ static spc_status launch_tc(const ConvParams &p0, int mode, int out_kind, void *
         configured = true;
     }
     // persistent: one CTA per SM (the WS tile count lives on the device)
-    int64_t tiles_cap = mode == 0 ? ((p.n_out_cap + p.bm - 1) / p.bm) * p.n_ntiles : (int64_t)num_sms();
+    int64_t tiles_cap = mode == 0 ? ((p.n_out_cap + p.bm - 1) / p.bm) * p.os_split * p.n_ntiles : (int64_t)num_sms();
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles_cap, num_sms()));
     if (p.bm == 256) {
         if (p.BK == 64) k_conv_tc<64, 256><<<grid, TC_THREADS, smem, st>>>(p);
@@ -971,6 +979,8 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
     // 256-row tiles (two MMAs per weight tile) whenever four accumulators fit TMEM
     p.bm = (4 * p.tmem_cols <= 512 && !getenv("SPC_BM128")) ? 256 : 128;
     if (has_os && (size_t)BLK_SLOTS * p.bm * km->k_dense * 4 > 96 * 1024) p.bm = 128;   // OS index blocks (K=5)
+    // small coordinate levels: 128-row tiles keep more SMs busy
+    if (p.bm == 256 && (km->n_out + 255) / 256 < 2 * num_sms()) p.bm = 128;
     p.kb_a = (uint32_t)(p.bm * p.BK * 2);
     p.kb_b = (uint32_t)(p.BN * p.BK * 2);
     // several K-blocks per stage: whole input rows per stage when they fit (fewer steps; the
@@ -984,16 +994,41 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
     p.b_bytes = p.nkb * p.kb_b;
     p.idesc = ptx::umma_idesc_f16(in_dtype == SPC_BF16, TC_BM, p.BN);
     p.wblob = static_cast<const char *>(weight);
+    // small layers: split each OS tile's offsets over several CTAs (reduced with red.add)
+    p.os_split = 1;
     if (has_os) {
+        const int64_t row_tiles = (km->n_out + p.bm - 1) / p.bm * p.n_ntiles;
+        if (row_tiles < num_sms() && km->k_dense >= 4 && !getenv("SPC_NO_OS_SPLIT"))
+            p.os_split = (int)std::max<int64_t>(1, std::min<int64_t>(num_sms() / row_tiles, km->k_dense / 2));
+    }
+    const bool use_acc = has_ws || p.os_split > 1;
+    if (use_acc && !acc) {
+        if (out_dtype == SPC_F32 && !residual) {
+            acc = static_cast<float *>(f_out);
+            ld_acc = ld_out;
+        } else {
+            if (!ws || ws_bytes < spc_conv_workspace_size(km, c_out, out_dtype))
+                return fail(SPC_ERR_WORKSPACE, "spc_conv_forward: ws too small");
+            acc = static_cast<float *>(ws);
+            ld_acc = c_out;
+        }
+    }
+    if (has_os && p.os_split == 1) {
         spc_status s = has_ws ? launch_tc(p, 0, OUT_F32_STORE, acc, ld_acc, st) : launch_tc(p, 0, OUT_FINAL, f_out, ld_out, st);
         if (s != SPC_OK) return s;
-    } else if (has_ws) {
+    } else if (use_acc) {
         k_zero_rows<<<1024, 256, 0, st>>>(acc, ld_acc, km->n_out, km->n_out_dev, c_out);
         SPC_LAUNCH_CHECK("k_zero_rows");
+        if (has_os) {
+            spc_status s = launch_tc(p, 0, OUT_F32_RED, acc, ld_acc, st);
+            if (s != SPC_OK) return s;
+        }
     }
     if (has_ws) {
         spc_status s = launch_tc(p, 1, OUT_F32_RED, acc, ld_acc, st);
         if (s != SPC_OK) return s;
+    }
+    if (use_acc) {
         if (acc != f_out) {
             const int64_t work = km->n_out * (c_out / 8);
             k_convert<<<(unsigned)std::min<int64_t>((work + 255) / 256, 8 * 148), 256, 0, st>>>(
