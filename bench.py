@@ -29,6 +29,14 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 METRIC = "MinkUNet scans/sec"
+WORKLOADS = {
+    2: "C2: MinkUNet-42 (42 K=3 SpC layers + 7 1x1) on one SemanticKITTI-shaped synthetic scan per GPU "
+       "(~100k voxels, 0.05 m), random bf16 weights",
+    3: "C3: SECOND/CenterPoint-style backbone (stem K3 + 16 SubM K5 + 3 strided K3) on one nuScenes-shaped "
+       "synthetic scan per GPU (~90k voxels, 10 sweeps)",
+    4: "C4: batch of 8 Waymo-shaped synthetic scans (~200k voxels each) sharded over the GPUs, MinkUNet-42, "
+       "network-wide kernel maps, NCCL gather of outputs",
+}
 UNIT = "scans/s"
 CONFIG_ID = 2
 
@@ -39,6 +47,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="spc", choices=["spc", "reference"])
+    ap.add_argument("--config", type=int, default=2, choices=[2, 3, 4],
+                    help="2: MinkUNet-42 on one KITTI-shaped scan per GPU (headline); 3: K=5 "
+                         "SECOND-style backbone on one nuScenes-shaped scan per GPU; 4: batch of 8 "
+                         "Waymo-shaped scans sharded over the GPUs (MinkUNet-42, NCCL output gather)")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-tune", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -54,11 +66,26 @@ def dist_env():
 # shared: the synthetic workload
 # ---------------------------------------------------------------------------------------
 
-def workload(rank: int):
+def workload(rank: int, config: int = CONFIG_ID, world: int = 1):
+    """Synthetic input of this rank: (coords int32 [n,4], raw features [n, c_raw], scans, net)."""
     import synth
-    coords = synth.make_scan(CONFIG_ID, scan_index=rank)
-    feats = synth.make_features(coords.shape[0], 4, seed=synth.scan_seed(CONFIG_ID, rank) + 1)
-    return coords, feats
+    if config == 4:
+        from paper_2511_20834_b200.distributed import assign_scans
+        # sizes are known from the generator; LPT-assign the 8 scans to ranks
+        scans = [synth.make_scan(4, i) for i in range(8)]
+        mine = assign_scans([s.shape[0] for s in scans], world)[rank]
+        parts = []
+        for b, i in enumerate(mine):
+            c = scans[i].copy()
+            c[:, 0] = b
+            parts.append(c)
+        coords = np.concatenate(parts)
+        feats = synth.make_features(coords.shape[0], 4, seed=synth.scan_seed(4, 100 + rank))
+        return coords, feats, len(mine), "minkunet42"
+    coords = synth.make_scan(config, scan_index=rank)
+    c_raw = 5 if config == 3 else 4
+    feats = synth.make_features(coords.shape[0], c_raw, seed=synth.scan_seed(config, rank) + 1)
+    return coords, feats, 1, ("secondk5" if config == 3 else "minkunet42")
 
 
 def spec_for(coords):
@@ -168,7 +195,7 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    coords, _ = workload(0)
+    coords, _, _, _ = workload(0)
     import synth  # noqa: F401
     for _ in range(args.warmup):
         oracle_scan_seconds(coords, rows_per_layer=32)
@@ -206,7 +233,7 @@ def main():
     import torch
     import paper_2511_20834_b200 as spc
     from paper_2511_20834_b200 import build as spc_build
-    from paper_2511_20834_b200.network import SparseUNet, C_IN_PAD
+    from paper_2511_20834_b200.network import SparseNet, C_IN_PAD
 
     rank, world, local = dist_env()
     if world > 1:
@@ -218,13 +245,14 @@ def main():
     spc_build.build()
     spc.lib()
 
-    coords_np, feats_np = workload(rank)
+    coords_np, feats_np, scans_here, net_name = workload(rank, args.config, world)
     n = coords_np.shape[0]
-    spec = spec_for(coords_np)
-    net = SparseUNet(n, spec, device=dev)
+    spec = spec_for(coords_np) if args.config != 4 else spc.spc_plan_pack(
+        coords_np[:, 1:].min(0), coords_np[:, 1:].max(0), 8, 16, 16)
+    net = SparseNet(n, spec, device=dev, net=net_name)
     coords = torch.from_numpy(coords_np).to(dev)
     feats = torch.zeros(n, C_IN_PAD, dtype=torch.bfloat16, device=dev)
-    feats[:, :4] = torch.from_numpy(feats_np).to(dev, torch.bfloat16)
+    feats[:, :feats_np.shape[1]] = torch.from_numpy(feats_np).to(dev, torch.bfloat16)
     stream = torch.cuda.current_stream(dev)
 
     # ---- one-time dataflow tuning per kernel map (not timed) ------------------
@@ -291,8 +319,22 @@ def main():
     if world > 1:
         from paper_2511_20834_b200.distributed import max_over_ranks
         t_total = max_over_ranks(t_total, device=dev)
-    value = world * args.steps / t_total
+    total_scans = 8 if args.config == 4 else world
+    value = total_scans * args.steps / t_total
     clocks = clk.summary()
+    gather_ms = None
+    if args.config == 4 and world > 1:
+        # the only data-path collective: gather the sharded outputs (timed separately)
+        from paper_2511_20834_b200.distributed import gather_rows, max_over_ranks
+        out = net.bufs[net.out_name][:n]
+        gather_rows(out)
+        torch.cuda.synchronize()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        gather_rows(out)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        gather_ms = max_over_ranks(g0.elapsed_time(g1), device=dev)
 
     # ---- per-layer breakdown + roofline of the dominant kernel (instrumented pass) -------
     flops = net.algorithmic_flops()
@@ -309,16 +351,18 @@ def main():
     e2e = None
     if rank == 0 or world > 1:
         e2e = end_to_end(net, coords_np, feats_np, dev, stream, args.steps, flush)
-    e2e_v = e2e["value"] * world if e2e else None
+    e2e_v = e2e["value"] * (total_scans / max(1, scans_here) if args.config == 4 else world) if e2e else None
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": METRIC if net_name == "minkunet42" else "SECOND-K5 backbone scans/sec", "value": value,
+            "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_total / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": "C2: MinkUNet-42 (42 K=3 SpC layers + 7 1x1) on one SemanticKITTI-shaped "
-                                   "synthetic scan per GPU (~100k voxels, 0.05 m), random bf16 weights",
-                       "model": "MinkUNet-42", "global_batch": world, "n_voxels": n,
+            "scaling": "strong" if args.config == 4 else "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic",
+            "config": {"workload": WORKLOADS[args.config],
+                       "model": "MinkUNet-42" if net_name == "minkunet42" else "SECOND/CenterPoint-K5 backbone",
+                       "global_batch": total_scans, "n_voxels": n, "nccl_gather_ms": gather_ms,
                        "parallelism": f"scan-sharded x{world}", "l2": "flushed (320 MB write) between timed steps",
                        "cuda_graph": graph is not None, "dataflow_t": {str(k): v for k, v in net.t.items()},
                        "pack_spec": list(spec.astuple())},
@@ -335,7 +379,7 @@ def main():
             "gpu_launches": launches["total"],
             "top_kernels": top,
         }
-        if world == 1 and not args.no_cpu_baseline:
+        if world == 1 and not args.no_cpu_baseline and args.config == 2:
             sec, sampled, nl = oracle_scan_seconds(coords_np, rows_per_layer=128)
             line["cpu_baseline"] = {"value": 1.0 / sec, "unit": UNIT, "cores": 1, "kind": "oracle",
                                     "sample": f"full sort + Eq.(1) levels + {nl} layers x 128 sampled output rows "
@@ -458,11 +502,11 @@ def end_to_end(net, coords_np, feats_np, dev, stream, steps, flush):
     n = coords_np.shape[0]
     h_coords = torch.from_numpy(coords_np).pin_memory()
     f16 = np.zeros((n, C_IN_PAD), np.float32)
-    f16[:, :4] = feats_np
+    f16[:, :feats_np.shape[1]] = feats_np
     h_feats = torch.from_numpy(f16).to(torch.bfloat16).pin_memory()
     d_coords = torch.empty_like(h_coords, device=dev)
     d_feats = torch.empty_like(h_feats, device=dev)
-    out = net.bufs["out"]
+    out = net.bufs[net.out_name]
     h_out = torch.empty(out.shape, dtype=out.dtype).pin_memory()
     ms = []
     for i in range(steps + 2):

@@ -62,6 +62,7 @@ struct ConvParams {
     int stages;
     int bm;               // rows per tile: 128 or 256 (two M=128 MMAs sharing the weight tile)
     int os_split;         // OS part: active offsets of a tile split over this many CTAs (red.add)
+    int blk_slots;        // gather-index blocks in flight (2, or 1 when a block is large: K=5 OS)
     uint32_t tmem_cols;   // per 128-row accumulator (power of two >= 32)
     uint32_t idesc;
     // output
@@ -330,8 +331,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             }
             ptx::mbar_arrive(ptx::smem_u32(&cs.trec_full[st]));
             // the tile's gather indices: one contiguous block
-            const int bs = ti % BLK_SLOTS;
-            ptx::mbar_wait_sleep(ptx::smem_u32(&cs.blk_empty[bs]), ((ti / BLK_SLOTS) & 1) ^ 1);
+            const int bs = ti % p.blk_slots;
+            ptx::mbar_wait_sleep(ptx::smem_u32(&cs.blk_empty[bs]), ((ti / p.blk_slots) & 1) ^ 1);
             int32_t *B = blk + bs * blk_stride;
             const uint32_t fb = ptx::smem_u32(&cs.blk_full[bs]);
             if (p.mode == 0) {
@@ -371,8 +372,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             const TileRec &R = cs.trec[st];
             if (R.end) break;
             const int rows = R.rows, ncols = R.ncols;
-            const int bs = ti % BLK_SLOTS;
-            ptx::mbar_wait(ptx::smem_u32(&cs.blk_full[bs]), (ti / BLK_SLOTS) & 1);
+            const int bs = ti % p.blk_slots;
+            ptx::mbar_wait(ptx::smem_u32(&cs.blk_full[bs]), (ti / p.blk_slots) & 1);
             const int32_t *B = blk + bs * blk_stride;
             for (int ci = 0; ci < ncols; ++ci) {
                 const int c = p.mode == 0 ? R.cols[ci] : 0;
@@ -853,8 +854,9 @@ static spc_status launch_tc(const ConvParams &p0, int mode, int out_kind, void *
     p.ld_out = ld_out;
     const size_t stage = (size_t)p.a_bytes + p.b_bytes;
     const int kd = mode == 0 ? p.k_dense : 1;
-    const size_t extra = ((sizeof(ConvSmem) + 127) & ~size_t(127)) + (size_t)BLK_SLOTS * ((p.bm * kd + 3) & ~3) * 4 +
-                         1024 + 64;   // + alignment slack
+    const size_t blk_bytes = (size_t)((p.bm * kd + 3) & ~3) * 4;
+    p.blk_slots = 2 * blk_bytes <= 64 * 1024 ? 2 : 1;
+    const size_t extra = ((sizeof(ConvSmem) + 127) & ~size_t(127)) + (size_t)p.blk_slots * blk_bytes + 1024 + 64;
     int S = (int)((TC_SMEM_BUDGET - extra) / stage);
 #ifndef SPC_MAX_STAGES
 #define SPC_MAX_STAGES 16

@@ -1,5 +1,8 @@
 """MinkUNet-42 (C2/C4) and a SECOND/CenterPoint-style K=5 backbone (C3) over libspc.
 
+``SparseNet`` runs any layer list (``ConvSpec``) built by ``minkunet42_layers()`` or
+``second_backbone_layers()``; ``SparseUNet`` is the MinkUNet-42 instance.
+
 Orchestration only: every step of a forward pass is a C-ABI call of libspc (pack+sort,
 row gather, network-wide kernel maps, 49 sparse convolutions with fused residual adds).
 BN/ReLU are identity (out of scope); weights are seeded random bf16.
@@ -97,6 +100,35 @@ def minkunet42_layers():
     return L, widths
 
 
+def second_backbone_layers(K: int = 5, c_in_raw: int = 5):
+    """C3: CenterPoint/SECOND-style sparse backbone (ResNL): stem SubM K3
+    c_in -> 16; 4 stages (16/32/64/128 channels) of 4 SubM K-conv layers (2 residual blocks);
+    3 strided K3 s2 downsamplings -> 20 SpC layers (17 submanifold + 3 strided)."""
+    L = []
+    chans = [16, 32, 64, 128]
+
+    def conv(name, mk, ci, co, src, dst, lo, res=None, ci_fl=None):
+        L.append(ConvSpec(name, mk, ci, co, src, 0, dst, 0, lo, res, ci_fl or ci))
+
+    conv("stem", (3, 1, 1, 0), C_IN_PAD, chans[0], "x0", "a0", 0, None, c_in_raw)
+    cur = "a0"
+    for st, ch in enumerate(chans):
+        l = st
+        if st > 0:
+            conv(f"down{st}", (3, 2, 2 ** (l - 1), 0), chans[st - 1], ch, cur, f"a{l}", l)
+            cur = f"a{l}"
+        for blk in range(2):
+            conv(f"s{st}.b{blk}.conv1", (K, 1, 2 ** l, 0), ch, ch, cur, f"h{l}", l)
+            nxt = f"b{l}" if cur != f"b{l}" else f"a{l}"
+            conv(f"s{st}.b{blk}.conv2", (K, 1, 2 ** l, 0), ch, ch, f"h{l}", nxt, l, (cur, 0))
+            cur = nxt
+    widths = {"x0": C_IN_PAD}
+    for s_ in L:
+        widths[s_.dst] = max(widths.get(s_.dst, 0), s_.dst_col + s_.c_out)
+    widths["out"] = chans[-1]
+    return L, widths, cur
+
+
 def default_t(map_key):
     """Dataflow threshold per map before tuning (reading: the paper's UNet uses WS in most
     layers).  K=1 maps are always dense."""
@@ -108,16 +140,24 @@ def default_t(map_key):
     return spc.SPC_T_ALL_OS
 
 
-class SparseUNet:
-    """MinkUNet-42 forward over libspc with every buffer pre-allocated for capacity n0."""
+class SparseNet:
+    """Forward pass of a sparse-conv layer list over libspc; every buffer pre-allocated for
+    capacity n0 (all levels), so a pass is a fixed launch sequence (CUDA-graph capturable)."""
 
     def __init__(self, n0_cap: int, spec: spc.PackSpec, device="cuda", seed: int = 20834, t_override=None,
-                 nnz_per_out: float = 10.0):
+                 nnz_per_out: float = 10.0, net: str = "minkunet42"):
         self.dev = torch.device(device)
         self.spec = spec
         self.n0 = int(n0_cap)
-        self.layers, widths = minkunet42_layers()
-        self.n_levels = 5
+        if net == "minkunet42":
+            self.layers, widths = minkunet42_layers()
+            self.out_name, self.n_levels = "out", 5
+        elif net.startswith("second"):
+            K = 5 if net.endswith("k5") else 3
+            self.layers, widths, self.out_name = second_backbone_layers(K)
+            self.n_levels = 4
+        else:
+            raise ValueError(net)
         self.map_keys = []
         for s in self.layers:
             if s.map_key not in self.map_keys:
@@ -194,7 +234,7 @@ class SparseUNet:
         self.index(stream)
         for i in range(len(self.layers)):
             self.conv(i, stream)
-        return self.bufs["out"]
+        return self.bufs[self.out_name]
 
     # ---------------------------------------------------------------------------------
     def algorithmic_flops(self) -> dict:
@@ -206,3 +246,10 @@ class SparseUNet:
             out[s.name] = 2.0 * nnz[s.map_key] * s.c_in_flops * s.c_out
         self.nnz = nnz
         return out
+
+
+class SparseUNet(SparseNet):
+    """MinkUNet-42 (configs C2, C4)."""
+
+    def __init__(self, n0_cap: int, spec: spc.PackSpec, **kw):
+        super().__init__(n0_cap, spec, net="minkunet42", **kw)

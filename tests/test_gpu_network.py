@@ -1,0 +1,98 @@
+"""Network-level GPU tests: full MinkUNet-42 / SECOND-K5 forward passes through the C ABI,
+with layer-local parity (SURVEY §8(c) "Stacks"): a layer is recomputed by the oracle
+from the GPU's own input to that layer, so bf16 error does not compound."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+import paper_2511_20834_b200 as spc
+from paper_2511_20834_b200.network import SparseNet, C_IN_PAD
+
+pytestmark = pytest.mark.gpu
+
+
+def _net(config, net_name, n_cut=None):
+    coords = synth.make_scan(config, 0)
+    if n_cut:
+        coords = coords[:n_cut]
+    spec = spc.spc_plan_pack(coords[:, 1:].min(0), coords[:, 1:].max(0), 1, 16, 16)
+    net = SparseNet(coords.shape[0], spec, net=net_name)
+    c_raw = 5 if net_name.startswith("second") else 4
+    feats = torch.zeros(coords.shape[0], C_IN_PAD, dtype=torch.bfloat16, device="cuda")
+    feats[:, :c_raw] = torch.from_numpy(synth.make_features(coords.shape[0], c_raw, seed=3)).cuda().bfloat16()
+    out = net.forward(torch.from_numpy(coords).cuda(), feats)
+    torch.cuda.synchronize()
+    return net, coords, out
+
+
+def _levels(coords, n_levels):
+    c0 = oracle.sort_coords(coords)[0]
+    return [c0] + [oracle.downsample(c0, 2 ** m) for m in range(1, n_levels)]
+
+
+def _unpack_weight(net, i):
+    """Recover W [K^3, C_in, C_out] from the seeded generator (same draw order as SparseNet)."""
+    g = torch.Generator().manual_seed(20834)
+    for j, s in enumerate(net.layers):
+        kv = s.map_key[0] ** 3
+        a = math.sqrt(3.0 / (min(kv, 10.0) * s.c_in_flops))
+        w = (torch.rand(kv, s.c_in, s.c_out, generator=g) * 2 - 1) * a
+        if s.c_in != s.c_in_flops:
+            w[:, s.c_in_flops:, :] = 0
+        if j == i:
+            return w.bfloat16().float().numpy().astype(np.float64)
+    raise IndexError(i)
+
+
+def _layer_local(net, lv, i):
+    s = net.layers[i]
+    K, stride, ts, tr = s.map_key
+    lf = int(round(math.log2(ts)))
+    if stride == 1:
+        inp = out = lv[lf]
+    elif tr:
+        inp, out = lv[lf + 1], lv[lf]
+    else:
+        inp, out = lv[lf], lv[lf + 1]
+    src = net.bufs[s.src][: len(inp), s.src_col:s.src_col + s.c_in].float().cpu().numpy().astype(np.float64)
+    net.conv(i)
+    torch.cuda.synchronize()
+    got = net.bufs[s.dst][: len(out), s.dst_col:s.dst_col + s.c_out].float().cpu().numpy().astype(np.float64)
+    ref = oracle.conv(inp, out, K, ts, src, _unpack_weight(net, i), transposed=bool(tr))
+    if s.residual is not None:
+        rb, rc = s.residual
+        ref = ref + net.bufs[rb][: len(out), rc:rc + s.c_out].float().cpu().numpy().astype(np.float64)
+    # bf16-stored output: within one bf16 ulp of the fp64 reference (reading A18) + fp32 slack
+    ulp = np.exp2(np.floor(np.log2(np.maximum(np.abs(ref), 1e-30))) - 7)
+    err = np.abs(got - ref) - ulp - 1e-5 * np.abs(ref).max()
+    return float(err.max())
+
+
+def test_minkunet42_forward_and_layer_local_parity():
+    net, coords, out = _net(1, "minkunet42")
+    assert torch.isfinite(out[: coords.shape[0]].float()).all()
+    lv = _levels(coords, 5)
+    names = [s.name for s in net.layers]
+    for name in ("stem.conv1", "enc1.down", "enc2.rb1.proj", "enc2.rb1.conv2", "dec1.up", "dec4.rb1.conv1",
+                 "dec4.rb2.conv2"):
+        assert _layer_local(net, lv, names.index(name)) <= 0, name
+
+
+def test_second_k5_backbone_forward_and_layer_local_parity():
+    net, coords, out = _net(1, "secondk5")
+    assert torch.isfinite(out[:1000].float()).all()
+    lv = _levels(coords, 4)
+    names = [s.name for s in net.layers]
+    for name in ("stem", "s0.b0.conv1", "down1", "s1.b1.conv2", "s3.b0.conv1"):
+        assert _layer_local(net, lv, names.index(name)) <= 0, name
+
+
+def test_network_index_levels_match_oracle():
+    net, coords, _ = _net(1, "minkunet42")
+    lv = _levels(coords, 5)
+    ln = net.level_n.cpu().tolist()
+    assert ln == [len(x) for x in lv]
