@@ -363,9 +363,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         const int r_in = lane % RPI, q_lane = lane / RPI;
         int s = 0;
         uint32_t ph = 0;   // stage ring position / phase
-#ifdef SPC_EXP_TRACE
-        uint32_t ptr_ctr = 0;
-#endif
         for (uint32_t ti = 0;; ++ti) {
             const int st = ti % TREC_SLOTS;
             ptx::mbar_wait(ptx::smem_u32(&cs.trec_full[st]), (ti / TREC_SLOTS) & 1);
@@ -375,46 +372,33 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             const int bs = ti % p.blk_slots;
             ptx::mbar_wait(ptx::smem_u32(&cs.blk_full[bs]), (ti / p.blk_slots) & 1);
             const int32_t *B = blk + bs * blk_stride;
-            for (int ci = 0; ci < ncols; ++ci) {
-                const int c = p.mode == 0 ? R.cols[ci] : 0;
-                if (threadIdx.x == 0) TR(0, ptr_ctr);
-                const char *gp[NB];
-                bool ok[NB];
-                uint32_t so[NB];
+            // flat sequence of (offset column, channel chunk) slices; a stage holds up to
+            // p.nkb consecutive slices (several chunks of one offset, or several offsets)
+            const int nsl = ncols * p.n_chunks;
+            for (int sl = 0; sl < nsl; sl += p.nkb) {
+                const int nin = min(p.nkb, nsl - sl);
+                ptx::mbar_wait(ptx::smem_u32(&cs.empty[s]), ph ^ 1);
+                const uint32_t abase = ptx::smem_u32(sa + (size_t)s * p.a_bytes);
+                for (int kb = 0; kb < nin; ++kb) {
+                    const int ci = (sl + kb) / p.n_chunks, cc = (sl + kb) - ci * p.n_chunks;
+                    const int c = p.mode == 0 ? R.cols[ci] : 0;
+                    const uint32_t kbo = kb * p.kb_a;
 #pragma unroll
-                for (int b = 0; b < NB; ++b) {
-                    const int r = warp * ROWS_W + b * RPI + r_in;
-                    const int32_t g = r < rows ? B[r * kd + c] : -1;
-                    const uint32_t f = rb == 128 ? (r & 7) : (rb == 64 ? ((r >> 1) & 3) : ((r >> 2) & 1));
-                    ok[b] = g >= 0;
-                    gp[b] = p.f_in + (ok[b] ? (int64_t)g * p.ld_in_bytes + q_lane * 16 : 0);
-                    so[b] = (uint32_t)r * rb + ((q_lane ^ f) * 16);
-                }
-                for (int cc = 0; cc < p.n_chunks; cc += p.nkb) {
-                    if (threadIdx.x == 0) TR(4, ptr_ctr);
-                    ptx::mbar_wait(ptx::smem_u32(&cs.empty[s]), ph ^ 1);
-                    if (threadIdx.x == 0) TR(1, ptr_ctr);
-                    const uint32_t abase = ptx::smem_u32(sa + (size_t)s * p.a_bytes);
-                    for (int kb = 0; kb < p.nkb; ++kb) {
-                        const uint32_t kbo = kb * p.kb_a;
-#pragma unroll
-                        for (int b = 0; b < NB; ++b) {
-                            // matched rows: one whole-line request per row; sentinel rows (no
-                            // input voxel) never touch L2: zero them with a shared store
-                            if (ok[b]) ptx::cp_async_16(abase + kbo + so[b], gp[b] + kb * rb, 16u);
-                            else asm volatile("st.shared.v4.b32 [%0], {%1,%1,%1,%1};" ::"r"(abase + kbo + so[b]), "r"(0)
-                                              : "memory");
-                        }
+                    for (int b = 0; b < NB; ++b) {
+                        const int r = warp * ROWS_W + b * RPI + r_in;
+                        const int32_t g = r < rows ? B[r * kd + c] : -1;
+                        const uint32_t f = rb == 128 ? (r & 7) : (rb == 64 ? ((r >> 1) & 3) : ((r >> 2) & 1));
+                        const uint32_t so = kbo + (uint32_t)r * rb + ((q_lane ^ f) * 16);
+                        // matched rows: one whole-line request per row; sentinel rows (no input
+                        // voxel) never touch L2: zero them with a shared store
+                        if (g >= 0)
+                            ptx::cp_async_16(abase + so, p.f_in + (int64_t)g * p.ld_in_bytes + cc * rb + q_lane * 16, 16u);
+                        else
+                            asm volatile("st.shared.v4.b32 [%0], {%1,%1,%1,%1};" ::"r"(abase + so), "r"(0) : "memory");
                     }
-                    ptx::cp_async_mbar_arrive(ptx::smem_u32(&cs.full[s]));
-                    if (threadIdx.x == 0) TR(5, ptr_ctr);
-#ifdef SPC_EXP_TRACE
-                    ++ptr_ctr;
-#endif
-#pragma unroll
-                    for (int b = 0; b < NB; ++b) gp[b] += ok[b] ? rb * p.nkb : 0;
-                    if (++s == S) { s = 0; ph ^= 1; }
                 }
+                ptx::cp_async_mbar_arrive(ptx::smem_u32(&cs.full[s]));
+                if (++s == S) { s = 0; ph ^= 1; }
             }
             __syncwarp();
             if (lane == 0) {
@@ -433,16 +417,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             if (R.end) break;
             if (lane == 0) {
                 const int nt = R.nt, kfix = R.k, ncols = R.ncols;
-                for (int ci = 0; ci < ncols; ++ci) {
-                    const int k = p.mode == 0 ? p.dense_k[R.cols[ci]] : kfix;
-                    for (int cc = 0; cc < p.n_chunks; cc += p.nkb, ++it) {
-                        const int s = it % S;
-                        ptx::mbar_wait(ptx::smem_u32(&cs.empty[s]), ((it / S) & 1) ^ 1);
-                        const uint32_t fb = ptx::smem_u32(&cs.full[s]);
-                        // nkb consecutive chunk blobs are contiguous: one bulk copy per stage
-                        ptx::mbar_arrive_expect_tx(fb, p.b_bytes);
+                const int nsl = ncols * p.n_chunks;
+                for (int sl = 0; sl < nsl; sl += p.nkb, ++it) {
+                    const int nin = min(p.nkb, nsl - sl);
+                    const int s = it % S;
+                    ptx::mbar_wait(ptx::smem_u32(&cs.empty[s]), ((it / S) & 1) ^ 1);
+                    const uint32_t fb = ptx::smem_u32(&cs.full[s]);
+                    ptx::mbar_arrive_expect_tx(fb, nin * p.kb_b);
+                    for (int kb = 0; kb < nin; ++kb) {
+                        const int ci = (sl + kb) / p.n_chunks, cc = (sl + kb) - ci * p.n_chunks;
+                        const int k = p.mode == 0 ? p.dense_k[R.cols[ci]] : kfix;
                         const int64_t blob = ((int64_t)k * p.n_ntiles + nt) * p.n_chunks + cc;
-                        ptx::bulk_g2s(ptx::smem_u32(sb + (size_t)s * p.b_bytes), p.wblob + blob * p.kb_b, p.b_bytes, fb);
+                        ptx::bulk_g2s(ptx::smem_u32(sb + (size_t)s * p.b_bytes + kb * p.kb_b), p.wblob + blob * p.kb_b,
+                                      p.kb_b, fb);
                     }
                 }
                 ptx::mbar_arrive(ptx::smem_u32(&cs.trec_empty[st]));
@@ -464,35 +451,33 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + a * NH * p.tmem_cols;
                 uint32_t acc = 0;
-                for (int ci = 0; ci < ncols; ++ci) {
-                    for (int cc = 0; cc < p.n_chunks; cc += p.nkb, ++it) {
-                        const int s = it % S;
-                        ptx::mbar_wait(ptx::smem_u32(&cs.full[s]), (it / S) & 1);
-                        TR(2, it);
-                        // the A tile was written by cp.async (generic proxy): order it before
-                        // the tensor core's async-proxy reads
-#ifndef SPC_EXP_NO_FENCE
-                        ptx::fence_proxy_async();
-#endif
-                        ptx::tc_fence_after();
-                        const uint32_t a_base = ptx::smem_u32(sa + (size_t)s * p.a_bytes);
-                        const uint32_t b_base = ptx::smem_u32(sb + (size_t)s * p.b_bytes);
-                        for (int kb = 0; kb < p.nkb; ++kb) {
+                const int nsl = ncols * p.n_chunks;
+                for (int sl = 0; sl < nsl; sl += p.nkb, ++it) {
+                    const int nin = min(p.nkb, nsl - sl);
+                    const int s = it % S;
+                    ptx::mbar_wait(ptx::smem_u32(&cs.full[s]), (it / S) & 1);
+                    TR(2, it);
+                    // the A tile was written by cp.async / st.shared (generic proxy): order it
+                    // before the tensor core's async-proxy reads
+                    ptx::fence_proxy_async();
+                    ptx::tc_fence_after();
+                    const uint32_t a_base = ptx::smem_u32(sa + (size_t)s * p.a_bytes);
+                    const uint32_t b_base = ptx::smem_u32(sb + (size_t)s * p.b_bytes);
+                    for (int kb = 0; kb < nin; ++kb) {
 #pragma unroll
-                            for (int kk = 0; kk < BK / 16; ++kk) {
-                                const uint64_t bd = ptx::umma_desc_kmajor_sw(b_base + kb * p.kb_b + kk * 32, rb);
+                        for (int kk = 0; kk < BK / 16; ++kk) {
+                            const uint64_t bd = ptx::umma_desc_kmajor_sw(b_base + kb * p.kb_b + kk * 32, rb);
 #pragma unroll
-                                for (int h = 0; h < NH; ++h) {
-                                    const uint64_t ad =
-                                        ptx::umma_desc_kmajor_sw(a_base + kb * p.kb_a + h * TC_BM * rb + kk * 32, rb);
-                                    ptx::mma_f16_ss(d_tmem + h * p.tmem_cols, ad, bd, p.idesc, acc);
-                                }
-                                acc = 1;
+                            for (int h = 0; h < NH; ++h) {
+                                const uint64_t ad =
+                                    ptx::umma_desc_kmajor_sw(a_base + kb * p.kb_a + h * TC_BM * rb + kk * 32, rb);
+                                ptx::mma_f16_ss(d_tmem + h * p.tmem_cols, ad, bd, p.idesc, acc);
                             }
+                            acc = 1;
                         }
-                        ptx::mma_commit(ptx::smem_u32(&cs.empty[s]));
-                        TR(3, it);
                     }
+                    ptx::mma_commit(ptx::smem_u32(&cs.empty[s]));
+                    TR(3, it);
                 }
                 ptx::mma_commit(ptx::smem_u32(&cs.tfull[a]));
                 ptx::mbar_arrive(ptx::smem_u32(&cs.trec_empty[st]));
@@ -987,10 +972,10 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
     p.kb_b = (uint32_t)(p.BN * p.BK * 2);
     // several K-blocks per stage: whole input rows per stage when they fit (fewer steps; the
     // per-stage cost is mostly fixed), keeping >= 3 stages in shared memory
-    p.nkb = 1;
+    // slices (one BK-channel chunk of one offset) per pipeline stage: a stage carries up
+    // to ~72 KB so narrow layers pack several offsets into one stage
     static const size_t stage_cap = getenv("SPC_STAGE_KB") ? (size_t)atoi(getenv("SPC_STAGE_KB")) * 1024 : 72 * 1024;
-    for (int d = p.n_chunks; d >= 1; --d)
-        if (p.n_chunks % d == 0 && (size_t)d * (p.kb_a + p.kb_b) <= stage_cap) { p.nkb = d; break; }
+    p.nkb = (int)std::max<size_t>(1, std::min<size_t>(8, stage_cap / (p.kb_a + p.kb_b)));
     if (getenv("SPC_NKB1")) p.nkb = 1;
     p.a_bytes = p.nkb * p.kb_a;
     p.b_bytes = p.nkb * p.kb_b;
