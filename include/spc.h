@@ -232,7 +232,16 @@ spc_status spc_kmap_export(const spc_kmap *kmap, int32_t *triples_host, int64_t 
  * f32 inputs -> FFMA (fp32).  c_in, c_out multiples of 16 (f16/bf16); f32: c_in % 4 == 0,
  * c_out % 8 == 0;
  * c_out <= 256 per weight tile (larger c_out is tiled).
- * ws     : >= spc_conv_workspace_size() bytes (fp32 accumulator of the WS part).
+ * ws     : >= spc_conv_workspace_size() bytes: the fp32 accumulator of the WS part and of
+ *          split output tiles (small levels: a tile's offsets are split over CTAs, the
+ *          last arriving CTA finishes the tile), followed by tile arrival counters.
+ *          CONTRACT: ws must be all-zero before its first use (cudaMemset once); every
+ *          call returns it to all-zero, so it can be reused by any later call of any
+ *          shape without clearing.  One ws per stream (calls sharing a ws must be
+ *          stream-ordered).  ws may be NULL only for maps without a WS part; then no
+ *          tile is split.
+ * Tile geometry (128/256-row tiles, split factor) is chosen on the device from the live
+ * row count *n_out_dev, so capacity-sized network maps need no host sync.
  * ================================================================================ */
 size_t spc_prepared_weight_bytes(int32_t k_vol, int32_t c_in, int32_t c_out, int32_t in_dtype);
 spc_status spc_prepare_weight(const void *weight, int32_t k_vol, int32_t c_in, int32_t c_out,

@@ -134,8 +134,9 @@ def _stream(stream=None):
     return ctypes.c_void_p(s.cuda_stream)
 
 
-def _ws(nbytes: int, device) -> torch.Tensor:
-    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+def _ws(nbytes: int, device, zero: bool = False) -> torch.Tensor:
+    n = max(int(nbytes), 256)
+    return torch.zeros(n, dtype=torch.uint8, device=device) if zero else torch.empty(n, dtype=torch.uint8, device=device)
 
 
 # ---------------------------------------------------------------------------------------
@@ -322,13 +323,17 @@ def spc_conv_workspace_size(km: KernelMap, c_out: int, out_dtype=torch.float32) 
 def spc_conv_forward(km: KernelMap, f_in: torch.Tensor, weight_prepared: torch.Tensor, c_in: int, c_out: int,
                      out: torch.Tensor | None = None, out_dtype=None, residual: torch.Tensor | None = None,
                      ws: torch.Tensor | None = None, stream=None) -> torch.Tensor:
-    """Eq. (2) for the map ``km``: f_in [n_in, >=c_in] (row stride = f_in.stride(0)) -> out [n_out, c_out]."""
+    """Eq. (2) for the map ``km``: f_in [n_in, >=c_in] (row stride = f_in.stride(0)) -> out [n_out, c_out].
+    ``ws``: byte tensor of >= spc_conv_workspace_size bytes, all-zero before its first use
+    (torch.zeros); every call leaves it all-zero again."""
     out_dtype = out_dtype or (out.dtype if out is not None else f_in.dtype)
     if out is None:
         out = torch.empty((km.n_out, c_out), dtype=out_dtype, device=f_in.device)
     need = spc_conv_workspace_size(km, c_out, out_dtype)
-    if ws is None or ws.numel() < need:
-        ws = _ws(need, f_in.device)
+    if ws is None:
+        ws = _ws(need, f_in.device, zero=True)   # must be all-zero on first use (spc.h)
+    elif ws.numel() < need:
+        raise ValueError(f"spc_conv_forward: ws has {ws.numel()} bytes, needs {need}")
     _check(lib().spc_conv_forward(ctypes.byref(km.c), _ptr(f_in), f_in.stride(0), _DT[f_in.dtype], int(c_in),
                                   _ptr(weight_prepared), int(c_out), _ptr(out), out.stride(0), _DT[out.dtype],
                                   _ptr(residual), residual.stride(0) if residual is not None else 0, _ptr(ws),

@@ -1,6 +1,8 @@
 """Build libspc.so (the C-ABI CUDA library) in-tree with nvcc for sm_100a.
 
 Usage: python -m paper_2511_20834_b200.build   (or __graft_entry__.build())
+Experiments: python -m paper_2511_20834_b200.build --exp NAME -DMACRO ...  -> exp_NAME.so
+(load it with SPC_LIB_OVERRIDE=.../exp_NAME.so)
 """
 from __future__ import annotations
 
@@ -27,16 +29,17 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, exp: str | None = None, defines=()) -> str:
+    lib = LIB if exp is None else os.path.join(HERE, f"exp_{exp}.so")
+    if exp is None and not force and not _stale():
         return LIB
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build" if exp is None else f"build_{exp}")
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
     for src in SOURCES:
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
-        cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *FLAGS, *defines, "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd), flush=True)
@@ -45,13 +48,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for p, src in zip(procs, SOURCES):
         if p.wait() != 0:
             raise RuntimeError(f"nvcc failed on {src}")
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     subprocess.check_call([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", tmp,
                            "-lcudart_static", "-lrt", "-ldl", "-lpthread"])
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    exp = sys.argv[sys.argv.index("--exp") + 1] if "--exp" in sys.argv else None
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, exp=exp,
+                defines=[a for a in sys.argv[1:] if a.startswith("-D")]))

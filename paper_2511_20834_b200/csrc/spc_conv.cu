@@ -56,12 +56,23 @@ struct ConvParams {
     int64_t ld_in_bytes;
     const char *wblob;
     int n_chunks, n_ntiles, BK, BN;
-    int nkb;              // K-blocks (of BK channels) per pipeline stage; n_chunks % nkb == 0
-    uint32_t kb_a, kb_b;  // bytes of one A / B K-block in a stage
-    uint32_t a_bytes, b_bytes;
-    int stages;
-    int bm;               // rows per tile: 128 or 256 (two M=128 MMAs sharing the weight tile)
-    int os_split;         // OS part: active offsets of a tile split over this many CTAs (red.add)
+    uint32_t kb_b;        // bytes of one B K-block (BN x BK weight slice)
+    // pipeline ring carved per tile height: ring[0] for BM-row tiles, ring[1] for 128-row
+    // tiles of a BM=256 kernel (half-height A slices, so more slices per stage)
+    struct Ring {
+        uint32_t kb_a;     // bytes of one A K-block (tile rows x BK)
+        uint32_t a_bytes, b_bytes;   // per stage
+        int nkb;           // K-blocks (slices) per stage
+        int stages;
+    } ring[2];
+    uint32_t hdr_off;     // byte offset of ConvSmem + index blocks (after the ring)
+    int bm;               // max rows per tile (template BM): 128 or 256 (two M=128 MMAs sharing the weight tile)
+    int split_ok;         // OS part may split a tile's offsets over CTAs (needs acc + tile_ctr)
+    int force_tr;         // experiments: 128/256 forces the tile rows (0 = device heuristic)
+    int num_sms;
+    float *acc;           // fp32 split-K accumulator (all-zero on entry, left all-zero)
+    int64_t ld_acc;
+    int *tile_ctr;        // per output tile arrival counters (zero on entry, left zero)
     int blk_slots;        // gather-index blocks in flight (2, or 1 when a block is large: K=5 OS)
     uint32_t tmem_cols;   // per 128-row accumulator (power of two >= 32)
     uint32_t idesc;
@@ -85,16 +96,17 @@ struct TileInfo {
     uint32_t mask[4];
 };
 
-// virtual tile v -> TileInfo; identical in every role (deterministic)
+// virtual tile v -> TileInfo; identical in every role (deterministic).  tr = rows per
+// tile and split = CTAs per OS tile, both chosen on the device from the live counts.
 __device__ __forceinline__ void decode_tile(const ConvParams &p, int64_t v, const int *list_prefix, int64_t n_out,
-                                            TileInfo &t) {
+                                            int tr, int split, TileInfo &t) {
     t.nt = (int)(v % p.n_ntiles);
     const int64_t tv = v / p.n_ntiles;
     if (p.mode == 0) {
-        t.list = (int)(tv % p.os_split);   // OS: split index of the tile's active offsets
-        const int64_t rt = tv / p.os_split;
-        t.row0 = rt * p.bm;
-        t.rows = (int)imin64(p.bm, n_out - t.row0);
+        t.list = (int)(tv % split);   // OS: split index of the tile's active offsets
+        const int64_t rt = tv / split;
+        t.row0 = rt * tr;
+        t.rows = (int)imin64(tr, n_out - t.row0);
         t.dir = 0;
         t.k = -1;
         bool any = false;
@@ -112,12 +124,12 @@ __device__ __forceinline__ void decode_tile(const ConvParams &p, int64_t v, cons
         while (l + 1 < p.n_lists && list_prefix[l + 1] <= tv) ++l;
         const int local = (int)(tv - list_prefix[l]);
         const int cnt = p.counts[SPC_MAX_KVOL + l];
-        const int per = (cnt + p.bm - 1) / p.bm;
+        const int per = (cnt + tr - 1) / tr;
         t.list = l;
         t.dir = local / per;
         const int tl = local - t.dir * per;
-        t.row0 = (int64_t)tl * p.bm;
-        t.rows = min(p.bm, cnt - tl * p.bm);
+        t.row0 = (int64_t)tl * tr;
+        t.rows = min(tr, cnt - tl * tr);
         t.k = t.dir ? p.k_vol - 1 - p.list_k[l] : p.list_k[l];
         t.mask[0] = 1u;
         t.mask[1] = t.mask[2] = t.mask[3] = 0u;
@@ -217,6 +229,9 @@ struct ConvSmem {
     uint64_t trec_full[TREC_SLOTS], trec_empty[TREC_SLOTS];
     uint64_t blk_full[BLK_SLOTS], blk_empty[BLK_SLOTS];
     uint32_t tmem_holder[4];
+    int tr, split;                 // device-chosen tile rows / OS split (see geometry below)
+    int64_t n_tiles;
+    int epi_flag[2], epi_last[2];  // split-K fixup decisions, double-buffered by tile parity
     int list_prefix[SPC_MAX_KVOL + 1];
     TileRec trec[TREC_SLOTS];
 };
@@ -228,27 +243,240 @@ __device__ long long g_tr[8][4096];
 #define TR(slot, i) do {} while (0)
 #endif
 
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+// OS split-K fixup, run by the 4 epilogue warps (thread = tile row within a 128-row half).
+// Every split of an output tile red.adds its partial into the fp32 accumulator and bumps
+// the tile's arrival counter; the split that completes the count reads the sum back, adds
+// the residual, writes the final dtype, and returns the accumulator rows and the counter
+// to zero (so the next launch needs no zero-fill).  A split that finds all others already
+// arrived skips its own red.add and adds its TMEM values directly.
+__device__ __noinline__ void os_split_fixup(const ConvParams &p, ConvSmem &cs, const TileRec &R, uint32_t ti, int tr,
+                                            int split, int nht, uint32_t tmem_tile, int e, int lane) {
+    const int fl = ti & 1;
+    const bool lead = threadIdx.x == 32 * W_EPI0;
+    int *ctr = p.tile_ctr + (R.row0 / tr) * p.n_ntiles + R.nt;
+    const bool own = R.ncols > 0;
+    if (lead) {
+        int c;
+        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(c) : "l"(ctr) : "memory");
+        cs.epi_flag[fl] = c == split - 1;
+    }
+    epi_bar();
+    const bool direct = cs.epi_flag[fl] != 0;
+    bool last = direct;
+    if (!direct) {
+        if (own) {
+            for (int h = 0; h < nht; ++h) {
+                const int r = h * TC_BM + e * 32 + lane;
+                const uint32_t tb = tmem_tile + h * p.tmem_cols + ((uint32_t)(e * 32) << 16);
+                for (int col = 0; col < p.BN; col += 32) {
+                    uint32_t v[32];
+                    const int n = min(32, p.BN - col);
+                    if (n == 32) ptx::tmem_ld32(tb + col, v);
+                    else ptx::tmem_ld16(tb + col, v);
+                    ptx::tmem_ld_wait();
+                    if (r < R.rows) {
+                        float *op = p.acc + (R.row0 + r) * p.ld_acc + R.nt * p.BN + col;
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            if (q * 4 < n) ptx::red_add_v4(op + 4 * q, to_f(v[4 * q]), to_f(v[4 * q + 1]), to_f(v[4 * q + 2]), to_f(v[4 * q + 3]));
+                    }
+                }
+            }
+        }
+        __threadfence();
+        epi_bar();
+        if (lead) {
+            const int old = atomicAdd(ctr, 1);
+            __threadfence();
+            cs.epi_last[fl] = old == split - 1;
+        }
+        epi_bar();
+        last = cs.epi_last[fl] != 0;
+    }
+    if (!last) return;
+    for (int h = 0; h < nht; ++h) {
+        const int r = h * TC_BM + e * 32 + lane;
+        const uint32_t tb = tmem_tile + h * p.tmem_cols + ((uint32_t)(e * 32) << 16);
+        for (int col = 0; col < p.BN; col += 32) {
+            uint32_t v[32];
+            const int n = min(32, p.BN - col);
+            if (direct && own) {
+                if (n == 32) ptx::tmem_ld32(tb + col, v);
+                else ptx::tmem_ld16(tb + col, v);
+                ptx::tmem_ld_wait();
+            } else {
+#pragma unroll
+                for (int q = 0; q < 32; ++q) v[q] = 0u;
+            }
+            if (r < R.rows) {
+                const int64_t row = R.row0 + r;
+                const int gcol = R.nt * p.BN + col;
+                float4 *ap = reinterpret_cast<float4 *>(p.acc + row * p.ld_acc + gcol);
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    if (q * 4 < n) {
+                        const float4 s4 = __ldcg(ap + q);
+                        v[4 * q] = __float_as_uint(to_f(v[4 * q]) + s4.x);
+                        v[4 * q + 1] = __float_as_uint(to_f(v[4 * q + 1]) + s4.y);
+                        v[4 * q + 2] = __float_as_uint(to_f(v[4 * q + 2]) + s4.z);
+                        v[4 * q + 3] = __float_as_uint(to_f(v[4 * q + 3]) + s4.w);
+                        __stcg(ap + q, make_float4(0.f, 0.f, 0.f, 0.f));
+                    }
+                store_row(p, row, gcol, v, n);
+            }
+        }
+    }
+    if (lead) *reinterpret_cast<volatile int *>(ctr) = 0;
+}
+
+// one pipeline stage of the gather: nin slices (offset column, channel chunk) x NBT*RPI*8
+// rows.  lane -> (row r_in of an RPI-row block, 16-byte chunk q_lane); every warp
+// instruction stores whole sectors of RPI rows into the swizzled K-major tile (chunk j of
+// row r lands at j ^ f(r)).  Matched rows: one whole-line request per row; sentinel rows
+// (no input voxel) never touch L2: zeroed with a shared store.
+template <int BK, int NBT>
+__device__ __forceinline__ void gather_slices(const ConvParams &p, const TileRec &R, const int32_t *B, int kd, int rows,
+                                              int sl, int nin, uint32_t abase, uint32_t kb_a, int warp, int r_in,
+                                              int q_lane) {
+    constexpr uint32_t rb = BK * 2;
+    constexpr int RPI = 32 / (BK / 8);
+    constexpr int ROWS_W = NBT * RPI;
+    for (int kb = 0; kb < nin; ++kb) {
+        const int ci = (sl + kb) / p.n_chunks, cc = (sl + kb) - ci * p.n_chunks;
+        const int c = p.mode == 0 ? R.cols[ci] : 0;
+        const uint32_t kbo = kb * kb_a;
+#pragma unroll
+        for (int b = 0; b < NBT; ++b) {
+            const int r = warp * ROWS_W + b * RPI + r_in;
+            const int32_t g = r < rows ? B[r * kd + c] : -1;
+            const uint32_t f = rb == 128 ? (r & 7) : (rb == 64 ? ((r >> 1) & 3) : ((r >> 2) & 1));
+            const uint32_t so = kbo + (uint32_t)r * rb + ((q_lane ^ f) * 16);
+            if (g >= 0)
+                ptx::cp_async_16(abase + so, p.f_in + (int64_t)g * p.ld_in_bytes + cc * rb + q_lane * 16, 16u);
+            else
+                asm volatile("st.shared.v4.b32 [%0], {%1,%1,%1,%1};" ::"r"(abase + so), "r"(0) : "memory");
+        }
+    }
+}
+
+// gather producer warps: per tile, wait for its record and index block, then fill the
+// stages with (offset column, channel chunk) slices; a stage holds up to nkb consecutive
+// slices (several chunks of one offset, or several offsets)
+template <int BK, int NBT>
+__device__ __forceinline__ void gather_role(const ConvParams &p, ConvSmem &cs, const int32_t *blk, int blk_stride, int kd,
+                                            uint8_t *sa, int S, int nkb, uint32_t a_bytes, uint32_t kb_a, int warp,
+                                            int lane) {
+    constexpr int RPI = 32 / (BK / 8);         // rows per warp instruction (4 / 8 / 16)
+    const int r_in = lane % RPI, q_lane = lane / RPI;
+    int s = 0;
+    uint32_t ph = 0;   // stage ring position / phase
+    for (uint32_t ti = 0;; ++ti) {
+        const int st = ti % TREC_SLOTS;
+        ptx::mbar_wait(ptx::smem_u32(&cs.trec_full[st]), (ti / TREC_SLOTS) & 1);
+        const TileRec &R = cs.trec[st];
+        if (R.end) break;
+        const int rows = R.rows, ncols = R.ncols;
+        const int bs = ti % p.blk_slots;
+        ptx::mbar_wait(ptx::smem_u32(&cs.blk_full[bs]), (ti / p.blk_slots) & 1);
+        const int32_t *B = blk + bs * blk_stride;
+        const int nsl = ncols * p.n_chunks;
+        for (int sl = 0; sl < nsl; sl += nkb) {
+            const int nin = min(nkb, nsl - sl);
+            ptx::mbar_wait(ptx::smem_u32(&cs.empty[s]), ph ^ 1);
+            gather_slices<BK, NBT>(p, R, B, kd, rows, sl, nin, ptx::smem_u32(sa + (size_t)s * a_bytes), kb_a, warp, r_in,
+                                   q_lane);
+            ptx::cp_async_mbar_arrive(ptx::smem_u32(&cs.full[s]));
+            if (++s == S) { s = 0; ph ^= 1; }
+        }
+        __syncwarp();
+        if (lane == 0) {
+            ptx::mbar_arrive(ptx::smem_u32(&cs.blk_empty[bs]));
+            ptx::mbar_arrive(ptx::smem_u32(&cs.trec_empty[st]));
+        }
+    }
+    ptx::cp_async_wait<0>();
+}
+
+// epilogue warps (8-11, thread = TMEM lane = tile row): TMEM -> OS: plain stores (final
+// dtype, fused residual, or fp32 accumulator) / WS: red.global.add.v4.f32 scatter;
+// FIX: OS split tiles go through the split-K fixup instead
+template <bool FIX>
+__device__ __forceinline__ void epi_role(const ConvParams &p, ConvSmem &cs, uint32_t tmem_base, int tr, int split, int nht,
+                                         int NH, int warp, int lane) {
+    const int e = warp - W_EPI0;   // == warp % 4: the TMEM lane quadrant this warp may access
+    for (uint32_t ti = 0;; ++ti) {
+        const int st = ti % TREC_SLOTS;
+        ptx::mbar_wait_sleep(ptx::smem_u32(&cs.trec_full[st]), (ti / TREC_SLOTS) & 1);
+        const TileRec &R = cs.trec[st];
+        if (R.end) break;
+        const uint32_t a = ti & 1;
+        const int nt = R.nt;
+        ptx::mbar_wait_sleep(ptx::smem_u32(&cs.tfull[a]), (ti >> 1) & 1);
+        if (threadIdx.x == 32 * W_EPI0) TR(6, ti);
+        ptx::tc_fence_after();
+        if (FIX) {
+            os_split_fixup(p, cs, R, ti, tr, split, nht, tmem_base + a * NH * p.tmem_cols, e, lane);
+        } else {
+#pragma unroll 1
+            for (int h = 0; h < nht; ++h) {
+                const int r = h * TC_BM + e * 32 + lane;
+                int64_t orow = -1;
+                if (r < R.rows && R.ncols > 0) orow = p.mode == 0 ? R.row0 + r : (int64_t)R.scatter[r];
+                const uint32_t tbase = tmem_base + (a * NH + h) * p.tmem_cols + ((uint32_t)(e * 32) << 16);
+                for (int col = 0; col < p.BN; col += 32) {
+                    uint32_t vals[32];
+                    const int n = min(32, p.BN - col);
+                    if (n == 32) ptx::tmem_ld32(tbase + col, vals);
+                    else ptx::tmem_ld16(tbase + col, vals);
+                    ptx::tmem_ld_wait();
+                    if (orow >= 0) {
+                        const int gcol = nt * p.BN + col;
+                        if (p.out_kind == OUT_F32_RED) {
+                            float *op = static_cast<float *>(p.out) + orow * p.ld_out + gcol;
+#pragma unroll
+                            for (int q = 0; q < 8; ++q)
+                                if (q * 4 < n)
+                                    ptx::red_add_v4(op + 4 * q, to_f(vals[4 * q]), to_f(vals[4 * q + 1]),
+                                                    to_f(vals[4 * q + 2]), to_f(vals[4 * q + 3]));
+                        } else {
+                            store_row(p, orow, gcol, vals, n);
+                        }
+                    }
+                }
+            }
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (threadIdx.x == 32 * W_EPI0) TR(7, ti);
+        if (lane == 0) {
+            ptx::mbar_arrive(ptx::smem_u32(&cs.tempty[a]));
+            ptx::mbar_arrive(ptx::smem_u32(&cs.trec_empty[st]));
+        }
+    }
+}
+
 template <int BK, int BM>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant__ ConvParams p) {
     constexpr int NH = BM / TC_BM;   // 128-row MMA halves per tile
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // stage buffers need 1024-byte alignment (swizzle atoms)
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const int S = p.stages;
-    uint8_t *sa = smem;
-    uint8_t *sb = smem + (size_t)S * p.a_bytes;
-    ConvSmem &cs = *reinterpret_cast<ConvSmem *>(sb + (size_t)S * p.b_bytes);
+    // layout: [ring: S x A stage][S x B stage] ... [ConvSmem][gather-index blocks]; the ring
+    // is carved per tile height below, the header sits after the largest carve
+    ConvSmem &cs = *reinterpret_cast<ConvSmem *>(smem + p.hdr_off);
     // gather-index blocks: OS: the tile's [rows x k_dense] slice of the OS table (one bulk
     // copy per tile); WS: the 128 gather indices of the tile's pairs
     const int kd = p.mode == 0 ? p.k_dense : 1;
-    int32_t *blk = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(&cs) + ((sizeof(ConvSmem) + 127) & ~size_t(127)));
+    int32_t *blk = reinterpret_cast<int32_t *>(smem + p.hdr_off + ((sizeof(ConvSmem) + 127) & ~size_t(127)));
     const int blk_stride = (BM * kd + 3) & ~3;      // int32 per block (16-byte multiple)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t n_out = dev_count(p.n_out_cap, p.n_out_dev);
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < S; ++s) {
+        for (int s = 0; s < 16; ++s) {
             ptx::mbar_init(ptx::smem_u32(&cs.full[s]), N_GATHER * 32 + 1);   // gather threads + weight expect_tx
             ptx::mbar_init(ptx::smem_u32(&cs.empty[s]), 1);
         }
@@ -268,25 +496,57 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         ptx::fence_proxy_async();
     }
     if (warp == W_MMA) ptx::tmem_alloc(ptx::smem_u32(cs.tmem_holder), 2 * NH * p.tmem_cols);
-    if (p.mode == 1 && warp == W_SCHED) {
-        // virtual-tile prefix over the WS lists (device-side counts, no host sync)
-        int carry = 0;
-        for (int base = 0; base < p.n_lists; base += 32) {
-            const int l = base + lane;
-            int v = 0;
-            if (l < p.n_lists) {
-                const int cnt = p.counts[SPC_MAX_KVOL + l];
-                v = ((cnt + BM - 1) / BM) * (p.list_mirror[l] ? 2 : 1);
+    if (warp == W_SCHED) {
+        // tile geometry from the live (device-side) counts, no host sync: 256-row tiles
+        // only when they still give >= 2 tiles per SM, else 128-row tiles; an OS part
+        // with fewer 128-row tiles than SMs splits each tile's offsets over CTAs
+        // (split-K, reduced in the epilogue fixup below)
+        if (p.mode == 0) {
+            int tr = BM;
+            if (BM == 256 && ((n_out + 255) / 256) * p.n_ntiles < 2 * p.num_sms) tr = 128;
+            if (p.force_tr) tr = min(p.force_tr, BM);
+            const int64_t rt = (n_out + tr - 1) / tr;
+            int split = 1;
+            if (p.split_ok && rt * p.n_ntiles < p.num_sms && p.k_dense >= 4)
+                split = (int)imin64(p.num_sms / (rt * p.n_ntiles), p.k_dense / 2);
+            if (split < 1) split = 1;
+            if (lane == 0) {
+                cs.tr = tr;
+                cs.split = split;
+                cs.n_tiles = rt * split * p.n_ntiles;
             }
-            int x = v;
-            for (int o = 1; o < 32; o <<= 1) {
-                int y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
+        } else {
+            // virtual-tile prefix over the WS lists
+            auto scan = [&](int tr, bool write) {
+                int carry = 0;
+                for (int base = 0; base < p.n_lists; base += 32) {
+                    const int l = base + lane;
+                    int v = 0;
+                    if (l < p.n_lists) {
+                        const int cnt = p.counts[SPC_MAX_KVOL + l];
+                        v = ((cnt + tr - 1) / tr) * (p.list_mirror[l] ? 2 : 1);
+                    }
+                    int x = v;
+                    for (int o = 1; o < 32; o <<= 1) {
+                        int y = __shfl_up_sync(0xffffffffu, x, o);
+                        if (lane >= o) x += y;
+                    }
+                    if (write && l < p.n_lists) cs.list_prefix[l] = carry + x - v;
+                    carry += __shfl_sync(0xffffffffu, x, 31);
+                }
+                return carry;
+            };
+            int tr = BM;
+            if (BM == 256 && (int64_t)scan(256, false) * p.n_ntiles < 2 * p.num_sms) tr = 128;
+            if (p.force_tr) tr = min(p.force_tr, BM);
+            const int total = scan(tr, true);
+            if (lane == 0) {
+                cs.list_prefix[p.n_lists] = total;
+                cs.tr = tr;
+                cs.split = 1;
+                cs.n_tiles = (int64_t)total * p.n_ntiles;
             }
-            if (l < p.n_lists) cs.list_prefix[l] = carry + x - v;
-            carry += __shfl_sync(0xffffffffu, x, 31);
         }
-        if (lane == 0) cs.list_prefix[p.n_lists] = carry;
         __syncwarp();
     }
     ptx::tc_fence_before();
@@ -294,12 +554,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     ptx::tc_fence_after();
     const uint32_t tmem_base = cs.tmem_holder[0];
     constexpr uint32_t rb = BK * 2;           // bytes per operand row (= swizzle span)
+    const int tr = cs.tr, split = cs.split, nht = tr / TC_BM;
+    // the ring carve of this tile height
+#ifdef SPC_EXP_RG0
+    const int rgi = 0;
+#else
+    const int rgi = (BM == 256 && tr == 128) ? 1 : 0;
+#endif
+    const int S = p.ring[rgi].stages, nkb = p.ring[rgi].nkb;
+    const uint32_t kb_a = p.ring[rgi].kb_a, a_bytes = p.ring[rgi].a_bytes, b_bytes = p.ring[rgi].b_bytes;
+    uint8_t *sa = smem;
+    uint8_t *sb = sa + (size_t)S * a_bytes;
 
     if (warp == W_SCHED) {
         // ===================== scheduler: tile records + gather indices ==================
-        int64_t n_tiles;
-        if (p.mode == 0) n_tiles = ((n_out + BM - 1) / BM) * p.os_split * p.n_ntiles;
-        else n_tiles = (int64_t)cs.list_prefix[p.n_lists] * p.n_ntiles;
+        const int64_t n_tiles = cs.n_tiles;
         uint32_t ti = 0;
         for (int64_t v = blockIdx.x;; v += gridDim.x, ++ti) {
             const int st = ti % TREC_SLOTS;
@@ -311,14 +580,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                 break;
             }
             TileInfo t;
-            decode_tile(p, v, cs.list_prefix, n_out, t);
+            decode_tile(p, v, cs.list_prefix, n_out, tr, split, t);
             if (lane == 0) {
                 R.row0 = t.row0; R.rows = t.rows; R.nt = t.nt; R.list = t.list; R.dir = t.dir; R.k = t.k; R.end = 0;
                 for (int w = 0; w < 4; ++w) R.mask[w] = t.mask[w];
                 int nc = 0;
                 for (int c = next_bit(t.mask, 0); c >= 0; c = next_bit(t.mask, c + 1)) R.cols[nc++] = (uint8_t)c;
-                if (p.mode == 0 && p.os_split > 1) {   // keep this split's contiguous share
-                    const int per = (nc + p.os_split - 1) / p.os_split;
+                if (p.mode == 0 && split > 1) {   // keep this split's contiguous share
+                    const int per = (nc + split - 1) / split;
                     const int c0 = min(nc, t.list * per), c1 = min(nc, c0 + per);
                     for (int q = c0; q < c1; ++q) R.cols[q - c0] = R.cols[q];
                     nc = c1 - c0;
@@ -351,62 +620,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         }
         ptx::cp_async_wait<0>();
     } else if (warp < N_GATHER) {
-        // ===================== gather producers (cp.async, 8 warps x 16 rows) ============
-        // lane -> (row r_in of an RPI-row block, 16-byte chunk q_lane); every warp
-        // instruction stores whole sectors of RPI rows into the swizzled K-major tile
-        // (chunk j of row r lands at j ^ f(r)), 4 shared wavefronts per 512 bytes.
-        constexpr int NQ = BK / 8;                 // 16-byte chunks per row segment
-        constexpr int Q = NQ;                      // chunks per warp instruction (whole rows)
-        constexpr int RPI = 32 / Q;                // rows per warp instruction (4 / 8 / 16)
-        constexpr int ROWS_W = BM / N_GATHER;      // rows per warp (16 or 32)
-        constexpr int NB = ROWS_W / RPI;           // row blocks per warp
-        const int r_in = lane % RPI, q_lane = lane / RPI;
-        int s = 0;
-        uint32_t ph = 0;   // stage ring position / phase
-        for (uint32_t ti = 0;; ++ti) {
-            const int st = ti % TREC_SLOTS;
-            ptx::mbar_wait(ptx::smem_u32(&cs.trec_full[st]), (ti / TREC_SLOTS) & 1);
-            const TileRec &R = cs.trec[st];
-            if (R.end) break;
-            const int rows = R.rows, ncols = R.ncols;
-            const int bs = ti % p.blk_slots;
-            ptx::mbar_wait(ptx::smem_u32(&cs.blk_full[bs]), (ti / p.blk_slots) & 1);
-            const int32_t *B = blk + bs * blk_stride;
-            // flat sequence of (offset column, channel chunk) slices; a stage holds up to
-            // p.nkb consecutive slices (several chunks of one offset, or several offsets)
-            const int nsl = ncols * p.n_chunks;
-            for (int sl = 0; sl < nsl; sl += p.nkb) {
-                const int nin = min(p.nkb, nsl - sl);
-                ptx::mbar_wait(ptx::smem_u32(&cs.empty[s]), ph ^ 1);
-                const uint32_t abase = ptx::smem_u32(sa + (size_t)s * p.a_bytes);
-                for (int kb = 0; kb < nin; ++kb) {
-                    const int ci = (sl + kb) / p.n_chunks, cc = (sl + kb) - ci * p.n_chunks;
-                    const int c = p.mode == 0 ? R.cols[ci] : 0;
-                    const uint32_t kbo = kb * p.kb_a;
-#pragma unroll
-                    for (int b = 0; b < NB; ++b) {
-                        const int r = warp * ROWS_W + b * RPI + r_in;
-                        const int32_t g = r < rows ? B[r * kd + c] : -1;
-                        const uint32_t f = rb == 128 ? (r & 7) : (rb == 64 ? ((r >> 1) & 3) : ((r >> 2) & 1));
-                        const uint32_t so = kbo + (uint32_t)r * rb + ((q_lane ^ f) * 16);
-                        // matched rows: one whole-line request per row; sentinel rows (no input
-                        // voxel) never touch L2: zero them with a shared store
-                        if (g >= 0)
-                            ptx::cp_async_16(abase + so, p.f_in + (int64_t)g * p.ld_in_bytes + cc * rb + q_lane * 16, 16u);
-                        else
-                            asm volatile("st.shared.v4.b32 [%0], {%1,%1,%1,%1};" ::"r"(abase + so), "r"(0) : "memory");
-                    }
-                }
-                ptx::cp_async_mbar_arrive(ptx::smem_u32(&cs.full[s]));
-                if (++s == S) { s = 0; ph ^= 1; }
-            }
-            __syncwarp();
-            if (lane == 0) {
-                ptx::mbar_arrive(ptx::smem_u32(&cs.blk_empty[bs]));
-                ptx::mbar_arrive(ptx::smem_u32(&cs.trec_empty[st]));
-            }
-        }
-        ptx::cp_async_wait<0>();
+        // ===================== gather producers (cp.async, 8 warps) =====================
+        // one loop per tile height (row blocks per warp fixed at compile time)
+        constexpr int NB = BM / N_GATHER / (32 / (BK / 8));
+        if (NB > 1 && tr < BM)
+            gather_role<BK, (NB > 1 ? NB / 2 : 1)>(p, cs, blk, blk_stride, kd, sa, S, nkb, a_bytes, kb_a, warp, lane);
+        else
+            gather_role<BK, NB>(p, cs, blk, blk_stride, kd, sa, S, nkb, a_bytes, kb_a, warp, lane);
     } else if (warp == W_BLOAD) {
         // ===================== weight loader (1-D bulk copies, TMA engine) ===============
         uint32_t it = 0;
@@ -418,8 +638,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             if (lane == 0) {
                 const int nt = R.nt, kfix = R.k, ncols = R.ncols;
                 const int nsl = ncols * p.n_chunks;
-                for (int sl = 0; sl < nsl; sl += p.nkb, ++it) {
-                    const int nin = min(p.nkb, nsl - sl);
+                for (int sl = 0; sl < nsl; sl += nkb, ++it) {
+                    const int nin = min(nkb, nsl - sl);
                     const int s = it % S;
                     ptx::mbar_wait(ptx::smem_u32(&cs.empty[s]), ((it / S) & 1) ^ 1);
                     const uint32_t fb = ptx::smem_u32(&cs.full[s]);
@@ -428,7 +648,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                         const int ci = (sl + kb) / p.n_chunks, cc = (sl + kb) - ci * p.n_chunks;
                         const int k = p.mode == 0 ? p.dense_k[R.cols[ci]] : kfix;
                         const int64_t blob = ((int64_t)k * p.n_ntiles + nt) * p.n_chunks + cc;
-                        ptx::bulk_g2s(ptx::smem_u32(sb + (size_t)s * p.b_bytes + kb * p.kb_b), p.wblob + blob * p.kb_b,
+                        ptx::bulk_g2s(ptx::smem_u32(sb + (size_t)s * b_bytes + kb * p.kb_b), p.wblob + blob * p.kb_b,
                                       p.kb_b, fb);
                     }
                 }
@@ -452,8 +672,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                 const uint32_t d_tmem = tmem_base + a * NH * p.tmem_cols;
                 uint32_t acc = 0;
                 const int nsl = ncols * p.n_chunks;
-                for (int sl = 0; sl < nsl; sl += p.nkb, ++it) {
-                    const int nin = min(p.nkb, nsl - sl);
+                for (int sl = 0; sl < nsl; sl += nkb, ++it) {
+                    const int nin = min(nkb, nsl - sl);
                     const int s = it % S;
                     ptx::mbar_wait(ptx::smem_u32(&cs.full[s]), (it / S) & 1);
                     TR(2, it);
@@ -461,16 +681,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                     // before the tensor core's async-proxy reads
                     ptx::fence_proxy_async();
                     ptx::tc_fence_after();
-                    const uint32_t a_base = ptx::smem_u32(sa + (size_t)s * p.a_bytes);
-                    const uint32_t b_base = ptx::smem_u32(sb + (size_t)s * p.b_bytes);
+                    const uint32_t a_base = ptx::smem_u32(sa + (size_t)s * a_bytes);
+                    const uint32_t b_base = ptx::smem_u32(sb + (size_t)s * b_bytes);
                     for (int kb = 0; kb < nin; ++kb) {
 #pragma unroll
                         for (int kk = 0; kk < BK / 16; ++kk) {
                             const uint64_t bd = ptx::umma_desc_kmajor_sw(b_base + kb * p.kb_b + kk * 32, rb);
 #pragma unroll
                             for (int h = 0; h < NH; ++h) {
+#ifndef SPC_EXP_NOBRK
+                                if (h >= nht) break;
+#endif
                                 const uint64_t ad =
-                                    ptx::umma_desc_kmajor_sw(a_base + kb * p.kb_a + h * TC_BM * rb + kk * 32, rb);
+                                    ptx::umma_desc_kmajor_sw(a_base + kb * kb_a + h * TC_BM * rb + kk * 32, rb);
                                 ptx::mma_f16_ss(d_tmem + h * p.tmem_cols, ad, bd, p.idesc, acc);
                             }
                             acc = 1;
@@ -486,52 +709,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         }
     } else if (warp >= W_EPI0 && warp < W_EPI0 + 4) {
         // ===================== epilogue (warps 8-11, thread = TMEM lane = tile row) ====
-        const int e = warp - W_EPI0;   // == warp % 4: the TMEM lane quadrant this warp may access
-        for (uint32_t ti = 0;; ++ti) {
-            const int st = ti % TREC_SLOTS;
-            ptx::mbar_wait_sleep(ptx::smem_u32(&cs.trec_full[st]), (ti / TREC_SLOTS) & 1);
-            const TileRec &R = cs.trec[st];
-            if (R.end) break;
-            const uint32_t a = ti & 1;
-            const int nt = R.nt;
-            ptx::mbar_wait_sleep(ptx::smem_u32(&cs.tfull[a]), (ti >> 1) & 1);
-            if (threadIdx.x == 32 * W_EPI0) TR(6, ti);
-            ptx::tc_fence_after();
-#pragma unroll 1
-            for (int h = 0; h < NH; ++h) {
-                const int r = h * TC_BM + e * 32 + lane;
-                int64_t orow = -1;
-                if (r < R.rows && R.ncols > 0) orow = p.mode == 0 ? R.row0 + r : (int64_t)R.scatter[r];
-                const uint32_t tbase = tmem_base + (a * NH + h) * p.tmem_cols + ((uint32_t)(e * 32) << 16);
-                for (int col = 0; col < p.BN; col += 32) {
-                    uint32_t vals[32];
-                    const int n = min(32, p.BN - col);
-                    if (n == 32) ptx::tmem_ld32(tbase + col, vals);
-                    else ptx::tmem_ld16(tbase + col, vals);
-                    ptx::tmem_ld_wait();
-                    if (orow >= 0) {
-                        const int gcol = nt * p.BN + col;
-                        if (p.out_kind == OUT_F32_RED) {
-                            float *op = static_cast<float *>(p.out) + orow * p.ld_out + gcol;
-#pragma unroll
-                            for (int q = 0; q < 8; ++q)
-                                if (q * 4 < n)
-                                    ptx::red_add_v4(op + 4 * q, to_f(vals[4 * q]), to_f(vals[4 * q + 1]),
-                                                    to_f(vals[4 * q + 2]), to_f(vals[4 * q + 3]));
-                        } else {
-                            store_row(p, orow, gcol, vals, n);
-                        }
-                    }
-                }
-            }
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (threadIdx.x == 32 * W_EPI0) TR(7, ti);
-            if (lane == 0) {
-                ptx::mbar_arrive(ptx::smem_u32(&cs.tempty[a]));
-                ptx::mbar_arrive(ptx::smem_u32(&cs.trec_empty[st]));
-            }
-        }
+        if (p.mode == 0 && split > 1)
+            epi_role<true>(p, cs, tmem_base, tr, split, nht, NH, warp, lane);
+        else
+            epi_role<false>(p, cs, tmem_base, tr, split, nht, NH, warp, lane);
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -683,17 +864,22 @@ __global__ void k_prepare_weight_tc(const uint16_t *__restrict__ w, int k_vol, i
 }
 
 // fp32 accumulator -> output dtype (+ residual): 8 columns per thread, 16/32-byte accesses
-__global__ void k_convert(const float *__restrict__ acc, int64_t ld_acc, int64_t n_cap, const int64_t *n_dev, int c_out,
+// clear != 0: the accumulator rows are returned to zero after the read (workspace invariant)
+__global__ void k_convert(float *__restrict__ acc, int64_t ld_acc, int64_t n_cap, const int64_t *n_dev, int c_out,
                           int out_dtype, void *__restrict__ out, int64_t ld_out, const void *__restrict__ res,
-                          int64_t ld_res) {
+                          int64_t ld_res, int clear) {
     const int64_t n = dev_count(n_cap, n_dev);
     const int g8 = c_out / 8;                 // c_out is a multiple of 16
     const int64_t total = n * g8;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t r = e / g8;
         const int c = (int)(e - r * g8) * 8;
-        const float4 a0 = *reinterpret_cast<const float4 *>(acc + r * ld_acc + c);
-        const float4 a1 = *reinterpret_cast<const float4 *>(acc + r * ld_acc + c + 4);
+        float4 *ap = reinterpret_cast<float4 *>(acc + r * ld_acc + c);
+        const float4 a0 = ap[0], a1 = ap[1];
+        if (clear) {
+            ap[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+            ap[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
         float v[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
         if (out_dtype == SPC_F32) {
             if (res) {
@@ -776,10 +962,13 @@ extern "C" spc_status spc_prepare_weight(const void *weight, int32_t k_vol, int3
     return SPC_OK;
 }
 
+// ws layout: [fp32 accumulator n_out x c_out][256 int32 tile arrival counters]; both
+// all-zero on entry and left all-zero on return (spc.h)
+static constexpr size_t WS_CTR_BYTES = 1024;
 extern "C" size_t spc_conv_workspace_size(const spc_kmap *km, int32_t c_out, int32_t out_dtype) {
     if (!km || c_out <= 0) return 0;
     (void)out_dtype;
-    return align_up((size_t)km->n_out * c_out * 4, 256) + 256;
+    return align_up((size_t)km->n_out * c_out * 4, 256) + WS_CTR_BYTES;
 }
 
 static void fill_map_params(ConvParams &p, const spc_kmap *km) {
@@ -837,19 +1026,29 @@ static spc_status launch_tc(const ConvParams &p0, int mode, int out_kind, void *
     p.out_kind = out_kind;
     p.out = out;
     p.ld_out = ld_out;
-    const size_t stage = (size_t)p.a_bytes + p.b_bytes;
     const int kd = mode == 0 ? p.k_dense : 1;
     const size_t blk_bytes = (size_t)((p.bm * kd + 3) & ~3) * 4;
     p.blk_slots = 2 * blk_bytes <= 64 * 1024 ? 2 : 1;
-    const size_t extra = ((sizeof(ConvSmem) + 127) & ~size_t(127)) + (size_t)p.blk_slots * blk_bytes + 1024 + 64;
-    int S = (int)((TC_SMEM_BUDGET - extra) / stage);
-#ifndef SPC_MAX_STAGES
-#define SPC_MAX_STAGES 16
-#endif
-    if (S > SPC_MAX_STAGES) S = SPC_MAX_STAGES;
-    if (S < 2) return fail(SPC_ERR_UNSUPPORTED, "spc_conv_forward: tile does not fit shared memory");
-    p.stages = S;
-    const size_t smem = stage * S + extra;
+    const size_t header = align_up(sizeof(ConvSmem), 128) + (size_t)p.blk_slots * blk_bytes;
+    const size_t avail = TC_SMEM_BUDGET - 1024 - header;   // 1024: alignment slack of the dynamic smem base
+    // slices (one BK-channel chunk of one offset) per pipeline stage: a stage carries up
+    // to ~72 KB so narrow layers pack several offsets into one stage
+    static const size_t stage_cap = getenv("SPC_STAGE_KB") ? (size_t)atoi(getenv("SPC_STAGE_KB")) * 1024 : 72 * 1024;
+    size_t ring_bytes = 0;
+    for (int g = 0; g < 2; ++g) {
+        const int rows = g == 0 ? p.bm : TC_BM;
+        ConvParams::Ring &R = p.ring[g];
+        R.kb_a = (uint32_t)(rows * p.BK * 2);
+        R.nkb = (int)std::max<size_t>(1, std::min<size_t>(8, stage_cap / (R.kb_a + p.kb_b)));
+        if (getenv("SPC_NKB1")) R.nkb = 1;
+        R.a_bytes = R.nkb * R.kb_a;
+        R.b_bytes = R.nkb * p.kb_b;
+        R.stages = (int)std::min<size_t>(16, avail / (R.a_bytes + R.b_bytes));
+        if (R.stages < 2) return fail(SPC_ERR_UNSUPPORTED, "spc_conv_forward: tile does not fit shared memory");
+        ring_bytes = std::max(ring_bytes, (size_t)R.stages * (R.a_bytes + R.b_bytes));
+    }
+    p.hdr_off = (uint32_t)align_up(ring_bytes, 128);
+    const size_t smem = 1024 + p.hdr_off + header;
     static bool configured = false;
     if (!configured) {
         SPC_CUDA(cudaFuncSetAttribute(k_conv_tc<16, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BUDGET));
@@ -860,8 +1059,10 @@ static spc_status launch_tc(const ConvParams &p0, int mode, int out_kind, void *
         SPC_CUDA(cudaFuncSetAttribute(k_conv_tc<64, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BUDGET));
         configured = true;
     }
-    // persistent: one CTA per SM (the WS tile count lives on the device)
-    int64_t tiles_cap = mode == 0 ? ((p.n_out_cap + p.bm - 1) / p.bm) * p.os_split * p.n_ntiles : (int64_t)num_sms();
+    // persistent: one CTA per SM (tile geometry and counts live on the device)
+    const int64_t tiles_cap = mode == 0 ? ((p.n_out_cap + TC_BM - 1) / TC_BM) * p.n_ntiles *
+                                              (p.split_ok ? std::max(1, p.k_dense / 2) : 1)
+                                        : (int64_t)num_sms();
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles_cap, num_sms()));
     if (p.bm == 256) {
         if (p.BK == 64) k_conv_tc<64, 256><<<grid, TC_THREADS, smem, st>>>(p);
@@ -932,7 +1133,7 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
             k_conv_simt<<<dim3((unsigned)((km->n_out + SM_TM - 1) / SM_TM), gy), block, 0, st>>>(
                 q, static_cast<const float *>(weight), c_in, c_out);
             SPC_LAUNCH_CHECK("k_conv_simt os");
-        } else if (has_ws) {
+        } else if (has_ws && acc == f_out) {
             k_zero_rows<<<1024, 256, 0, st>>>(acc, ld_acc, km->n_out, km->n_out_dev, c_out);
         }
         if (has_ws) {
@@ -948,7 +1149,7 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
             if (acc != f_out) {
                 const int64_t work = km->n_out * (c_out / 8);
                 k_convert<<<(unsigned)std::min<int64_t>((work + 255) / 256, 8 * 148), 256, 0, st>>>(
-                    acc, ld_acc, km->n_out, km->n_out_dev, c_out, out_dtype, f_out, ld_out, residual, ld_res);
+                    acc, ld_acc, km->n_out, km->n_out_dev, c_out, out_dtype, f_out, ld_out, residual, ld_res, 1);
                 SPC_LAUNCH_CHECK("k_convert");
             }
         }
@@ -963,65 +1164,48 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
     p.n_chunks = c_in / p.BK;
     p.n_ntiles = c_out / p.BN;
     p.tmem_cols = pow2_cols(p.BN);
-    // 256-row tiles (two MMAs per weight tile) whenever four accumulators fit TMEM
+    p.num_sms = num_sms();
+    p.force_tr = getenv("SPC_TR") ? atoi(getenv("SPC_TR")) : 0;
+    // 256-row tiles (two MMAs per weight tile) whenever four accumulators fit TMEM; the
+    // kernel drops to 128-row tiles on the device when the live row count is small
     p.bm = (4 * p.tmem_cols <= 512 && !getenv("SPC_BM128")) ? 256 : 128;
     if (has_os && (size_t)BLK_SLOTS * p.bm * km->k_dense * 4 > 96 * 1024) p.bm = 128;   // OS index blocks (K=5)
-    // small coordinate levels: 128-row tiles keep more SMs busy
-    if (p.bm == 256 && (km->n_out + 255) / 256 < 2 * num_sms()) p.bm = 128;
-    p.kb_a = (uint32_t)(p.bm * p.BK * 2);
     p.kb_b = (uint32_t)(p.BN * p.BK * 2);
-    // several K-blocks per stage: whole input rows per stage when they fit (fewer steps; the
-    // per-stage cost is mostly fixed), keeping >= 3 stages in shared memory
-    // slices (one BK-channel chunk of one offset) per pipeline stage: a stage carries up
-    // to ~72 KB so narrow layers pack several offsets into one stage
-    static const size_t stage_cap = getenv("SPC_STAGE_KB") ? (size_t)atoi(getenv("SPC_STAGE_KB")) * 1024 : 72 * 1024;
-    p.nkb = (int)std::max<size_t>(1, std::min<size_t>(8, stage_cap / (p.kb_a + p.kb_b)));
-    if (getenv("SPC_NKB1")) p.nkb = 1;
-    p.a_bytes = p.nkb * p.kb_a;
-    p.b_bytes = p.nkb * p.kb_b;
     p.idesc = ptx::umma_idesc_f16(in_dtype == SPC_BF16, TC_BM, p.BN);
     p.wblob = static_cast<const char *>(weight);
-    // small layers: split each OS tile's offsets over several CTAs (reduced with red.add)
-    p.os_split = 1;
+    // workspace: fp32 accumulator + tile counters (zero on entry, zero on return)
+    float *wacc = nullptr;
+    int *wctr = nullptr;
+    if (ws && ws_bytes >= spc_conv_workspace_size(km, c_out, out_dtype)) {
+        wacc = static_cast<float *>(ws);
+        wctr = reinterpret_cast<int *>(static_cast<char *>(ws) + align_up((size_t)km->n_out * c_out * 4, 256));
+    }
+    p.acc = wacc;
+    p.ld_acc = c_out;
+    p.tile_ctr = wctr;
+    if (!has_ws) {
+        // OS only: one launch; small levels split offsets over CTAs with the in-kernel fixup
+        p.split_ok = (wacc && km->k_dense >= 4 && !getenv("SPC_NO_OS_SPLIT")) ? 1 : 0;
+        return launch_tc(p, 0, OUT_FINAL, f_out, ld_out, st);
+    }
+    p.split_ok = 0;
+    if (!acc) return fail(SPC_ERR_WORKSPACE, "spc_conv_forward: ws too small");
     if (has_os) {
-        const int64_t row_tiles = (km->n_out + p.bm - 1) / p.bm * p.n_ntiles;
-        if (row_tiles < num_sms() && km->k_dense >= 4 && !getenv("SPC_NO_OS_SPLIT"))
-            p.os_split = (int)std::max<int64_t>(1, std::min<int64_t>(num_sms() / row_tiles, km->k_dense / 2));
-    }
-    const bool use_acc = has_ws || p.os_split > 1;
-    if (use_acc && !acc) {
-        if (out_dtype == SPC_F32 && !residual) {
-            acc = static_cast<float *>(f_out);
-            ld_acc = ld_out;
-        } else {
-            if (!ws || ws_bytes < spc_conv_workspace_size(km, c_out, out_dtype))
-                return fail(SPC_ERR_WORKSPACE, "spc_conv_forward: ws too small");
-            acc = static_cast<float *>(ws);
-            ld_acc = c_out;
-        }
-    }
-    if (has_os && p.os_split == 1) {
-        spc_status s = has_ws ? launch_tc(p, 0, OUT_F32_STORE, acc, ld_acc, st) : launch_tc(p, 0, OUT_FINAL, f_out, ld_out, st);
+        spc_status s = launch_tc(p, 0, OUT_F32_STORE, acc, ld_acc, st);
         if (s != SPC_OK) return s;
-    } else if (use_acc) {
+    } else if (acc == f_out) {
         k_zero_rows<<<1024, 256, 0, st>>>(acc, ld_acc, km->n_out, km->n_out_dev, c_out);
         SPC_LAUNCH_CHECK("k_zero_rows");
-        if (has_os) {
-            spc_status s = launch_tc(p, 0, OUT_F32_RED, acc, ld_acc, st);
-            if (s != SPC_OK) return s;
-        }
     }
-    if (has_ws) {
+    {
         spc_status s = launch_tc(p, 1, OUT_F32_RED, acc, ld_acc, st);
         if (s != SPC_OK) return s;
     }
-    if (use_acc) {
-        if (acc != f_out) {
-            const int64_t work = km->n_out * (c_out / 8);
-            k_convert<<<(unsigned)std::min<int64_t>((work + 255) / 256, 8 * 148), 256, 0, st>>>(
-                acc, ld_acc, km->n_out, km->n_out_dev, c_out, out_dtype, f_out, ld_out, residual, ld_res);
-            SPC_LAUNCH_CHECK("k_convert");
-        }
+    if (acc != f_out) {
+        const int64_t work = km->n_out * (c_out / 8);
+        k_convert<<<(unsigned)std::min<int64_t>((work + 255) / 256, 8 * 148), 256, 0, st>>>(
+            acc, ld_acc, km->n_out, km->n_out_dev, c_out, out_dtype, f_out, ld_out, residual, ld_res, 1);
+        SPC_LAUNCH_CHECK("k_convert");
     }
     return SPC_OK;
 }

@@ -181,7 +181,7 @@ class SparseNet:
         self.status = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self.sort_ws = torch.empty(int(spc.lib().spc_pack_sort_workspace_size(self.n0)), dtype=torch.uint8,
                                    device=self.dev)
-        self.conv_ws = torch.empty(self.n0 * 256 * 4 + 1024, dtype=torch.uint8, device=self.dev)
+        self.conv_ws = torch.zeros(self.n0 * 256 * 4 + 1024, dtype=torch.uint8, device=self.dev)
         self.netidx = None
         self.maps = None
 

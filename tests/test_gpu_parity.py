@@ -291,6 +291,35 @@ def test_conv_channel_slices():
     assert not got[:, :16].any() and not got[:, 64:].any()
 
 
+def test_conv_split_fixup_and_workspace_invariant():
+    """Small levels split each output tile's offsets over CTAs (in-kernel split-K fixup):
+    every one of repeated calls on one ws matches Eq. (2) (fp32 atomics make the summation
+    order, hence the last bit, run-dependent), and every call (OS split, WS, hybrid;
+    different c_out) leaves the workspace all-zero (spc.h contract)."""
+    coords = synth.make_scan(1, 0)[:3000]
+    spec = _spec_for(coords)
+    keys, _, _ = _pack_sort(coords, spec)
+    c = oracle.sort_coords(coords)[0]
+    ws = torch.zeros(len(c) * 256 * 4 + 4096, dtype=torch.uint8, device=DEV)
+    for t, flags, ci, co in ((-1, 0, 32, 64), (-1, 0, 64, 256), (0, 1, 32, 32), (2, 1, 64, 96), (-1, 1, 16, 128)):
+        km = spc.spc_build_kmap(keys, keys, spec, spc.Geom(3, 1, 1, 1, 0), t, flags)
+        F = synth.make_features(len(c), ci, seed=ci)
+        W = synth.make_weights(27, ci, co, seed=co, nnz_per_out=10)
+        R = synth.make_features(len(c), co, seed=co + 1)
+        Fg = torch.from_numpy(F).to(DEV).bfloat16()
+        Rg = torch.from_numpy(R).to(DEV).bfloat16()
+        Wg = spc.spc_prepare_weight(torch.from_numpy(W).to(DEV).bfloat16())
+        outs = [spc.spc_conv_forward(km, Fg, Wg, ci, co, out_dtype=torch.bfloat16, residual=Rg, ws=ws)
+                for _ in range(3)]
+        torch.cuda.synchronize()
+        assert not ws.any(), (t, ci, co)
+        ref = oracle.conv(c, c, 3, 1, F, W) + R.astype(np.float64)
+        ulp = np.exp2(np.floor(np.log2(np.maximum(np.abs(ref), 1e-30))) - 7)
+        for o in outs:
+            got = o.float().cpu().numpy().astype(np.float64)
+            assert (np.abs(got - ref) <= ulp + 1e-5 * np.abs(ref).max()).all(), (t, ci, co)
+
+
 @pytest.mark.slow
 def test_full_size_c2_sampled_parity():
     """Config C2 (~100k voxels) in the launch configuration bench.py uses: full kernel
