@@ -156,6 +156,10 @@ typedef struct {
 #define SPC_KMAP_HALVE_SYMMETRIC 0x1u /* submanifold: store WS pairs of k < centre only */
 #define SPC_KMAP_CHECK_SORTED 0x2u    /* debug: flag unsorted / duplicate input keys          */
 #define SPC_KMAP_COUNT_SEARCHES 0x4u  /* debug: count binary searches and scan probes        */
+#define SPC_KMAP_DENSITY_ORDER 0x8u   /* OS part: also build a density-ordered copy of the OS
+                                       * table (outputs stably sorted by their match mask) that
+                                       * spc_conv_forward uses: tiles of outputs with similar
+                                       * neighbour patterns skip more empty offset chunks     */
 
 #define SPC_MAX_KVOL 125
 
@@ -171,7 +175,12 @@ typedef struct {
  *           equals that of K^3-1-k by symmetry); counts_dev[SPC_MAX_KVOL + l] = pairs
  *           stored in WS list l.
  * tile_mask_dev (OS): bit c of word [tile*words + c/32] set iff some output of the
- *           128-row tile has a match at dense offset c (empty chunks are skipped). */
+ *           128-row tile has a match at dense offset c (empty chunks are skipped).
+ * os_rows / os_table_ord / tile_mask_ord (SPC_KMAP_DENSITY_ORDER, else NULL): the OS
+ *           table with its rows permuted (row p holds output os_rows[p]; outputs stably
+ *           sorted by the bit mask of their matched dense offsets, the centre column
+ *           excluded) and the tile masks of that order.  Same values as os_table, other
+ *           row order; the feature computation writes row p's result to output os_rows[p]. */
 typedef struct {
     spc_geom geom;
     int32_t t;            /* effective threshold (SPC_T_ALL_OS resolved)            */
@@ -191,6 +200,9 @@ typedef struct {
     int32_t *counts_dev;
     uint32_t *tile_mask_dev;
     unsigned long long *search_stats_dev; /* [2]: binary searches, scan probes (or NULL) */
+    int32_t *os_rows;        /* [n_out] density order -> output index (or NULL)     */
+    int32_t *os_table_ord;   /* [n_out * k_dense] OS table in density order          */
+    uint32_t *tile_mask_ord; /* tile masks of the density order                      */
     int16_t dense_k[SPC_MAX_KVOL];
     int16_t list_k[SPC_MAX_KVOL];
     int8_t list_mirror[SPC_MAX_KVOL];

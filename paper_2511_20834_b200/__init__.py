@@ -24,6 +24,7 @@ SPC_T_ALL_WS = 0
 SPC_KMAP_HALVE_SYMMETRIC = 0x1
 SPC_KMAP_CHECK_SORTED = 0x2
 SPC_KMAP_COUNT_SEARCHES = 0x4
+SPC_KMAP_DENSITY_ORDER = 0x8
 SPC_FLAG_RANGE, SPC_FLAG_DUPLICATE, SPC_FLAG_UNSORTED, SPC_FLAG_CAPACITY = 1, 2, 4, 8
 SPC_MAX_KVOL = 125
 
@@ -71,6 +72,7 @@ class _Kmap(ctypes.Structure):
                 ("in_keys", ctypes.c_void_p), ("out_keys", ctypes.c_void_p),
                 ("os_table", ctypes.c_void_p), ("ws_pairs", ctypes.c_void_p), ("counts_dev", ctypes.c_void_p),
                 ("tile_mask_dev", ctypes.c_void_p), ("search_stats_dev", ctypes.c_void_p),
+                ("os_rows", ctypes.c_void_p), ("os_table_ord", ctypes.c_void_p), ("tile_mask_ord", ctypes.c_void_p),
                 ("dense_k", ctypes.c_int16 * SPC_MAX_KVOL), ("list_k", ctypes.c_int16 * SPC_MAX_KVOL),
                 ("list_mirror", ctypes.c_int8 * SPC_MAX_KVOL)]
 
@@ -255,6 +257,17 @@ class KernelMap:
     def os_table(self) -> torch.Tensor:
         return self._view(self.c.os_table, self.c.n_out * self.c.k_dense, torch.int32).view(self.c.n_out,
                                                                                               self.c.k_dense)
+
+    def density_order(self):
+        """(os_rows [n_out], os_table_ord [n_out, k_dense], tile_mask_ord [tiles, words]) of a
+        map built with SPC_KMAP_DENSITY_ORDER, else None (views of the map buffer)."""
+        if not self.c.os_rows:
+            return None
+        n, kd, w = self.c.n_out, self.c.k_dense, self.c.tile_words
+        tiles = (n + 127) // 128
+        return (self._view(self.c.os_rows, n, torch.int32),
+                self._view(self.c.os_table_ord, n * kd, torch.int32).view(n, kd),
+                self._view(self.c.tile_mask_ord, tiles * w, torch.int32).view(tiles, w))
 
     def counts(self) -> torch.Tensor:
         return self._view(self.c.counts_dev, 2 * SPC_MAX_KVOL, torch.int32)

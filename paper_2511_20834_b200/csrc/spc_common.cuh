@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 
 #include "spc.h"
 
@@ -65,10 +66,36 @@ struct Sizer {
 };
 
 int num_sms();
+bool pdl_enabled();   // programmatic dependent launch (off with SPC_NO_PDL=1)
+
+// Launch with programmatic stream serialisation (PDL): the kernel may start while the
+// previous kernel in the stream drains.  Every kernel launched this way executes
+// pdl_wait() before touching memory another kernel writes, and pdl_trigger() only after
+// that wait, so when a kernel starts its predecessor's predecessor has completed.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // ------------------------------------------------------------------------------------
 // device helpers
 // ------------------------------------------------------------------------------------
+// PDL: wait for the preceding kernel's completion (and memory flush); no-op when the
+// kernel was launched without the attribute
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// PDL: let the next kernel in the stream begin its prologue
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ int64_t dev_count(int64_t cap, const int64_t *n_dev) {
     if (!n_dev) return cap;
     int64_t n = *n_dev;
@@ -101,7 +128,10 @@ spc_status radix_sort(const uint64_t *keys_in, const int32_t *vals_in /*nullable
 namespace spc {
 // network-wide phase 2: spc_build_kmap calls between begin/end are collected and built by
 // one grouped launch (spc_kmap.cu)
-void kmap_defer_begin();
+void kmap_defer_begin(void *order_scratch, size_t order_scratch_bytes);
+size_t kmap_bytes_batched(spc_geom geom, int32_t t, uint32_t flags, int64_t n_out);   // map buffer in a batch
+size_t kmap_order_rows(spc_geom geom, int32_t t, uint32_t flags, int64_t n_out);      // rows it adds to the order sort
+size_t kmap_order_scratch_bytes(int64_t rows);
 void kmap_defer_abort();
 spc_status kmap_defer_end(cudaStream_t st);
 }  // namespace spc

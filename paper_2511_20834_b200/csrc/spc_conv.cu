@@ -41,6 +41,7 @@ struct ConvParams {
     int mode;   // 0 = OS part, 1 = WS part
     // map
     const int32_t *os;
+    const int32_t *os_rows;   // OS density order: table row -> output row (NULL: identity)
     int k_dense;
     const uint32_t *tile_mask;
     int tile_words;
@@ -221,7 +222,7 @@ struct TileRec {
     int rows, nt, list, dir, k, end, ncols;
     uint32_t mask[4];
     uint8_t cols[128];        // active step columns (OS: dense offsets with a match; WS: {0})
-    int32_t scatter[256];     // WS: output row of each pair row (OS: unused)
+    int32_t scatter[256];     // output row of each tile row (WS pairs; OS with os_rows)
 };
 
 struct ConvSmem {
@@ -311,7 +312,7 @@ __device__ __noinline__ void os_split_fixup(const ConvParams &p, ConvSmem &cs, c
                 for (int q = 0; q < 32; ++q) v[q] = 0u;
             }
             if (r < R.rows) {
-                const int64_t row = R.row0 + r;
+                const int64_t row = R.row0 + r;   // accumulator row (tile order)
                 const int gcol = R.nt * p.BN + col;
                 float4 *ap = reinterpret_cast<float4 *>(p.acc + row * p.ld_acc + gcol);
 #pragma unroll
@@ -324,7 +325,7 @@ __device__ __noinline__ void os_split_fixup(const ConvParams &p, ConvSmem &cs, c
                         v[4 * q + 3] = __float_as_uint(to_f(v[4 * q + 3]) + s4.w);
                         __stcg(ap + q, make_float4(0.f, 0.f, 0.f, 0.f));
                     }
-                store_row(p, row, gcol, v, n);
+                store_row(p, p.os_rows ? (int64_t)R.scatter[r] : row, gcol, v, n);
             }
         }
     }
@@ -423,7 +424,8 @@ __device__ __forceinline__ void epi_role(const ConvParams &p, ConvSmem &cs, uint
             for (int h = 0; h < nht; ++h) {
                 const int r = h * TC_BM + e * 32 + lane;
                 int64_t orow = -1;
-                if (r < R.rows && R.ncols > 0) orow = p.mode == 0 ? R.row0 + r : (int64_t)R.scatter[r];
+                if (r < R.rows && R.ncols > 0)
+                    orow = (p.mode == 0 && !p.os_rows) ? R.row0 + r : (int64_t)R.scatter[r];
                 const uint32_t tbase = tmem_base + (a * NH + h) * p.tmem_cols + ((uint32_t)(e * 32) << 16);
                 for (int col = 0; col < p.BN; col += 32) {
                     uint32_t vals[32];
@@ -473,7 +475,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     const int blk_stride = (BM * kd + 3) & ~3;      // int32 per block (16-byte multiple)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t n_out = dev_count(p.n_out_cap, p.n_out_dev);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < 16; ++s) {
@@ -496,6 +497,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         ptx::fence_proxy_async();
     }
     if (warp == W_MMA) ptx::tmem_alloc(ptx::smem_u32(cs.tmem_holder), 2 * NH * p.tmem_cols);
+    // everything above overlaps the previous kernel's tail (PDL); maps, features, weights
+    // and outputs are touched only after this point
+    pdl_wait();
+    pdl_trigger();
+    const int64_t n_out = dev_count(p.n_out_cap, p.n_out_dev);
     if (warp == W_SCHED) {
         // tile geometry from the live (device-side) counts, no host sync: 256-row tiles
         // only when they still give >= 2 tiles per SM, else 128-row tiles; an OS part
@@ -597,6 +603,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             if (p.mode == 1) {
                 const int32_t *pr = reinterpret_cast<const int32_t *>(p.pairs + t.list * p.list_stride + t.row0);
                 for (int r = lane; r < BM; r += 32) R.scatter[r] = r < t.rows ? pr[2 * r + (t.dir ? 0 : 1)] : -1;
+            } else if (p.os_rows) {
+                for (int r = lane; r < tr; r += 32) R.scatter[r] = r < t.rows ? p.os_rows[t.row0 + r] : -1;
             }
             ptx::mbar_arrive(ptx::smem_u32(&cs.trec_full[st]));
             // the tile's gather indices: one contiguous block
@@ -734,6 +742,8 @@ __global__ void __launch_bounds__(256) k_conv_simt(const __grid_constant__ ConvP
     __shared__ int32_t gidx[SM_TM];
     __shared__ int64_t sidx[SM_TM];
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    pdl_wait();
+    pdl_trigger();
     const int64_t n_out = dev_count(p.n_out_cap, p.n_out_dev);
     const int col0 = blockIdx.y * SM_TN;
     int64_t row0;
@@ -771,7 +781,7 @@ __global__ void __launch_bounds__(256) k_conv_simt(const __grid_constant__ ConvP
             if (r < rows) {
                 if (p.mode == 0) {
                     g = p.os[(row0 + r) * p.k_dense + st];
-                    so = row0 + r;
+                    so = p.os_rows ? p.os_rows[row0 + r] : row0 + r;
                 } else {
                     const int2 pr = p.pairs[list * p.list_stride + row0 + r];
                     g = dir ? pr.y : pr.x;
@@ -868,6 +878,8 @@ __global__ void k_prepare_weight_tc(const uint16_t *__restrict__ w, int k_vol, i
 __global__ void k_convert(float *__restrict__ acc, int64_t ld_acc, int64_t n_cap, const int64_t *n_dev, int c_out,
                           int out_dtype, void *__restrict__ out, int64_t ld_out, const void *__restrict__ res,
                           int64_t ld_res, int clear) {
+    pdl_wait();
+    pdl_trigger();
     const int64_t n = dev_count(n_cap, n_dev);
     const int g8 = c_out / 8;                 // c_out is a multiple of 16
     const int64_t total = n * g8;
@@ -910,6 +922,8 @@ __global__ void k_convert(float *__restrict__ acc, int64_t ld_acc, int64_t n_cap
 }
 
 __global__ void k_zero_rows(float *__restrict__ acc, int64_t ld, int64_t n_cap, const int64_t *n_dev, int c) {
+    pdl_wait();
+    pdl_trigger();
     const int64_t n = dev_count(n_cap, n_dev);
     const int64_t total = n * c;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
@@ -972,9 +986,12 @@ extern "C" size_t spc_conv_workspace_size(const spc_kmap *km, int32_t c_out, int
 }
 
 static void fill_map_params(ConvParams &p, const spc_kmap *km) {
-    p.os = km->os_table;
+    // density-ordered OS part when the map has one (SPC_KMAP_DENSITY_ORDER)
+    const bool ord = km->os_rows && km->os_table_ord && km->tile_mask_ord && !getenv("SPC_NO_DENSITY_ORDER");
+    p.os = ord ? km->os_table_ord : km->os_table;
+    p.os_rows = ord ? km->os_rows : nullptr;
     p.k_dense = km->k_dense;
-    p.tile_mask = km->tile_mask_dev;
+    p.tile_mask = ord ? km->tile_mask_ord : km->tile_mask_dev;
     p.tile_words = km->tile_words;
     p.pairs = reinterpret_cast<const int2 *>(km->ws_pairs);
     p.list_stride = km->n_out;
@@ -1064,16 +1081,9 @@ static spc_status launch_tc(const ConvParams &p0, int mode, int out_kind, void *
                                               (p.split_ok ? std::max(1, p.k_dense / 2) : 1)
                                         : (int64_t)num_sms();
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles_cap, num_sms()));
-    if (p.bm == 256) {
-        if (p.BK == 64) k_conv_tc<64, 256><<<grid, TC_THREADS, smem, st>>>(p);
-        else if (p.BK == 32) k_conv_tc<32, 256><<<grid, TC_THREADS, smem, st>>>(p);
-        else k_conv_tc<16, 256><<<grid, TC_THREADS, smem, st>>>(p);
-    } else {
-        if (p.BK == 64) k_conv_tc<64, 128><<<grid, TC_THREADS, smem, st>>>(p);
-        else if (p.BK == 32) k_conv_tc<32, 128><<<grid, TC_THREADS, smem, st>>>(p);
-        else k_conv_tc<16, 128><<<grid, TC_THREADS, smem, st>>>(p);
-    }
-    SPC_LAUNCH_CHECK("k_conv_tc");
+    void (*k)(ConvParams) = p.bm == 256 ? (p.BK == 64 ? k_conv_tc<64, 256> : p.BK == 32 ? k_conv_tc<32, 256> : k_conv_tc<16, 256>)
+                                        : (p.BK == 64 ? k_conv_tc<64, 128> : p.BK == 32 ? k_conv_tc<32, 128> : k_conv_tc<16, 128>);
+    SPC_CUDA(launch_pdl(k, dim3(grid), dim3(TC_THREADS), smem, st, p));
     return SPC_OK;
 }
 
@@ -1130,11 +1140,11 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
             q.out_kind = has_ws ? OUT_F32_STORE : OUT_FINAL;
             q.out = has_ws ? (void *)acc : f_out;
             q.ld_out = has_ws ? ld_acc : ld_out;
-            k_conv_simt<<<dim3((unsigned)((km->n_out + SM_TM - 1) / SM_TM), gy), block, 0, st>>>(
-                q, static_cast<const float *>(weight), c_in, c_out);
+            SPC_CUDA(launch_pdl(k_conv_simt, dim3((unsigned)((km->n_out + SM_TM - 1) / SM_TM), gy), block, 0, st, q,
+                                static_cast<const float *>(weight), (int)c_in, (int)c_out));
             SPC_LAUNCH_CHECK("k_conv_simt os");
         } else if (has_ws && acc == f_out) {
-            k_zero_rows<<<1024, 256, 0, st>>>(acc, ld_acc, km->n_out, km->n_out_dev, c_out);
+            SPC_CUDA(launch_pdl(k_zero_rows, dim3(1024), dim3(256), 0, st, acc, ld_acc, km->n_out, km->n_out_dev, (int)c_out));
         }
         if (has_ws) {
             ConvParams q = p;
@@ -1143,13 +1153,13 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
             q.out = acc;
             q.ld_out = ld_acc;
             const int64_t tiles_per = (km->n_out + SM_TM - 1) / SM_TM;
-            k_conv_simt<<<dim3((unsigned)(tiles_per * 2 * km->n_lists), gy), block, 0, st>>>(
-                q, static_cast<const float *>(weight), c_in, c_out);
+            SPC_CUDA(launch_pdl(k_conv_simt, dim3((unsigned)(tiles_per * 2 * km->n_lists), gy), block, 0, st, q,
+                                static_cast<const float *>(weight), (int)c_in, (int)c_out));
             SPC_LAUNCH_CHECK("k_conv_simt ws");
             if (acc != f_out) {
                 const int64_t work = km->n_out * (c_out / 8);
-                k_convert<<<(unsigned)std::min<int64_t>((work + 255) / 256, 8 * 148), 256, 0, st>>>(
-                    acc, ld_acc, km->n_out, km->n_out_dev, c_out, out_dtype, f_out, ld_out, residual, ld_res, 1);
+                SPC_CUDA(launch_pdl(k_convert, dim3((unsigned)std::min<int64_t>((work + 255) / 256, 8 * 148)), dim3(256), 0, st,
+                    acc, ld_acc, km->n_out, km->n_out_dev, (int)c_out, (int)out_dtype, f_out, ld_out, residual, ld_res, 1));
                 SPC_LAUNCH_CHECK("k_convert");
             }
         }
@@ -1194,7 +1204,7 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
         spc_status s = launch_tc(p, 0, OUT_F32_STORE, acc, ld_acc, st);
         if (s != SPC_OK) return s;
     } else if (acc == f_out) {
-        k_zero_rows<<<1024, 256, 0, st>>>(acc, ld_acc, km->n_out, km->n_out_dev, c_out);
+        SPC_CUDA(launch_pdl(k_zero_rows, dim3(1024), dim3(256), 0, st, acc, ld_acc, km->n_out, km->n_out_dev, (int)c_out));
         SPC_LAUNCH_CHECK("k_zero_rows");
     }
     {
@@ -1203,8 +1213,8 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
     }
     if (acc != f_out) {
         const int64_t work = km->n_out * (c_out / 8);
-        k_convert<<<(unsigned)std::min<int64_t>((work + 255) / 256, 8 * 148), 256, 0, st>>>(
-            acc, ld_acc, km->n_out, km->n_out_dev, c_out, out_dtype, f_out, ld_out, residual, ld_res, 1);
+        SPC_CUDA(launch_pdl(k_convert, dim3((unsigned)std::min<int64_t>((work + 255) / 256, 8 * 148)), dim3(256), 0, st,
+            acc, ld_acc, km->n_out, km->n_out_dev, (int)c_out, (int)out_dtype, f_out, ld_out, residual, ld_res, 1));
         SPC_LAUNCH_CHECK("k_convert");
     }
     return SPC_OK;

@@ -1,3 +1,4 @@
+#include <cstdlib>
 // spc_host.cu -- host-side C ABI of libspc: status plumbing, pack planning, offset and
 // mask helpers, and network-wide voxel indexing (A13, §5.5).
 #include <cuda_runtime.h>
@@ -22,6 +23,12 @@ spc_status fail(spc_status st, const std::string &detail) {
 spc_status cuda_fail(cudaError_t e, const char *what) {
     g_detail = std::string(what) + ": " + cudaGetErrorString(e);
     return SPC_ERR_CUDA;
+}
+
+bool pdl_enabled() {
+    static int on = -1;
+    if (on < 0) on = getenv("SPC_NO_PDL") ? 0 : 1;
+    return on != 0;
 }
 
 int num_sms() {
@@ -148,13 +155,17 @@ extern "C" size_t spc_network_workspace_size(int64_t n0, int32_t n_levels, const
                                              const int32_t *ts, const uint32_t *flags, int32_t n_maps) {
     if (n0 < 0 || n_levels < 1 || n_levels > 5) return 0;
     size_t total = align_up(spc_downsample_workspace_size(n0, n_levels > 1 ? n_levels - 1 : 1), 256);
+    int64_t order_rows = 0;
     for (int i = 0; i < n_maps; ++i) {
         bool dup = false;
         for (int j = 0; j < i; ++j) dup |= same_map(geoms[i], ts[i], flags ? flags[i] : 0, geoms[j], ts[j],
                                                     flags ? flags[j] : 0);
         if (dup) continue;
-        total += align_up(spc_kmap_bytes(geoms[i], ts[i], flags ? flags[i] : 0, n0, n0), 256);
+        total += align_up(kmap_bytes_batched(geoms[i], ts[i], flags ? flags[i] : 0, n0), 256);
+        order_rows += (int64_t)kmap_order_rows(geoms[i], ts[i], flags ? flags[i] : 0, n0);
     }
+    // one density-order sort over all ordered maps (end of the workspace)
+    total += align_up(kmap_order_scratch_bytes(order_rows), 256);
     return total + 256;
 }
 
@@ -187,7 +198,17 @@ extern "C" spc_status spc_network_kmaps(const uint64_t *v0_keys, int64_t n0, con
         if (s != SPC_OK) return s;
     }
     // ---- phase 2: every distinct map, one grouped launch ---------------------------------
-    kmap_defer_begin();
+    int64_t order_rows = 0;
+    size_t maps_bytes = 0;
+    for (int i = 0; i < n_maps; ++i) {
+        const uint32_t fi = flags ? flags[i] : 0;
+        bool dup = false;
+        for (int j = 0; j < i; ++j) dup |= same_map(geoms[i], ts[i], fi, geoms[j], ts[j], flags ? flags[j] : 0);
+        if (dup) continue;
+        maps_bytes += align_up(kmap_bytes_batched(geoms[i], ts[i], fi, n0), 256);
+        order_rows += (int64_t)kmap_order_rows(geoms[i], ts[i], fi, n0);
+    }
+    kmap_defer_begin(base + off + maps_bytes, kmap_order_scratch_bytes(order_rows));
     for (int i = 0; i < n_maps; ++i) {
         const uint32_t fi = flags ? flags[i] : 0;
         int dup = -1;
@@ -203,7 +224,7 @@ extern "C" spc_status spc_network_kmaps(const uint64_t *v0_keys, int64_t n0, con
             kmap_defer_abort();
             return s;
         }
-        const size_t bytes = spc_kmap_bytes(geoms[i], ts[i], fi, n0, n0);
+        const size_t bytes = kmap_bytes_batched(geoms[i], ts[i], fi, n0);
         s = spc_build_kmap(level_keys + (size_t)li * n0, n0, level_n_dev + li, level_keys + (size_t)lo * n0, n0,
                            level_n_dev + lo, spec, geoms[i], ts[i], fi, base + off, bytes, status, &maps_out[i],
                            stream);

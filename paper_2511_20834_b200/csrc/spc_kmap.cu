@@ -288,13 +288,163 @@ __global__ void __launch_bounds__(KM_THREADS) k_kmap_zdelta(const __grid_constan
 }
 
 // ------------------------------------------------------------------------------------
+// density order of the OS part (SPC_KMAP_DENSITY_ORDER): outputs stably sorted by which
+// offset directions they have neighbours in, so a 128-row tile of similar neighbour
+// patterns has fewer non-empty offset chunks and fewer sentinel rows.  Any row order
+// gives the same Eq. (2) result; this one only changes the work per tile.
+// Key of an output: bit cls[c] set iff it matches at dense column c, where cls maps an
+// offset and its mirror (k, K^3-1-k) to one bit (the centre of a submanifold map, always
+// matched, to none), folded onto <= 16 bits.  All ordered maps of a build are sorted
+// together: key = map tag above the mask bits, rows concatenated by live counts.
+// ------------------------------------------------------------------------------------
+constexpr int ORD_MAX = 8;
+struct OrderJob {
+    const int32_t *os;
+    int32_t *os_ord;
+    uint32_t *mask_ord;
+    int32_t *rows;
+    const int64_t *n_dev;
+    int64_t n_cap;
+    int64_t tile0;            // first permute CTA of this map
+    int k_dense, words;
+    int8_t cls[SPC_MAX_KVOL];
+};
+struct OrderBatch {
+    int n_jobs, key_bits;
+    int64_t *total_dev;       // sum of live rows (written by k_ord_keys)
+    uint64_t *keys;
+    OrderJob j[ORD_MAX];
+};
+
+__device__ __forceinline__ int64_t ord_base(const OrderBatch &B, int job, int64_t &n_job) {
+    int64_t base = 0;
+    for (int q = 0; q < job; ++q) base += dev_count(B.j[q].n_cap, B.j[q].n_dev);
+    n_job = dev_count(B.j[job].n_cap, B.j[job].n_dev);
+    return base;
+}
+
+__global__ void k_ord_keys(const __grid_constant__ OrderBatch B) {
+    int64_t base = 0;
+    for (int q = 0; q < B.n_jobs; ++q) {
+        const OrderJob &J = B.j[q];
+        const int64_t n = dev_count(J.n_cap, J.n_dev);
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+            const int32_t *row = J.os + i * J.k_dense;
+            uint32_t m = 0;
+            for (int c = 0; c < J.k_dense; ++c)
+                if (J.cls[c] >= 0 && row[c] >= 0) m |= 1u << J.cls[c];
+            B.keys[base + i] = ((uint64_t)q << B.key_bits) | m;
+        }
+        base += n;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *B.total_dev = base;
+}
+
+// one CTA per 128-row tile of one map: row p of the ordered table = row rows[p] of the
+// canonical one (warp-cooperative row copies), tile mask words by warp ballots
+__global__ void __launch_bounds__(128) k_ord_permute(const __grid_constant__ OrderBatch B,
+                                                     const int32_t *__restrict__ sorted_pos) {
+    __shared__ int32_t src_s[128];
+    __shared__ uint32_t wm[4][4];
+    int job = 0;
+    while (job + 1 < B.n_jobs && B.j[job + 1].tile0 <= blockIdx.x) ++job;
+    const OrderJob &J = B.j[job];
+    int64_t n;
+    const int64_t base = ord_base(B, job, n);
+    const int64_t p0 = (int64_t)(blockIdx.x - J.tile0) * 128;
+    if (p0 >= n) return;
+    const int64_t p = p0 + threadIdx.x;
+    int32_t src = -1;
+    if (p < n) {
+        src = (int32_t)(sorted_pos[base + p] - base);
+        J.rows[p] = src;
+    }
+    src_s[threadIdx.x] = src;
+    __syncthreads();
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t m[4] = {0u, 0u, 0u, 0u};
+    for (int i = 0; i < 32; ++i) {
+        const int r = w * 32 + i;
+        const int32_t sr = src_s[r];
+        if (sr < 0) break;
+        const int32_t *srow = J.os + (int64_t)sr * J.k_dense;
+        int32_t *drow = J.os_ord + (p0 + r) * J.k_dense;
+        for (int c0 = 0, q = 0; c0 < J.k_dense; c0 += 32, ++q) {
+            const int c = c0 + lane;
+            int32_t v = -1;
+            if (c < J.k_dense) {
+                v = srow[c];
+                drow[c] = v;
+            }
+            m[q & 3] |= __ballot_sync(0xffffffffu, v >= 0);
+        }
+    }
+    if (lane == 0)
+        for (int q = 0; q < 4; ++q) wm[w][q] = m[q];
+    __syncthreads();
+    if (threadIdx.x < J.words) {
+        const int q = threadIdx.x;
+        J.mask_ord[(p0 / 128) * J.words + q] = wm[0][q] | wm[1][q] | wm[2][q] | wm[3][q];
+    }
+}
+
+// scratch of one grouped order over `rows_cap` concatenated rows
+static size_t order_scratch_bytes(int64_t rows_cap) {
+    Sizer z;
+    z.take<int64_t>(4);
+    z.take<uint64_t>((size_t)rows_cap);   // keys
+    z.take<uint64_t>((size_t)rows_cap);   // sorted keys
+    z.take<int32_t>((size_t)rows_cap);    // sorted positions
+    return z.used + radix_sort_workspace(rows_cap, true) + 512;
+}
+
+static spc_status run_orders(const std::vector<OrderJob> &jobs, void *scratch, size_t scratch_bytes, cudaStream_t st) {
+    for (size_t j0 = 0; j0 < jobs.size(); j0 += ORD_MAX) {
+        OrderBatch B;
+        memset(&B, 0, sizeof(B));
+        B.n_jobs = (int)std::min<size_t>(ORD_MAX, jobs.size() - j0);
+        int64_t cap = 0, tiles = 0;
+        int bits = 1;
+        for (int q = 0; q < B.n_jobs; ++q) {
+            B.j[q] = jobs[j0 + q];
+            B.j[q].tile0 = tiles;
+            tiles += (B.j[q].n_cap + 127) / 128;
+            cap += B.j[q].n_cap;
+            for (int c = 0; c < B.j[q].k_dense; ++c) bits = std::max(bits, (int)B.j[q].cls[c] + 1);
+        }
+        if (cap == 0) continue;
+        int tag_bits = 0;
+        while ((1 << tag_bits) < B.n_jobs) ++tag_bits;
+        B.key_bits = bits;
+        Bump b(scratch, scratch_bytes);
+        B.total_dev = b.take<int64_t>(4);
+        B.keys = b.take<uint64_t>((size_t)cap);
+        uint64_t *keys_sorted = b.take<uint64_t>((size_t)cap);
+        int32_t *pos = b.take<int32_t>((size_t)cap);
+        const size_t rws = radix_sort_workspace(cap, true);
+        void *rw = b.take<uint8_t>(rws);
+        if (!b.ok()) return fail(SPC_ERR_WORKSPACE, "kernel-map density order: scratch too small");
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((cap + 255) / 256, 4 * (int64_t)num_sms()));
+        k_ord_keys<<<grid, 256, 0, st>>>(B);
+        SPC_LAUNCH_CHECK("k_ord_keys");
+        spc_status s = radix_sort(B.keys, nullptr, cap, B.total_dev, bits + tag_bits, keys_sorted, pos, rw, rws, st,
+                                  false);
+        if (s != SPC_OK) return s;
+        k_ord_permute<<<(unsigned)tiles, 128, 0, st>>>(B, pos);
+        SPC_LAUNCH_CHECK("k_ord_permute");
+    }
+    return SPC_OK;
+}
+
+// ------------------------------------------------------------------------------------
 // host: plan (offset tables, dense/sparse split, lists) and entry points
 // ------------------------------------------------------------------------------------
 struct KmapPlan {
-    int K = 0, r = 0, k_vol = 0, k_dense = 0, n_lists = 0, halved = 0, t_eff = 0, spacing = 1;
+    int K = 0, r = 0, k_vol = 0, k_dense = 0, n_lists = 0, halved = 0, t_eff = 0, spacing = 1, centre_col = -1;
     int16_t dense_k[SPC_MAX_KVOL], list_k[SPC_MAX_KVOL];
     int8_t list_mirror[SPC_MAX_KVOL];
     int16_t dense_col[SPC_MAX_KVOL], list_id[SPC_MAX_KVOL];
+    int8_t ord_cls[SPC_MAX_KVOL];   // density-order key bit of each dense column (-1: none)
     uint8_t group_needed[25];
 };
 
@@ -316,18 +466,38 @@ static spc_status make_plan(const spc_geom &g, int32_t t, uint32_t flags, KmapPl
     pl.halved = (flags & SPC_KMAP_HALVE_SYMMETRIC) && subm ? 1 : 0;
     const int centre = (pl.k_vol - 1) / 2;
     pl.k_dense = pl.n_lists = 0;
+    pl.centre_col = -1;
     for (int k = 0; k < pl.k_vol; ++k) {
         int ex = k / (pl.K * pl.K) - pl.r, ey = (k / pl.K) % pl.K - pl.r, ez = k % pl.K - pl.r;
         int l1 = abs(ex) + abs(ey) + abs(ez);
         pl.dense_col[k] = -1;
         pl.list_id[k] = -1;
         if (l1 < pl.t_eff) {
+            if (subm && k == centre) pl.centre_col = pl.k_dense;   // always matched
             pl.dense_col[k] = (int16_t)pl.k_dense;
             pl.dense_k[pl.k_dense++] = (int16_t)k;
         } else if (!pl.halved || k <= centre) {
             pl.list_id[k] = (int16_t)pl.n_lists;
             pl.list_mirror[pl.n_lists] = (pl.halved && k < centre) ? 1 : 0;
             pl.list_k[pl.n_lists++] = (int16_t)k;
+        }
+    }
+    // density-order key: an offset and its mirror share a bit; the centre of a
+    // submanifold map (always matched) has none; <= 16 bits (classes folded)
+    {
+        int rank[SPC_MAX_KVOL];
+        for (int k = 0; k < pl.k_vol; ++k) rank[k] = -1;
+        int ncls = 0;
+        for (int k = 0; k < pl.k_vol; ++k) {   // ascending pair index min(k, mirror)
+            const int m = pl.k_vol - 1 - k;
+            if (k > m) continue;
+            const bool used = pl.dense_col[k] >= 0 || pl.dense_col[m] >= 0;
+            if (!used || (subm && k == centre)) continue;
+            rank[k] = rank[m] = ncls++;
+        }
+        for (int c = 0; c < pl.k_dense; ++c) {
+            const int r = rank[pl.dense_k[c]];
+            pl.ord_cls[c] = (int8_t)(r < 0 ? -1 : r % 16);
         }
     }
     for (int gi = 0; gi < pl.K * pl.K; ++gi) {
@@ -343,11 +513,16 @@ static spc_status make_plan(const spc_geom &g, int32_t t, uint32_t flags, KmapPl
 
 struct KmapLayout {
     size_t os, pairs, counts, mask, stats, total;
+    size_t rows, os_ord, mask_ord, scratch, scratch_bytes;   // density order
     int64_t tiles;
     int words;
 };
 
-static KmapLayout layout_of(const KmapPlan &pl, int64_t n_out) {
+static bool wants_order(const KmapPlan &pl, uint32_t flags) { return (flags & SPC_KMAP_DENSITY_ORDER) && pl.k_dense >= 2; }
+
+// scratch: include the density-order sort scratch (standalone builds; a network build
+// sorts all its maps together in scratch of its own)
+static KmapLayout layout_of(const KmapPlan &pl, int64_t n_out, uint32_t flags, bool scratch = true) {
     KmapLayout L{};
     L.tiles = (n_out + KM_BM - 1) / KM_BM;
     L.words = (pl.k_dense + 31) / 32;
@@ -358,9 +533,19 @@ static KmapLayout layout_of(const KmapPlan &pl, int64_t n_out) {
     L.counts = take(sizeof(int32_t) * 2 * SPC_MAX_KVOL);
     L.mask = take(sizeof(uint32_t) * (size_t)(L.tiles * L.words));
     L.stats = take(sizeof(unsigned long long) * 2 + 64);   // + a launch work counter
+    if (wants_order(pl, flags)) {
+        L.rows = take(sizeof(int32_t) * (size_t)n_out);
+        L.os_ord = take(sizeof(int32_t) * (size_t)n_out * pl.k_dense);
+        L.mask_ord = take(sizeof(uint32_t) * (size_t)(L.tiles * L.words));
+        if (scratch) {
+            L.scratch_bytes = order_scratch_bytes(n_out);
+            L.scratch = take(L.scratch_bytes);
+        }
+    }
     L.total = align_up(off, 256);
     return L;
 }
+
 
 size_t kmap_smem_bytes(int k_dense) { return (size_t)KM_BM * k_dense * 4 + (size_t)KM_WIN_CAP * 8; }
 
@@ -369,6 +554,9 @@ struct DeferState {
     KmapBatch b;
     int max_kd = 0;
     int64_t tiles = 0;
+    std::vector<OrderJob> orders;
+    void *scratch = nullptr;   // density-order scratch of the batch
+    size_t scratch_bytes = 0;
 };
 static thread_local DeferState g_defer;
 
@@ -422,7 +610,7 @@ extern "C" size_t spc_kmap_bytes(spc_geom geom, int32_t t, uint32_t flags, int64
     KmapPlan pl;
     if (make_plan(geom, t, flags, pl) != SPC_OK || n_out < 0) return 0;
     (void)n_in;
-    return layout_of(pl, n_out).total;
+    return layout_of(pl, n_out, flags).total;
 }
 
 namespace spc {
@@ -441,7 +629,7 @@ extern "C" spc_status spc_build_kmap(const uint64_t *in_keys, int64_t n_in, cons
     KmapPlan pl;
     spc_status s = make_plan(geom, t, flags, pl);
     if (s != SPC_OK) return s;
-    const KmapLayout L = layout_of(pl, n_out);
+    const KmapLayout L = layout_of(pl, n_out, flags, !g_defer.active);
     SPC_CHECK_ARG(buf && ((uintptr_t)buf % 256) == 0, "buf must be non-null and 256-byte aligned");
     if (buf_bytes < L.total) return fail(SPC_ERR_WORKSPACE, "spc_build_kmap: buffer too small");
     // reach check (reading A4): the planner guarantees headroom; here we only refuse
@@ -479,6 +667,23 @@ extern "C" spc_status spc_build_kmap(const uint64_t *in_keys, int64_t n_in, cons
         km.list_k[l] = pl.list_k[l];
         km.list_mirror[l] = pl.list_mirror[l];
     }
+    OrderJob job;
+    memset(&job, 0, sizeof(job));
+    const bool order = wants_order(pl, flags) && n_out > 0;
+    if (order) {
+        km.os_rows = reinterpret_cast<int32_t *>(base + L.rows);
+        km.os_table_ord = reinterpret_cast<int32_t *>(base + L.os_ord);
+        km.tile_mask_ord = reinterpret_cast<uint32_t *>(base + L.mask_ord);
+        job.os = km.os_table;
+        job.os_ord = km.os_table_ord;
+        job.mask_ord = km.tile_mask_ord;
+        job.rows = km.os_rows;
+        job.n_dev = n_out_dev;
+        job.n_cap = n_out;
+        job.k_dense = pl.k_dense;
+        job.words = L.words;
+        for (int c = 0; c < pl.k_dense; ++c) job.cls[c] = pl.ord_cls[c];
+    }
     if (n_out == 0) {
         SPC_CUDA(cudaMemsetAsync(base + L.counts, 0, L.stats + 2 * sizeof(unsigned long long) - L.counts, st));
         return SPC_OK;
@@ -502,6 +707,7 @@ extern "C" spc_status spc_build_kmap(const uint64_t *in_keys, int64_t n_in, cons
         fill_desc(b.d[b.n_maps++], km, pl);
         g_defer.max_kd = std::max(g_defer.max_kd, pl.k_dense);
         g_defer.tiles += (int64_t)L.tiles;
+        if (order) g_defer.orders.push_back(job);
         return SPC_OK;
     }
     KmapBatch b;
@@ -511,21 +717,39 @@ extern "C" spc_status spc_build_kmap(const uint64_t *in_keys, int64_t n_in, cons
     b.bits_z = spec.bits_z;
     b.work_ctr = reinterpret_cast<unsigned int *>(base + L.stats) + 4;   // scratch after the stats
     fill_desc(b.d[0], km, pl);
-    return launch_kmaps(b, pl.k_dense, (int64_t)L.tiles, st);
+    s = launch_kmaps(b, pl.k_dense, (int64_t)L.tiles, st);
+    if (s == SPC_OK && order) s = run_orders(std::vector<OrderJob>{job}, base + L.scratch, L.scratch_bytes, st);
+    return s;
 }
 
 namespace spc {
-void kmap_defer_begin() {
+void kmap_defer_begin(void *order_scratch, size_t order_scratch_bytes) {
     memset(&g_defer.b, 0, sizeof(g_defer.b));
     g_defer.max_kd = 0;
     g_defer.tiles = 0;
+    g_defer.orders.clear();
+    g_defer.scratch = order_scratch;
+    g_defer.scratch_bytes = order_scratch_bytes;
     g_defer.active = true;
 }
+size_t kmap_bytes_batched(spc_geom geom, int32_t t, uint32_t flags, int64_t n_out) {
+    KmapPlan pl;
+    if (make_plan(geom, t, flags, pl) != SPC_OK || n_out < 0) return 0;
+    return layout_of(pl, n_out, flags, false).total;
+}
+size_t kmap_order_rows(spc_geom geom, int32_t t, uint32_t flags, int64_t n_out) {
+    KmapPlan pl;
+    if (make_plan(geom, t, flags, pl) != SPC_OK) return 0;
+    return wants_order(pl, flags) ? (size_t)n_out : 0;
+}
+size_t kmap_order_scratch_bytes(int64_t rows) { return rows > 0 ? order_scratch_bytes(rows) : 0; }
 void kmap_defer_abort() { g_defer.active = false; }
 spc_status kmap_defer_end(cudaStream_t st) {
     g_defer.active = false;
     if (g_defer.b.n_maps == 0) return SPC_OK;
-    return launch_kmaps(g_defer.b, g_defer.max_kd, g_defer.tiles, st);
+    spc_status s = launch_kmaps(g_defer.b, g_defer.max_kd, g_defer.tiles, st);
+    if (s == SPC_OK && !g_defer.orders.empty()) s = run_orders(g_defer.orders, g_defer.scratch, g_defer.scratch_bytes, st);
+    return s;
 }
 }  // namespace spc
 

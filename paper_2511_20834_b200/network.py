@@ -145,8 +145,9 @@ class SparseNet:
     capacity n0 (all levels), so a pass is a fixed launch sequence (CUDA-graph capturable)."""
 
     def __init__(self, n0_cap: int, spec: spc.PackSpec, device="cuda", seed: int = 20834, t_override=None,
-                 nnz_per_out: float = 10.0, net: str = "minkunet42"):
+                 nnz_per_out: float = 10.0, net: str = "minkunet42", density_order: bool = True):
         self.dev = torch.device(device)
+        self.density_order = bool(density_order)
         self.spec = spec
         self.n0 = int(n0_cap)
         if net == "minkunet42":
@@ -193,7 +194,10 @@ class SparseNet:
             geoms.append(spc.Geom(K, stride, 1, tsd, tr))
             t = self.t[mk]
             ts.append(t)
-            flags.append(spc.SPC_KMAP_HALVE_SYMMETRIC if (stride == 1 and K > 1) else 0)
+            f = spc.SPC_KMAP_HALVE_SYMMETRIC if (stride == 1 and K > 1) else 0
+            if self.density_order:
+                f |= spc.SPC_KMAP_DENSITY_ORDER      # OS part only; ignored when t leaves no OS part
+            flags.append(f)
         return geoms, ts, flags
 
     def index(self, stream=None):

@@ -169,6 +169,56 @@ def test_kmap_os_table_exact_and_centre():
     assert (tab[:, 13] == np.arange(len(c))).all()          # centre maps i -> i
 
 
+@pytest.mark.parametrize("K,kind,t", [(3, "subm", -1), (3, "subm", 2), (5, "subm", 3), (3, "strided", -1),
+                                      (3, "transposed", -1)])
+def test_kmap_density_order_exact(K, kind, t):
+    """SPC_KMAP_DENSITY_ORDER: os_rows is the STABLE sort of the outputs by their direction
+    key (bit j set iff the output matches offset k or its mirror K^3-1-k, j = rank of the
+    pair min(k, mirror) among the pairs with a dense member, the submanifold centre pair
+    skipped, folded mod 16) -- unique, so checked bit-exactly against numpy's stable
+    argsort of the oracle map; the ordered table is the canonical one permuted; tile
+    masks are the OR of each 128-row tile."""
+    coords = synth.make_scan(1, 1)
+    spec = _spec_for(coords)
+    lv = _levels(coords, spec, [2])
+    fine_k, fine_c = lv[1]
+    coarse_k, coarse_c = lv[2]
+    if kind == "subm":
+        g, ik, ok, ic, oc = spc.Geom(K, 1, 1, 1, 0), fine_k, fine_k, fine_c, fine_c
+    elif kind == "strided":
+        g, ik, ok, ic, oc = spc.Geom(K, 2, 1, 1, 0), fine_k, coarse_k, fine_c, coarse_c
+    else:
+        g, ik, ok, ic, oc = spc.Geom(K, 2, 1, 1, 1), coarse_k, fine_k, coarse_c, fine_c
+    km = spc.spc_build_kmap(ik, ok, spec, g, t, spc.SPC_KMAP_DENSITY_ORDER)
+    rows, tab_ord, masks = [x.cpu().numpy() for x in km.density_order()]
+    tab = km.os_table().cpu().numpy()
+    ref = oracle.kmap(ic, oc, K, 1, transposed=(kind == "transposed"))
+    n, kd = tab.shape
+    dense = km.dense_k
+    col = {k: c for c, k in enumerate(dense)}
+    full = np.full((n, kd), -1, np.int64)
+    sel = np.isin(ref[:, 0], dense)
+    full[ref[sel, 1], [col[k] for k in ref[sel, 0]]] = ref[sel, 2]
+    np.testing.assert_array_equal(tab, full)
+    kv = K ** 3
+    centre = (kv - 1) // 2
+    pairs = sorted({min(k, kv - 1 - k) for k in dense if not (kind == "subm" and k == centre)})
+    rank = {pr: i % 16 for i, pr in enumerate(pairs)}
+    key = np.zeros(n, np.int64)
+    for c, k in enumerate(dense):
+        pr = min(k, kv - 1 - k)
+        if pr in rank:
+            key |= (full[:, c] >= 0).astype(np.int64) << rank[pr]
+    np.testing.assert_array_equal(rows, np.argsort(key, kind="stable"))
+    np.testing.assert_array_equal(tab_ord, full[rows])
+    pad = (-n) % 128
+    hit = np.concatenate([(full[rows] >= 0), np.zeros((pad, kd), bool)]).reshape(-1, 128, kd).any(axis=1)
+    words = np.zeros((hit.shape[0], masks.shape[1]), np.int64)
+    for c in range(kd):
+        words[:, c // 32] |= hit[:, c].astype(np.int64) << (c % 32)
+    np.testing.assert_array_equal(masks.view(np.uint32).astype(np.int64), words)
+
+
 def test_kmap_edge_cases():
     spec = spc.PackSpec(0, 8, 8, 8)
     one = torch.tensor([(128 << 16) | (128 << 8) | 128], dtype=torch.int64, device=DEV)
@@ -220,6 +270,9 @@ CONV_CASES = [
     (3, "strided", -1, 0, 32, 64, "bf16"), (3, "strided", 0, 0, 64, 64, "bf16"),
     (3, "transposed", -1, 0, 64, 32, "bf16"), (3, "transposed", 2, 0, 48, 384, "bf16"),
     (3, "subm", 2, 1, 16, 32, "f32"), (3, "strided", 0, 0, 32, 16, "f32"),
+    # density-ordered OS part (SPC_KMAP_DENSITY_ORDER = 8): all-OS, hybrid, strided, transposed, K=5, f32
+    (3, "subm", -1, 8, 32, 32, "bf16"), (3, "subm", 2, 9, 64, 96, "bf16"), (3, "strided", -1, 8, 32, 64, "bf16"),
+    (3, "transposed", -1, 8, 64, 32, "bf16"), (5, "subm", 3, 9, 32, 32, "bf16"), (3, "subm", -1, 8, 16, 32, "f32"),
 ]
 
 
@@ -301,7 +354,8 @@ def test_conv_split_fixup_and_workspace_invariant():
     keys, _, _ = _pack_sort(coords, spec)
     c = oracle.sort_coords(coords)[0]
     ws = torch.zeros(len(c) * 256 * 4 + 4096, dtype=torch.uint8, device=DEV)
-    for t, flags, ci, co in ((-1, 0, 32, 64), (-1, 0, 64, 256), (0, 1, 32, 32), (2, 1, 64, 96), (-1, 1, 16, 128)):
+    for t, flags, ci, co in ((-1, 0, 32, 64), (-1, 0, 64, 256), (0, 1, 32, 32), (2, 1, 64, 96), (-1, 1, 16, 128),
+                             (-1, 8, 32, 64), (2, 9, 64, 96)):
         km = spc.spc_build_kmap(keys, keys, spec, spc.Geom(3, 1, 1, 1, 0), t, flags)
         F = synth.make_features(len(c), ci, seed=ci)
         W = synth.make_weights(27, ci, co, seed=co, nnz_per_out=10)
