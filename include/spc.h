@@ -178,9 +178,11 @@ typedef struct {
  *           128-row tile has a match at dense offset c (empty chunks are skipped).
  * os_rows / os_table_ord / tile_mask_ord (SPC_KMAP_DENSITY_ORDER, else NULL): the OS
  *           table with its rows permuted (row p holds output os_rows[p]; outputs stably
- *           sorted by the bit mask of their matched dense offsets, the centre column
- *           excluded) and the tile masks of that order.  Same values as os_table, other
- *           row order; the feature computation writes row p's result to output os_rows[p]. */
+ *           sorted by a direction key: bit j set iff the output matches offset k or its
+ *           mirror K^3-1-k, j = rank of the pair among the dense pairs (submanifold centre
+ *           skipped), folded onto 16 bits (16 - ceil(log2 #ordered maps) in a network
+ *           build)) and the tile masks of that order.  Same values as os_table, other row
+ *           order; the feature computation writes row p's result to output os_rows[p]. */
 typedef struct {
     spc_geom geom;
     int32_t t;            /* effective threshold (SPC_T_ALL_OS resolved)            */

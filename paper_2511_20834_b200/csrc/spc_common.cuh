@@ -128,7 +128,7 @@ spc_status radix_sort(const uint64_t *keys_in, const int32_t *vals_in /*nullable
 namespace spc {
 // network-wide phase 2: spc_build_kmap calls between begin/end are collected and built by
 // one grouped launch (spc_kmap.cu)
-void kmap_defer_begin(void *order_scratch, size_t order_scratch_bytes);
+void kmap_defer_begin(void *order_scratch, size_t order_scratch_bytes, int64_t order_rows);
 size_t kmap_bytes_batched(spc_geom geom, int32_t t, uint32_t flags, int64_t n_out);   // map buffer in a batch
 size_t kmap_order_rows(spc_geom geom, int32_t t, uint32_t flags, int64_t n_out);      // rows it adds to the order sort
 size_t kmap_order_scratch_bytes(int64_t rows);

@@ -42,8 +42,6 @@ int num_sms() {
     return n;
 }
 
-size_t kmap_smem_bytes(int k_dense);
-
 __global__ void k_fill_i64(int64_t *p, int64_t v) { *p = v; }
 spc_status fill_i64(int64_t *p, int64_t v, cudaStream_t st) {
     k_fill_i64<<<1, 1, 0, st>>>(p, v);
@@ -208,7 +206,7 @@ extern "C" spc_status spc_network_kmaps(const uint64_t *v0_keys, int64_t n0, con
         maps_bytes += align_up(kmap_bytes_batched(geoms[i], ts[i], fi, n0), 256);
         order_rows += (int64_t)kmap_order_rows(geoms[i], ts[i], fi, n0);
     }
-    kmap_defer_begin(base + off + maps_bytes, kmap_order_scratch_bytes(order_rows));
+    kmap_defer_begin(base + off + maps_bytes, kmap_order_scratch_bytes(order_rows), order_rows);
     for (int i = 0; i < n_maps; ++i) {
         const uint32_t fi = flags ? flags[i] : 0;
         int dup = -1;

@@ -1,17 +1,19 @@
 // spc_kmap.cu -- A4-A8: one-shot z-delta kernel-map build on packed keys (§5.2,
 // P:341 packed queries, P:393-421 layouts and symmetric halving).
 //
-// CTA = tile of KM_BM sorted outputs.  For a fixed offset group the queries of a tile are
-// sorted, so every match of (tile, group g) lies in ONE contiguous window of the sorted
-// input keys: [lb(q_first + d_anchor(g)), lb(q_last + d_last(g) + 1)).  Phase A finds the
-// 2*K^2 window bounds (parallel global lower_bounds), phase A' stages the windows in
-// shared memory (coalesced), phase B runs the paper's z-delta search per (output, group)
-// inside the window: one lower_bound for the anchor query, then a forward cursor for the
-// other K-1 members.  Both layouts are written straight from phase B:
-//   OS (dense offsets): staged as a [KM_BM x K_dense] int32 block in smem, flushed with
-//       coalesced 16-byte stores (no transpose pass);
-//   WS (sparse offsets): (in, out) pairs appended with one warp-aggregated atomicAdd per
-//       (warp, offset) (no filter pass); halved for submanifold layers.
+// Outputs are cut into tiles of KM_BM sorted keys.  For a fixed offset group g (the K
+// offsets sharing (dx, dy)) the queries of a tile are sorted, so every match of (tile, g)
+// lies in ONE contiguous window of the sorted input keys:
+// [lb(q_first + d_anchor(g)), lb(q_last + d_last(g) + 1)).
+//   k_kmap_bounds: every window bound of every (map, tile, group) in one parallel pass.
+//   k_kmap_zdelta: one WARP per (tile, group) task: stage the window in shared memory
+//       (coalesced), then the paper's z-delta search per output: one lower_bound for the
+//       anchor query, then a forward cursor for the other K-1 members.  Tasks
+//       are independent (no CTA barriers); both layouts are written straight from the
+//       search: OS (dense offsets) entries into the [n_out x K_dense] table (every entry
+//       written once, -1 for no match: no transpose pass); WS (sparse offsets)
+//       (in, out) pairs appended with one warp-aggregated atomicAdd per (warp, offset) (no
+//       filter pass), halved for submanifold layers.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -23,7 +25,8 @@ namespace spc {
 
 constexpr int KM_BM = 128;          // outputs per tile
 constexpr int KM_THREADS = 256;
-constexpr int KM_WIN_CAP = 4096;    // staged window keys per tile (32 KB)
+constexpr int KM_WARPS = KM_THREADS / 32;
+constexpr int KM_WWIN = 512;        // staged window keys per warp task (4 KB); larger: global search
 
 // Compact per-map descriptor; the offset tables (packed query deltas, weight slots,
 // dense columns, WS lists) are rebuilt in shared memory from it, so one launch can build
@@ -40,10 +43,13 @@ struct KmapDesc {
     int32_t *counts;
     uint32_t *tile_mask;
     unsigned long long *stats;
+    int32_t *bounds;          // [tiles][K^2][2] window bounds (k_kmap_bounds)
     int64_t list_stride;
     int32_t spacing;
     int16_t K, k_dense, tile_words, t_eff;
     int8_t transposed, halved;
+    int8_t ord_idx;                 // density order: index among the ordered maps (-1: none)
+    int8_t ord_cls[SPC_MAX_KVOL];   // density-order key bit of each dense column (-1: none)
 };
 
 constexpr int KM_MAX_MAPS = 24;
@@ -52,6 +58,10 @@ struct KmapBatch {
     int n_maps;
     int bits_y, bits_z;
     unsigned int *work_ctr;   // zeroed before the launch
+    // density order: keys of all ordered maps, concatenated in ord_idx order by live counts
+    uint64_t *ord_keys;
+    int64_t *ord_total;       // sum of their live rows (written by k_kmap_prep)
+    int ord_key_bits;         // mask bits below the map tag
     KmapDesc d[KM_MAX_MAPS];
 };
 
@@ -86,204 +96,237 @@ __device__ __forceinline__ int lower_bound_s(const uint64_t *a, int n, uint64_t 
 // zero the per-map counters / stats and the work counter
 __global__ void k_kmap_prep(const __grid_constant__ KmapBatch b) {
     const int m = blockIdx.x;
-    if (m == 0 && threadIdx.x == 0) *b.work_ctr = 0;
+    if (m == 0 && threadIdx.x == 0) {
+        *b.work_ctr = 0;
+        if (b.ord_total) {
+            int64_t tot = 0;
+            for (int q = 0; q < b.n_maps; ++q)
+                if (b.d[q].ord_idx >= 0) tot += dev_count(b.d[q].n_out_cap, b.d[q].n_out_dev);
+            *b.ord_total = tot;
+        }
+    }
     if (m >= b.n_maps) return;
     for (int i = threadIdx.x; i < 2 * SPC_MAX_KVOL; i += blockDim.x) b.d[m].counts[i] = 0;
     if (b.d[m].stats && threadIdx.x < 2) b.d[m].stats[threadIdx.x] = 0;
 }
 
-__global__ void __launch_bounds__(KM_THREADS) k_kmap_zdelta(const __grid_constant__ KmapBatch B) {
-    extern __shared__ __align__(16) unsigned char km_smem[];
-    __shared__ int64_t win_lo[25];
-    __shared__ int win_len[25];
-    __shared__ int win_base[25];    // -1: window not staged, use global search
-    __shared__ uint32_t smask[4];   // tile bit mask over dense columns (<= 125)
-    __shared__ int64_t s_delta[SPC_MAX_KVOL];
-    __shared__ int16_t s_kslot[SPC_MAX_KVOL], s_dcol[SPC_MAX_KVOL], s_list[SPC_MAX_KVOL];
-    __shared__ uint8_t s_need[25];
-    __shared__ int s_prefix[KM_MAX_MAPS + 1];
-    __shared__ int s_work, s_cur_map;
+// packed query delta of member mm (ascending query order) of offset group g
+__device__ __forceinline__ int64_t group_delta(const KmapDesc &p, int by, int bz, int g, int mm) {
+    const int K = p.K, r = (K - 1) / 2;
+    const int ex = g / K - r, ey = g % K - r;
+    const int ez = p.transposed ? r - mm : mm - r;
+    const int64_t d = (int64_t)ex * p.spacing * (1ll << (by + bz)) + (int64_t)ey * p.spacing * (1ll << bz) +
+                      (int64_t)ez * p.spacing;
+    return p.transposed ? -d : d;
+}
 
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) {
-        int acc = 0;
+// phase A of every (map, tile, group) at once: the window [lo, hi) of the sorted input
+// keys holding all matches of a tile's outputs for one offset group.  One thread per
+// bound, so the global binary searches' latency chains all run concurrently instead of
+// once per tile inside the build kernel.
+// It also zeroes each tile's OS mask words and writes each row's density-order key tag
+// (the build ORs the direction bits in).
+__global__ void __launch_bounds__(256) k_kmap_bounds(const __grid_constant__ KmapBatch B) {
+    __shared__ int64_t s_pre[KM_MAX_MAPS + 1];
+    __shared__ int64_t s_ordbase[KM_MAX_MAPS];
+    if (threadIdx.x == 0) {
+        int64_t acc = 0, ob = 0;
         for (int m = 0; m < B.n_maps; ++m) {
-            s_prefix[m] = acc;
+            s_pre[m] = acc;
             const int64_t n_out = dev_count(B.d[m].n_out_cap, B.d[m].n_out_dev);
-            acc += (int)((n_out + KM_BM - 1) / KM_BM);
+            acc += ((n_out + KM_BM - 1) / KM_BM) * 2 * B.d[m].K * B.d[m].K;
+            s_ordbase[m] = ob;
+            if (B.d[m].ord_idx >= 0) ob += n_out;
         }
-        s_prefix[B.n_maps] = acc;
-        s_cur_map = -1;
+        s_pre[B.n_maps] = acc;
     }
     __syncthreads();
-    const int total = s_prefix[B.n_maps];
-
-    for (;;) {
-        if (tid == 0) s_work = (int)atomicAdd(B.work_ctr, 1u);
-        __syncthreads();
-        const int v = s_work;
-        if (v >= total) break;
+    const int64_t total = s_pre[B.n_maps];
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < total; v += (int64_t)gridDim.x * blockDim.x) {
         int m = 0;
-        while (s_prefix[m + 1] <= v) ++m;
+        while (s_pre[m + 1] <= v) ++m;
         const KmapDesc &p = B.d[m];
-        const int tile = v - s_prefix[m];
-        const int K = p.K, G = K * K, KD = p.k_dense, r = (K - 1) / 2, kv = K * K * K;
-        // ---- per-map tables (rebuilt only when the map changes) -------------------------
-        if (s_cur_map != m) {
-            if (tid < kv) {
-                const int g = tid / K, mm = tid % K;
-                const int ex = g / K - r, ey = g % K - r;
-                const int ez = p.transposed ? r - mm : mm - r;   // ascending query order
-                const int k = ((ex + r) * K + (ey + r)) * K + (ez + r);
-                int64_t d = (int64_t)ex * p.spacing * (1ll << (B.bits_y + B.bits_z)) +
-                            (int64_t)ey * p.spacing * (1ll << B.bits_z) + (int64_t)ez * p.spacing;
-                s_delta[tid] = p.transposed ? -d : d;
-                s_kslot[tid] = (int16_t)k;
-                // per weight offset k == tid: dense column / WS list (same rule as make_plan)
-                const int kx = tid / (K * K) - r, ky = (tid / K) % K - r, kz = tid % K - r;
-                const int centre = (kv - 1) / 2;
-                int dcol = -1, lst = -1, nd = 0, nl = 0;
-                for (int k2 = 0; k2 <= tid; ++k2) {
-                    const int l1 = abs(k2 / (K * K) - r) + abs((k2 / K) % K - r) + abs(k2 % K - r);
-                    const bool dense = l1 < p.t_eff;
-                    const bool stored = !dense && (!p.halved || k2 <= centre);
-                    if (k2 == tid) {
-                        dcol = dense ? nd : -1;
-                        lst = stored ? nl : -1;
-                    }
-                    nd += dense;
-                    nl += stored;
-                }
-                (void)kx; (void)ky; (void)kz;
-                s_dcol[tid] = (int16_t)dcol;
-                s_list[tid] = (int16_t)lst;
-            }
-            __syncthreads();
-            if (tid < G) {
-                bool need = false;
-                for (int mm = 0; mm < K; ++mm) {
-                    const int k = s_kslot[tid * K + mm];
-                    need |= s_dcol[k] >= 0 || s_list[k] >= 0;
-                }
-                s_need[tid] = need;
-            }
-            if (tid == 0) s_cur_map = m;
-        }
-        if (tid < 4) smask[tid] = 0;
-        __syncthreads();
-
+        const int G2 = 2 * p.K * p.K;
+        const int64_t local = v - s_pre[m];
+        const int64_t tile = local / G2;
+        const int j = (int)(local - tile * G2), g = j >> 1, hi = j & 1;
         const int64_t n_out = dev_count(p.n_out_cap, p.n_out_dev);
         const int64_t n_in = dev_count(p.n_in_cap, p.n_in_dev);
-        const int64_t row0 = (int64_t)tile * KM_BM;
+        const int64_t row0 = tile * KM_BM;
         const int rows = (int)imin64(KM_BM, n_out - row0);
-        int32_t *os_tile = reinterpret_cast<int32_t *>(km_smem);
-        uint64_t *win = reinterpret_cast<uint64_t *>(km_smem + KM_BM * KD * 4);   // KM_BM*4 = 512 B multiple
+        if (j < p.tile_words) p.tile_mask[tile * p.tile_words + j] = 0u;
+        if (p.ord_idx >= 0)
+            for (int r = j; r < rows; r += G2)
+                B.ord_keys[s_ordbase[m] + row0 + r] = (uint64_t)p.ord_idx << B.ord_key_bits;
+        const uint64_t q = hi ? p.out[row0 + rows - 1] + (uint64_t)group_delta(p, B.bits_y, B.bits_z, g, p.K - 1) + 1ull
+                              : p.out[row0] + (uint64_t)group_delta(p, B.bits_y, B.bits_z, g, 0);
+        p.bounds[local] = (int32_t)lower_bound_g(p.in, n_in, q);
+    }
+}
 
-        // ---- phase A: window bounds of every (tile, group) ----------------------------
-        const uint64_t q_first = p.out[row0];
-        const uint64_t q_last = p.out[row0 + rows - 1];
-        if (tid < 2 * G) {
-            const int g = tid >> 1;
-            if (s_need[g]) {
-                const uint64_t q = (tid & 1) ? q_last + (uint64_t)s_delta[g * K + K - 1] + 1ull
-                                             : q_first + (uint64_t)s_delta[g * K];
-                const int64_t b = lower_bound_g(p.in, n_in, q);
-                if (tid & 1) win_len[g] = (int)imin64(b, INT32_MAX);   // hi for now
-                else win_lo[g] = b;
-            }
+// one (tile, group) task of k_kmap_zdelta, run by one warp
+template <int K>
+__device__ __forceinline__ void zdelta_task(const KmapBatch &B, const KmapDesc &p, int m, int64_t local,
+                                            const int8_t *dcol, const int8_t *lstv, int64_t ordbase, uint64_t *win,
+                                            int lane, unsigned long long &n_search, unsigned long long &n_probe) {
+    constexpr int G = K * K, r = (K - 1) / 2;
+    const int KD = p.k_dense;
+    const int64_t tile = local / G;
+    const int g = (int)(local - tile * G);
+    const int ex = g / K - r, ey = g % K - r;
+    int ks[K];
+    bool need = false;
+#pragma unroll
+    for (int mm = 0; mm < K; ++mm) {   // weight offsets of the members, ascending query order
+        const int ez = p.transposed ? r - mm : mm - r;
+        ks[mm] = ((ex + r) * K + (ey + r)) * K + (ez + r);
+        need |= dcol[ks[mm]] >= 0 || lstv[ks[mm]] >= 0;
+    }
+    if (!need) return;
+    const int64_t n_out = dev_count(p.n_out_cap, p.n_out_dev);
+    const int64_t row0 = tile * KM_BM;
+    const int rows = (int)imin64(KM_BM, n_out - row0);
+    const int32_t lo = p.bounds[local * 2], hi = p.bounds[local * 2 + 1];
+    const int wl = max(0, hi - lo);
+    const bool staged = wl <= KM_WWIN;
+    if (staged) {
+        for (int e = lane; e < wl; e += 32) win[e] = __ldg(p.in + lo + e);
+        __syncwarp();
+    }
+    const uint64_t *wk = staged ? win : p.in + lo;
+    int64_t dl[K];
+#pragma unroll
+    for (int mm = 0; mm < K; ++mm) dl[mm] = group_delta(p, B.bits_y, B.bits_z, g, mm);
+    uint32_t colbal[K];
+    int cnt[K];
+#pragma unroll
+    for (int mm = 0; mm < K; ++mm) { colbal[mm] = 0u; cnt[mm] = 0; }
+    const bool ord = p.ord_idx >= 0;
+    for (int ch = 0; ch * 32 < rows; ++ch) {
+        const int lr = ch * 32 + lane;
+        const bool valid = lr < rows;
+        const int64_t i = row0 + lr;
+        const uint64_t q = valid ? p.out[i] : 0;
+        int pos = 0;
+        if (valid) {
+            pos = lower_bound_s(wk, wl, q + (uint64_t)dl[0]);
+            ++n_search;
         }
-        __syncthreads();
-        if (tid == 0) {
-            int base = 0;
-            for (int g = 0; g < G; ++g) {
-                if (!s_need[g]) { win_base[g] = -1; win_len[g] = 0; continue; }
-                int64_t len = (int64_t)win_len[g] - win_lo[g];
-                if (len < 0) len = 0;
-                win_len[g] = (int)len;
-                if (base + len <= KM_WIN_CAP) { win_base[g] = base; base += (int)len; }
-                else win_base[g] = -1;
-            }
-        }
-        __syncthreads();
-        // ---- phase A': stage windows (one warp per group, coalesced) -----------------------
-        for (int g = warp; g < G; g += KM_THREADS / 32) {
-            if (win_base[g] < 0) continue;
-            const uint64_t *src = p.in + win_lo[g];
-            uint64_t *dst = win + win_base[g];
-            for (int e = lane; e < win_len[g]; e += 32) dst[e] = __ldg(src + e);
-        }
-        __syncthreads();
-
-        // ---- phase B: z-delta search per (output, group) ---------------------------------
-        unsigned long long n_search = 0, n_probe = 0;
-        const int chunks = KM_BM / 32;
-        for (int item = warp; item < G * chunks; item += KM_THREADS / 32) {
-            const int g = item / chunks, ch = item - g * chunks;
-            if (!s_need[g]) continue;
-            const int lr = ch * 32 + lane;               // local row
-            const bool valid = lr < rows;
-            const int64_t i = row0 + lr;
-            const uint64_t q = valid ? p.out[i] : 0;
-            const bool staged = win_base[g] >= 0;
-            const uint64_t *wk = staged ? win + win_base[g] : p.in + win_lo[g];
-            const int wl = win_len[g];
-            int pos = 0;
+        uint32_t key = 0;
+#pragma unroll
+        for (int mm = 0; mm < K; ++mm) {
+            const uint64_t query = q + (uint64_t)dl[mm];
+            bool match = false;
             if (valid) {
-                pos = lower_bound_s(wk, wl, q + (uint64_t)s_delta[g * K]);
-                ++n_search;
+                while (pos < wl && wk[pos] < query) { ++pos; ++n_probe; }
+                match = pos < wl && wk[pos] == query;
             }
-            for (int mm = 0; mm < K; ++mm) {
-                const uint64_t query = q + (uint64_t)s_delta[g * K + mm];
-                bool match = false;
-                if (valid) {
-                    while (pos < wl && wk[pos] < query) { ++pos; ++n_probe; }
-                    match = pos < wl && wk[pos] == query;
-                }
-                const int k = s_kslot[g * K + mm];
-                const int32_t j = match ? (int32_t)(win_lo[g] + pos) : -1;
-                const unsigned bal = __ballot_sync(0xffffffffu, match);
-                if (lane == 0 && bal) atomicAdd(&p.counts[k], __popc(bal));
-                const int col = s_dcol[k];
-                if (col >= 0) {
-                    if (valid) os_tile[lr * KD + col] = j;
-                    if (lane == 0 && bal) atomicOr(&smask[col >> 5], 1u << (col & 31));
-                } else {
-                    const int l = s_list[k];
-                    if (l >= 0 && bal) {
-                        int base = 0;
-                        if (lane == 0) base = atomicAdd(&p.counts[SPC_MAX_KVOL + l], __popc(bal));
-                        base = __shfl_sync(0xffffffffu, base, 0);
-                        if (match) {
-                            int2 pr = make_int2(j, (int32_t)i);
-                            p.pairs[(int64_t)l * p.list_stride + base + __popc(bal & lanemask_lt())] = pr;
-                        }
-                    }
+            const int32_t j = match ? lo + pos : -1;
+            const unsigned bal = __ballot_sync(0xffffffffu, match);
+            cnt[mm] += __popc(bal);
+            const int col = dcol[ks[mm]];
+            if (col >= 0) {
+                if (valid) p.os[i * KD + col] = j;
+                colbal[mm] |= bal;
+                if (ord && match && p.ord_cls[col] >= 0) key |= 1u << (p.ord_cls[col] % B.ord_key_bits);
+            } else {
+                const int l = lstv[ks[mm]];
+                if (l >= 0 && bal) {
+                    int base = 0;
+                    if (lane == 0) base = atomicAdd(&p.counts[SPC_MAX_KVOL + l], __popc(bal));
+                    base = __shfl_sync(0xffffffffu, base, 0);
+                    if (match)
+                        p.pairs[(int64_t)l * p.list_stride + base + __popc(bal & lanemask_lt())] = make_int2(j, (int32_t)i);
                 }
             }
         }
-        if (p.stats) {
-            for (int o = 16; o > 0; o >>= 1) {
-                n_search += __shfl_xor_sync(0xffffffffu, n_search, o);
-                n_probe += __shfl_xor_sync(0xffffffffu, n_probe, o);
-            }
-            if (lane == 0) {
-                atomicAdd(&p.stats[0], n_search);
-                atomicAdd(&p.stats[1], n_probe);
-            }
+        if (ord && key) atomicOr(reinterpret_cast<unsigned long long *>(&B.ord_keys[ordbase + i]), (unsigned long long)key);
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int mm = 0; mm < K; ++mm) {
+            if (cnt[mm]) atomicAdd(&p.counts[ks[mm]], cnt[mm]);
+            const int col = dcol[ks[mm]];
+            if (col >= 0 && colbal[mm]) atomicOr(&p.tile_mask[tile * p.tile_words + (col >> 5)], 1u << (col & 31));
         }
-        __syncthreads();
-        // ---- phase C: flush the OS block (contiguous rows*KD int32) -----------------------
-        if (KD > 0) {
-            int32_t *dst = p.os + row0 * KD;
-            const int totalv = rows * KD;
-            const int nvec = totalv / 4;   // row0*KD*4 is 16-byte aligned (KM_BM = 128)
-            int4 *d4 = reinterpret_cast<int4 *>(dst);
-            const int4 *s4 = reinterpret_cast<const int4 *>(os_tile);
-            for (int e = tid; e < nvec; e += KM_THREADS) d4[e] = s4[e];
-            for (int e = nvec * 4 + tid; e < totalv; e += KM_THREADS) dst[e] = os_tile[e];
-            if (tid < p.tile_words) p.tile_mask[(int64_t)tile * p.tile_words + tid] = smask[tid];
+    }
+    (void)m;
+}
+
+__global__ void __launch_bounds__(KM_THREADS, 4) k_kmap_zdelta(const __grid_constant__ KmapBatch B) {
+    __shared__ int8_t s_dcol[KM_MAX_MAPS][SPC_MAX_KVOL];   // weight offset -> dense column / -1
+    __shared__ int8_t s_lst[KM_MAX_MAPS][SPC_MAX_KVOL];    // weight offset -> WS list / -1
+    __shared__ int64_t s_pre[KM_MAX_MAPS + 1];             // task prefix (tiles * K^2)
+    __shared__ int64_t s_ordbase[KM_MAX_MAPS];
+    __shared__ __align__(16) uint64_t s_win[KM_WARPS][KM_WWIN];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // ---- prologue: per-map offset tables (same rule as make_plan) ----------------------
+    for (int e = tid; e < B.n_maps * 128; e += KM_THREADS) {
+        const int m = e >> 7, k = e & 127;
+        const KmapDesc &p = B.d[m];
+        const int K = p.K, r = (K - 1) / 2, kv = K * K * K, centre = (kv - 1) / 2;
+        if (k >= kv) continue;
+        int nd = 0, nl = 0, dcol = -1, lst = -1;
+        for (int k2 = 0; k2 <= k; ++k2) {
+            const int l1 = abs(k2 / (K * K) - r) + abs((k2 / K) % K - r) + abs(k2 % K - r);
+            const bool dense = l1 < p.t_eff;
+            const bool stored = !dense && (!p.halved || k2 <= centre);
+            if (k2 == k) {
+                dcol = dense ? nd : -1;
+                lst = stored ? nl : -1;
+            }
+            nd += dense;
+            nl += stored;
         }
-        __syncthreads();
+        s_dcol[m][k] = (int8_t)dcol;
+        s_lst[m][k] = (int8_t)lst;
+    }
+    if (tid == 0) {
+        int64_t acc = 0, ob = 0;
+        for (int m = 0; m < B.n_maps; ++m) {
+            s_pre[m] = acc;
+            const int64_t n_out = dev_count(B.d[m].n_out_cap, B.d[m].n_out_dev);
+            acc += ((n_out + KM_BM - 1) / KM_BM) * B.d[m].K * B.d[m].K;
+            s_ordbase[m] = ob;
+            if (B.d[m].ord_idx >= 0) ob += n_out;
+        }
+        s_pre[B.n_maps] = acc;
+    }
+    __syncthreads();
+    const int64_t total = s_pre[B.n_maps];
+    uint64_t *win = s_win[warp];
+    unsigned long long n_search = 0, n_probe = 0;
+    int stats_map = -1;
+
+    // ---- one warp per (map, tile, group) task -------------------------------------------
+    for (int64_t v = (int64_t)blockIdx.x * KM_WARPS + warp; v < total; v += (int64_t)gridDim.x * KM_WARPS) {
+        int m = 0;
+        while (s_pre[m + 1] <= v) ++m;
+        const KmapDesc &p = B.d[m];
+        if (p.stats && stats_map != m) {   // flush the stats of the previous map
+            if (stats_map >= 0 && lane == 0) {
+                atomicAdd(&B.d[stats_map].stats[0], n_search);
+                atomicAdd(&B.d[stats_map].stats[1], n_probe);
+            }
+            n_search = n_probe = 0;
+            stats_map = m;
+        }
+        const int64_t local = v - s_pre[m];
+        if (p.K == 3) zdelta_task<3>(B, p, m, local, s_dcol[m], s_lst[m], s_ordbase[m], win, lane, n_search, n_probe);
+        else if (p.K == 5) zdelta_task<5>(B, p, m, local, s_dcol[m], s_lst[m], s_ordbase[m], win, lane, n_search, n_probe);
+        else zdelta_task<1>(B, p, m, local, s_dcol[m], s_lst[m], s_ordbase[m], win, lane, n_search, n_probe);
+        __syncwarp();   // the window buffer is reused by the next task
+    }
+    if (stats_map >= 0) {
+        for (int o = 16; o > 0; o >>= 1) {
+            n_search += __shfl_xor_sync(0xffffffffu, n_search, o);
+            n_probe += __shfl_xor_sync(0xffffffffu, n_probe, o);
+        }
+        if (lane == 0) {
+            atomicAdd(&B.d[stats_map].stats[0], n_search);
+            atomicAdd(&B.d[stats_map].stats[1], n_probe);
+        }
     }
 }
 
@@ -307,14 +350,40 @@ struct OrderJob {
     int64_t n_cap;
     int64_t tile0;            // first permute CTA of this map
     int k_dense, words;
-    int8_t cls[SPC_MAX_KVOL];
 };
 struct OrderBatch {
-    int n_jobs, key_bits;
-    int64_t *total_dev;       // sum of live rows (written by k_ord_keys)
-    uint64_t *keys;
+    int n_jobs;
     OrderJob j[ORD_MAX];
 };
+
+// the grouped order's scratch: key array (written by the z-delta build), live total,
+// sorted keys / positions, radix workspace
+struct OrderScratch {
+    int64_t *total;
+    uint64_t *keys, *keys_sorted;
+    int32_t *pos;
+    void *rws;
+    size_t rws_bytes;
+    bool ok;
+};
+static OrderScratch order_scratch(void *base, size_t bytes, int64_t rows_cap) {
+    OrderScratch o{};
+    Bump b(base, bytes);
+    o.total = b.take<int64_t>(4);
+    o.keys = b.take<uint64_t>((size_t)rows_cap);
+    o.keys_sorted = b.take<uint64_t>((size_t)rows_cap);
+    o.pos = b.take<int32_t>((size_t)rows_cap);
+    o.rws_bytes = radix_sort_workspace(rows_cap, true);
+    o.rws = b.take<uint8_t>(o.rws_bytes);
+    o.ok = b.ok();
+    return o;
+}
+static int ord_tag_bits(int n_jobs) {
+    int t = 0;
+    while ((1 << t) < n_jobs) ++t;
+    return t;
+}
+static int ord_key_bits(int n_jobs) { return 16 - ord_tag_bits(n_jobs); }   // 2 radix passes
 
 __device__ __forceinline__ int64_t ord_base(const OrderBatch &B, int job, int64_t &n_job) {
     int64_t base = 0;
@@ -323,25 +392,9 @@ __device__ __forceinline__ int64_t ord_base(const OrderBatch &B, int job, int64_
     return base;
 }
 
-__global__ void k_ord_keys(const __grid_constant__ OrderBatch B) {
-    int64_t base = 0;
-    for (int q = 0; q < B.n_jobs; ++q) {
-        const OrderJob &J = B.j[q];
-        const int64_t n = dev_count(J.n_cap, J.n_dev);
-        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-            const int32_t *row = J.os + i * J.k_dense;
-            uint32_t m = 0;
-            for (int c = 0; c < J.k_dense; ++c)
-                if (J.cls[c] >= 0 && row[c] >= 0) m |= 1u << J.cls[c];
-            B.keys[base + i] = ((uint64_t)q << B.key_bits) | m;
-        }
-        base += n;
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) *B.total_dev = base;
-}
-
 // one CTA per 128-row tile of one map: row p of the ordered table = row rows[p] of the
-// canonical one (warp-cooperative row copies), tile mask words by warp ballots
+// canonical one.  Each warp copies its 32 rows as one flat range of 32*k_dense elements
+// (independent loads, coalesced stores); tile mask words from per-lane column masks.
 __global__ void __launch_bounds__(128) k_ord_permute(const __grid_constant__ OrderBatch B,
                                                      const int32_t *__restrict__ sorted_pos) {
     __shared__ int32_t src_s[128];
@@ -362,25 +415,25 @@ __global__ void __launch_bounds__(128) k_ord_permute(const __grid_constant__ Ord
     src_s[threadIdx.x] = src;
     __syncthreads();
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int KD = J.k_dense;
+    const int nrows = (int)imin64(32, n - (p0 + w * 32));
     uint32_t m[4] = {0u, 0u, 0u, 0u};
-    for (int i = 0; i < 32; ++i) {
-        const int r = w * 32 + i;
-        const int32_t sr = src_s[r];
-        if (sr < 0) break;
-        const int32_t *srow = J.os + (int64_t)sr * J.k_dense;
-        int32_t *drow = J.os_ord + (p0 + r) * J.k_dense;
-        for (int c0 = 0, q = 0; c0 < J.k_dense; c0 += 32, ++q) {
-            const int c = c0 + lane;
-            int32_t v = -1;
-            if (c < J.k_dense) {
-                v = srow[c];
-                drow[c] = v;
-            }
-            m[q & 3] |= __ballot_sync(0xffffffffu, v >= 0);
+    if (nrows > 0) {
+        const int total = nrows * KD;
+        int32_t *dst = J.os_ord + (p0 + w * 32) * KD;
+#pragma unroll 4
+        for (int e = lane; e < total; e += 32) {
+            const int r = e / KD, c = e - r * KD;
+            const int32_t v = J.os[(int64_t)src_s[w * 32 + r] * KD + c];
+            dst[e] = v;
+            if (v >= 0) m[c >> 5] |= 1u << (c & 31);
         }
     }
-    if (lane == 0)
-        for (int q = 0; q < 4; ++q) wm[w][q] = m[q];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const uint32_t r = __reduce_or_sync(0xffffffffu, m[q]);
+        if (lane == 0) wm[w][q] = r;
+    }
     __syncthreads();
     if (threadIdx.x < J.words) {
         const int q = threadIdx.x;
@@ -398,41 +451,25 @@ static size_t order_scratch_bytes(int64_t rows_cap) {
     return z.used + radix_sort_workspace(rows_cap, true) + 512;
 }
 
-static spc_status run_orders(const std::vector<OrderJob> &jobs, void *scratch, size_t scratch_bytes, cudaStream_t st) {
-    for (size_t j0 = 0; j0 < jobs.size(); j0 += ORD_MAX) {
-        OrderBatch B;
-        memset(&B, 0, sizeof(B));
-        B.n_jobs = (int)std::min<size_t>(ORD_MAX, jobs.size() - j0);
-        int64_t cap = 0, tiles = 0;
-        int bits = 1;
-        for (int q = 0; q < B.n_jobs; ++q) {
-            B.j[q] = jobs[j0 + q];
-            B.j[q].tile0 = tiles;
-            tiles += (B.j[q].n_cap + 127) / 128;
-            cap += B.j[q].n_cap;
-            for (int c = 0; c < B.j[q].k_dense; ++c) bits = std::max(bits, (int)B.j[q].cls[c] + 1);
-        }
-        if (cap == 0) continue;
-        int tag_bits = 0;
-        while ((1 << tag_bits) < B.n_jobs) ++tag_bits;
-        B.key_bits = bits;
-        Bump b(scratch, scratch_bytes);
-        B.total_dev = b.take<int64_t>(4);
-        B.keys = b.take<uint64_t>((size_t)cap);
-        uint64_t *keys_sorted = b.take<uint64_t>((size_t)cap);
-        int32_t *pos = b.take<int32_t>((size_t)cap);
-        const size_t rws = radix_sort_workspace(cap, true);
-        void *rw = b.take<uint8_t>(rws);
-        if (!b.ok()) return fail(SPC_ERR_WORKSPACE, "kernel-map density order: scratch too small");
-        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((cap + 255) / 256, 4 * (int64_t)num_sms()));
-        k_ord_keys<<<grid, 256, 0, st>>>(B);
-        SPC_LAUNCH_CHECK("k_ord_keys");
-        spc_status s = radix_sort(B.keys, nullptr, cap, B.total_dev, bits + tag_bits, keys_sorted, pos, rw, rws, st,
-                                  false);
-        if (s != SPC_OK) return s;
-        k_ord_permute<<<(unsigned)tiles, 128, 0, st>>>(B, pos);
-        SPC_LAUNCH_CHECK("k_ord_permute");
+// sort the keys of `jobs` (already written by the z-delta build) and permute their OS tables
+static spc_status run_orders(const std::vector<OrderJob> &jobs, const OrderScratch &o, int64_t rows_cap,
+                             cudaStream_t st) {
+    if (jobs.empty() || rows_cap == 0) return SPC_OK;
+    if (!o.ok) return fail(SPC_ERR_WORKSPACE, "kernel-map density order: scratch too small");
+    OrderBatch B;
+    memset(&B, 0, sizeof(B));
+    B.n_jobs = (int)jobs.size();
+    int64_t tiles = 0;
+    for (int q = 0; q < B.n_jobs; ++q) {
+        B.j[q] = jobs[q];
+        B.j[q].tile0 = tiles;
+        tiles += (B.j[q].n_cap + 127) / 128;
     }
+    spc_status s = radix_sort(o.keys, nullptr, rows_cap, o.total, 16, o.keys_sorted, o.pos, o.rws, o.rws_bytes, st,
+                              false);
+    if (s != SPC_OK) return s;
+    k_ord_permute<<<(unsigned)tiles, 128, 0, st>>>(B, o.pos);
+    SPC_LAUNCH_CHECK("k_ord_permute");
     return SPC_OK;
 }
 
@@ -512,7 +549,7 @@ static spc_status make_plan(const spc_geom &g, int32_t t, uint32_t flags, KmapPl
 }
 
 struct KmapLayout {
-    size_t os, pairs, counts, mask, stats, total;
+    size_t os, pairs, counts, mask, stats, bounds, total;
     size_t rows, os_ord, mask_ord, scratch, scratch_bytes;   // density order
     int64_t tiles;
     int words;
@@ -533,6 +570,7 @@ static KmapLayout layout_of(const KmapPlan &pl, int64_t n_out, uint32_t flags, b
     L.counts = take(sizeof(int32_t) * 2 * SPC_MAX_KVOL);
     L.mask = take(sizeof(uint32_t) * (size_t)(L.tiles * L.words));
     L.stats = take(sizeof(unsigned long long) * 2 + 64);   // + a launch work counter
+    L.bounds = take(sizeof(int32_t) * (size_t)L.tiles * 2 * pl.K * pl.K);
     if (wants_order(pl, flags)) {
         L.rows = take(sizeof(int32_t) * (size_t)n_out);
         L.os_ord = take(sizeof(int32_t) * (size_t)n_out * pl.k_dense);
@@ -547,7 +585,6 @@ static KmapLayout layout_of(const KmapPlan &pl, int64_t n_out, uint32_t flags, b
 }
 
 
-size_t kmap_smem_bytes(int k_dense) { return (size_t)KM_BM * k_dense * 4 + (size_t)KM_WIN_CAP * 8; }
 
 struct DeferState {
     bool active = false;
@@ -555,13 +592,14 @@ struct DeferState {
     int max_kd = 0;
     int64_t tiles = 0;
     std::vector<OrderJob> orders;
-    void *scratch = nullptr;   // density-order scratch of the batch
-    size_t scratch_bytes = 0;
+    OrderScratch scratch{};    // density-order scratch of the batch
+    int64_t order_rows = 0;    // its row capacity
 };
 static thread_local DeferState g_defer;
 
-static void fill_desc(KmapDesc &d, const spc_kmap &km, const KmapPlan &pl) {
+static void fill_desc(KmapDesc &d, const spc_kmap &km, const KmapPlan &pl, int32_t *bounds) {
     memset(&d, 0, sizeof(d));
+    d.bounds = bounds;
     d.in = km.in_keys;
     d.out = km.out_keys;
     d.n_in_cap = km.n_in;
@@ -581,23 +619,30 @@ static void fill_desc(KmapDesc &d, const spc_kmap &km, const KmapPlan &pl) {
     d.t_eff = (int16_t)pl.t_eff;
     d.transposed = (int8_t)km.geom.transposed;
     d.halved = (int8_t)pl.halved;
+    d.ord_idx = -1;
+    for (int c = 0; c < pl.k_dense; ++c) d.ord_cls[c] = pl.ord_cls[c];
 }
 
 static spc_status launch_kmaps(const KmapBatch &b, int max_k_dense, int64_t max_tiles, cudaStream_t st) {
-    static int configured = 0;
-    if (!configured) {
-        SPC_CUDA(cudaFuncSetAttribute(k_kmap_zdelta, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)kmap_smem_bytes(SPC_MAX_KVOL)));
-        configured = 1;
-    }
+    (void)max_k_dense;
     k_kmap_prep<<<b.n_maps > 0 ? b.n_maps : 1, 256, 0, st>>>(b);
     SPC_LAUNCH_CHECK("k_kmap_prep");
-    const size_t smem = kmap_smem_bytes(max_k_dense);
-    int per_sm = (int)((228 * 1024) / (smem + 4096));
-    if (per_sm < 1) per_sm = 1;
-    if (per_sm > 8) per_sm = 8;
-    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(max_tiles, (int64_t)num_sms() * per_sm));
-    k_kmap_zdelta<<<(unsigned)grid, KM_THREADS, smem, st>>>(b);
+    {
+        int64_t items = 0;
+        for (int m = 0; m < b.n_maps; ++m) items += ((b.d[m].n_out_cap + KM_BM - 1) / KM_BM) * 2 * b.d[m].K * b.d[m].K;
+        const int g = (int)std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, 16 * (int64_t)num_sms()));
+        k_kmap_bounds<<<g, 256, 0, st>>>(b);
+        SPC_LAUNCH_CHECK("k_kmap_bounds");
+    }
+    // one warp per (tile, group) task; enough CTAs to fill every SM (static task stride)
+    int per_sm = 0;
+    SPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_kmap_zdelta, KM_THREADS, 0));
+    int64_t tasks = 0;
+    for (int m = 0; m < b.n_maps; ++m) tasks += ((b.d[m].n_out_cap + KM_BM - 1) / KM_BM) * b.d[m].K * b.d[m].K;
+    (void)max_tiles;
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((tasks + KM_WARPS - 1) / KM_WARPS,
+                                                                (int64_t)num_sms() * std::max(1, per_sm)));
+    k_kmap_zdelta<<<(unsigned)grid, KM_THREADS, 0, st>>>(b);
     SPC_LAUNCH_CHECK("k_kmap_zdelta");
     return SPC_OK;
 }
@@ -669,7 +714,8 @@ extern "C" spc_status spc_build_kmap(const uint64_t *in_keys, int64_t n_in, cons
     }
     OrderJob job;
     memset(&job, 0, sizeof(job));
-    const bool order = wants_order(pl, flags) && n_out > 0;
+    // a batch orders at most ORD_MAX maps (one tag each); later ones keep the canonical order
+    const bool order = wants_order(pl, flags) && n_out > 0 && (!g_defer.active || g_defer.orders.size() < ORD_MAX);
     if (order) {
         km.os_rows = reinterpret_cast<int32_t *>(base + L.rows);
         km.os_table_ord = reinterpret_cast<int32_t *>(base + L.os_ord);
@@ -682,7 +728,6 @@ extern "C" spc_status spc_build_kmap(const uint64_t *in_keys, int64_t n_in, cons
         job.n_cap = n_out;
         job.k_dense = pl.k_dense;
         job.words = L.words;
-        for (int c = 0; c < pl.k_dense; ++c) job.cls[c] = pl.ord_cls[c];
     }
     if (n_out == 0) {
         SPC_CUDA(cudaMemsetAsync(base + L.counts, 0, L.stats + 2 * sizeof(unsigned long long) - L.counts, st));
@@ -704,10 +749,14 @@ extern "C" spc_status spc_build_kmap(const uint64_t *in_keys, int64_t n_in, cons
         } else if (b.bits_y != spec.bits_y || b.bits_z != spec.bits_z) {
             return fail(SPC_ERR_INVALID_ARG, "batched kernel maps must share one pack spec");
         }
-        fill_desc(b.d[b.n_maps++], km, pl);
+        KmapDesc &d = b.d[b.n_maps++];
+        fill_desc(d, km, pl, reinterpret_cast<int32_t *>(base + L.bounds));
         g_defer.max_kd = std::max(g_defer.max_kd, pl.k_dense);
         g_defer.tiles += (int64_t)L.tiles;
-        if (order) g_defer.orders.push_back(job);
+        if (order) {
+            d.ord_idx = (int8_t)g_defer.orders.size();
+            g_defer.orders.push_back(job);
+        }
         return SPC_OK;
     }
     KmapBatch b;
@@ -716,20 +765,29 @@ extern "C" spc_status spc_build_kmap(const uint64_t *in_keys, int64_t n_in, cons
     b.bits_y = spec.bits_y;
     b.bits_z = spec.bits_z;
     b.work_ctr = reinterpret_cast<unsigned int *>(base + L.stats) + 4;   // scratch after the stats
-    fill_desc(b.d[0], km, pl);
+    fill_desc(b.d[0], km, pl, reinterpret_cast<int32_t *>(base + L.bounds));
+    OrderScratch os{};
+    if (order) {
+        os = order_scratch(base + L.scratch, L.scratch_bytes, n_out);
+        if (!os.ok) return fail(SPC_ERR_WORKSPACE, "spc_build_kmap: density-order scratch too small");
+        b.d[0].ord_idx = 0;
+        b.ord_keys = os.keys;
+        b.ord_total = os.total;
+        b.ord_key_bits = ord_key_bits(1);
+    }
     s = launch_kmaps(b, pl.k_dense, (int64_t)L.tiles, st);
-    if (s == SPC_OK && order) s = run_orders(std::vector<OrderJob>{job}, base + L.scratch, L.scratch_bytes, st);
+    if (s == SPC_OK && order) s = run_orders(std::vector<OrderJob>{job}, os, n_out, st);
     return s;
 }
 
 namespace spc {
-void kmap_defer_begin(void *order_scratch, size_t order_scratch_bytes) {
+void kmap_defer_begin(void *scratch, size_t scratch_bytes, int64_t order_rows) {
     memset(&g_defer.b, 0, sizeof(g_defer.b));
     g_defer.max_kd = 0;
     g_defer.tiles = 0;
     g_defer.orders.clear();
-    g_defer.scratch = order_scratch;
-    g_defer.scratch_bytes = order_scratch_bytes;
+    g_defer.order_rows = order_rows;
+    g_defer.scratch = order_rows > 0 ? order_scratch(scratch, scratch_bytes, order_rows) : OrderScratch{};
     g_defer.active = true;
 }
 size_t kmap_bytes_batched(spc_geom geom, int32_t t, uint32_t flags, int64_t n_out) {
@@ -747,8 +805,15 @@ void kmap_defer_abort() { g_defer.active = false; }
 spc_status kmap_defer_end(cudaStream_t st) {
     g_defer.active = false;
     if (g_defer.b.n_maps == 0) return SPC_OK;
-    spc_status s = launch_kmaps(g_defer.b, g_defer.max_kd, g_defer.tiles, st);
-    if (s == SPC_OK && !g_defer.orders.empty()) s = run_orders(g_defer.orders, g_defer.scratch, g_defer.scratch_bytes, st);
+    KmapBatch &b = g_defer.b;
+    if (!g_defer.orders.empty()) {
+        if (!g_defer.scratch.ok) return fail(SPC_ERR_WORKSPACE, "network kmaps: density-order scratch too small");
+        b.ord_keys = g_defer.scratch.keys;
+        b.ord_total = g_defer.scratch.total;
+        b.ord_key_bits = ord_key_bits((int)g_defer.orders.size());
+    }
+    spc_status s = launch_kmaps(b, g_defer.max_kd, g_defer.tiles, st);
+    if (s == SPC_OK) s = run_orders(g_defer.orders, g_defer.scratch, g_defer.order_rows, st);
     return s;
 }
 }  // namespace spc
