@@ -73,6 +73,7 @@ class _Kmap(ctypes.Structure):
                 ("os_table", ctypes.c_void_p), ("ws_pairs", ctypes.c_void_p), ("counts_dev", ctypes.c_void_p),
                 ("tile_mask_dev", ctypes.c_void_p), ("search_stats_dev", ctypes.c_void_p),
                 ("os_rows", ctypes.c_void_p), ("os_table_ord", ctypes.c_void_p), ("tile_mask_ord", ctypes.c_void_p),
+                ("tile_order", ctypes.c_void_p),
                 ("dense_k", ctypes.c_int16 * SPC_MAX_KVOL), ("list_k", ctypes.c_int16 * SPC_MAX_KVOL),
                 ("list_mirror", ctypes.c_int8 * SPC_MAX_KVOL)]
 

@@ -33,6 +33,7 @@ constexpr int TC_THREADS = 480;   // 15 warps: 8 gather, 4 epilogue, MMA, weight
 constexpr int N_GATHER = 8;        // gather warps (two per SM sub-partition)
 constexpr int TC_BM = 128;
 constexpr int TC_SMEM_BUDGET = 225 * 1024;
+constexpr int CTR_EXIT = 254, CTR_FETCH = 255;   // ws counter slots (split tiles use [0, 254))
 
 enum OutKind : int { OUT_FINAL = 0, OUT_F32_STORE = 1, OUT_F32_RED = 2 };
 
@@ -42,6 +43,8 @@ struct ConvParams {
     // map
     const int32_t *os;
     const int32_t *os_rows;   // OS density order: table row -> output row (NULL: identity)
+    const int32_t *tile_order;   // OS density order: [2][tiles128] heaviest-first tile orders (or NULL)
+    int64_t tiles128_cap;
     int k_dense;
     const uint32_t *tile_mask;
     int tile_words;
@@ -73,7 +76,8 @@ struct ConvParams {
     int num_sms;
     float *acc;           // fp32 split-K accumulator (all-zero on entry, left all-zero)
     int64_t ld_acc;
-    int *tile_ctr;        // per output tile arrival counters (zero on entry, left zero)
+    int *tile_ctr;        // ws counters (zero on entry, left zero): [0, 254) split-tile arrivals,
+                          // [254] CTAs exited, [255] dynamic tile fetch
     int blk_slots;        // gather-index blocks in flight (2, or 1 when a block is large: K=5 OS)
     uint32_t tmem_cols;   // per 128-row accumulator (power of two >= 32)
     uint32_t idesc;
@@ -105,7 +109,8 @@ __device__ __forceinline__ void decode_tile(const ConvParams &p, int64_t v, cons
     const int64_t tv = v / p.n_ntiles;
     if (p.mode == 0) {
         t.list = (int)(tv % split);   // OS: split index of the tile's active offsets
-        const int64_t rt = tv / split;
+        int64_t rt = tv / split;
+        if (p.tile_order) rt = p.tile_order[(tr == 256 ? p.tiles128_cap : 0) + rt];   // heaviest first
         t.row0 = rt * tr;
         t.rows = (int)imin64(tr, n_out - t.row0);
         t.dir = 0;
@@ -229,6 +234,7 @@ struct ConvSmem {
     uint64_t full[16], empty[16], tfull[2], tempty[2];
     uint64_t trec_full[TREC_SLOTS], trec_empty[TREC_SLOTS];
     uint64_t blk_full[BLK_SLOTS], blk_empty[BLK_SLOTS];
+    uint64_t tstart;               // one phase per tile the gather warps begin (claim gate)
     uint32_t tmem_holder[4];
     int tr, split;                 // device-chosen tile rows / OS split (see geometry below)
     int64_t n_tiles;
@@ -237,6 +243,19 @@ struct ConvSmem {
     TileRec trec[TREC_SLOTS];
 };
 
+#ifdef SPC_EXP_TRACE2
+// per-CTA timeline (globaltimer ns): 0 entry, 1 after setup sync, 2 first stage full (MMA),
+// 3 last commit, 4 exit, 5 tiles done, 6 stages done
+__device__ unsigned long long g_tl[8][1024];
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define TL(slot, v) do { if (blockIdx.x < 1024) g_tl[slot][blockIdx.x] = (v); } while (0)
+#else
+#define TL(slot, v) do {} while (0)
+#endif
 #ifdef SPC_EXP_TRACE
 __device__ long long g_tr[8][4096];
 #define TR(slot, i) do { if (blockIdx.x == 0 && (i) < 4096) g_tr[slot][(i)] = clock64(); } while (0)
@@ -378,6 +397,7 @@ __device__ __forceinline__ void gather_role(const ConvParams &p, ConvSmem &cs, c
         ptx::mbar_wait(ptx::smem_u32(&cs.trec_full[st]), (ti / TREC_SLOTS) & 1);
         const TileRec &R = cs.trec[st];
         if (R.end) break;
+        if (warp == 0 && lane == 0) ptx::mbar_arrive(ptx::smem_u32(&cs.tstart));
         const int rows = R.rows, ncols = R.ncols;
         const int bs = ti % p.blk_slots;
         ptx::mbar_wait(ptx::smem_u32(&cs.blk_full[bs]), (ti / p.blk_slots) & 1);
@@ -475,6 +495,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     const int blk_stride = (BM * kd + 3) & ~3;      // int32 per block (16-byte multiple)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef SPC_EXP_TRACE2
+    if (threadIdx.x == 0) TL(0, gtime());
+#endif
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < 16; ++s) {
@@ -493,6 +516,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             ptx::mbar_init(ptx::smem_u32(&cs.blk_full[i]), 32);
             ptx::mbar_init(ptx::smem_u32(&cs.blk_empty[i]), N_GATHER);
         }
+        ptx::mbar_init(ptx::smem_u32(&cs.tstart), 1);
         ptx::fence_mbar_init();
         ptx::fence_proxy_async();
     }
@@ -559,6 +583,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = cs.tmem_holder[0];
+#ifdef SPC_EXP_TRACE2
+    if (threadIdx.x == 0) TL(1, gtime());
+#endif
     constexpr uint32_t rb = BK * 2;           // bytes per operand row (= swizzle span)
     const int tr = cs.tr, split = cs.split, nht = tr / TC_BM;
     // the ring carve of this tile height
@@ -575,10 +602,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     if (warp == W_SCHED) {
         // ===================== scheduler: tile records + gather indices ==================
         const int64_t n_tiles = cs.n_tiles;
+        // tiles are claimed dynamically from a ws counter (heaviest first after the density
+        // order), so uneven tiles balance across SMs; static round-robin without a ws
+        int *fetch = p.tile_ctr ? p.tile_ctr + CTR_FETCH : nullptr;
         uint32_t ti = 0;
-        for (int64_t v = blockIdx.x;; v += gridDim.x, ++ti) {
+        for (int64_t vs = blockIdx.x;; vs += gridDim.x, ++ti) {
             const int st = ti % TREC_SLOTS;
             ptx::mbar_wait_sleep(ptx::smem_u32(&cs.trec_empty[st]), ((ti / TREC_SLOTS) & 1) ^ 1);
+            int64_t v = vs;
+            if (fetch) {
+                // claim gate: at most one tile claimed beyond the one the gather warps are on
+                if (ti > 0) ptx::mbar_wait(ptx::smem_u32(&cs.tstart), (ti - 1) & 1);
+                int x = 0;
+                if (lane == 0) x = atomicAdd(fetch, 1);
+                v = __shfl_sync(0xffffffffu, x, 0);
+            }
             TileRec &R = cs.trec[st];
             if (v >= n_tiles) {
                 if (lane == 0) R.end = 1;
@@ -685,10 +723,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                     const int s = it % S;
                     ptx::mbar_wait(ptx::smem_u32(&cs.full[s]), (it / S) & 1);
                     TR(2, it);
+#ifdef SPC_EXP_TRACE2
+                    if (it == 0) TL(2, gtime());
+#endif
                     // the A tile was written by cp.async / st.shared (generic proxy): order it
                     // before the tensor core's async-proxy reads
                     ptx::fence_proxy_async();
                     ptx::tc_fence_after();
+                    TR(4, it);
                     const uint32_t a_base = ptx::smem_u32(sa + (size_t)s * a_bytes);
                     const uint32_t b_base = ptx::smem_u32(sb + (size_t)s * b_bytes);
                     for (int kb = 0; kb < nin; ++kb) {
@@ -707,10 +749,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                             acc = 1;
                         }
                     }
+                    TR(5, it);
                     ptx::mma_commit(ptx::smem_u32(&cs.empty[s]));
                     TR(3, it);
                 }
                 ptx::mma_commit(ptx::smem_u32(&cs.tfull[a]));
+#ifdef SPC_EXP_TRACE2
+                TL(3, gtime());
+                TL(5, ti + 1);
+                TL(6, it);
+#endif
                 ptx::mbar_arrive(ptx::smem_u32(&cs.trec_empty[st]));
             }
             __syncwarp();
@@ -727,6 +775,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     if (warp == W_MMA) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem_base, 2 * NH * p.tmem_cols);
+    }
+#ifdef SPC_EXP_TRACE2
+    if (threadIdx.x == 0) TL(4, gtime());
+#endif
+    if (p.tile_ctr && threadIdx.x == 0) {
+        // the last CTA out returns the fetch / exit counters to zero (ws contract); every
+        // CTA's scheduler has made its final claim before its CTA gets here
+        __threadfence();
+        if (atomicAdd(p.tile_ctr + CTR_EXIT, 1) == (int)gridDim.x - 1) {
+            atomicExch(p.tile_ctr + CTR_FETCH, 0);
+            atomicExch(p.tile_ctr + CTR_EXIT, 0);
+        }
     }
 }
 
@@ -992,6 +1052,8 @@ static void fill_map_params(ConvParams &p, const spc_kmap *km) {
     p.os_rows = ord ? km->os_rows : nullptr;
     p.k_dense = km->k_dense;
     p.tile_mask = ord ? km->tile_mask_ord : km->tile_mask_dev;
+    p.tile_order = ord ? km->tile_order : nullptr;
+    p.tiles128_cap = (km->n_out + 127) / 128;
     p.tile_words = km->tile_words;
     p.pairs = reinterpret_cast<const int2 *>(km->ws_pairs);
     p.list_stride = km->n_out;
@@ -1220,6 +1282,17 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
     return SPC_OK;
 }
 
+#ifdef SPC_EXP_TRACE2
+extern "C" int spc_exp_tl_read(unsigned long long *host) {
+    cudaMemcpyFromSymbol(host, spc::g_tl, sizeof(spc::g_tl));
+    return (int)cudaMemset(nullptr, 0, 0);
+}
+extern "C" int spc_exp_tl_clear() {
+    void *p;
+    cudaGetSymbolAddress(&p, spc::g_tl);
+    return (int)cudaMemset(p, 0, sizeof(spc::g_tl));
+}
+#endif
 #ifdef SPC_EXP_TRACE
 extern "C" int spc_exp_trace_read(long long *host) {
     return (int)cudaMemcpyFromSymbol(host, spc::g_tr, sizeof(spc::g_tr));

@@ -50,6 +50,8 @@ struct KmapDesc {
     int8_t transposed, halved;
     int8_t ord_idx;                 // density order: index among the ordered maps (-1: none)
     int8_t ord_cls[SPC_MAX_KVOL];   // density-order key bit of each dense column (-1: none)
+    int8_t dcol[SPC_MAX_KVOL];      // weight offset -> dense column (-1: not dense)
+    int8_t lst[SPC_MAX_KVOL];       // weight offset -> stored WS list (-1: none)
 };
 
 constexpr int KM_MAX_MAPS = 24;
@@ -61,7 +63,7 @@ struct KmapBatch {
     // density order: keys of all ordered maps, concatenated in ord_idx order by live counts
     uint64_t *ord_keys;
     int64_t *ord_total;       // sum of their live rows (written by k_kmap_prep)
-    int ord_key_bits;         // mask bits below the map tag
+    int ord_key_bits;         // bit of the map tag (direction mask below, then the weight field)
     KmapDesc d[KM_MAX_MAPS];
 };
 
@@ -199,10 +201,12 @@ __device__ __forceinline__ void zdelta_task(const KmapBatch &B, const KmapDesc &
     for (int mm = 0; mm < K; ++mm) dl[mm] = group_delta(p, B.bits_y, B.bits_z, g, mm);
     uint32_t colbal[K];
     int cnt[K];
+    int32_t jj[KM_BM / 32][K];       // WS matches of the task, written after one reservation per offset
 #pragma unroll
     for (int mm = 0; mm < K; ++mm) { colbal[mm] = 0u; cnt[mm] = 0; }
     const bool ord = p.ord_idx >= 0;
-    for (int ch = 0; ch * 32 < rows; ++ch) {
+#pragma unroll
+    for (int ch = 0; ch < KM_BM / 32; ++ch) {
         const int lr = ch * 32 + lane;
         const bool valid = lr < rows;
         const int64_t i = row0 + lr;
@@ -225,22 +229,36 @@ __device__ __forceinline__ void zdelta_task(const KmapBatch &B, const KmapDesc &
             const unsigned bal = __ballot_sync(0xffffffffu, match);
             cnt[mm] += __popc(bal);
             const int col = dcol[ks[mm]];
+            jj[ch][mm] = j;
             if (col >= 0) {
                 if (valid) p.os[i * KD + col] = j;
                 colbal[mm] |= bal;
-                if (ord && match && p.ord_cls[col] >= 0) key |= 1u << (p.ord_cls[col] % B.ord_key_bits);
-            } else {
-                const int l = lstv[ks[mm]];
-                if (l >= 0 && bal) {
-                    int base = 0;
-                    if (lane == 0) base = atomicAdd(&p.counts[SPC_MAX_KVOL + l], __popc(bal));
-                    base = __shfl_sync(0xffffffffu, base, 0);
-                    if (match)
-                        p.pairs[(int64_t)l * p.list_stride + base + __popc(bal & lanemask_lt())] = make_int2(j, (int32_t)i);
-                }
+                if (ord && match && p.ord_cls[col] >= 0) key |= 1u << p.ord_cls[col];
             }
         }
         if (ord && key) atomicOr(reinterpret_cast<unsigned long long *>(&B.ord_keys[ordbase + i]), (unsigned long long)key);
+    }
+    // WS pairs: one reservation per stored offset per task (issued together), then writes
+    int base[K];
+#pragma unroll
+    for (int mm = 0; mm < K; ++mm) {
+        base[mm] = 0;
+        const int l = lstv[ks[mm]];
+        if (l >= 0 && dcol[ks[mm]] < 0 && cnt[mm] && lane == 0) base[mm] = atomicAdd(&p.counts[SPC_MAX_KVOL + l], cnt[mm]);
+    }
+#pragma unroll
+    for (int mm = 0; mm < K; ++mm) {
+        const int l = lstv[ks[mm]];
+        if (l < 0 || dcol[ks[mm]] >= 0 || !cnt[mm]) continue;
+        int b = __shfl_sync(0xffffffffu, base[mm], 0);
+#pragma unroll
+        for (int ch = 0; ch < KM_BM / 32; ++ch) {
+            const uint32_t bal = __ballot_sync(0xffffffffu, jj[ch][mm] >= 0);
+            if (jj[ch][mm] >= 0)
+                p.pairs[(int64_t)l * p.list_stride + b + __popc(bal & lanemask_lt())] =
+                    make_int2(jj[ch][mm], (int32_t)(row0 + ch * 32 + lane));
+            b += __popc(bal);
+        }
     }
     if (lane == 0) {
 #pragma unroll
@@ -253,7 +271,10 @@ __device__ __forceinline__ void zdelta_task(const KmapBatch &B, const KmapDesc &
     (void)m;
 }
 
-__global__ void __launch_bounds__(KM_THREADS, 4) k_kmap_zdelta(const __grid_constant__ KmapBatch B) {
+#ifndef SPC_KM_MIN_BLOCKS
+#define SPC_KM_MIN_BLOCKS 3
+#endif
+__global__ void __launch_bounds__(KM_THREADS, SPC_KM_MIN_BLOCKS) k_kmap_zdelta(const __grid_constant__ KmapBatch B) {
     __shared__ int8_t s_dcol[KM_MAX_MAPS][SPC_MAX_KVOL];   // weight offset -> dense column / -1
     __shared__ int8_t s_lst[KM_MAX_MAPS][SPC_MAX_KVOL];    // weight offset -> WS list / -1
     __shared__ int64_t s_pre[KM_MAX_MAPS + 1];             // task prefix (tiles * K^2)
@@ -261,26 +282,11 @@ __global__ void __launch_bounds__(KM_THREADS, 4) k_kmap_zdelta(const __grid_cons
     __shared__ __align__(16) uint64_t s_win[KM_WARPS][KM_WWIN];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // ---- prologue: per-map offset tables (same rule as make_plan) ----------------------
-    for (int e = tid; e < B.n_maps * 128; e += KM_THREADS) {
-        const int m = e >> 7, k = e & 127;
-        const KmapDesc &p = B.d[m];
-        const int K = p.K, r = (K - 1) / 2, kv = K * K * K, centre = (kv - 1) / 2;
-        if (k >= kv) continue;
-        int nd = 0, nl = 0, dcol = -1, lst = -1;
-        for (int k2 = 0; k2 <= k; ++k2) {
-            const int l1 = abs(k2 / (K * K) - r) + abs((k2 / K) % K - r) + abs(k2 % K - r);
-            const bool dense = l1 < p.t_eff;
-            const bool stored = !dense && (!p.halved || k2 <= centre);
-            if (k2 == k) {
-                dcol = dense ? nd : -1;
-                lst = stored ? nl : -1;
-            }
-            nd += dense;
-            nl += stored;
-        }
-        s_dcol[m][k] = (int8_t)dcol;
-        s_lst[m][k] = (int8_t)lst;
+    // ---- prologue: per-map offset tables (planned on the host, make_plan) --------------
+    for (int e = tid; e < B.n_maps * SPC_MAX_KVOL; e += KM_THREADS) {
+        const int m = e / SPC_MAX_KVOL, k = e - m * SPC_MAX_KVOL;
+        s_dcol[m][k] = B.d[m].dcol[k];
+        s_lst[m][k] = B.d[m].lst[k];
     }
     if (tid == 0) {
         int64_t acc = 0, ob = 0;
@@ -346,6 +352,7 @@ struct OrderJob {
     int32_t *os_ord;
     uint32_t *mask_ord;
     int32_t *rows;
+    int32_t *tile_order;      // [2][tiles128]
     const int64_t *n_dev;
     int64_t n_cap;
     int64_t tile0;            // first permute CTA of this map
@@ -383,7 +390,20 @@ static int ord_tag_bits(int n_jobs) {
     while ((1 << t) < n_jobs) ++t;
     return t;
 }
-static int ord_key_bits(int n_jobs) { return 16 - ord_tag_bits(n_jobs); }   // 2 radix passes
+// key = [map tag | 16 - popcount(dirs) (5 bits) | dirs (16 bits)]: heaviest rows first, then
+// grouped by direction pattern; <= 24 bits = 3 radix passes
+constexpr int ORD_DIR_BITS = 16, ORD_TAG_SHIFT = 21;
+static int ord_key_bits(int n_jobs) { (void)n_jobs; return ORD_TAG_SHIFT; }
+
+// weight field of every key (the build ORs only the direction bits in)
+__global__ void k_ord_weight(uint64_t *__restrict__ keys, const int64_t *total) {
+    const int64_t n = *total;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = keys[i];
+        const uint32_t dirs = (uint32_t)k & ((1u << ORD_DIR_BITS) - 1);
+        keys[i] = k | ((uint64_t)(ORD_DIR_BITS - __popc(dirs)) << ORD_DIR_BITS);
+    }
+}
 
 __device__ __forceinline__ int64_t ord_base(const OrderBatch &B, int job, int64_t &n_job) {
     int64_t base = 0;
@@ -441,6 +461,44 @@ __global__ void __launch_bounds__(128) k_ord_permute(const __grid_constant__ Ord
     }
 }
 
+// tile orders of one map (CTA pair per map: 128-row tiles, 256-row tiles): tiles by
+// descending weight = popcount of the tile mask (the number of offset slices a conv CTA
+// runs for it), so a dynamic scheduler claiming them in this order balances like LPT.
+// Equal weights in any order (the conv's result does not depend on the tile order).
+__global__ void __launch_bounds__(1024) k_ord_tiles(const __grid_constant__ OrderBatch B) {
+    __shared__ int hist[SPC_MAX_KVOL + 2];
+    const OrderJob &J = B.j[blockIdx.x >> 1];
+    const int T = (blockIdx.x & 1) ? 256 : 128, f = T / 128;
+    const int64_t n = dev_count(J.n_cap, J.n_dev);
+    const int64_t tiles128 = (J.n_cap + 127) / 128;
+    const int64_t nt = (n + T - 1) / T, nt128 = (n + 127) / 128;
+    int32_t *order = J.tile_order + (f == 2 ? tiles128 : 0);
+    for (int i = threadIdx.x; i < SPC_MAX_KVOL + 2; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    auto weight = [&](int64_t t) {
+        int w = 0;
+        for (int q = 0; q < J.words; ++q) {
+            uint32_t m = 0;
+            for (int h = 0; h < f; ++h)
+                if (t * f + h < nt128) m |= J.mask_ord[(t * f + h) * J.words + q];
+            w += __popc(m);
+        }
+        return min(w, SPC_MAX_KVOL);
+    };
+    for (int64_t t = threadIdx.x; t < nt; t += blockDim.x) atomicAdd(&hist[SPC_MAX_KVOL - weight(t)], 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int i = 0; i <= SPC_MAX_KVOL; ++i) {
+            const int c = hist[i];
+            hist[i] = acc;
+            acc += c;
+        }
+    }
+    __syncthreads();
+    for (int64_t t = threadIdx.x; t < nt; t += blockDim.x) order[atomicAdd(&hist[SPC_MAX_KVOL - weight(t)], 1)] = (int32_t)t;
+}
+
 // scratch of one grouped order over `rows_cap` concatenated rows
 static size_t order_scratch_bytes(int64_t rows_cap) {
     Sizer z;
@@ -465,11 +523,16 @@ static spc_status run_orders(const std::vector<OrderJob> &jobs, const OrderScrat
         B.j[q].tile0 = tiles;
         tiles += (B.j[q].n_cap + 127) / 128;
     }
-    spc_status s = radix_sort(o.keys, nullptr, rows_cap, o.total, 16, o.keys_sorted, o.pos, o.rws, o.rws_bytes, st,
-                              false);
+    k_ord_weight<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((rows_cap + 255) / 256, 4 * (int64_t)num_sms())), 256,
+                   0, st>>>(o.keys, o.total);
+    SPC_LAUNCH_CHECK("k_ord_weight");
+    spc_status s = radix_sort(o.keys, nullptr, rows_cap, o.total, ORD_TAG_SHIFT + ord_tag_bits(B.n_jobs), o.keys_sorted,
+                              o.pos, o.rws, o.rws_bytes, st, false);
     if (s != SPC_OK) return s;
     k_ord_permute<<<(unsigned)tiles, 128, 0, st>>>(B, o.pos);
     SPC_LAUNCH_CHECK("k_ord_permute");
+    k_ord_tiles<<<(unsigned)(2 * B.n_jobs), 1024, 0, st>>>(B);
+    SPC_LAUNCH_CHECK("k_ord_tiles");
     return SPC_OK;
 }
 
@@ -550,7 +613,7 @@ static spc_status make_plan(const spc_geom &g, int32_t t, uint32_t flags, KmapPl
 
 struct KmapLayout {
     size_t os, pairs, counts, mask, stats, bounds, total;
-    size_t rows, os_ord, mask_ord, scratch, scratch_bytes;   // density order
+    size_t rows, os_ord, mask_ord, tile_order, scratch, scratch_bytes;   // density order
     int64_t tiles;
     int words;
 };
@@ -575,6 +638,7 @@ static KmapLayout layout_of(const KmapPlan &pl, int64_t n_out, uint32_t flags, b
         L.rows = take(sizeof(int32_t) * (size_t)n_out);
         L.os_ord = take(sizeof(int32_t) * (size_t)n_out * pl.k_dense);
         L.mask_ord = take(sizeof(uint32_t) * (size_t)(L.tiles * L.words));
+        L.tile_order = take(sizeof(int32_t) * 2 * (size_t)L.tiles);
         if (scratch) {
             L.scratch_bytes = order_scratch_bytes(n_out);
             L.scratch = take(L.scratch_bytes);
@@ -621,6 +685,10 @@ static void fill_desc(KmapDesc &d, const spc_kmap &km, const KmapPlan &pl, int32
     d.halved = (int8_t)pl.halved;
     d.ord_idx = -1;
     for (int c = 0; c < pl.k_dense; ++c) d.ord_cls[c] = pl.ord_cls[c];
+    for (int k = 0; k < SPC_MAX_KVOL; ++k) {
+        d.dcol[k] = (int8_t)(k < pl.k_vol ? pl.dense_col[k] : -1);
+        d.lst[k] = (int8_t)(k < pl.k_vol ? pl.list_id[k] : -1);
+    }
 }
 
 static spc_status launch_kmaps(const KmapBatch &b, int max_k_dense, int64_t max_tiles, cudaStream_t st) {
@@ -720,6 +788,8 @@ extern "C" spc_status spc_build_kmap(const uint64_t *in_keys, int64_t n_in, cons
         km.os_rows = reinterpret_cast<int32_t *>(base + L.rows);
         km.os_table_ord = reinterpret_cast<int32_t *>(base + L.os_ord);
         km.tile_mask_ord = reinterpret_cast<uint32_t *>(base + L.mask_ord);
+        km.tile_order = reinterpret_cast<int32_t *>(base + L.tile_order);
+        job.tile_order = km.tile_order;
         job.os = km.os_table;
         job.os_ord = km.os_table_ord;
         job.mask_ord = km.tile_mask_ord;

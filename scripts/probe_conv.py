@@ -22,6 +22,7 @@ ap.add_argument("--halve", type=int, default=1)
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--config", type=int, default=2)
 ap.add_argument("--n", type=int, default=0, help="keep the first n points of the scan")
+ap.add_argument("--order", type=int, default=1, help="SPC_KMAP_DENSITY_ORDER")
 a = ap.parse_args()
 
 coords = synth.make_scan(a.config, 0)
@@ -29,7 +30,8 @@ if a.n:
     coords = coords[:a.n]
 spec = spc.spc_plan_pack(coords[:, 1:].min(0), coords[:, 1:].max(0), 1, 16, 16)
 keys, perm, _ = spc.spc_pack_sort(torch.from_numpy(coords).cuda(), spec)
-km = spc.spc_build_kmap(keys, keys, spec, spc.Geom(a.K, 1, 1, 1, 0), a.t, spc.SPC_KMAP_HALVE_SYMMETRIC if a.halve else 0)
+km = spc.spc_build_kmap(keys, keys, spec, spc.Geom(a.K, 1, 1, 1, 0), a.t,
+                        (spc.SPC_KMAP_HALVE_SYMMETRIC if a.halve else 0) | (spc.SPC_KMAP_DENSITY_ORDER if a.order else 0))
 n = keys.shape[0]
 F = torch.randn(n, a.cin, device="cuda").bfloat16()
 W = spc.spc_prepare_weight((torch.randn(a.K ** 3, a.cin, a.cout, device="cuda") * 0.05).bfloat16())

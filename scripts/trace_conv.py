@@ -11,7 +11,7 @@ L = spc.lib()
 buf = np.zeros((8, 4096), np.int64)
 L.spc_exp_trace_read.argtypes = [ctypes.c_void_p]
 L.spc_exp_trace_read(buf.ctypes.data)
-names = {0: "p_col", 4: "p_pre_wait", 1: "p_post_wait", 5: "p_issued", 2: "mma_full", 3: "mma_commit", 6: "epi_tfull", 7: "epi_done"}
+names = {2: "mma_full", 4: "fenced", 5: "issued", 3: "committed", 6: "epi_tfull", 7: "epi_done"}
 t0 = buf[buf > 0].min()
 for i in range(0, 40):
     print(i, " ".join(f"{n}={(buf[k, i] - t0) if buf[k, i] else -1:8d}" for k, n in names.items()))

@@ -172,10 +172,11 @@ def test_kmap_os_table_exact_and_centre():
 @pytest.mark.parametrize("K,kind,t", [(3, "subm", -1), (3, "subm", 2), (5, "subm", 3), (3, "strided", -1),
                                       (3, "transposed", -1)])
 def test_kmap_density_order_exact(K, kind, t):
-    """SPC_KMAP_DENSITY_ORDER: os_rows is the STABLE sort of the outputs by their direction
-    key (bit j set iff the output matches offset k or its mirror K^3-1-k, j = rank of the
-    pair min(k, mirror) among the pairs with a dense member, the submanifold centre pair
-    skipped, folded mod 16) -- unique, so checked bit-exactly against numpy's stable
+    """SPC_KMAP_DENSITY_ORDER: os_rows is the STABLE sort of the outputs by the key
+    ((16 - popcount(dirs)) << 16) | dirs, dirs bit j set iff the output matches offset k or
+    its mirror K^3-1-k (j = rank of the pair min(k, mirror) among the pairs with a dense
+    member, the submanifold centre pair skipped, folded mod 16): most directions first,
+    then grouped by pattern -- unique, so checked bit-exactly against numpy's stable
     argsort of the oracle map; the ordered table is the canonical one permuted; tile
     masks are the OR of each 128-row tile."""
     coords = synth.make_scan(1, 1)
@@ -209,6 +210,8 @@ def test_kmap_density_order_exact(K, kind, t):
         pr = min(k, kv - 1 - k)
         if pr in rank:
             key |= (full[:, c] >= 0).astype(np.int64) << rank[pr]
+    pop = np.array([bin(int(x)).count("1") for x in key])
+    key = ((16 - pop) << 16) | key
     np.testing.assert_array_equal(rows, np.argsort(key, kind="stable"))
     np.testing.assert_array_equal(tab_ord, full[rows])
     pad = (-n) % 128
