@@ -206,7 +206,8 @@ typedef struct {
     int32_t *os_table_ord;   /* [n_out * k_dense] OS table in density order          */
     uint32_t *tile_mask_ord; /* tile masks of the density order                      */
     int32_t *tile_order;     /* density order: 128-row tiles by descending weight (popcount
-                              * of the tile mask), then 256-row tiles likewise ([2][ceil(n_out/128)]) */
+                              * of the tile mask), then 256-row tiles likewise; then the
+                              * weights in those two orders ([4][ceil(n_out/128)])           */
     int16_t dense_k[SPC_MAX_KVOL];
     int16_t list_k[SPC_MAX_KVOL];
     int8_t list_mirror[SPC_MAX_KVOL];

@@ -33,7 +33,9 @@ constexpr int TC_THREADS = 480;   // 15 warps: 8 gather, 4 epilogue, MMA, weight
 constexpr int N_GATHER = 8;        // gather warps (two per SM sub-partition)
 constexpr int TC_BM = 128;
 constexpr int TC_SMEM_BUDGET = 225 * 1024;
-constexpr int CTR_EXIT = 254, CTR_FETCH = 255;   // ws counter slots (split tiles use [0, 254))
+constexpr int WS_CTR_SLOTS = 2048;                // ws counters (int32) after the accumulator
+constexpr int CTR_EXIT = WS_CTR_SLOTS - 2, CTR_FETCH = WS_CTR_SLOTS - 1;   // split tiles use [0, 1024)
+constexpr int SPLIT_MAX_TILES = 512;              // weighted split: tiles per launch (x n_ntiles <= 2)
 
 enum OutKind : int { OUT_FINAL = 0, OUT_F32_STORE = 1, OUT_F32_RED = 2 };
 
@@ -73,11 +75,13 @@ struct ConvParams {
     int bm;               // max rows per tile (template BM): 128 or 256 (two M=128 MMAs sharing the weight tile)
     int split_ok;         // OS part may split a tile's offsets over CTAs (needs acc + tile_ctr)
     int force_tr;         // experiments: 128/256 forces the tile rows (0 = device heuristic)
+    int split_min_unit;   // weighted split: minimum offsets per part
+    int split_tiles_per_sm2;   // weighted split when 2 * tiles <= this (default: SM count)
     int num_sms;
     float *acc;           // fp32 split-K accumulator (all-zero on entry, left all-zero)
     int64_t ld_acc;
-    int *tile_ctr;        // ws counters (zero on entry, left zero): [0, 254) split-tile arrivals,
-                          // [254] CTAs exited, [255] dynamic tile fetch
+    int *tile_ctr;        // ws counters (zero on entry, left zero): [0, 1024) split-tile arrivals,
+                          // [CTR_EXIT] CTAs exited, [CTR_FETCH] dynamic tile fetch
     int blk_slots;        // gather-index blocks in flight (2, or 1 when a block is large: K=5 OS)
     uint32_t tmem_cols;   // per 128-row accumulator (power of two >= 32)
     uint32_t idesc;
@@ -97,19 +101,34 @@ struct TileInfo {
     int64_t row0;   // first output (OS) or first pair (WS)
     int rows;
     int nt;         // C_out tile
-    int list, dir, k;
+    int list, dir, k;   // OS: list = split part
+    int nsplit, ctr;    // OS: parts of this tile (split-K) and its arrival counter slot
     uint32_t mask[4];
 };
 
-// virtual tile v -> TileInfo; identical in every role (deterministic).  tr = rows per
-// tile and split = CTAs per OS tile, both chosen on the device from the live counts.
+// virtual tile v -> TileInfo (scheduler warp).  tr = rows per tile, chosen on the device
+// from the live counts; OS: sp_pre/sp_cnt (weighted split, or NULL) give each tile's parts.
 __device__ __forceinline__ void decode_tile(const ConvParams &p, int64_t v, const int *list_prefix, int64_t n_out,
-                                            int tr, int split, TileInfo &t) {
+                                            int tr, const int *sp_pre, const uint16_t *sp_cnt, int n_sp, TileInfo &t) {
     t.nt = (int)(v % p.n_ntiles);
     const int64_t tv = v / p.n_ntiles;
     if (p.mode == 0) {
-        t.list = (int)(tv % split);   // OS: split index of the tile's active offsets
-        int64_t rt = tv / split;
+        int64_t ti = tv;
+        t.list = 0;
+        t.nsplit = 1;
+        if (sp_pre) {   // weighted split: tile = last prefix <= tv
+            int lo = 0, hi = n_sp - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (sp_pre[mid] <= tv) lo = mid;
+                else hi = mid - 1;
+            }
+            ti = lo;
+            t.list = (int)(tv - sp_pre[lo]);
+            t.nsplit = sp_cnt[lo];
+        }
+        t.ctr = (int)(ti * p.n_ntiles + t.nt);
+        int64_t rt = ti;
         if (p.tile_order) rt = p.tile_order[(tr == 256 ? p.tiles128_cap : 0) + rt];   // heaviest first
         t.row0 = rt * tr;
         t.rows = (int)imin64(tr, n_out - t.row0);
@@ -224,7 +243,7 @@ constexpr int W_EPI0 = 8, W_MMA = 12, W_BLOAD = 13, W_SCHED = 14;
 
 struct TileRec {
     int64_t row0;
-    int rows, nt, list, dir, k, end, ncols;
+    int rows, nt, list, dir, k, end, ncols, nsplit, ctr;
     uint32_t mask[4];
     uint8_t cols[128];        // active step columns (OS: dense offsets with a match; WS: {0})
     int32_t scatter[256];     // output row of each tile row (WS pairs; OS with os_rows)
@@ -236,9 +255,12 @@ struct ConvSmem {
     uint64_t blk_full[BLK_SLOTS], blk_empty[BLK_SLOTS];
     uint64_t tstart;               // one phase per tile the gather warps begin (claim gate)
     uint32_t tmem_holder[4];
-    int tr, split;                 // device-chosen tile rows / OS split (see geometry below)
+    int tr, wsplit;                // device-chosen tile rows / weighted OS split active
+    int n_sp;                      // tiles in the weighted split
     int64_t n_tiles;
-    int epi_flag[2], epi_last[2];  // split-K fixup decisions, double-buffered by tile parity
+    int sp_pre[SPLIT_MAX_TILES + 1];       // weighted split: first part of each tile (claim order)
+    uint16_t sp_cnt[SPLIT_MAX_TILES];      // parts of each tile
+    int epi_last[2];               // split-K fixup decisions, double-buffered by tile parity
     int list_prefix[SPC_MAX_KVOL + 1];
     TileRec trec[TREC_SLOTS];
 };
@@ -266,86 +288,76 @@ __device__ long long g_tr[8][4096];
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
 // OS split-K fixup, run by the 4 epilogue warps (thread = tile row within a 128-row half).
-// Every split of an output tile red.adds its partial into the fp32 accumulator and bumps
-// the tile's arrival counter; the split that completes the count reads the sum back, adds
-// the residual, writes the final dtype, and returns the accumulator rows and the counter
-// to zero (so the next launch needs no zero-fill).  A split that finds all others already
-// arrived skips its own red.add and adds its TMEM values directly.
-__device__ __noinline__ void os_split_fixup(const ConvParams &p, ConvSmem &cs, const TileRec &R, uint32_t ti, int tr,
-                                            int split, int nht, uint32_t tmem_tile, int e, int lane) {
+// Every part of an output tile red.adds its partial into the fp32 accumulator, releases
+// its TMEM accumulator at once (the MMA warp moves on), then bumps the tile's arrival
+// counter; the part that completes the count reads the sum back, adds the residual,
+// writes the final dtype, and returns the accumulator rows and the counter to zero (so
+// the next launch needs no zero-fill).
+__device__ __noinline__ void os_split_fixup(const ConvParams &p, ConvSmem &cs, const TileRec &R, uint32_t ti,
+                                            int split, int nht, uint32_t tmem_tile, uint32_t tempty_bar, int e,
+                                            int lane) {
     const int fl = ti & 1;
     const bool lead = threadIdx.x == 32 * W_EPI0;
-    int *ctr = p.tile_ctr + (R.row0 / tr) * p.n_ntiles + R.nt;
-    const bool own = R.ncols > 0;
-    if (lead) {
-        int c;
-        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(c) : "l"(ctr) : "memory");
-        cs.epi_flag[fl] = c == split - 1;
-    }
-    epi_bar();
-    const bool direct = cs.epi_flag[fl] != 0;
-    bool last = direct;
-    if (!direct) {
-        if (own) {
-            for (int h = 0; h < nht; ++h) {
-                const int r = h * TC_BM + e * 32 + lane;
-                const uint32_t tb = tmem_tile + h * p.tmem_cols + ((uint32_t)(e * 32) << 16);
-                for (int col = 0; col < p.BN; col += 32) {
-                    uint32_t v[32];
-                    const int n = min(32, p.BN - col);
-                    if (n == 32) ptx::tmem_ld32(tb + col, v);
-                    else ptx::tmem_ld16(tb + col, v);
-                    ptx::tmem_ld_wait();
-                    if (r < R.rows) {
-                        float *op = p.acc + (R.row0 + r) * p.ld_acc + R.nt * p.BN + col;
-#pragma unroll
-                        for (int q = 0; q < 8; ++q)
-                            if (q * 4 < n) ptx::red_add_v4(op + 4 * q, to_f(v[4 * q]), to_f(v[4 * q + 1]), to_f(v[4 * q + 2]), to_f(v[4 * q + 3]));
-                    }
-                }
-            }
-        }
-        __threadfence();
-        epi_bar();
-        if (lead) {
-            const int old = atomicAdd(ctr, 1);
-            __threadfence();
-            cs.epi_last[fl] = old == split - 1;
-        }
-        epi_bar();
-        last = cs.epi_last[fl] != 0;
-    }
-    if (!last) return;
-    for (int h = 0; h < nht; ++h) {
-        const int r = h * TC_BM + e * 32 + lane;
-        const uint32_t tb = tmem_tile + h * p.tmem_cols + ((uint32_t)(e * 32) << 16);
-        for (int col = 0; col < p.BN; col += 32) {
-            uint32_t v[32];
-            const int n = min(32, p.BN - col);
-            if (direct && own) {
+    int *ctr = p.tile_ctr + R.ctr;
+    if (R.ncols > 0) {
+        const int ncc = (p.BN + 31) / 32;
+        for (int h = 0; h < nht; ++h) {
+            const int r = h * TC_BM + e * 32 + lane;
+            const uint32_t tb = tmem_tile + h * p.tmem_cols + ((uint32_t)(e * 32) << 16);
+            for (int cc = 0; cc < ncc; ++cc) {
+                const int col = ((cc + R.list) % ncc) * 32;   // parts of a tile start on different columns
+                uint32_t v[32];
+                const int n = min(32, p.BN - col);
                 if (n == 32) ptx::tmem_ld32(tb + col, v);
                 else ptx::tmem_ld16(tb + col, v);
                 ptx::tmem_ld_wait();
-            } else {
+                if (r < R.rows) {
+                    float *op = p.acc + (R.row0 + r) * p.ld_acc + R.nt * p.BN + col;
 #pragma unroll
-                for (int q = 0; q < 32; ++q) v[q] = 0u;
+                    for (int q = 0; q < 8; ++q)
+                        if (q * 4 < n)
+                            ptx::red_add_v4(op + 4 * q, to_f(v[4 * q]), to_f(v[4 * q + 1]), to_f(v[4 * q + 2]),
+                                            to_f(v[4 * q + 3]));
+                }
             }
-            if (r < R.rows) {
-                const int64_t row = R.row0 + r;   // accumulator row (tile order)
-                const int gcol = R.nt * p.BN + col;
-                float4 *ap = reinterpret_cast<float4 *>(p.acc + row * p.ld_acc + gcol);
+        }
+    }
+    // TMEM no longer needed: hand the accumulator back to the MMA warp
+    ptx::tc_fence_before();
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(tempty_bar);
+    // release: the barrier orders the 128 threads' reductions before the lead's
+    // gpu-scope fence (cumulative), then the arrival count
+    epi_bar();
+    if (lead) {
+        __threadfence();
+        const int old = atomicAdd(ctr, 1);
+        __threadfence();
+        cs.epi_last[fl] = old == split - 1;
+    }
+    epi_bar();
+    if (!cs.epi_last[fl]) return;
+    for (int h = 0; h < nht; ++h) {
+        const int r = h * TC_BM + e * 32 + lane;
+        if (r >= R.rows) continue;
+        const int64_t row = R.row0 + r;   // accumulator row (tile order)
+        const int64_t orow = p.os_rows ? (int64_t)R.scatter[r] : row;
+        for (int col = 0; col < p.BN; col += 32) {
+            uint32_t v[32];
+            const int n = min(32, p.BN - col);
+            const int gcol = R.nt * p.BN + col;
+            float4 *ap = reinterpret_cast<float4 *>(p.acc + row * p.ld_acc + gcol);
 #pragma unroll
-                for (int q = 0; q < 8; ++q)
-                    if (q * 4 < n) {
-                        const float4 s4 = __ldcg(ap + q);
-                        v[4 * q] = __float_as_uint(to_f(v[4 * q]) + s4.x);
-                        v[4 * q + 1] = __float_as_uint(to_f(v[4 * q + 1]) + s4.y);
-                        v[4 * q + 2] = __float_as_uint(to_f(v[4 * q + 2]) + s4.z);
-                        v[4 * q + 3] = __float_as_uint(to_f(v[4 * q + 3]) + s4.w);
-                        __stcg(ap + q, make_float4(0.f, 0.f, 0.f, 0.f));
-                    }
-                store_row(p, p.os_rows ? (int64_t)R.scatter[r] : row, gcol, v, n);
-            }
+            for (int q = 0; q < 8; ++q)
+                if (q * 4 < n) {
+                    const float4 s4 = __ldcg(ap + q);
+                    v[4 * q] = __float_as_uint(s4.x);
+                    v[4 * q + 1] = __float_as_uint(s4.y);
+                    v[4 * q + 2] = __float_as_uint(s4.z);
+                    v[4 * q + 3] = __float_as_uint(s4.w);
+                    __stcg(ap + q, make_float4(0.f, 0.f, 0.f, 0.f));
+                }
+            store_row(p, orow, gcol, v, n);
         }
     }
     if (lead) *reinterpret_cast<volatile int *>(ctr) = 0;
@@ -424,7 +436,7 @@ __device__ __forceinline__ void gather_role(const ConvParams &p, ConvSmem &cs, c
 // dtype, fused residual, or fp32 accumulator) / WS: red.global.add.v4.f32 scatter;
 // FIX: OS split tiles go through the split-K fixup instead
 template <bool FIX>
-__device__ __forceinline__ void epi_role(const ConvParams &p, ConvSmem &cs, uint32_t tmem_base, int tr, int split, int nht,
+__device__ __forceinline__ void epi_role(const ConvParams &p, ConvSmem &cs, uint32_t tmem_base, int tr, int nht,
                                          int NH, int warp, int lane) {
     const int e = warp - W_EPI0;   // == warp % 4: the TMEM lane quadrant this warp may access
     for (uint32_t ti = 0;; ++ti) {
@@ -436,9 +448,14 @@ __device__ __forceinline__ void epi_role(const ConvParams &p, ConvSmem &cs, uint
         const int nt = R.nt;
         ptx::mbar_wait_sleep(ptx::smem_u32(&cs.tfull[a]), (ti >> 1) & 1);
         if (threadIdx.x == 32 * W_EPI0) TR(6, ti);
+#ifdef SPC_EXP_TRACE2
+        if (threadIdx.x == 32 * W_EPI0) TL(5, gtime());
+#endif
         ptx::tc_fence_after();
-        if (FIX) {
-            os_split_fixup(p, cs, R, ti, tr, split, nht, tmem_base + a * NH * p.tmem_cols, e, lane);
+        const bool fix = FIX && R.nsplit > 1;
+        if (fix) {
+            os_split_fixup(p, cs, R, ti, R.nsplit, nht, tmem_base + a * NH * p.tmem_cols, ptx::smem_u32(&cs.tempty[a]),
+                           e, lane);
         } else {
 #pragma unroll 1
             for (int h = 0; h < nht; ++h) {
@@ -472,11 +489,17 @@ __device__ __forceinline__ void epi_role(const ConvParams &p, ConvSmem &cs, uint
         ptx::tc_fence_before();
         __syncwarp();
         if (threadIdx.x == 32 * W_EPI0) TR(7, ti);
+#ifdef SPC_EXP_TRACE2
+        if (threadIdx.x == 32 * W_EPI0) TL(6, gtime());
+#endif
         if (lane == 0) {
-            ptx::mbar_arrive(ptx::smem_u32(&cs.tempty[a]));
+            if (!fix) ptx::mbar_arrive(ptx::smem_u32(&cs.tempty[a]));   // (the fixup released it already)
             ptx::mbar_arrive(ptx::smem_u32(&cs.trec_empty[st]));
         }
     }
+#ifdef SPC_EXP_TRACE2
+    if (threadIdx.x == 32 * W_EPI0) TL(7, gtime());
+#endif
 }
 
 template <int BK, int BM>
@@ -536,14 +559,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             if (BM == 256 && ((n_out + 255) / 256) * p.n_ntiles < 2 * p.num_sms) tr = 128;
             if (p.force_tr) tr = min(p.force_tr, BM);
             const int64_t rt = (n_out + tr - 1) / tr;
-            int split = 1;
-            if (p.split_ok && rt * p.n_ntiles < p.num_sms && p.k_dense >= 4)
-                split = (int)imin64(p.num_sms / (rt * p.n_ntiles), p.k_dense / 2);
-            if (split < 1) split = 1;
+            // weighted split-K for small launches (parts computed by the scheduler role)
+            // (only when tiles leave at least half the SMs idle: the parts' fp32 reductions
+            // land in one burst at the end of the launch and cost more than mild imbalance)
+            const bool wsplit = p.split_ok && p.k_dense >= 4 && 2 * rt * p.n_ntiles <= p.split_tiles_per_sm2 &&
+                                rt <= SPLIT_MAX_TILES && p.n_ntiles <= 2;
+            const int64_t units = rt;
             if (lane == 0) {
                 cs.tr = tr;
-                cs.split = split;
-                cs.n_tiles = rt * split * p.n_ntiles;
+                cs.wsplit = wsplit ? 1 : 0;
+                cs.n_sp = (int)rt;
+                cs.n_tiles = units * p.n_ntiles;
             }
         } else {
             // virtual-tile prefix over the WS lists
@@ -573,7 +599,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             if (lane == 0) {
                 cs.list_prefix[p.n_lists] = total;
                 cs.tr = tr;
-                cs.split = 1;
+                cs.wsplit = 0;
                 cs.n_tiles = (int64_t)total * p.n_ntiles;
             }
         }
@@ -587,7 +613,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     if (threadIdx.x == 0) TL(1, gtime());
 #endif
     constexpr uint32_t rb = BK * 2;           // bytes per operand row (= swizzle span)
-    const int tr = cs.tr, split = cs.split, nht = tr / TC_BM;
+    const int tr = cs.tr, wsplit = cs.wsplit, nht = tr / TC_BM;
     // the ring carve of this tile height
 #ifdef SPC_EXP_RG0
     const int rgi = 0;
@@ -601,7 +627,56 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
 
     if (warp == W_SCHED) {
         // ===================== scheduler: tile records + gather indices ==================
-        const int64_t n_tiles = cs.n_tiles;
+        int64_t n_tiles = cs.n_tiles;
+        if (wsplit) {
+            // tile t (claim order, heaviest first) of w_t active offsets runs as
+            // ceil(w_t / U) parts, U = ceil(total / SMs) (>= 2); weights precomputed by the
+            // density-order pass, else popcounts of the tile masks
+            const int64_t rt = cs.n_sp;
+            const int f = tr / 128;
+            const int64_t nt128 = (n_out + 127) / 128;
+            const int32_t *wpre = p.tile_order ? p.tile_order + 2 * p.tiles128_cap + (tr == 256 ? p.tiles128_cap : 0) : nullptr;
+            int wsum = 0;
+#pragma unroll 4
+            for (int t = lane; t < rt; t += 32) {
+                int w = 0;
+                if (wpre) {
+                    w = wpre[t];
+                } else {
+                    for (int q = 0; q < p.tile_words; ++q) {
+                        uint32_t m = 0;
+                        for (int h = 0; h < f; ++h)
+                            if (t * f + h < nt128) m |= p.tile_mask[(t * f + h) * p.tile_words + q];
+                        w += __popc(m);
+                    }
+                }
+                w = max(w, 1);
+                cs.sp_cnt[t] = (uint16_t)w;
+                wsum += w;
+            }
+            for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+            const int U = max(p.split_min_unit, (int)((wsum * (int64_t)p.n_ntiles + p.num_sms - 1) / p.num_sms));
+            __syncwarp();
+            int carry = 0;
+            for (int base = 0; base < rt; base += 32) {
+                const int t = base + lane;
+                int c = 0;
+                if (t < rt) {
+                    const int w = cs.sp_cnt[t];
+                    c = min((w + U - 1) / U, w);
+                    cs.sp_cnt[t] = (uint16_t)c;
+                }
+                int x = c;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += y;
+                }
+                if (t < rt) cs.sp_pre[t] = carry + x - c;
+                carry += __shfl_sync(0xffffffffu, x, 31);
+            }
+            __syncwarp();
+            n_tiles = (int64_t)carry * p.n_ntiles;
+        }
         // tiles are claimed dynamically from a ws counter (heaviest first after the density
         // order), so uneven tiles balance across SMs; static round-robin without a ws
         int *fetch = p.tile_ctr ? p.tile_ctr + CTR_FETCH : nullptr;
@@ -610,12 +685,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             const int st = ti % TREC_SLOTS;
             ptx::mbar_wait_sleep(ptx::smem_u32(&cs.trec_empty[st]), ((ti / TREC_SLOTS) & 1) ^ 1);
             int64_t v = vs;
-            if (fetch) {
-                // claim gate: at most one tile claimed beyond the one the gather warps are on
-                if (ti > 0) ptx::mbar_wait(ptx::smem_u32(&cs.tstart), (ti - 1) & 1);
+            if (fetch && ti > 0) {
+                // first tile: blockIdx.x (no claim latency); then claims from the counter,
+                // at most one tile beyond the one the gather warps are on (claim gate)
+                ptx::mbar_wait(ptx::smem_u32(&cs.tstart), (ti - 1) & 1);
                 int x = 0;
                 if (lane == 0) x = atomicAdd(fetch, 1);
-                v = __shfl_sync(0xffffffffu, x, 0);
+                v = (int64_t)gridDim.x + __shfl_sync(0xffffffffu, x, 0);
             }
             TileRec &R = cs.trec[st];
             if (v >= n_tiles) {
@@ -624,14 +700,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                 break;
             }
             TileInfo t;
-            decode_tile(p, v, cs.list_prefix, n_out, tr, split, t);
+            decode_tile(p, v, cs.list_prefix, n_out, tr, wsplit ? cs.sp_pre : nullptr, cs.sp_cnt, cs.n_sp, t);
             if (lane == 0) {
                 R.row0 = t.row0; R.rows = t.rows; R.nt = t.nt; R.list = t.list; R.dir = t.dir; R.k = t.k; R.end = 0;
+                R.nsplit = p.mode == 0 ? t.nsplit : 1;
+                R.ctr = t.ctr;
                 for (int w = 0; w < 4; ++w) R.mask[w] = t.mask[w];
                 int nc = 0;
                 for (int c = next_bit(t.mask, 0); c >= 0; c = next_bit(t.mask, c + 1)) R.cols[nc++] = (uint8_t)c;
-                if (p.mode == 0 && split > 1) {   // keep this split's contiguous share
-                    const int per = (nc + split - 1) / split;
+                if (p.mode == 0 && t.nsplit > 1) {   // keep this part's contiguous share
+                    const int per = (nc + t.nsplit - 1) / t.nsplit;
                     const int c0 = min(nc, t.list * per), c1 = min(nc, c0 + per);
                     for (int q = c0; q < c1; ++q) R.cols[q - c0] = R.cols[q];
                     nc = c1 - c0;
@@ -756,8 +834,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                 ptx::mma_commit(ptx::smem_u32(&cs.tfull[a]));
 #ifdef SPC_EXP_TRACE2
                 TL(3, gtime());
-                TL(5, ti + 1);
-                TL(6, it);
 #endif
                 ptx::mbar_arrive(ptx::smem_u32(&cs.trec_empty[st]));
             }
@@ -765,10 +841,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         }
     } else if (warp >= W_EPI0 && warp < W_EPI0 + 4) {
         // ===================== epilogue (warps 8-11, thread = TMEM lane = tile row) ====
-        if (p.mode == 0 && split > 1)
-            epi_role<true>(p, cs, tmem_base, tr, split, nht, NH, warp, lane);
+        if (wsplit)
+            epi_role<true>(p, cs, tmem_base, tr, nht, NH, warp, lane);
         else
-            epi_role<false>(p, cs, tmem_base, tr, split, nht, NH, warp, lane);
+            epi_role<false>(p, cs, tmem_base, tr, nht, NH, warp, lane);
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -1038,7 +1114,7 @@ extern "C" spc_status spc_prepare_weight(const void *weight, int32_t k_vol, int3
 
 // ws layout: [fp32 accumulator n_out x c_out][256 int32 tile arrival counters]; both
 // all-zero on entry and left all-zero on return (spc.h)
-static constexpr size_t WS_CTR_BYTES = 1024;
+static constexpr size_t WS_CTR_BYTES = WS_CTR_SLOTS * sizeof(int);
 extern "C" size_t spc_conv_workspace_size(const spc_kmap *km, int32_t c_out, int32_t out_dtype) {
     if (!km || c_out <= 0) return 0;
     (void)out_dtype;
@@ -1238,6 +1314,8 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
     p.tmem_cols = pow2_cols(p.BN);
     p.num_sms = num_sms();
     p.force_tr = getenv("SPC_TR") ? atoi(getenv("SPC_TR")) : 0;
+    p.split_min_unit = getenv("SPC_SPLIT_MIN") ? atoi(getenv("SPC_SPLIT_MIN")) : 2;
+    p.split_tiles_per_sm2 = getenv("SPC_SPLIT_TILES2") ? atoi(getenv("SPC_SPLIT_TILES2")) : p.num_sms;
     // 256-row tiles (two MMAs per weight tile) whenever four accumulators fit TMEM; the
     // kernel drops to 128-row tiles on the device when the live row count is small
     p.bm = (4 * p.tmem_cols <= 512 && !getenv("SPC_BM128")) ? 256 : 128;

@@ -473,6 +473,7 @@ __global__ void __launch_bounds__(1024) k_ord_tiles(const __grid_constant__ Orde
     const int64_t tiles128 = (J.n_cap + 127) / 128;
     const int64_t nt = (n + T - 1) / T, nt128 = (n + 127) / 128;
     int32_t *order = J.tile_order + (f == 2 ? tiles128 : 0);
+    int32_t *wout = J.tile_order + 2 * tiles128 + (f == 2 ? tiles128 : 0);   // weights in claim order
     for (int i = threadIdx.x; i < SPC_MAX_KVOL + 2; i += blockDim.x) hist[i] = 0;
     __syncthreads();
     auto weight = [&](int64_t t) {
@@ -496,7 +497,12 @@ __global__ void __launch_bounds__(1024) k_ord_tiles(const __grid_constant__ Orde
         }
     }
     __syncthreads();
-    for (int64_t t = threadIdx.x; t < nt; t += blockDim.x) order[atomicAdd(&hist[SPC_MAX_KVOL - weight(t)], 1)] = (int32_t)t;
+    for (int64_t t = threadIdx.x; t < nt; t += blockDim.x) {
+        const int w = weight(t);
+        const int at = atomicAdd(&hist[SPC_MAX_KVOL - w], 1);
+        order[at] = (int32_t)t;
+        wout[at] = w;
+    }
 }
 
 // scratch of one grouped order over `rows_cap` concatenated rows
@@ -638,7 +644,7 @@ static KmapLayout layout_of(const KmapPlan &pl, int64_t n_out, uint32_t flags, b
         L.rows = take(sizeof(int32_t) * (size_t)n_out);
         L.os_ord = take(sizeof(int32_t) * (size_t)n_out * pl.k_dense);
         L.mask_ord = take(sizeof(uint32_t) * (size_t)(L.tiles * L.words));
-        L.tile_order = take(sizeof(int32_t) * 2 * (size_t)L.tiles);
+        L.tile_order = take(sizeof(int32_t) * 4 * (size_t)L.tiles);   // orders + weights
         if (scratch) {
             L.scratch_bytes = order_scratch_bytes(n_out);
             L.scratch = take(L.scratch_bytes);

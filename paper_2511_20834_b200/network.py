@@ -182,7 +182,7 @@ class SparseNet:
         self.status = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self.sort_ws = torch.empty(int(spc.lib().spc_pack_sort_workspace_size(self.n0)), dtype=torch.uint8,
                                    device=self.dev)
-        self.conv_ws = torch.zeros(self.n0 * 256 * 4 + 1024, dtype=torch.uint8, device=self.dev)
+        self.conv_ws = None      # sized from spc_conv_workspace_size once the maps exist (index())
         self.netidx = None
         self.maps = None
 
@@ -208,6 +208,9 @@ class SparseNet:
         kms = self.netidx.run(self.keys, status=self.status, stream=stream)
         self.level_keys, self.level_n = self.netidx.level_keys, self.netidx.level_n
         self.maps = dict(zip(self.map_keys, kms))
+        need = max(spc.spc_conv_workspace_size(self.maps[s.map_key], s.c_out) for s in self.layers)
+        if self.conv_ws is None or self.conv_ws.numel() < need:
+            self.conv_ws = torch.zeros(need, dtype=torch.uint8, device=self.dev)   # zero once (spc.h ws contract)
 
     def set_t(self, t_map: dict):
         self.t.update(t_map)

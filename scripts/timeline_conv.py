@@ -30,7 +30,8 @@ print(f"CTAs {n}: times in us from the first CTA entry")
 for name, row in zip(["entry", "setup", "first_full", "last_commit", "exit"], rel):
     v = row[t[list(["entry", "setup", "first_full", "last_commit", "exit"]).index(name)] > 0] if False else row
     print(f"  {name:12s} min {v.min():7.2f}  median {np.median(v):7.2f}  max {v.max():7.2f}")
-print(f"  tiles/CTA  min {t[5].min()} median {np.median(t[5])} max {t[5].max()}")
-print(f"  stages/CTA min {t[6].min()} median {np.median(t[6])} max {t[6].max()}")
+for nm, sl in (("last tfull seen", 5), ("last tile stored", 6), ("epilogue end", 7)):
+    v = (t[sl] - t0) / 1000.0
+    print(f"  {nm:14s} min {v.min():7.2f}  median {np.median(v):7.2f}  max {v.max():7.2f}")
 busy = rel[3] - rel[2]
 print(f"  first_full->last_commit  median {np.median(busy):.2f} max {busy.max():.2f};  setup->first_full median {np.median(rel[2]-rel[1]):.2f}")

@@ -356,7 +356,8 @@ def test_conv_split_fixup_and_workspace_invariant():
     spec = _spec_for(coords)
     keys, _, _ = _pack_sort(coords, spec)
     c = oracle.sort_coords(coords)[0]
-    ws = torch.zeros(len(c) * 256 * 4 + 4096, dtype=torch.uint8, device=DEV)
+    probe = spc.spc_build_kmap(keys, keys, spec, spc.Geom(3, 1, 1, 1, 0), -1, 0)
+    ws = torch.zeros(spc.spc_conv_workspace_size(probe, 256), dtype=torch.uint8, device=DEV)
     for t, flags, ci, co in ((-1, 0, 32, 64), (-1, 0, 64, 256), (0, 1, 32, 32), (2, 1, 64, 96), (-1, 1, 16, 128),
                              (-1, 8, 32, 64), (2, 9, 64, 96)):
         km = spc.spc_build_kmap(keys, keys, spec, spc.Geom(3, 1, 1, 1, 0), t, flags)
