@@ -53,6 +53,8 @@ def parse():
                          "Waymo-shaped scans sharded over the GPUs (MinkUNet-42, NCCL output gather)")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-tune", action="store_true")
+    ap.add_argument("--t-from", default=None, help="take the per-map dataflow t from a previous bench JSON line "
+                                                   "(config.dataflow_t) instead of tuning")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-layers", action="store_true", help="print the per-layer table to stderr")
     return ap.parse_args()
@@ -265,7 +267,9 @@ def main():
 
     # ---- one-time dataflow tuning per kernel map (not timed) ------------------
     tuned = {}
-    if not args.no_tune:
+    if args.t_from:
+        net.set_t(load_t(args.t_from))
+    elif not args.no_tune:
         tuned = tune(net, coords, feats, stream)
 
     # ---- warm-up ------------------------------------------------------------------------
@@ -401,6 +405,13 @@ def main():
     if world > 1:
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()
+
+
+def load_t(path):
+    """{map_key: t} from the config.dataflow_t of a bench JSON line (last line of the file)."""
+    import ast
+    line = [ln for ln in open(path).read().splitlines() if ln.startswith("{")][-1]
+    return {ast.literal_eval(k): int(v) for k, v in json.loads(line)["config"]["dataflow_t"].items()}
 
 
 def measured_peaks():
