@@ -6,13 +6,13 @@
 // lies in ONE contiguous window of the sorted input keys:
 // [lb(q_first + d_anchor(g)), lb(q_last + d_last(g) + 1)).
 //   k_kmap_bounds: every window bound of every (map, tile, group) in one parallel pass.
-//   k_kmap_zdelta: one WARP per (tile, group) task: stage the window in shared memory
-//       (coalesced), then the paper's z-delta search per output: one lower_bound for the
-//       anchor query, then a forward cursor for the other K-1 members.  Tasks
-//       are independent (no CTA barriers); both layouts are written straight from the
-//       search: OS (dense offsets) entries into the [n_out x K_dense] table (every entry
-//       written once, -1 for no match: no transpose pass); WS (sparse offsets)
-//       (in, out) pairs appended with one warp-aggregated atomicAdd per (warp, offset) (no
+//   k_kmap_zdelta: one CTA per (map, tile): the tile's K^2 windows staged in one shared
+//       pool (coalesced), then the paper's z-delta search per output: one lower_bound for
+//       the anchor query, then a forward cursor for the other K-1 members, one
+//       warp per (group, 32-output chunk).  Both layouts are assembled in shared memory and
+//       leave as contiguous streams: the OS block of the [n_out x K_dense] table (every
+//       entry written once, -1 for no match: no transpose pass); each WS list's
+//       (in, out) pairs compacted with one warp-aggregated reservation per (tile, list) (no
 //       filter pass), halved for submanifold layers.
 #include <cuda_runtime.h>
 
@@ -126,19 +126,14 @@ __device__ __forceinline__ int64_t group_delta(const KmapDesc &p, int by, int bz
 // keys holding all matches of a tile's outputs for one offset group.  One thread per
 // bound, so the global binary searches' latency chains all run concurrently instead of
 // once per tile inside the build kernel.
-// It also zeroes each tile's OS mask words and writes each row's density-order key tag
-// (the build ORs the direction bits in).
 __global__ void __launch_bounds__(256) k_kmap_bounds(const __grid_constant__ KmapBatch B) {
     __shared__ int64_t s_pre[KM_MAX_MAPS + 1];
-    __shared__ int64_t s_ordbase[KM_MAX_MAPS];
     if (threadIdx.x == 0) {
-        int64_t acc = 0, ob = 0;
+        int64_t acc = 0;
         for (int m = 0; m < B.n_maps; ++m) {
             s_pre[m] = acc;
             const int64_t n_out = dev_count(B.d[m].n_out_cap, B.d[m].n_out_dev);
             acc += ((n_out + KM_BM - 1) / KM_BM) * 2 * B.d[m].K * B.d[m].K;
-            s_ordbase[m] = ob;
-            if (B.d[m].ord_idx >= 0) ob += n_out;
         }
         s_pre[B.n_maps] = acc;
     }
@@ -156,130 +151,112 @@ __global__ void __launch_bounds__(256) k_kmap_bounds(const __grid_constant__ Kma
         const int64_t n_in = dev_count(p.n_in_cap, p.n_in_dev);
         const int64_t row0 = tile * KM_BM;
         const int rows = (int)imin64(KM_BM, n_out - row0);
-        if (j < p.tile_words) p.tile_mask[tile * p.tile_words + j] = 0u;
-        if (p.ord_idx >= 0)
-            for (int r = j; r < rows; r += G2)
-                B.ord_keys[s_ordbase[m] + row0 + r] = (uint64_t)p.ord_idx << B.ord_key_bits;
         const uint64_t q = hi ? p.out[row0 + rows - 1] + (uint64_t)group_delta(p, B.bits_y, B.bits_z, g, p.K - 1) + 1ull
                               : p.out[row0] + (uint64_t)group_delta(p, B.bits_y, B.bits_z, g, 0);
         p.bounds[local] = (int32_t)lower_bound_g(p.in, n_in, q);
     }
 }
 
-// one (tile, group) task of k_kmap_zdelta, run by one warp
-template <int K>
-__device__ __forceinline__ void zdelta_task(const KmapBatch &B, const KmapDesc &p, int m, int64_t local,
-                                            const int8_t *dcol, const int8_t *lstv, int64_t ordbase, uint64_t *win,
-                                            int lane, unsigned long long &n_search, unsigned long long &n_probe) {
-    constexpr int G = K * K, r = (K - 1) / 2;
-    const int KD = p.k_dense;
-    const int64_t tile = local / G;
-    const int g = (int)(local - tile * G);
-    const int ex = g / K - r, ey = g % K - r;
-    int ks[K];
-    bool need = false;
-#pragma unroll
-    for (int mm = 0; mm < K; ++mm) {   // weight offsets of the members, ascending query order
-        const int ez = p.transposed ? r - mm : mm - r;
-        ks[mm] = ((ex + r) * K + (ey + r)) * K + (ez + r);
-        need |= dcol[ks[mm]] >= 0 || lstv[ks[mm]] >= 0;
+// per-tile shared state of k_kmap_zdelta (the tile's OS / WS tables live in dynamic smem)
+constexpr int KM_POOL = 4096;      // staged window keys per CTA (32 KB); a group that does not fit searches global
+struct ZTile {
+    uint64_t q[KM_BM];              // the tile's output keys
+    uint32_t ordk[KM_BM];           // density-order direction bits per row
+    int32_t cnt[SPC_MAX_KVOL];      // matches per weight offset
+    int32_t wlo[25], wlen[25], woff[25];   // per offset group: window start / length / pool offset (-1: global)
+    int64_t dq[SPC_MAX_KVOL];       // packed query delta of member mm of group g, at g * K + mm
+    int32_t dsc[SPC_MAX_KVOL];      // its weight offset k | dense column + 1 << 8 | WS list + 1 << 16 | order bit + 1 << 24
+    uint32_t mask[4];               // OS tile mask words
+    int mslot[2];                   // map of this / the next tile (thread 0, parity-buffered)
+};
+
+__device__ __forceinline__ int tile_map(const int64_t *pre, int n_maps, int64_t v) {
+    int m = 0;
+    while (m + 1 < n_maps && pre[m + 1] <= v) ++m;
+    return m;
+}
+
+// lower bound in a staged (shared) or global window
+template <bool SM>
+__device__ __forceinline__ int lb_win(const uint64_t *a, int n, uint64_t q) {
+    int lo = 0, len = n;
+    while (len > 0) {
+        const int half = len >> 1;
+        uint64_t v;
+        if (SM) v = a[lo + half];
+        else v = __ldg(a + lo + half);
+        if (v < q) {
+            lo += half + 1;
+            len -= half + 1;
+        } else {
+            len = half;
+        }
     }
-    if (!need) return;
-    const int64_t n_out = dev_count(p.n_out_cap, p.n_out_dev);
-    const int64_t row0 = tile * KM_BM;
-    const int rows = (int)imin64(KM_BM, n_out - row0);
-    const int32_t lo = p.bounds[local * 2], hi = p.bounds[local * 2 + 1];
-    const int wl = max(0, hi - lo);
-    const bool staged = wl <= KM_WWIN;
-    if (staged) {
-        for (int e = lane; e < wl; e += 32) win[e] = __ldg(p.in + lo + e);
-        __syncwarp();
-    }
-    const uint64_t *wk = staged ? win : p.in + lo;
-    int64_t dl[K];
+    return lo;
+}
+
+// one (offset group, 32-output chunk) task of a tile, one warp: the paper's z-delta search
+// per output -- one lower_bound for the anchor query, then a forward cursor for the other
+// K-1 members -- in the group's window of input keys.  Every stored entry is
+// written to the tile's shared tables (-1 = no match): OS columns [row][K_dense], WS lists
+// [list][row]; counts, mask bits and density-order bits go to shared accumulators.
+template <int K, bool SM>
+__device__ __forceinline__ int zdelta_chunk(ZTile &zt, int32_t *s_os, int32_t *s_ws, int KD, const uint64_t *wk,
+                                            int wl, int32_t lo, int g, int ch, int rows, int lane) {
+    const int lr = ch * 32 + lane;
+    const bool valid = lr < rows;
+    const uint64_t q = valid ? zt.q[lr] : 0;
+    int pos = 0;
+    if (valid) pos = lb_win<SM>(wk, wl, q + (uint64_t)zt.dq[g * K]);
+    const int pos0 = pos;
+    uint32_t key = 0;
 #pragma unroll
-    for (int mm = 0; mm < K; ++mm) dl[mm] = group_delta(p, B.bits_y, B.bits_z, g, mm);
-    uint32_t colbal[K];
-    int cnt[K];
-    int32_t jj[KM_BM / 32][K];       // WS matches of the task, written after one reservation per offset
-#pragma unroll
-    for (int mm = 0; mm < K; ++mm) { colbal[mm] = 0u; cnt[mm] = 0; }
-    const bool ord = p.ord_idx >= 0;
-#pragma unroll
-    for (int ch = 0; ch < KM_BM / 32; ++ch) {
-        const int lr = ch * 32 + lane;
-        const bool valid = lr < rows;
-        const int64_t i = row0 + lr;
-        const uint64_t q = valid ? p.out[i] : 0;
-        int pos = 0;
+    for (int mm = 0; mm < K; ++mm) {   // members in ascending query order
+        const uint64_t query = q + (uint64_t)zt.dq[g * K + mm];
+        const int32_t dsc = zt.dsc[g * K + mm];
+        bool match = false;
         if (valid) {
-            pos = lower_bound_s(wk, wl, q + (uint64_t)dl[0]);
-            ++n_search;
+            uint64_t v = 0;
+            while (pos < wl && (v = (SM ? wk[pos] : __ldg(wk + pos))) < query) ++pos;
+            match = pos < wl && v == query;
         }
-        uint32_t key = 0;
-#pragma unroll
-        for (int mm = 0; mm < K; ++mm) {
-            const uint64_t query = q + (uint64_t)dl[mm];
-            bool match = false;
-            if (valid) {
-                while (pos < wl && wk[pos] < query) { ++pos; ++n_probe; }
-                match = pos < wl && wk[pos] == query;
-            }
-            const int32_t j = match ? lo + pos : -1;
-            const unsigned bal = __ballot_sync(0xffffffffu, match);
-            cnt[mm] += __popc(bal);
-            const int col = dcol[ks[mm]];
-            jj[ch][mm] = j;
-            if (col >= 0) {
-                if (valid) p.os[i * KD + col] = j;
-                colbal[mm] |= bal;
-                if (ord && match && p.ord_cls[col] >= 0) key |= 1u << p.ord_cls[col];
-            }
+        const int32_t j = match ? lo + pos : -1;
+        const unsigned bal = __ballot_sync(0xffffffffu, match);
+        const int col = ((dsc >> 8) & 0xff) - 1, l = ((dsc >> 16) & 0xff) - 1, ob = ((dsc >> 24) & 0x1f) - 1;
+        if (valid) {
+            if (col >= 0) s_os[lr * KD + col] = j;
+            else if (l >= 0) s_ws[l * KM_BM + lr] = j;
         }
-        if (ord && key) atomicOr(reinterpret_cast<unsigned long long *>(&B.ord_keys[ordbase + i]), (unsigned long long)key);
-    }
-    // WS pairs: one reservation per stored offset per task (issued together), then writes
-    int base[K];
-#pragma unroll
-    for (int mm = 0; mm < K; ++mm) {
-        base[mm] = 0;
-        const int l = lstv[ks[mm]];
-        if (l >= 0 && dcol[ks[mm]] < 0 && cnt[mm] && lane == 0) base[mm] = atomicAdd(&p.counts[SPC_MAX_KVOL + l], cnt[mm]);
-    }
-#pragma unroll
-    for (int mm = 0; mm < K; ++mm) {
-        const int l = lstv[ks[mm]];
-        if (l < 0 || dcol[ks[mm]] >= 0 || !cnt[mm]) continue;
-        int b = __shfl_sync(0xffffffffu, base[mm], 0);
-#pragma unroll
-        for (int ch = 0; ch < KM_BM / 32; ++ch) {
-            const uint32_t bal = __ballot_sync(0xffffffffu, jj[ch][mm] >= 0);
-            if (jj[ch][mm] >= 0)
-                p.pairs[(int64_t)l * p.list_stride + b + __popc(bal & lanemask_lt())] =
-                    make_int2(jj[ch][mm], (int32_t)(row0 + ch * 32 + lane));
-            b += __popc(bal);
+        if (lane == 0 && bal) {
+            atomicAdd(&zt.cnt[dsc & 0xff], __popc(bal));
+            if (col >= 0) atomicOr(&zt.mask[col >> 5], 1u << (col & 31));
         }
+        if (match && ob >= 0) key |= 1u << ob;
     }
-    if (lane == 0) {
-#pragma unroll
-        for (int mm = 0; mm < K; ++mm) {
-            if (cnt[mm]) atomicAdd(&p.counts[ks[mm]], cnt[mm]);
-            const int col = dcol[ks[mm]];
-            if (col >= 0 && colbal[mm]) atomicOr(&p.tile_mask[tile * p.tile_words + (col >> 5)], 1u << (col & 31));
-        }
-    }
-    (void)m;
+    if (key) atomicOr(&zt.ordk[lr], key);
+    return pos - pos0;   // cursor advances (search-count statistics)
 }
 
 #ifndef SPC_KM_MIN_BLOCKS
-#define SPC_KM_MIN_BLOCKS 3
+#define SPC_KM_MIN_BLOCKS 4
 #endif
+// one CTA per (map, tile of KM_BM outputs), grid-strided over every tile of every map of
+// the batch.  Per tile: (1) every warp stages its share of the K^2 group windows
+// [lo, hi) (k_kmap_bounds) into one shared pool, coalesced; (2) the warps share the
+// (group, 32-output chunk) search tasks; (3) the tile leaves as contiguous streams: the OS
+// block [rows x K_dense] (each entry written once, -1 for no match: no transpose pass,
+// P:400) as 16-byte stores, each WS list's pairs compacted with one reservation per
+// (tile, list) (warp ballots, no filter pass; halved for submanifold maps,
+// P:418-421), the tile mask, per-offset counts and density-order keys.
 __global__ void __launch_bounds__(KM_THREADS, SPC_KM_MIN_BLOCKS) k_kmap_zdelta(const __grid_constant__ KmapBatch B) {
     __shared__ int8_t s_dcol[KM_MAX_MAPS][SPC_MAX_KVOL];   // weight offset -> dense column / -1
     __shared__ int8_t s_lst[KM_MAX_MAPS][SPC_MAX_KVOL];    // weight offset -> WS list / -1
-    __shared__ int64_t s_pre[KM_MAX_MAPS + 1];             // task prefix (tiles * K^2)
+    __shared__ int64_t s_pre[KM_MAX_MAPS + 1];             // tile prefix over the maps
     __shared__ int64_t s_ordbase[KM_MAX_MAPS];
-    __shared__ __align__(16) uint64_t s_win[KM_WARPS][KM_WWIN];
+    __shared__ int64_t s_nout[KM_MAX_MAPS];
+    __shared__ __align__(16) uint64_t s_pool[KM_POOL];
+    __shared__ ZTile zt;
+    extern __shared__ __align__(16) int32_t s_tab[];        // [KM_BM x K_dense] OS, then [lists x KM_BM] WS
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     // ---- prologue: per-map offset tables (planned on the host, make_plan) --------------
@@ -293,24 +270,112 @@ __global__ void __launch_bounds__(KM_THREADS, SPC_KM_MIN_BLOCKS) k_kmap_zdelta(c
         for (int m = 0; m < B.n_maps; ++m) {
             s_pre[m] = acc;
             const int64_t n_out = dev_count(B.d[m].n_out_cap, B.d[m].n_out_dev);
-            acc += ((n_out + KM_BM - 1) / KM_BM) * B.d[m].K * B.d[m].K;
+            s_nout[m] = n_out;
+            acc += (n_out + KM_BM - 1) / KM_BM;
             s_ordbase[m] = ob;
             if (B.d[m].ord_idx >= 0) ob += n_out;
         }
         s_pre[B.n_maps] = acc;
+        zt.mslot[0] = tile_map(s_pre, B.n_maps, blockIdx.x);
     }
     __syncthreads();
     const int64_t total = s_pre[B.n_maps];
-    uint64_t *win = s_win[warp];
     unsigned long long n_search = 0, n_probe = 0;
     int stats_map = -1;
+    // software pipeline: the next tile's output keys and window bounds are loaded into
+    // registers while the current tile flushes (one global round trip off the tile chain)
+    uint64_t pf_q = 0;
+    int32_t pf_lo = 0, pf_hi = 0;
+    auto prefetch = [&](int64_t vn, int mn) {
+        if (vn >= total) return;
+        const KmapDesc &pn = B.d[mn];
+        const int64_t tn = vn - s_pre[mn];
+        const int rn = (int)imin64(KM_BM, s_nout[mn] - tn * KM_BM);
+        if (tid < rn) pf_q = pn.out[tn * KM_BM + tid];
+        const int Gn = pn.K * pn.K;
+        if (lane < Gn) {
+            const int2 b2 = *reinterpret_cast<const int2 *>(pn.bounds + (tn * Gn + lane) * 2);
+            pf_lo = b2.x;
+            pf_hi = b2.y;
+        }
+    };
+    prefetch(blockIdx.x, zt.mslot[0]);
 
-    // ---- one warp per (map, tile, group) task -------------------------------------------
-    for (int64_t v = (int64_t)blockIdx.x * KM_WARPS + warp; v < total; v += (int64_t)gridDim.x * KM_WARPS) {
-        int m = 0;
-        while (s_pre[m + 1] <= v) ++m;
+    uint32_t it = 0;
+    for (int64_t v = blockIdx.x; v < total; v += gridDim.x, ++it) {
+        const int m = zt.mslot[it & 1];
+        if (tid == 0) zt.mslot[(it + 1) & 1] = tile_map(s_pre, B.n_maps, v + gridDim.x);
         const KmapDesc &p = B.d[m];
+        const int8_t *dcol = s_dcol[m], *lstv = s_lst[m];
+        const int64_t tile = v - s_pre[m];
+        const int64_t row0 = tile * KM_BM;
+        const int rows = (int)imin64(KM_BM, s_nout[m] - row0);
+        const int K = p.K, G = K * K, KD = p.k_dense;
+        int32_t *s_os = s_tab;
+        int32_t *s_ws = s_tab + KM_BM * KD;
+        // ---- (1) tile state; group windows (every warp scans the <= 25 group sizes) ----
+        if (tid < KM_BM) {
+            zt.q[tid] = tid < rows ? pf_q : 0;
+            zt.ordk[tid] = 0;
+        }
+        for (int e = tid; e < G * K; e += KM_THREADS) {
+            zt.cnt[e] = 0;
+            const int g = e / K, mm = e - g * K, r = (K - 1) / 2;
+            const int ez = p.transposed ? r - mm : mm - r;
+            const int k = ((g / K) * K + g % K) * K + (ez + r);
+            zt.dq[e] = group_delta(p, B.bits_y, B.bits_z, g, mm);
+            const int col = dcol[k], l = lstv[k];
+            const int ob = (p.ord_idx >= 0 && col >= 0) ? p.ord_cls[col] : -1;
+            zt.dsc[e] = k | ((col + 1) << 8) | ((l + 1) << 16) | ((ob + 1) << 24);
+        }
+        if (tid < 4) zt.mask[tid] = 0;
+        {
+            int lo = 0, wl = 0;
+            bool need = false;
+            if (lane < G) {
+                for (int mm = 0; mm < K; ++mm) {
+                    const int k = lane * K + mm;
+                    need |= dcol[k] >= 0 || lstv[k] >= 0;
+                }
+                if (need) {
+                    lo = pf_lo;
+                    wl = max(0, pf_hi - lo);
+                }
+            }
+            int x = wl;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            const int off = x - wl;
+            const bool fits = x <= KM_POOL;
+            if (warp == 0 && lane < G) {
+                zt.wlo[lane] = lo;
+                zt.wlen[lane] = need ? wl : -1;   // -1: group not needed
+                zt.woff[lane] = fits ? off : -1;
+            }
+            // stage: warp w copies groups w, w + 8, ...
+            for (int gg = warp; gg < G; gg += KM_WARPS) {
+                const int glo = __shfl_sync(0xffffffffu, lo, gg), gwl = __shfl_sync(0xffffffffu, wl, gg);
+                const int goff = __shfl_sync(0xffffffffu, off, gg);
+                if (!__shfl_sync(0xffffffffu, fits ? 1 : 0, gg)) continue;
+                const uint64_t *src = p.in + glo;
+                uint64_t *dst = s_pool + goff;
+                int e = lane;
+                for (; e + 96 < gwl; e += 128) {
+                    const uint64_t a0 = __ldg(src + e), a1 = __ldg(src + e + 32), a2 = __ldg(src + e + 64),
+                                   a3 = __ldg(src + e + 96);
+                    dst[e] = a0; dst[e + 32] = a1; dst[e + 64] = a2; dst[e + 96] = a3;
+                }
+                for (; e < gwl; e += 32) dst[e] = __ldg(src + e);
+            }
+        }
+        __syncthreads();
         if (p.stats && stats_map != m) {   // flush the stats of the previous map
+            for (int o = 16; o > 0; o >>= 1) {
+                n_search += __shfl_xor_sync(0xffffffffu, n_search, o);
+                n_probe += __shfl_xor_sync(0xffffffffu, n_probe, o);
+            }
             if (stats_map >= 0 && lane == 0) {
                 atomicAdd(&B.d[stats_map].stats[0], n_search);
                 atomicAdd(&B.d[stats_map].stats[1], n_probe);
@@ -318,11 +383,73 @@ __global__ void __launch_bounds__(KM_THREADS, SPC_KM_MIN_BLOCKS) k_kmap_zdelta(c
             n_search = n_probe = 0;
             stats_map = m;
         }
-        const int64_t local = v - s_pre[m];
-        if (p.K == 3) zdelta_task<3>(B, p, m, local, s_dcol[m], s_lst[m], s_ordbase[m], win, lane, n_search, n_probe);
-        else if (p.K == 5) zdelta_task<5>(B, p, m, local, s_dcol[m], s_lst[m], s_ordbase[m], win, lane, n_search, n_probe);
-        else zdelta_task<1>(B, p, m, local, s_dcol[m], s_lst[m], s_ordbase[m], win, lane, n_search, n_probe);
-        __syncwarp();   // the window buffer is reused by the next task
+        // ---- (2) search tasks: (group, chunk) -------------------------------------------
+        const int nch = (rows + 31) / 32;
+        for (int t = warp; t < G * nch; t += KM_WARPS) {
+            const int g = t / nch, ch = t - g * nch;
+            const int wl = zt.wlen[g];
+            if (wl < 0) continue;
+            const int32_t lo = zt.wlo[g];
+            const int off = zt.woff[g];
+            if (p.stats && lane == 0) n_search += (unsigned long long)min(32, rows - ch * 32);
+            int adv;
+            if (off >= 0) {
+                if (K == 3) adv = zdelta_chunk<3, true>(zt, s_os, s_ws, KD, s_pool + off, wl, lo, g, ch, rows, lane);
+                else if (K == 5) adv = zdelta_chunk<5, true>(zt, s_os, s_ws, KD, s_pool + off, wl, lo, g, ch, rows, lane);
+                else adv = zdelta_chunk<1, true>(zt, s_os, s_ws, KD, s_pool + off, wl, lo, g, ch, rows, lane);
+            } else {
+                if (K == 3) adv = zdelta_chunk<3, false>(zt, s_os, s_ws, KD, p.in + lo, wl, lo, g, ch, rows, lane);
+                else if (K == 5) adv = zdelta_chunk<5, false>(zt, s_os, s_ws, KD, p.in + lo, wl, lo, g, ch, rows, lane);
+                else adv = zdelta_chunk<1, false>(zt, s_os, s_ws, KD, p.in + lo, wl, lo, g, ch, rows, lane);
+            }
+            n_probe += (unsigned long long)adv;
+        }
+        __syncthreads();
+        prefetch(v + gridDim.x, zt.mslot[(it + 1) & 1]);
+        // ---- (3) flush ------------------------------------------------------------------
+        if (KD > 0) {   // OS block: rows x K_dense contiguous int32 (16-byte aligned: 512 * tile * KD)
+            const int n_el = rows * KD;
+            int32_t *dst = p.os + row0 * KD;
+            const int n4 = n_el >> 2;
+            for (int e = tid; e < n4; e += KM_THREADS)
+                __stcs(reinterpret_cast<int4 *>(dst) + e, reinterpret_cast<const int4 *>(s_os)[e]);
+            for (int e = 4 * n4 + tid; e < n_el; e += KM_THREADS) __stcs(dst + e, s_os[e]);
+            if (tid < p.tile_words) p.tile_mask[tile * p.tile_words + tid] = zt.mask[tid];
+        }
+        {   // WS lists: warp w compacts lists w, w + 8, ... (one reservation per tile and list)
+            int nl = 0;
+            for (int k = 0; k < G * K; ++k) nl = max(nl, lstv[k] + 1);
+            for (int l = warp; l < nl; l += KM_WARPS) {
+                const int32_t *col = s_ws + l * KM_BM;
+                int32_t jv[KM_BM / 32];
+                unsigned bal[KM_BM / 32];
+                int c = 0;
+#pragma unroll
+                for (int ch = 0; ch < KM_BM / 32; ++ch) {
+                    const int lr = ch * 32 + lane;
+                    jv[ch] = lr < rows ? col[lr] : -1;
+                    bal[ch] = __ballot_sync(0xffffffffu, jv[ch] >= 0);
+                    c += __popc(bal[ch]);
+                }
+                if (c == 0) continue;
+                int b = 0;
+                if (lane == 0) b = atomicAdd(&p.counts[SPC_MAX_KVOL + l], c);
+                b = __shfl_sync(0xffffffffu, b, 0);
+                int2 *dst = p.pairs + (int64_t)l * p.list_stride;
+#pragma unroll
+                for (int ch = 0; ch < KM_BM / 32; ++ch) {
+                    if (jv[ch] >= 0)
+                        __stcs(dst + b + __popc(bal[ch] & lanemask_lt()), make_int2(jv[ch], (int32_t)(row0 + ch * 32 + lane)));
+                    b += __popc(bal[ch]);
+                }
+            }
+        }
+        for (int k = tid; k < G * K; k += KM_THREADS)
+            if (zt.cnt[k]) atomicAdd(&p.counts[k], zt.cnt[k]);
+        if (p.ord_idx >= 0 && tid < rows)
+            __stcs(reinterpret_cast<unsigned long long *>(B.ord_keys) + s_ordbase[m] + row0 + tid,
+                   (unsigned long long)(((uint64_t)p.ord_idx << B.ord_key_bits) | zt.ordk[tid]));
+        __syncthreads();
     }
     if (stats_map >= 0) {
         for (int o = 16; o > 0; o >>= 1) {
@@ -698,7 +825,6 @@ static void fill_desc(KmapDesc &d, const spc_kmap &km, const KmapPlan &pl, int32
 }
 
 static spc_status launch_kmaps(const KmapBatch &b, int max_k_dense, int64_t max_tiles, cudaStream_t st) {
-    (void)max_k_dense;
     k_kmap_prep<<<b.n_maps > 0 ? b.n_maps : 1, 256, 0, st>>>(b);
     SPC_LAUNCH_CHECK("k_kmap_prep");
     {
@@ -708,15 +834,27 @@ static spc_status launch_kmaps(const KmapBatch &b, int max_k_dense, int64_t max_
         k_kmap_bounds<<<g, 256, 0, st>>>(b);
         SPC_LAUNCH_CHECK("k_kmap_bounds");
     }
-    // one warp per (tile, group) task; enough CTAs to fill every SM (static task stride)
+    // one CTA per (map, tile); the OS block of a tile is staged in dynamic shared memory
+    int max_cols = 1;
+    for (int m = 0; m < b.n_maps; ++m) {
+        int nl = 0;
+        for (int k = 0; k < SPC_MAX_KVOL; ++k) nl = std::max(nl, (int)b.d[m].lst[k] + 1);
+        max_cols = std::max(max_cols, (int)b.d[m].k_dense + nl);
+    }
+    (void)max_k_dense;
+    const size_t dsm = (size_t)KM_BM * max_cols * sizeof(int32_t);
+    static size_t dsm_set = 0;
+    if (dsm > dsm_set) {
+        SPC_CUDA(cudaFuncSetAttribute(k_kmap_zdelta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+        dsm_set = dsm;
+    }
     int per_sm = 0;
-    SPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_kmap_zdelta, KM_THREADS, 0));
-    int64_t tasks = 0;
-    for (int m = 0; m < b.n_maps; ++m) tasks += ((b.d[m].n_out_cap + KM_BM - 1) / KM_BM) * b.d[m].K * b.d[m].K;
+    SPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_kmap_zdelta, KM_THREADS, dsm));
+    int64_t tiles = 0;
+    for (int m = 0; m < b.n_maps; ++m) tiles += (b.d[m].n_out_cap + KM_BM - 1) / KM_BM;
     (void)max_tiles;
-    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((tasks + KM_WARPS - 1) / KM_WARPS,
-                                                                (int64_t)num_sms() * std::max(1, per_sm)));
-    k_kmap_zdelta<<<(unsigned)grid, KM_THREADS, 0, st>>>(b);
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)num_sms() * std::max(1, per_sm)));
+    k_kmap_zdelta<<<(unsigned)grid, KM_THREADS, dsm, st>>>(b);
     SPC_LAUNCH_CHECK("k_kmap_zdelta");
     return SPC_OK;
 }
