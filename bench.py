@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--t-from", default=None, help="take the per-map dataflow t from a previous bench JSON line "
                                                    "(config.dataflow_t) instead of tuning")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-order", action="store_true", help="kernel maps without the OS density order (ablation)")
     ap.add_argument("--profile-layers", action="store_true", help="print the per-layer table to stderr")
     return ap.parse_args()
 
@@ -259,7 +260,7 @@ def main():
     n = coords_np.shape[0]
     spec = spec_for(coords_np) if args.config != 4 else spc.spc_plan_pack(
         coords_np[:, 1:].min(0), coords_np[:, 1:].max(0), 8, 16, 16)
-    net = SparseNet(n, spec, device=dev, net=net_name)
+    net = SparseNet(n, spec, device=dev, net=net_name, density_order=not args.no_order)
     coords = torch.from_numpy(coords_np).to(dev)
     feats = torch.zeros(n, C_IN_PAD, dtype=torch.bfloat16, device=dev)
     feats[:, :feats_np.shape[1]] = torch.from_numpy(feats_np).to(dev, torch.bfloat16)

@@ -160,6 +160,12 @@ typedef struct {
                                        * table (outputs stably sorted by their match mask) that
                                        * spc_conv_forward uses: tiles of outputs with similar
                                        * neighbour patterns skip more empty offset chunks     */
+#define SPC_KMAP_SIMPLE_BSEARCH 0x10u /* ablation: build the OS table with the
+                                       * paper's "Simple BSearch" baseline:
+                                       * one global binary search per (output, offset) =
+                                       * |V_q|*K^3 searches instead of |V_q|*K^2 (z-delta).
+                                       * Needs an all-OS t (SPC_ERR_UNSUPPORTED otherwise);
+                                       * DENSITY_ORDER is ignored; standalone builds only.   */
 
 #define SPC_MAX_KVOL 125
 

@@ -25,6 +25,7 @@ SPC_KMAP_HALVE_SYMMETRIC = 0x1
 SPC_KMAP_CHECK_SORTED = 0x2
 SPC_KMAP_COUNT_SEARCHES = 0x4
 SPC_KMAP_DENSITY_ORDER = 0x8
+SPC_KMAP_SIMPLE_BSEARCH = 0x10
 SPC_FLAG_RANGE, SPC_FLAG_DUPLICATE, SPC_FLAG_UNSORTED, SPC_FLAG_CAPACITY = 1, 2, 4, 8
 SPC_MAX_KVOL = 125
 
@@ -258,6 +259,12 @@ class KernelMap:
     def os_table(self) -> torch.Tensor:
         return self._view(self.c.os_table, self.c.n_out * self.c.k_dense, torch.int32).view(self.c.n_out,
                                                                                               self.c.k_dense)
+
+    def tile_mask(self) -> torch.Tensor:
+        """[tiles, words] int32: bit c of a 128-row tile set iff dense column c has a match in it."""
+        n, w = self.c.n_out, self.c.tile_words
+        tiles = (n + 127) // 128
+        return self._view(self.c.tile_mask_dev, tiles * w, torch.int32).view(tiles, w)
 
     def density_order(self):
         """(os_rows [n_out], os_table_ord [n_out, k_dense], tile_mask_ord [tiles, words]) of a

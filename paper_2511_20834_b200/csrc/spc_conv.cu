@@ -134,16 +134,6 @@ __device__ __forceinline__ void decode_tile(const ConvParams &p, int64_t v, cons
         t.rows = (int)imin64(tr, n_out - t.row0);
         t.dir = 0;
         t.k = -1;
-        bool any = false;
-        const int64_t mt0 = t.row0 / 128, mt1 = (t.row0 + t.rows - 1) / 128;   // kernel-map mask tiles
-        for (int w = 0; w < 4; ++w) {
-            uint32_t m = 0;
-            if (w < p.tile_words)
-                for (int64_t mt = mt0; mt <= mt1; ++mt) m |= p.tile_mask[mt * p.tile_words + w];
-            t.mask[w] = m;
-            any |= t.mask[w] != 0;
-        }
-        if (!any) t.mask[0] = 1u;   // keep one (all-sentinel) step so the tile is written
     } else {
         int l = 0;
         while (l + 1 < p.n_lists && list_prefix[l + 1] <= tv) ++l;
@@ -159,6 +149,20 @@ __device__ __forceinline__ void decode_tile(const ConvParams &p, int64_t v, cons
         t.mask[0] = 1u;
         t.mask[1] = t.mask[2] = t.mask[3] = 0u;
     }
+}
+
+// OS: the tile's active offset columns (kernel-map tile mask words of its 128-row tiles)
+__device__ __forceinline__ void decode_tile_mask(const ConvParams &p, TileInfo &t) {
+    bool any = false;
+    const int64_t mt0 = t.row0 / 128, mt1 = (t.row0 + t.rows - 1) / 128;   // kernel-map mask tiles
+    for (int w = 0; w < 4; ++w) {
+        uint32_t m = 0;
+        if (w < p.tile_words)
+            for (int64_t mt = mt0; mt <= mt1; ++mt) m |= p.tile_mask[mt * p.tile_words + w];
+        t.mask[w] = m;
+        any |= t.mask[w] != 0;
+    }
+    if (!any) t.mask[0] = 1u;   // keep one (all-sentinel) step so the tile is written
 }
 
 __device__ __forceinline__ int next_bit(const uint32_t (&m)[4], int from) {
@@ -265,6 +269,9 @@ struct ConvSmem {
     TileRec trec[TREC_SLOTS];
 };
 
+#ifdef SPC_EXP_TRACE3
+#define SPC_EXP_TRACE2
+#endif
 #ifdef SPC_EXP_TRACE2
 // per-CTA timeline (globaltimer ns): 0 entry, 1 after setup sync, 2 first stage full (MMA),
 // 3 last commit, 4 exit, 5 tiles done, 6 stages done
@@ -274,9 +281,19 @@ __device__ __forceinline__ unsigned long long gtime() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
+#ifdef SPC_EXP_TRACE3
+// first-tile events instead: 0 entry, 1 setup, 2 sched decoded, 3 sched record done,
+// 4 gather saw index block, 5 gather issued stage 0, 6 weights issued stage 0, 7 MMA full
+#define TL(slot, v) do {} while (0)
+#define TF(slot) do { if (blockIdx.x < 1024) g_tl[slot][blockIdx.x] = gtime(); } while (0)
+#else
 #define TL(slot, v) do { if (blockIdx.x < 1024) g_tl[slot][blockIdx.x] = (v); } while (0)
+#endif
 #else
 #define TL(slot, v) do {} while (0)
+#endif
+#ifndef TF
+#define TF(slot) do {} while (0)
 #endif
 #ifdef SPC_EXP_TRACE
 __device__ long long g_tr[8][4096];
@@ -369,24 +386,35 @@ __device__ __noinline__ void os_split_fixup(const ConvParams &p, ConvSmem &cs, c
 // row r lands at j ^ f(r)).  Matched rows: one whole-line request per row; sentinel rows
 // (no input voxel) never touch L2: zeroed with a shared store.
 template <int BK, int NBT>
-__device__ __forceinline__ void gather_slices(const ConvParams &p, const TileRec &R, const int32_t *B, int kd, int rows,
+__device__ __forceinline__ void gather_slices(const ConvParams &p, const TileRec &R, uint32_t Bs, int kd, int rows,
                                               int sl, int nin, uint32_t abase, uint32_t kb_a, int warp, int r_in,
                                               int q_lane) {
     constexpr uint32_t rb = BK * 2;
     constexpr int RPI = 32 / (BK / 8);
     constexpr int ROWS_W = NBT * RPI;
-    for (int kb = 0; kb < nin; ++kb) {
-        const int ci = (sl + kb) / p.n_chunks, cc = (sl + kb) - ci * p.n_chunks;
+    // all of a slice's gather indices are loaded (explicit ld.shared, independent) before
+    // its copies are issued
+    auto load_idx = [&](int kb, int32_t (&g)[NBT]) {
+        const int ci = (sl + kb) / p.n_chunks;
         const int c = p.mode == 0 ? R.cols[ci] : 0;
+#pragma unroll
+        for (int b = 0; b < NBT; ++b) {
+            const int r = warp * ROWS_W + b * RPI + r_in;
+            g[b] = r < rows ? ptx::lds_s32(Bs + (uint32_t)(r * kd + c) * 4u) : -1;
+        }
+    };
+    for (int kb = 0; kb < nin; ++kb) {
+        int32_t g[NBT];
+        load_idx(kb, g);
+        const int cc = (sl + kb) % p.n_chunks;
         const uint32_t kbo = kb * kb_a;
 #pragma unroll
         for (int b = 0; b < NBT; ++b) {
             const int r = warp * ROWS_W + b * RPI + r_in;
-            const int32_t g = r < rows ? B[r * kd + c] : -1;
             const uint32_t f = rb == 128 ? (r & 7) : (rb == 64 ? ((r >> 1) & 3) : ((r >> 2) & 1));
             const uint32_t so = kbo + (uint32_t)r * rb + ((q_lane ^ f) * 16);
-            if (g >= 0)
-                ptx::cp_async_16(abase + so, p.f_in + (int64_t)g * p.ld_in_bytes + cc * rb + q_lane * 16, 16u);
+            if (g[b] >= 0)
+                ptx::cp_async_16(abase + so, p.f_in + (int64_t)g[b] * p.ld_in_bytes + cc * rb + q_lane * 16, 16u);
             else
                 asm volatile("st.shared.v4.b32 [%0], {%1,%1,%1,%1};" ::"r"(abase + so), "r"(0) : "memory");
         }
@@ -413,14 +441,16 @@ __device__ __forceinline__ void gather_role(const ConvParams &p, ConvSmem &cs, c
         const int rows = R.rows, ncols = R.ncols;
         const int bs = ti % p.blk_slots;
         ptx::mbar_wait(ptx::smem_u32(&cs.blk_full[bs]), (ti / p.blk_slots) & 1);
+        if (ti == 0 && warp == 0 && lane == 0) TF(4);
         const int32_t *B = blk + bs * blk_stride;
         const int nsl = ncols * p.n_chunks;
         for (int sl = 0; sl < nsl; sl += nkb) {
             const int nin = min(nkb, nsl - sl);
             ptx::mbar_wait(ptx::smem_u32(&cs.empty[s]), ph ^ 1);
-            gather_slices<BK, NBT>(p, R, B, kd, rows, sl, nin, ptx::smem_u32(sa + (size_t)s * a_bytes), kb_a, warp, r_in,
-                                   q_lane);
+            gather_slices<BK, NBT>(p, R, ptx::smem_u32(B), kd, rows, sl, nin, ptx::smem_u32(sa + (size_t)s * a_bytes), kb_a,
+                                   warp, r_in, q_lane);
             ptx::cp_async_mbar_arrive(ptx::smem_u32(&cs.full[s]));
+            if (ti == 0 && sl == 0 && warp == 0 && lane == 0) TF(5);
             if (++s == S) { s = 0; ph ^= 1; }
         }
         __syncwarp();
@@ -502,6 +532,51 @@ __device__ __forceinline__ void epi_role(const ConvParams &p, ConvSmem &cs, uint
 #endif
 }
 
+// fp32 accumulator rows -> output dtype (+ residual), 8 columns per work item; the
+// accumulator is returned to zero (workspace invariant).
+__device__ __forceinline__ void convert_items(float *__restrict__ acc, int64_t ld_acc, int64_t n, int c_out, int out_dtype,
+                                              void *__restrict__ out, int64_t ld_out, const void *__restrict__ res,
+                                              int64_t ld_res, int clear, int64_t first, int64_t stride) {
+    const int g8 = c_out / 8;                 // c_out is a multiple of 16
+    const int64_t total = n * g8;
+    for (int64_t e = first; e < total; e += stride) {
+        const int64_t r = e / g8;
+        const int c = (int)(e - r * g8) * 8;
+        float4 *ap = reinterpret_cast<float4 *>(acc + r * ld_acc + c);
+        const float4 a0 = __ldcg(ap), a1 = __ldcg(ap + 1);
+        if (clear) {
+            __stcg(ap, make_float4(0.f, 0.f, 0.f, 0.f));
+            __stcg(ap + 1, make_float4(0.f, 0.f, 0.f, 0.f));
+        }
+        float v[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+        if (out_dtype == SPC_F32) {
+            if (res) {
+                const float4 b0 = *reinterpret_cast<const float4 *>(static_cast<const float *>(res) + r * ld_res + c);
+                const float4 b1 = *reinterpret_cast<const float4 *>(static_cast<const float *>(res) + r * ld_res + c + 4);
+                v[0] += b0.x; v[1] += b0.y; v[2] += b0.z; v[3] += b0.w;
+                v[4] += b1.x; v[5] += b1.y; v[6] += b1.z; v[7] += b1.w;
+            }
+            float *o = static_cast<float *>(out) + r * ld_out + c;
+            *reinterpret_cast<float4 *>(o) = make_float4(v[0], v[1], v[2], v[3]);
+            *reinterpret_cast<float4 *>(o + 4) = make_float4(v[4], v[5], v[6], v[7]);
+        } else {
+            if (res) {
+                const uint4 u = *reinterpret_cast<const uint4 *>(static_cast<const uint16_t *>(res) + r * ld_res + c);
+                const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float2 f = unpack2(w[q], out_dtype);
+                    v[2 * q] += f.x;
+                    v[2 * q + 1] += f.y;
+                }
+            }
+            *reinterpret_cast<uint4 *>(static_cast<uint16_t *>(out) + r * ld_out + c) =
+                make_uint4(pack2(v[0], v[1], out_dtype), pack2(v[2], v[3], out_dtype), pack2(v[4], v[5], out_dtype),
+                           pack2(v[6], v[7], out_dtype));
+        }
+    }
+}
+
 template <int BK, int BM>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant__ ConvParams p) {
     constexpr int NH = BM / TC_BM;   // 128-row MMA halves per tile
@@ -521,6 +596,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
 #ifdef SPC_EXP_TRACE2
     if (threadIdx.x == 0) TL(0, gtime());
 #endif
+    if (threadIdx.x == 0) TF(0);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < 16; ++s) {
@@ -612,6 +688,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
 #ifdef SPC_EXP_TRACE2
     if (threadIdx.x == 0) TL(1, gtime());
 #endif
+    if (threadIdx.x == 0) TF(1);
     constexpr uint32_t rb = BK * 2;           // bytes per operand row (= swizzle span)
     const int tr = cs.tr, wsplit = cs.wsplit, nht = tr / TC_BM;
     // the ring carve of this tile height
@@ -701,6 +778,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             }
             TileInfo t;
             decode_tile(p, v, cs.list_prefix, n_out, tr, wsplit ? cs.sp_pre : nullptr, cs.sp_cnt, cs.n_sp, t);
+            if (ti == 0 && lane == 0) TF(2);
+            // the tile's gather indices first (they depend only on its rows): the block's
+            // load overlaps the record's mask / column / scatter work below
+            const int bs = ti % p.blk_slots;
+            ptx::mbar_wait_sleep(ptx::smem_u32(&cs.blk_empty[bs]), ((ti / p.blk_slots) & 1) ^ 1);
+            int32_t *B = blk + bs * blk_stride;
+            const uint32_t fb = ptx::smem_u32(&cs.blk_full[bs]);
+            if (p.mode == 0) {
+                // OS: rows [row0, row0+rows) of the [n_out x k_dense] table are contiguous
+                const uint32_t bytes = (uint32_t)((t.rows * p.k_dense * 4 + 15) & ~15);
+                if (lane == 0) {
+                    ptx::mbar_arrive_expect_tx(fb, bytes);
+                    ptx::bulk_g2s(ptx::smem_u32(B), p.os + t.row0 * p.k_dense, bytes, fb);
+                }
+                if (lane != 0) ptx::mbar_arrive(fb);
+                decode_tile_mask(p, t);
+            }
             if (lane == 0) {
                 R.row0 = t.row0; R.rows = t.rows; R.nt = t.nt; R.list = t.list; R.dir = t.dir; R.k = t.k; R.end = 0;
                 R.nsplit = p.mode == 0 ? t.nsplit : 1;
@@ -718,29 +812,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             }
             if (p.mode == 1) {
                 const int32_t *pr = reinterpret_cast<const int32_t *>(p.pairs + t.list * p.list_stride + t.row0);
-                for (int r = lane; r < BM; r += 32) R.scatter[r] = r < t.rows ? pr[2 * r + (t.dir ? 0 : 1)] : -1;
+                for (int r = lane; r < BM; r += 32) {
+                    const int2 pq = r < t.rows ? reinterpret_cast<const int2 *>(pr)[r] : make_int2(-1, -1);
+                    R.scatter[r] = t.dir ? pq.x : pq.y;
+                    B[r] = t.dir ? pq.y : pq.x;
+                }
+                ptx::mbar_arrive(fb);
             } else if (p.os_rows) {
                 for (int r = lane; r < tr; r += 32) R.scatter[r] = r < t.rows ? p.os_rows[t.row0 + r] : -1;
             }
             ptx::mbar_arrive(ptx::smem_u32(&cs.trec_full[st]));
-            // the tile's gather indices: one contiguous block
-            const int bs = ti % p.blk_slots;
-            ptx::mbar_wait_sleep(ptx::smem_u32(&cs.blk_empty[bs]), ((ti / p.blk_slots) & 1) ^ 1);
-            int32_t *B = blk + bs * blk_stride;
-            const uint32_t fb = ptx::smem_u32(&cs.blk_full[bs]);
-            if (p.mode == 0) {
-                // OS: rows [row0, row0+rows) of the [n_out x k_dense] table are contiguous
-                const uint32_t bytes = (uint32_t)((t.rows * p.k_dense * 4 + 15) & ~15);
-                if (lane == 0) {
-                    ptx::mbar_arrive_expect_tx(fb, bytes);
-                    ptx::bulk_g2s(ptx::smem_u32(B), p.os + t.row0 * p.k_dense, bytes, fb);
-                }
-                if (lane != 0) ptx::mbar_arrive(fb);
-            } else {
-                const int32_t *pr = reinterpret_cast<const int32_t *>(p.pairs + t.list * p.list_stride + t.row0);
-                for (int r = lane; r < BM; r += 32) B[r] = r < t.rows ? pr[2 * r + (t.dir ? 1 : 0)] : -1;
-                ptx::mbar_arrive(fb);
-            }
+            if (ti == 0 && lane == 0) TF(3);
         }
         ptx::cp_async_wait<0>();
     } else if (warp < N_GATHER) {
@@ -775,6 +857,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                         ptx::bulk_g2s(ptx::smem_u32(sb + (size_t)s * b_bytes + kb * p.kb_b), p.wblob + blob * p.kb_b,
                                       p.kb_b, fb);
                     }
+                    if (it == 0) TF(6);
                 }
                 ptx::mbar_arrive(ptx::smem_u32(&cs.trec_empty[st]));
             }
@@ -804,6 +887,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
 #ifdef SPC_EXP_TRACE2
                     if (it == 0) TL(2, gtime());
 #endif
+                    if (it == 0) TF(7);
                     // the A tile was written by cp.async / st.shared (generic proxy): order it
                     // before the tensor core's async-proxy reads
                     ptx::fence_proxy_async();
@@ -1017,44 +1101,8 @@ __global__ void k_convert(float *__restrict__ acc, int64_t ld_acc, int64_t n_cap
     pdl_wait();
     pdl_trigger();
     const int64_t n = dev_count(n_cap, n_dev);
-    const int g8 = c_out / 8;                 // c_out is a multiple of 16
-    const int64_t total = n * g8;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = e / g8;
-        const int c = (int)(e - r * g8) * 8;
-        float4 *ap = reinterpret_cast<float4 *>(acc + r * ld_acc + c);
-        const float4 a0 = ap[0], a1 = ap[1];
-        if (clear) {
-            ap[0] = make_float4(0.f, 0.f, 0.f, 0.f);
-            ap[1] = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-        float v[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-        if (out_dtype == SPC_F32) {
-            if (res) {
-                const float4 b0 = *reinterpret_cast<const float4 *>(static_cast<const float *>(res) + r * ld_res + c);
-                const float4 b1 = *reinterpret_cast<const float4 *>(static_cast<const float *>(res) + r * ld_res + c + 4);
-                v[0] += b0.x; v[1] += b0.y; v[2] += b0.z; v[3] += b0.w;
-                v[4] += b1.x; v[5] += b1.y; v[6] += b1.z; v[7] += b1.w;
-            }
-            float *o = static_cast<float *>(out) + r * ld_out + c;
-            *reinterpret_cast<float4 *>(o) = make_float4(v[0], v[1], v[2], v[3]);
-            *reinterpret_cast<float4 *>(o + 4) = make_float4(v[4], v[5], v[6], v[7]);
-        } else {
-            if (res) {
-                const uint4 u = *reinterpret_cast<const uint4 *>(static_cast<const uint16_t *>(res) + r * ld_res + c);
-                const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const float2 f = unpack2(w[q], out_dtype);
-                    v[2 * q] += f.x;
-                    v[2 * q + 1] += f.y;
-                }
-            }
-            *reinterpret_cast<uint4 *>(static_cast<uint16_t *>(out) + r * ld_out + c) =
-                make_uint4(pack2(v[0], v[1], out_dtype), pack2(v[2], v[3], out_dtype), pack2(v[4], v[5], out_dtype),
-                           pack2(v[6], v[7], out_dtype));
-        }
-    }
+    convert_items(acc, ld_acc, n, c_out, out_dtype, out, ld_out, res, ld_res, clear,
+                  blockIdx.x * (int64_t)blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x);
 }
 
 __global__ void k_zero_rows(float *__restrict__ acc, int64_t ld, int64_t n_cap, const int64_t *n_dev, int c) {

@@ -464,6 +464,47 @@ __global__ void __launch_bounds__(KM_THREADS, SPC_KM_MIN_BLOCKS) k_kmap_zdelta(c
 }
 
 // ------------------------------------------------------------------------------------
+// ablation (SPC_KMAP_SIMPLE_BSEARCH): the paper's "Simple BSearch" mapping baseline
+// (P:257-259): one independent binary search over the whole sorted input per (output,
+// offset), |V_q| K^3 searches.  One thread per (offset k, output i), i fastest, so a warp
+// holds 32 consecutive outputs of one offset (one ballot for the counts and tile mask).
+// ------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_kmap_bsearch(const __grid_constant__ KmapDesc p, int bits_y, int bits_z) {
+    const int64_t n_out = dev_count(p.n_out_cap, p.n_out_dev);
+    const int64_t n_in = dev_count(p.n_in_cap, p.n_in_dev);
+    const int64_t n_pad = (n_out + 31) & ~int64_t(31);
+    const int K = p.K, r = (K - 1) / 2, kv = K * K * K;
+    const int lane = threadIdx.x & 31;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < kv * n_pad; e += (int64_t)gridDim.x * blockDim.x) {
+        const int k = (int)(e / n_pad);
+        const int64_t i = e - k * n_pad;
+        const int col = p.dcol[k];
+        const int ex = k / (K * K) - r, ey = (k / K) % K - r, ez = k % K - r;
+        int64_t d = (int64_t)ex * p.spacing * (1ll << (bits_y + bits_z)) + (int64_t)ey * p.spacing * (1ll << bits_z) +
+                    (int64_t)ez * p.spacing;
+        if (p.transposed) d = -d;
+        const bool valid = i < n_out;
+        bool match = false;
+        int32_t j = -1;
+        if (valid) {
+            const uint64_t q = p.out[i] + (uint64_t)d;
+            const int64_t pos = lower_bound_g(p.in, n_in, q);
+            match = pos < n_in && __ldg(p.in + pos) == q;
+            if (match) j = (int32_t)pos;
+            p.os[i * p.k_dense + col] = j;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, match), vb = __ballot_sync(0xffffffffu, valid);
+        if (lane == 0) {
+            if (bal) {
+                atomicAdd(&p.counts[k], __popc(bal));
+                atomicOr(&p.tile_mask[(i / KM_BM) * p.tile_words + (col >> 5)], 1u << (col & 31));
+            }
+            if (p.stats && vb) atomicAdd(&p.stats[0], (unsigned long long)__popc(vb));
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
 // density order of the OS part (SPC_KMAP_DENSITY_ORDER): outputs stably sorted by which
 // offset directions they have neighbours in, so a 128-row tile of similar neighbour
 // patterns has fewer non-empty offset chunks and fewer sentinel rows.  Any row order
@@ -971,6 +1012,22 @@ extern "C" spc_status spc_build_kmap(const uint64_t *in_keys, int64_t n_in, cons
             d.ord_idx = (int8_t)g_defer.orders.size();
             g_defer.orders.push_back(job);
         }
+        return SPC_OK;
+    }
+    if (flags & SPC_KMAP_SIMPLE_BSEARCH) {
+        // ablation baseline: all-OS maps only, no density order
+        if (pl.n_lists != 0) return fail(SPC_ERR_UNSUPPORTED, "SPC_KMAP_SIMPLE_BSEARCH needs an all-OS t (SPC_T_ALL_OS)");
+        KmapDesc d;
+        fill_desc(d, km, pl, reinterpret_cast<int32_t *>(base + L.bounds));
+        km.os_rows = nullptr;
+        km.os_table_ord = nullptr;
+        km.tile_mask_ord = nullptr;
+        km.tile_order = nullptr;
+        SPC_CUDA(cudaMemsetAsync(base + L.counts, 0, L.stats + 2 * sizeof(unsigned long long) - L.counts, st));
+        const int64_t items = (int64_t)pl.k_vol * ((n_out + 31) & ~int64_t(31));
+        k_kmap_bsearch<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, 32 * (int64_t)num_sms())), 256,
+                         0, st>>>(d, spec.bits_y, spec.bits_z);
+        SPC_LAUNCH_CHECK("k_kmap_bsearch");
         return SPC_OK;
     }
     KmapBatch b;

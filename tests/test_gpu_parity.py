@@ -155,6 +155,39 @@ def test_kmap_bit_exact(K, d, kind, t, flags):
             assert st[0] <= n_out * K * K                              # halving skips groups
 
 
+@pytest.mark.parametrize("K,d,kind", [(3, 1, "subm"), (5, 1, "subm"), (3, 2, "subm"), (3, 1, "strided"),
+                                      (3, 1, "transposed"), (1, 1, "subm")])
+def test_kmap_simple_bsearch_ablation(K, d, kind):
+    """NEXT-1 ablation: the paper's Simple BSearch mapping builds the same map
+    as the oracle with exactly |V_q| K^3 binary searches; it needs an all-OS t."""
+    coords = synth.make_scan(1, 1)
+    spec = _spec_for(coords)
+    lv = _levels(coords, spec, [2])
+    fine_k, fine_c = lv[1]
+    coarse_k, coarse_c = lv[2]
+    fl = spc.SPC_KMAP_SIMPLE_BSEARCH | spc.SPC_KMAP_COUNT_SEARCHES
+    if kind == "subm":
+        km = spc.spc_build_kmap(fine_k, fine_k, spec, spc.Geom(K, 1, d, 1, 0), -1, fl)
+        ref, n_out = oracle.kmap(fine_c, fine_c, K, d), len(fine_c)
+    elif kind == "strided":
+        km = spc.spc_build_kmap(fine_k, coarse_k, spec, spc.Geom(K, 2, d, 1, 0), -1, fl)
+        ref, n_out = oracle.kmap(fine_c, coarse_c, K, d), len(coarse_c)
+    else:
+        km = spc.spc_build_kmap(coarse_k, fine_k, spec, spc.Geom(K, 2, d, 1, 1), -1, fl)
+        ref, n_out = oracle.kmap(coarse_c, fine_c, K, d, transposed=True), len(fine_c)
+    np.testing.assert_array_equal(spc.spc_kmap_export(km), ref)
+    assert km.search_stats().cpu().numpy()[0] == n_out * K ** 3          # P:257-259 |V_q| K^3 searches
+    # the tile mask marks exactly the (128-row tile, offset) chunks with a match
+    tab = km.os_table().cpu().numpy().reshape(n_out, -1)
+    words = km.tile_mask().cpu().numpy().view(np.uint32)
+    for t0 in range(0, n_out, 128):
+        any_c = (tab[t0:t0 + 128] >= 0).any(0)
+        got = np.array([(words[t0 // 128, c // 32] >> (c % 32)) & 1 for c in range(tab.shape[1])], bool)
+        assert np.array_equal(got, any_c)
+    with pytest.raises(spc.SpcError):
+        spc.spc_build_kmap(fine_k, fine_k, spec, spc.Geom(3, 1, 1, 1, 0), 2, spc.SPC_KMAP_SIMPLE_BSEARCH)
+
+
 def test_kmap_os_table_exact_and_centre():
     coords = synth.make_scan(1, 0)
     spec = _spec_for(coords)
