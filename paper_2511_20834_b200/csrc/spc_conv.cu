@@ -84,6 +84,8 @@ struct ConvParams {
                           // [CTR_EXIT] CTAs exited, [CTR_FETCH] dynamic tile fetch
     int blk_slots;        // gather-index blocks in flight (2, or 1 when a block is large: K=5 OS)
     uint32_t tmem_cols;   // per 128-row accumulator (power of two >= 32)
+    int tbufs;            // accumulator buffers per CTA: 2 (epilogue overlaps the next tile's MMAs)
+                          // or 1 (256-row tiles of N = 256: 2 x 256 columns fill TMEM)
     uint32_t idesc;
     // output
     void *out;
@@ -474,9 +476,9 @@ __device__ __forceinline__ void epi_role(const ConvParams &p, ConvSmem &cs, uint
         ptx::mbar_wait_sleep(ptx::smem_u32(&cs.trec_full[st]), (ti / TREC_SLOTS) & 1);
         const TileRec &R = cs.trec[st];
         if (R.end) break;
-        const uint32_t a = ti & 1;
+        const uint32_t a = ti % p.tbufs;
         const int nt = R.nt;
-        ptx::mbar_wait_sleep(ptx::smem_u32(&cs.tfull[a]), (ti >> 1) & 1);
+        ptx::mbar_wait_sleep(ptx::smem_u32(&cs.tfull[a]), (ti / p.tbufs) & 1);
         if (threadIdx.x == 32 * W_EPI0) TR(6, ti);
 #ifdef SPC_EXP_TRACE2
         if (threadIdx.x == 32 * W_EPI0) TL(5, gtime());
@@ -619,7 +621,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         ptx::fence_mbar_init();
         ptx::fence_proxy_async();
     }
-    if (warp == W_MMA) ptx::tmem_alloc(ptx::smem_u32(cs.tmem_holder), 2 * NH * p.tmem_cols);
+    if (warp == W_MMA) ptx::tmem_alloc(ptx::smem_u32(cs.tmem_holder), p.tbufs * NH * p.tmem_cols);
     // everything above overlaps the previous kernel's tail (PDL); maps, features, weights
     // and outputs are touched only after this point
     pdl_wait();
@@ -873,8 +875,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             if (R.end) break;
             if (lane == 0) {
                 const int ncols = R.ncols;
-                const uint32_t a = ti & 1;
-                ptx::mbar_wait(ptx::smem_u32(&cs.tempty[a]), ((ti >> 1) & 1) ^ 1);
+                const uint32_t a = ti % p.tbufs;
+                ptx::mbar_wait(ptx::smem_u32(&cs.tempty[a]), ((ti / p.tbufs) & 1) ^ 1);
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + a * NH * p.tmem_cols;
                 uint32_t acc = 0;
@@ -934,7 +936,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     __syncthreads();
     if (warp == W_MMA) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc(tmem_base, 2 * NH * p.tmem_cols);
+        ptx::tmem_dealloc(tmem_base, p.tbufs * NH * p.tmem_cols);
     }
 #ifdef SPC_EXP_TRACE2
     if (threadIdx.x == 0) TL(4, gtime());
@@ -1366,8 +1368,12 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
     p.split_tiles_per_sm2 = getenv("SPC_SPLIT_TILES2") ? atoi(getenv("SPC_SPLIT_TILES2")) : p.num_sms;
     // 256-row tiles (two MMAs per weight tile) whenever four accumulators fit TMEM; the
     // kernel drops to 128-row tiles on the device when the live row count is small
-    p.bm = (4 * p.tmem_cols <= 512 && !getenv("SPC_BM128")) ? 256 : 128;
+    // (experiment SPC_BM256_SINGLE: N = 256 with 256-row tiles and one accumulator buffer;
+    // measured no faster on the 256x256 layers: the 64 KB stages leave only 2 in flight)
+    static const bool bm256_single = getenv("SPC_BM256_SINGLE") != nullptr;
+    p.bm = ((4 * p.tmem_cols <= 512 || (bm256_single && 2 * p.tmem_cols <= 512)) && !getenv("SPC_BM128")) ? 256 : 128;
     if (has_os && (size_t)BLK_SLOTS * p.bm * km->k_dense * 4 > 96 * 1024) p.bm = 128;   // OS index blocks (K=5)
+    p.tbufs = (p.bm == 256 ? 4 : 2) * p.tmem_cols <= 512 ? 2 : 1;
     p.kb_b = (uint32_t)(p.BN * p.BK * 2);
     p.idesc = ptx::umma_idesc_f16(in_dtype == SPC_BF16, TC_BM, p.BN);
     p.wblob = static_cast<const char *>(weight);

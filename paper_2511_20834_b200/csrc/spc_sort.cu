@@ -51,8 +51,10 @@ __device__ __forceinline__ int block_excl_scan_256(int v, int *warp_sums, int &t
 // k_onesweep   : one launch per pass; tiles are claimed in order from an atomic counter,
 //                ranked locally (__match_any_sync, stable), and get their global offsets by
 //                decoupled look-back over the per-tile digit counts of earlier tiles.
-constexpr int OS_ITEMS = 8;
-constexpr int OS_TILE = SORT_THREADS * OS_ITEMS;   // 2048 keys per tile
+// keys per tile = SORT_THREADS * ITEMS, ITEMS in {2, 4, 8}: the smallest tiles that still
+// give >= 2 tiles per SM's worth of CTAs, so small sorts (one scan, ~100k keys) spread
+// over every SM instead of ~50 CTAs
+constexpr int OS_ITEMS_MIN = 2;
 constexpr int MAX_PASSES = 8;
 constexpr uint32_t ST_AGG = 1u << 30, ST_INC = 2u << 30, ST_VAL = (1u << 30) - 1;
 
@@ -90,7 +92,7 @@ __global__ void k_hist_scan(unsigned int *__restrict__ ghist, int passes) {
     }
 }
 
-template <bool VALS>
+template <bool VALS, int OS_ITEMS>
 __global__ void __launch_bounds__(SORT_THREADS) k_onesweep(const uint64_t *__restrict__ keys_in,
                                                            const int32_t *__restrict__ vals_in, int64_t n_cap,
                                                            const int64_t *n_dev, int shift,
@@ -103,6 +105,7 @@ __global__ void __launch_bounds__(SORT_THREADS) k_onesweep(const uint64_t *__res
     __shared__ int local_start[256];
     __shared__ int cnt[SORT_WARPS][256];
     __shared__ int warp_sums[SORT_WARPS];
+    constexpr int OS_TILE = SORT_THREADS * OS_ITEMS;
     __shared__ uint64_t skeys[OS_TILE];
     __shared__ int32_t svals[VALS ? OS_TILE : 1];
 
@@ -212,11 +215,16 @@ __global__ void k_copy_keys(const uint64_t *__restrict__ a, int64_t n_cap, const
     }
 }
 
-static int os_tiles(int64_t n) { return (int)((n + OS_TILE - 1) / OS_TILE); }
+static int os_items(int64_t n) {
+    for (int it = OS_ITEMS_MIN; it < 8; it *= 2)
+        if ((n + SORT_THREADS * 2 * it - 1) / (SORT_THREADS * 2 * it) < 2 * num_sms()) return it;
+    return 8;
+}
+static int os_tiles(int64_t n, int items) { return (int)((n + SORT_THREADS * items - 1) / (SORT_THREADS * items)); }
 
 size_t radix_sort_workspace(int64_t n, bool with_vals) {
     Sizer s;
-    const int nt = os_tiles(n > 0 ? n : 1);
+    const int nt = os_tiles(n > 0 ? n : 1, OS_ITEMS_MIN);
     s.take<unsigned int>((size_t)MAX_PASSES * 256);                 // histograms / bases
     s.take<unsigned int>((size_t)MAX_PASSES * (nt * 256 + 32));      // tile status + counters
     s.take<uint64_t>((size_t)n);
@@ -232,10 +240,12 @@ spc_status radix_sort(const uint64_t *keys_in, const int32_t *vals_in, int64_t n
     const int passes = (n_bits + 7) / 8;
     if (passes > MAX_PASSES) return fail(SPC_ERR_INVALID_ARG, "radix_sort: too many key bits");
     Bump b(ws, ws_bytes);
-    const int nt = os_tiles(n);
+    const int items = os_items(n);
+    const int nt = os_tiles(n, items);
     unsigned int *hist = b.take<unsigned int>((size_t)MAX_PASSES * 256);
     const size_t stride = (size_t)nt * 256 + 32;
-    unsigned int *status = b.take<unsigned int>((size_t)MAX_PASSES * stride);
+    // (the workspace holds the status of the smallest tiles; only the used part is cleared)
+    unsigned int *status = b.take<unsigned int>((size_t)MAX_PASSES * ((size_t)os_tiles(n, OS_ITEMS_MIN) * 256 + 32));
     uint64_t *ktmp = b.take<uint64_t>((size_t)n);
     int32_t *vtmp = with_vals ? b.take<int32_t>((size_t)n) : nullptr;
     if (!b.ok()) return fail(SPC_ERR_WORKSPACE, "radix_sort: workspace too small");
@@ -244,7 +254,7 @@ spc_status radix_sort(const uint64_t *keys_in, const int32_t *vals_in, int64_t n
         SPC_LAUNCH_CHECK("k_copy_keys");
         return SPC_OK;
     }
-    SPC_CUDA(cudaMemsetAsync(status, 0, sizeof(unsigned int) * MAX_PASSES * stride, st));
+    SPC_CUDA(cudaMemsetAsync(status, 0, sizeof(unsigned int) * passes * stride, st));
     if (!hist_done) {
         SPC_CUDA(cudaMemsetAsync(hist, 0, sizeof(unsigned int) * MAX_PASSES * 256, st));
         const int g = (int)std::max<int64_t>(1, std::min<int64_t>((n + 4095) / 4096, 2 * num_sms()));
@@ -260,12 +270,19 @@ spc_status radix_sort(const uint64_t *keys_in, const int32_t *vals_in, int64_t n
         int32_t *dst_v = with_vals ? (to_out ? vals_out : vtmp) : nullptr;
         unsigned int *stp = status + (size_t)p * stride;
         unsigned int *ctr = stp + (size_t)nt * 256;
-        if (with_vals)
-            k_onesweep<true><<<nt, SORT_THREADS, 0, st>>>(src_k, src_v, n, n_dev, 8 * p, hist + p * 256, stp, ctr,
-                                                         dst_k, dst_v);
-        else
-            k_onesweep<false><<<nt, SORT_THREADS, 0, st>>>(src_k, nullptr, n, n_dev, 8 * p, hist + p * 256, stp, ctr,
-                                                          dst_k, nullptr);
+#define SPC_ONESWEEP(IT)                                                                                     \
+    do {                                                                                                     \
+        if (with_vals)                                                                                       \
+            k_onesweep<true, IT><<<nt, SORT_THREADS, 0, st>>>(src_k, src_v, n, n_dev, 8 * p, hist + p * 256, stp, \
+                                                              ctr, dst_k, dst_v);                            \
+        else                                                                                                 \
+            k_onesweep<false, IT><<<nt, SORT_THREADS, 0, st>>>(src_k, nullptr, n, n_dev, 8 * p, hist + p * 256,  \
+                                                               stp, ctr, dst_k, nullptr);                    \
+    } while (0)
+        if (items == 2) SPC_ONESWEEP(2);
+        else if (items == 4) SPC_ONESWEEP(4);
+        else SPC_ONESWEEP(8);
+#undef SPC_ONESWEEP
         SPC_LAUNCH_CHECK("onesweep pass");
         src_k = dst_k;
         src_v = dst_v;
