@@ -167,6 +167,12 @@ __device__ __forceinline__ void decode_tile_mask(const ConvParams &p, TileInfo &
     if (!any) t.mask[0] = 1u;   // keep one (all-sentinel) step so the tile is written
 }
 
+__device__ __forceinline__ uint32_t ptx_lanemask_lt() {
+    uint32_t r;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+    return r;
+}
+
 __device__ __forceinline__ int next_bit(const uint32_t (&m)[4], int from) {
     if (from >= 128) return -1;
 #pragma unroll
@@ -795,33 +801,69 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                     ptx::bulk_g2s(ptx::smem_u32(B), p.os + t.row0 * p.k_dense, bytes, fb);
                 }
                 if (lane != 0) ptx::mbar_arrive(fb);
-                decode_tile_mask(p, t);
+            }
+            // output-row scatter values (WS pairs / OS density order) are loaded before the
+            // mask is consumed, so the two round trips overlap
+            constexpr int SCN = BM / 32;
+            int32_t sc[SCN], gx[SCN];
+            if (p.mode == 1) {
+                const int2 *pr = p.pairs + t.list * p.list_stride + t.row0;
+#pragma unroll
+                for (int q = 0; q < SCN; ++q) {
+                    const int r = q * 32 + lane;
+                    const int2 pq = r < t.rows ? pr[r] : make_int2(-1, -1);
+                    sc[q] = t.dir ? pq.x : pq.y;
+                    gx[q] = t.dir ? pq.y : pq.x;
+                }
+            } else if (p.os_rows) {
+#pragma unroll
+                for (int q = 0; q < SCN; ++q) {
+                    const int r = q * 32 + lane;
+                    sc[q] = (r < tr && r < t.rows) ? p.os_rows[t.row0 + r] : -1;
+                }
+            }
+            if (p.mode == 0) decode_tile_mask(p, t);
+            // active columns: warp-parallel compaction of the mask bits (ballot prefix),
+            // then this part's contiguous share when the tile is split
+            int nc = 0;
+            {
+                int c0 = 0, c1 = 128;
+                int total = 0;
+#pragma unroll
+                for (int w = 0; w < 4; ++w) total += __popc(t.mask[w]);
+                if (p.mode == 0 && t.nsplit > 1) {
+                    const int per = (total + t.nsplit - 1) / t.nsplit;
+                    c0 = min(total, t.list * per);
+                    c1 = min(total, c0 + per);
+                }
+                int base = 0;
+#pragma unroll
+                for (int w = 0; w < 4; ++w) {
+                    const uint32_t bits = t.mask[w];
+                    const int pos = base + __popc(bits & ptx_lanemask_lt());
+                    if (((bits >> lane) & 1u) && pos >= c0 && pos < c1) R.cols[pos - c0] = (uint8_t)(w * 32 + lane);
+                    base += __popc(bits);
+                }
+                nc = max(0, min(total, c1) - c0);
             }
             if (lane == 0) {
                 R.row0 = t.row0; R.rows = t.rows; R.nt = t.nt; R.list = t.list; R.dir = t.dir; R.k = t.k; R.end = 0;
                 R.nsplit = p.mode == 0 ? t.nsplit : 1;
                 R.ctr = t.ctr;
                 for (int w = 0; w < 4; ++w) R.mask[w] = t.mask[w];
-                int nc = 0;
-                for (int c = next_bit(t.mask, 0); c >= 0; c = next_bit(t.mask, c + 1)) R.cols[nc++] = (uint8_t)c;
-                if (p.mode == 0 && t.nsplit > 1) {   // keep this part's contiguous share
-                    const int per = (nc + t.nsplit - 1) / t.nsplit;
-                    const int c0 = min(nc, t.list * per), c1 = min(nc, c0 + per);
-                    for (int q = c0; q < c1; ++q) R.cols[q - c0] = R.cols[q];
-                    nc = c1 - c0;
-                }
                 R.ncols = nc;
             }
             if (p.mode == 1) {
-                const int32_t *pr = reinterpret_cast<const int32_t *>(p.pairs + t.list * p.list_stride + t.row0);
-                for (int r = lane; r < BM; r += 32) {
-                    const int2 pq = r < t.rows ? reinterpret_cast<const int2 *>(pr)[r] : make_int2(-1, -1);
-                    R.scatter[r] = t.dir ? pq.x : pq.y;
-                    B[r] = t.dir ? pq.y : pq.x;
+#pragma unroll
+                for (int q = 0; q < SCN; ++q) {
+                    R.scatter[q * 32 + lane] = sc[q];
+                    B[q * 32 + lane] = gx[q];
                 }
                 ptx::mbar_arrive(fb);
             } else if (p.os_rows) {
-                for (int r = lane; r < tr; r += 32) R.scatter[r] = r < t.rows ? p.os_rows[t.row0 + r] : -1;
+#pragma unroll
+                for (int q = 0; q < SCN; ++q)
+                    if (q * 32 < tr) R.scatter[q * 32 + lane] = sc[q];
             }
             ptx::mbar_arrive(ptx::smem_u32(&cs.trec_full[st]));
             if (ti == 0 && lane == 0) TF(3);
