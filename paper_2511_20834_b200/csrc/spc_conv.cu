@@ -1120,6 +1120,8 @@ __global__ void __launch_bounds__(256) k_conv_simt(const __grid_constant__ ConvP
 // tile the MMA reads: row n (BK elements = rb bytes), 16-byte chunk j stored at j ^ f(n)
 __global__ void k_prepare_weight_tc(const uint16_t *__restrict__ w, int k_vol, int c_in, int c_out, int BK, int BN,
                                     uint16_t *__restrict__ out) {
+    pdl_wait();   // PDL launch: the predecessor has completed and flushed
+    pdl_trigger();
     const int64_t total = (int64_t)k_vol * c_in * c_out;
     const int n_nt = c_out / BN, n_ch = c_in / BK;
     const int rb = BK * 2;
@@ -1197,9 +1199,9 @@ extern "C" spc_status spc_prepare_weight(const void *weight, int32_t k_vol, int3
     if (c_in % 16 || c_out % 16)
         return fail(SPC_ERR_UNSUPPORTED, "spc_prepare_weight: f16/bf16 needs c_in and c_out multiples of 16");
     const int64_t total = (int64_t)k_vol * c_in * c_out;
-    k_prepare_weight_tc<<<(unsigned)std::min<int64_t>((total + 255) / 256, 4096), 256, 0, st>>>(
+    SPC_CUDA(launch_pdl(k_prepare_weight_tc, dim3((unsigned)std::min<int64_t>((total + 255) / 256, 4096)), dim3(256), 0, st, 
         static_cast<const uint16_t *>(weight), k_vol, c_in, c_out, pick_bk(c_in), pick_bn(c_out),
-        static_cast<uint16_t *>(prepared));
+        static_cast<uint16_t *>(prepared)));
     SPC_LAUNCH_CHECK("k_prepare_weight_tc");
     return SPC_OK;
 }

@@ -42,9 +42,11 @@ int num_sms() {
     return n;
 }
 
-__global__ void k_fill_i64(int64_t *p, int64_t v) { *p = v; }
+__global__ void k_fill_i64(int64_t *p, int64_t v) {
+    pdl_wait();   // PDL launch: the predecessor has completed and flushed
+    pdl_trigger(); *p = v; }
 spc_status fill_i64(int64_t *p, int64_t v, cudaStream_t st) {
-    k_fill_i64<<<1, 1, 0, st>>>(p, v);
+    SPC_CUDA(launch_pdl(k_fill_i64, dim3(1), dim3(1), 0, st, p, v));
     SPC_LAUNCH_CHECK("k_fill_i64");
     return SPC_OK;
 }

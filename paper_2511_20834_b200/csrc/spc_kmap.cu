@@ -97,6 +97,8 @@ __device__ __forceinline__ int lower_bound_s(const uint64_t *a, int n, uint64_t 
 
 // zero the per-map counters / stats and the work counter
 __global__ void k_kmap_prep(const __grid_constant__ KmapBatch b) {
+    pdl_wait();   // PDL launch: the predecessor has completed and flushed
+    pdl_trigger();
     const int m = blockIdx.x;
     if (m == 0 && threadIdx.x == 0) {
         *b.work_ctr = 0;
@@ -127,6 +129,8 @@ __device__ __forceinline__ int64_t group_delta(const KmapDesc &p, int by, int bz
 // bound, so the global binary searches' latency chains all run concurrently instead of
 // once per tile inside the build kernel.
 __global__ void __launch_bounds__(256) k_kmap_bounds(const __grid_constant__ KmapBatch B) {
+    pdl_wait();   // PDL launch: the predecessor has completed and flushed
+    pdl_trigger();
     __shared__ int64_t s_pre[KM_MAX_MAPS + 1];
     if (threadIdx.x == 0) {
         int64_t acc = 0;
@@ -249,6 +253,8 @@ __device__ __forceinline__ int zdelta_chunk(ZTile &zt, int32_t *s_os, int32_t *s
 // (tile, list) (warp ballots, no filter pass; halved for submanifold maps,
 // P:418-421), the tile mask, per-offset counts and density-order keys.
 __global__ void __launch_bounds__(KM_THREADS, SPC_KM_MIN_BLOCKS) k_kmap_zdelta(const __grid_constant__ KmapBatch B) {
+    pdl_wait();   // PDL launch: the predecessor has completed and flushed
+    pdl_trigger();
     __shared__ int8_t s_dcol[KM_MAX_MAPS][SPC_MAX_KVOL];   // weight offset -> dense column / -1
     __shared__ int8_t s_lst[KM_MAX_MAPS][SPC_MAX_KVOL];    // weight offset -> WS list / -1
     __shared__ int64_t s_pre[KM_MAX_MAPS + 1];             // tile prefix over the maps
@@ -470,6 +476,8 @@ __global__ void __launch_bounds__(KM_THREADS, SPC_KM_MIN_BLOCKS) k_kmap_zdelta(c
 // holds 32 consecutive outputs of one offset (one ballot for the counts and tile mask).
 // ------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_kmap_bsearch(const __grid_constant__ KmapDesc p, int bits_y, int bits_z) {
+    pdl_wait();   // PDL launch: the predecessor has completed and flushed
+    pdl_trigger();
     const int64_t n_out = dev_count(p.n_out_cap, p.n_out_dev);
     const int64_t n_in = dev_count(p.n_in_cap, p.n_in_dev);
     const int64_t n_pad = (n_out + 31) & ~int64_t(31);
@@ -565,6 +573,8 @@ static int ord_key_bits(int n_jobs) { (void)n_jobs; return ORD_TAG_SHIFT; }
 
 // weight field of every key (the build ORs only the direction bits in)
 __global__ void k_ord_weight(uint64_t *__restrict__ keys, const int64_t *total) {
+    pdl_wait();   // PDL launch: the predecessor has completed and flushed
+    pdl_trigger();
     const int64_t n = *total;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const uint64_t k = keys[i];
@@ -585,6 +595,8 @@ __device__ __forceinline__ int64_t ord_base(const OrderBatch &B, int job, int64_
 // (independent loads, coalesced stores); tile mask words from per-lane column masks.
 __global__ void __launch_bounds__(128) k_ord_permute(const __grid_constant__ OrderBatch B,
                                                      const int32_t *__restrict__ sorted_pos) {
+    pdl_wait();   // PDL launch: the predecessor has completed and flushed
+    pdl_trigger();
     __shared__ int32_t src_s[128];
     __shared__ uint32_t wm[4][4];
     int job = 0;
@@ -634,6 +646,8 @@ __global__ void __launch_bounds__(128) k_ord_permute(const __grid_constant__ Ord
 // runs for it), so a dynamic scheduler claiming them in this order balances like LPT.
 // Equal weights in any order (the conv's result does not depend on the tile order).
 __global__ void __launch_bounds__(1024) k_ord_tiles(const __grid_constant__ OrderBatch B) {
+    pdl_wait();   // PDL launch: the predecessor has completed and flushed
+    pdl_trigger();
     __shared__ int hist[SPC_MAX_KVOL + 2];
     const OrderJob &J = B.j[blockIdx.x >> 1];
     const int T = (blockIdx.x & 1) ? 256 : 128, f = T / 128;
@@ -697,15 +711,14 @@ static spc_status run_orders(const std::vector<OrderJob> &jobs, const OrderScrat
         B.j[q].tile0 = tiles;
         tiles += (B.j[q].n_cap + 127) / 128;
     }
-    k_ord_weight<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((rows_cap + 255) / 256, 4 * (int64_t)num_sms())), 256,
-                   0, st>>>(o.keys, o.total);
+    SPC_CUDA(launch_pdl(k_ord_weight, dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>((rows_cap + 255) / 256, 4 * (int64_t)num_sms()))), dim3(256), 0, st, o.keys, o.total));
     SPC_LAUNCH_CHECK("k_ord_weight");
     spc_status s = radix_sort(o.keys, nullptr, rows_cap, o.total, ORD_TAG_SHIFT + ord_tag_bits(B.n_jobs), o.keys_sorted,
                               o.pos, o.rws, o.rws_bytes, st, false);
     if (s != SPC_OK) return s;
-    k_ord_permute<<<(unsigned)tiles, 128, 0, st>>>(B, o.pos);
+    SPC_CUDA(launch_pdl(k_ord_permute, dim3((unsigned)tiles), dim3(128), 0, st, B, o.pos));
     SPC_LAUNCH_CHECK("k_ord_permute");
-    k_ord_tiles<<<(unsigned)(2 * B.n_jobs), 1024, 0, st>>>(B);
+    SPC_CUDA(launch_pdl(k_ord_tiles, dim3((unsigned)(2 * B.n_jobs)), dim3(1024), 0, st, B));
     SPC_LAUNCH_CHECK("k_ord_tiles");
     return SPC_OK;
 }
@@ -866,13 +879,13 @@ static void fill_desc(KmapDesc &d, const spc_kmap &km, const KmapPlan &pl, int32
 }
 
 static spc_status launch_kmaps(const KmapBatch &b, int max_k_dense, int64_t max_tiles, cudaStream_t st) {
-    k_kmap_prep<<<b.n_maps > 0 ? b.n_maps : 1, 256, 0, st>>>(b);
+    SPC_CUDA(launch_pdl(k_kmap_prep, dim3(b.n_maps > 0 ? b.n_maps : 1), dim3(256), 0, st, b));
     SPC_LAUNCH_CHECK("k_kmap_prep");
     {
         int64_t items = 0;
         for (int m = 0; m < b.n_maps; ++m) items += ((b.d[m].n_out_cap + KM_BM - 1) / KM_BM) * 2 * b.d[m].K * b.d[m].K;
         const int g = (int)std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, 16 * (int64_t)num_sms()));
-        k_kmap_bounds<<<g, 256, 0, st>>>(b);
+        SPC_CUDA(launch_pdl(k_kmap_bounds, dim3(g), dim3(256), 0, st, b));
         SPC_LAUNCH_CHECK("k_kmap_bounds");
     }
     // one CTA per (map, tile); the OS block of a tile is staged in dynamic shared memory
@@ -895,7 +908,7 @@ static spc_status launch_kmaps(const KmapBatch &b, int max_k_dense, int64_t max_
     for (int m = 0; m < b.n_maps; ++m) tiles += (b.d[m].n_out_cap + KM_BM - 1) / KM_BM;
     (void)max_tiles;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)num_sms() * std::max(1, per_sm)));
-    k_kmap_zdelta<<<(unsigned)grid, KM_THREADS, dsm, st>>>(b);
+    SPC_CUDA(launch_pdl(k_kmap_zdelta, dim3((unsigned)grid), dim3(KM_THREADS), dsm, st, b));
     SPC_LAUNCH_CHECK("k_kmap_zdelta");
     return SPC_OK;
 }
@@ -989,8 +1002,8 @@ extern "C" spc_status spc_build_kmap(const uint64_t *in_keys, int64_t n_in, cons
         return SPC_OK;
     }
     if ((flags & SPC_KMAP_CHECK_SORTED) && status) {
-        k_flag_dups<<<64, 256, 0, st>>>(in_keys, n_in, n_in_dev, status, SPC_FLAG_UNSORTED);
-        k_flag_dups<<<64, 256, 0, st>>>(out_keys, n_out, n_out_dev, status, SPC_FLAG_UNSORTED);
+        SPC_CUDA(launch_pdl(k_flag_dups, dim3(64), dim3(256), 0, st, in_keys, n_in, n_in_dev, status, SPC_FLAG_UNSORTED));
+        SPC_CUDA(launch_pdl(k_flag_dups, dim3(64), dim3(256), 0, st, out_keys, n_out, n_out_dev, status, SPC_FLAG_UNSORTED));
     }
 
     if (g_defer.active) {
@@ -1025,8 +1038,7 @@ extern "C" spc_status spc_build_kmap(const uint64_t *in_keys, int64_t n_in, cons
         km.tile_order = nullptr;
         SPC_CUDA(cudaMemsetAsync(base + L.counts, 0, L.stats + 2 * sizeof(unsigned long long) - L.counts, st));
         const int64_t items = (int64_t)pl.k_vol * ((n_out + 31) & ~int64_t(31));
-        k_kmap_bsearch<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, 32 * (int64_t)num_sms())), 256,
-                         0, st>>>(d, spec.bits_y, spec.bits_z);
+        SPC_CUDA(launch_pdl(k_kmap_bsearch, dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, 32 * (int64_t)num_sms()))), dim3(256), 0, st, d, spec.bits_y, spec.bits_z));
         SPC_LAUNCH_CHECK("k_kmap_bsearch");
         return SPC_OK;
     }

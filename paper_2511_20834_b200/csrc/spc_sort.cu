@@ -61,6 +61,8 @@ constexpr uint32_t ST_AGG = 1u << 30, ST_INC = 2u << 30, ST_VAL = (1u << 30) - 1
 __global__ void __launch_bounds__(SORT_THREADS) k_hist_all(const uint64_t *__restrict__ keys, int64_t n_cap,
                                                            const int64_t *n_dev, int passes,
                                                            unsigned int *__restrict__ ghist) {
+    pdl_wait();   // PDL launch: the predecessor has completed and flushed
+    pdl_trigger();
     __shared__ unsigned int h[MAX_PASSES][256];
     for (int i = threadIdx.x; i < passes * 256; i += SORT_THREADS) h[i / 256][i % 256] = 0;
     __syncthreads();
@@ -75,6 +77,8 @@ __global__ void __launch_bounds__(SORT_THREADS) k_hist_all(const uint64_t *__res
 }
 
 __global__ void k_hist_scan(unsigned int *__restrict__ ghist, int passes) {
+    pdl_wait();   // PDL launch: the predecessor has completed and flushed
+    pdl_trigger();
     // one warp per pass: exclusive scan of 256 counters in place
     const int p = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (p >= passes) return;
@@ -100,6 +104,8 @@ __global__ void __launch_bounds__(SORT_THREADS) k_onesweep(const uint64_t *__res
                                                            unsigned int *tile_status, unsigned int *tile_counter,
                                                            uint64_t *__restrict__ keys_out,
                                                            int32_t *__restrict__ vals_out) {
+    pdl_wait();   // PDL launch: the predecessor has completed and flushed
+    pdl_trigger();
     __shared__ int tile_s;
     __shared__ unsigned int excl_s[256];
     __shared__ int local_start[256];
@@ -208,6 +214,8 @@ __global__ void __launch_bounds__(SORT_THREADS) k_onesweep(const uint64_t *__res
 
 __global__ void k_copy_keys(const uint64_t *__restrict__ a, int64_t n_cap, const int64_t *n_dev,
                             uint64_t *__restrict__ b, const int32_t *vals_in, int32_t *vals_out) {
+    pdl_wait();   // PDL launch: the predecessor has completed and flushed
+    pdl_trigger();
     const int64_t n = dev_count(n_cap, n_dev);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         b[i] = a[i];
@@ -250,7 +258,7 @@ spc_status radix_sort(const uint64_t *keys_in, const int32_t *vals_in, int64_t n
     int32_t *vtmp = with_vals ? b.take<int32_t>((size_t)n) : nullptr;
     if (!b.ok()) return fail(SPC_ERR_WORKSPACE, "radix_sort: workspace too small");
     if (passes == 0) {
-        k_copy_keys<<<256, 256, 0, st>>>(keys_in, n, n_dev, keys_out, vals_in, vals_out);
+        SPC_CUDA(launch_pdl(k_copy_keys, dim3(256), dim3(256), 0, st, keys_in, n, n_dev, keys_out, vals_in, vals_out));
         SPC_LAUNCH_CHECK("k_copy_keys");
         return SPC_OK;
     }
@@ -258,9 +266,9 @@ spc_status radix_sort(const uint64_t *keys_in, const int32_t *vals_in, int64_t n
     if (!hist_done) {
         SPC_CUDA(cudaMemsetAsync(hist, 0, sizeof(unsigned int) * MAX_PASSES * 256, st));
         const int g = (int)std::max<int64_t>(1, std::min<int64_t>((n + 4095) / 4096, 2 * num_sms()));
-        k_hist_all<<<g, SORT_THREADS, 0, st>>>(keys_in, n, n_dev, passes, hist);
+        SPC_CUDA(launch_pdl(k_hist_all, dim3(g), dim3(SORT_THREADS), 0, st, keys_in, n, n_dev, passes, hist));
     }
-    k_hist_scan<<<1, 32 * MAX_PASSES, 0, st>>>(hist, passes);
+    SPC_CUDA(launch_pdl(k_hist_scan, dim3(1), dim3(32 * MAX_PASSES), 0, st, hist, passes));
     SPC_LAUNCH_CHECK("radix histograms");
     const uint64_t *src_k = keys_in;
     const int32_t *src_v = vals_in;
@@ -273,11 +281,11 @@ spc_status radix_sort(const uint64_t *keys_in, const int32_t *vals_in, int64_t n
 #define SPC_ONESWEEP(IT)                                                                                     \
     do {                                                                                                     \
         if (with_vals)                                                                                       \
-            k_onesweep<true, IT><<<nt, SORT_THREADS, 0, st>>>(src_k, src_v, n, n_dev, 8 * p, hist + p * 256, stp, \
-                                                              ctr, dst_k, dst_v);                            \
+            SPC_CUDA(launch_pdl(k_onesweep<true, IT>, dim3(nt), dim3(SORT_THREADS), 0, st, src_k, src_v, n, n_dev, 8 * p, hist + p * 256, stp, \
+                                                              ctr, dst_k, dst_v));                            \
         else                                                                                                 \
-            k_onesweep<false, IT><<<nt, SORT_THREADS, 0, st>>>(src_k, nullptr, n, n_dev, 8 * p, hist + p * 256,  \
-                                                               stp, ctr, dst_k, nullptr);                    \
+            SPC_CUDA(launch_pdl(k_onesweep<false, IT>, dim3(nt), dim3(SORT_THREADS), 0, st, src_k, nullptr, n, n_dev, 8 * p, hist + p * 256,  \
+                                                               stp, ctr, dst_k, nullptr));                    \
     } while (0)
         if (items == 2) SPC_ONESWEEP(2);
         else if (items == 4) SPC_ONESWEEP(4);
@@ -300,6 +308,8 @@ struct PackDev {
 __global__ void __launch_bounds__(256) k_pack(const int4 *__restrict__ coords, int64_t n, PackDev s,
                                               uint64_t *__restrict__ keys, uint32_t *status, int passes,
                                               unsigned int *__restrict__ ghist) {
+    pdl_wait();   // PDL launch: the predecessor has completed and flushed
+    pdl_trigger();
     __shared__ unsigned int h[MAX_PASSES][256];
     for (int i = threadIdx.x; i < passes * 256; i += blockDim.x) h[i / 256][i % 256] = 0;
     __syncthreads();
@@ -326,6 +336,8 @@ __global__ void __launch_bounds__(256) k_pack(const int4 *__restrict__ coords, i
 
 __global__ void k_flag_dups(const uint64_t *__restrict__ keys, int64_t n_cap, const int64_t *n_dev,
                             uint32_t *status, uint32_t flag) {
+    pdl_wait();   // PDL launch: the predecessor has completed and flushed
+    pdl_trigger();
     const int64_t n = dev_count(n_cap, n_dev);
     bool dup = false;
     for (int64_t i = 1 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -336,6 +348,8 @@ __global__ void k_flag_dups(const uint64_t *__restrict__ keys, int64_t n_cap, co
 __global__ void k_gather_rows(const char *__restrict__ src, int64_t ld_src, const int32_t *__restrict__ perm,
                               int64_t n_cap, const int64_t *n_dev, int row_bytes, char *__restrict__ dst,
                               int64_t ld_dst) {
+    pdl_wait();   // PDL launch: the predecessor has completed and flushed
+    pdl_trigger();
     const int64_t n = dev_count(n_cap, n_dev);
     const int vec = row_bytes / 16;
     const int64_t total = n * vec;
@@ -358,6 +372,8 @@ struct LevelMasks {
 __global__ void k_build_tagged(const uint64_t *__restrict__ v0, int64_t n_cap, const int64_t *n_dev, int L,
                                LevelMasks m, int used_bits, uint64_t *__restrict__ tagged,
                                int64_t *__restrict__ total_dev) {
+    pdl_wait();   // PDL launch: the predecessor has completed and flushed
+    pdl_trigger();
     const int64_t n = dev_count(n_cap, n_dev);
     if (blockIdx.x == 0 && threadIdx.x == 0) *total_dev = n * L;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * L; i += (int64_t)gridDim.x * blockDim.x) {
@@ -369,6 +385,8 @@ __global__ void k_build_tagged(const uint64_t *__restrict__ v0, int64_t n_cap, c
 
 __global__ void __launch_bounds__(SORT_THREADS) k_unique_count(const uint64_t *__restrict__ k, const int64_t *total_dev,
                                                                int *__restrict__ tile_cnt) {
+    pdl_wait();   // PDL launch: the predecessor has completed and flushed
+    pdl_trigger();
     __shared__ int ws[SORT_WARPS];
     const int64_t total = *total_dev;
     const int64_t base = (int64_t)blockIdx.x * SORT_TILE;
@@ -388,6 +406,8 @@ __global__ void __launch_bounds__(1024) k_unique_scan(int *__restrict__ tile_cnt
                                                       const uint64_t *__restrict__ k, const int64_t *total_dev,
                                                       int64_t n_cap, const int64_t *n_dev, int L,
                                                       int64_t *__restrict__ level_base, int64_t *__restrict__ level_n) {
+    pdl_wait();   // PDL launch: the predecessor has completed and flushed
+    pdl_trigger();
     __shared__ int wsum[32];
     __shared__ int carry_s;
     __shared__ int red[32];
@@ -455,6 +475,8 @@ __global__ void __launch_bounds__(SORT_THREADS) k_unique_write(const uint64_t *_
                                                                const int64_t *__restrict__ level_base,
                                                                uint64_t strip_mask, uint64_t *__restrict__ out,
                                                                int64_t out_stride) {
+    pdl_wait();   // PDL launch: the predecessor has completed and flushed
+    pdl_trigger();
     __shared__ int ws[SORT_WARPS];
     const int64_t total = *total_dev;
     const int64_t n = dev_count(n_cap, n_dev);
@@ -512,13 +534,13 @@ extern "C" spc_status spc_pack_sort(const int32_t *coords, int64_t n, spc_pack_s
     // the first region of the radix workspace)
     unsigned int *hist = reinterpret_cast<unsigned int *>(rws);   // == radix_sort's first workspace block
     SPC_CUDA(cudaMemsetAsync(hist, 0, sizeof(unsigned int) * MAX_PASSES * 256, st));
-    k_pack<<<grid, 256, 0, st>>>(reinterpret_cast<const int4 *>(coords), n, pd, raw, status, (used + 7) / 8, hist);
+    SPC_CUDA(launch_pdl(k_pack, dim3(grid), dim3(256), 0, st, reinterpret_cast<const int4 *>(coords), n, pd, raw, status, (used + 7) / 8, hist));
     SPC_LAUNCH_CHECK("k_pack");
     int32_t *perm = perm_out;
     spc_status s = radix_sort(raw, nullptr, n, nullptr, used, keys_out, perm, rws, rws_bytes, st, true);
     if (s != SPC_OK) return s;
     if (status) {
-        k_flag_dups<<<grid, 256, 0, st>>>(keys_out, n, nullptr, status, SPC_FLAG_DUPLICATE);
+        SPC_CUDA(launch_pdl(k_flag_dups, dim3(grid), dim3(256), 0, st, keys_out, n, nullptr, status, SPC_FLAG_DUPLICATE));
         SPC_LAUNCH_CHECK("k_flag_dups");
     }
     return SPC_OK;
@@ -535,8 +557,8 @@ extern "C" spc_status spc_gather_rows(const void *src, int64_t ld_src_bytes, con
                   "rows must be 16-byte aligned multiples of 16 bytes");
     int64_t work = n * (row_bytes / 16);
     int grid = (int)imin64((work + 255) / 256, 8 * 148);
-    k_gather_rows<<<grid, 256, 0, as_stream(stream)>>>((const char *)src, ld_src_bytes, perm, n, n_dev, row_bytes,
-                                                      (char *)dst, ld_dst_bytes);
+    SPC_CUDA(launch_pdl(k_gather_rows, dim3(grid), dim3(256), 0, as_stream(stream), (const char *)src, ld_src_bytes, perm, n, n_dev, row_bytes,
+                                                      (char *)dst, ld_dst_bytes));
     SPC_LAUNCH_CHECK("k_gather_rows");
     return SPC_OK;
 }
@@ -583,15 +605,15 @@ extern "C" spc_status spc_downsample(const uint64_t *keys, int64_t n, const int6
     void *rws = b.base + align_up(b.used, 256);
     size_t rws_bytes = ws_bytes - align_up(b.used, 256);
     int grid = (int)imin64((tot + 255) / 256, 8 * 148);
-    k_build_tagged<<<grid, 256, 0, st>>>(keys, n, n_dev, n_levels, lm, used, tagged, scal);
+    SPC_CUDA(launch_pdl(k_build_tagged, dim3(grid), dim3(256), 0, st, keys, n, n_dev, n_levels, lm, used, tagged, scal));
     SPC_LAUNCH_CHECK("k_build_tagged");
     const int tag_bits = n_levels > 2 ? 2 : (n_levels > 1 ? 1 : 0);
     spc_status s = radix_sort(tagged, nullptr, tot, scal, used + tag_bits, sorted, nullptr, rws, rws_bytes, st, false);
     if (s != SPC_OK) return s;
-    k_unique_count<<<nt, SORT_THREADS, 0, st>>>(sorted, scal, tile_cnt);
-    k_unique_scan<<<1, 1024, 0, st>>>(tile_cnt, nt, sorted, scal, n, n_dev, n_levels, scal + 1, level_n_dev);
+    SPC_CUDA(launch_pdl(k_unique_count, dim3(nt), dim3(SORT_THREADS), 0, st, sorted, scal, tile_cnt));
+    SPC_CUDA(launch_pdl(k_unique_scan, dim3(1), dim3(1024), 0, st, tile_cnt, nt, sorted, scal, n, n_dev, n_levels, scal + 1, level_n_dev));
     const uint64_t strip = used >= 64 ? ~0ull : ((1ull << used) - 1);
-    k_unique_write<<<nt, SORT_THREADS, 0, st>>>(sorted, scal, n, n_dev, tile_cnt, scal + 1, strip, level_keys, n);
+    SPC_CUDA(launch_pdl(k_unique_write, dim3(nt), dim3(SORT_THREADS), 0, st, sorted, scal, n, n_dev, tile_cnt, scal + 1, strip, level_keys, n));
     SPC_LAUNCH_CHECK("unique");
     return SPC_OK;
 }
