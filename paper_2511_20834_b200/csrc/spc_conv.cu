@@ -76,6 +76,7 @@ struct ConvParams {
     int split_ok;         // OS part may split a tile's offsets over CTAs (needs acc + tile_ctr)
     int force_tr;         // experiments: 128/256 forces the tile rows (0 = device heuristic)
     int split_min_unit;   // weighted split: minimum offsets per part
+    int claim_ahead;      // dynamic claims: tile ti is claimed once the gather warps began tile ti - claim_ahead
     int split_tiles_per_sm2;   // weighted split when 2 * tiles <= this (default: SM count)
     int num_sms;
     float *acc;           // fp32 split-K accumulator (all-zero on entry, left all-zero)
@@ -265,7 +266,8 @@ struct ConvSmem {
     uint64_t full[16], empty[16], tfull[2], tempty[2];
     uint64_t trec_full[TREC_SLOTS], trec_empty[TREC_SLOTS];
     uint64_t blk_full[BLK_SLOTS], blk_empty[BLK_SLOTS];
-    uint64_t tstart;               // one phase per tile the gather warps begin (claim gate)
+    uint64_t tstart;               // (unused)
+    volatile int started;          // tiles the gather warps have begun (claim gate)
     uint32_t tmem_holder[4];
     int tr, wsplit;                // device-chosen tile rows / weighted OS split active
     int n_sp;                      // tiles in the weighted split
@@ -445,7 +447,7 @@ __device__ __forceinline__ void gather_role(const ConvParams &p, ConvSmem &cs, c
         ptx::mbar_wait(ptx::smem_u32(&cs.trec_full[st]), (ti / TREC_SLOTS) & 1);
         const TileRec &R = cs.trec[st];
         if (R.end) break;
-        if (warp == 0 && lane == 0) ptx::mbar_arrive(ptx::smem_u32(&cs.tstart));
+        if (warp == 0 && lane == 0) cs.started = (int)ti + 1;
         const int rows = R.rows, ncols = R.ncols;
         const int bs = ti % p.blk_slots;
         ptx::mbar_wait(ptx::smem_u32(&cs.blk_full[bs]), (ti / p.blk_slots) & 1);
@@ -624,6 +626,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             ptx::mbar_init(ptx::smem_u32(&cs.blk_empty[i]), N_GATHER);
         }
         ptx::mbar_init(ptx::smem_u32(&cs.tstart), 1);
+        cs.started = 0;
         ptx::fence_mbar_init();
         ptx::fence_proxy_async();
     }
@@ -772,8 +775,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             int64_t v = vs;
             if (fetch && ti > 0) {
                 // first tile: blockIdx.x (no claim latency); then claims from the counter,
-                // at most one tile beyond the one the gather warps are on (claim gate)
-                ptx::mbar_wait(ptx::smem_u32(&cs.tstart), (ti - 1) & 1);
+                // at most claim_ahead tiles beyond the one the gather warps are on (claim
+                // gate: keeps the dynamic balance while the record of a light tile is ready
+                // before the gather warps finish the previous one)
+                {
+                    const int need = (int)ti + 1 - p.claim_ahead;
+                    uint32_t ns = 32;
+                    while (cs.started < need) {
+                        __nanosleep(ns);
+                        if (ns < 256) ns <<= 1;
+                    }
+                }
                 int x = 0;
                 if (lane == 0) x = atomicAdd(fetch, 1);
                 v = (int64_t)gridDim.x + __shfl_sync(0xffffffffu, x, 0);
@@ -1409,6 +1421,7 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
     p.num_sms = num_sms();
     p.force_tr = getenv("SPC_TR") ? atoi(getenv("SPC_TR")) : 0;
     p.split_min_unit = getenv("SPC_SPLIT_MIN") ? atoi(getenv("SPC_SPLIT_MIN")) : 2;
+    p.claim_ahead = getenv("SPC_CLAIM_AHEAD") ? std::max(1, std::min(3, atoi(getenv("SPC_CLAIM_AHEAD")))) : 1;
     p.split_tiles_per_sm2 = getenv("SPC_SPLIT_TILES2") ? atoi(getenv("SPC_SPLIT_TILES2")) : p.num_sms;
     // 256-row tiles (two MMAs per weight tile) whenever four accumulators fit TMEM; the
     // kernel drops to 128-row tiles on the device when the live row count is small
