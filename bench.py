@@ -364,7 +364,8 @@ def main():
     e2e = None
     if rank == 0 or world > 1:
         e2e = end_to_end(net, coords_np, feats_np, dev, stream, args.steps, flush, graph, coords, feats)
-    e2e_v = e2e["value"] * (total_scans / max(1, scans_here) if args.config == 4 else world) if e2e else None
+    # whole-job scans/s: every rank pushes its own scans through the pipeline concurrently
+    e2e_v = e2e["value"] * (total_scans if args.config == 4 else world) if e2e else None
 
     if rank == 0:
         line = {
