@@ -354,6 +354,8 @@ def main():
     layer_ms, index_ms = per_layer_times(net, coords, feats, stream, flush)
     conv_ms = float(sum(layer_ms.values()))
     total_flop = float(sum(flops.values()))
+    alg_bytes = float(sum(net.algorithmic_bytes().values()))
+    traffic = conv_traffic(args.config, n)
     achieved = total_flop / (conv_ms / 1e3) / 1e12
     peaks = measured_peaks()
     peak = peaks.get("bf16_tflops", 1590.0)
@@ -381,7 +383,13 @@ def main():
                        "cuda_graph": graph is not None, "dataflow_t": {str(k): v for k, v in net.t.items()},
                        "pack_spec": list(spec.astuple())},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak,
+                         "traffic": traffic["dram_bytes_per_step"] if traffic else None,
+                         "traffic_note": (f"bytes per step: DRAM read+write summed over the {traffic['n_launches']} "
+                                          f"feature-computation launches of one step, one ncu --set full capture "
+                                          f"({traffic['file']}; serialised, cold-cache)") if traffic else
+                                         "no ncu capture for this config",
+                         "algorithmic_bytes_per_step": alg_bytes,
                          "kernel": "feature computation (k_conv_tc OS+WS launches, 49 layers)",
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst, measured)" if "bf16_tflops" in peaks
                          else "fallback 1.59 PFLOP/s (B200_PROFILING.md)",
@@ -414,6 +422,20 @@ def load_t(path):
     import ast
     line = [ln for ln in open(path).read().splitlines() if ln.startswith("{")][-1]
     return {ast.literal_eval(k): int(v) for k, v in json.loads(line)["config"]["dataflow_t"].items()}
+
+
+def conv_traffic(config, n_voxels):
+    """Per-step DRAM bytes of the feature-computation launches from the committed ncu
+    capture (scripts/conv_traffic.py), when it was taken on this workload."""
+    p = os.path.join(ROOT, "profiles", f"r1_conv_traffic_c{config}.json")
+    try:
+        d = json.load(open(p))
+    except Exception:
+        return None
+    if d.get("n_voxels") not in (None, n_voxels):
+        return None
+    d["file"] = os.path.relpath(p, ROOT)
+    return d
 
 
 def measured_peaks():

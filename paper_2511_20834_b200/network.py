@@ -247,11 +247,31 @@ class SparseNet:
     def algorithmic_flops(self) -> dict:
         """2 * nnz * C_in * C_out per layer (valid pairs only; OS sentinel rows not credited).
         [sync] -- exports every map once."""
-        nnz = {mk: int(spc.spc_kmap_export(km).shape[0]) for mk, km in self.maps.items()}
+        nnz, self.live_n = {}, {}
+        for mk, km in self.maps.items():
+            tr = spc.spc_kmap_export(km)
+            nnz[mk] = int(tr.shape[0])
+            # live sizes: every output row and every input row appears in >= 1 triple
+            # (submanifold centre; strided / transposed K=3 s_l=2 parent offsets, SURVEY 8(c))
+            self.live_n[mk] = (int(tr[:, 2].max()) + 1 if len(tr) else 0, int(tr[:, 1].max()) + 1 if len(tr) else 0)
         out = {}
         for s in self.layers:
             out[s.name] = 2.0 * nnz[s.map_key] * s.c_in_flops * s.c_out
         self.nnz = nnz
+        return out
+
+    def algorithmic_bytes(self) -> dict:
+        """SURVEY 8(d) per layer: 2 N_in C_in + 2 N_out C_out (bf16 in/out) + 2 K^3 C_in C_out
+        (weights) + 8 N_out C_out when the layer has a WS part (fp32 accumulator read + write).
+        Call after algorithmic_flops()."""
+        out = {}
+        for s in self.layers:
+            n_in, n_out = self.live_n[s.map_key]
+            km = self.maps[s.map_key]
+            b = 2 * n_in * s.c_in + 2 * n_out * s.c_out + 2 * s.map_key[0] ** 3 * s.c_in * s.c_out
+            if km.c.n_lists > 0:
+                b += 8 * n_out * s.c_out
+            out[s.name] = float(b)
         return out
 
 

@@ -35,3 +35,6 @@ for nm, sl in (("last tfull seen", 5), ("last tile stored", 6), ("epilogue end",
     print(f"  {nm:14s} min {v.min():7.2f}  median {np.median(v):7.2f}  max {v.max():7.2f}")
 busy = rel[3] - rel[2]
 print(f"  first_full->last_commit  median {np.median(busy):.2f} max {busy.max():.2f};  setup->first_full median {np.median(rel[2]-rel[1]):.2f}")
+ex = rel[4]
+for b in np.argsort(-ex)[:6]:
+    print(f"  slow CTA {b:4d}: " + " ".join(f"{nm}={rel[i][b]:7.2f}" for i, nm in enumerate(["entry", "setup", "first_full", "last_commit", "exit"])))
