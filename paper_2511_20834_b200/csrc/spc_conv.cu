@@ -920,6 +920,70 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             __syncwarp();
         }
     } else if (warp == W_MMA) {
+#ifndef SPC_MMA_LANE0
+        // ===================== MMA issuer (whole warp, elected lane issues) ================
+        // every lane runs the loop on warp-uniform values (shuffled from lane 0), so the
+        // descriptors stay uniform and each tcgen05.mma is one predicated instruction
+        uint32_t it = 0;
+        const uint32_t tb = __shfl_sync(0xffffffffu, tmem_base, 0);
+        const uint32_t kb_a_u = __shfl_sync(0xffffffffu, kb_a, 0), a_bytes_u = __shfl_sync(0xffffffffu, a_bytes, 0);
+        const uint32_t b_bytes_u = __shfl_sync(0xffffffffu, b_bytes, 0);
+        const int S_u = __shfl_sync(0xffffffffu, S, 0), nkb_u = __shfl_sync(0xffffffffu, nkb, 0);
+        const int nht_u = __shfl_sync(0xffffffffu, nht, 0);
+        const uint32_t sa_u = __shfl_sync(0xffffffffu, ptx::smem_u32(sa), 0);
+        const uint32_t sb_u = __shfl_sync(0xffffffffu, ptx::smem_u32(sb), 0);
+        for (uint32_t ti = 0;; ++ti) {
+            const int st = ti % TREC_SLOTS;
+            ptx::mbar_wait(ptx::smem_u32(&cs.trec_full[st]), (ti / TREC_SLOTS) & 1);
+            const TileRec &R = cs.trec[st];
+            if (__shfl_sync(0xffffffffu, R.end, 0)) break;
+            const int ncols = __shfl_sync(0xffffffffu, R.ncols, 0);
+            const uint32_t a = ti % p.tbufs;
+            ptx::mbar_wait(ptx::smem_u32(&cs.tempty[a]), ((ti / p.tbufs) & 1) ^ 1);
+            ptx::tc_fence_after();
+            const uint32_t d_tmem = tb + a * NH * p.tmem_cols;
+            uint32_t acc = 0;
+            const int nsl = ncols * p.n_chunks;
+            for (int sl = 0; sl < nsl; sl += nkb_u, ++it) {
+                const int nin = min(nkb_u, nsl - sl);
+                const int s = it % S_u;
+                ptx::mbar_wait(ptx::smem_u32(&cs.full[s]), (it / S_u) & 1);
+                if (lane == 0) TR(2, it);
+#ifdef SPC_EXP_TRACE2
+                if (it == 0 && lane == 0) TL(2, gtime());
+#endif
+                if (it == 0 && lane == 0) TF(7);
+                ptx::fence_proxy_async();
+                ptx::tc_fence_after();
+                if (lane == 0) TR(4, it);
+                const uint32_t a_base = sa_u + (uint32_t)s * a_bytes_u;
+                const uint32_t b_base = sb_u + (uint32_t)s * b_bytes_u;
+                for (int kb = 0; kb < nin; ++kb) {
+#pragma unroll
+                    for (int kk = 0; kk < BK / 16; ++kk) {
+                        const uint64_t bd = ptx::umma_desc_kmajor_sw(b_base + kb * p.kb_b + kk * 32, rb);
+#pragma unroll
+                        for (int h = 0; h < NH; ++h) {
+                            if (h >= nht_u) break;
+                            const uint64_t ad =
+                                ptx::umma_desc_kmajor_sw(a_base + kb * kb_a_u + h * TC_BM * rb + kk * 32, rb);
+                            ptx::mma_f16_ss_elect(d_tmem + h * p.tmem_cols, ad, bd, p.idesc, acc);
+                        }
+                        acc = 1;
+                    }
+                }
+                if (lane == 0) TR(5, it);
+                ptx::mma_commit_elect(ptx::smem_u32(&cs.empty[s]));
+                if (lane == 0) TR(3, it);
+            }
+            ptx::mma_commit_elect(ptx::smem_u32(&cs.tfull[a]));
+#ifdef SPC_EXP_TRACE2
+            if (lane == 0) TL(3, gtime());
+#endif
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&cs.trec_empty[st]));
+        }
+#else
         // ===================== MMA issuer ===============================================
         uint32_t it = 0;
         for (uint32_t ti = 0;; ++ti) {
@@ -979,6 +1043,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             }
             __syncwarp();
         }
+#endif
     } else if (warp >= W_EPI0 && warp < W_EPI0 + 4) {
         // ===================== epilogue (warps 8-11, thread = TMEM lane = tile row) ====
         if (wsplit)
