@@ -930,6 +930,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         const uint32_t b_bytes_u = __shfl_sync(0xffffffffu, b_bytes, 0);
         const int S_u = __shfl_sync(0xffffffffu, S, 0), nkb_u = __shfl_sync(0xffffffffu, nkb, 0);
         const int nht_u = __shfl_sync(0xffffffffu, nht, 0);
+        const uint32_t idesc_u = p.idesc;
         const uint32_t sa_u = __shfl_sync(0xffffffffu, ptx::smem_u32(sa), 0);
         const uint32_t sb_u = __shfl_sync(0xffffffffu, ptx::smem_u32(sb), 0);
         for (uint32_t ti = 0;; ++ti) {
@@ -956,18 +957,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                 ptx::fence_proxy_async();
                 ptx::tc_fence_after();
                 if (lane == 0) TR(4, it);
-                const uint32_t a_base = sa_u + (uint32_t)s * a_bytes_u;
-                const uint32_t b_base = sb_u + (uint32_t)s * b_bytes_u;
+                // descriptors built once per stage; the K / row-half / slice steps add to
+                // the 14-bit start-address field (shared addresses < 256 KB: no carry out)
+                const uint64_t a_d0 = ptx::umma_desc_kmajor_sw(sa_u + (uint32_t)s * a_bytes_u, rb);
+                const uint64_t b_d0 = ptx::umma_desc_kmajor_sw(sb_u + (uint32_t)s * b_bytes_u, rb);
                 for (int kb = 0; kb < nin; ++kb) {
+                    const uint64_t a_dk = a_d0 + ((kb * kb_a_u) >> 4), b_dk = b_d0 + ((kb * p.kb_b) >> 4);
 #pragma unroll
                     for (int kk = 0; kk < BK / 16; ++kk) {
-                        const uint64_t bd = ptx::umma_desc_kmajor_sw(b_base + kb * p.kb_b + kk * 32, rb);
 #pragma unroll
                         for (int h = 0; h < NH; ++h) {
                             if (h >= nht_u) break;
-                            const uint64_t ad =
-                                ptx::umma_desc_kmajor_sw(a_base + kb * kb_a_u + h * TC_BM * rb + kk * 32, rb);
-                            ptx::mma_f16_ss_elect(d_tmem + h * p.tmem_cols, ad, bd, p.idesc, acc);
+                            ptx::mma_f16_ss_elect(d_tmem + h * p.tmem_cols, a_dk + ((h * TC_BM * rb + kk * 32) >> 4),
+                                                  b_dk + (kk * 32 >> 4), idesc_u, acc);
                         }
                         acc = 1;
                     }
