@@ -963,6 +963,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                 const uint64_t b_d0 = ptx::umma_desc_kmajor_sw(sb_u + (uint32_t)s * b_bytes_u, rb);
                 for (int kb = 0; kb < nin; ++kb) {
                     const uint64_t a_dk = a_d0 + ((kb * kb_a_u) >> 4), b_dk = b_d0 + ((kb * p.kb_b) >> 4);
+#ifdef SPC_MMA_PER_K
 #pragma unroll
                     for (int kk = 0; kk < BK / 16; ++kk) {
 #pragma unroll
@@ -973,6 +974,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                         }
                         acc = 1;
                     }
+#else
+                    // one asm block per 128-row half: the slice's BK/16 K steps
+#pragma unroll
+                    for (int h = 0; h < NH; ++h) {
+                        if (h >= nht_u) break;
+                        ptx::mma_f16_ss_chain<BK / 16>(d_tmem + h * p.tmem_cols, a_dk + ((h * TC_BM * rb) >> 4), b_dk,
+                                                       idesc_u, acc);
+                    }
+                    acc = 1;
+#endif
                 }
                 if (lane == 0) TR(5, it);
                 ptx::mma_commit_elect(ptx::smem_u32(&cs.empty[s]));

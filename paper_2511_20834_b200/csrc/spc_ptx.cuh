@@ -142,6 +142,35 @@ __device__ __forceinline__ void mma_f16_ss_elect(uint32_t d_tmem, uint64_t a_des
         "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// NK consecutive K=16 steps of one accumulator in one asm block: the elected lane issues
+// NK MMAs whose A / B descriptors advance by 32 bytes (+2 in the start-address field)
+template <int NK>
+__device__ __forceinline__ void mma_f16_ss_chain(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                                 uint32_t accumulate) {
+    static_assert(NK == 1 || NK == 2 || NK == 4, "NK");
+    if constexpr (NK == 1) {
+        mma_f16_ss_elect(d_tmem, a_desc, b_desc, idesc, accumulate);
+    } else if constexpr (NK == 2) {
+        asm volatile(
+            "{\n.reg .pred p, e, t;\n.reg .b64 a1, b1;\nsetp.ne.b32 p, %4, 0;\nsetp.eq.u32 t, 0, 0;\n"
+            "add.s64 a1, %1, 2;\nadd.s64 b1, %2, 2;\nelect.sync _|e, 0xffffffff;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, t;\n}" ::"r"(d_tmem),
+            "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+            : "memory");
+    } else {
+        asm volatile(
+            "{\n.reg .pred p, e, t;\n.reg .b64 a1, b1, a2, b2, a3, b3;\nsetp.ne.b32 p, %4, 0;\nsetp.eq.u32 t, 0, 0;\n"
+            "add.s64 a1, %1, 2;\nadd.s64 b1, %2, 2;\nadd.s64 a2, %1, 4;\nadd.s64 b2, %2, 4;\n"
+            "add.s64 a3, %1, 6;\nadd.s64 b3, %2, 6;\nelect.sync _|e, 0xffffffff;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, t;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, t;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, t;\n}" ::"r"(d_tmem),
+            "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+            : "memory");
+    }
+}
 __device__ __forceinline__ void mma_commit_elect(uint32_t bar) {
     asm volatile(
         "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
