@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define SPC_VERSION 1
+#define SPC_VERSION 2
 
 typedef enum {
     SPC_OK = 0,
@@ -60,6 +60,25 @@ const char *spc_last_error_detail(void);   /* thread-local, last failing call */
 int spc_version(void);
 size_t spc_kmap_struct_bytes(void);        /* sizeof(spc_kmap), for binding layout checks */
 
+/* Process-wide tuning options of the feature computation (performance only: every
+ * value gives the same Eq. (2) result).  Read by later spc_conv_forward calls; not
+ * thread-safe against concurrent calls.  value < 0 restores the default.
+ * Returns SPC_ERR_INVALID_ARG for an unknown option. */
+typedef enum {
+    SPC_OPT_CONV_TILE_ROWS = 0,   /* 0 = device heuristic (default); 128 / 256 force the OS/WS tile rows */
+    SPC_OPT_CONV_STAGE_KB = 1,    /* pipeline stage size cap in KB (default 72)                   */
+    SPC_OPT_CONV_OS_SPLIT = 2,    /* 1 (default): small OS launches split a tile's offsets over CTAs */
+    SPC_OPT_CONV_SPLIT_MIN = 3,   /* minimum offsets per split part (default 2)                   */
+    SPC_OPT_CONV_CLAIM_AHEAD = 4, /* dynamic tile claims ahead of the gather warps, 1..3 (default 1) */
+    SPC_OPT_CONV_DENSITY_ORDER = 5, /* 1 (default): use a map's density-ordered OS table if it has one */
+    SPC_OPT_PDL = 6,              /* 1 (default): programmatic dependent launches               */
+    SPC_OPT_KMAP_POOL_KEYS = 7,   /* test hook: shared window pool of the z-delta build in keys
+                                   * (default 4096; smaller forces the global-memory fallback)    */
+    SPC_OPT_COUNT = 8
+} spc_option;
+spc_status spc_set_option(int32_t option, int64_t value);
+int64_t spc_get_option(int32_t option);
+
 /* ================================================================================
  * A1  Packed keys (§5.3)
  *
@@ -75,12 +94,22 @@ size_t spc_kmap_struct_bytes(void);        /* sizeof(spc_kmap), for binding layo
  * ================================================================================ */
 typedef struct {
     int32_t bits_b, bits_x, bits_y, bits_z;
+    /* headroom the field widths were planned for (reading A4): every packed
+     * coordinate v must satisfy  -2^(B-1) + (out_stride-1) + reach <= v <= 2^(B-1)-1 - reach
+     * per axis (spc_pack_sort flags SPC_FLAG_RANGE otherwise), so downsampling up to
+     * stride out_stride and queries q +- delta with |delta| <= reach per axis never
+     * carry or borrow across fields.  spc_downsample refuses strides > out_stride and
+     * spc_build_kmap / spc_network_kmaps refuse maps whose reach r*tensor_stride*dilation
+     * exceeds `reach` (SPC_ERR_RANGE): no silent truncation. */
+    int32_t reach;       /* >= 0                                                       */
+    int32_t out_stride;  /* >= 1, a power of two                                       */
 } spc_pack_spec;
 
 /* Smallest field widths such that every coordinate in [lo_host, hi_host] (per axis),
  * every output of downsampling up to stride max_out_stride (rounding moves a
  * coordinate down by at most max_out_stride-1) and every query q +- delta with
- * |delta| <= max_reach stays inside its biased field (reading A4/A6).
+ * |delta| <= max_reach stays inside its biased field (reading A4/A6).  The planned
+ * max_reach / max_out_stride are recorded in the spec (reach, out_stride).
  * Returns SPC_ERR_RANGE (detail names the axis and the bits required) if the total
  * exceeds 62 bits. */
 spc_status spc_plan_pack(const int32_t lo_host[3], const int32_t hi_host[3], int32_t n_batch,
@@ -96,16 +125,20 @@ uint64_t spc_downsample_mask(spc_pack_spec spec, int32_t m);
 /* ================================================================================
  * A1+A2  spc_pack_sort -- pack int32 coordinates and sort them once
  *
- * coords   : int32 [n][4] rows (b, x, y, z), any row order.
+ * coords   : int32 [n][4] rows (b, x, y, z), any row order.  n is the capacity; n_dev
+ *            (nullable) the live row count on the device (rows [0, *n_dev) are packed and
+ *            sorted), so a whole pass stays graph-capturable for any scan size <= n.
  * keys_out : uint64 [n], ascending (stable LSD radix sort over the used key bits).
  * perm_out : int32 [n] (nullable): keys_out[p] = key(coords[perm_out[p]]).  The caller
  *            gathers feature rows with it (spc_gather_rows).
- * status   : device uint32, OR-ed with SPC_FLAG_RANGE (a coordinate does not fit; its
- *            key is undefined) and SPC_FLAG_DUPLICATE (two rows with equal coordinates).
+ * status   : device uint32, OR-ed with SPC_FLAG_RANGE (a coordinate does not fit its
+ *            field with the planned headroom spec.reach / spec.out_stride; its key is
+ *            undefined if it does not fit the field at all) and SPC_FLAG_DUPLICATE (two
+ *            rows with equal coordinates).
  * ws       : >= spc_pack_sort_workspace_size(n) bytes.
  * ================================================================================ */
 size_t spc_pack_sort_workspace_size(int64_t n);
-spc_status spc_pack_sort(const int32_t *coords, int64_t n, spc_pack_spec spec, uint64_t *keys_out,
+spc_status spc_pack_sort(const int32_t *coords, int64_t n, const int64_t *n_dev, spc_pack_spec spec, uint64_t *keys_out,
                          int32_t *perm_out, uint32_t *status, void *ws, size_t ws_bytes, void *stream);
 
 /* dst row r = src row perm[r] (row_bytes each, 16-byte aligned rows).  n_dev nullable. */
@@ -231,7 +264,9 @@ size_t spc_kmap_bytes(spc_geom geom, int32_t t, uint32_t flags, int64_t n_in, in
  * in_keys/out_keys: sorted unique keys of the input/output coordinate sets (the same
  * array for a submanifold layer).  buf: >= spc_kmap_bytes() bytes, 256-byte aligned.
  * status: device uint32 (nullable) for SPC_FLAG_UNSORTED / SPC_FLAG_CAPACITY.
- * kmap_out_host: filled with pointers into buf. */
+ * kmap_out_host: filled with pointers into buf.
+ * Returns SPC_ERR_RANGE if the map's reach r*tensor_stride*dilation exceeds spec.reach
+ * or its coarse stride tensor_stride*stride exceeds spec.out_stride (reading A4). */
 spc_status spc_build_kmap(const uint64_t *in_keys, int64_t n_in, const int64_t *n_in_dev,
                           const uint64_t *out_keys, int64_t n_out, const int64_t *n_out_dev,
                           spc_pack_spec spec, spc_geom geom, int32_t t, uint32_t flags, void *buf,

@@ -28,6 +28,9 @@ SPC_KMAP_DENSITY_ORDER = 0x8
 SPC_KMAP_SIMPLE_BSEARCH = 0x10
 SPC_FLAG_RANGE, SPC_FLAG_DUPLICATE, SPC_FLAG_UNSORTED, SPC_FLAG_CAPACITY = 1, 2, 4, 8
 SPC_MAX_KVOL = 125
+# spc_option
+SPC_OPT_CONV_TILE_ROWS, SPC_OPT_CONV_STAGE_KB, SPC_OPT_CONV_OS_SPLIT, SPC_OPT_CONV_SPLIT_MIN = 0, 1, 2, 3
+SPC_OPT_CONV_CLAIM_AHEAD, SPC_OPT_CONV_DENSITY_ORDER, SPC_OPT_PDL, SPC_OPT_KMAP_POOL_KEYS = 4, 5, 6, 7
 
 _DT = {torch.float32: SPC_F32, torch.float16: SPC_F16, torch.bfloat16: SPC_BF16}
 _TORCH_DT = {v: k for k, v in _DT.items()}
@@ -38,17 +41,23 @@ class SpcError(RuntimeError):
 
 
 class PackSpec(ctypes.Structure):
+    """spc_pack_spec: field widths (z least significant) and the headroom they were
+    planned for (``reach`` per axis, ``out_stride``; reading A4)."""
     _fields_ = [("bits_b", ctypes.c_int32), ("bits_x", ctypes.c_int32), ("bits_y", ctypes.c_int32),
-                ("bits_z", ctypes.c_int32)]
+                ("bits_z", ctypes.c_int32), ("reach", ctypes.c_int32), ("out_stride", ctypes.c_int32)]
+
+    def __init__(self, bits_b=0, bits_x=0, bits_y=0, bits_z=0, reach=0, out_stride=1):
+        super().__init__(bits_b, bits_x, bits_y, bits_z, reach, out_stride)
 
     def used_bits(self) -> int:
         return self.bits_b + self.bits_x + self.bits_y + self.bits_z
 
     def astuple(self):
+        """(bits_b, bits_x, bits_y, bits_z)"""
         return (self.bits_b, self.bits_x, self.bits_y, self.bits_z)
 
     def __repr__(self):
-        return f"PackSpec{self.astuple()}"
+        return f"PackSpec{self.astuple()}(reach={self.reach}, out_stride={self.out_stride})"
 
 
 class Geom(ctypes.Structure):
@@ -95,11 +104,13 @@ def lib():
             "spc_last_error_detail": ([], ctypes.c_char_p),
             "spc_version": ([], ctypes.c_int),
             "spc_kmap_struct_bytes": ([], SZ),
+            "spc_set_option": ([I32, I64], ctypes.c_int),
+            "spc_get_option": ([I32], I64),
             "spc_plan_pack": ([P, P, I32, I32, I32, ctypes.POINTER(PackSpec)], ctypes.c_int),
             "spc_pack_offset": ([PackSpec, I32, I32, I32], I64),
             "spc_downsample_mask": ([PackSpec, I32], ctypes.c_uint64),
             "spc_pack_sort_workspace_size": ([I64], SZ),
-            "spc_pack_sort": ([P, I64, PackSpec, P, P, P, P, SZ, P], ctypes.c_int),
+            "spc_pack_sort": ([P, I64, P, PackSpec, P, P, P, P, SZ, P], ctypes.c_int),
             "spc_gather_rows": ([P, I64, P, I64, P, I32, P, I64, P], ctypes.c_int),
             "spc_downsample_workspace_size": ([I64, I32], SZ),
             "spc_downsample": ([P, I64, P, PackSpec, I32, P, P, P, P, SZ, P], ctypes.c_int),
@@ -138,9 +149,40 @@ def _stream(stream=None):
     return ctypes.c_void_p(s.cuda_stream)
 
 
-def _ws(nbytes: int, device, zero: bool = False) -> torch.Tensor:
+def _tstream(stream, device):
+    """The torch stream the library call will be enqueued on."""
+    return stream if stream is not None else torch.cuda.current_stream(device)
+
+
+def _alloc(shape, dtype, device, stream, zero: bool = False) -> torch.Tensor:
+    """A temporary the library fills on ``stream``: allocated (and zero-filled) ON that
+    stream, so the caching allocator orders its reuse and the fill before the kernels that
+    use it, whichever stream is current.  Callers that drop it before the
+    stream has consumed it call ``_release(t, stream)``."""
+    st = _tstream(stream, device)
+    with torch.cuda.stream(st):
+        return torch.zeros(shape, dtype=dtype, device=device) if zero else torch.empty(shape, dtype=dtype,
+                                                                                       device=device)
+
+
+def _release(t, stream):
+    """Mark a temporary as in use on ``stream`` until the work enqueued so far completes."""
+    if t is not None and t.is_cuda:
+        t.record_stream(_tstream(stream, t.device))
+
+
+def _ws(nbytes: int, device, zero: bool = False, stream=None) -> torch.Tensor:
     n = max(int(nbytes), 256)
-    return torch.zeros(n, dtype=torch.uint8, device=device) if zero else torch.empty(n, dtype=torch.uint8, device=device)
+    return _alloc((n,), torch.uint8, device, stream, zero)
+
+
+def spc_set_option(option: int, value: int):
+    """Process-wide performance option (spc.h spc_option); value < 0 restores the default."""
+    _check(lib().spc_set_option(int(option), int(value)), "spc_set_option")
+
+
+def spc_get_option(option: int) -> int:
+    return int(lib().spc_get_option(int(option)))
 
 
 # ---------------------------------------------------------------------------------------
@@ -165,21 +207,25 @@ def spc_downsample_mask(spec: PackSpec, m: int) -> int:
 
 
 def spc_pack_sort(coords: torch.Tensor, spec: PackSpec, status: torch.Tensor | None = None, stream=None,
-                  keys_out=None, perm_out=None, ws=None):
-    """coords int32 [n,4] (b,x,y,z) on the GPU -> (keys uint64-as-int64 [n], perm int32 [n], status uint32[1])."""
+                  keys_out=None, perm_out=None, ws=None, n_dev=None):
+    """coords int32 [n,4] (b,x,y,z) on the GPU -> (keys uint64-as-int64 [n], perm int32 [n], status uint32[1]).
+    ``n_dev``: optional device int64 live row count (<= n); rows beyond it are ignored."""
     assert coords.is_cuda and coords.dtype == torch.int32 and coords.is_contiguous() and coords.shape[-1] == 4
     n = coords.shape[0]
     dev = coords.device
-    keys = keys_out if keys_out is not None else torch.empty(n, dtype=torch.int64, device=dev)
-    perm = perm_out if perm_out is not None else torch.empty(n, dtype=torch.int32, device=dev)
+    keys = keys_out if keys_out is not None else _alloc(n, torch.int64, dev, stream)
+    perm = perm_out if perm_out is not None else _alloc(n, torch.int32, dev, stream)
     if status is None:
-        status = torch.zeros(1, dtype=torch.int32, device=dev)
+        status = _alloc(1, torch.int32, dev, stream, zero=True)
     L = lib()
     wsb = int(L.spc_pack_sort_workspace_size(n))
-    if ws is None or ws.numel() < wsb:
-        ws = _ws(wsb, dev)
-    _check(L.spc_pack_sort(_ptr(coords), n, spec, _ptr(keys), _ptr(perm), _ptr(status), _ptr(ws), ws.numel(),
+    own_ws = ws is None or ws.numel() < wsb
+    if own_ws:
+        ws = _ws(wsb, dev, stream=stream)
+    _check(L.spc_pack_sort(_ptr(coords), n, _ptr(n_dev), spec, _ptr(keys), _ptr(perm), _ptr(status), _ptr(ws), ws.numel(),
                            _stream(stream)), "spc_pack_sort")
+    if own_ws:
+        _release(ws, stream)
     return keys, perm, status
 
 
@@ -188,7 +234,7 @@ def spc_gather_rows(src: torch.Tensor, perm: torch.Tensor, out: torch.Tensor | N
     """out[r] = src[perm[r]] (rows of a 2-D tensor; row bytes multiple of 16)."""
     n = perm.shape[0]
     if out is None:
-        out = torch.empty((n,) + tuple(src.shape[1:]), dtype=src.dtype, device=src.device)
+        out = _alloc((n,) + tuple(src.shape[1:]), src.dtype, src.device, stream)
     row_bytes = src[0].numel() * src.element_size() if src.shape[0] else out[0].numel() * out.element_size()
     _check(lib().spc_gather_rows(_ptr(src), src.stride(0) * src.element_size(), _ptr(perm), n, _ptr(n_dev),
                                  row_bytes, _ptr(out), out.stride(0) * out.element_size(), _stream(stream)),
@@ -205,13 +251,14 @@ def spc_downsample(keys: torch.Tensor, spec: PackSpec, log2_strides, n_dev=None,
     n = keys.shape[0]
     L_ = len(log2_strides)
     dev = keys.device
-    out = torch.empty((L_, n), dtype=torch.int64, device=dev)
-    level_n = torch.empty(L_, dtype=torch.int64, device=dev)
+    out = _alloc((L_, n), torch.int64, dev, stream)
+    level_n = _alloc(L_, torch.int64, dev, stream)
     m = (ctypes.c_int32 * L_)(*[int(v) for v in log2_strides])
     L = lib()
-    ws = _ws(L.spc_downsample_workspace_size(n, L_), dev)
+    ws = _ws(L.spc_downsample_workspace_size(n, L_), dev, stream=stream)
     _check(L.spc_downsample(_ptr(keys), n, _ptr(n_dev), spec, L_, m, _ptr(out), _ptr(level_n), _ptr(ws), ws.numel(),
                             _stream(stream)), "spc_downsample")
+    _release(ws, stream)
     return out, level_n
 
 
@@ -302,7 +349,7 @@ def spc_build_kmap(in_keys: torch.Tensor, out_keys: torch.Tensor, spec: PackSpec
     nbytes = spc_kmap_bytes(geom, t, flags, n_in, n_out)
     if nbytes == 0:
         raise SpcError(f"spc_kmap_bytes: unsupported geometry {geom!r}")
-    buf = torch.empty(nbytes + 256, dtype=torch.uint8, device=in_keys.device)
+    buf = _alloc(nbytes + 256, torch.uint8, in_keys.device, stream)
     off = (-buf.data_ptr()) % 256
     buf = buf[off:off + nbytes]
     km = _Kmap()
@@ -332,7 +379,7 @@ def spc_prepare_weight(weight: torch.Tensor, stream=None) -> torch.Tensor:
     kv, ci, co = weight.shape
     w = weight.contiguous()
     dt = _DT[w.dtype]
-    out = torch.empty(w.numel(), dtype=w.dtype, device=w.device)
+    out = _alloc(w.numel(), w.dtype, w.device, stream)
     _check(lib().spc_prepare_weight(_ptr(w), kv, ci, co, dt, _ptr(out), _stream(stream)), "spc_prepare_weight")
     return out
 
@@ -349,16 +396,19 @@ def spc_conv_forward(km: KernelMap, f_in: torch.Tensor, weight_prepared: torch.T
     (torch.zeros); every call leaves it all-zero again."""
     out_dtype = out_dtype or (out.dtype if out is not None else f_in.dtype)
     if out is None:
-        out = torch.empty((km.n_out, c_out), dtype=out_dtype, device=f_in.device)
+        out = _alloc((km.n_out, c_out), out_dtype, f_in.device, stream)
     need = spc_conv_workspace_size(km, c_out, out_dtype)
-    if ws is None:
-        ws = _ws(need, f_in.device, zero=True)   # must be all-zero on first use (spc.h)
+    own_ws = ws is None
+    if own_ws:
+        ws = _ws(need, f_in.device, zero=True, stream=stream)   # all-zero on first use (spc.h), filled on `stream`
     elif ws.numel() < need:
         raise ValueError(f"spc_conv_forward: ws has {ws.numel()} bytes, needs {need}")
     _check(lib().spc_conv_forward(ctypes.byref(km.c), _ptr(f_in), f_in.stride(0), _DT[f_in.dtype], int(c_in),
                                   _ptr(weight_prepared), int(c_out), _ptr(out), out.stride(0), _DT[out.dtype],
                                   _ptr(residual), residual.stride(0) if residual is not None else 0, _ptr(ws),
                                   ws.numel(), _stream(stream)), "spc_conv_forward")
+    if own_ws:
+        _release(ws, stream)
     return out
 
 

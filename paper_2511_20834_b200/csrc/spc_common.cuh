@@ -65,8 +65,10 @@ struct Sizer {
     }
 };
 
-int num_sms();
-bool pdl_enabled();   // programmatic dependent launch (off with SPC_NO_PDL=1)
+int num_sms();           // SM count of the current device (cached per device)
+int current_device();
+bool pdl_enabled();      // programmatic dependent launch (spc_set_option(SPC_OPT_PDL, 0) turns it off)
+int64_t option(int o);   // spc_set_option value
 
 // Launch with programmatic stream serialisation (PDL): the kernel may start while the
 // previous kernel in the stream drains.  Every kernel launched this way executes

@@ -40,7 +40,6 @@ constexpr int SPLIT_MAX_TILES = 512;              // weighted split: tiles per l
 enum OutKind : int { OUT_FINAL = 0, OUT_F32_STORE = 1, OUT_F32_RED = 2 };
 
 struct ConvParams {
-    CUtensorMap tmap_a;   // f_in rows: 2-D {c_in, n_in}, box {BK, 1}, swizzle rb = 2*BK bytes
     int mode;   // 0 = OS part, 1 = WS part
     // map
     const int32_t *os;
@@ -266,8 +265,7 @@ struct ConvSmem {
     uint64_t full[16], empty[16], tfull[2], tempty[2];
     uint64_t trec_full[TREC_SLOTS], trec_empty[TREC_SLOTS];
     uint64_t blk_full[BLK_SLOTS], blk_empty[BLK_SLOTS];
-    uint64_t tstart;               // (unused)
-    volatile int started;          // tiles the gather warps have begun (claim gate)
+    int started;                   // tiles the gather warps have begun (claim gate; ld/st.volatile.shared)
     uint32_t tmem_holder[4];
     int tr, wsplit;                // device-chosen tile rows / weighted OS split active
     int n_sp;                      // tiles in the weighted split
@@ -278,39 +276,6 @@ struct ConvSmem {
     int list_prefix[SPC_MAX_KVOL + 1];
     TileRec trec[TREC_SLOTS];
 };
-
-#ifdef SPC_EXP_TRACE3
-#define SPC_EXP_TRACE2
-#endif
-#ifdef SPC_EXP_TRACE2
-// per-CTA timeline (globaltimer ns): 0 entry, 1 after setup sync, 2 first stage full (MMA),
-// 3 last commit, 4 exit, 5 tiles done, 6 stages done
-__device__ unsigned long long g_tl[8][1024];
-__device__ __forceinline__ unsigned long long gtime() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-#ifdef SPC_EXP_TRACE3
-// first-tile events instead: 0 entry, 1 setup, 2 sched decoded, 3 sched record done,
-// 4 gather saw index block, 5 gather issued stage 0, 6 weights issued stage 0, 7 MMA full
-#define TL(slot, v) do {} while (0)
-#define TF(slot) do { if (blockIdx.x < 1024) g_tl[slot][blockIdx.x] = gtime(); } while (0)
-#else
-#define TL(slot, v) do { if (blockIdx.x < 1024) g_tl[slot][blockIdx.x] = (v); } while (0)
-#endif
-#else
-#define TL(slot, v) do {} while (0)
-#endif
-#ifndef TF
-#define TF(slot) do {} while (0)
-#endif
-#ifdef SPC_EXP_TRACE
-__device__ long long g_tr[8][4096];
-#define TR(slot, i) do { if (blockIdx.x == 0 && (i) < 4096) g_tr[slot][(i)] = clock64(); } while (0)
-#else
-#define TR(slot, i) do {} while (0)
-#endif
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
@@ -447,11 +412,10 @@ __device__ __forceinline__ void gather_role(const ConvParams &p, ConvSmem &cs, c
         ptx::mbar_wait(ptx::smem_u32(&cs.trec_full[st]), (ti / TREC_SLOTS) & 1);
         const TileRec &R = cs.trec[st];
         if (R.end) break;
-        if (warp == 0 && lane == 0) cs.started = (int)ti + 1;
+        if (warp == 0 && lane == 0) ptx::sts_volatile_s32(ptx::smem_u32(&cs.started), (int)ti + 1);
         const int rows = R.rows, ncols = R.ncols;
         const int bs = ti % p.blk_slots;
         ptx::mbar_wait(ptx::smem_u32(&cs.blk_full[bs]), (ti / p.blk_slots) & 1);
-        if (ti == 0 && warp == 0 && lane == 0) TF(4);
         const int32_t *B = blk + bs * blk_stride;
         const int nsl = ncols * p.n_chunks;
         for (int sl = 0; sl < nsl; sl += nkb) {
@@ -460,7 +424,6 @@ __device__ __forceinline__ void gather_role(const ConvParams &p, ConvSmem &cs, c
             gather_slices<BK, NBT>(p, R, ptx::smem_u32(B), kd, rows, sl, nin, ptx::smem_u32(sa + (size_t)s * a_bytes), kb_a,
                                    warp, r_in, q_lane);
             ptx::cp_async_mbar_arrive(ptx::smem_u32(&cs.full[s]));
-            if (ti == 0 && sl == 0 && warp == 0 && lane == 0) TF(5);
             if (++s == S) { s = 0; ph ^= 1; }
         }
         __syncwarp();
@@ -487,10 +450,6 @@ __device__ __forceinline__ void epi_role(const ConvParams &p, ConvSmem &cs, uint
         const uint32_t a = ti % p.tbufs;
         const int nt = R.nt;
         ptx::mbar_wait_sleep(ptx::smem_u32(&cs.tfull[a]), (ti / p.tbufs) & 1);
-        if (threadIdx.x == 32 * W_EPI0) TR(6, ti);
-#ifdef SPC_EXP_TRACE2
-        if (threadIdx.x == 32 * W_EPI0) TL(5, gtime());
-#endif
         ptx::tc_fence_after();
         const bool fix = FIX && R.nsplit > 1;
         if (fix) {
@@ -528,18 +487,11 @@ __device__ __forceinline__ void epi_role(const ConvParams &p, ConvSmem &cs, uint
         }
         ptx::tc_fence_before();
         __syncwarp();
-        if (threadIdx.x == 32 * W_EPI0) TR(7, ti);
-#ifdef SPC_EXP_TRACE2
-        if (threadIdx.x == 32 * W_EPI0) TL(6, gtime());
-#endif
         if (lane == 0) {
             if (!fix) ptx::mbar_arrive(ptx::smem_u32(&cs.tempty[a]));   // (the fixup released it already)
             ptx::mbar_arrive(ptx::smem_u32(&cs.trec_empty[st]));
         }
     }
-#ifdef SPC_EXP_TRACE2
-    if (threadIdx.x == 32 * W_EPI0) TL(7, gtime());
-#endif
 }
 
 // fp32 accumulator rows -> output dtype (+ residual), 8 columns per work item; the
@@ -603,10 +555,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     const int blk_stride = (BM * kd + 3) & ~3;      // int32 per block (16-byte multiple)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#ifdef SPC_EXP_TRACE2
-    if (threadIdx.x == 0) TL(0, gtime());
-#endif
-    if (threadIdx.x == 0) TF(0);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < 16; ++s) {
@@ -625,7 +573,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             ptx::mbar_init(ptx::smem_u32(&cs.blk_full[i]), 32);
             ptx::mbar_init(ptx::smem_u32(&cs.blk_empty[i]), N_GATHER);
         }
-        ptx::mbar_init(ptx::smem_u32(&cs.tstart), 1);
         cs.started = 0;
         ptx::fence_mbar_init();
         ptx::fence_proxy_async();
@@ -696,18 +643,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = cs.tmem_holder[0];
-#ifdef SPC_EXP_TRACE2
-    if (threadIdx.x == 0) TL(1, gtime());
-#endif
-    if (threadIdx.x == 0) TF(1);
     constexpr uint32_t rb = BK * 2;           // bytes per operand row (= swizzle span)
     const int tr = cs.tr, wsplit = cs.wsplit, nht = tr / TC_BM;
     // the ring carve of this tile height
-#ifdef SPC_EXP_RG0
-    const int rgi = 0;
-#else
     const int rgi = (BM == 256 && tr == 128) ? 1 : 0;
-#endif
     const int S = p.ring[rgi].stages, nkb = p.ring[rgi].nkb;
     const uint32_t kb_a = p.ring[rgi].kb_a, a_bytes = p.ring[rgi].a_bytes, b_bytes = p.ring[rgi].b_bytes;
     uint8_t *sa = smem;
@@ -781,7 +720,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                 {
                     const int need = (int)ti + 1 - p.claim_ahead;
                     uint32_t ns = 32;
-                    while (cs.started < need) {
+                    while (ptx::lds_volatile_s32(ptx::smem_u32(&cs.started)) < need) {
                         __nanosleep(ns);
                         if (ns < 256) ns <<= 1;
                     }
@@ -798,7 +737,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             }
             TileInfo t;
             decode_tile(p, v, cs.list_prefix, n_out, tr, wsplit ? cs.sp_pre : nullptr, cs.sp_cnt, cs.n_sp, t);
-            if (ti == 0 && lane == 0) TF(2);
             // the tile's gather indices first (they depend only on its rows): the block's
             // load overlaps the record's mask / column / scatter work below
             const int bs = ti % p.blk_slots;
@@ -878,7 +816,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                     if (q * 32 < tr) R.scatter[q * 32 + lane] = sc[q];
             }
             ptx::mbar_arrive(ptx::smem_u32(&cs.trec_full[st]));
-            if (ti == 0 && lane == 0) TF(3);
         }
         ptx::cp_async_wait<0>();
     } else if (warp < N_GATHER) {
@@ -913,14 +850,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                         ptx::bulk_g2s(ptx::smem_u32(sb + (size_t)s * b_bytes + kb * p.kb_b), p.wblob + blob * p.kb_b,
                                       p.kb_b, fb);
                     }
-                    if (it == 0) TF(6);
                 }
                 ptx::mbar_arrive(ptx::smem_u32(&cs.trec_empty[st]));
             }
             __syncwarp();
         }
     } else if (warp == W_MMA) {
-#ifndef SPC_MMA_LANE0
         // ===================== MMA issuer (whole warp, elected lane issues) ================
         // every lane runs the loop on warp-uniform values (shuffled from lane 0), so the
         // descriptors stay uniform and each tcgen05.mma is one predicated instruction
@@ -949,32 +884,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                 const int nin = min(nkb_u, nsl - sl);
                 const int s = it % S_u;
                 ptx::mbar_wait(ptx::smem_u32(&cs.full[s]), (it / S_u) & 1);
-                if (lane == 0) TR(2, it);
-#ifdef SPC_EXP_TRACE2
-                if (it == 0 && lane == 0) TL(2, gtime());
-#endif
-                if (it == 0 && lane == 0) TF(7);
                 ptx::fence_proxy_async();
                 ptx::tc_fence_after();
-                if (lane == 0) TR(4, it);
                 // descriptors built once per stage; the K / row-half / slice steps add to
                 // the 14-bit start-address field (shared addresses < 256 KB: no carry out)
                 const uint64_t a_d0 = ptx::umma_desc_kmajor_sw(sa_u + (uint32_t)s * a_bytes_u, rb);
                 const uint64_t b_d0 = ptx::umma_desc_kmajor_sw(sb_u + (uint32_t)s * b_bytes_u, rb);
                 for (int kb = 0; kb < nin; ++kb) {
                     const uint64_t a_dk = a_d0 + ((kb * kb_a_u) >> 4), b_dk = b_d0 + ((kb * p.kb_b) >> 4);
-#ifdef SPC_MMA_PER_K
-#pragma unroll
-                    for (int kk = 0; kk < BK / 16; ++kk) {
-#pragma unroll
-                        for (int h = 0; h < NH; ++h) {
-                            if (h >= nht_u) break;
-                            ptx::mma_f16_ss_elect(d_tmem + h * p.tmem_cols, a_dk + ((h * TC_BM * rb + kk * 32) >> 4),
-                                                  b_dk + (kk * 32 >> 4), idesc_u, acc);
-                        }
-                        acc = 1;
-                    }
-#else
                     // one asm block per 128-row half: the slice's BK/16 K steps
 #pragma unroll
                     for (int h = 0; h < NH; ++h) {
@@ -983,80 +900,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                                                        idesc_u, acc);
                     }
                     acc = 1;
-#endif
                 }
-                if (lane == 0) TR(5, it);
                 ptx::mma_commit_elect(ptx::smem_u32(&cs.empty[s]));
-                if (lane == 0) TR(3, it);
             }
             ptx::mma_commit_elect(ptx::smem_u32(&cs.tfull[a]));
-#ifdef SPC_EXP_TRACE2
-            if (lane == 0) TL(3, gtime());
-#endif
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&cs.trec_empty[st]));
         }
-#else
-        // ===================== MMA issuer ===============================================
-        uint32_t it = 0;
-        for (uint32_t ti = 0;; ++ti) {
-            const int st = ti % TREC_SLOTS;
-            ptx::mbar_wait(ptx::smem_u32(&cs.trec_full[st]), (ti / TREC_SLOTS) & 1);
-            const TileRec &R = cs.trec[st];
-            if (R.end) break;
-            if (lane == 0) {
-                const int ncols = R.ncols;
-                const uint32_t a = ti % p.tbufs;
-                ptx::mbar_wait(ptx::smem_u32(&cs.tempty[a]), ((ti / p.tbufs) & 1) ^ 1);
-                ptx::tc_fence_after();
-                const uint32_t d_tmem = tmem_base + a * NH * p.tmem_cols;
-                uint32_t acc = 0;
-                const int nsl = ncols * p.n_chunks;
-                for (int sl = 0; sl < nsl; sl += nkb, ++it) {
-                    const int nin = min(nkb, nsl - sl);
-                    const int s = it % S;
-                    ptx::mbar_wait(ptx::smem_u32(&cs.full[s]), (it / S) & 1);
-                    TR(2, it);
-#ifdef SPC_EXP_TRACE2
-                    if (it == 0) TL(2, gtime());
-#endif
-                    if (it == 0) TF(7);
-                    // the A tile was written by cp.async / st.shared (generic proxy): order it
-                    // before the tensor core's async-proxy reads
-                    ptx::fence_proxy_async();
-                    ptx::tc_fence_after();
-                    TR(4, it);
-                    const uint32_t a_base = ptx::smem_u32(sa + (size_t)s * a_bytes);
-                    const uint32_t b_base = ptx::smem_u32(sb + (size_t)s * b_bytes);
-                    for (int kb = 0; kb < nin; ++kb) {
-#pragma unroll
-                        for (int kk = 0; kk < BK / 16; ++kk) {
-                            const uint64_t bd = ptx::umma_desc_kmajor_sw(b_base + kb * p.kb_b + kk * 32, rb);
-#pragma unroll
-                            for (int h = 0; h < NH; ++h) {
-#ifndef SPC_EXP_NOBRK
-                                if (h >= nht) break;
-#endif
-                                const uint64_t ad =
-                                    ptx::umma_desc_kmajor_sw(a_base + kb * kb_a + h * TC_BM * rb + kk * 32, rb);
-                                ptx::mma_f16_ss(d_tmem + h * p.tmem_cols, ad, bd, p.idesc, acc);
-                            }
-                            acc = 1;
-                        }
-                    }
-                    TR(5, it);
-                    ptx::mma_commit(ptx::smem_u32(&cs.empty[s]));
-                    TR(3, it);
-                }
-                ptx::mma_commit(ptx::smem_u32(&cs.tfull[a]));
-#ifdef SPC_EXP_TRACE2
-                TL(3, gtime());
-#endif
-                ptx::mbar_arrive(ptx::smem_u32(&cs.trec_empty[st]));
-            }
-            __syncwarp();
-        }
-#endif
     } else if (warp >= W_EPI0 && warp < W_EPI0 + 4) {
         // ===================== epilogue (warps 8-11, thread = TMEM lane = tile row) ====
         if (wsplit)
@@ -1070,9 +920,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem_base, p.tbufs * NH * p.tmem_cols);
     }
-#ifdef SPC_EXP_TRACE2
-    if (threadIdx.x == 0) TL(4, gtime());
-#endif
     if (p.tile_ctr && threadIdx.x == 0) {
         // the last CTA out returns the fetch / exit counters to zero (ws contract); every
         // CTA's scheduler has made its final claim before its CTA gets here
@@ -1307,7 +1154,7 @@ extern "C" size_t spc_conv_workspace_size(const spc_kmap *km, int32_t c_out, int
 
 static void fill_map_params(ConvParams &p, const spc_kmap *km) {
     // density-ordered OS part when the map has one (SPC_KMAP_DENSITY_ORDER)
-    const bool ord = km->os_rows && km->os_table_ord && km->tile_mask_ord && !getenv("SPC_NO_DENSITY_ORDER");
+    const bool ord = km->os_rows && km->os_table_ord && km->tile_mask_ord && option(SPC_OPT_CONV_DENSITY_ORDER) != 0;
     p.os = ord ? km->os_table_ord : km->os_table;
     p.os_rows = ord ? km->os_rows : nullptr;
     p.k_dense = km->k_dense;
@@ -1329,36 +1176,6 @@ static void fill_map_params(ConvParams &p, const spc_kmap *km) {
     }
 }
 
-static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    if (!fn) {
-        cudaDriverEntryPointQueryResult q;
-        void *p = nullptr;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    }
-    return fn;
-}
-
-[[maybe_unused]] static spc_status encode_rows_tmap(CUtensorMap *tm, const void *base, int64_t n_rows, int c_in, int64_t ld_bytes,
-                                   int BK, int dtype) {
-    auto enc = tmap_encoder();
-    if (!enc) return fail(SPC_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
-    const int rb = BK * 2;
-    const CUtensorMapSwizzle sw = rb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
-                                            : (rb == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
-    cuuint64_t gdim[2] = {(cuuint64_t)c_in, (cuuint64_t)(n_rows > 0 ? n_rows : 1)};
-    cuuint64_t gstride[1] = {(cuuint64_t)ld_bytes};
-    cuuint32_t box[2] = {(cuuint32_t)BK, 1u};
-    cuuint32_t estr[2] = {1, 1};
-    CUresult r = enc(tm, dtype == SPC_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
-                     const_cast<void *>(base), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return fail(SPC_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
-    return SPC_OK;
-}
-
 static spc_status launch_tc(const ConvParams &p0, int mode, int out_kind, void *out, int64_t ld_out, cudaStream_t st) {
     ConvParams p = p0;
     p.mode = mode;
@@ -1372,14 +1189,13 @@ static spc_status launch_tc(const ConvParams &p0, int mode, int out_kind, void *
     const size_t avail = TC_SMEM_BUDGET - 1024 - header;   // 1024: alignment slack of the dynamic smem base
     // slices (one BK-channel chunk of one offset) per pipeline stage: a stage carries up
     // to ~72 KB so narrow layers pack several offsets into one stage
-    static const size_t stage_cap = getenv("SPC_STAGE_KB") ? (size_t)atoi(getenv("SPC_STAGE_KB")) * 1024 : 72 * 1024;
+    const size_t stage_cap = (size_t)std::max<int64_t>(8, option(SPC_OPT_CONV_STAGE_KB)) * 1024;
     size_t ring_bytes = 0;
     for (int g = 0; g < 2; ++g) {
         const int rows = g == 0 ? p.bm : TC_BM;
         ConvParams::Ring &R = p.ring[g];
         R.kb_a = (uint32_t)(rows * p.BK * 2);
         R.nkb = (int)std::max<size_t>(1, std::min<size_t>(8, stage_cap / (R.kb_a + p.kb_b)));
-        if (getenv("SPC_NKB1")) R.nkb = 1;
         R.a_bytes = R.nkb * R.kb_a;
         R.b_bytes = R.nkb * p.kb_b;
         R.stages = (int)std::min<size_t>(16, avail / (R.a_bytes + R.b_bytes));
@@ -1388,15 +1204,16 @@ static spc_status launch_tc(const ConvParams &p0, int mode, int out_kind, void *
     }
     p.hdr_off = (uint32_t)align_up(ring_bytes, 128);
     const size_t smem = 1024 + p.hdr_off + header;
-    static bool configured = false;
-    if (!configured) {
+    static uint64_t configured = 0;   // bit d: smem attributes set on device d
+    const int dev = current_device();
+    if (!(configured >> dev & 1)) {
         SPC_CUDA(cudaFuncSetAttribute(k_conv_tc<16, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BUDGET));
         SPC_CUDA(cudaFuncSetAttribute(k_conv_tc<32, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BUDGET));
         SPC_CUDA(cudaFuncSetAttribute(k_conv_tc<64, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BUDGET));
         SPC_CUDA(cudaFuncSetAttribute(k_conv_tc<16, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BUDGET));
         SPC_CUDA(cudaFuncSetAttribute(k_conv_tc<32, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BUDGET));
         SPC_CUDA(cudaFuncSetAttribute(k_conv_tc<64, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BUDGET));
-        configured = true;
+        configured |= 1ull << dev;
     }
     // persistent: one CTA per SM (tile geometry and counts live on the device)
     const int64_t tiles_cap = mode == 0 ? ((p.n_out_cap + TC_BM - 1) / TC_BM) * p.n_ntiles *
@@ -1497,16 +1314,14 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
     p.n_ntiles = c_out / p.BN;
     p.tmem_cols = pow2_cols(p.BN);
     p.num_sms = num_sms();
-    p.force_tr = getenv("SPC_TR") ? atoi(getenv("SPC_TR")) : 0;
-    p.split_min_unit = getenv("SPC_SPLIT_MIN") ? atoi(getenv("SPC_SPLIT_MIN")) : 2;
-    p.claim_ahead = getenv("SPC_CLAIM_AHEAD") ? std::max(1, std::min(3, atoi(getenv("SPC_CLAIM_AHEAD")))) : 1;
-    p.split_tiles_per_sm2 = getenv("SPC_SPLIT_TILES2") ? atoi(getenv("SPC_SPLIT_TILES2")) : p.num_sms;
+    const int64_t force_tr = option(SPC_OPT_CONV_TILE_ROWS);
+    p.force_tr = (force_tr == 128 || force_tr == 256) ? (int)force_tr : 0;
+    p.split_min_unit = (int)std::max<int64_t>(1, option(SPC_OPT_CONV_SPLIT_MIN));
+    p.claim_ahead = (int)std::max<int64_t>(1, std::min<int64_t>(3, option(SPC_OPT_CONV_CLAIM_AHEAD)));
+    p.split_tiles_per_sm2 = p.num_sms;
     // 256-row tiles (two MMAs per weight tile) whenever four accumulators fit TMEM; the
     // kernel drops to 128-row tiles on the device when the live row count is small
-    // (experiment SPC_BM256_SINGLE: N = 256 with 256-row tiles and one accumulator buffer;
-    // measured no faster on the 256x256 layers: the 64 KB stages leave only 2 in flight)
-    static const bool bm256_single = getenv("SPC_BM256_SINGLE") != nullptr;
-    p.bm = ((4 * p.tmem_cols <= 512 || (bm256_single && 2 * p.tmem_cols <= 512)) && !getenv("SPC_BM128")) ? 256 : 128;
+    p.bm = (4 * p.tmem_cols <= 512) ? 256 : 128;
     if (has_os && (size_t)BLK_SLOTS * p.bm * km->k_dense * 4 > 96 * 1024) p.bm = 128;   // OS index blocks (K=5)
     p.tbufs = (p.bm == 256 ? 4 : 2) * p.tmem_cols <= 512 ? 2 : 1;
     p.kb_b = (uint32_t)(p.BN * p.BK * 2);
@@ -1524,7 +1339,7 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
     p.tile_ctr = wctr;
     if (!has_ws) {
         // OS only: one launch; small levels split offsets over CTAs with the in-kernel fixup
-        p.split_ok = (wacc && km->k_dense >= 4 && !getenv("SPC_NO_OS_SPLIT")) ? 1 : 0;
+        p.split_ok = (wacc && km->k_dense >= 4 && option(SPC_OPT_CONV_OS_SPLIT) != 0) ? 1 : 0;
         return launch_tc(p, 0, OUT_FINAL, f_out, ld_out, st);
     }
     p.split_ok = 0;
@@ -1549,19 +1364,3 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
     return SPC_OK;
 }
 
-#ifdef SPC_EXP_TRACE2
-extern "C" int spc_exp_tl_read(unsigned long long *host) {
-    cudaMemcpyFromSymbol(host, spc::g_tl, sizeof(spc::g_tl));
-    return (int)cudaMemset(nullptr, 0, 0);
-}
-extern "C" int spc_exp_tl_clear() {
-    void *p;
-    cudaGetSymbolAddress(&p, spc::g_tl);
-    return (int)cudaMemset(p, 0, sizeof(spc::g_tl));
-}
-#endif
-#ifdef SPC_EXP_TRACE
-extern "C" int spc_exp_trace_read(long long *host) {
-    return (int)cudaMemcpyFromSymbol(host, spc::g_tr, sizeof(spc::g_tr));
-}
-#endif

@@ -1,4 +1,3 @@
-#include <cstdlib>
 // spc_host.cu -- host-side C ABI of libspc: status plumbing, pack planning, offset and
 // mask helpers, and network-wide voxel indexing (A13, §5.5).
 #include <cuda_runtime.h>
@@ -25,19 +24,31 @@ spc_status cuda_fail(cudaError_t e, const char *what) {
     return SPC_ERR_CUDA;
 }
 
-bool pdl_enabled() {
-    static int on = -1;
-    if (on < 0) on = getenv("SPC_NO_PDL") ? 0 : 1;
-    return on != 0;
+// process-wide tuning options (spc_set_option); performance only
+static const int64_t kOptDefault[SPC_OPT_COUNT] = {0, 72, 1, 2, 1, 1, 1, 4096};
+static int64_t g_opt[SPC_OPT_COUNT] = {0, 72, 1, 2, 1, 1, 1, 4096};
+
+int64_t option(int o) { return (o >= 0 && o < SPC_OPT_COUNT) ? g_opt[o] : 0; }
+
+bool pdl_enabled() { return g_opt[SPC_OPT_PDL] != 0; }
+
+// device attributes cached per device (a process may drive several GPUs)
+constexpr int MAX_DEVICES = 64;
+static int g_num_sms[MAX_DEVICES];
+
+int current_device() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return (dev >= 0 && dev < MAX_DEVICES) ? dev : 0;
 }
 
 int num_sms() {
-    static int n = 0;
+    const int dev = current_device();
+    int n = g_num_sms[dev];
     if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
         if (n <= 0) n = 148;
+        g_num_sms[dev] = n;
     }
     return n;
 }
@@ -76,6 +87,14 @@ extern "C" int spc_version(void) { return SPC_VERSION; }
 
 extern "C" size_t spc_kmap_struct_bytes(void) { return sizeof(spc_kmap); }
 
+extern "C" spc_status spc_set_option(int32_t o, int64_t value) {
+    if (o < 0 || o >= SPC_OPT_COUNT) return fail(SPC_ERR_INVALID_ARG, "spc_set_option: unknown option " + std::to_string(o));
+    g_opt[o] = value < 0 ? kOptDefault[o] : value;
+    return SPC_OK;
+}
+
+extern "C" int64_t spc_get_option(int32_t o) { return option(o); }
+
 extern "C" spc_status spc_plan_pack(const int32_t lo[3], const int32_t hi[3], int32_t n_batch,
                                     int32_t max_out_stride, int32_t max_reach, spc_pack_spec *out) {
     SPC_CHECK_ARG(lo && hi && out, "null pointer");
@@ -106,6 +125,8 @@ extern "C" spc_status spc_plan_pack(const int32_t lo[3], const int32_t hi[3], in
     out->bits_x = bits[0];
     out->bits_y = bits[1];
     out->bits_z = bits[2];
+    out->reach = max_reach;
+    out->out_stride = max_out_stride;
     return SPC_OK;
 }
 

@@ -26,7 +26,6 @@ namespace spc {
 constexpr int KM_BM = 128;          // outputs per tile
 constexpr int KM_THREADS = 256;
 constexpr int KM_WARPS = KM_THREADS / 32;
-constexpr int KM_WWIN = 512;        // staged window keys per warp task (4 KB); larger: global search
 
 // Compact per-map descriptor; the offset tables (packed query deltas, weight slots,
 // dense columns, WS lists) are rebuilt in shared memory from it, so one launch can build
@@ -60,6 +59,7 @@ struct KmapBatch {
     int n_maps;
     int bits_y, bits_z;
     unsigned int *work_ctr;   // zeroed before the launch
+    int pool_keys;            // usable keys of the shared window pool (<= KM_POOL; SPC_OPT_KMAP_POOL_KEYS)
     // density order: keys of all ordered maps, concatenated in ord_idx order by live counts
     uint64_t *ord_keys;
     int64_t *ord_total;       // sum of their live rows (written by k_kmap_prep)
@@ -180,9 +180,11 @@ __device__ __forceinline__ int tile_map(const int64_t *pre, int n_maps, int64_t 
     return m;
 }
 
-// lower bound in a staged (shared) or global window
+// lower bound in a staged (shared) or global window; every call is counted in n_calls
+// (the search-count law |V_q| K^2 of P:297 is checked against this counter)
 template <bool SM>
-__device__ __forceinline__ int lb_win(const uint64_t *a, int n, uint64_t q) {
+__device__ __forceinline__ int lb_win(const uint64_t *a, int n, uint64_t q, unsigned &n_calls) {
+    ++n_calls;
     int lo = 0, len = n;
     while (len > 0) {
         const int half = len >> 1;
@@ -206,12 +208,12 @@ __device__ __forceinline__ int lb_win(const uint64_t *a, int n, uint64_t q) {
 // [list][row]; counts, mask bits and density-order bits go to shared accumulators.
 template <int K, bool SM>
 __device__ __forceinline__ int zdelta_chunk(ZTile &zt, int32_t *s_os, int32_t *s_ws, int KD, const uint64_t *wk,
-                                            int wl, int32_t lo, int g, int ch, int rows, int lane) {
+                                            int wl, int32_t lo, int g, int ch, int rows, int lane, unsigned &n_calls) {
     const int lr = ch * 32 + lane;
     const bool valid = lr < rows;
     const uint64_t q = valid ? zt.q[lr] : 0;
     int pos = 0;
-    if (valid) pos = lb_win<SM>(wk, wl, q + (uint64_t)zt.dq[g * K]);
+    if (valid) pos = lb_win<SM>(wk, wl, q + (uint64_t)zt.dq[g * K], n_calls);
     const int pos0 = pos;
     uint32_t key = 0;
 #pragma unroll
@@ -241,9 +243,7 @@ __device__ __forceinline__ int zdelta_chunk(ZTile &zt, int32_t *s_os, int32_t *s
     return pos - pos0;   // cursor advances (search-count statistics)
 }
 
-#ifndef SPC_KM_MIN_BLOCKS
-#define SPC_KM_MIN_BLOCKS 4
-#endif
+constexpr int KM_MIN_BLOCKS = 4;
 // one CTA per (map, tile of KM_BM outputs), grid-strided over every tile of every map of
 // the batch.  Per tile: (1) every warp stages its share of the K^2 group windows
 // [lo, hi) (k_kmap_bounds) into one shared pool, coalesced; (2) the warps share the
@@ -252,7 +252,7 @@ __device__ __forceinline__ int zdelta_chunk(ZTile &zt, int32_t *s_os, int32_t *s
 // P:400) as 16-byte stores, each WS list's pairs compacted with one reservation per
 // (tile, list) (warp ballots, no filter pass; halved for submanifold maps,
 // P:418-421), the tile mask, per-offset counts and density-order keys.
-__global__ void __launch_bounds__(KM_THREADS, SPC_KM_MIN_BLOCKS) k_kmap_zdelta(const __grid_constant__ KmapBatch B) {
+__global__ void __launch_bounds__(KM_THREADS, KM_MIN_BLOCKS) k_kmap_zdelta(const __grid_constant__ KmapBatch B) {
     pdl_wait();   // PDL launch: the predecessor has completed and flushed
     pdl_trigger();
     __shared__ int8_t s_dcol[KM_MAX_MAPS][SPC_MAX_KVOL];   // weight offset -> dense column / -1
@@ -287,6 +287,7 @@ __global__ void __launch_bounds__(KM_THREADS, SPC_KM_MIN_BLOCKS) k_kmap_zdelta(c
     __syncthreads();
     const int64_t total = s_pre[B.n_maps];
     unsigned long long n_search = 0, n_probe = 0;
+    unsigned n_calls = 0;   // lower_bound calls of this thread (lb_win)
     int stats_map = -1;
     // software pipeline: the next tile's output keys and window bounds are loaded into
     // registers while the current tile flushes (one global round trip off the tile chain)
@@ -354,7 +355,7 @@ __global__ void __launch_bounds__(KM_THREADS, SPC_KM_MIN_BLOCKS) k_kmap_zdelta(c
                 if (lane >= o) x += y;
             }
             const int off = x - wl;
-            const bool fits = x <= KM_POOL;
+            const bool fits = x <= B.pool_keys;
             if (warp == 0 && lane < G) {
                 zt.wlo[lane] = lo;
                 zt.wlen[lane] = need ? wl : -1;   // -1: group not needed
@@ -378,6 +379,8 @@ __global__ void __launch_bounds__(KM_THREADS, SPC_KM_MIN_BLOCKS) k_kmap_zdelta(c
         }
         __syncthreads();
         if (p.stats && stats_map != m) {   // flush the stats of the previous map
+            n_search += n_calls;
+            n_calls = 0;
             for (int o = 16; o > 0; o >>= 1) {
                 n_search += __shfl_xor_sync(0xffffffffu, n_search, o);
                 n_probe += __shfl_xor_sync(0xffffffffu, n_probe, o);
@@ -397,16 +400,15 @@ __global__ void __launch_bounds__(KM_THREADS, SPC_KM_MIN_BLOCKS) k_kmap_zdelta(c
             if (wl < 0) continue;
             const int32_t lo = zt.wlo[g];
             const int off = zt.woff[g];
-            if (p.stats && lane == 0) n_search += (unsigned long long)min(32, rows - ch * 32);
             int adv;
             if (off >= 0) {
-                if (K == 3) adv = zdelta_chunk<3, true>(zt, s_os, s_ws, KD, s_pool + off, wl, lo, g, ch, rows, lane);
-                else if (K == 5) adv = zdelta_chunk<5, true>(zt, s_os, s_ws, KD, s_pool + off, wl, lo, g, ch, rows, lane);
-                else adv = zdelta_chunk<1, true>(zt, s_os, s_ws, KD, s_pool + off, wl, lo, g, ch, rows, lane);
+                if (K == 3) adv = zdelta_chunk<3, true>(zt, s_os, s_ws, KD, s_pool + off, wl, lo, g, ch, rows, lane, n_calls);
+                else if (K == 5) adv = zdelta_chunk<5, true>(zt, s_os, s_ws, KD, s_pool + off, wl, lo, g, ch, rows, lane, n_calls);
+                else adv = zdelta_chunk<1, true>(zt, s_os, s_ws, KD, s_pool + off, wl, lo, g, ch, rows, lane, n_calls);
             } else {
-                if (K == 3) adv = zdelta_chunk<3, false>(zt, s_os, s_ws, KD, p.in + lo, wl, lo, g, ch, rows, lane);
-                else if (K == 5) adv = zdelta_chunk<5, false>(zt, s_os, s_ws, KD, p.in + lo, wl, lo, g, ch, rows, lane);
-                else adv = zdelta_chunk<1, false>(zt, s_os, s_ws, KD, p.in + lo, wl, lo, g, ch, rows, lane);
+                if (K == 3) adv = zdelta_chunk<3, false>(zt, s_os, s_ws, KD, p.in + lo, wl, lo, g, ch, rows, lane, n_calls);
+                else if (K == 5) adv = zdelta_chunk<5, false>(zt, s_os, s_ws, KD, p.in + lo, wl, lo, g, ch, rows, lane, n_calls);
+                else adv = zdelta_chunk<1, false>(zt, s_os, s_ws, KD, p.in + lo, wl, lo, g, ch, rows, lane, n_calls);
             }
             n_probe += (unsigned long long)adv;
         }
@@ -458,6 +460,7 @@ __global__ void __launch_bounds__(KM_THREADS, SPC_KM_MIN_BLOCKS) k_kmap_zdelta(c
         __syncthreads();
     }
     if (stats_map >= 0) {
+        n_search += n_calls;
         for (int o = 16; o > 0; o >>= 1) {
             n_search += __shfl_xor_sync(0xffffffffu, n_search, o);
             n_probe += __shfl_xor_sync(0xffffffffu, n_probe, o);
@@ -878,7 +881,9 @@ static void fill_desc(KmapDesc &d, const spc_kmap &km, const KmapPlan &pl, int32
     }
 }
 
-static spc_status launch_kmaps(const KmapBatch &b, int max_k_dense, int64_t max_tiles, cudaStream_t st) {
+static spc_status launch_kmaps(const KmapBatch &b0, int max_k_dense, int64_t max_tiles, cudaStream_t st) {
+    KmapBatch b = b0;
+    b.pool_keys = (int)std::max<int64_t>(0, std::min<int64_t>(KM_POOL, option(SPC_OPT_KMAP_POOL_KEYS)));
     SPC_CUDA(launch_pdl(k_kmap_prep, dim3(b.n_maps > 0 ? b.n_maps : 1), dim3(256), 0, st, b));
     SPC_LAUNCH_CHECK("k_kmap_prep");
     {
@@ -897,10 +902,11 @@ static spc_status launch_kmaps(const KmapBatch &b, int max_k_dense, int64_t max_
     }
     (void)max_k_dense;
     const size_t dsm = (size_t)KM_BM * max_cols * sizeof(int32_t);
-    static size_t dsm_set = 0;
-    if (dsm > dsm_set) {
+    static size_t dsm_set[64] = {};   // per device
+    const int dev = current_device();
+    if (dsm > dsm_set[dev]) {
         SPC_CUDA(cudaFuncSetAttribute(k_kmap_zdelta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
-        dsm_set = dsm;
+        dsm_set[dev] = dsm;
     }
     int per_sm = 0;
     SPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_kmap_zdelta, KM_THREADS, dsm));
@@ -943,12 +949,17 @@ extern "C" spc_status spc_build_kmap(const uint64_t *in_keys, int64_t n_in, cons
     const KmapLayout L = layout_of(pl, n_out, flags, !g_defer.active);
     SPC_CHECK_ARG(buf && ((uintptr_t)buf % 256) == 0, "buf must be non-null and 256-byte aligned");
     if (buf_bytes < L.total) return fail(SPC_ERR_WORKSPACE, "spc_build_kmap: buffer too small");
-    // reach check (reading A4): the planner guarantees headroom; here we only refuse
-    // offsets that cannot be represented in the z field at all
-    const int reach = pl.r * pl.spacing;
-    if (reach >= (1 << (spec.bits_z - 1)) || reach >= (1 << (spec.bits_y - 1)) || reach >= (1 << (spec.bits_x - 1)))
-        return fail(SPC_ERR_RANGE, "spc_build_kmap: kernel reach " + std::to_string(reach) +
-                                       " does not fit the key fields");
+    // reach check (reading A4): spc_pack_sort guarantees every key leaves `spec.reach`
+    // (and out_stride - 1 below) of headroom in each field; a map reaching further could
+    // carry or borrow into a neighbouring field, so it is refused, never truncated
+    const int64_t reach = (int64_t)pl.r * pl.spacing;
+    if (reach > spec.reach)
+        return fail(SPC_ERR_RANGE, "spc_build_kmap: kernel reach r*tensor_stride*dilation = " + std::to_string(reach) +
+                                       " exceeds the planned spec.reach = " + std::to_string(spec.reach));
+    if ((int64_t)geom.tensor_stride * geom.stride > spec.out_stride)
+        return fail(SPC_ERR_RANGE, "spc_build_kmap: coarse stride " +
+                                       std::to_string((int64_t)geom.tensor_stride * geom.stride) +
+                                       " exceeds the planned spec.out_stride = " + std::to_string(spec.out_stride));
     cudaStream_t st = as_stream(stream);
     char *base = static_cast<char *>(buf);
 

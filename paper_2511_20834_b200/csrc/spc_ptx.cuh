@@ -15,6 +15,17 @@ __device__ __forceinline__ int32_t lds_s32(uint32_t addr) {
     return v;
 }
 
+// volatile shared-space load / store (a flag polled across warps of one CTA; the explicit
+// .shared space keeps it an LDS, not a generic LD.E.STRONG.SYS)
+__device__ __forceinline__ int32_t lds_volatile_s32(uint32_t addr) {
+    int32_t v;
+    asm volatile("ld.volatile.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts_volatile_s32(uint32_t addr, int32_t v) {
+    asm volatile("st.volatile.shared.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
 // ---- mbarrier ------------------------------------------------------------------------
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
@@ -41,13 +52,8 @@ __device__ __forceinline__ bool mbar_test_wait(uint32_t bar, uint32_t parity) {
     return ok != 0;
 }
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-#ifdef SPC_EXP_TESTWAIT
-    while (!mbar_test_wait(bar, parity)) {
-    }
-#else
     while (!mbar_try_wait(bar, parity)) {
     }
-#endif
 }
 // wait with exponential back-off: for waiters off the critical path (epilogue, scheduler),
 // so their polling does not compete with the pipeline's own mbarrier traffic

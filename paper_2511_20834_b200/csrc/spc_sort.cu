@@ -1,10 +1,12 @@
 // spc_sort.cu -- A1 pack, A2 sort-once, A3 grouped downsampling (Eq. 1 / Eq. 3).
 //
-// LSD radix sort over the USED key bits only (8-bit digits).  One pass = three kernels:
-//   k_radix_hist   : per-tile digit histograms (warp-aggregated smem atomics)
-//   k_radix_scan   : per-digit exclusive scan over tiles (digit-major, one CTA per digit)
-//   k_radix_scatter: stable in-tile ranking with __match_any_sync, tile staged in smem,
-//                    then written out digit-run by digit-run (coalesced runs).
+// LSD radix sort over the USED key bits only (8-bit digits), onesweep style:
+//   k_hist_all  : the digit histograms of EVERY pass in one read of the keys (k_pack
+//                 computes them itself while packing, so spc_pack_sort skips this)
+//   k_hist_scan : exclusive scans of those histograms (one CTA per pass)
+//   k_onesweep  : one launch per pass: stable in-tile ranking, then the tile's global
+//                 digit offsets by decoupled look-back over the preceding tiles, then a
+//                 scatter staged through shared memory (coalesced digit runs)
 // Every kernel reads the element count from device memory (n_dev), so the whole
 // indexing phase runs without host syncs.
 #include <cuda_runtime.h>
@@ -303,9 +305,10 @@ spc_status radix_sort(const uint64_t *keys_in, const int32_t *vals_in, int64_t n
 // ------------------------------------------------------------------------------------
 struct PackDev {
     int bb, bx, by, bz;
+    int lo_room, hi_room;   // planned headroom below / above (reading A4): (out_stride-1)+reach / reach
 };
 
-__global__ void __launch_bounds__(256) k_pack(const int4 *__restrict__ coords, int64_t n, PackDev s,
+__global__ void __launch_bounds__(256) k_pack(const int4 *__restrict__ coords, int64_t n_cap, const int64_t *n_dev, PackDev s,
                                               uint64_t *__restrict__ keys, uint32_t *status, int passes,
                                               unsigned int *__restrict__ ghist) {
     pdl_wait();   // PDL launch: the predecessor has completed and flushed
@@ -313,6 +316,7 @@ __global__ void __launch_bounds__(256) k_pack(const int4 *__restrict__ coords, i
     __shared__ unsigned int h[MAX_PASSES][256];
     for (int i = threadIdx.x; i < passes * 256; i += blockDim.x) h[i / 256][i % 256] = 0;
     __syncthreads();
+    const int64_t n = dev_count(n_cap, n_dev);
     bool bad = false;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         int4 c = coords[i];
@@ -320,8 +324,11 @@ __global__ void __launch_bounds__(256) k_pack(const int4 *__restrict__ coords, i
         int64_t fx = (int64_t)c.y + (1ll << (s.bx - 1));
         int64_t fy = (int64_t)c.z + (1ll << (s.by - 1));
         int64_t fz = (int64_t)c.w + (1ll << (s.bz - 1));
-        bool ok = fb >= 0 && fb < (1ll << s.bb) && fx >= 0 && fx < (1ll << s.bx) && fy >= 0 &&
-                  fy < (1ll << s.by) && fz >= 0 && fz < (1ll << s.bz);
+        // inside the field with the planned headroom on both sides, so downsampled
+        // coordinates and kernel-map queries never carry or borrow into a neighbour field
+        bool ok = fb >= 0 && fb < (1ll << s.bb) && fx >= s.lo_room && fx < (1ll << s.bx) - s.hi_room &&
+                  fy >= s.lo_room && fy < (1ll << s.by) - s.hi_room && fz >= s.lo_room &&
+                  fz < (1ll << s.bz) - s.hi_room;
         bad |= !ok;
         uint64_t k = ((uint64_t)fb << (s.bx + s.by + s.bz)) | ((uint64_t)fx << (s.by + s.bz)) |
                      ((uint64_t)fy << s.bz) | (uint64_t)fz;
@@ -512,7 +519,7 @@ extern "C" size_t spc_pack_sort_workspace_size(int64_t n) {
     return align_up(sizeof(uint64_t) * (size_t)n, 256) + radix_sort_workspace(n, true) + 256;
 }
 
-extern "C" spc_status spc_pack_sort(const int32_t *coords, int64_t n, spc_pack_spec spec, uint64_t *keys_out,
+extern "C" spc_status spc_pack_sort(const int32_t *coords, int64_t n, const int64_t *n_dev, spc_pack_spec spec, uint64_t *keys_out,
                                     int32_t *perm_out, uint32_t *status, void *ws, size_t ws_bytes,
                                     void *stream) {
     SPC_CHECK_ARG(n >= 0, "n < 0");
@@ -522,25 +529,27 @@ extern "C" spc_status spc_pack_sort(const int32_t *coords, int64_t n, spc_pack_s
     const int used = spec.bits_b + spec.bits_x + spec.bits_y + spec.bits_z;
     SPC_CHECK_ARG(spec.bits_b >= 0 && spec.bits_x >= 2 && spec.bits_y >= 2 && spec.bits_z >= 2 && used <= 62,
                   "bad pack spec");
+    SPC_CHECK_ARG(spec.reach >= 0 && spec.out_stride >= 1 && (spec.out_stride & (spec.out_stride - 1)) == 0,
+                  "pack spec: reach must be >= 0 and out_stride a power of two >= 1");
     if (ws_bytes < spc_pack_sort_workspace_size(n)) return fail(SPC_ERR_WORKSPACE, "spc_pack_sort: ws too small");
     cudaStream_t st = as_stream(stream);
     Bump b(ws, ws_bytes);
     uint64_t *raw = b.take<uint64_t>((size_t)n);
     void *rws = b.base + align_up(b.used, 256);
     size_t rws_bytes = ws_bytes - align_up(b.used, 256);
-    PackDev pd{spec.bits_b, spec.bits_x, spec.bits_y, spec.bits_z};
+    PackDev pd{spec.bits_b, spec.bits_x, spec.bits_y, spec.bits_z, spec.out_stride - 1 + spec.reach, spec.reach};
     int grid = (int)imin64((n + 2047) / 2048, 2 * 148);
     // pack + all radix histograms in one pass over the coordinates (the histogram block is
     // the first region of the radix workspace)
     unsigned int *hist = reinterpret_cast<unsigned int *>(rws);   // == radix_sort's first workspace block
     SPC_CUDA(cudaMemsetAsync(hist, 0, sizeof(unsigned int) * MAX_PASSES * 256, st));
-    SPC_CUDA(launch_pdl(k_pack, dim3(grid), dim3(256), 0, st, reinterpret_cast<const int4 *>(coords), n, pd, raw, status, (used + 7) / 8, hist));
+    SPC_CUDA(launch_pdl(k_pack, dim3(grid), dim3(256), 0, st, reinterpret_cast<const int4 *>(coords), n, n_dev, pd, raw, status, (used + 7) / 8, hist));
     SPC_LAUNCH_CHECK("k_pack");
     int32_t *perm = perm_out;
-    spc_status s = radix_sort(raw, nullptr, n, nullptr, used, keys_out, perm, rws, rws_bytes, st, true);
+    spc_status s = radix_sort(raw, nullptr, n, n_dev, used, keys_out, perm, rws, rws_bytes, st, true);
     if (s != SPC_OK) return s;
     if (status) {
-        SPC_CUDA(launch_pdl(k_flag_dups, dim3(grid), dim3(256), 0, st, keys_out, n, nullptr, status, SPC_FLAG_DUPLICATE));
+        SPC_CUDA(launch_pdl(k_flag_dups, dim3(grid), dim3(256), 0, st, keys_out, n, n_dev, status, SPC_FLAG_DUPLICATE));
         SPC_LAUNCH_CHECK("k_flag_dups");
     }
     return SPC_OK;
@@ -585,6 +594,9 @@ extern "C" spc_status spc_downsample(const uint64_t *keys, int64_t n, const int6
         int m = log2_stride_host[l];
         if (m < 0 || m > minb - 1)
             return fail(SPC_ERR_INVALID_ARG, "spc_downsample: log2 stride " + std::to_string(m) + " out of range");
+        if ((1ll << m) > spec.out_stride)
+            return fail(SPC_ERR_RANGE, "spc_downsample: stride " + std::to_string(1ll << m) +
+                                           " exceeds the planned spec.out_stride " + std::to_string(spec.out_stride));
         lm.mask[l] = spc_downsample_mask(spec, m);
     }
     if (ws_bytes < spc_downsample_workspace_size(n, n_levels))

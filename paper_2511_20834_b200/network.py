@@ -180,6 +180,7 @@ class SparseNet:
         self.keys = torch.empty(self.n0, dtype=torch.int64, device=self.dev)
         self.perm = torch.empty(self.n0, dtype=torch.int32, device=self.dev)
         self.status = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self.n_live = torch.zeros(1, dtype=torch.int64, device=self.dev)   # live voxel count (scans < n0)
         self.sort_ws = torch.empty(int(spc.lib().spc_pack_sort_workspace_size(self.n0)), dtype=torch.uint8,
                                    device=self.dev)
         self.conv_ws = None      # sized from spc_conv_workspace_size once the maps exist (index())
@@ -200,17 +201,19 @@ class SparseNet:
             flags.append(f)
         return geoms, ts, flags
 
-    def index(self, stream=None):
-        """Network-wide voxel indexing: all levels, then all maps."""
+    def index(self, stream=None, n_dev=None):
+        """Network-wide voxel indexing: all levels, then all maps.  ``n_dev``: device
+        int64 live voxel count when the scan is smaller than the capacity n0."""
         if self.netidx is None:
             geoms, ts, flags = self._geoms()
             self.netidx = spc.NetworkIndex(self.n0, self.spec, self.n_levels, geoms, ts, flags, device=self.dev)
-        kms = self.netidx.run(self.keys, status=self.status, stream=stream)
+        kms = self.netidx.run(self.keys, n0_dev=n_dev, status=self.status, stream=stream)
         self.level_keys, self.level_n = self.netidx.level_keys, self.netidx.level_n
         self.maps = dict(zip(self.map_keys, kms))
         need = max(spc.spc_conv_workspace_size(self.maps[s.map_key], s.c_out) for s in self.layers)
         if self.conv_ws is None or self.conv_ws.numel() < need:
-            self.conv_ws = torch.zeros(need, dtype=torch.uint8, device=self.dev)   # zero once (spc.h ws contract)
+            # zero once (spc.h ws contract), on the stream the convolutions run on
+            self.conv_ws = spc._ws(need, self.dev, zero=True, stream=stream)
 
     def set_t(self, t_map: dict):
         self.t.update(t_map)
@@ -228,17 +231,26 @@ class SparseNet:
         spc.spc_conv_forward(km, src, self.weights[i], s.c_in, s.c_out, out=dst, residual=res, ws=self.conv_ws,
                              stream=stream)
 
-    def forward(self, coords: torch.Tensor, feats: torch.Tensor, stream=None) -> torch.Tensor:
-        """coords int32 [n,4] (any order), feats bf16 [n, 16] (first 4 channels real) -> out [n, 96]
-        in sorted (canonical) voxel order."""
+    def forward(self, coords: torch.Tensor, feats: torch.Tensor, stream=None, n_live=None) -> torch.Tensor:
+        """coords int32 [n,4] (any order), feats bf16 [n, 16] (first 4 channels real) -> out
+        [n0, 96] whose first n rows are the scan's voxels in sorted (canonical) order.
+
+        Any scan size n <= n0 (the capacity) runs on the same buffers: the live count
+        travels on the device (``n_live``, int64 [1]; filled from n when omitted), so
+        a CUDA graph captured once replays for every scan size when the caller pads
+        coords / feats to n0 rows and writes the live count into ``n_live``."""
         n = coords.shape[0]
-        assert n <= self.n0
+        if n > self.n0:
+            raise ValueError(f"scan of {n} voxels exceeds the capacity {self.n0}")
+        if n_live is None and n < self.n0:
+            n_live = self.n_live
+            st = stream if stream is not None else torch.cuda.current_stream(self.dev)
+            with torch.cuda.stream(st):
+                n_live.fill_(n)
         spc.spc_pack_sort(coords, self.spec, status=self.status, keys_out=self.keys[:n], perm_out=self.perm[:n],
-                          ws=self.sort_ws, stream=stream)
-        spc.spc_gather_rows(feats, self.perm[:n], out=self.bufs["x0"][:n], stream=stream)
-        if n != self.n0:
-            raise ValueError("capacity must equal the scan size (allocate per scan)")
-        self.index(stream)
+                          ws=self.sort_ws, stream=stream, n_dev=n_live)
+        spc.spc_gather_rows(feats, self.perm[:n], out=self.bufs["x0"][:n], n_dev=n_live, stream=stream)
+        self.index(stream, n_dev=n_live)
         for i in range(len(self.layers)):
             self.conv(i, stream)
         return self.bufs[self.out_name]

@@ -63,3 +63,49 @@ def test_kmap_bytes_and_errors(L):
     g = spc.Geom(3, 1, 1, 1, 0)
     assert spc.spc_kmap_bytes(g, -1, 0, 1000, 1000) >= 1000 * 27 * 4
     assert spc.spc_kmap_bytes(spc.Geom(2, 1, 1, 1, 0), -1, 0, 10, 10) == 0     # even K unsupported
+
+
+def test_plan_records_headroom(L):
+    s = spc.spc_plan_pack((-1024, -1024, -80), (1023, 1023, 48), n_batch=1, max_out_stride=16, max_reach=16)
+    assert (s.reach, s.out_stride) == (16, 16)
+
+
+def _build_kmap_status(L, spec, geom):
+    """spc_build_kmap's host-side checks only (no keys, no device work): returns the status."""
+    km = spc._Kmap()
+    nbytes = spc.spc_kmap_bytes(geom, -1, 0, 0, 0)
+    return L.spc_build_kmap(None, 0, None, None, 0, None, spec, geom, -1, 0, ctypes.c_void_p(1 << 20),
+                            nbytes, None, ctypes.byref(km), None)
+
+
+def test_build_kmap_refuses_reach_beyond_plan(L):
+    """Reading A4 / S:84: a map reaching further than the planned headroom is an
+    error (SPC_ERR_RANGE), never a silent carry into the neighbouring field."""
+    spec = spc.spc_plan_pack((-100, -100, -20), (100, 100, 20), 1, max_out_stride=4, max_reach=2)
+    # within the plan: past the host checks (without a GPU the enqueue itself then fails)
+    assert _build_kmap_status(L, spec, spc.Geom(3, 1, 1, 2, 0)) != 3          # r*ts*d = 2
+    assert _build_kmap_status(L, spec, spc.Geom(5, 1, 1, 1, 0)) != 3          # r = 2
+    assert _build_kmap_status(L, spec, spc.Geom(3, 1, 2, 2, 0)) == 3          # 1*2*2 = 4 > 2
+    assert _build_kmap_status(L, spec, spc.Geom(5, 1, 1, 2, 0)) == 3          # 2*2 = 4 > 2
+    assert _build_kmap_status(L, spec, spc.Geom(3, 2, 1, 4, 0)) == 3          # coarse stride 8 > 4
+    assert b"reach" in L.spc_last_error_detail() or b"stride" in L.spc_last_error_detail()
+
+
+def test_options_roundtrip(L):
+    assert spc.spc_get_option(spc.SPC_OPT_CONV_STAGE_KB) == 72
+    spc.spc_set_option(spc.SPC_OPT_CONV_STAGE_KB, 48)
+    assert spc.spc_get_option(spc.SPC_OPT_CONV_STAGE_KB) == 48
+    spc.spc_set_option(spc.SPC_OPT_CONV_STAGE_KB, -1)
+    assert spc.spc_get_option(spc.SPC_OPT_CONV_STAGE_KB) == 72
+    with pytest.raises(spc.SpcError):
+        spc.spc_set_option(99, 1)
+
+
+def test_no_environment_knobs_in_the_product():
+    """The product library reads no environment variables (tuning is explicit through
+    spc_set_option) and carries no experiment-only code paths."""
+    csrc = os.path.join(ROOT, "paper_2511_20834_b200", "csrc")
+    for f in os.listdir(csrc):
+        src = open(os.path.join(csrc, f)).read()
+        assert "getenv" not in src, f
+        assert "SPC_EXP_" not in src, f

@@ -256,7 +256,7 @@ def test_kmap_density_order_exact(K, kind, t):
 
 
 def test_kmap_edge_cases():
-    spec = spc.PackSpec(0, 8, 8, 8)
+    spec = spc.PackSpec(0, 8, 8, 8, 1, 1)
     one = torch.tensor([(128 << 16) | (128 << 8) | 128], dtype=torch.int64, device=DEV)
     km = spc.spc_build_kmap(one, one, spec, spc.Geom(3, 1, 1, 1, 0), -1, 0)
     assert spc.spc_kmap_export(km).tolist() == [[13, 0, 0]]
