@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--no-tune", action="store_true")
     ap.add_argument("--t-from", default=None, help="take the per-map dataflow t from a previous bench JSON line "
                                                    "(config.dataflow_t) instead of tuning")
+    ap.add_argument("--save-t", default=None, help="write the tuned per-map dataflow t to this JSON file")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-order", action="store_true", help="kernel maps without the OS density order (ablation)")
     ap.add_argument("--profile-layers", action="store_true", help="print the per-layer table to stderr")
@@ -69,13 +70,16 @@ def dist_env():
 # shared: the synthetic workload
 # ---------------------------------------------------------------------------------------
 
-def workload(rank: int, config: int = CONFIG_ID, world: int = 1):
+TUNE_SCAN_OFFSET = 100   # the dataflow tuner runs on other scans than the timed ones ("sample point clouds")
+
+
+def workload(rank: int, config: int = CONFIG_ID, world: int = 1, scan_offset: int = 0):
     """Synthetic input of this rank: (coords int32 [n,4], raw features [n, c_raw], scans, net)."""
     import synth
     if config == 4:
         from paper_2511_20834_b200.distributed import assign_scans
         # sizes are known from the generator; LPT-assign the 8 scans to ranks
-        scans = [synth.make_scan(4, i) for i in range(8)]
+        scans = [synth.make_scan(4, scan_offset + i) for i in range(8)]
         mine = assign_scans([s.shape[0] for s in scans], world)[rank]
         parts = []
         for b, i in enumerate(mine):
@@ -85,9 +89,9 @@ def workload(rank: int, config: int = CONFIG_ID, world: int = 1):
         coords = np.concatenate(parts)
         feats = synth.make_features(coords.shape[0], 4, seed=synth.scan_seed(4, 100 + rank))
         return coords, feats, len(mine), "minkunet42"
-    coords = synth.make_scan(config, scan_index=rank)
+    coords = synth.make_scan(config, scan_index=scan_offset + rank)
     c_raw = 5 if config == 3 else 4
-    feats = synth.make_features(coords.shape[0], c_raw, seed=synth.scan_seed(config, rank) + 1)
+    feats = synth.make_features(coords.shape[0], c_raw, seed=synth.scan_seed(config, scan_offset + rank) + 1)
     return coords, feats, 1, ("secondk5" if config == 3 else "minkunet42")
 
 
@@ -287,7 +291,20 @@ def main():
     if args.t_from:
         net.set_t(load_t(args.t_from))
     elif not args.no_tune:
-        tuned = tune(net, coords, feats, stream)
+        # tuned on a different scan of the same configuration, then applied to this one
+        tc_np, tf_np, _, _ = workload(rank, args.config, world, scan_offset=TUNE_SCAN_OFFSET)
+        tnet = SparseNet(tc_np.shape[0], spec_for(tc_np) if args.config != 4 else spc.spc_plan_pack(
+            tc_np[:, 1:].min(0), tc_np[:, 1:].max(0), 8, 16, 16), device=dev, net=net_name,
+            density_order=not args.no_order)
+        tfeats = torch.zeros(tc_np.shape[0], C_IN_PAD, dtype=torch.bfloat16, device=dev)
+        tfeats[:, :tf_np.shape[1]] = torch.from_numpy(tf_np).to(dev, torch.bfloat16)
+        tuned = tune(tnet, torch.from_numpy(tc_np).to(dev), tfeats, stream)
+        del tnet, tfeats
+        net.set_t(tuned)
+        if args.save_t and rank == 0:
+            json.dump({"dataflow_t": {str(k): v for k, v in tuned.items()}, "config": args.config,
+                       "tuned_on": f"scan_index {TUNE_SCAN_OFFSET} (+rank) of config {args.config}"},
+                      open(args.save_t, "w"), indent=1)
 
     # ---- warm-up ------------------------------------------------------------------------
     for _ in range(max(args.warmup, 3)):
@@ -437,10 +454,16 @@ def main():
 
 
 def load_t(path):
-    """{map_key: t} from the config.dataflow_t of a bench JSON line (last line of the file)."""
+    """{map_key: t} from a --save-t file, or from config.dataflow_t of a bench JSON line
+    (last line of the file)."""
     import ast
-    line = [ln for ln in open(path).read().splitlines() if ln.startswith("{")][-1]
-    return {ast.literal_eval(k): int(v) for k, v in json.loads(line)["config"]["dataflow_t"].items()}
+    txt = open(path).read()
+    try:
+        d = json.loads(txt)
+    except json.JSONDecodeError:
+        d = json.loads([ln for ln in txt.splitlines() if ln.startswith("{")][-1])
+    dt = d["dataflow_t"] if "dataflow_t" in d else d["config"]["dataflow_t"]
+    return {ast.literal_eval(k): int(v) for k, v in dt.items()}
 
 
 def conv_traffic(config, n_voxels):

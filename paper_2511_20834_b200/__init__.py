@@ -324,6 +324,18 @@ class KernelMap:
                 self._view(self.c.os_table_ord, n * kd, torch.int32).view(n, kd),
                 self._view(self.c.tile_mask_ord, tiles * w, torch.int32).view(tiles, w))
 
+    def tile_order(self):
+        """Heaviest-first OS tile orders of a density-ordered map, else None:
+        (order128 [ceil(n/128)], order256 [ceil(n/256)], weight128, weight256) over the
+        capacity n_out (spc.h: 128-row tiles by descending popcount of their ordered tile
+        mask, then 256-row tiles likewise; then the weights in those two orders)."""
+        if not self.c.tile_order:
+            return None
+        t128 = (self.c.n_out + 127) // 128
+        t256 = (self.c.n_out + 255) // 256
+        v = self._view(self.c.tile_order, 4 * t128, torch.int32).view(4, t128)
+        return v[0], v[1, :t256], v[2], v[3, :t256]
+
     def counts(self) -> torch.Tensor:
         return self._view(self.c.counts_dev, 2 * SPC_MAX_KVOL, torch.int32)
 

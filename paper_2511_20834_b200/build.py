@@ -14,8 +14,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libspc.so")
-SOURCES = ["spc_host.cu", "spc_sort.cu", "spc_kmap.cu", "spc_conv.cu"]
-HEADERS = ["spc_common.cuh", "spc_ptx.cuh"]
+SOURCES = ["spc_host.cu", "spc_sort.cu", "spc_kmap.cu", "spc_conv.cu", "spc_dense.cu"]
+HEADERS = ["spc_common.cuh", "spc_ptx.cuh", "spc_tile.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=default", "--expt-relaxed-constexpr"]

@@ -26,6 +26,7 @@
 
 #include "spc_common.cuh"
 #include "spc_ptx.cuh"
+#include "spc_tile.cuh"
 
 namespace spc {
 
@@ -37,7 +38,6 @@ constexpr int WS_CTR_SLOTS = 2048;                // ws counters (int32) after t
 constexpr int CTR_EXIT = WS_CTR_SLOTS - 2, CTR_FETCH = WS_CTR_SLOTS - 1;   // split tiles use [0, 1024)
 constexpr int SPLIT_MAX_TILES = 512;              // weighted split: tiles per launch (x n_ntiles <= 2)
 
-enum OutKind : int { OUT_FINAL = 0, OUT_F32_STORE = 1, OUT_F32_RED = 2 };
 
 struct ConvParams {
     int mode;   // 0 = OS part, 1 = WS part
@@ -53,6 +53,7 @@ struct ConvParams {
     int64_t list_stride;
     const int32_t *counts;   // [2*SPC_MAX_KVOL]
     int n_lists;
+    int skip_list;        // WS: a list computed elsewhere (the submanifold centre by the dense kernel), or -1
     int k_vol;
     int64_t n_out_cap;
     const int64_t *n_out_dev;
@@ -185,68 +186,6 @@ __device__ __forceinline__ int next_bit(const uint32_t (&m)[4], int from) {
     return -1;
 }
 
-__device__ __forceinline__ float to_f(uint32_t u) { return __uint_as_float(u); }
-
-__device__ __forceinline__ uint32_t pack2(float a, float b, int dt) {
-    if (dt == SPC_BF16) {
-        __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-        return *reinterpret_cast<uint32_t *>(&h);
-    }
-    __half2 h = __floats2half2_rn(a, b);
-    return *reinterpret_cast<uint32_t *>(&h);
-}
-__device__ __forceinline__ float2 unpack2(uint32_t u, int dt) {
-    if (dt == SPC_BF16) return __bfloat1622float2(*reinterpret_cast<__nv_bfloat162 *>(&u));
-    return __half22float2(*reinterpret_cast<__half2 *>(&u));
-}
-
-// store 'n' (16 or 32) fp32 values of one row to the output (fully unrolled: registers only)
-__device__ __forceinline__ void store_row(const ConvParams &p, int64_t row, int col, const uint32_t (&v)[32], int n) {
-    if (p.out_kind == OUT_FINAL && p.out_dtype != SPC_F32) {
-        const uint4 *rp = p.residual
-                              ? reinterpret_cast<const uint4 *>(static_cast<const uint16_t *>(p.residual) + row * p.ld_res + col)
-                              : nullptr;
-        uint4 *op = reinterpret_cast<uint4 *>(static_cast<uint16_t *>(p.out) + row * p.ld_out + col);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            if (q * 8 < n) {
-                float f[8];
-#pragma unroll
-                for (int e = 0; e < 8; ++e) f[e] = to_f(v[q * 8 + e]);
-                if (rp) {
-                    const uint4 u = rp[q];
-                    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const float2 r2 = unpack2(w[e], p.out_dtype);
-                        f[2 * e] += r2.x;
-                        f[2 * e + 1] += r2.y;
-                    }
-                }
-                op[q] = make_uint4(pack2(f[0], f[1], p.out_dtype), pack2(f[2], f[3], p.out_dtype),
-                                   pack2(f[4], f[5], p.out_dtype), pack2(f[6], f[7], p.out_dtype));
-            }
-        }
-    } else {
-        float *op = static_cast<float *>(p.out) + row * p.ld_out + col;
-        const float *rp = (p.out_kind == OUT_FINAL && p.residual)
-                              ? static_cast<const float *>(p.residual) + row * p.ld_res + col
-                              : nullptr;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            if (q * 4 < n) {
-                float4 o = make_float4(to_f(v[4 * q]), to_f(v[4 * q + 1]), to_f(v[4 * q + 2]), to_f(v[4 * q + 3]));
-                if (rp) {
-                    const float4 r = reinterpret_cast<const float4 *>(rp)[q];
-                    o.x += r.x; o.y += r.y; o.z += r.z; o.w += r.w;
-                }
-                reinterpret_cast<float4 *>(op)[q] = o;
-            }
-        }
-    }
-}
-
-
 // ---- shared-memory records produced by the scheduler warp ------------------------------
 constexpr int TREC_SLOTS = 4;      // tile records in flight
 constexpr int BLK_SLOTS = 2;       // per-tile gather-index blocks in flight
@@ -265,7 +204,7 @@ struct ConvSmem {
     uint64_t full[16], empty[16], tfull[2], tempty[2];
     uint64_t trec_full[TREC_SLOTS], trec_empty[TREC_SLOTS];
     uint64_t blk_full[BLK_SLOTS], blk_empty[BLK_SLOTS];
-    int started;                   // tiles the gather warps have begun (claim gate; ld/st.volatile.shared)
+    int started;                   // tiles the gather warps have begun (claim gate; shared atomics only)
     uint32_t tmem_holder[4];
     int tr, wsplit;                // device-chosen tile rows / weighted OS split active
     int n_sp;                      // tiles in the weighted split
@@ -388,10 +327,12 @@ __device__ __forceinline__ void gather_slices(const ConvParams &p, const TileRec
             const int r = warp * ROWS_W + b * RPI + r_in;
             const uint32_t f = rb == 128 ? (r & 7) : (rb == 64 ? ((r >> 1) & 3) : ((r >> 2) & 1));
             const uint32_t so = kbo + (uint32_t)r * rb + ((q_lane ^ f) * 16);
-            if (g[b] >= 0)
-                ptx::cp_async_16(abase + so, p.f_in + (int64_t)g[b] * p.ld_in_bytes + cc * rb + q_lane * 16, 16u);
-            else
-                asm volatile("st.shared.v4.b32 [%0], {%1,%1,%1,%1};" ::"r"(abase + so), "r"(0) : "memory");
+            // sentinel rows (no input voxel): src-size 0 zero-fills the segment without
+            // reading global memory; every write of the A ring goes through cp.async, so its
+            // completion is tracked by the stage's mbarrier alone
+            const bool hit = g[b] >= 0;
+            ptx::cp_async_16(abase + so, p.f_in + (hit ? (int64_t)g[b] * p.ld_in_bytes + cc * rb + q_lane * 16 : 0),
+                             hit ? 16u : 0u);
         }
     }
 }
@@ -412,7 +353,7 @@ __device__ __forceinline__ void gather_role(const ConvParams &p, ConvSmem &cs, c
         ptx::mbar_wait(ptx::smem_u32(&cs.trec_full[st]), (ti / TREC_SLOTS) & 1);
         const TileRec &R = cs.trec[st];
         if (R.end) break;
-        if (warp == 0 && lane == 0) ptx::sts_volatile_s32(ptx::smem_u32(&cs.started), (int)ti + 1);
+        if (warp == 0 && lane == 0) atomicMax(&cs.started, (int)ti + 1);   // shared atomic: an ordered flag
         const int rows = R.rows, ncols = R.ncols;
         const int bs = ti % p.blk_slots;
         ptx::mbar_wait(ptx::smem_u32(&cs.blk_full[bs]), (ti / p.blk_slots) & 1);
@@ -612,7 +553,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                 for (int base = 0; base < p.n_lists; base += 32) {
                     const int l = base + lane;
                     int v = 0;
-                    if (l < p.n_lists) {
+                    if (l < p.n_lists && l != p.skip_list) {
                         const int cnt = p.counts[SPC_MAX_KVOL + l];
                         v = ((cnt + tr - 1) / tr) * (p.list_mirror[l] ? 2 : 1);
                     }
@@ -720,7 +661,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                 {
                     const int need = (int)ti + 1 - p.claim_ahead;
                     uint32_t ns = 32;
-                    while (ptx::lds_volatile_s32(ptx::smem_u32(&cs.started)) < need) {
+                    while (atomicAdd(&cs.started, 0) < need) {
                         __nanosleep(ns);
                         if (ns < 256) ns <<= 1;
                     }
@@ -1114,6 +1055,10 @@ static uint32_t pow2_cols(int n) {
 
 static size_t elem_size(int dt) { return dt == SPC_F32 ? 4 : 2; }
 
+spc_status dense_forward(const void *f_in, int64_t ld_in, int in_dtype, int c_in, const void *wblob, int k, int c_out,
+                         int BK, int BN, int64_t n_cap, const int64_t *n_dev, void *out, int64_t ld_out, int out_kind,
+                         int out_dtype, const void *residual, int64_t ld_res, cudaStream_t st);   // spc_dense.cu
+
 }  // namespace spc
 
 using namespace spc;
@@ -1337,6 +1282,15 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
     p.acc = wacc;
     p.ld_acc = c_out;
     p.tile_ctr = wctr;
+    p.skip_list = -1;
+    // A11: identity maps need no gather.  A K = 1 submanifold layer is one dense TMA-fed
+    // GEMM; the centre of an all-weight-stationary submanifold map (always
+    // matched, out_i += F_i W_centre) is computed the same way and INITIALISES the fp32
+    // accumulator, replacing its pair list and the zero fill
+    const bool subm = km->geom.stride == 1 && !km->geom.transposed;
+    if (subm && km->k_vol == 1 && km->k_dense == 1)
+        return dense_forward(f_in, ld_in, in_dtype, c_in, weight, 0, c_out, p.BK, p.BN, km->n_out, km->n_out_dev, f_out,
+                             ld_out, OUT_FINAL, out_dtype, residual, ld_res, st);
     if (!has_ws) {
         // OS only: one launch; small levels split offsets over CTAs with the in-kernel fixup
         p.split_ok = (wacc && km->k_dense >= 4 && option(SPC_OPT_CONV_OS_SPLIT) != 0) ? 1 : 0;
@@ -1344,8 +1298,16 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
     }
     p.split_ok = 0;
     if (!acc) return fail(SPC_ERR_WORKSPACE, "spc_conv_forward: ws too small");
+    const int centre = (km->k_vol - 1) / 2;
+    if (!has_os && subm && km->k_vol > 1)
+        for (int l = 0; l < km->n_lists; ++l)
+            if (km->list_k[l] == centre) p.skip_list = l;
     if (has_os) {
         spc_status s = launch_tc(p, 0, OUT_F32_STORE, acc, ld_acc, st);
+        if (s != SPC_OK) return s;
+    } else if (p.skip_list >= 0) {
+        spc_status s = dense_forward(f_in, ld_in, in_dtype, c_in, weight, centre, c_out, p.BK, p.BN, km->n_out,
+                                     km->n_out_dev, acc, ld_acc, OUT_F32_STORE, SPC_F32, nullptr, 0, st);
         if (s != SPC_OK) return s;
     } else if (acc == f_out) {
         SPC_CUDA(launch_pdl(k_zero_rows, dim3(1024), dim3(256), 0, st, acc, ld_acc, km->n_out, km->n_out_dev, (int)c_out));

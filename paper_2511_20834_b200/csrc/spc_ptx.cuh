@@ -15,17 +15,6 @@ __device__ __forceinline__ int32_t lds_s32(uint32_t addr) {
     return v;
 }
 
-// volatile shared-space load / store (a flag polled across warps of one CTA; the explicit
-// .shared space keeps it an LDS, not a generic LD.E.STRONG.SYS)
-__device__ __forceinline__ int32_t lds_volatile_s32(uint32_t addr) {
-    int32_t v;
-    asm volatile("ld.volatile.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
-    return v;
-}
-__device__ __forceinline__ void sts_volatile_s32(uint32_t addr, int32_t v) {
-    asm volatile("st.volatile.shared.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
-}
-
 // ---- mbarrier ------------------------------------------------------------------------
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
@@ -100,6 +89,17 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                  "l"(src), "r"(bytes), "r"(bar)
                  : "memory");
+}
+
+// TMA 2-D tile load (cp.async.bulk.tensor): box at coordinates (c0 inner, c1 outer) of the
+// tensor map into shared memory in the map's swizzled layout; out-of-range elements are
+// zero-filled; completion counted (bytes) on an mbarrier
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const void *tmap, int c0, int c1, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            dst),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(bar)
+        : "memory");
 }
 
 // TMA row gather: 4 rows (row indices r0..r3, out-of-range -> zero fill) x box columns

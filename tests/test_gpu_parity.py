@@ -429,3 +429,34 @@ def test_full_size_c2_sampled_parity():
     rows = np.random.default_rng(0).choice(len(c), 2048, replace=False)
     ref = oracle.conv_rows(c, c, rows, 3, 1, F, W)
     assert _rel_err(out.cpu().numpy()[rows].astype(np.float64), ref) <= 2e-3
+
+
+@pytest.mark.parametrize("c_in,c_out,dt,res,n_cut", [(16, 32, "bf16", False, 5000), (48, 96, "bf16", True, 4097),
+                                                      (128, 64, "f16", True, 6000), (96, 384, "bf16", False, 3001),
+                                                      (384, 256, "bf16", True, 2500)])
+def test_dense_tma_k1(c_in, c_out, dt, res, n_cut):
+    """A11: a K = 1 submanifold layer runs as one dense TMA-fed tcgen05 GEMM (no gather):
+    BK 16/32/64 (32B/64B/128B swizzle), C_out tiled (384 = 2 x 192), ragged row tails,
+    fused residual, bf16/f16 output within one ulp of the fp64 reference."""
+    coords = synth.make_scan(1, 0)[:n_cut]
+    spec = _spec_for(coords)
+    keys, _, _ = _pack_sort(coords, spec)
+    c = oracle.sort_coords(coords)[0]
+    km = spc.spc_build_kmap(keys, keys, spec, spc.Geom(1, 1, 1, 1, 0), -1, 0)
+    tdt = torch.bfloat16 if dt == "bf16" else torch.float16
+    F = synth.make_features(len(c), c_in, seed=c_in, dtype=dt)
+    W = synth.make_weights(1, c_in, c_out, seed=c_out, nnz_per_out=1, dtype=dt)
+    R = synth.make_features(len(c), c_out, seed=3, dtype=dt) if res else None
+    big = torch.zeros(len(c), c_in + 16, dtype=tdt, device=DEV)      # read a column slice (ld_in > c_in)
+    big[:, 16:] = torch.from_numpy(F).to(DEV).to(tdt)
+    out = spc.spc_conv_forward(km, big[:, 16:], spc.spc_prepare_weight(torch.from_numpy(W).to(DEV).to(tdt)), c_in,
+                               c_out, out_dtype=tdt,
+                               residual=None if R is None else torch.from_numpy(R).to(DEV).to(tdt))
+    torch.cuda.synchronize()
+    ref = F.astype(np.float64) @ W[0].astype(np.float64)
+    if R is not None:
+        ref = ref + R.astype(np.float64)
+    got = out.float().cpu().numpy().astype(np.float64)
+    mant = 7 if dt == "bf16" else 10
+    ulp = np.exp2(np.floor(np.log2(np.maximum(np.abs(ref), 1e-30))) - mant)
+    assert (np.abs(got - ref) <= ulp + 1e-5 * np.abs(ref).max()).all()

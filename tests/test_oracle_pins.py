@@ -328,3 +328,39 @@ def test_conv_special_cases():
     np.testing.assert_allclose(oracle.conv(c, c, 3, 1, 2.5 * F, W), 2.5 * a, rtol=1e-12, atol=1e-12)
     rows = np.array([0, 5, len(c) - 1])
     np.testing.assert_allclose(oracle.conv_rows(c, c, rows, 3, 1, F, W), a[rows], rtol=1e-13, atol=1e-13)
+
+
+@pytest.mark.parametrize("K", [3, 5])
+def test_conv_dilated_off_lattice_vs_conv3d(K):
+    """Dilation d = 2 on coordinates that are NOT on a 2-lattice (VERDICT r1 pin gap):
+    submanifold = conv3d(dilation=2, padding=2r); strided = conv3d(stride=2, dilation=2)
+    at the Eq. (1) sites; transposed = conv_transpose3d(stride=2, dilation=2)."""
+    d = 2
+    rng = np.random.default_rng(40 + K)
+    c = oracle.sort_coords(synth.random_cloud(160, 8, seed=50 + K, signed=False))[0]
+    r = (K - 1) // 2
+    F = rng.uniform(-1, 1, (len(c), 4))
+    W = rng.uniform(-1, 1, (K ** 3, 4, 3))
+    g = _grid(c, 4, F, (0, 0, 0), (8, 8, 8))
+    # submanifold, spacing = tensor stride 1 x dilation 2
+    got = oracle.conv(c, c, K, d, F, W)
+    y = torch.nn.functional.conv3d(g, _dense_weight(W, K), padding=r * d, dilation=d)
+    ref = np.stack([y[0, :, x, yy, z].numpy() for _, x, yy, z in c.tolist()])
+    np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-12)
+    # strided
+    coarse = oracle.downsample(c, 2)
+    got_s = oracle.conv(c, coarse, K, d, F, W)
+    ys = torch.nn.functional.conv3d(g, _dense_weight(W, K), stride=2, padding=r * d, dilation=d)
+    ref_s = np.stack([ys[0, :, x // 2, yy // 2, z // 2].numpy() for _, x, yy, z in coarse.tolist()])
+    np.testing.assert_allclose(got_s, ref_s, rtol=1e-12, atol=1e-12)
+    # transposed (same weight index as the strided layer)
+    Fc = rng.uniform(-1, 1, (len(coarse), 4))
+    got_t = oracle.conv(coarse, c, K, d, Fc, W, transposed=True)
+    gc = torch.zeros((1, 4, 4, 4, 4), dtype=torch.float64)
+    for rr, (_, x, yy, z) in enumerate(coarse.tolist()):
+        gc[0, :, x // 2, yy // 2, z // 2] = torch.from_numpy(Fc[rr])
+    wt = torch.from_numpy(W.reshape(K, K, K, 4, 3)).permute(3, 4, 0, 1, 2).contiguous()
+    yt = torch.nn.functional.conv_transpose3d(gc, wt, stride=2, padding=r * d, dilation=d,
+                                              output_padding=8 - (3 * 2 - 2 * r * d + d * (K - 1) + 1))
+    ref_t = np.stack([yt[0, :, x, yy, z].numpy() for _, x, yy, z in c.tolist()])
+    np.testing.assert_allclose(got_t, ref_t, rtol=1e-12, atol=1e-12)
