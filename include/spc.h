@@ -74,7 +74,9 @@ typedef enum {
     SPC_OPT_PDL = 6,              /* 1 (default): programmatic dependent launches               */
     SPC_OPT_KMAP_POOL_KEYS = 7,   /* test hook: shared window pool of the z-delta build in keys
                                    * (default 4096; smaller forces the global-memory fallback)    */
-    SPC_OPT_COUNT = 8
+    SPC_OPT_CONV_DENSE_CENTRE = 8, /* 1: the centre of an all-WS submanifold map runs as a dense
+                                   * TMA-fed GEMM that initialises the accumulator (default 0)    */
+    SPC_OPT_COUNT = 9
 } spc_option;
 spc_status spc_set_option(int32_t option, int64_t value);
 int64_t spc_get_option(int32_t option);
@@ -329,6 +331,25 @@ spc_status spc_network_kmaps(const uint64_t *v0_keys, int64_t n0, const int64_t 
                              const int32_t *t_host, const uint32_t *flags_host, int32_t n_maps,
                              uint64_t *level_keys_out, int64_t *level_n_dev, spc_kmap *maps_out_host,
                              uint32_t *status, void *ws, size_t ws_bytes, void *stream);
+
+/* ================================================================================
+ * Multi-GPU, one large scene: output-key ranges with input halos
+ *
+ * Shard r of n_shards owns the sorted outputs [out_lo, out_hi) = [r*n/R, (r+1)*n/R)
+ * (n = *n_out_dev or n_out) and needs only the inputs
+ *     [in_lo, in_hi) = [lb(out[out_lo] + d_min), lb(out[out_hi-1] + d_max + 1))
+ * where d_min / d_max are the smallest / largest packed query offsets of the map (
+ * negated for a transposed map): the keys are sorted lexicographically, so every match
+ * of the shard's outputs lies in this ONE contiguous halo range.  A shard's
+ * map is then spc_build_kmap(in_keys + in_lo, in_hi - in_lo, out_keys + out_lo,
+ * out_hi - out_lo, ...) and its features spc_conv_forward on F_in + in_lo rows into
+ * F_out + out_lo rows; the shards' maps (indices shifted back) are exactly the
+ * single-device map.  Kernel maps never cross GPUs.
+ * bounds_dev: device int64 [n_shards][4] = (out_lo, out_hi, in_lo, in_hi).
+ * ================================================================================ */
+spc_status spc_shard_ranges(const uint64_t *in_keys, int64_t n_in, const int64_t *n_in_dev, const uint64_t *out_keys,
+                            int64_t n_out, const int64_t *n_out_dev, spc_pack_spec spec, spc_geom geom,
+                            int32_t n_shards, int64_t *bounds_dev, void *stream);
 
 #ifdef __cplusplus
 }

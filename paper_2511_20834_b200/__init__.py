@@ -15,7 +15,7 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("SPC_LIB_OVERRIDE") or os.path.join(_HERE, "libspc.so")   # override: experiments only
+LIB_PATH = os.path.join(_HERE, "libspc.so")
 
 SPC_OK = 0
 SPC_F32, SPC_F16, SPC_BF16 = 0, 1, 2
@@ -31,6 +31,7 @@ SPC_MAX_KVOL = 125
 # spc_option
 SPC_OPT_CONV_TILE_ROWS, SPC_OPT_CONV_STAGE_KB, SPC_OPT_CONV_OS_SPLIT, SPC_OPT_CONV_SPLIT_MIN = 0, 1, 2, 3
 SPC_OPT_CONV_CLAIM_AHEAD, SPC_OPT_CONV_DENSITY_ORDER, SPC_OPT_PDL, SPC_OPT_KMAP_POOL_KEYS = 4, 5, 6, 7
+SPC_OPT_CONV_DENSE_CENTRE = 8
 
 _DT = {torch.float32: SPC_F32, torch.float16: SPC_F16, torch.bfloat16: SPC_BF16}
 _TORCH_DT = {v: k for k, v in _DT.items()}
@@ -124,6 +125,7 @@ def lib():
             "spc_conv_forward": ([ctypes.POINTER(_Kmap), P, I64, I32, I32, P, I32, P, I64, I32, P, I64, P, SZ, P],
                                  ctypes.c_int),
             "spc_network_workspace_size": ([I64, I32, P, P, P, I32], SZ),
+            "spc_shard_ranges": ([P, I64, P, P, I64, P, PackSpec, Geom, I32, P, P], ctypes.c_int),
             "spc_network_kmaps": ([P, I64, P, PackSpec, I32, P, P, P, I32, P, P, P, P, P, SZ, P], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
@@ -469,3 +471,18 @@ def spc_network_kmaps(v0_keys: torch.Tensor, spec: PackSpec, n_levels: int, geom
     for m in maps:
         m._keep = m._keep + (ni,)
     return ni.level_keys, ni.level_n, maps
+
+
+# ---------------------------------------------------------------------------------------
+# multi-GPU, one large scene: output ranges + input halos
+# ---------------------------------------------------------------------------------------
+
+def spc_shard_ranges(in_keys: torch.Tensor, out_keys: torch.Tensor, spec: PackSpec, geom: Geom, n_shards: int,
+                     n_in_dev=None, n_out_dev=None, stream=None) -> torch.Tensor:
+    """-> device int64 [n_shards, 4]: (out_lo, out_hi, in_lo, in_hi) per shard (spc.h)."""
+    b = _alloc((int(n_shards), 4), torch.int64, in_keys.device, stream)
+    _check(lib().spc_shard_ranges(_ptr(in_keys), in_keys.shape[0], _ptr(n_in_dev), _ptr(out_keys), out_keys.shape[0],
+                                  _ptr(n_out_dev), spec, geom, int(n_shards), _ptr(b), _stream(stream)),
+           "spc_shard_ranges")
+    return b
+

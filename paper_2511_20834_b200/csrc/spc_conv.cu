@@ -327,12 +327,12 @@ __device__ __forceinline__ void gather_slices(const ConvParams &p, const TileRec
             const int r = warp * ROWS_W + b * RPI + r_in;
             const uint32_t f = rb == 128 ? (r & 7) : (rb == 64 ? ((r >> 1) & 3) : ((r >> 2) & 1));
             const uint32_t so = kbo + (uint32_t)r * rb + ((q_lane ^ f) * 16);
-            // sentinel rows (no input voxel): src-size 0 zero-fills the segment without
-            // reading global memory; every write of the A ring goes through cp.async, so its
-            // completion is tracked by the stage's mbarrier alone
-            const bool hit = g[b] >= 0;
-            ptx::cp_async_16(abase + so, p.f_in + (hit ? (int64_t)g[b] * p.ld_in_bytes + cc * rb + q_lane * 16 : 0),
-                             hit ? 16u : 0u);
+            // sentinel rows (no input voxel) never touch L2: a shared store of zeros
+            // (measured faster than a src-size-0 cp.async zero fill on the level-0 layers)
+            if (g[b] >= 0)
+                ptx::cp_async_16(abase + so, p.f_in + (int64_t)g[b] * p.ld_in_bytes + cc * rb + q_lane * 16, 16u);
+            else
+                asm volatile("st.shared.v4.b32 [%0], {%1,%1,%1,%1};" ::"r"(abase + so), "r"(0) : "memory");
         }
     }
 }
@@ -364,6 +364,9 @@ __device__ __forceinline__ void gather_role(const ConvParams &p, ConvSmem &cs, c
             ptx::mbar_wait(ptx::smem_u32(&cs.empty[s]), ph ^ 1);
             gather_slices<BK, NBT>(p, R, ptx::smem_u32(B), kd, rows, sl, nin, ptx::smem_u32(sa + (size_t)s * a_bytes), kb_a,
                                    warp, r_in, q_lane);
+            // the zero rows were written through the generic proxy: order them before the
+            // tensor core's async-proxy reads, then arrive once this thread's copies land
+            ptx::fence_proxy_async();
             ptx::cp_async_mbar_arrive(ptx::smem_u32(&cs.full[s]));
             if (++s == S) { s = 0; ph ^= 1; }
         }
@@ -1284,9 +1287,11 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
     p.tile_ctr = wctr;
     p.skip_list = -1;
     // A11: identity maps need no gather.  A K = 1 submanifold layer is one dense TMA-fed
-    // GEMM; the centre of an all-weight-stationary submanifold map (always
-    // matched, out_i += F_i W_centre) is computed the same way and INITIALISES the fp32
-    // accumulator, replacing its pair list and the zero fill
+    // GEMM; with SPC_OPT_CONV_DENSE_CENTRE the centre of an all-weight-stationary
+    // submanifold map (always matched, out_i += F_i W_centre) is computed the same
+    // way and INITIALISES the fp32 accumulator, replacing its pair list and the zero fill
+    // (off by default: on C2's small deep levels the extra launch costs more than the
+    // centre list's scatter)
     const bool subm = km->geom.stride == 1 && !km->geom.transposed;
     if (subm && km->k_vol == 1 && km->k_dense == 1)
         return dense_forward(f_in, ld_in, in_dtype, c_in, weight, 0, c_out, p.BK, p.BN, km->n_out, km->n_out_dev, f_out,
@@ -1299,7 +1304,7 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
     p.split_ok = 0;
     if (!acc) return fail(SPC_ERR_WORKSPACE, "spc_conv_forward: ws too small");
     const int centre = (km->k_vol - 1) / 2;
-    if (!has_os && subm && km->k_vol > 1)
+    if (!has_os && subm && km->k_vol > 1 && option(SPC_OPT_CONV_DENSE_CENTRE) != 0)
         for (int l = 0; l < km->n_lists; ++l)
             if (km->list_k[l] == centre) p.skip_list = l;
     if (has_os) {

@@ -1112,6 +1112,50 @@ spc_status kmap_defer_end(cudaStream_t st) {
 }
 }  // namespace spc
 
+// ------------------------------------------------------------------------------------
+// multi-GPU range sharding of one scene: per shard the output range and its input halo
+// ------------------------------------------------------------------------------------
+namespace spc {
+__global__ void k_shard_ranges(const uint64_t *__restrict__ in, int64_t n_in_cap, const int64_t *n_in_dev,
+                               const uint64_t *__restrict__ out, int64_t n_out_cap, const int64_t *n_out_dev,
+                               int64_t d_min, int64_t d_max, int n_shards, int64_t *__restrict__ bounds) {
+    pdl_wait();
+    pdl_trigger();
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n_shards) return;
+    const int64_t n_in = dev_count(n_in_cap, n_in_dev), n_out = dev_count(n_out_cap, n_out_dev);
+    const int64_t lo = n_out * r / n_shards, hi = n_out * (r + 1) / n_shards;
+    int64_t ilo = 0, ihi = 0;
+    if (hi > lo) {
+        ilo = lower_bound_g(in, n_in, out[lo] + (uint64_t)d_min);
+        ihi = lower_bound_g(in, n_in, out[hi - 1] + (uint64_t)d_max + 1ull);
+    }
+    bounds[4 * r] = lo;
+    bounds[4 * r + 1] = hi;
+    bounds[4 * r + 2] = ilo;
+    bounds[4 * r + 3] = ihi > ilo ? ihi : ilo;
+}
+}  // namespace spc
+
+extern "C" spc_status spc_shard_ranges(const uint64_t *in_keys, int64_t n_in, const int64_t *n_in_dev,
+                                       const uint64_t *out_keys, int64_t n_out, const int64_t *n_out_dev,
+                                       spc_pack_spec spec, spc_geom geom, int32_t n_shards, int64_t *bounds_dev,
+                                       void *stream) {
+    SPC_CHECK_ARG(n_shards >= 1 && bounds_dev && n_in >= 0 && n_out >= 0, "bad shard arguments");
+    SPC_CHECK_ARG((in_keys || n_in == 0) && (out_keys || n_out == 0), "null keys");
+    KmapPlan pl;
+    spc_status s = make_plan(geom, SPC_T_ALL_OS, 0, pl);
+    if (s != SPC_OK) return s;
+    // packed query offsets of the map: +-delta per axis, delta = e * spacing, e in [-r, r];
+    // the set is symmetric, so a transposed map (negated queries) has the same extremes
+    const int64_t ext = (int64_t)pl.r * pl.spacing;
+    const int64_t d_max = ext * (1ll << (spec.bits_y + spec.bits_z)) + ext * (1ll << spec.bits_z) + ext;
+    SPC_CUDA(launch_pdl(k_shard_ranges, dim3((n_shards + 127) / 128), dim3(128), 0, as_stream(stream), in_keys, n_in,
+                        n_in_dev, out_keys, n_out, n_out_dev, -d_max, d_max, (int)n_shards, bounds_dev));
+    SPC_LAUNCH_CHECK("k_shard_ranges");
+    return SPC_OK;
+}
+
 extern "C" spc_status spc_kmap_export(const spc_kmap *km, int32_t *triples_host, int64_t cap, int64_t *nnz_host,
                                       void *stream) {
     SPC_CHECK_ARG(km && nnz_host, "null pointer");

@@ -460,3 +460,32 @@ def test_dense_tma_k1(c_in, c_out, dt, res, n_cut):
     mant = 7 if dt == "bf16" else 10
     ulp = np.exp2(np.floor(np.log2(np.maximum(np.abs(ref), 1e-30))) - mant)
     assert (np.abs(got - ref) <= ulp + 1e-5 * np.abs(ref).max()).all()
+
+
+@pytest.mark.parametrize("c_in,c_out,K,halve", [(32, 32, 3, 1), (256, 256, 3, 1), (64, 96, 5, 1), (32, 64, 3, 0)])
+def test_dense_centre_initialises_ws_accumulator(c_in, c_out, K, halve):
+    """SPC_OPT_CONV_DENSE_CENTRE: the centre of an all-WS submanifold map as the dense
+    TMA GEMM that initialises the fp32 accumulator; the WS lists add the rest."""
+    coords = synth.make_scan(1, 0)[:5000]
+    spec = _spec_for(coords)
+    keys, _, _ = _pack_sort(coords, spec)
+    c = oracle.sort_coords(coords)[0]
+    km = spc.spc_build_kmap(keys, keys, spec, spc.Geom(K, 1, 1, 1, 0), 0, halve)
+    F = synth.make_features(len(c), c_in, seed=c_in)
+    W = synth.make_weights(K ** 3, c_in, c_out, seed=c_out, nnz_per_out=10)
+    R = synth.make_features(len(c), c_out, seed=4)
+    Wg = spc.spc_prepare_weight(torch.from_numpy(W).to(DEV).bfloat16())
+    try:
+        spc.spc_set_option(spc.SPC_OPT_CONV_DENSE_CENTRE, 1)
+        o32 = spc.spc_conv_forward(km, torch.from_numpy(F).to(DEV).bfloat16(), Wg, c_in, c_out, out_dtype=torch.float32)
+        o16 = spc.spc_conv_forward(km, torch.from_numpy(F).to(DEV).bfloat16(), Wg, c_in, c_out,
+                                   out_dtype=torch.bfloat16, residual=torch.from_numpy(R).to(DEV).bfloat16())
+        torch.cuda.synchronize()
+    finally:
+        spc.spc_set_option(spc.SPC_OPT_CONV_DENSE_CENTRE, -1)
+    ref = oracle.conv(c, c, K, 1, F, W)
+    assert _rel_err(o32.cpu().numpy().astype(np.float64), ref) <= 2e-3
+    ref16 = ref + R.astype(np.float64)
+    got = o16.float().cpu().numpy().astype(np.float64)
+    ulp = np.exp2(np.floor(np.log2(np.maximum(np.abs(ref16), 1e-30))) - 7)
+    assert (np.abs(got - ref16) <= ulp + 1e-5 * np.abs(ref16).max()).all()

@@ -1,0 +1,68 @@
+"""Output-range sharding of one scene, emulated on one GPU: for R in
+{2, 3, 4} ranks, every rank's map (outputs [out_lo, out_hi) against the input halo
+[in_lo, in_hi) from spc_shard_ranges) with its indices shifted back is exactly its slice
+of the single-device map, the shards' maps together ARE the single-device map
+(bit-exact), and the concatenated shard features match the oracle's Eq. (2)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+import paper_2511_20834_b200 as spc
+from paper_2511_20834_b200.distributed import range_shard_plan, shard_conv, shard_out_ranges
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def _keys(c, spec):
+    return torch.from_numpy(oracle.pack(c, spec.astuple())[0].view(np.int64)).to(DEV)
+
+
+@pytest.mark.parametrize("R", [2, 3, 4])
+@pytest.mark.parametrize("kind,K,t,flags", [("subm", 3, -1, 8), ("subm", 3, 2, 1), ("subm", 5, 3, 9),
+                                            ("strided", 3, -1, 0), ("transposed", 3, 0, 0), ("subm_d2", 3, -1, 0)])
+def test_range_sharded_map_and_conv(R, kind, K, t, flags):
+    coords = synth.make_scan(1, 1)
+    spec = spc.spc_plan_pack(coords[:, 1:].min(0), coords[:, 1:].max(0), 1, 16, 16)
+    fine = oracle.sort_coords(coords)[0]
+    coarse = oracle.downsample(fine, 2)
+    d = 2 if kind == "subm_d2" else 1
+    if kind.startswith("subm"):
+        ic, oc, g = fine, fine, spc.Geom(K, 1, d, 1, 0)
+    elif kind == "strided":
+        ic, oc, g = fine, coarse, spc.Geom(K, 2, 1, 1, 0)
+    else:
+        ic, oc, g = coarse, fine, spc.Geom(K, 2, 1, 1, 1)
+    ik, ok = _keys(ic, spec), _keys(oc, spec)
+    plan = range_shard_plan(ik, ok, spec, g, R)
+    assert [(a, b) for a, b, _, _ in plan] == shard_out_ranges(len(oc), R)
+    full = spc.spc_kmap_export(spc.spc_build_kmap(ik, ok, spec, g, t, flags))
+    ref = oracle.kmap(ic, oc, K, d, transposed=(kind == "transposed"))
+    np.testing.assert_array_equal(full, ref)
+    c_in, c_out = 32, 48
+    F = synth.make_features(len(ic), c_in, seed=9)
+    W = synth.make_weights(K ** 3, c_in, c_out, seed=10, nnz_per_out=10)
+    Fg = torch.from_numpy(F).to(DEV).bfloat16()
+    Wg = spc.spc_prepare_weight(torch.from_numpy(W).to(DEV).bfloat16())
+    parts, outs = [], []
+    for b in plan:
+        out_lo, out_hi, in_lo, in_hi = b
+        assert 0 <= in_lo <= in_hi <= len(ic)
+        rows, km = shard_conv(b, ik, ok, spec, g, t, flags, Fg, Wg, c_in, c_out, out_dtype=torch.float32)
+        tr = spc.spc_kmap_export(km).astype(np.int64)
+        tr[:, 1] += out_lo
+        tr[:, 2] += in_lo
+        parts.append(tr)
+        outs.append(rows.cpu().numpy())
+        # a shard's map is exactly the single-device map's rows of its outputs
+        sel = (full[:, 1] >= out_lo) & (full[:, 1] < out_hi)
+        srt = tr[np.lexsort((tr[:, 2], tr[:, 1], tr[:, 0]))]
+        np.testing.assert_array_equal(srt, full[sel])
+    allp = np.concatenate(parts)
+    allp = allp[np.lexsort((allp[:, 2], allp[:, 1], allp[:, 0]))]
+    np.testing.assert_array_equal(allp, full)
+    got = np.concatenate(outs).astype(np.float64)
+    refF = oracle.conv(ic, oc, K, d, F, W, transposed=(kind == "transposed"))
+    assert np.abs(got - refF).max() <= 2e-3 * np.abs(refF).max()
