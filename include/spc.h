@@ -81,6 +81,17 @@ typedef enum {
 spc_status spc_set_option(int32_t option, int64_t value);
 int64_t spc_get_option(int32_t option);
 
+/* Device-side event trace of the feature kernels (observability; off by default).
+ * buf: device uint64 [1 + 2*cap]; buf[0] counts records (the caller zeroes it), record i
+ * = (buf[1+2i] = %globaltimer ns, buf[2+2i] = launch << 48 | event << 40 | cta << 24 | aux).
+ * Events: 0 CTA entry, 1 after the PDL wait, 2 setup done, 3 tile record published,
+ * 4 first stage of a tile full, 5 tile's MMAs committed, 6 tile's epilogue done, 7 CTA
+ * exit (aux = tile sequence number of the CTA where it applies).  Launches are numbered
+ * from 0 after every spc_set_trace call; spc_trace_launch_desc(launch) names one.
+ * buf = NULL turns tracing off.  Captured CUDA graphs keep the buffer they saw. */
+spc_status spc_set_trace(void *buf, int64_t cap);
+const char *spc_trace_launch_desc(int32_t launch);
+
 /* ================================================================================
  * A1  Packed keys (§5.3)
  *

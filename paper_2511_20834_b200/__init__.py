@@ -107,6 +107,8 @@ def lib():
             "spc_kmap_struct_bytes": ([], SZ),
             "spc_set_option": ([I32, I64], ctypes.c_int),
             "spc_get_option": ([I32], I64),
+            "spc_set_trace": ([P, I64], ctypes.c_int),
+            "spc_trace_launch_desc": ([I32], ctypes.c_char_p),
             "spc_plan_pack": ([P, P, I32, I32, I32, ctypes.POINTER(PackSpec)], ctypes.c_int),
             "spc_pack_offset": ([PackSpec, I32, I32, I32], I64),
             "spc_downsample_mask": ([PackSpec, I32], ctypes.c_uint64),
@@ -185,6 +187,33 @@ def spc_set_option(option: int, value: int):
 
 def spc_get_option(option: int) -> int:
     return int(lib().spc_get_option(int(option)))
+
+
+def spc_set_trace(buf: torch.Tensor | None):
+    """Device event trace of the feature kernels (spc.h): buf int64 [1 + 2*cap] (zero buf[0]
+    before a traced pass), or None to turn tracing off."""
+    cap = 0 if buf is None else (buf.numel() - 1) // 2
+    _check(lib().spc_set_trace(_ptr(buf), cap), "spc_set_trace")
+
+
+def spc_trace_records(buf: torch.Tensor):
+    """[sync] -> numpy structured records (t_ns, launch, event, cta, aux) of a trace buffer."""
+    h = buf.cpu().numpy().view(np.uint64)
+    n = int(min(h[0], (h.size - 1) // 2))
+    r = h[1:1 + 2 * n].reshape(n, 2)
+    info = r[:, 1]
+    out = np.zeros(n, dtype=[("t", np.int64), ("launch", np.int32), ("event", np.int32), ("cta", np.int32),
+                             ("aux", np.int32)])
+    out["t"] = r[:, 0].astype(np.int64)
+    out["launch"] = (info >> np.uint64(48)).astype(np.int32)
+    out["event"] = ((info >> np.uint64(40)) & np.uint64(0xff)).astype(np.int32)
+    out["cta"] = ((info >> np.uint64(24)) & np.uint64(0xffff)).astype(np.int32)
+    out["aux"] = (info & np.uint64(0xffffff)).astype(np.int32)
+    return out
+
+
+def spc_trace_launch_desc(launch: int) -> str:
+    return lib().spc_trace_launch_desc(int(launch)).decode()
 
 
 # ---------------------------------------------------------------------------------------

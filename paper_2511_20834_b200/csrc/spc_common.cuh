@@ -98,6 +98,26 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 // PDL: let the next kernel in the stream begin its prologue
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// device-side event trace (spc_set_trace): null buffer = off
+struct Trace {
+    unsigned long long *buf;
+    int64_t cap;
+    uint32_t launch;
+};
+__device__ __forceinline__ void trace_event(const Trace &t, int ev, uint32_t aux) {
+    if (!t.buf) return;
+    unsigned long long ts;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts));
+    const unsigned long long i = atomicAdd(t.buf, 1ull);
+    if ((int64_t)i < t.cap) {
+        t.buf[1 + 2 * i] = ts;
+        t.buf[2 + 2 * i] = ((unsigned long long)t.launch << 48) | ((unsigned long long)ev << 40) |
+                           ((unsigned long long)(blockIdx.x & 0xffff) << 24) | (aux & 0xffffffu);
+    }
+}
+// host: the trace descriptor for the next launch (launch numbered, described for the log)
+Trace trace_next(const std::string &desc);
+
 __device__ __forceinline__ int64_t dev_count(int64_t cap, const int64_t *n_dev) {
     if (!n_dev) return cap;
     int64_t n = *n_dev;

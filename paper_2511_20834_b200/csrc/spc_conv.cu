@@ -98,6 +98,7 @@ struct ConvParams {
     int16_t dense_k[SPC_MAX_KVOL];
     int16_t list_k[SPC_MAX_KVOL];
     int8_t list_mirror[SPC_MAX_KVOL];
+    Trace trace;          // device event trace (spc_set_trace), buf NULL = off
 };
 
 struct TileInfo {
@@ -431,6 +432,7 @@ __device__ __forceinline__ void epi_role(const ConvParams &p, ConvSmem &cs, uint
         }
         ptx::tc_fence_before();
         __syncwarp();
+        if (threadIdx.x == 32 * W_EPI0) trace_event(p.trace, 6, ti);
         if (lane == 0) {
             if (!fix) ptx::mbar_arrive(ptx::smem_u32(&cs.tempty[a]));   // (the fixup released it already)
             ptx::mbar_arrive(ptx::smem_u32(&cs.trec_empty[st]));
@@ -520,12 +522,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         cs.started = 0;
         ptx::fence_mbar_init();
         ptx::fence_proxy_async();
+        trace_event(p.trace, 0, 0);
     }
     if (warp == W_MMA) ptx::tmem_alloc(ptx::smem_u32(cs.tmem_holder), p.tbufs * NH * p.tmem_cols);
     // everything above overlaps the previous kernel's tail (PDL); maps, features, weights
     // and outputs are touched only after this point
     pdl_wait();
     pdl_trigger();
+    if (threadIdx.x == 0) trace_event(p.trace, 1, 0);
     const int64_t n_out = dev_count(p.n_out_cap, p.n_out_dev);
     if (warp == W_SCHED) {
         // tile geometry from the live (device-side) counts, no host sync: 256-row tiles
@@ -587,6 +591,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = cs.tmem_holder[0];
+    if (threadIdx.x == 0) trace_event(p.trace, 2, 0);
     constexpr uint32_t rb = BK * 2;           // bytes per operand row (= swizzle span)
     const int tr = cs.tr, wsplit = cs.wsplit, nht = tr / TC_BM;
     // the ring carve of this tile height
@@ -760,6 +765,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                     if (q * 32 < tr) R.scatter[q * 32 + lane] = sc[q];
             }
             ptx::mbar_arrive(ptx::smem_u32(&cs.trec_full[st]));
+            if (lane == 0) trace_event(p.trace, 3, ti);
         }
         ptx::cp_async_wait<0>();
     } else if (warp < N_GATHER) {
@@ -828,6 +834,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                 const int nin = min(nkb_u, nsl - sl);
                 const int s = it % S_u;
                 ptx::mbar_wait(ptx::smem_u32(&cs.full[s]), (it / S_u) & 1);
+                if (sl == 0 && lane == 0) trace_event(p.trace, 4, ti);
                 ptx::fence_proxy_async();
                 ptx::tc_fence_after();
                 // descriptors built once per stage; the K / row-half / slice steps add to
@@ -848,6 +855,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                 ptx::mma_commit_elect(ptx::smem_u32(&cs.empty[s]));
             }
             ptx::mma_commit_elect(ptx::smem_u32(&cs.tfull[a]));
+            if (lane == 0) trace_event(p.trace, 5, ti);
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&cs.trec_empty[st]));
         }
@@ -864,6 +872,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem_base, p.tbufs * NH * p.tmem_cols);
     }
+    if (threadIdx.x == 0) trace_event(p.trace, 7, 0);
     if (p.tile_ctr && threadIdx.x == 0) {
         // the last CTA out returns the fetch / exit counters to zero (ws contract); every
         // CTA's scheduler has made its final claim before its CTA gets here
@@ -1168,6 +1177,9 @@ static spc_status launch_tc(const ConvParams &p0, int mode, int out_kind, void *
                                               (p.split_ok ? std::max(1, p.k_dense / 2) : 1)
                                         : (int64_t)num_sms();
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles_cap, num_sms()));
+    p.trace = trace_next(std::string("k_conv_tc ") + (mode == 0 ? "os" : "ws") + " n_out=" + std::to_string(p.n_out_cap) +
+                         " c_in=" + std::to_string(p.n_chunks * p.BK) + " c_out=" + std::to_string(p.n_ntiles * p.BN) +
+                         " k_dense=" + std::to_string(p.k_dense) + " lists=" + std::to_string(p.n_lists));
     void (*k)(ConvParams) = p.bm == 256 ? (p.BK == 64 ? k_conv_tc<64, 256> : p.BK == 32 ? k_conv_tc<32, 256> : k_conv_tc<16, 256>)
                                         : (p.BK == 64 ? k_conv_tc<64, 128> : p.BK == 32 ? k_conv_tc<32, 128> : k_conv_tc<16, 128>);
     SPC_CUDA(launch_pdl(k, dim3(grid), dim3(TC_THREADS), smem, st, p));

@@ -47,6 +47,7 @@ struct DenseParams {
     int out_dtype;
     const void *residual;
     int64_t ld_res;
+    Trace trace;
 };
 
 struct DenseSmem {
@@ -71,11 +72,13 @@ __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_tc(const __grid_constan
         }
         ptx::fence_mbar_init();
         ptx::prefetch_tmap(&p.tmap_a);
+        trace_event(p.trace, 0, 0);
     }
     if (warp == 1) ptx::tmem_alloc(ptx::smem_u32(ds.tmem_holder), 2 * p.tmem_cols);
     // barrier init and TMEM allocation overlap the previous kernel's tail (PDL)
     pdl_wait();
     pdl_trigger();
+    if (threadIdx.x == 0) trace_event(p.trace, 1, 0);
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
@@ -153,6 +156,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_tc(const __grid_constan
     }
     ptx::tc_fence_before();
     __syncthreads();
+    if (threadIdx.x == 0) trace_event(p.trace, 7, 0);
     if (warp == 1) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem_base, 2 * p.tmem_cols);
@@ -237,6 +241,8 @@ spc_status dense_forward(const void *f_in, int64_t ld_in, int in_dtype, int c_in
     }
     const int64_t tiles_cap = ((n_cap + DN_BM - 1) / DN_BM) * p.n_ntiles;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles_cap, num_sms()));
+    p.trace = trace_next("k_dense_tc n=" + std::to_string(n_cap) + " c_in=" + std::to_string(c_in) +
+                         " c_out=" + std::to_string(c_out) + " k=" + std::to_string(k));
     SPC_CUDA(launch_pdl(k_dense_tc, dim3(grid), dim3(DN_THREADS), smem, st, p));
     SPC_LAUNCH_CHECK("k_dense_tc");
     return SPC_OK;

@@ -28,6 +28,19 @@ spc_status cuda_fail(cudaError_t e, const char *what) {
 static const int64_t kOptDefault[SPC_OPT_COUNT] = {0, 72, 1, 2, 1, 1, 1, 4096, 0};
 static int64_t g_opt[SPC_OPT_COUNT] = {0, 72, 1, 2, 1, 1, 1, 4096, 0};
 
+static unsigned long long *g_trace_buf = nullptr;
+static int64_t g_trace_cap = 0;
+static std::vector<std::string> g_trace_desc;
+
+Trace trace_next(const std::string &desc) {
+    Trace t{g_trace_buf, g_trace_cap, 0};
+    if (g_trace_buf) {
+        t.launch = (uint32_t)g_trace_desc.size();
+        g_trace_desc.push_back(desc);
+    }
+    return t;
+}
+
 int64_t option(int o) { return (o >= 0 && o < SPC_OPT_COUNT) ? g_opt[o] : 0; }
 
 bool pdl_enabled() { return g_opt[SPC_OPT_PDL] != 0; }
@@ -94,6 +107,19 @@ extern "C" spc_status spc_set_option(int32_t o, int64_t value) {
 }
 
 extern "C" int64_t spc_get_option(int32_t o) { return option(o); }
+
+extern "C" spc_status spc_set_trace(void *buf, int64_t cap) {
+    SPC_CHECK_ARG(cap >= 0, "cap < 0");
+    g_trace_buf = static_cast<unsigned long long *>(buf);
+    g_trace_cap = buf ? cap : 0;
+    g_trace_desc.clear();
+    return SPC_OK;
+}
+
+extern "C" const char *spc_trace_launch_desc(int32_t launch) {
+    if (launch < 0 || launch >= (int32_t)g_trace_desc.size()) return "";
+    return g_trace_desc[launch].c_str();
+}
 
 extern "C" spc_status spc_plan_pack(const int32_t lo[3], const int32_t hi[3], int32_t n_batch,
                                     int32_t max_out_stride, int32_t max_reach, spc_pack_spec *out) {
