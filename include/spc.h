@@ -199,7 +199,8 @@ typedef struct {
 #define SPC_T_ALL_OS (-1)
 #define SPC_T_ALL_WS 0
 
-#define SPC_KMAP_HALVE_SYMMETRIC 0x1u /* submanifold: store WS pairs of k < centre only */
+#define SPC_KMAP_HALVE_SYMMETRIC 0x1u /* submanifold: store WS pairs of k < centre only;
+                                       * needs in_keys == out_keys (else SPC_ERR_INVALID_ARG)   */
 #define SPC_KMAP_CHECK_SORTED 0x2u    /* debug: flag unsorted / duplicate input keys          */
 #define SPC_KMAP_COUNT_SEARCHES 0x4u  /* debug: count binary searches and scan probes        */
 #define SPC_KMAP_DENSITY_ORDER 0x8u   /* OS part: also build a density-ordered copy of the OS

@@ -1304,7 +1304,9 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
     // way and INITIALISES the fp32 accumulator, replacing its pair list and the zero fill
     // (off by default: on C2's small deep levels the extra launch costs more than the
     // centre list's scatter)
-    const bool subm = km->geom.stride == 1 && !km->geom.transposed;
+    // identity centre: one coordinate set in and out (not a range shard of one)
+    const bool subm = km->geom.stride == 1 && !km->geom.transposed && km->in_keys == km->out_keys &&
+                      km->n_in == km->n_out && km->n_in_dev == km->n_out_dev;
     if (subm && km->k_vol == 1 && km->k_dense == 1)
         return dense_forward(f_in, ld_in, in_dtype, c_in, weight, 0, c_out, p.BK, p.BN, km->n_out, km->n_out_dev, f_out,
                              ld_out, OUT_FINAL, out_dtype, residual, ld_res, st);

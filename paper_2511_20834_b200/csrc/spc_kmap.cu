@@ -943,6 +943,11 @@ extern "C" spc_status spc_build_kmap(const uint64_t *in_keys, int64_t n_in, cons
     SPC_CHECK_ARG(n_in >= 0 && n_out >= 0, "negative size");
     SPC_CHECK_ARG(n_in < INT32_MAX && n_out < INT32_MAX, "sizes must fit int32 indices");
     SPC_CHECK_ARG((in_keys || n_in == 0) && (out_keys || n_out == 0), "null keys");
+    // symmetric halving needs ONE coordinate set: the same key array as input
+    // and output (a range shard of a submanifold layer has different in / out index spaces)
+    if ((flags & SPC_KMAP_HALVE_SYMMETRIC) && geom.stride == 1 && !geom.transposed &&
+        (in_keys != out_keys || n_in != n_out || n_in_dev != n_out_dev))
+        return fail(SPC_ERR_INVALID_ARG, "spc_build_kmap: SPC_KMAP_HALVE_SYMMETRIC needs in_keys == out_keys");
     KmapPlan pl;
     spc_status s = make_plan(geom, t, flags, pl);
     if (s != SPC_OK) return s;

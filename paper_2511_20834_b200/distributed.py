@@ -76,6 +76,8 @@ def shard_conv(bounds, in_keys, out_keys, spec, geom, t, flags, f_in, weight_pre
     halo [in_lo, in_hi) and its features.  Returns (rows [out_hi - out_lo, c_out], map)."""
     import paper_2511_20834_b200 as spc
     out_lo, out_hi, in_lo, in_hi = bounds
+    # a shard's input and output index spaces differ: no symmetric halving (it needs one set)
+    flags = int(flags) & ~spc.SPC_KMAP_HALVE_SYMMETRIC
     km = spc.spc_build_kmap(in_keys[in_lo:in_hi], out_keys[out_lo:out_hi], spec, geom, t, flags, stream=stream)
     out = spc.spc_conv_forward(km, f_in[in_lo:in_hi], weight_prepared, c_in, c_out, out_dtype=out_dtype,
                                stream=stream)

@@ -59,7 +59,10 @@ else:
         g.replay()
 torch.cuda.synchronize()
 rec = spc.spc_trace_records(buf)
+descs = {L: spc.spc_trace_launch_desc(L) for L in set(rec["launch"].tolist())}
 spc.spc_set_trace(None)
+if a.out:
+    np.save(a.out.replace(".json", "_raw.npy"), rec)
 t0 = rec["t"].min()
 launches = sorted(set(rec["launch"].tolist()))
 rows = []
@@ -77,7 +80,7 @@ for L in launches:
     med, end = float(np.median(ends)), float(ends.max())
     tiles = len(ev(6))
     gap = (start - prev_end) if prev_end is not None else 0
-    d = spc.spc_trace_launch_desc(L)
+    d = descs[L]
     rows.append((L, start, gap, wait, setup, rec0, full0, med, end, len(ends), tiles, d))
     print(f"{L:6d} {start/1e3:8.1f} {gap/1e3:6.1f} {(wait-start)/1e3:6.1f} {(setup-wait)/1e3:6.1f} {(rec0-setup)/1e3:6.1f} "
           f"{(full0-setup)/1e3:6.1f} {(med-start)/1e3:7.1f} {(end-start)/1e3:7.1f} {len(ends):5d} {tiles:5d}  {d}")
@@ -88,6 +91,7 @@ print(f"traced span {tot:.1f} us; sum of launch spans {busy:.1f} us; sum of med-
       f"{sum((r[7] - r[1]) for r in rows) / 1e3:.1f} us")
 if a.out:
     import json
+    json.dump({"descs": {int(k): v for k, v in descs.items()}}, open(a.out.replace(".json", "_descs.json"), "w"))
     json.dump([dict(zip(["launch", "start", "gap", "wait", "setup", "rec0", "full0", "med", "end", "ctas", "tiles",
                          "desc"], [int(x) if isinstance(x, (np.integer,)) else (float(x) if not isinstance(x, str) else x)
                                    for x in row])) for row in rows], open(a.out, "w"), indent=0)
