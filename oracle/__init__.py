@@ -31,22 +31,40 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "spc_oracle.c")
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_LIB_OMP_PATH = os.path.join(_HERE, "liboracle_omp.so")
 _lib = None
+_use_omp = False
 
 
 def build(force: bool = False) -> str:
-    """Compile the oracle with gcc (plain C11, -O2, no OpenMP)."""
-    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < max(
-            os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "spc_oracle.h"))):
+    """Compile the oracle with gcc: liboracle.so (plain C11, -O2, single-threaded, what the
+    parity tests use) and liboracle_omp.so (the same source with -fopenmp: Eq. (2) output
+    rows spread over the host cores, for timing the CPU baseline)."""
+    dep = max(os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "spc_oracle.h")))
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < dep:
         subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", _SRC, "-o", _LIB_PATH])
+    if force or not os.path.exists(_LIB_OMP_PATH) or os.path.getmtime(_LIB_OMP_PATH) < dep:
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-fopenmp", _SRC, "-o", _LIB_OMP_PATH])
     return _LIB_PATH
+
+
+def use_openmp(on: bool = True):
+    """Route later calls to the OpenMP build (bench.py's cpu_baseline / reference arm)."""
+    global _use_omp, _lib
+    if bool(on) != _use_omp:
+        _use_omp = bool(on)
+        _lib = None
+
+
+def num_threads() -> int:
+    return int(_L().orc_num_threads())
 
 
 def _L():
     global _lib
     if _lib is None:
         build()
-        lib = ctypes.CDLL(_LIB_PATH)
+        lib = ctypes.CDLL(_LIB_OMP_PATH if _use_omp else _LIB_PATH)
         P = ctypes.c_void_p
         I64 = ctypes.c_int64
         I = ctypes.c_int
@@ -66,6 +84,8 @@ def _L():
         lib.orc_conv.restype = I64
         lib.orc_conv_rows.argtypes = [P, I64, P, P, I64, I, I, I, P, I, P, I, P]
         lib.orc_conv_rows.restype = I64
+        lib.orc_num_threads.argtypes = []
+        lib.orc_num_threads.restype = ctypes.c_int
         _lib = lib
     return _lib
 

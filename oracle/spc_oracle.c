@@ -240,8 +240,12 @@ int64_t orc_conv(const int32_t *in_coords, int64_t n_in, const int32_t *out_coor
     int64_t nnz = 0;
     int32_t t[4];
     if (order == 0) { /* output-stationary: each output row finished before the next */
+        /* rows are independent (each row's sum runs in the same order either way): the
+         * OpenMP build (liboracle_omp.so) spreads them over the host cores */
+#pragma omp parallel for reduction(+ : nnz) schedule(dynamic, 64)
         for (int64_t i = 0; i < n_out; ++i)
             for (int k = 0; k < kv; ++k) {
+                int32_t t[4];
                 make_query(out_coords + 4 * i, off + 3 * k, transposed, t);
                 int64_t j = hash_find(&h, t);
                 if (j < 0) continue;
@@ -276,9 +280,10 @@ int64_t orc_conv_rows(const int32_t *in_coords, int64_t n_in, const int32_t *out
     if (hash_build(&h, in_coords, n_in)) { free(off); return -1; }
     memset(F_out, 0, sizeof(double) * (size_t)n_rows * (size_t)c_out);
     int64_t nnz = 0;
-    int32_t t[4];
+#pragma omp parallel for reduction(+ : nnz) schedule(dynamic, 64)
     for (int64_t r = 0; r < n_rows; ++r)
         for (int k = 0; k < kv; ++k) {
+            int32_t t[4];
             make_query(out_coords + 4 * rows[r], off + 3 * k, transposed, t);
             int64_t j = hash_find(&h, t);
             if (j < 0) continue;
@@ -290,3 +295,10 @@ int64_t orc_conv_rows(const int32_t *in_coords, int64_t n_in, const int32_t *out
     free(off);
     return nnz;
 }
+
+#ifdef _OPENMP
+#include <omp.h>
+int orc_num_threads(void) { return omp_get_max_threads(); }
+#else
+int orc_num_threads(void) { return 1; }
+#endif

@@ -70,6 +70,10 @@ int64_t orc_conv_rows(const int32_t *in_coords, int64_t n_in, const int32_t *out
                       const int64_t *rows, int64_t n_rows, int K, int spacing, int transposed,
                       const double *F_in, int c_in, const double *W, int c_out, double *F_out);
 
+/* Threads the Eq. (2) row loops use: 1 in the plain build (liboracle.so), the OpenMP
+ * thread count in liboracle_omp.so (same arithmetic per row, rows in parallel). */
+int orc_num_threads(void);
+
 #ifdef __cplusplus
 }
 #endif

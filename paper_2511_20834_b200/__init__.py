@@ -387,12 +387,15 @@ def spc_kmap_bytes(geom: Geom, t: int, flags: int, n_in: int, n_out: int) -> int
 
 def spc_build_kmap(in_keys: torch.Tensor, out_keys: torch.Tensor, spec: PackSpec, geom: Geom,
                    t: int = SPC_T_ALL_OS, flags: int = 0, n_in_dev=None, n_out_dev=None, status=None,
-                   stream=None) -> KernelMap:
+                   stream=None, buf: torch.Tensor | None = None) -> KernelMap:
+    """``buf``: optional pre-allocated uint8 buffer (>= spc_kmap_bytes + 256 bytes), so a
+    build can be re-issued (and graph-captured) without allocating."""
     n_in, n_out = in_keys.shape[0], out_keys.shape[0]
     nbytes = spc_kmap_bytes(geom, t, flags, n_in, n_out)
     if nbytes == 0:
         raise SpcError(f"spc_kmap_bytes: unsupported geometry {geom!r}")
-    buf = _alloc(nbytes + 256, torch.uint8, in_keys.device, stream)
+    if buf is None or buf.numel() < nbytes + 256:
+        buf = _alloc(nbytes + 256, torch.uint8, in_keys.device, stream)
     off = (-buf.data_ptr()) % 256
     buf = buf[off:off + nbytes]
     km = _Kmap()

@@ -287,6 +287,28 @@ class SparseNet:
         return out
 
 
+    def index_algorithmic_bytes(self) -> dict:
+        """SURVEY 8(d) algorithmic bytes of the indexing phase of one pass (call after
+        algorithmic_flops()): pack + sort 16 B in + 12 B out per voxel; each downsampled
+        level 8 B read per input voxel + 8 B per unique output; each distinct kernel map
+        8 N_in + 8 N_out (keys) + 4 N_out K_dense (OS table) + 8 per stored WS pair + 4 K^3."""
+        n0 = int(self.level_n[0].item())
+        ln = [int(v) for v in self.level_n.cpu().tolist()]
+        out = {"pack_sort": 28.0 * n0, "downsample": float(sum(8 * n0 + 8 * m for m in ln[1:]))}
+        maps = 0.0
+        for mk, km in self.maps.items():
+            n_in, n_out = self.live_n[mk]
+            cnt = km.counts().cpu().numpy()
+            pairs = int(cnt[spc.SPC_MAX_KVOL:spc.SPC_MAX_KVOL + km.n_lists].sum())
+            maps += 8 * n_in + 8 * n_out + 4 * n_out * km.k_dense + 8 * pairs + 4 * km.k_vol
+        out["kernel_maps"] = maps
+        return out
+
+    def nnz_per_out(self) -> dict:
+        """Matches per output voxel of every distinct map (call after algorithmic_flops())."""
+        return {mk: self.nnz[mk] / max(1, self.live_n[mk][1]) for mk in self.maps}
+
+
 class SparseUNet(SparseNet):
     """MinkUNet-42 (configs C2, C4)."""
 

@@ -364,3 +364,20 @@ def test_conv_dilated_off_lattice_vs_conv3d(K):
                                               output_padding=8 - (3 * 2 - 2 * r * d + d * (K - 1) + 1))
     ref_t = np.stack([yt[0, :, x, yy, z].numpy() for _, x, yy, z in c.tolist()])
     np.testing.assert_allclose(got_t, ref_t, rtol=1e-12, atol=1e-12)
+
+
+def test_openmp_build_is_bit_identical():
+    """The OpenMP oracle build (cpu_baseline timing) computes every Eq. (2) row in the same
+    order as the plain build: results are bit-identical."""
+    rng = np.random.default_rng(5)
+    c = oracle.sort_coords(synth.surface_cloud(3000, seed=4))[0]
+    F = rng.uniform(-1, 1, (len(c), 16))
+    W = rng.uniform(-1, 1, (27, 16, 8))
+    rows = rng.choice(len(c), 500, replace=False)
+    a, ar = oracle.conv(c, c, 3, 1, F, W), oracle.conv_rows(c, c, rows, 3, 1, F, W)
+    try:
+        oracle.use_openmp(True)
+        b, br = oracle.conv(c, c, 3, 1, F, W), oracle.conv_rows(c, c, rows, 3, 1, F, W)
+    finally:
+        oracle.use_openmp(False)
+    assert np.array_equal(a, b) and np.array_equal(ar, br)
