@@ -76,7 +76,9 @@ typedef enum {
                                    * (default 4096; smaller forces the global-memory fallback)    */
     SPC_OPT_CONV_DENSE_CENTRE = 8, /* 1: the centre of an all-WS submanifold map runs as a dense
                                    * TMA-fed GEMM that initialises the accumulator (default 0)    */
-    SPC_OPT_COUNT = 9
+    SPC_OPT_CONV_CTA_PAIR = 9,    /* CTA pairs (cta_group::2, M = 256) for outputs >= 192 wide:
+                                   * 0 off, 1 auto (default), 2 wherever the shape allows       */
+    SPC_OPT_COUNT = 10
 } spc_option;
 spc_status spc_set_option(int32_t option, int64_t value);
 int64_t spc_get_option(int32_t option);

@@ -84,6 +84,8 @@ struct ConvParams {
     int *tile_ctr;        // ws counters (zero on entry, left zero): [0, 1024) split-tile arrivals,
                           // [CTR_EXIT] CTAs exited, [CTR_FETCH] dynamic tile fetch
     int blk_slots;        // gather-index blocks in flight (2, or 1 when a block is large: K=5 OS)
+    int cg;               // 2: CTA pairs (cta_group::2, M = 256 per MMA, each CTA holds half of every
+                          //    weight tile and 128 of the pair tile's 256 rows); 1: single CTAs
     uint32_t tmem_cols;   // per 128-row accumulator (power of two >= 32)
     int tbufs;            // accumulator buffers per CTA: 2 (epilogue overlaps the next tile's MMAs)
                           // or 1 (256-row tiles of N = 256: 2 x 256 columns fill TMEM)
@@ -205,6 +207,8 @@ struct ConvSmem {
     uint64_t full[16], empty[16], tfull[2], tempty[2];
     uint64_t trec_full[TREC_SLOTS], trec_empty[TREC_SLOTS];
     uint64_t blk_full[BLK_SLOTS], blk_empty[BLK_SLOTS];
+    uint64_t claim_full[TREC_SLOTS], claim_empty[TREC_SLOTS];   // CTA pair: the leader's tile claims
+    int64_t claim_v[TREC_SLOTS];                                 //   forwarded to the peer
     int started;                   // tiles the gather warps have begun (claim gate; shared atomics only)
     uint32_t tmem_holder[4];
     int tr, wsplit;                // device-chosen tile rows / weighted OS split active
@@ -354,7 +358,7 @@ __device__ __forceinline__ void gather_role(const ConvParams &p, ConvSmem &cs, c
         ptx::mbar_wait(ptx::smem_u32(&cs.trec_full[st]), (ti / TREC_SLOTS) & 1);
         const TileRec &R = cs.trec[st];
         if (R.end) break;
-        if (warp == 0 && lane == 0) atomicMax(&cs.started, (int)ti + 1);   // shared atomic: an ordered flag
+        if (warp == 0 && lane == 0) ptx::red_max_shared(ptx::smem_u32(&cs.started), (int)ti + 1);   // ordered flag
         const int rows = R.rows, ncols = R.ncols;
         const int bs = ti % p.blk_slots;
         ptx::mbar_wait(ptx::smem_u32(&cs.blk_full[bs]), (ti / p.blk_slots) & 1);
@@ -363,10 +367,13 @@ __device__ __forceinline__ void gather_role(const ConvParams &p, ConvSmem &cs, c
         for (int sl = 0; sl < nsl; sl += nkb) {
             const int nin = min(nkb, nsl - sl);
             ptx::mbar_wait(ptx::smem_u32(&cs.empty[s]), ph ^ 1);
+            const bool fine = p.trace.buf && blockIdx.x < 2 && warp == 0 && lane == 0;   // per-stage trace (CTAs 0, 1)
+            if (fine) trace_event(p.trace, 8, sl);
             gather_slices<BK, NBT>(p, R, ptx::smem_u32(B), kd, rows, sl, nin, ptx::smem_u32(sa + (size_t)s * a_bytes), kb_a,
                                    warp, r_in, q_lane);
             // the zero rows were written through the generic proxy: order them before the
             // tensor core's async-proxy reads, then arrive once this thread's copies land
+            if (fine) trace_event(p.trace, 9, sl);
             ptx::fence_proxy_async();
             ptx::cp_async_mbar_arrive(ptx::smem_u32(&cs.full[s]));
             if (++s == S) { s = 0; ph ^= 1; }
@@ -385,7 +392,7 @@ __device__ __forceinline__ void gather_role(const ConvParams &p, ConvSmem &cs, c
 // FIX: OS split tiles go through the split-K fixup instead
 template <bool FIX>
 __device__ __forceinline__ void epi_role(const ConvParams &p, ConvSmem &cs, uint32_t tmem_base, int tr, int nht,
-                                         int NH, int warp, int lane) {
+                                         int NH, int warp, int lane, int pair_rank) {
     const int e = warp - W_EPI0;   // == warp % 4: the TMEM lane quadrant this warp may access
     for (uint32_t ti = 0;; ++ti) {
         const int st = ti % TREC_SLOTS;
@@ -434,7 +441,10 @@ __device__ __forceinline__ void epi_role(const ConvParams &p, ConvSmem &cs, uint
         __syncwarp();
         if (threadIdx.x == 32 * W_EPI0) trace_event(p.trace, 6, ti);
         if (lane == 0) {
-            if (!fix) ptx::mbar_arrive(ptx::smem_u32(&cs.tempty[a]));   // (the fixup released it already)
+            // the accumulator is free again: a CTA pair's MMAs are issued by the leader, so
+            // the peer releases the leader's barrier
+            if (pair_rank == 1) ptx::mbar_arrive_remote_relaxed(ptx::mapa(ptx::smem_u32(&cs.tempty[a]), 0));
+            else if (!fix) ptx::mbar_arrive(ptx::smem_u32(&cs.tempty[a]));   // (the fixup released it already)
             ptx::mbar_arrive(ptx::smem_u32(&cs.trec_empty[st]));
         }
     }
@@ -485,9 +495,10 @@ __device__ __forceinline__ void convert_items(float *__restrict__ acc, int64_t l
     }
 }
 
-template <int BK, int BM>
+template <int BK, int BM, int CG>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant__ ConvParams p) {
-    constexpr int NH = BM / TC_BM;   // 128-row MMA halves per tile
+    constexpr int NH = BM / TC_BM;   // 128-row MMA halves per tile (per CTA)
+    static_assert(CG == 1 || BM == TC_BM, "a CTA of a pair holds 128 rows");
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // stage buffers need 1024-byte alignment (swizzle atoms)
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -501,15 +512,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     const int blk_stride = (BM * kd + 3) & ~3;      // int32 per block (16-byte multiple)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // CTA pair (cta_group::2): rank 0 issues the MMAs of both CTAs; rank 1 forwards its
+    // stage completions and accumulator releases to rank 0's barriers
+    const uint32_t rank = CG == 2 ? ptx::cluster_ctarank() : 0u;
+    const bool leader = rank == 0;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < 16; ++s) {
-            ptx::mbar_init(ptx::smem_u32(&cs.full[s]), N_GATHER * 32 + 1);   // gather threads + weight expect_tx
+            // gather threads + weight expect_tx (+ the peer's forwarded stage on a pair's leader)
+            ptx::mbar_init(ptx::smem_u32(&cs.full[s]), N_GATHER * 32 + 1 + (CG == 2 && leader ? 1 : 0));
             ptx::mbar_init(ptx::smem_u32(&cs.empty[s]), 1);
         }
         for (int a = 0; a < 2; ++a) {
             ptx::mbar_init(ptx::smem_u32(&cs.tfull[a]), 1);
-            ptx::mbar_init(ptx::smem_u32(&cs.tempty[a]), 4);
+            ptx::mbar_init(ptx::smem_u32(&cs.tempty[a]), 4 + (CG == 2 && leader ? 4 : 0));
         }
         for (int i = 0; i < TREC_SLOTS; ++i) {
             ptx::mbar_init(ptx::smem_u32(&cs.trec_full[i]), 32);
@@ -519,12 +535,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             ptx::mbar_init(ptx::smem_u32(&cs.blk_full[i]), 32);
             ptx::mbar_init(ptx::smem_u32(&cs.blk_empty[i]), N_GATHER);
         }
+        for (int i = 0; i < TREC_SLOTS; ++i) {
+            ptx::mbar_init(ptx::smem_u32(&cs.claim_full[i]), 1);
+            ptx::mbar_init(ptx::smem_u32(&cs.claim_empty[i]), 1);
+        }
         cs.started = 0;
         ptx::fence_mbar_init();
         ptx::fence_proxy_async();
         trace_event(p.trace, 0, 0);
     }
-    if (warp == W_MMA) ptx::tmem_alloc(ptx::smem_u32(cs.tmem_holder), p.tbufs * NH * p.tmem_cols);
+    if (warp == W_MMA) {
+        if constexpr (CG == 2) ptx::tmem_alloc2(ptx::smem_u32(cs.tmem_holder), p.tbufs * NH * p.tmem_cols);
+        else ptx::tmem_alloc(ptx::smem_u32(cs.tmem_holder), p.tbufs * NH * p.tmem_cols);
+    }
+    // a pair's barriers are initialised before either CTA signals the other's
+    if constexpr (CG == 2) ptx::cluster_sync();
     // everything above overlaps the previous kernel's tail (PDL); maps, features, weights
     // and outputs are touched only after this point
     pdl_wait();
@@ -537,15 +562,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         // with fewer 128-row tiles than SMs splits each tile's offsets over CTAs
         // (split-K, reduced in the epilogue fixup below)
         if (p.mode == 0) {
-            int tr = BM;
-            if (BM == 256 && ((n_out + 255) / 256) * p.n_ntiles < 2 * p.num_sms) tr = 128;
-            if (p.force_tr) tr = min(p.force_tr, BM);
+            int tr = CG == 2 ? 256 : BM;   // a pair's tile: 256 rows, 128 per CTA
+            if (CG == 1 && BM == 256 && ((n_out + 255) / 256) * p.n_ntiles < 2 * p.num_sms) tr = 128;
+            if (CG == 1 && p.force_tr) tr = min(p.force_tr, BM);
             const int64_t rt = (n_out + tr - 1) / tr;
             // weighted split-K for small launches (parts computed by the scheduler role)
             // (only when tiles leave at least half the SMs idle: the parts' fp32 reductions
             // land in one burst at the end of the launch and cost more than mild imbalance)
-            const bool wsplit = p.split_ok && p.k_dense >= 4 && 2 * rt * p.n_ntiles <= p.split_tiles_per_sm2 &&
-                                rt <= SPLIT_MAX_TILES && p.n_ntiles <= 2;
+            const bool wsplit = CG == 1 && p.split_ok && p.k_dense >= 4 &&
+                                2 * rt * p.n_ntiles <= p.split_tiles_per_sm2 && rt <= SPLIT_MAX_TILES &&
+                                p.n_ntiles <= 2;
             const int64_t units = rt;
             if (lane == 0) {
                 cs.tr = tr;
@@ -574,9 +600,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                 }
                 return carry;
             };
-            int tr = BM;
-            if (BM == 256 && (int64_t)scan(256, false) * p.n_ntiles < 2 * p.num_sms) tr = 128;
-            if (p.force_tr) tr = min(p.force_tr, BM);
+            int tr = CG == 2 ? 256 : BM;
+            if (CG == 1 && BM == 256 && (int64_t)scan(256, false) * p.n_ntiles < 2 * p.num_sms) tr = 128;
+            if (CG == 1 && p.force_tr) tr = min(p.force_tr, BM);
             const int total = scan(tr, true);
             if (lane == 0) {
                 cs.list_prefix[p.n_lists] = total;
@@ -593,7 +619,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     const uint32_t tmem_base = cs.tmem_holder[0];
     if (threadIdx.x == 0) trace_event(p.trace, 2, 0);
     constexpr uint32_t rb = BK * 2;           // bytes per operand row (= swizzle span)
-    const int tr = cs.tr, wsplit = cs.wsplit, nht = tr / TC_BM;
+    // tr: rows of a tile (a pair's tile for CG = 2); nht: 128-row MMA halves held by this CTA
+    const int tr = cs.tr, wsplit = cs.wsplit, nht = CG == 2 ? 1 : tr / TC_BM;
     // the ring carve of this tile height
     const int rgi = (BM == 256 && tr == 128) ? 1 : 0;
     const int S = p.ring[rgi].stages, nkb = p.ring[rgi].nkb;
@@ -657,11 +684,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         // order), so uneven tiles balance across SMs; static round-robin without a ws
         int *fetch = p.tile_ctr ? p.tile_ctr + CTR_FETCH : nullptr;
         uint32_t ti = 0;
-        for (int64_t vs = blockIdx.x;; vs += gridDim.x, ++ti) {
+        // a pair's tiles: the leader claims (or walks statically without a ws) and forwards
+        // every tile index to the peer, so both CTAs decode the same sequence
+        const int64_t v_first = CG == 2 ? (int64_t)(blockIdx.x >> 1) : (int64_t)blockIdx.x;
+        const int64_t v_step = CG == 2 ? (int64_t)(gridDim.x >> 1) : (int64_t)gridDim.x;
+        for (int64_t vs = v_first;; vs += v_step, ++ti) {
             const int st = ti % TREC_SLOTS;
             ptx::mbar_wait_sleep(ptx::smem_u32(&cs.trec_empty[st]), ((ti / TREC_SLOTS) & 1) ^ 1);
             int64_t v = vs;
-            if (fetch && ti > 0) {
+            if (CG == 2 && !leader) {
+                ptx::mbar_wait_cluster(ptx::smem_u32(&cs.claim_full[st]), (ti / TREC_SLOTS) & 1);
+                v = *reinterpret_cast<volatile int64_t *>(&cs.claim_v[st]);
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive_remote_relaxed(ptx::mapa(ptx::smem_u32(&cs.claim_empty[st]), 0));
+            } else if (fetch && ti > 0) {
                 // first tile: blockIdx.x (no claim latency); then claims from the counter,
                 // at most claim_ahead tiles beyond the one the gather warps are on (claim
                 // gate: keeps the dynamic balance while the record of a light tile is ready
@@ -669,14 +705,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                 {
                     const int need = (int)ti + 1 - p.claim_ahead;
                     uint32_t ns = 32;
-                    while (atomicAdd(&cs.started, 0) < need) {
+                    while (ptx::atom_add_shared(ptx::smem_u32(&cs.started), 0) < need) {
                         __nanosleep(ns);
                         if (ns < 256) ns <<= 1;
                     }
                 }
                 int x = 0;
                 if (lane == 0) x = atomicAdd(fetch, 1);
-                v = (int64_t)gridDim.x + __shfl_sync(0xffffffffu, x, 0);
+                v = v_step + __shfl_sync(0xffffffffu, x, 0);
+            }
+            if (CG == 2 && leader) {
+                ptx::mbar_wait(ptx::smem_u32(&cs.claim_empty[st]), ((ti / TREC_SLOTS) & 1) ^ 1);
+                if (lane == 0) {
+                    ptx::st_cluster_s64(ptx::mapa(ptx::smem_u32(&cs.claim_v[st]), 1), v);
+                    ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_u32(&cs.claim_full[st]), 1));
+                }
+                __syncwarp();
             }
             TileRec &R = cs.trec[st];
             if (v >= n_tiles) {
@@ -686,6 +730,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             }
             TileInfo t;
             decode_tile(p, v, cs.list_prefix, n_out, tr, wsplit ? cs.sp_pre : nullptr, cs.sp_cnt, cs.n_sp, t);
+            if constexpr (CG == 2) {
+                // the pair's active offsets span all 256 rows; this CTA takes rows
+                // [128 rank, 128 rank + 128) of the tile (maybe none in a ragged tail)
+                if (p.mode == 0) decode_tile_mask(p, t);
+                t.row0 += 128 * rank;
+                t.rows = max(0, min(128, t.rows - 128 * (int)rank));
+            }
             // the tile's gather indices first (they depend only on its rows): the block's
             // load overlaps the record's mask / column / scatter work below
             const int bs = ti % p.blk_slots;
@@ -695,11 +746,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             if (p.mode == 0) {
                 // OS: rows [row0, row0+rows) of the [n_out x k_dense] table are contiguous
                 const uint32_t bytes = (uint32_t)((t.rows * p.k_dense * 4 + 15) & ~15);
-                if (lane == 0) {
+                if (lane == 0 && bytes) {
                     ptx::mbar_arrive_expect_tx(fb, bytes);
                     ptx::bulk_g2s(ptx::smem_u32(B), p.os + t.row0 * p.k_dense, bytes, fb);
                 }
-                if (lane != 0) ptx::mbar_arrive(fb);
+                if (lane != 0 || !bytes) ptx::mbar_arrive(fb);
             }
             // output-row scatter values (WS pairs / OS density order) are loaded before the
             // mask is consumed, so the two round trips overlap
@@ -721,7 +772,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                     sc[q] = (r < tr && r < t.rows) ? p.os_rows[t.row0 + r] : -1;
                 }
             }
-            if (p.mode == 0) decode_tile_mask(p, t);
+            if (CG == 1 && p.mode == 0) decode_tile_mask(p, t);
             // active columns: warp-parallel compaction of the mask bits (ballot prefix),
             // then this part's contiguous share when the tile is split
             int nc = 0;
@@ -791,19 +842,43 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                     const int nin = min(nkb, nsl - sl);
                     const int s = it % S;
                     ptx::mbar_wait(ptx::smem_u32(&cs.empty[s]), ((it / S) & 1) ^ 1);
+                    if (p.trace.buf && blockIdx.x < 2) trace_event(p.trace, 10, it);
                     const uint32_t fb = ptx::smem_u32(&cs.full[s]);
-                    ptx::mbar_arrive_expect_tx(fb, nin * p.kb_b);
+                    // a CTA of a pair loads its N half of each weight tile (rows
+                    // [rank BN/2, (rank+1) BN/2) of the K-major blob: contiguous, atom-aligned)
+                    const uint32_t kb_bl = p.kb_b / CG;
+                    ptx::mbar_arrive_expect_tx(fb, nin * kb_bl);
                     for (int kb = 0; kb < nin; ++kb) {
                         const int ci = (sl + kb) / p.n_chunks, cc = (sl + kb) - ci * p.n_chunks;
                         const int k = p.mode == 0 ? p.dense_k[R.cols[ci]] : kfix;
                         const int64_t blob = ((int64_t)k * p.n_ntiles + nt) * p.n_chunks + cc;
-                        ptx::bulk_g2s(ptx::smem_u32(sb + (size_t)s * b_bytes + kb * p.kb_b), p.wblob + blob * p.kb_b,
-                                      p.kb_b, fb);
+                        ptx::bulk_g2s(ptx::smem_u32(sb + (size_t)s * b_bytes + kb * kb_bl),
+                                      p.wblob + blob * p.kb_b + rank * kb_bl, kb_bl, fb);
                     }
                 }
                 ptx::mbar_arrive(ptx::smem_u32(&cs.trec_empty[st]));
             }
             __syncwarp();
+        }
+    } else if (CG == 2 && warp == W_MMA && !leader) {
+        // ===================== pair peer: stage forwarder =====================================
+        // the leader's MMAs read this CTA's A rows and B half: once a stage is complete here,
+        // make it visible to the async proxy and arrive on the leader's full barrier
+        uint32_t it = 0;
+        for (uint32_t ti = 0;; ++ti) {
+            const int st = ti % TREC_SLOTS;
+            ptx::mbar_wait(ptx::smem_u32(&cs.trec_full[st]), (ti / TREC_SLOTS) & 1);
+            const TileRec &R = cs.trec[st];
+            if (__shfl_sync(0xffffffffu, R.end, 0)) break;
+            const int nsl = __shfl_sync(0xffffffffu, R.ncols, 0) * p.n_chunks;
+            for (int sl = 0; sl < nsl; sl += nkb, ++it) {
+                const int s = it % S;
+                ptx::mbar_wait(ptx::smem_u32(&cs.full[s]), (it / S) & 1);
+                ptx::fence_proxy_async();
+                if (lane == 0) ptx::mbar_arrive_remote_relaxed(ptx::mapa(ptx::smem_u32(&cs.full[s]), 0));
+            }
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&cs.trec_empty[st]));
         }
     } else if (warp == W_MMA) {
         // ===================== MMA issuer (whole warp, elected lane issues) ================
@@ -830,11 +905,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             const uint32_t d_tmem = tb + a * NH * p.tmem_cols;
             uint32_t acc = 0;
             const int nsl = ncols * p.n_chunks;
+            const uint32_t kb_bl = p.kb_b / CG;
             for (int sl = 0; sl < nsl; sl += nkb_u, ++it) {
                 const int nin = min(nkb_u, nsl - sl);
                 const int s = it % S_u;
                 ptx::mbar_wait(ptx::smem_u32(&cs.full[s]), (it / S_u) & 1);
                 if (sl == 0 && lane == 0) trace_event(p.trace, 4, ti);
+                if (p.trace.buf && blockIdx.x < 2 && lane == 0) trace_event(p.trace, 11, it);
                 ptx::fence_proxy_async();
                 ptx::tc_fence_after();
                 // descriptors built once per stage; the K / row-half / slice steps add to
@@ -842,35 +919,48 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                 const uint64_t a_d0 = ptx::umma_desc_kmajor_sw(sa_u + (uint32_t)s * a_bytes_u, rb);
                 const uint64_t b_d0 = ptx::umma_desc_kmajor_sw(sb_u + (uint32_t)s * b_bytes_u, rb);
                 for (int kb = 0; kb < nin; ++kb) {
-                    const uint64_t a_dk = a_d0 + ((kb * kb_a_u) >> 4), b_dk = b_d0 + ((kb * p.kb_b) >> 4);
-                    // one asm block per 128-row half: the slice's BK/16 K steps
+                    const uint64_t a_dk = a_d0 + ((kb * kb_a_u) >> 4), b_dk = b_d0 + ((kb * kb_bl) >> 4);
+                    if constexpr (CG == 2) {
+                        // one M = 256 MMA chain for the pair (A rows and B halves at the same
+                        // smem offsets in both CTAs, accumulators at the same TMEM address)
+                        ptx::mma2_f16_ss_chain<BK / 16>(d_tmem, a_dk, b_dk, idesc_u, acc);
+                    } else {
+                        // one asm block per 128-row half: the slice's BK/16 K steps
 #pragma unroll
-                    for (int h = 0; h < NH; ++h) {
-                        if (h >= nht_u) break;
-                        ptx::mma_f16_ss_chain<BK / 16>(d_tmem + h * p.tmem_cols, a_dk + ((h * TC_BM * rb) >> 4), b_dk,
-                                                       idesc_u, acc);
+                        for (int h = 0; h < NH; ++h) {
+                            if (h >= nht_u) break;
+                            ptx::mma_f16_ss_chain<BK / 16>(d_tmem + h * p.tmem_cols, a_dk + ((h * TC_BM * rb) >> 4),
+                                                           b_dk, idesc_u, acc);
+                        }
                     }
                     acc = 1;
                 }
-                ptx::mma_commit_elect(ptx::smem_u32(&cs.empty[s]));
+                if constexpr (CG == 2) ptx::mma2_commit_multicast_elect(ptx::smem_u32(&cs.empty[s]));
+                else ptx::mma_commit_elect(ptx::smem_u32(&cs.empty[s]));
             }
-            ptx::mma_commit_elect(ptx::smem_u32(&cs.tfull[a]));
+            if constexpr (CG == 2) ptx::mma2_commit_multicast_elect(ptx::smem_u32(&cs.tfull[a]));
+            else ptx::mma_commit_elect(ptx::smem_u32(&cs.tfull[a]));
             if (lane == 0) trace_event(p.trace, 5, ti);
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&cs.trec_empty[st]));
         }
     } else if (warp >= W_EPI0 && warp < W_EPI0 + 4) {
         // ===================== epilogue (warps 8-11, thread = TMEM lane = tile row) ====
+        const int pair_rank = CG == 2 ? (int)rank : -1;
         if (wsplit)
-            epi_role<true>(p, cs, tmem_base, tr, nht, NH, warp, lane);
+            epi_role<true>(p, cs, tmem_base, tr, nht, NH, warp, lane, pair_rank);
         else
-            epi_role<false>(p, cs, tmem_base, tr, nht, NH, warp, lane);
+            epi_role<false>(p, cs, tmem_base, tr, nht, NH, warp, lane, pair_rank);
     }
     ptx::tc_fence_before();
-    __syncthreads();
+    // a pair frees its TMEM and exits together (the leader's MMAs and commits reach the
+    // peer's TMEM and barriers until its last tile)
+    if constexpr (CG == 2) ptx::cluster_sync();
+    else __syncthreads();
     if (warp == W_MMA) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc(tmem_base, p.tbufs * NH * p.tmem_cols);
+        if constexpr (CG == 2) ptx::tmem_dealloc2(tmem_base, p.tbufs * NH * p.tmem_cols);
+        else ptx::tmem_dealloc(tmem_base, p.tbufs * NH * p.tmem_cols);
     }
     if (threadIdx.x == 0) trace_event(p.trace, 7, 0);
     if (p.tile_ctr && threadIdx.x == 0) {
@@ -1151,10 +1241,11 @@ static spc_status launch_tc(const ConvParams &p0, int mode, int out_kind, void *
     for (int g = 0; g < 2; ++g) {
         const int rows = g == 0 ? p.bm : TC_BM;
         ConvParams::Ring &R = p.ring[g];
+        const uint32_t kb_bl = p.kb_b / p.cg;   // this CTA's share of a weight tile
         R.kb_a = (uint32_t)(rows * p.BK * 2);
-        R.nkb = (int)std::max<size_t>(1, std::min<size_t>(8, stage_cap / (R.kb_a + p.kb_b)));
+        R.nkb = (int)std::max<size_t>(1, std::min<size_t>(8, stage_cap / (R.kb_a + kb_bl)));
         R.a_bytes = R.nkb * R.kb_a;
-        R.b_bytes = R.nkb * p.kb_b;
+        R.b_bytes = R.nkb * kb_bl;
         R.stages = (int)std::min<size_t>(16, avail / (R.a_bytes + R.b_bytes));
         if (R.stages < 2) return fail(SPC_ERR_UNSUPPORTED, "spc_conv_forward: tile does not fit shared memory");
         ring_bytes = std::max(ring_bytes, (size_t)R.stages * (R.a_bytes + R.b_bytes));
@@ -1164,24 +1255,29 @@ static spc_status launch_tc(const ConvParams &p0, int mode, int out_kind, void *
     static uint64_t configured = 0;   // bit d: smem attributes set on device d
     const int dev = current_device();
     if (!(configured >> dev & 1)) {
-        SPC_CUDA(cudaFuncSetAttribute(k_conv_tc<16, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BUDGET));
-        SPC_CUDA(cudaFuncSetAttribute(k_conv_tc<32, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BUDGET));
-        SPC_CUDA(cudaFuncSetAttribute(k_conv_tc<64, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BUDGET));
-        SPC_CUDA(cudaFuncSetAttribute(k_conv_tc<16, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BUDGET));
-        SPC_CUDA(cudaFuncSetAttribute(k_conv_tc<32, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BUDGET));
-        SPC_CUDA(cudaFuncSetAttribute(k_conv_tc<64, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BUDGET));
+        void (*ks[])(ConvParams) = {k_conv_tc<16, 128, 1>, k_conv_tc<32, 128, 1>, k_conv_tc<64, 128, 1>,
+                                    k_conv_tc<16, 256, 1>, k_conv_tc<32, 256, 1>, k_conv_tc<64, 256, 1>,
+                                    k_conv_tc<16, 128, 2>, k_conv_tc<32, 128, 2>, k_conv_tc<64, 128, 2>};
+        for (auto k : ks) SPC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BUDGET));
         configured |= 1ull << dev;
     }
     // persistent: one CTA per SM (tile geometry and counts live on the device)
     const int64_t tiles_cap = mode == 0 ? ((p.n_out_cap + TC_BM - 1) / TC_BM) * p.n_ntiles *
                                               (p.split_ok ? std::max(1, p.k_dense / 2) : 1)
                                         : (int64_t)num_sms();
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles_cap, num_sms()));
-    p.trace = trace_next(std::string("k_conv_tc ") + (mode == 0 ? "os" : "ws") + " n_out=" + std::to_string(p.n_out_cap) +
-                         " c_in=" + std::to_string(p.n_chunks * p.BK) + " c_out=" + std::to_string(p.n_ntiles * p.BN) +
-                         " k_dense=" + std::to_string(p.k_dense) + " lists=" + std::to_string(p.n_lists));
-    void (*k)(ConvParams) = p.bm == 256 ? (p.BK == 64 ? k_conv_tc<64, 256> : p.BK == 32 ? k_conv_tc<32, 256> : k_conv_tc<16, 256>)
-                                        : (p.BK == 64 ? k_conv_tc<64, 128> : p.BK == 32 ? k_conv_tc<32, 128> : k_conv_tc<16, 128>);
+    int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles_cap, num_sms()));
+    if (p.cg == 2) grid = 2 * std::max(1, std::min(grid, num_sms()) / 2);   // whole CTA pairs
+    p.trace = trace_next(std::string("k_conv_tc ") + (mode == 0 ? "os" : "ws") + (p.cg == 2 ? " pair" : "") +
+                         " n_out=" + std::to_string(p.n_out_cap) + " c_in=" + std::to_string(p.n_chunks * p.BK) +
+                         " c_out=" + std::to_string(p.n_ntiles * p.BN) + " k_dense=" + std::to_string(p.k_dense) +
+                         " lists=" + std::to_string(p.n_lists));
+    if (p.cg == 2) {
+        void (*k)(ConvParams) = p.BK == 64 ? k_conv_tc<64, 128, 2> : p.BK == 32 ? k_conv_tc<32, 128, 2> : k_conv_tc<16, 128, 2>;
+        SPC_CUDA(launch_pdl_cluster(k, dim3(grid), dim3(TC_THREADS), smem, st, 2, p));
+        return SPC_OK;
+    }
+    void (*k)(ConvParams) = p.bm == 256 ? (p.BK == 64 ? k_conv_tc<64, 256, 1> : p.BK == 32 ? k_conv_tc<32, 256, 1> : k_conv_tc<16, 256, 1>)
+                                        : (p.BK == 64 ? k_conv_tc<64, 128, 1> : p.BK == 32 ? k_conv_tc<32, 128, 1> : k_conv_tc<16, 128, 1>);
     SPC_CUDA(launch_pdl(k, dim3(grid), dim3(TC_THREADS), smem, st, p));
     return SPC_OK;
 }
@@ -1283,9 +1379,21 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
     // kernel drops to 128-row tiles on the device when the live row count is small
     p.bm = (4 * p.tmem_cols <= 512) ? 256 : 128;
     if (has_os && (size_t)BLK_SLOTS * p.bm * km->k_dense * 4 > 96 * 1024) p.bm = 128;   // OS index blocks (K=5)
+    // CTA pairs (cta_group::2) for wide outputs, where a 128-row tile would re-read the whole
+    // weight tile per 128 rows: a pair runs 256-row tiles with M = 256 MMAs, each CTA loading
+    // half of every weight tile (half the L2 weight traffic per row, half the MMA issues).
+    // Pairs walk their tiles statically and never split a tile's offsets, so an all-OS map
+    // whose live size is unknown on the host (network maps) keeps single CTAs.
+    {
+        const int64_t pair_opt = option(SPC_OPT_CONV_CTA_PAIR);
+        const bool wide = p.BN >= 192 && p.bm == 128 && (p.BN / 2) % 16 == 0;
+        const bool big_os = !has_os || has_ws ||
+                            (!km->n_out_dev && ((km->n_out + 255) / 256) * p.n_ntiles >= p.num_sms / 2);
+        p.cg = (pair_opt != 0 && wide && (big_os || pair_opt == 2)) ? 2 : 1;
+    }
     p.tbufs = (p.bm == 256 ? 4 : 2) * p.tmem_cols <= 512 ? 2 : 1;
     p.kb_b = (uint32_t)(p.BN * p.BK * 2);
-    p.idesc = ptx::umma_idesc_f16(in_dtype == SPC_BF16, TC_BM, p.BN);
+    p.idesc = ptx::umma_idesc_f16(in_dtype == SPC_BF16, TC_BM * p.cg, p.BN);
     p.wblob = static_cast<const char *>(weight);
     // workspace: fp32 accumulator + tile counters (zero on entry, zero on return)
     float *wacc = nullptr;
@@ -1312,7 +1420,7 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
                              ld_out, OUT_FINAL, out_dtype, residual, ld_res, st);
     if (!has_ws) {
         // OS only: one launch; small levels split offsets over CTAs with the in-kernel fixup
-        p.split_ok = (wacc && km->k_dense >= 4 && option(SPC_OPT_CONV_OS_SPLIT) != 0) ? 1 : 0;
+        p.split_ok = (p.cg == 1 && wacc && km->k_dense >= 4 && option(SPC_OPT_CONV_OS_SPLIT) != 0) ? 1 : 0;
         return launch_tc(p, 0, OUT_FINAL, f_out, ld_out, st);
     }
     p.split_ok = 0;

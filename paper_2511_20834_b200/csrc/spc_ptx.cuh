@@ -15,6 +15,17 @@ __device__ __forceinline__ int32_t lds_s32(uint32_t addr) {
     return v;
 }
 
+// shared-memory atomics on an explicit .shared address (a flag polled across warps: atomics
+// keep it race-free, the explicit state space keeps it an ATOMS, not a generic .GPU atomic)
+__device__ __forceinline__ int32_t atom_add_shared(uint32_t addr, int32_t v) {
+    int32_t r;
+    asm volatile("atom.shared.add.s32 %0, [%1], %2;" : "=r"(r) : "r"(addr), "r"(v) : "memory");
+    return r;
+}
+__device__ __forceinline__ void red_max_shared(uint32_t addr, int32_t v) {
+    asm volatile("red.shared.max.s32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
 // ---- mbarrier ------------------------------------------------------------------------
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
@@ -58,6 +69,47 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 }
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+
+// ---- clusters (CTA pairs) --------------------------------------------------------------
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+// every thread of both CTAs: release this CTA's prior writes, wait for the pair
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared address of the same variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+// arrive on an mbarrier of another CTA of the cluster (address from mapa), release at
+// cluster scope: this thread's prior writes are visible to the waiter's acquire
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// plain remote arrive (default semantics; what a stage hand-off needs, no cluster fence)
+__device__ __forceinline__ void mbar_arrive_remote_relaxed(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void st_cluster_s64(uint32_t cluster_addr, int64_t v) {
+    asm volatile("st.shared::cluster.s64 [%0], %1;" ::"r"(cluster_addr), "l"(v) : "memory");
+}
+// wait whose acquire covers writes released at cluster scope by the peer CTA
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+    uint32_t ok = 0;
+    while (!ok) {
+        asm volatile(
+            "{\n.reg .pred p;\nmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(ok)
+            : "r"(bar), "r"(parity)
+            : "memory");
+    }
 }
 
 // ---- async copies ----------------------------------------------------------------------
@@ -126,6 +178,16 @@ __device__ __forceinline__ void tmem_alloc(uint32_t dst_smem, uint32_t ncols) {
 __device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
 }
+// CTA pair (cta_group::2): the same warp of BOTH CTAs allocates; the columns are reserved at
+// the same TMEM address in each CTA (the M = 256 accumulator's rows 0-127 / 128-255)
+__device__ __forceinline__ void tmem_alloc2(uint32_t dst_smem, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(dst_smem), "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc2(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -176,6 +238,32 @@ __device__ __forceinline__ void mma_f16_ss_chain(uint32_t d_tmem, uint64_t a_des
             "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
             : "memory");
     }
+}
+// CTA pair: NK K=16 steps of D[tmem] (M = 256: rows 0-127 from this CTA's A and TMEM,
+// 128-255 from the peer's at the same addresses; B's N halves in the two CTAs' smem),
+// issued by the leader CTA's elected lane
+template <int NK>
+__device__ __forceinline__ void mma2_f16_ss_chain(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                                  uint32_t accumulate) {
+#pragma unroll
+    for (int k = 0; k < NK; ++k) {
+        const uint64_t ad = a_desc + 2 * k, bd = b_desc + 2 * k;
+        const uint32_t acc = (k == 0) ? accumulate : 1u;
+        asm volatile(
+            "{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
+            "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+            "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
+            : "memory");
+    }
+}
+// CTA pair: arrive on the mbarrier at this smem offset in BOTH CTAs once the leader's
+// previously issued tcgen05.mma complete
+__device__ __forceinline__ void mma2_commit_multicast_elect(uint32_t bar) {
+    asm volatile(
+        "{\n.reg .pred e;\n.reg .b16 m;\nmov.b16 m, 3;\nelect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n}" ::"r"(
+            bar)
+        : "memory");
 }
 __device__ __forceinline__ void mma_commit_elect(uint32_t bar) {
     asm volatile(

@@ -23,7 +23,13 @@ ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--config", type=int, default=2)
 ap.add_argument("--n", type=int, default=0, help="keep the first n points of the scan")
 ap.add_argument("--order", type=int, default=1, help="SPC_KMAP_DENSITY_ORDER")
+ap.add_argument("--pair", type=int, default=-1, help="SPC_OPT_CONV_CTA_PAIR (0 off, 1 auto, 2 force; -1 default)")
+ap.add_argument("--opt", action="append", default=[], help="NAME=VALUE spc_set_option (e.g. CONV_STAGE_KB=96)")
 a = ap.parse_args()
+spc.spc_set_option(spc.SPC_OPT_CONV_CTA_PAIR, a.pair)
+for o in a.opt:
+    k, v = o.split("=")
+    spc.spc_set_option(getattr(spc, "SPC_OPT_" + k), int(v))
 
 coords = synth.make_scan(a.config, 0)
 if a.n:
@@ -49,7 +55,7 @@ e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / a.reps
 fl = 2.0 * nnz * a.cin * a.cout
-print(f"n={n} nnz={nnz} k_dense={km.k_dense} lists={km.n_lists} cin={a.cin} cout={a.cout} t={a.t}: "
+print(f"n={n} nnz={nnz} k_dense={km.k_dense} lists={km.n_lists} cin={a.cin} cout={a.cout} t={a.t} pair={a.pair}: "
       f"{ms * 1e3:.1f} us  {fl / ms / 1e9:.1f} TFLOP/s (algorithmic)")
 if os.environ.get("PROBE_KERNELS"):
     from torch.profiler import profile, ProfilerActivity
