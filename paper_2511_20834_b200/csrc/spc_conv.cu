@@ -1387,8 +1387,11 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
     {
         const int64_t pair_opt = option(SPC_OPT_CONV_CTA_PAIR);
         const bool wide = p.BN >= 192 && p.bm == 128 && (p.BN / 2) % 16 == 0;
-        const bool big_os = !has_os || has_ws ||
-                            (!km->n_out_dev && ((km->n_out + 255) / 256) * p.n_ntiles >= p.num_sms / 2);
+        // measured: pairs win on large output-stationary launches (C5 256x256: 177 -> 169 us,
+        // 192x192: 133 -> 116 us) and lose on the small weight-stationary levels of C2 (the
+        // scatter epilogue dominates there and the pair hand-off adds latency)
+        const bool big_os = has_os && !has_ws && !km->n_out_dev &&
+                            ((km->n_out + 255) / 256) * p.n_ntiles >= p.num_sms / 2;
         p.cg = (pair_opt != 0 && wide && (big_os || pair_opt == 2)) ? 2 : 1;
     }
     p.tbufs = (p.bm == 256 ? 4 : 2) * p.tmem_cols <= 512 ? 2 : 1;
