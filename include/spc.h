@@ -78,7 +78,13 @@ typedef enum {
                                    * TMA-fed GEMM that initialises the accumulator (default 0)    */
     SPC_OPT_CONV_CTA_PAIR = 9,    /* CTA pairs (cta_group::2, M = 256) for outputs >= 192 wide:
                                    * 0 off, 1 auto (default), 2 wherever the shape allows       */
-    SPC_OPT_COUNT = 10
+    SPC_OPT_CONV_MAPS_READY = 10, /* 1: the caller asserts that the kernel map and the prepared
+                                   * weights of the next spc_conv_forward calls were complete
+                                   * before the preceding kernel of their stream STARTED (true
+                                   * for every layer but the first of a network pass): the
+                                   * kernel then decodes tiles and streams weights while that
+                                   * kernel drains (programmatic dependent launch) (default 0)  */
+    SPC_OPT_COUNT = 11
 } spc_option;
 spc_status spc_set_option(int32_t option, int64_t value);
 int64_t spc_get_option(int32_t option);

@@ -125,8 +125,23 @@ struct Trace {
     int64_t cap;
     uint32_t launch;
 };
+static __device__ __noinline__ void trace_record(const Trace &t, int ev, uint32_t aux);
+// launch-level events (entry, PDL release, setup, exit): a predicated out-of-line call
 __device__ __forceinline__ void trace_event(const Trace &t, int ev, uint32_t aux) {
-    if (!t.buf) return;
+    if (t.buf) trace_record(t, ev, aux);
+}
+// per-tile events (records, first full stage, commits, epilogues) sit in the pipeline
+// loops, where even a predicated call measurably costs (~1% of a C2 step): they are
+// compiled only into the tracing build of the library
+// (python -m paper_2511_20834_b200.build --exp trace -DSPC_TRACE_TILES; scripts/timeline.py)
+__device__ __forceinline__ void trace_tile_event(const Trace &t, int ev, uint32_t aux) {
+#ifdef SPC_TRACE_TILES
+    if (t.buf) trace_record(t, ev, aux);
+#else
+    (void)t; (void)ev; (void)aux;
+#endif
+}
+static __device__ __noinline__ void trace_record(const Trace &t, int ev, uint32_t aux) {
     unsigned long long ts;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts));
     const unsigned long long i = atomicAdd(t.buf, 1ull);

@@ -84,6 +84,7 @@ struct ConvParams {
     int *tile_ctr;        // ws counters (zero on entry, left zero): [0, 1024) split-tile arrivals,
                           // [CTR_EXIT] CTAs exited, [CTR_FETCH] dynamic tile fetch
     int blk_slots;        // gather-index blocks in flight (2, or 1 when a block is large: K=5 OS)
+    int maps_ready;       // map + weights complete before the previous kernel started (PDL early start)
     int cg;               // 2: CTA pairs (cta_group::2, M = 256 per MMA, each CTA holds half of every
                           //    weight tile and 128 of the pair tile's 256 rows); 1: single CTAs
     uint32_t tmem_cols;   // per 128-row accumulator (power of two >= 32)
@@ -367,13 +368,10 @@ __device__ __forceinline__ void gather_role(const ConvParams &p, ConvSmem &cs, c
         for (int sl = 0; sl < nsl; sl += nkb) {
             const int nin = min(nkb, nsl - sl);
             ptx::mbar_wait(ptx::smem_u32(&cs.empty[s]), ph ^ 1);
-            const bool fine = p.trace.buf && blockIdx.x < 2 && warp == 0 && lane == 0;   // per-stage trace (CTAs 0, 1)
-            if (fine) trace_event(p.trace, 8, sl);
             gather_slices<BK, NBT>(p, R, ptx::smem_u32(B), kd, rows, sl, nin, ptx::smem_u32(sa + (size_t)s * a_bytes), kb_a,
                                    warp, r_in, q_lane);
             // the zero rows were written through the generic proxy: order them before the
             // tensor core's async-proxy reads, then arrive once this thread's copies land
-            if (fine) trace_event(p.trace, 9, sl);
             ptx::fence_proxy_async();
             ptx::cp_async_mbar_arrive(ptx::smem_u32(&cs.full[s]));
             if (++s == S) { s = 0; ph ^= 1; }
@@ -439,7 +437,7 @@ __device__ __forceinline__ void epi_role(const ConvParams &p, ConvSmem &cs, uint
         }
         ptx::tc_fence_before();
         __syncwarp();
-        if (threadIdx.x == 32 * W_EPI0) trace_event(p.trace, 6, ti);
+        if (threadIdx.x == 32 * W_EPI0) trace_tile_event(p.trace, 6, ti);
         if (lane == 0) {
             // the accumulator is free again: a CTA pair's MMAs are issued by the leader, so
             // the peer releases the leader's barrier
@@ -550,9 +548,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     }
     // a pair's barriers are initialised before either CTA signals the other's
     if constexpr (CG == 2) ptx::cluster_sync();
-    // everything above overlaps the previous kernel's tail (PDL); maps, features, weights
-    // and outputs are touched only after this point
-    pdl_wait();
+    // everything above overlaps the previous kernel's tail (PDL).  With maps_ready (the
+    // caller asserts that the kernel map and weights were complete before the previous
+    // kernel of the stream started -- every layer after the first of a pass), the
+    // scheduler decodes its first tile and fetches its index block and the weight loader
+    // streams weights while the previous layer drains; the roles that read features, write
+    // outputs or touch the workspace wait for the previous kernel first
+    const bool early = p.maps_ready && (warp == W_SCHED || warp == W_BLOAD || warp == W_MMA);
+    if (!early) pdl_wait();
     pdl_trigger();
     if (threadIdx.x == 0) trace_event(p.trace, 1, 0);
     const int64_t n_out = dev_count(p.n_out_cap, p.n_out_dev);
@@ -698,6 +701,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive_remote_relaxed(ptx::mapa(ptx::smem_u32(&cs.claim_empty[st]), 0));
             } else if (fetch && ti > 0) {
+                if (ti == 1 && p.maps_ready) pdl_wait();   // the fetch counter is shared with the previous layer
                 // first tile: blockIdx.x (no claim latency); then claims from the counter,
                 // at most claim_ahead tiles beyond the one the gather warps are on (claim
                 // gate: keeps the dynamic balance while the record of a light tile is ready
@@ -816,7 +820,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                     if (q * 32 < tr) R.scatter[q * 32 + lane] = sc[q];
             }
             ptx::mbar_arrive(ptx::smem_u32(&cs.trec_full[st]));
-            if (lane == 0) trace_event(p.trace, 3, ti);
+            if (lane == 0) trace_tile_event(p.trace, 3, ti);
         }
         ptx::cp_async_wait<0>();
     } else if (warp < N_GATHER) {
@@ -842,7 +846,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                     const int nin = min(nkb, nsl - sl);
                     const int s = it % S;
                     ptx::mbar_wait(ptx::smem_u32(&cs.empty[s]), ((it / S) & 1) ^ 1);
-                    if (p.trace.buf && blockIdx.x < 2) trace_event(p.trace, 10, it);
                     const uint32_t fb = ptx::smem_u32(&cs.full[s]);
                     // a CTA of a pair loads its N half of each weight tile (rows
                     // [rank BN/2, (rank+1) BN/2) of the K-major blob: contiguous, atom-aligned)
@@ -910,8 +913,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                 const int nin = min(nkb_u, nsl - sl);
                 const int s = it % S_u;
                 ptx::mbar_wait(ptx::smem_u32(&cs.full[s]), (it / S_u) & 1);
-                if (sl == 0 && lane == 0) trace_event(p.trace, 4, ti);
-                if (p.trace.buf && blockIdx.x < 2 && lane == 0) trace_event(p.trace, 11, it);
+                if (sl == 0 && lane == 0) trace_tile_event(p.trace, 4, ti);
                 ptx::fence_proxy_async();
                 ptx::tc_fence_after();
                 // descriptors built once per stage; the K / row-half / slice steps add to
@@ -940,7 +942,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             }
             if constexpr (CG == 2) ptx::mma2_commit_multicast_elect(ptx::smem_u32(&cs.tfull[a]));
             else ptx::mma_commit_elect(ptx::smem_u32(&cs.tfull[a]));
-            if (lane == 0) trace_event(p.trace, 5, ti);
+            if (lane == 0) trace_tile_event(p.trace, 5, ti);
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&cs.trec_empty[st]));
         }
@@ -1409,6 +1411,7 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
     p.ld_acc = c_out;
     p.tile_ctr = wctr;
     p.skip_list = -1;
+    p.maps_ready = option(SPC_OPT_CONV_MAPS_READY) != 0 ? 1 : 0;
     // A11: identity maps need no gather.  A K = 1 submanifold layer is one dense TMA-fed
     // GEMM; with SPC_OPT_CONV_DENSE_CENTRE the centre of an all-weight-stationary
     // submanifold map (always matched, out_i += F_i W_centre) is computed the same

@@ -148,6 +148,7 @@ class SparseNet:
                  nnz_per_out: float = 10.0, net: str = "minkunet42", density_order: bool = True):
         self.dev = torch.device(device)
         self.density_order = bool(density_order)
+        self.early_maps = True   # layers >= 1 start their tile decode during the previous layer
         self.spec = spec
         self.n0 = int(n0_cap)
         if net == "minkunet42":
@@ -251,8 +252,14 @@ class SparseNet:
                           ws=self.sort_ws, stream=stream, n_dev=n_live)
         spc.spc_gather_rows(feats, self.perm[:n], out=self.bufs["x0"][:n], n_dev=n_live, stream=stream)
         self.index(stream, n_dev=n_live)
-        for i in range(len(self.layers)):
-            self.conv(i, stream)
+        try:
+            for i in range(len(self.layers)):
+                # after the first layer the maps and weights are long complete when the
+                # preceding kernel starts: let each layer decode tiles early (PDL)
+                spc.spc_set_option(spc.SPC_OPT_CONV_MAPS_READY, 1 if (i > 0 and self.early_maps) else 0)
+                self.conv(i, stream)
+        finally:
+            spc.spc_set_option(spc.SPC_OPT_CONV_MAPS_READY, 0)
         return self.bufs[self.out_name]
 
     # ---------------------------------------------------------------------------------

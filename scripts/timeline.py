@@ -15,6 +15,10 @@ import torch  # noqa: E402
 
 import bench  # noqa: E402
 import paper_2511_20834_b200 as spc  # noqa: E402
+from paper_2511_20834_b200 import build as spc_build  # noqa: E402
+
+# per-tile events are compiled only into the tracing build of the library
+spc.LIB_PATH = spc_build.build(exp="trace", defines=["-DSPC_TRACE_TILES"])
 from paper_2511_20834_b200.network import SparseNet, C_IN_PAD  # noqa: E402
 
 ap = argparse.ArgumentParser()
