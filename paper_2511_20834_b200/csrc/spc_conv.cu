@@ -305,28 +305,27 @@ __device__ __noinline__ void os_split_fixup(const ConvParams &p, ConvSmem &cs, c
 // instruction stores whole sectors of RPI rows into the swizzled K-major tile (chunk j of
 // row r lands at j ^ f(r)).  Matched rows: one whole-line request per row; sentinel rows
 // (no input voxel) never touch L2: zeroed with a shared store.
+// (ci, cc): offset column and channel chunk of the stage's first slice, advanced per slice
+// (no integer division in the loop)
 template <int BK, int NBT>
 __device__ __forceinline__ void gather_slices(const ConvParams &p, const TileRec &R, uint32_t Bs, int kd, int rows,
-                                              int sl, int nin, uint32_t abase, uint32_t kb_a, int warp, int r_in,
-                                              int q_lane) {
+                                              int ci, int cc, int nin, uint32_t abase, uint32_t kb_a, int warp,
+                                              int r_in, int q_lane) {
     constexpr uint32_t rb = BK * 2;
     constexpr int RPI = 32 / (BK / 8);
     constexpr int ROWS_W = NBT * RPI;
-    // all of a slice's gather indices are loaded (explicit ld.shared, independent) before
-    // its copies are issued
-    auto load_idx = [&](int kb, int32_t (&g)[NBT]) {
-        const int ci = (sl + kb) / p.n_chunks;
-        const int c = p.mode == 0 ? R.cols[ci] : 0;
-#pragma unroll
-        for (int b = 0; b < NBT; ++b) {
-            const int r = warp * ROWS_W + b * RPI + r_in;
-            g[b] = r < rows ? ptx::lds_s32(Bs + (uint32_t)(r * kd + c) * 4u) : -1;
-        }
-    };
     for (int kb = 0; kb < nin; ++kb) {
+        // all of a slice's gather indices are loaded (explicit ld.shared, independent)
+        // before its copies are issued
         int32_t g[NBT];
-        load_idx(kb, g);
-        const int cc = (sl + kb) % p.n_chunks;
+        {
+            const int c = p.mode == 0 ? R.cols[ci] : 0;
+#pragma unroll
+            for (int b = 0; b < NBT; ++b) {
+                const int r = warp * ROWS_W + b * RPI + r_in;
+                g[b] = r < rows ? ptx::lds_s32(Bs + (uint32_t)(r * kd + c) * 4u) : -1;
+            }
+        }
         const uint32_t kbo = kb * kb_a;
 #pragma unroll
         for (int b = 0; b < NBT; ++b) {
@@ -339,6 +338,10 @@ __device__ __forceinline__ void gather_slices(const ConvParams &p, const TileRec
                 ptx::cp_async_16(abase + so, p.f_in + (int64_t)g[b] * p.ld_in_bytes + cc * rb + q_lane * 16, 16u);
             else
                 asm volatile("st.shared.v4.b32 [%0], {%1,%1,%1,%1};" ::"r"(abase + so), "r"(0) : "memory");
+        }
+        if (++cc == p.n_chunks) {
+            cc = 0;
+            ++ci;
         }
     }
 }
@@ -365,11 +368,17 @@ __device__ __forceinline__ void gather_role(const ConvParams &p, ConvSmem &cs, c
         ptx::mbar_wait(ptx::smem_u32(&cs.blk_full[bs]), (ti / p.blk_slots) & 1);
         const int32_t *B = blk + bs * blk_stride;
         const int nsl = ncols * p.n_chunks;
+        int ci = 0, cc = 0;   // (offset column, channel chunk) of slice sl
         for (int sl = 0; sl < nsl; sl += nkb) {
             const int nin = min(nkb, nsl - sl);
             ptx::mbar_wait(ptx::smem_u32(&cs.empty[s]), ph ^ 1);
-            gather_slices<BK, NBT>(p, R, ptx::smem_u32(B), kd, rows, sl, nin, ptx::smem_u32(sa + (size_t)s * a_bytes), kb_a,
-                                   warp, r_in, q_lane);
+            gather_slices<BK, NBT>(p, R, ptx::smem_u32(B), kd, rows, ci, cc, nin, ptx::smem_u32(sa + (size_t)s * a_bytes),
+                                   kb_a, warp, r_in, q_lane);
+            for (int k = 0; k < nin; ++k)
+                if (++cc == p.n_chunks) {
+                    cc = 0;
+                    ++ci;
+                }
             // the zero rows were written through the generic proxy: order them before the
             // tensor core's async-proxy reads, then arrive once this thread's copies land
             ptx::fence_proxy_async();
