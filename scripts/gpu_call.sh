@@ -1,2 +1,2 @@
-timeout 600 python -m pytest tests/test_gpu_parity.py -q -x 2>&1 | tail -2
-python scripts/ab_lib.py paper_2511_20834_b200/exp_prev.so paper_2511_20834_b200/libspc.so
+python scripts/indexing_modes.py --config 2 --reps 20 | tee gpurun_out/r2_indexing_modes.jsonl
+python scripts/indexing_modes.py --config 4 --reps 10 | tee -a gpurun_out/r2_indexing_modes.jsonl
