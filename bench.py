@@ -711,10 +711,15 @@ def load_t(path):
 def conv_traffic(config, n_voxels):
     """Per-step DRAM bytes of the feature-computation launches from the committed ncu
     capture (scripts/conv_traffic.py), when it was taken on this workload."""
-    p = os.path.join(ROOT, "profiles", f"r1_conv_traffic_c{config}.json")
-    try:
-        d = json.load(open(p))
-    except Exception:
+    d = None
+    for rnd in ("r2", "r1"):
+        p = os.path.join(ROOT, "profiles", f"{rnd}_conv_traffic_c{config}.json")
+        try:
+            d = json.load(open(p))
+            break
+        except Exception:
+            continue
+    if d is None:
         return None
     if d.get("n_voxels") not in (None, n_voxels):
         return None

@@ -162,6 +162,12 @@ size_t spc_pack_sort_workspace_size(int64_t n);
 spc_status spc_pack_sort(const int32_t *coords, int64_t n, const int64_t *n_dev, spc_pack_spec spec, uint64_t *keys_out,
                          int32_t *perm_out, uint32_t *status, void *ws, size_t ws_bytes, void *stream);
 
+/* 32-bit keys (NEXT-1 ablation): the same pack + sort when bits_b+x+y+z <= 32 (e.g. one
+ * scan at 12/12/8); SPC_ERR_RANGE otherwise.  Same workspace size. */
+spc_status spc_pack_sort32(const int32_t *coords, int64_t n, const int64_t *n_dev, spc_pack_spec spec,
+                           uint32_t *keys_out, int32_t *perm_out, uint32_t *status, void *ws, size_t ws_bytes,
+                           void *stream);
+
 /* dst row r = src row perm[r] (row_bytes each, 16-byte aligned rows).  n_dev nullable. */
 spc_status spc_gather_rows(const void *src, int64_t ld_src_bytes, const int32_t *perm, int64_t n,
                            const int64_t *n_dev, int32_t row_bytes, void *dst, int64_t ld_dst_bytes,
@@ -251,6 +257,8 @@ typedef struct {
     int32_t k_dense;      /* number of dense offsets (OS part)                      */
     int32_t n_lists;      /* number of stored WS lists                              */
     int32_t halved;       /* 1 if SPC_KMAP_HALVE_SYMMETRIC was applied              */
+    int32_t key_bits;     /* 64, or 32 for maps built by spc_build_kmap32 (in_keys /
+                           * out_keys then point to uint32 keys)                    */
     int32_t tile_words;   /* 32-bit words per OS tile in tile_mask_dev              */
     int64_t n_in;         /* capacities (host)                                      */
     int64_t n_out;
@@ -293,6 +301,15 @@ spc_status spc_build_kmap(const uint64_t *in_keys, int64_t n_in, const int64_t *
                           const uint64_t *out_keys, int64_t n_out, const int64_t *n_out_dev,
                           spc_pack_spec spec, spc_geom geom, int32_t t, uint32_t flags, void *buf,
                           size_t buf_bytes, uint32_t *status, spc_kmap *kmap_out_host, void *stream);
+
+/* NEXT-1 ablation (the paper packs one scan into 32 bits, 12/12/8):
+ * the same build over uint32 keys from spc_pack_sort32.  The spec's fields must total
+ * <= 32 bits (SPC_ERR_RANGE otherwise); network-wide builds and SPC_KMAP_SIMPLE_BSEARCH
+ * stay 64-bit (SPC_ERR_UNSUPPORTED).  The map is used by spc_conv_forward unchanged. */
+spc_status spc_build_kmap32(const uint32_t *in_keys, int64_t n_in, const int64_t *n_in_dev,
+                            const uint32_t *out_keys, int64_t n_out, const int64_t *n_out_dev,
+                            spc_pack_spec spec, spc_geom geom, int32_t t, uint32_t flags, void *buf,
+                            size_t buf_bytes, uint32_t *status, spc_kmap *kmap_out_host, void *stream);
 
 /* Export the map as (k, out, in) int32 triples sorted lexicographically (parity
  * tooling; [sync]: synchronises `stream`).  Returns the nnz in *nnz_host; writes at

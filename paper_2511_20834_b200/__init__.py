@@ -77,7 +77,8 @@ class Geom(ctypes.Structure):
 
 class _Kmap(ctypes.Structure):
     _fields_ = [("geom", Geom), ("t", ctypes.c_int32), ("k_vol", ctypes.c_int32), ("k_dense", ctypes.c_int32),
-                ("n_lists", ctypes.c_int32), ("halved", ctypes.c_int32), ("tile_words", ctypes.c_int32),
+                ("n_lists", ctypes.c_int32), ("halved", ctypes.c_int32), ("key_bits", ctypes.c_int32),
+                ("tile_words", ctypes.c_int32),
                 ("n_in", ctypes.c_int64), ("n_out", ctypes.c_int64),
                 ("n_in_dev", ctypes.c_void_p), ("n_out_dev", ctypes.c_void_p),
                 ("in_keys", ctypes.c_void_p), ("out_keys", ctypes.c_void_p),
@@ -114,12 +115,15 @@ def lib():
             "spc_downsample_mask": ([PackSpec, I32], ctypes.c_uint64),
             "spc_pack_sort_workspace_size": ([I64], SZ),
             "spc_pack_sort": ([P, I64, P, PackSpec, P, P, P, P, SZ, P], ctypes.c_int),
+            "spc_pack_sort32": ([P, I64, P, PackSpec, P, P, P, P, SZ, P], ctypes.c_int),
             "spc_gather_rows": ([P, I64, P, I64, P, I32, P, I64, P], ctypes.c_int),
             "spc_downsample_workspace_size": ([I64, I32], SZ),
             "spc_downsample": ([P, I64, P, PackSpec, I32, P, P, P, P, SZ, P], ctypes.c_int),
             "spc_kmap_bytes": ([Geom, I32, U32, I64, I64], SZ),
             "spc_build_kmap": ([P, I64, P, P, I64, P, PackSpec, Geom, I32, U32, P, SZ, P,
                                 ctypes.POINTER(_Kmap), P], ctypes.c_int),
+            "spc_build_kmap32": ([P, I64, P, P, I64, P, PackSpec, Geom, I32, U32, P, SZ, P,
+                                  ctypes.POINTER(_Kmap), P], ctypes.c_int),
             "spc_kmap_export": ([ctypes.POINTER(_Kmap), P, I64, ctypes.POINTER(I64), P], ctypes.c_int),
             "spc_prepared_weight_bytes": ([I32, I32, I32, I32], SZ),
             "spc_prepare_weight": ([P, I32, I32, I32, I32, P, P], ctypes.c_int),
@@ -238,13 +242,14 @@ def spc_downsample_mask(spec: PackSpec, m: int) -> int:
 
 
 def spc_pack_sort(coords: torch.Tensor, spec: PackSpec, status: torch.Tensor | None = None, stream=None,
-                  keys_out=None, perm_out=None, ws=None, n_dev=None):
+                  keys_out=None, perm_out=None, ws=None, n_dev=None, key_bits: int = 64):
     """coords int32 [n,4] (b,x,y,z) on the GPU -> (keys uint64-as-int64 [n], perm int32 [n], status uint32[1]).
-    ``n_dev``: optional device int64 live row count (<= n); rows beyond it are ignored."""
+    ``n_dev``: optional device int64 live row count (<= n); rows beyond it are ignored.
+    ``key_bits=32``: uint32 keys (as int32) through spc_pack_sort32 (spec fields <= 32 bits)."""
     assert coords.is_cuda and coords.dtype == torch.int32 and coords.is_contiguous() and coords.shape[-1] == 4
     n = coords.shape[0]
     dev = coords.device
-    keys = keys_out if keys_out is not None else _alloc(n, torch.int64, dev, stream)
+    keys = keys_out if keys_out is not None else _alloc(n, torch.int32 if key_bits == 32 else torch.int64, dev, stream)
     perm = perm_out if perm_out is not None else _alloc(n, torch.int32, dev, stream)
     if status is None:
         status = _alloc(1, torch.int32, dev, stream, zero=True)
@@ -253,7 +258,8 @@ def spc_pack_sort(coords: torch.Tensor, spec: PackSpec, status: torch.Tensor | N
     own_ws = ws is None or ws.numel() < wsb
     if own_ws:
         ws = _ws(wsb, dev, stream=stream)
-    _check(L.spc_pack_sort(_ptr(coords), n, _ptr(n_dev), spec, _ptr(keys), _ptr(perm), _ptr(status), _ptr(ws), ws.numel(),
+    fn = L.spc_pack_sort32 if keys.dtype == torch.int32 else L.spc_pack_sort
+    _check(fn(_ptr(coords), n, _ptr(n_dev), spec, _ptr(keys), _ptr(perm), _ptr(status), _ptr(ws), ws.numel(),
                            _stream(stream)), "spc_pack_sort")
     if own_ws:
         _release(ws, stream)
@@ -399,7 +405,8 @@ def spc_build_kmap(in_keys: torch.Tensor, out_keys: torch.Tensor, spec: PackSpec
     off = (-buf.data_ptr()) % 256
     buf = buf[off:off + nbytes]
     km = _Kmap()
-    _check(lib().spc_build_kmap(_ptr(in_keys), n_in, _ptr(n_in_dev), _ptr(out_keys), n_out, _ptr(n_out_dev), spec,
+    fn = lib().spc_build_kmap32 if in_keys.dtype == torch.int32 else lib().spc_build_kmap
+    _check(fn(_ptr(in_keys), n_in, _ptr(n_in_dev), _ptr(out_keys), n_out, _ptr(n_out_dev), spec,
                                 geom, int(t), int(flags), _ptr(buf), nbytes, _ptr(status), ctypes.byref(km),
                                 _stream(stream)), "spc_build_kmap")
     return KernelMap(km, buf, (in_keys, out_keys, n_in_dev, n_out_dev))

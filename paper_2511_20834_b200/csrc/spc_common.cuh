@@ -178,6 +178,10 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 namespace spc {
 // radix sort of (keys, optional int32 values) over bits [0, n_bits); result in keys_out / vals_out
 size_t radix_sort_workspace(int64_t n, bool with_vals);
+spc_status radix_sort(const uint32_t *keys_in, const int32_t *vals_in, int64_t n, const int64_t *n_dev, int n_bits,
+                      uint32_t *keys_out, int32_t *vals_out, void *ws, size_t ws_bytes, cudaStream_t st, bool hist_done);
+spc_status flag_unsorted(const void *keys, int key_bytes, int64_t n_cap, const int64_t *n_dev, uint32_t *status,
+                         cudaStream_t st);
 spc_status radix_sort(const uint64_t *keys_in, const int32_t *vals_in /*nullable: identity*/, int64_t n,
                       const int64_t *n_dev, int n_bits, uint64_t *keys_out, int32_t *vals_out /*nullable*/,
                       void *ws, size_t ws_bytes, cudaStream_t st, bool hist_done);

@@ -32,8 +32,8 @@ constexpr int KM_WARPS = KM_THREADS / 32;
 // every map of a network (phase 2 of network-wide indexing) with the descriptors
 // passed as kernel parameters.
 struct KmapDesc {
-    const uint64_t *in;
-    const uint64_t *out;
+    const void *in;           // sorted keys: uint64 (KmapBatch.key_bytes 8) or uint32 (4)
+    const void *out;
     int64_t n_in_cap, n_out_cap;
     const int64_t *n_in_dev;
     const int64_t *n_out_dev;
@@ -60,6 +60,7 @@ struct KmapBatch {
     int bits_y, bits_z;
     unsigned int *work_ctr;   // zeroed before the launch
     int pool_keys;            // usable keys of the shared window pool (<= KM_POOL; SPC_OPT_KMAP_POOL_KEYS)
+    int key_bytes;            // 8: 64-bit keys, 4: 32-bit single-scan keys
     // density order: keys of all ordered maps, concatenated in ord_idx order by live counts
     uint64_t *ord_keys;
     int64_t *ord_total;       // sum of their live rows (written by k_kmap_prep)
@@ -67,7 +68,8 @@ struct KmapBatch {
     KmapDesc d[KM_MAX_MAPS];
 };
 
-__device__ __forceinline__ int64_t lower_bound_g(const uint64_t *__restrict__ a, int64_t n, uint64_t q) {
+template <typename KeyT>
+__device__ __forceinline__ int64_t lower_bound_g(const KeyT *__restrict__ a, int64_t n, KeyT q) {
     int64_t lo = 0, len = n;
     while (len > 0) {
         int64_t half = len >> 1;
@@ -128,6 +130,7 @@ __device__ __forceinline__ int64_t group_delta(const KmapDesc &p, int by, int bz
 // keys holding all matches of a tile's outputs for one offset group.  One thread per
 // bound, so the global binary searches' latency chains all run concurrently instead of
 // once per tile inside the build kernel.
+template <typename KeyT>
 __global__ void __launch_bounds__(256) k_kmap_bounds(const __grid_constant__ KmapBatch B) {
     pdl_wait();   // PDL launch: the predecessor has completed and flushed
     pdl_trigger();
@@ -155,16 +158,20 @@ __global__ void __launch_bounds__(256) k_kmap_bounds(const __grid_constant__ Kma
         const int64_t n_in = dev_count(p.n_in_cap, p.n_in_dev);
         const int64_t row0 = tile * KM_BM;
         const int rows = (int)imin64(KM_BM, n_out - row0);
-        const uint64_t q = hi ? p.out[row0 + rows - 1] + (uint64_t)group_delta(p, B.bits_y, B.bits_z, g, p.K - 1) + 1ull
-                              : p.out[row0] + (uint64_t)group_delta(p, B.bits_y, B.bits_z, g, 0);
-        p.bounds[local] = (int32_t)lower_bound_g(p.in, n_in, q);
+        const KeyT *in = static_cast<const KeyT *>(p.in), *out = static_cast<const KeyT *>(p.out);
+        // packed(q) + packed(delta) in KeyT arithmetic: the planned headroom keeps the
+        // true sum inside the key range, so the wrap-around addition is exact
+        const KeyT q = hi ? (KeyT)(out[row0 + rows - 1] + (KeyT)group_delta(p, B.bits_y, B.bits_z, g, p.K - 1) + (KeyT)1)
+                          : (KeyT)(out[row0] + (KeyT)group_delta(p, B.bits_y, B.bits_z, g, 0));
+        p.bounds[local] = (int32_t)lower_bound_g(in, n_in, q);
     }
 }
 
 // per-tile shared state of k_kmap_zdelta (the tile's OS / WS tables live in dynamic smem)
 constexpr int KM_POOL = 4096;      // staged window keys per CTA (32 KB); a group that does not fit searches global
+template <typename KeyT>
 struct ZTile {
-    uint64_t q[KM_BM];              // the tile's output keys
+    KeyT q[KM_BM];                  // the tile's output keys
     uint32_t ordk[KM_BM];           // density-order direction bits per row
     int32_t cnt[SPC_MAX_KVOL];      // matches per weight offset
     int32_t wlo[25], wlen[25], woff[25];   // per offset group: window start / length / pool offset (-1: global)
@@ -182,13 +189,13 @@ __device__ __forceinline__ int tile_map(const int64_t *pre, int n_maps, int64_t 
 
 // lower bound in a staged (shared) or global window; every call is counted in n_calls
 // (the search-count law |V_q| K^2 of P:297 is checked against this counter)
-template <bool SM>
-__device__ __forceinline__ int lb_win(const uint64_t *a, int n, uint64_t q, unsigned &n_calls) {
+template <typename KeyT, bool SM>
+__device__ __forceinline__ int lb_win(const KeyT *a, int n, KeyT q, unsigned &n_calls) {
     ++n_calls;
     int lo = 0, len = n;
     while (len > 0) {
         const int half = len >> 1;
-        uint64_t v;
+        KeyT v;
         if (SM) v = a[lo + half];
         else v = __ldg(a + lo + half);
         if (v < q) {
@@ -206,23 +213,23 @@ __device__ __forceinline__ int lb_win(const uint64_t *a, int n, uint64_t q, unsi
 // K-1 members -- in the group's window of input keys.  Every stored entry is
 // written to the tile's shared tables (-1 = no match): OS columns [row][K_dense], WS lists
 // [list][row]; counts, mask bits and density-order bits go to shared accumulators.
-template <int K, bool SM>
-__device__ __forceinline__ int zdelta_chunk(ZTile &zt, int32_t *s_os, int32_t *s_ws, int KD, const uint64_t *wk,
+template <typename KeyT, int K, bool SM>
+__device__ __forceinline__ int zdelta_chunk(ZTile<KeyT> &zt, int32_t *s_os, int32_t *s_ws, int KD, const KeyT *wk,
                                             int wl, int32_t lo, int g, int ch, int rows, int lane, unsigned &n_calls) {
     const int lr = ch * 32 + lane;
     const bool valid = lr < rows;
-    const uint64_t q = valid ? zt.q[lr] : 0;
+    const KeyT q = valid ? zt.q[lr] : (KeyT)0;
     int pos = 0;
-    if (valid) pos = lb_win<SM>(wk, wl, q + (uint64_t)zt.dq[g * K], n_calls);
+    if (valid) pos = lb_win<KeyT, SM>(wk, wl, (KeyT)(q + (KeyT)zt.dq[g * K]), n_calls);
     const int pos0 = pos;
     uint32_t key = 0;
 #pragma unroll
     for (int mm = 0; mm < K; ++mm) {   // members in ascending query order
-        const uint64_t query = q + (uint64_t)zt.dq[g * K + mm];
+        const KeyT query = (KeyT)(q + (KeyT)zt.dq[g * K + mm]);
         const int32_t dsc = zt.dsc[g * K + mm];
         bool match = false;
         if (valid) {
-            uint64_t v = 0;
+            KeyT v = 0;
             while (pos < wl && (v = (SM ? wk[pos] : __ldg(wk + pos))) < query) ++pos;
             match = pos < wl && v == query;
         }
@@ -252,6 +259,7 @@ constexpr int KM_MIN_BLOCKS = 4;
 // P:400) as 16-byte stores, each WS list's pairs compacted with one reservation per
 // (tile, list) (warp ballots, no filter pass; halved for submanifold maps,
 // P:418-421), the tile mask, per-offset counts and density-order keys.
+template <typename KeyT>
 __global__ void __launch_bounds__(KM_THREADS, KM_MIN_BLOCKS) k_kmap_zdelta(const __grid_constant__ KmapBatch B) {
     pdl_wait();   // PDL launch: the predecessor has completed and flushed
     pdl_trigger();
@@ -260,8 +268,8 @@ __global__ void __launch_bounds__(KM_THREADS, KM_MIN_BLOCKS) k_kmap_zdelta(const
     __shared__ int64_t s_pre[KM_MAX_MAPS + 1];             // tile prefix over the maps
     __shared__ int64_t s_ordbase[KM_MAX_MAPS];
     __shared__ int64_t s_nout[KM_MAX_MAPS];
-    __shared__ __align__(16) uint64_t s_pool[KM_POOL];
-    __shared__ ZTile zt;
+    __shared__ __align__(16) KeyT s_pool[KM_POOL];
+    __shared__ ZTile<KeyT> zt;
     extern __shared__ __align__(16) int32_t s_tab[];        // [KM_BM x K_dense] OS, then [lists x KM_BM] WS
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -291,14 +299,14 @@ __global__ void __launch_bounds__(KM_THREADS, KM_MIN_BLOCKS) k_kmap_zdelta(const
     int stats_map = -1;
     // software pipeline: the next tile's output keys and window bounds are loaded into
     // registers while the current tile flushes (one global round trip off the tile chain)
-    uint64_t pf_q = 0;
+    KeyT pf_q = 0;
     int32_t pf_lo = 0, pf_hi = 0;
     auto prefetch = [&](int64_t vn, int mn) {
         if (vn >= total) return;
         const KmapDesc &pn = B.d[mn];
         const int64_t tn = vn - s_pre[mn];
         const int rn = (int)imin64(KM_BM, s_nout[mn] - tn * KM_BM);
-        if (tid < rn) pf_q = pn.out[tn * KM_BM + tid];
+        if (tid < rn) pf_q = static_cast<const KeyT *>(pn.out)[tn * KM_BM + tid];
         const int Gn = pn.K * pn.K;
         if (lane < Gn) {
             const int2 b2 = *reinterpret_cast<const int2 *>(pn.bounds + (tn * Gn + lane) * 2);
@@ -366,12 +374,12 @@ __global__ void __launch_bounds__(KM_THREADS, KM_MIN_BLOCKS) k_kmap_zdelta(const
                 const int glo = __shfl_sync(0xffffffffu, lo, gg), gwl = __shfl_sync(0xffffffffu, wl, gg);
                 const int goff = __shfl_sync(0xffffffffu, off, gg);
                 if (!__shfl_sync(0xffffffffu, fits ? 1 : 0, gg)) continue;
-                const uint64_t *src = p.in + glo;
-                uint64_t *dst = s_pool + goff;
+                const KeyT *src = static_cast<const KeyT *>(p.in) + glo;
+                KeyT *dst = s_pool + goff;
                 int e = lane;
                 for (; e + 96 < gwl; e += 128) {
-                    const uint64_t a0 = __ldg(src + e), a1 = __ldg(src + e + 32), a2 = __ldg(src + e + 64),
-                                   a3 = __ldg(src + e + 96);
+                    const KeyT a0 = __ldg(src + e), a1 = __ldg(src + e + 32), a2 = __ldg(src + e + 64),
+                               a3 = __ldg(src + e + 96);
                     dst[e] = a0; dst[e + 32] = a1; dst[e + 64] = a2; dst[e + 96] = a3;
                 }
                 for (; e < gwl; e += 32) dst[e] = __ldg(src + e);
@@ -402,13 +410,15 @@ __global__ void __launch_bounds__(KM_THREADS, KM_MIN_BLOCKS) k_kmap_zdelta(const
             const int off = zt.woff[g];
             int adv;
             if (off >= 0) {
-                if (K == 3) adv = zdelta_chunk<3, true>(zt, s_os, s_ws, KD, s_pool + off, wl, lo, g, ch, rows, lane, n_calls);
-                else if (K == 5) adv = zdelta_chunk<5, true>(zt, s_os, s_ws, KD, s_pool + off, wl, lo, g, ch, rows, lane, n_calls);
-                else adv = zdelta_chunk<1, true>(zt, s_os, s_ws, KD, s_pool + off, wl, lo, g, ch, rows, lane, n_calls);
+                const KeyT *wk = s_pool + off;
+                if (K == 3) adv = zdelta_chunk<KeyT, 3, true>(zt, s_os, s_ws, KD, wk, wl, lo, g, ch, rows, lane, n_calls);
+                else if (K == 5) adv = zdelta_chunk<KeyT, 5, true>(zt, s_os, s_ws, KD, wk, wl, lo, g, ch, rows, lane, n_calls);
+                else adv = zdelta_chunk<KeyT, 1, true>(zt, s_os, s_ws, KD, wk, wl, lo, g, ch, rows, lane, n_calls);
             } else {
-                if (K == 3) adv = zdelta_chunk<3, false>(zt, s_os, s_ws, KD, p.in + lo, wl, lo, g, ch, rows, lane, n_calls);
-                else if (K == 5) adv = zdelta_chunk<5, false>(zt, s_os, s_ws, KD, p.in + lo, wl, lo, g, ch, rows, lane, n_calls);
-                else adv = zdelta_chunk<1, false>(zt, s_os, s_ws, KD, p.in + lo, wl, lo, g, ch, rows, lane, n_calls);
+                const KeyT *wk = static_cast<const KeyT *>(p.in) + lo;
+                if (K == 3) adv = zdelta_chunk<KeyT, 3, false>(zt, s_os, s_ws, KD, wk, wl, lo, g, ch, rows, lane, n_calls);
+                else if (K == 5) adv = zdelta_chunk<KeyT, 5, false>(zt, s_os, s_ws, KD, wk, wl, lo, g, ch, rows, lane, n_calls);
+                else adv = zdelta_chunk<KeyT, 1, false>(zt, s_os, s_ws, KD, wk, wl, lo, g, ch, rows, lane, n_calls);
             }
             n_probe += (unsigned long long)adv;
         }
@@ -498,9 +508,10 @@ __global__ void __launch_bounds__(256) k_kmap_bsearch(const __grid_constant__ Km
         bool match = false;
         int32_t j = -1;
         if (valid) {
-            const uint64_t q = p.out[i] + (uint64_t)d;
-            const int64_t pos = lower_bound_g(p.in, n_in, q);
-            match = pos < n_in && __ldg(p.in + pos) == q;
+            const uint64_t *in = static_cast<const uint64_t *>(p.in);
+            const uint64_t q = static_cast<const uint64_t *>(p.out)[i] + (uint64_t)d;
+            const int64_t pos = lower_bound_g(in, n_in, q);
+            match = pos < n_in && __ldg(in + pos) == q;
             if (match) j = (int32_t)pos;
             p.os[i * p.k_dense + col] = j;
         }
@@ -890,7 +901,8 @@ static spc_status launch_kmaps(const KmapBatch &b0, int max_k_dense, int64_t max
         int64_t items = 0;
         for (int m = 0; m < b.n_maps; ++m) items += ((b.d[m].n_out_cap + KM_BM - 1) / KM_BM) * 2 * b.d[m].K * b.d[m].K;
         const int g = (int)std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, 16 * (int64_t)num_sms()));
-        SPC_CUDA(launch_pdl(k_kmap_bounds, dim3(g), dim3(256), 0, st, b));
+        if (b.key_bytes == 4) SPC_CUDA(launch_pdl(k_kmap_bounds<uint32_t>, dim3(g), dim3(256), 0, st, b));
+        else SPC_CUDA(launch_pdl(k_kmap_bounds<uint64_t>, dim3(g), dim3(256), 0, st, b));
         SPC_LAUNCH_CHECK("k_kmap_bounds");
     }
     // one CTA per (map, tile); the OS block of a tile is staged in dynamic shared memory
@@ -902,19 +914,20 @@ static spc_status launch_kmaps(const KmapBatch &b0, int max_k_dense, int64_t max
     }
     (void)max_k_dense;
     const size_t dsm = (size_t)KM_BM * max_cols * sizeof(int32_t);
-    static size_t dsm_set[64] = {};   // per device
+    void (*kz)(KmapBatch) = b.key_bytes == 4 ? k_kmap_zdelta<uint32_t> : k_kmap_zdelta<uint64_t>;
+    static size_t dsm_set[2][64] = {};   // per key width and device
     const int dev = current_device();
-    if (dsm > dsm_set[dev]) {
-        SPC_CUDA(cudaFuncSetAttribute(k_kmap_zdelta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
-        dsm_set[dev] = dsm;
+    if (dsm > dsm_set[b.key_bytes == 4][dev]) {
+        SPC_CUDA(cudaFuncSetAttribute(kz, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+        dsm_set[b.key_bytes == 4][dev] = dsm;
     }
     int per_sm = 0;
-    SPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_kmap_zdelta, KM_THREADS, dsm));
+    SPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kz, KM_THREADS, dsm));
     int64_t tiles = 0;
     for (int m = 0; m < b.n_maps; ++m) tiles += (b.d[m].n_out_cap + KM_BM - 1) / KM_BM;
     (void)max_tiles;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)num_sms() * std::max(1, per_sm)));
-    SPC_CUDA(launch_pdl(k_kmap_zdelta, dim3((unsigned)grid), dim3(KM_THREADS), dsm, st, b));
+    SPC_CUDA(launch_pdl(kz, dim3((unsigned)grid), dim3(KM_THREADS), dsm, st, b));
     SPC_LAUNCH_CHECK("k_kmap_zdelta");
     return SPC_OK;
 }
@@ -931,14 +944,11 @@ extern "C" size_t spc_kmap_bytes(spc_geom geom, int32_t t, uint32_t flags, int64
 }
 
 namespace spc {
-__global__ void k_flag_dups(const uint64_t *keys, int64_t n_cap, const int64_t *n_dev, uint32_t *status,
-                            uint32_t flag);
-}
-
-extern "C" spc_status spc_build_kmap(const uint64_t *in_keys, int64_t n_in, const int64_t *n_in_dev,
-                                     const uint64_t *out_keys, int64_t n_out, const int64_t *n_out_dev,
-                                     spc_pack_spec spec, spc_geom geom, int32_t t, uint32_t flags, void *buf,
-                                     size_t buf_bytes, uint32_t *status, spc_kmap *kmap_out, void *stream) {
+// one build for 64-bit (key_bytes 8) or 32-bit single-scan (key_bytes 4) sorted keys
+static spc_status build_kmap(const void *in_keys, int64_t n_in, const int64_t *n_in_dev, const void *out_keys,
+                             int64_t n_out, const int64_t *n_out_dev, spc_pack_spec spec, spc_geom geom, int32_t t,
+                             uint32_t flags, void *buf, size_t buf_bytes, uint32_t *status, spc_kmap *kmap_out,
+                             void *stream, int key_bytes) {
     SPC_CHECK_ARG(kmap_out, "null kmap_out");
     SPC_CHECK_ARG(n_in >= 0 && n_out >= 0, "negative size");
     SPC_CHECK_ARG(n_in < INT32_MAX && n_out < INT32_MAX, "sizes must fit int32 indices");
@@ -981,8 +991,9 @@ extern "C" spc_status spc_build_kmap(const uint64_t *in_keys, int64_t n_in, cons
     km.n_out = n_out;
     km.n_in_dev = n_in_dev;
     km.n_out_dev = n_out_dev;
-    km.in_keys = in_keys;
-    km.out_keys = out_keys;
+    km.in_keys = static_cast<const uint64_t *>(in_keys);     // (uint32 keys when key_bits == 32)
+    km.out_keys = static_cast<const uint64_t *>(out_keys);
+    km.key_bits = 8 * key_bytes;
     km.os_table = reinterpret_cast<int32_t *>(base + L.os);
     km.ws_pairs = reinterpret_cast<int32_t *>(base + L.pairs);
     km.counts_dev = reinterpret_cast<int32_t *>(base + L.counts);
@@ -1018,15 +1029,18 @@ extern "C" spc_status spc_build_kmap(const uint64_t *in_keys, int64_t n_in, cons
         return SPC_OK;
     }
     if ((flags & SPC_KMAP_CHECK_SORTED) && status) {
-        SPC_CUDA(launch_pdl(k_flag_dups, dim3(64), dim3(256), 0, st, in_keys, n_in, n_in_dev, status, SPC_FLAG_UNSORTED));
-        SPC_CUDA(launch_pdl(k_flag_dups, dim3(64), dim3(256), 0, st, out_keys, n_out, n_out_dev, status, SPC_FLAG_UNSORTED));
+        s = flag_unsorted(in_keys, key_bytes, n_in, n_in_dev, status, st);
+        if (s == SPC_OK) s = flag_unsorted(out_keys, key_bytes, n_out, n_out_dev, status, st);
+        if (s != SPC_OK) return s;
     }
 
     if (g_defer.active) {
         // network-wide phase 2: collect, launch once in kmap_defer_end()
+        if (key_bytes != 8) return fail(SPC_ERR_UNSUPPORTED, "network-wide kernel maps use 64-bit keys");
         KmapBatch &b = g_defer.b;
         if (b.n_maps >= KM_MAX_MAPS) return fail(SPC_ERR_CAPACITY, "too many distinct kernel maps in one batch");
         if (b.n_maps == 0) {
+            b.key_bytes = 8;
             b.bits_y = spec.bits_y;
             b.bits_z = spec.bits_z;
             b.work_ctr = reinterpret_cast<unsigned int *>(base + L.stats) + 4;
@@ -1045,6 +1059,7 @@ extern "C" spc_status spc_build_kmap(const uint64_t *in_keys, int64_t n_in, cons
     }
     if (flags & SPC_KMAP_SIMPLE_BSEARCH) {
         // ablation baseline: all-OS maps only, no density order
+        if (key_bytes != 8) return fail(SPC_ERR_UNSUPPORTED, "SPC_KMAP_SIMPLE_BSEARCH uses 64-bit keys");
         if (pl.n_lists != 0) return fail(SPC_ERR_UNSUPPORTED, "SPC_KMAP_SIMPLE_BSEARCH needs an all-OS t (SPC_T_ALL_OS)");
         KmapDesc d;
         fill_desc(d, km, pl, reinterpret_cast<int32_t *>(base + L.bounds));
@@ -1064,6 +1079,7 @@ extern "C" spc_status spc_build_kmap(const uint64_t *in_keys, int64_t n_in, cons
     b.bits_y = spec.bits_y;
     b.bits_z = spec.bits_z;
     b.work_ctr = reinterpret_cast<unsigned int *>(base + L.stats) + 4;   // scratch after the stats
+    b.key_bytes = key_bytes;
     fill_desc(b.d[0], km, pl, reinterpret_cast<int32_t *>(base + L.bounds));
     OrderScratch os{};
     if (order) {
@@ -1077,6 +1093,25 @@ extern "C" spc_status spc_build_kmap(const uint64_t *in_keys, int64_t n_in, cons
     s = launch_kmaps(b, pl.k_dense, (int64_t)L.tiles, st);
     if (s == SPC_OK && order) s = run_orders(std::vector<OrderJob>{job}, os, n_out, st);
     return s;
+}
+}  // namespace spc
+
+extern "C" spc_status spc_build_kmap(const uint64_t *in_keys, int64_t n_in, const int64_t *n_in_dev,
+                                     const uint64_t *out_keys, int64_t n_out, const int64_t *n_out_dev,
+                                     spc_pack_spec spec, spc_geom geom, int32_t t, uint32_t flags, void *buf,
+                                     size_t buf_bytes, uint32_t *status, spc_kmap *kmap_out, void *stream) {
+    return build_kmap(in_keys, n_in, n_in_dev, out_keys, n_out, n_out_dev, spec, geom, t, flags, buf, buf_bytes, status,
+                      kmap_out, stream, 8);
+}
+
+extern "C" spc_status spc_build_kmap32(const uint32_t *in_keys, int64_t n_in, const int64_t *n_in_dev,
+                                       const uint32_t *out_keys, int64_t n_out, const int64_t *n_out_dev,
+                                       spc_pack_spec spec, spc_geom geom, int32_t t, uint32_t flags, void *buf,
+                                       size_t buf_bytes, uint32_t *status, spc_kmap *kmap_out, void *stream) {
+    if (spec.bits_b + spec.bits_x + spec.bits_y + spec.bits_z > 32)
+        return fail(SPC_ERR_RANGE, "spc_build_kmap32: the pack spec needs more than 32 bits");
+    return build_kmap(in_keys, n_in, n_in_dev, out_keys, n_out, n_out_dev, spec, geom, t, flags, buf, buf_bytes, status,
+                      kmap_out, stream, 4);
 }
 
 namespace spc {
@@ -1132,8 +1167,8 @@ __global__ void k_shard_ranges(const uint64_t *__restrict__ in, int64_t n_in_cap
     const int64_t lo = n_out * r / n_shards, hi = n_out * (r + 1) / n_shards;
     int64_t ilo = 0, ihi = 0;
     if (hi > lo) {
-        ilo = lower_bound_g(in, n_in, out[lo] + (uint64_t)d_min);
-        ihi = lower_bound_g(in, n_in, out[hi - 1] + (uint64_t)d_max + 1ull);
+        ilo = lower_bound_g<uint64_t>(in, n_in, out[lo] + (uint64_t)d_min);
+        ihi = lower_bound_g<uint64_t>(in, n_in, out[hi - 1] + (uint64_t)d_max + 1ull);
     }
     bounds[4 * r] = lo;
     bounds[4 * r + 1] = hi;

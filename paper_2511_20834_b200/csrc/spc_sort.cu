@@ -60,7 +60,8 @@ constexpr int OS_ITEMS_MIN = 2;
 constexpr int MAX_PASSES = 8;
 constexpr uint32_t ST_AGG = 1u << 30, ST_INC = 2u << 30, ST_VAL = (1u << 30) - 1;
 
-__global__ void __launch_bounds__(SORT_THREADS) k_hist_all(const uint64_t *__restrict__ keys, int64_t n_cap,
+template <typename KeyT>
+__global__ void __launch_bounds__(SORT_THREADS) k_hist_all(const KeyT *__restrict__ keys, int64_t n_cap,
                                                            const int64_t *n_dev, int passes,
                                                            unsigned int *__restrict__ ghist) {
     pdl_wait();   // PDL launch: the predecessor has completed and flushed
@@ -70,7 +71,7 @@ __global__ void __launch_bounds__(SORT_THREADS) k_hist_all(const uint64_t *__res
     __syncthreads();
     const int64_t n = dev_count(n_cap, n_dev);
     for (int64_t i = blockIdx.x * (int64_t)SORT_THREADS + threadIdx.x; i < n; i += (int64_t)gridDim.x * SORT_THREADS) {
-        const uint64_t k = keys[i];
+        const KeyT k = keys[i];
         for (int p = 0; p < passes; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 255u], 1u);
     }
     __syncthreads();
@@ -98,13 +99,13 @@ __global__ void k_hist_scan(unsigned int *__restrict__ ghist, int passes) {
     }
 }
 
-template <bool VALS, int OS_ITEMS>
-__global__ void __launch_bounds__(SORT_THREADS) k_onesweep(const uint64_t *__restrict__ keys_in,
+template <typename KeyT, bool VALS, int OS_ITEMS>
+__global__ void __launch_bounds__(SORT_THREADS) k_onesweep(const KeyT *__restrict__ keys_in,
                                                            const int32_t *__restrict__ vals_in, int64_t n_cap,
                                                            const int64_t *n_dev, int shift,
                                                            const unsigned int *__restrict__ gbase,
                                                            unsigned int *tile_status, unsigned int *tile_counter,
-                                                           uint64_t *__restrict__ keys_out,
+                                                           KeyT *__restrict__ keys_out,
                                                            int32_t *__restrict__ vals_out) {
     pdl_wait();   // PDL launch: the predecessor has completed and flushed
     pdl_trigger();
@@ -114,7 +115,7 @@ __global__ void __launch_bounds__(SORT_THREADS) k_onesweep(const uint64_t *__res
     __shared__ int cnt[SORT_WARPS][256];
     __shared__ int warp_sums[SORT_WARPS];
     constexpr int OS_TILE = SORT_THREADS * OS_ITEMS;
-    __shared__ uint64_t skeys[OS_TILE];
+    __shared__ KeyT skeys[OS_TILE];
     __shared__ int32_t svals[VALS ? OS_TILE : 1];
 
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -128,7 +129,7 @@ __global__ void __launch_bounds__(SORT_THREADS) k_onesweep(const uint64_t *__res
     if (base >= n) return;
     const int tile_valid = (int)imin64(OS_TILE, n - base);
 
-    uint64_t key[OS_ITEMS];
+    KeyT key[OS_ITEMS];
     int32_t val[OS_ITEMS];
     int rank[OS_ITEMS];
     unsigned dig[OS_ITEMS];
@@ -137,7 +138,7 @@ __global__ void __launch_bounds__(SORT_THREADS) k_onesweep(const uint64_t *__res
         const int li = w * (32 * OS_ITEMS) + r * 32 + lane;   // warp-contiguous chunk: stable order
         const int64_t idx = base + li;
         const bool valid = li < tile_valid;
-        key[r] = valid ? keys_in[idx] : ~0ull;
+        key[r] = valid ? keys_in[idx] : (KeyT)~0ull;
         if (VALS) val[r] = valid ? (vals_in ? vals_in[idx] : (int32_t)idx) : 0;
         dig[r] = valid ? (unsigned)((key[r] >> shift) & 255u) : 256u + lane;
         const unsigned peers = __match_any_sync(0xffffffffu, dig[r]);
@@ -206,7 +207,7 @@ __global__ void __launch_bounds__(SORT_THREADS) k_onesweep(const uint64_t *__res
     }
     __syncthreads();
     for (int s = tid; s < tile_valid; s += SORT_THREADS) {
-        const uint64_t k = skeys[s];
+        const KeyT k = skeys[s];
         const int d = (int)((k >> shift) & 255u);
         const int64_t g = (int64_t)gbase[d] + excl_s[d] + (s - local_start[d]);
         keys_out[g] = k;
@@ -214,8 +215,9 @@ __global__ void __launch_bounds__(SORT_THREADS) k_onesweep(const uint64_t *__res
     }
 }
 
-__global__ void k_copy_keys(const uint64_t *__restrict__ a, int64_t n_cap, const int64_t *n_dev,
-                            uint64_t *__restrict__ b, const int32_t *vals_in, int32_t *vals_out) {
+template <typename KeyT>
+__global__ void k_copy_keys(const KeyT *__restrict__ a, int64_t n_cap, const int64_t *n_dev,
+                            KeyT *__restrict__ b, const int32_t *vals_in, int32_t *vals_out) {
     pdl_wait();   // PDL launch: the predecessor has completed and flushed
     pdl_trigger();
     const int64_t n = dev_count(n_cap, n_dev);
@@ -242,9 +244,10 @@ size_t radix_sort_workspace(int64_t n, bool with_vals) {
     return s.used + 256;
 }
 
-spc_status radix_sort(const uint64_t *keys_in, const int32_t *vals_in, int64_t n, const int64_t *n_dev, int n_bits,
-                      uint64_t *keys_out, int32_t *vals_out, void *ws, size_t ws_bytes, cudaStream_t st,
-                      bool hist_done) {
+template <typename KeyT>
+static spc_status radix_sort_t(const KeyT *keys_in, const int32_t *vals_in, int64_t n, const int64_t *n_dev, int n_bits,
+                               KeyT *keys_out, int32_t *vals_out, void *ws, size_t ws_bytes, cudaStream_t st,
+                               bool hist_done) {
     if (n <= 0) return SPC_OK;
     const bool with_vals = vals_out != nullptr;
     const int passes = (n_bits + 7) / 8;
@@ -256,11 +259,11 @@ spc_status radix_sort(const uint64_t *keys_in, const int32_t *vals_in, int64_t n
     const size_t stride = (size_t)nt * 256 + 32;
     // (the workspace holds the status of the smallest tiles; only the used part is cleared)
     unsigned int *status = b.take<unsigned int>((size_t)MAX_PASSES * ((size_t)os_tiles(n, OS_ITEMS_MIN) * 256 + 32));
-    uint64_t *ktmp = b.take<uint64_t>((size_t)n);
+    KeyT *ktmp = b.take<KeyT>((size_t)n);
     int32_t *vtmp = with_vals ? b.take<int32_t>((size_t)n) : nullptr;
     if (!b.ok()) return fail(SPC_ERR_WORKSPACE, "radix_sort: workspace too small");
     if (passes == 0) {
-        SPC_CUDA(launch_pdl(k_copy_keys, dim3(256), dim3(256), 0, st, keys_in, n, n_dev, keys_out, vals_in, vals_out));
+        SPC_CUDA(launch_pdl(k_copy_keys<KeyT>, dim3(256), dim3(256), 0, st, keys_in, n, n_dev, keys_out, vals_in, vals_out));
         SPC_LAUNCH_CHECK("k_copy_keys");
         return SPC_OK;
     }
@@ -268,25 +271,25 @@ spc_status radix_sort(const uint64_t *keys_in, const int32_t *vals_in, int64_t n
     if (!hist_done) {
         SPC_CUDA(cudaMemsetAsync(hist, 0, sizeof(unsigned int) * MAX_PASSES * 256, st));
         const int g = (int)std::max<int64_t>(1, std::min<int64_t>((n + 4095) / 4096, 2 * num_sms()));
-        SPC_CUDA(launch_pdl(k_hist_all, dim3(g), dim3(SORT_THREADS), 0, st, keys_in, n, n_dev, passes, hist));
+        SPC_CUDA(launch_pdl(k_hist_all<KeyT>, dim3(g), dim3(SORT_THREADS), 0, st, keys_in, n, n_dev, passes, hist));
     }
     SPC_CUDA(launch_pdl(k_hist_scan, dim3(1), dim3(32 * MAX_PASSES), 0, st, hist, passes));
     SPC_LAUNCH_CHECK("radix histograms");
-    const uint64_t *src_k = keys_in;
+    const KeyT *src_k = keys_in;
     const int32_t *src_v = vals_in;
     for (int p = 0; p < passes; ++p) {
         const bool to_out = ((passes - 1 - p) % 2) == 0;
-        uint64_t *dst_k = to_out ? keys_out : ktmp;
+        KeyT *dst_k = to_out ? keys_out : ktmp;
         int32_t *dst_v = with_vals ? (to_out ? vals_out : vtmp) : nullptr;
         unsigned int *stp = status + (size_t)p * stride;
         unsigned int *ctr = stp + (size_t)nt * 256;
 #define SPC_ONESWEEP(IT)                                                                                     \
     do {                                                                                                     \
         if (with_vals)                                                                                       \
-            SPC_CUDA(launch_pdl(k_onesweep<true, IT>, dim3(nt), dim3(SORT_THREADS), 0, st, src_k, src_v, n, n_dev, 8 * p, hist + p * 256, stp, \
+            SPC_CUDA(launch_pdl(k_onesweep<KeyT, true, IT>, dim3(nt), dim3(SORT_THREADS), 0, st, src_k, src_v, n, n_dev, 8 * p, hist + p * 256, stp, \
                                                               ctr, dst_k, dst_v));                            \
         else                                                                                                 \
-            SPC_CUDA(launch_pdl(k_onesweep<false, IT>, dim3(nt), dim3(SORT_THREADS), 0, st, src_k, nullptr, n, n_dev, 8 * p, hist + p * 256,  \
+            SPC_CUDA(launch_pdl(k_onesweep<KeyT, false, IT>, dim3(nt), dim3(SORT_THREADS), 0, st, src_k, nullptr, n, n_dev, 8 * p, hist + p * 256,  \
                                                                stp, ctr, dst_k, nullptr));                    \
     } while (0)
         if (items == 2) SPC_ONESWEEP(2);
@@ -300,6 +303,17 @@ spc_status radix_sort(const uint64_t *keys_in, const int32_t *vals_in, int64_t n
     return SPC_OK;
 }
 
+spc_status radix_sort(const uint64_t *keys_in, const int32_t *vals_in, int64_t n, const int64_t *n_dev, int n_bits,
+                      uint64_t *keys_out, int32_t *vals_out, void *ws, size_t ws_bytes, cudaStream_t st,
+                      bool hist_done) {
+    return radix_sort_t(keys_in, vals_in, n, n_dev, n_bits, keys_out, vals_out, ws, ws_bytes, st, hist_done);
+}
+spc_status radix_sort(const uint32_t *keys_in, const int32_t *vals_in, int64_t n, const int64_t *n_dev, int n_bits,
+                      uint32_t *keys_out, int32_t *vals_out, void *ws, size_t ws_bytes, cudaStream_t st,
+                      bool hist_done) {
+    return radix_sort_t(keys_in, vals_in, n, n_dev, n_bits, keys_out, vals_out, ws, ws_bytes, st, hist_done);
+}
+
 // ------------------------------------------------------------------------------------
 // A1 pack + duplicate flag
 // ------------------------------------------------------------------------------------
@@ -308,8 +322,9 @@ struct PackDev {
     int lo_room, hi_room;   // planned headroom below / above (reading A4): (out_stride-1)+reach / reach
 };
 
+template <typename KeyT>
 __global__ void __launch_bounds__(256) k_pack(const int4 *__restrict__ coords, int64_t n_cap, const int64_t *n_dev, PackDev s,
-                                              uint64_t *__restrict__ keys, uint32_t *status, int passes,
+                                              KeyT *__restrict__ keys, uint32_t *status, int passes,
                                               unsigned int *__restrict__ ghist) {
     pdl_wait();   // PDL launch: the predecessor has completed and flushed
     pdl_trigger();
@@ -332,7 +347,7 @@ __global__ void __launch_bounds__(256) k_pack(const int4 *__restrict__ coords, i
         bad |= !ok;
         uint64_t k = ((uint64_t)fb << (s.bx + s.by + s.bz)) | ((uint64_t)fx << (s.by + s.bz)) |
                      ((uint64_t)fy << s.bz) | (uint64_t)fz;
-        keys[i] = k;
+        keys[i] = (KeyT)k;
         for (int p = 0; p < passes; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 255u], 1u);   // sort histograms
     }
     if (__any_sync(0xffffffffu, bad) && status && (threadIdx.x & 31) == 0) atomicOr(status, SPC_FLAG_RANGE);
@@ -341,7 +356,8 @@ __global__ void __launch_bounds__(256) k_pack(const int4 *__restrict__ coords, i
         if (h[i / 256][i % 256]) atomicAdd(&ghist[i], h[i / 256][i % 256]);
 }
 
-__global__ void k_flag_dups(const uint64_t *__restrict__ keys, int64_t n_cap, const int64_t *n_dev,
+template <typename KeyT>
+__global__ void k_flag_dups(const KeyT *__restrict__ keys, int64_t n_cap, const int64_t *n_dev,
                             uint32_t *status, uint32_t flag) {
     pdl_wait();   // PDL launch: the predecessor has completed and flushed
     pdl_trigger();
@@ -519,9 +535,12 @@ extern "C" size_t spc_pack_sort_workspace_size(int64_t n) {
     return align_up(sizeof(uint64_t) * (size_t)n, 256) + radix_sort_workspace(n, true) + 256;
 }
 
-extern "C" spc_status spc_pack_sort(const int32_t *coords, int64_t n, const int64_t *n_dev, spc_pack_spec spec, uint64_t *keys_out,
-                                    int32_t *perm_out, uint32_t *status, void *ws, size_t ws_bytes,
-                                    void *stream) {
+namespace spc {
+// pack + sort for 64-bit keys, or 32-bit keys when the spec's fields total <= 32 bits (the
+// paper's default single-scan packing)
+template <typename KeyT>
+static spc_status pack_sort_t(const int32_t *coords, int64_t n, const int64_t *n_dev, spc_pack_spec spec, KeyT *keys_out,
+                              int32_t *perm_out, uint32_t *status, void *ws, size_t ws_bytes, void *stream) {
     SPC_CHECK_ARG(n >= 0, "n < 0");
     if (n == 0) return SPC_OK;
     SPC_CHECK_ARG(coords && keys_out, "null coords/keys_out");
@@ -529,12 +548,14 @@ extern "C" spc_status spc_pack_sort(const int32_t *coords, int64_t n, const int6
     const int used = spec.bits_b + spec.bits_x + spec.bits_y + spec.bits_z;
     SPC_CHECK_ARG(spec.bits_b >= 0 && spec.bits_x >= 2 && spec.bits_y >= 2 && spec.bits_z >= 2 && used <= 62,
                   "bad pack spec");
+    if (used > (int)(8 * sizeof(KeyT)))
+        return fail(SPC_ERR_RANGE, "spc_pack_sort32: the pack spec needs " + std::to_string(used) + " bits > 32");
     SPC_CHECK_ARG(spec.reach >= 0 && spec.out_stride >= 1 && (spec.out_stride & (spec.out_stride - 1)) == 0,
                   "pack spec: reach must be >= 0 and out_stride a power of two >= 1");
     if (ws_bytes < spc_pack_sort_workspace_size(n)) return fail(SPC_ERR_WORKSPACE, "spc_pack_sort: ws too small");
     cudaStream_t st = as_stream(stream);
     Bump b(ws, ws_bytes);
-    uint64_t *raw = b.take<uint64_t>((size_t)n);
+    KeyT *raw = b.take<KeyT>((size_t)n);
     void *rws = b.base + align_up(b.used, 256);
     size_t rws_bytes = ws_bytes - align_up(b.used, 256);
     PackDev pd{spec.bits_b, spec.bits_x, spec.bits_y, spec.bits_z, spec.out_stride - 1 + spec.reach, spec.reach};
@@ -543,16 +564,42 @@ extern "C" spc_status spc_pack_sort(const int32_t *coords, int64_t n, const int6
     // the first region of the radix workspace)
     unsigned int *hist = reinterpret_cast<unsigned int *>(rws);   // == radix_sort's first workspace block
     SPC_CUDA(cudaMemsetAsync(hist, 0, sizeof(unsigned int) * MAX_PASSES * 256, st));
-    SPC_CUDA(launch_pdl(k_pack, dim3(grid), dim3(256), 0, st, reinterpret_cast<const int4 *>(coords), n, n_dev, pd, raw, status, (used + 7) / 8, hist));
+    SPC_CUDA(launch_pdl(k_pack<KeyT>, dim3(grid), dim3(256), 0, st, reinterpret_cast<const int4 *>(coords), n, n_dev, pd,
+                        raw, status, (used + 7) / 8, hist));
     SPC_LAUNCH_CHECK("k_pack");
-    int32_t *perm = perm_out;
-    spc_status s = radix_sort(raw, nullptr, n, n_dev, used, keys_out, perm, rws, rws_bytes, st, true);
+    spc_status s = radix_sort(raw, nullptr, n, n_dev, used, keys_out, perm_out, rws, rws_bytes, st, true);
     if (s != SPC_OK) return s;
     if (status) {
-        SPC_CUDA(launch_pdl(k_flag_dups, dim3(grid), dim3(256), 0, st, keys_out, n, n_dev, status, SPC_FLAG_DUPLICATE));
+        SPC_CUDA(launch_pdl(k_flag_dups<KeyT>, dim3(grid), dim3(256), 0, st, keys_out, n, n_dev, status, SPC_FLAG_DUPLICATE));
         SPC_LAUNCH_CHECK("k_flag_dups");
     }
     return SPC_OK;
+}
+
+// SPC_KMAP_CHECK_SORTED: flag keys that are not strictly ascending
+spc_status flag_unsorted(const void *keys, int key_bytes, int64_t n_cap, const int64_t *n_dev, uint32_t *status,
+                         cudaStream_t st) {
+    if (key_bytes == 4)
+        SPC_CUDA(launch_pdl(k_flag_dups<uint32_t>, dim3(64), dim3(256), 0, st, static_cast<const uint32_t *>(keys), n_cap,
+                            n_dev, status, SPC_FLAG_UNSORTED));
+    else
+        SPC_CUDA(launch_pdl(k_flag_dups<uint64_t>, dim3(64), dim3(256), 0, st, static_cast<const uint64_t *>(keys), n_cap,
+                            n_dev, status, SPC_FLAG_UNSORTED));
+    SPC_LAUNCH_CHECK("k_flag_dups");
+    return SPC_OK;
+}
+}  // namespace spc
+
+extern "C" spc_status spc_pack_sort(const int32_t *coords, int64_t n, const int64_t *n_dev, spc_pack_spec spec,
+                                    uint64_t *keys_out, int32_t *perm_out, uint32_t *status, void *ws, size_t ws_bytes,
+                                    void *stream) {
+    return pack_sort_t(coords, n, n_dev, spec, keys_out, perm_out, status, ws, ws_bytes, stream);
+}
+
+extern "C" spc_status spc_pack_sort32(const int32_t *coords, int64_t n, const int64_t *n_dev, spc_pack_spec spec,
+                                      uint32_t *keys_out, int32_t *perm_out, uint32_t *status, void *ws, size_t ws_bytes,
+                                      void *stream) {
+    return pack_sort_t(coords, n, n_dev, spec, keys_out, perm_out, status, ws, ws_bytes, stream);
 }
 
 extern "C" spc_status spc_gather_rows(const void *src, int64_t ld_src_bytes, const int32_t *perm, int64_t n,

@@ -1,2 +1,2 @@
-python scripts/indexing_modes.py --config 2 --reps 20 | tee gpurun_out/r2_indexing_modes.jsonl
-python scripts/indexing_modes.py --config 4 --reps 10 | tee -a gpurun_out/r2_indexing_modes.jsonl
+timeout 900 python -m pytest tests/test_gpu_keys32.py -x -q 2>&1 | tail -4
+python scripts/keys32_ablation.py | tee gpurun_out/r2_keys32.jsonl

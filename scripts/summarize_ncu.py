@@ -24,23 +24,32 @@ def launches(path, out):
     h = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     hdr, data = rows[h], rows[h + 1:]
     ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
-    tot, cnt = collections.defaultdict(float), collections.Counter()
+    mi = hdr.index("Metric Name") if "Metric Name" in hdr else None
+    ui = hdr.index("Metric Unit") if "Metric Unit" in hdr else None
+    scale = {"nsecond": 1.0, "usecond": 1e3, "msecond": 1e6, "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    tot, dram, cnt = collections.defaultdict(float), collections.defaultdict(float), collections.Counter()
     for r in data:
         try:
-            v = float(r[vi].replace(",", ""))
+            v = float(r[vi].replace(",", "")) * (scale.get(r[ui], 1.0) if ui is not None else 1.0)
         except (ValueError, IndexError):
             continue
         k = r[ki].split("(")[0]
-        tot[k] += v
-        cnt[k] += 1
+        m = r[mi] if mi is not None else "gpu__time_duration.sum"
+        if m == "gpu__time_duration.sum":
+            tot[k] += v
+            cnt[k] += 1
+        elif m.startswith("dram__bytes"):
+            dram[k] += v
     T = sum(tot.values())
+    D = sum(dram.values())
     with open(out, "w") as f:
         f.write(f"# ncu launch list summary ({path})\n\n")
-        f.write("Per-launch gpu__time_duration.sum, --clock-control none, serialised and cold-cache:\n")
-        f.write("compare SHARES, not absolute times.\n\n| kernel | launches | total us | share |\n|---|---|---|---|\n")
+        f.write("Per-launch gpu__time_duration.sum (+ DRAM read+write), --clock-control none, serialised and\n")
+        f.write("cold-cache: compare SHARES, not absolute times.\n\n| kernel | launches | total us | share | DRAM MB |\n"
+                "|---|---|---|---|---|\n")
         for k, v in sorted(tot.items(), key=lambda x: -x[1]):
-            f.write(f"| {k} | {cnt[k]} | {v / 1e3:.1f} | {100 * v / T:.1f}% |\n")
-        f.write(f"\n{len(data)} launches, {T / 1e3:.1f} us total\n")
+            f.write(f"| {k} | {cnt[k]} | {v / 1e3:.1f} | {100 * v / T:.1f}% | {dram[k] / 1e6:.1f} |\n")
+        f.write(f"\n{sum(cnt.values())} launches, {T / 1e3:.1f} us total, {D / 1e6:.1f} MB DRAM\n")
 
 
 def full(rep, out):
