@@ -842,7 +842,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             gather_role<BK, NB>(p, cs, blk, blk_stride, kd, sa, S, nkb, a_bytes, kb_a, warp, lane);
     } else if (warp == W_BLOAD) {
         // ===================== weight loader (1-D bulk copies, TMA engine) ===============
-        uint32_t it = 0;
+        int s = 0;
+        uint32_t ph = 0;   // stage ring position / phase (no division per stage)
         for (uint32_t ti = 0;; ++ti) {
             const int st = ti % TREC_SLOTS;
             ptx::mbar_wait(ptx::smem_u32(&cs.trec_full[st]), (ti / TREC_SLOTS) & 1);
@@ -851,22 +852,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             if (lane == 0) {
                 const int nt = R.nt, kfix = R.k, ncols = R.ncols;
                 const int nsl = ncols * p.n_chunks;
-                for (int sl = 0; sl < nsl; sl += nkb, ++it) {
+                int ci = 0, cc = 0;   // (offset column, channel chunk) of the next slice
+                for (int sl = 0; sl < nsl; sl += nkb) {
                     const int nin = min(nkb, nsl - sl);
-                    const int s = it % S;
-                    ptx::mbar_wait(ptx::smem_u32(&cs.empty[s]), ((it / S) & 1) ^ 1);
+                    ptx::mbar_wait(ptx::smem_u32(&cs.empty[s]), ph ^ 1);
                     const uint32_t fb = ptx::smem_u32(&cs.full[s]);
                     // a CTA of a pair loads its N half of each weight tile (rows
                     // [rank BN/2, (rank+1) BN/2) of the K-major blob: contiguous, atom-aligned)
                     const uint32_t kb_bl = p.kb_b / CG;
                     ptx::mbar_arrive_expect_tx(fb, nin * kb_bl);
                     for (int kb = 0; kb < nin; ++kb) {
-                        const int ci = (sl + kb) / p.n_chunks, cc = (sl + kb) - ci * p.n_chunks;
                         const int k = p.mode == 0 ? p.dense_k[R.cols[ci]] : kfix;
                         const int64_t blob = ((int64_t)k * p.n_ntiles + nt) * p.n_chunks + cc;
                         ptx::bulk_g2s(ptx::smem_u32(sb + (size_t)s * b_bytes + kb * kb_bl),
                                       p.wblob + blob * p.kb_b + rank * kb_bl, kb_bl, fb);
+                        if (++cc == p.n_chunks) {
+                            cc = 0;
+                            ++ci;
+                        }
                     }
+                    if (++s == S) { s = 0; ph ^= 1; }
                 }
                 ptx::mbar_arrive(ptx::smem_u32(&cs.trec_empty[st]));
             }
@@ -876,18 +881,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         // ===================== pair peer: stage forwarder =====================================
         // the leader's MMAs read this CTA's A rows and B half: once a stage is complete here,
         // make it visible to the async proxy and arrive on the leader's full barrier
-        uint32_t it = 0;
+        int s = 0;
+        uint32_t ph = 0;
         for (uint32_t ti = 0;; ++ti) {
             const int st = ti % TREC_SLOTS;
             ptx::mbar_wait(ptx::smem_u32(&cs.trec_full[st]), (ti / TREC_SLOTS) & 1);
             const TileRec &R = cs.trec[st];
             if (__shfl_sync(0xffffffffu, R.end, 0)) break;
             const int nsl = __shfl_sync(0xffffffffu, R.ncols, 0) * p.n_chunks;
-            for (int sl = 0; sl < nsl; sl += nkb, ++it) {
-                const int s = it % S;
-                ptx::mbar_wait(ptx::smem_u32(&cs.full[s]), (it / S) & 1);
+            for (int sl = 0; sl < nsl; sl += nkb) {
+                ptx::mbar_wait(ptx::smem_u32(&cs.full[s]), ph);
                 ptx::fence_proxy_async();
                 if (lane == 0) ptx::mbar_arrive_remote_relaxed(ptx::mapa(ptx::smem_u32(&cs.full[s]), 0));
+                if (++s == S) { s = 0; ph ^= 1; }
             }
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&cs.trec_empty[st]));
@@ -896,7 +902,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         // ===================== MMA issuer (whole warp, elected lane issues) ================
         // every lane runs the loop on warp-uniform values (shuffled from lane 0), so the
         // descriptors stay uniform and each tcgen05.mma is one predicated instruction
-        uint32_t it = 0;
+        int ring_s = 0;
+        uint32_t ring_ph = 0;   // stage ring position / phase (no division per stage)
         const uint32_t tb = __shfl_sync(0xffffffffu, tmem_base, 0);
         const uint32_t kb_a_u = __shfl_sync(0xffffffffu, kb_a, 0), a_bytes_u = __shfl_sync(0xffffffffu, a_bytes, 0);
         const uint32_t b_bytes_u = __shfl_sync(0xffffffffu, b_bytes, 0);
@@ -918,10 +925,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             uint32_t acc = 0;
             const int nsl = ncols * p.n_chunks;
             const uint32_t kb_bl = p.kb_b / CG;
-            for (int sl = 0; sl < nsl; sl += nkb_u, ++it) {
+            for (int sl = 0; sl < nsl; sl += nkb_u) {
                 const int nin = min(nkb_u, nsl - sl);
-                const int s = it % S_u;
-                ptx::mbar_wait(ptx::smem_u32(&cs.full[s]), (it / S_u) & 1);
+                const int s = ring_s;
+                ptx::mbar_wait(ptx::smem_u32(&cs.full[s]), ring_ph);
+                if (++ring_s == S_u) { ring_s = 0; ring_ph ^= 1; }
                 if (sl == 0 && lane == 0) trace_tile_event(p.trace, 4, ti);
                 ptx::fence_proxy_async();
                 ptx::tc_fence_after();
