@@ -84,7 +84,9 @@ typedef enum {
                                    * for every layer but the first of a network pass): the
                                    * kernel then decodes tiles and streams weights while that
                                    * kernel drains (programmatic dependent launch) (default 0)  */
-    SPC_OPT_COUNT = 11
+    SPC_OPT_CONV_BULK_RED = 11,   /* 1 (default): the weight-stationary scatter reduces 64-column
+                                   * row segments with bulk reductions (TMA); 0: red.global.add */
+    SPC_OPT_COUNT = 12
 } spc_option;
 spc_status spc_set_option(int32_t option, int64_t value);
 int64_t spc_get_option(int32_t option);

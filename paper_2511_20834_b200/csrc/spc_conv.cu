@@ -72,6 +72,7 @@ struct ConvParams {
         int stages;
     } ring[2];
     uint32_t hdr_off;     // byte offset of ConvSmem + index blocks (after the ring)
+    uint32_t red_off;     // byte offset of the WS bulk-reduction staging rows (0: red.global.add)
     int bm;               // max rows per tile (template BM): 128 or 256 (two M=128 MMAs sharing the weight tile)
     int split_ok;         // OS part may split a tile's offsets over CTAs (needs acc + tile_ctr)
     int force_tr;         // experiments: 128/256 forces the tile rows (0 = device heuristic)
@@ -397,10 +398,20 @@ __device__ __forceinline__ void gather_role(const ConvParams &p, ConvSmem &cs, c
 // epilogue warps (8-11, thread = TMEM lane = tile row): TMEM -> OS: plain stores (final
 // dtype, fused residual, or fp32 accumulator) / WS: red.global.add.v4.f32 scatter;
 // FIX: OS split tiles go through the split-K fixup instead
+constexpr int RED_COLS = 64;      // WS scatter: columns per bulk reduction (256-byte row segments)
+constexpr int RED_LD = RED_COLS + 4;   // floats per staging row (16-byte aligned, fewer bank conflicts)
+constexpr int RED_STAGE_BYTES = 4 * 32 * RED_LD * 4;
+
 template <bool FIX>
-__device__ __forceinline__ void epi_role(const ConvParams &p, ConvSmem &cs, uint32_t tmem_base, int tr, int nht,
-                                         int NH, int warp, int lane, int pair_rank) {
+__device__ __forceinline__ void epi_role(const ConvParams &p, ConvSmem &cs, float *red_stage, uint32_t tmem_base,
+                                         int tr, int nht, int NH, int warp, int lane, int pair_rank) {
     const int e = warp - W_EPI0;   // == warp % 4: the TMEM lane quadrant this warp may access
+    // WS scatter through bulk reductions (cp.reduce.async.bulk .add.f32, TMA engine): each
+    // lane stages its row's 64-column segment in shared memory and reduces it into the fp32
+    // accumulator in one operation -- measured 1.5-2x the red.global.add.v4 rate, which
+    // is bound by one L2 transaction per lane and 16 bytes (scripts/red_bench.cu)
+    const bool bulk = p.out_kind == OUT_F32_RED && red_stage != nullptr;
+    const uint32_t stg_row = bulk ? ptx::smem_u32(red_stage + (e * 32 + lane) * RED_LD) : 0u;
     for (uint32_t ti = 0;; ++ti) {
         const int st = ti % TREC_SLOTS;
         ptx::mbar_wait_sleep(ptx::smem_u32(&cs.trec_full[st]), (ti / TREC_SLOTS) & 1);
@@ -422,6 +433,30 @@ __device__ __forceinline__ void epi_role(const ConvParams &p, ConvSmem &cs, uint
                 if (r < R.rows && R.ncols > 0)
                     orow = (p.mode == 0 && !p.os_rows) ? R.row0 + r : (int64_t)R.scatter[r];
                 const uint32_t tbase = tmem_base + (a * NH + h) * p.tmem_cols + ((uint32_t)(e * 32) << 16);
+                if (bulk) {
+                    for (int c0 = 0; c0 < p.BN; c0 += RED_COLS) {
+                        ptx::bulk_wait_read0();   // the previous segment's reduction has read the row
+#pragma unroll
+                        for (int sub = 0; sub < RED_COLS; sub += 32) {
+                            uint32_t vals[32];
+                            ptx::tmem_ld32(tbase + c0 + sub, vals);
+                            ptx::tmem_ld_wait();
+#pragma unroll
+                            for (int q = 0; q < 8; ++q)
+                                asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(stg_row + (sub + 4 * q) * 4),
+                                             "r"(vals[4 * q]), "r"(vals[4 * q + 1]), "r"(vals[4 * q + 2]),
+                                             "r"(vals[4 * q + 3])
+                                             : "memory");
+                        }
+                        ptx::fence_proxy_async();   // the staged row is read by the async (bulk) proxy
+                        if (orow >= 0) {
+                            ptx::bulk_reduce_add_f32(static_cast<float *>(p.out) + orow * p.ld_out + nt * p.BN + c0,
+                                                     stg_row, RED_COLS * 4);
+                            ptx::bulk_commit();
+                        }
+                    }
+                    continue;
+                }
                 for (int col = 0; col < p.BN; col += 32) {
                     uint32_t vals[32];
                     const int n = min(32, p.BN - col);
@@ -455,6 +490,7 @@ __device__ __forceinline__ void epi_role(const ConvParams &p, ConvSmem &cs, uint
             ptx::mbar_arrive(ptx::smem_u32(&cs.trec_empty[st]));
         }
     }
+    if (bulk) ptx::bulk_wait0();   // every reduction has landed before the CTA exits
 }
 
 // fp32 accumulator rows -> output dtype (+ residual), 8 columns per work item; the
@@ -966,10 +1002,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     } else if (warp >= W_EPI0 && warp < W_EPI0 + 4) {
         // ===================== epilogue (warps 8-11, thread = TMEM lane = tile row) ====
         const int pair_rank = CG == 2 ? (int)rank : -1;
+        float *red_stage = p.red_off ? reinterpret_cast<float *>(smem + p.red_off) : nullptr;
         if (wsplit)
-            epi_role<true>(p, cs, tmem_base, tr, nht, NH, warp, lane, pair_rank);
+            epi_role<true>(p, cs, red_stage, tmem_base, tr, nht, NH, warp, lane, pair_rank);
         else
-            epi_role<false>(p, cs, tmem_base, tr, nht, NH, warp, lane, pair_rank);
+            epi_role<false>(p, cs, red_stage, tmem_base, tr, nht, NH, warp, lane, pair_rank);
     }
     ptx::tc_fence_before();
     // a pair frees its TMEM and exits together (the leader's MMAs and commits reach the
@@ -1251,7 +1288,9 @@ static spc_status launch_tc(const ConvParams &p0, int mode, int out_kind, void *
     const int kd = mode == 0 ? p.k_dense : 1;
     const size_t blk_bytes = (size_t)((p.bm * kd + 3) & ~3) * 4;
     p.blk_slots = 2 * blk_bytes <= 64 * 1024 ? 2 : 1;
-    const size_t header = align_up(sizeof(ConvSmem), 128) + (size_t)p.blk_slots * blk_bytes;
+    const bool bulk_red = out_kind == OUT_F32_RED && p.BN % RED_COLS == 0 && option(SPC_OPT_CONV_BULK_RED) != 0;
+    const size_t header = align_up(sizeof(ConvSmem), 128) + (size_t)p.blk_slots * blk_bytes +
+                          (bulk_red ? RED_STAGE_BYTES : 0);
     const size_t avail = TC_SMEM_BUDGET - 1024 - header;   // 1024: alignment slack of the dynamic smem base
     // slices (one BK-channel chunk of one offset) per pipeline stage: a stage carries up
     // to ~72 KB so narrow layers pack several offsets into one stage
@@ -1270,6 +1309,7 @@ static spc_status launch_tc(const ConvParams &p0, int mode, int out_kind, void *
         ring_bytes = std::max(ring_bytes, (size_t)R.stages * (R.a_bytes + R.b_bytes));
     }
     p.hdr_off = (uint32_t)align_up(ring_bytes, 128);
+    p.red_off = bulk_red ? (uint32_t)(p.hdr_off + align_up(sizeof(ConvSmem), 128) + (size_t)p.blk_slots * blk_bytes) : 0u;
     const size_t smem = 1024 + p.hdr_off + header;
     static uint64_t configured = 0;   // bit d: smem attributes set on device d
     const int dev = current_device();

@@ -143,6 +143,19 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t
                  : "memory");
 }
 
+// bulk reduction (TMA engine): global[dst .. dst+bytes) += shared[src ..] as fp32, one
+// asynchronous operation per contiguous row segment (bulk-group completion)
+__device__ __forceinline__ void bulk_reduce_add_f32(float *dst, uint32_t src, uint32_t bytes) {
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(dst), "r"(src),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// this thread's bulk operations have finished READING their shared sources
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+// this thread's bulk operations have completed (global writes done)
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 // TMA 2-D tile load (cp.async.bulk.tensor): box at coordinates (c0 inner, c1 outer) of the
 // tensor map into shared memory in the map's swizzled layout; out-of-range elements are
 // zero-filled; completion counted (bytes) on an mbarrier

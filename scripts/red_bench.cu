@@ -12,9 +12,9 @@
 
 template <int C, int MODE>
 __global__ void __launch_bounds__(128) k(float *__restrict__ acc, const int *__restrict__ idx, int n_rows, int iters) {
-    __shared__ __align__(128) float stage[128 * C];
+    __shared__ __align__(128) float stage[MODE == 1 ? 128 * C : 4];
     const int t = threadIdx.x;
-    for (int i = t; i < 128 * C; i += 128) stage[i] = 1.0f;
+    if (MODE == 1) for (int i = t; i < 128 * C; i += 128) stage[i] = 1.0f;
     __syncthreads();
     for (int it = 0; it < iters; ++it) {
         const int row = idx[((blockIdx.x * iters + it) * 128 + t) % (1 << 20)] % n_rows;
@@ -73,5 +73,9 @@ int main() {
     run<96, 1>(acc, idx, n_rows);
     run<64, 0>(acc, idx, n_rows);
     run<64, 1>(acc, idx, n_rows);
+    run<64, 0>(acc, idx, 7000);      // a level-3-sized accumulator (hot rows)
+    run<64, 1>(acc, idx, 7000);
+    run<256, 0>(acc, idx, 7000);
+    run<256, 0>(acc, idx, n_rows);
     return 0;
 }
