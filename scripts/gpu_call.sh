@@ -1,3 +1,3 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_pair.py tests/test_gpu_headline.py -q -x 2>&1 | tail -1
-python scripts/ab_net.py CONV_BULK_RED=0 CONV_BULK_RED=1 2>&1 | tail -2
-for o in 0 1; do python scripts/probe_conv.py --opt CONV_BULK_RED=$o --cin 256 --cout 256 --t 0 --reps 10 --config 5 2>&1 | grep "n="; python scripts/probe_conv.py --opt CONV_BULK_RED=$o --cin 256 --cout 256 --t 0 --reps 10 --config 2 --n 7000 2>&1 | grep "n="; done
+python scripts/timeline.py --out gpurun_out/r2_timeline4.json > gpurun_out/r2_timeline4.txt 2>&1; tail -3 gpurun_out/r2_timeline4.txt
+python bench.py --steps 100 --warmup 5 --no-cpu-baseline --t-from profiles/r2_tuned_t_c2.json --profile-layers > gpurun_out/r2_bench_i.json 2> gpurun_out/r2_bench_i.err
+python -c "import json;d=json.loads(open('gpurun_out/r2_bench_i.json').read().splitlines()[-1]);print(d['value'],d['e2e']['value'],d['roofline']['frac'],d['roofline']['conv_ms_per_step'],d['roofline']['index_ms_per_step'])"
