@@ -20,7 +20,7 @@ keys, perm, _ = spc.spc_pack_sort(torch.from_numpy(coords).cuda(), spec)
 lv, ln = spc.spc_downsample(keys, spec, [1])
 n1 = int(ln[0].item())
 coarse = lv[0, :n1].contiguous()
-ws = torch.zeros(keys.shape[0] * 256 * 4 + 1024, dtype=torch.uint8, device="cuda")
+ws = torch.zeros(keys.shape[0] * 256 * 4 + (1 << 16), dtype=torch.uint8, device="cuda")   # accumulator + tile counters
 
 
 def med(fn, reps=7):
