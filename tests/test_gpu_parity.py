@@ -489,3 +489,34 @@ def test_dense_centre_initialises_ws_accumulator(c_in, c_out, K, halve):
     got = o16.float().cpu().numpy().astype(np.float64)
     ulp = np.exp2(np.floor(np.log2(np.maximum(np.abs(ref16), 1e-30))) - 7)
     assert (np.abs(got - ref16) <= ulp + 1e-5 * np.abs(ref16).max()).all()
+
+
+@pytest.mark.parametrize("bulk", [1, 0])
+@pytest.mark.parametrize("c_in,c_out,t", [(64, 64, 0), (128, 256, 0), (32, 96, 2)])
+def test_ws_epilogue_variants_and_workspace_contract(bulk, c_in, c_out, t):
+    """The weight-stationary scatter (bulk reductions or red.global.add) gives the
+    oracle's result with a residual and leaves the caller's workspace all-zero (spc.h), so
+    the next call on the same workspace is right too."""
+    coords = synth.make_scan(1, 0)[:7000]
+    spec = _spec_for(coords)
+    keys, _, _ = _pack_sort(coords, spec)
+    c = oracle.sort_coords(coords)[0]
+    km = spc.spc_build_kmap(keys, keys, spec, spc.Geom(3, 1, 1, 1, 0), t, 1)
+    F = synth.make_features(len(c), c_in, seed=c_in + 1)
+    W = synth.make_weights(27, c_in, c_out, seed=c_out + 2, nnz_per_out=8)
+    R = synth.make_features(len(c), c_out, seed=5)
+    Wg = spc.spc_prepare_weight(torch.from_numpy(W).to(DEV).bfloat16())
+    ws = torch.zeros(spc.spc_conv_workspace_size(km, c_out, torch.bfloat16), dtype=torch.uint8, device=DEV)
+    ref = oracle.conv(c, c, 3, 1, F, W) + R.astype(np.float64)
+    ulp = np.exp2(np.floor(np.log2(np.maximum(np.abs(ref), 1e-30))) - 7)
+    try:
+        spc.spc_set_option(spc.SPC_OPT_CONV_BULK_RED, bulk)
+        for _ in range(2):
+            o = spc.spc_conv_forward(km, torch.from_numpy(F).to(DEV).bfloat16(), Wg, c_in, c_out,
+                                     out_dtype=torch.bfloat16, residual=torch.from_numpy(R).to(DEV).bfloat16(), ws=ws)
+            torch.cuda.synchronize()
+            got = o.float().cpu().numpy().astype(np.float64)
+            assert (np.abs(got - ref) <= ulp + 1e-5 * np.abs(ref).max()).all()
+            assert int(torch.count_nonzero(ws)) == 0
+    finally:
+        spc.spc_set_option(spc.SPC_OPT_CONV_BULK_RED, -1)
