@@ -15,6 +15,7 @@ arrays through ctypes.  Every function follows a definition in PAPER.md:
 ``kmap``               M[i,k] = j iff p_j = q_i + delta_k, hash-set lookup
 ``conv``               Eq. (2) in fp64, OS or WS loop order
 ``conv_rows``          Eq. (2) for sampled output rows (full-size sampled parity)
+``voxelize``           v = floor(p/g) in float32, unique, mean feature (§2.1)
 =====================  =============================================================
 
 Parity pins: tests/test_oracle_pins.py (brute force, closed forms, paper examples,
@@ -42,9 +43,9 @@ def build(force: bool = False) -> str:
     rows spread over the host cores, for timing the CPU baseline)."""
     dep = max(os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "spc_oracle.h")))
     if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < dep:
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", _SRC, "-o", _LIB_PATH])
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", _SRC, "-o", _LIB_PATH, "-lm"])
     if force or not os.path.exists(_LIB_OMP_PATH) or os.path.getmtime(_LIB_OMP_PATH) < dep:
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-fopenmp", _SRC, "-o", _LIB_OMP_PATH])
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-fopenmp", _SRC, "-o", _LIB_OMP_PATH, "-lm"])
     return _LIB_PATH
 
 
@@ -84,6 +85,8 @@ def _L():
         lib.orc_conv.restype = I64
         lib.orc_conv_rows.argtypes = [P, I64, P, P, I64, I, I, I, P, I, P, I, P]
         lib.orc_conv_rows.restype = I64
+        lib.orc_voxelize.argtypes = [P, I64, P, I64, P, P, I64, I, P, P, P]
+        lib.orc_voxelize.restype = I64
         lib.orc_num_threads.argtypes = []
         lib.orc_num_threads.restype = ctypes.c_int
         _lib = lib
@@ -187,3 +190,25 @@ def conv_rows(in_coords, out_coords, rows, K: int, spacing: int, F_in, W, transp
     if r < 0:
         raise ValueError("orc_conv_rows failed")
     return out
+
+
+def voxelize(points, grid, batch=None, feats=None):
+    """Voxelization: points float32 [n, >=3] (x, y, z first),
+    grid (gx, gy, gz), batch int32 [n] or None, feats float32 [n, c] or None.
+    -> (coords int32 [V, 4] canonical (b, x, y, z), point_voxel int32 [n],
+        mean fp64 [V, c] or None).  ValueError names the first non-finite point."""
+    P = np.ascontiguousarray(points, dtype=np.float32)
+    n, ld = P.shape
+    g = _c(grid, np.float32).reshape(3)
+    b = None if batch is None else _c(batch, np.int32).reshape(n)
+    F = None if feats is None else _c(feats, np.float32).reshape(n, -1)
+    c = 0 if F is None else F.shape[1]
+    coords = np.empty((max(n, 1), 4), np.int32)
+    pv = np.empty(max(n, 1), np.int32)
+    mean = np.empty((max(n, 1), max(c, 1)), np.float64) if F is not None else None
+    nv = _L().orc_voxelize(_p(P), ld, _p(b) if b is not None else None, n, _p(g),
+                           _p(F) if F is not None else None, c, c, _p(coords), _p(pv),
+                           _p(mean) if mean is not None else None)
+    if nv < 0:
+        raise ValueError(f"voxelize: point {-nv - 1} is not finite (or its quotient leaves int32)")
+    return coords[:nv], pv[:n], (mean[:nv, :c] if mean is not None else None)

@@ -296,6 +296,54 @@ int64_t orc_conv_rows(const int32_t *in_coords, int64_t n_in, const int32_t *out
     return nnz;
 }
 
+/* ------------------------------------------------------------------------------------
+ * voxelization: §2.1 "v_i = floor(p_i^(raw) / g)"; S:70-78 quantize
+ * (floor toward -infinity, duplicates merged, point -> voxel index map); S:132 merged
+ * voxels' features averaged
+ * ---------------------------------------------------------------------------------- */
+#include <math.h>
+
+int64_t orc_voxelize(const float *pts, int64_t ld, const int32_t *batch, int64_t n, const float *g,
+                     const float *feats, int64_t ld_f, int c, int32_t *coords_out, int32_t *point_voxel,
+                     double *feats_out) {
+    if (n < 0) return -1;
+    orc_row *r = (orc_row *)malloc(sizeof(orc_row) * (size_t)(n > 0 ? n : 1));
+    for (int64_t i = 0; i < n; ++i) {
+        r[i].c[0] = batch ? batch[i] : 0;
+        for (int d = 0; d < 3; ++d) {
+            float p = pts[i * ld + d];
+            float q = p / g[d]; /* float32 quotient, IEEE round-to-nearest (reading V1) */
+            if (!isfinite(p) || !isfinite(q)) { free(r); return -(1 + i); }
+            double v = floor((double)q); /* floor toward -infinity ("floor(-0.6) = -1") */
+            if (v < -2147483648.0 || v > 2147483647.0) { free(r); return -(1 + i); }
+            r[i].c[1 + d] = (int32_t)v;
+        }
+        r[i].row = (int32_t)i;
+    }
+    /* canonical order of the (b, v) rows; equal rows keep ascending point index */
+    qsort(r, (size_t)n, sizeof(orc_row), cmp_row);
+    int64_t nv = 0;
+    if (feats_out) memset(feats_out, 0, sizeof(double) * (size_t)n * (size_t)(c > 0 ? c : 0));
+    int64_t first = 0; /* sorted position of the current voxel's first point */
+    for (int64_t i = 0; i < n; ++i) {
+        if (i == 0 || cmp_tuple(r[i - 1].c, r[i].c) != 0) {
+            memcpy(coords_out + 4 * nv, r[i].c, sizeof(int32_t) * 4);
+            ++nv;
+            first = i;
+        }
+        const int64_t v = nv - 1;
+        if (point_voxel) point_voxel[r[i].row] = (int32_t)v;
+        if (feats && feats_out) {
+            for (int ch = 0; ch < c; ++ch) feats_out[v * c + ch] += (double)feats[(int64_t)r[i].row * ld_f + ch];
+            const int last = (i + 1 == n) || cmp_tuple(r[i].c, r[i + 1].c) != 0;
+            if (last)
+                for (int ch = 0; ch < c; ++ch) feats_out[v * c + ch] /= (double)(i - first + 1);
+        }
+    }
+    free(r);
+    return nv;
+}
+
 #ifdef _OPENMP
 #include <omp.h>
 int orc_num_threads(void) { return omp_get_max_threads(); }

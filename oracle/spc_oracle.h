@@ -15,6 +15,7 @@
  *                              indicator of Eq. (2))                             (§2.2)
  *   - features Eq. (2)       : f_i = sum_k sum_j 1[p_j = q_i + delta_k] f_j W_k  in fp64
  *                                                                                (§2.1)
+ *   - voxelization           : v = floor(p_raw / g), unique, mean feature        (§2.1)
  *
  * Coordinates are int32 rows (b, x, y, z).  Index spaces are positions in the
  * canonical (sorted) order of each coordinate set.  All functions are
@@ -69,6 +70,19 @@ int64_t orc_conv(const int32_t *in_coords, int64_t n_in, const int32_t *out_coor
 int64_t orc_conv_rows(const int32_t *in_coords, int64_t n_in, const int32_t *out_coords,
                       const int64_t *rows, int64_t n_rows, int K, int spacing, int transposed,
                       const double *F_in, int c_in, const double *W, int c_out, double *F_out);
+
+/* Voxelization: v = floor(p_raw / g) per axis (§2.1), the
+ * quotient taken in float32 (the points are float32; reading V1) and floored
+ * toward -infinity.  Point i: coordinates pts[i*ld + 0..2], batch b_i = batch[i] (batch
+ * NULL: 0).  The voxel set is the canonical (sorted, unique) set of rows (b_i, v_i)
+ * written to coords_out [n][4]; point_voxel[i] = the position of point i's row in it;
+ * feats_out[v][0..c) = the mean of feats[i*ld_f + 0..c) over the points of voxel v
+ * (duplicate voxels averaged), summed in fp64 in ascending point index.  feats /
+ * feats_out / point_voxel may be NULL.  Returns the voxel count, or -(1 + i) for the
+ * first point i whose coordinates are not finite or whose quotient leaves int32. */
+int64_t orc_voxelize(const float *pts, int64_t ld, const int32_t *batch, int64_t n, const float *g,
+                     const float *feats, int64_t ld_f, int c, int32_t *coords_out, int32_t *point_voxel,
+                     double *feats_out);
 
 /* Threads the Eq. (2) row loops use: 1 in the plain build (liboracle.so), the OpenMP
  * thread count in liboracle_omp.so (same arithmetic per row, rows in parallel). */

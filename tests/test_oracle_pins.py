@@ -381,3 +381,68 @@ def test_openmp_build_is_bit_identical():
     finally:
         oracle.use_openmp(False)
     assert np.array_equal(a, b) and np.array_equal(ar, br)
+
+
+# ---------------------------------------------------------------------------------------
+# voxelization: P:96 v = floor(p / g); S:70-78 quantize; S:132 averaging
+# ---------------------------------------------------------------------------------------
+
+def test_voxelize_spec_examples():
+    """(1.25, -0.30, 0.999) at g = 0.5 -> (2, -1, 1) (floor(-0.6) = -1, not
+    truncation); the origin maps to the origin for any g."""
+    c, pv, _ = oracle.voxelize(np.array([[1.25, -0.30, 0.999]], np.float32), (0.5, 0.5, 0.5))
+    assert c.tolist() == [[0, 2, -1, 1]] and pv.tolist() == [0]
+    c, _, _ = oracle.voxelize(np.zeros((1, 3), np.float32), (0.05, 0.1, 0.2))
+    assert c.tolist() == [[0, 0, 0, 0]]
+
+
+def test_voxelize_matches_set_bruteforce():
+    """random points in a 10 m cube at g = 0.1: the voxel set is the set of floored
+    triples (Python set over math.floor of numpy float32 quotients), canonical order is
+    Python's tuple sort, every point's index points at its own voxel, and each mean is
+    the plain Python mean of the voxel's features in point order (bit-equal)."""
+    import math
+    rng = np.random.default_rng(11)
+    n = 1000
+    P = rng.uniform(-5, 5, (n, 3)).astype(np.float32)
+    P[::7] = P[3]                       # repeated points (merged voxels)
+    b = rng.integers(0, 3, n).astype(np.int32)
+    F = rng.uniform(-1, 1, (n, 5)).astype(np.float32)
+    g = np.float32(0.1)
+    vox = [(int(b[i]),) + tuple(math.floor(float(P[i, d] / g)) for d in range(3)) for i in range(n)]
+    ref = sorted(set(vox))
+    c, pv, m = oracle.voxelize(P, (0.1, 0.1, 0.1), batch=b, feats=F)
+    assert [tuple(r) for r in c.tolist()] == ref
+    assert all(tuple(c[pv[i]].tolist()) == vox[i] for i in range(n))
+    members = {}
+    for i in range(n):
+        members.setdefault(vox[i], []).append(i)
+    for v, rows in members.items():
+        for ch in range(5):
+            s = 0.0
+            for i in rows:
+                s += float(F[i, ch])
+            assert m[ref.index(v), ch] == s / len(rows)
+
+
+def test_voxelize_boundaries_and_negatives():
+    """Points exactly on grid planes belong to the voxel above (floor of an exact
+    quotient); tiny negative values floor to -1; a repeated point's mean is itself."""
+    P = np.array([[-0.5, 0.25, 0.0], [-1e-8, 1e-8, -0.25], [0.75, -0.75, 2.5], [0.75, -0.75, 2.5]], np.float32)
+    F = np.array([[1.0], [2.0], [3.0], [5.0]], np.float32)
+    c, pv, m = oracle.voxelize(P, (0.25, 0.25, 0.25), feats=F)
+    assert c.tolist() == [[0, -2, 1, 0], [0, -1, 0, -1], [0, 3, -3, 10]]
+    assert pv.tolist() == [0, 1, 2, 2]
+    assert m[:, 0].tolist() == [1.0, 2.0, 4.0]
+
+
+def test_voxelize_rejects_non_finite():
+    """a non-finite point is rejected with a diagnostic naming its index."""
+    P = np.zeros((10, 3), np.float32)
+    P[7, 1] = np.nan
+    with pytest.raises(ValueError, match="point 7"):
+        oracle.voxelize(P, (0.1, 0.1, 0.1))
+    P[7, 1] = 0
+    P[3, 2] = np.inf
+    with pytest.raises(ValueError, match="point 3"):
+        oracle.voxelize(P, (0.1, 0.1, 0.1))
