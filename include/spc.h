@@ -52,6 +52,7 @@ typedef enum {
 #define SPC_FLAG_DUPLICATE 0x2u  /* pack_sort: two equal keys                         */
 #define SPC_FLAG_UNSORTED 0x4u   /* build_kmap (SPC_KMAP_CHECK_SORTED): input unsorted */
 #define SPC_FLAG_CAPACITY 0x8u   /* a device count exceeded its host capacity          */
+#define SPC_FLAG_NONFINITE 0x10u /* voxelize: a point coordinate (or p/g) is not finite  */
 
 typedef enum { SPC_F32 = 0, SPC_F16 = 1, SPC_BF16 = 2 } spc_dtype;
 
@@ -169,6 +170,42 @@ spc_status spc_pack_sort(const int32_t *coords, int64_t n, const int64_t *n_dev,
 spc_status spc_pack_sort32(const int32_t *coords, int64_t n, const int64_t *n_dev, spc_pack_spec spec,
                            uint32_t *keys_out, int32_t *perm_out, uint32_t *status, void *ws, size_t ws_bytes,
                            void *stream);
+
+/* ================================================================================
+ * NEXT-2  spc_voxelize -- the voxelization front-end fused with pack + sort
+ *         (§2.1 v = floor(p_raw / g); SPEC S:70-78 quantize, S:132 averaging)
+ *
+ * points  : float32 rows, point i at points[i*ld + 0..2] = (x, y, z) in metres.  n is
+ *           the capacity, n_dev (nullable) the live point count on the device.
+ * batch   : int32 [n] batch index per point (nullable: 0).
+ * grid    : host float[3], g > 0.  v = floor(p / g) per axis with the quotient rounded
+ *           to float32 (IEEE round-to-nearest division; reading V1), floor
+ *           toward -infinity.
+ * spec    : pack spec for the voxel coordinates (spc_plan_pack over the expected voxel
+ *           range); a voxel outside its field with the planned headroom sets
+ *           SPC_FLAG_RANGE as in spc_pack_sort.
+ * feats   : float32 rows feats[i*ld_feats + 0..c) (nullable when c == 0).
+ * keys_out: uint64 [n]: the n_vox sorted unique voxel keys (A1 layout) first -- the same
+ *           keys spc_pack_sort would give for the voxel coordinates, ready for
+ *           spc_downsample / spc_build_kmap.
+ * n_vox_dev   : device int64, the voxel count.
+ * point_voxel : int32 [n] (nullable): index in keys_out of point i's voxel.
+ * feats_out   : [n][ld_out] rows of out_dtype (SPC_F32 or SPC_BF16; nullable when c == 0):
+ *           row v = the mean of the features of voxel v's points, summed in fp32 in
+ *           ascending point index (the sort is stable), divided by the count, rounded once.
+ * status  : device uint32 (nullable), OR-ed with SPC_FLAG_NONFINITE (a coordinate or its
+ *           quotient is not finite or leaves int32) and SPC_FLAG_RANGE; outputs are
+ *           undefined when a flag is set.
+ * bad_point_dev : device int64 (nullable): the smallest index of a non-finite point, or
+ *           -1 when there is none (the S:73 diagnostic, on the device).
+ * ws      : >= spc_voxelize_workspace_size(n) bytes, stream-ordered scratch.
+ * ================================================================================ */
+size_t spc_voxelize_workspace_size(int64_t n);
+spc_status spc_voxelize(const float *points, int64_t ld, const int32_t *batch, int64_t n, const int64_t *n_dev,
+                        const float *grid_host, spc_pack_spec spec, const float *feats, int64_t ld_feats, int32_t c,
+                        uint64_t *keys_out, int64_t *n_vox_dev, int32_t *point_voxel, void *feats_out, int64_t ld_out,
+                        int32_t out_dtype, uint32_t *status, int64_t *bad_point_dev, void *ws, size_t ws_bytes,
+                        void *stream);
 
 /* dst row r = src row perm[r] (row_bytes each, 16-byte aligned rows).  n_dev nullable. */
 spc_status spc_gather_rows(const void *src, int64_t ld_src_bytes, const int32_t *perm, int64_t n,

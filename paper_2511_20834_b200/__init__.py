@@ -117,6 +117,9 @@ def lib():
             "spc_pack_sort": ([P, I64, P, PackSpec, P, P, P, P, SZ, P], ctypes.c_int),
             "spc_pack_sort32": ([P, I64, P, PackSpec, P, P, P, P, SZ, P], ctypes.c_int),
             "spc_gather_rows": ([P, I64, P, I64, P, I32, P, I64, P], ctypes.c_int),
+            "spc_voxelize_workspace_size": ([I64], SZ),
+            "spc_voxelize": ([P, I64, P, I64, P, P, PackSpec, P, I64, I32, P, P, P, P, I64, I32, P, P, P, SZ, P],
+                             ctypes.c_int),
             "spc_downsample_workspace_size": ([I64, I32], SZ),
             "spc_downsample": ([P, I64, P, PackSpec, I32, P, P, P, P, SZ, P], ctypes.c_int),
             "spc_kmap_bytes": ([Geom, I32, U32, I64, I64], SZ),
@@ -277,6 +280,41 @@ def spc_gather_rows(src: torch.Tensor, perm: torch.Tensor, out: torch.Tensor | N
                                  row_bytes, _ptr(out), out.stride(0) * out.element_size(), _stream(stream)),
            "spc_gather_rows")
     return out
+
+
+# ---------------------------------------------------------------------------------------
+# NEXT-2 voxelization front-end
+# ---------------------------------------------------------------------------------------
+
+def spc_voxelize(points: torch.Tensor, grid, spec: PackSpec, batch: torch.Tensor | None = None,
+                 feats: torch.Tensor | None = None, out_dtype=torch.float32, n_dev=None, status=None, stream=None):
+    """Raw points -> voxels (P:96 v = floor(p/g)): points float32 [n, >=3] (x, y, z
+    first, row stride = points.stride(0)), grid (gx, gy, gz) metres, batch int32 [n] or None,
+    feats float32 [n, c] or None.  Returns (keys int64 [n] -- the first n_vox are the sorted
+    unique voxel keys --, n_vox int64 [1], point_voxel int32 [n], mean features [n, c] of
+    out_dtype or None, status uint32[1], bad_point int64 [1] (-1 or the first non-finite point))."""
+    assert points.is_cuda and points.dtype == torch.float32 and points.dim() == 2 and points.stride(1) == 1
+    n = points.shape[0]
+    dev = points.device
+    c = 0 if feats is None else feats.shape[1]
+    if feats is not None:
+        assert feats.dtype == torch.float32 and feats.stride(1) == 1
+    keys = _alloc(n, torch.int64, dev, stream)
+    n_vox = _alloc(1, torch.int64, dev, stream)
+    pv = _alloc(n, torch.int32, dev, stream)
+    out = _alloc((n, c), out_dtype, dev, stream) if c else None
+    if status is None:
+        status = _alloc(1, torch.int32, dev, stream, zero=True)
+    bad = _alloc(1, torch.int64, dev, stream)
+    g = (ctypes.c_float * 3)(*[float(x) for x in grid])
+    L = lib()
+    ws = _ws(int(L.spc_voxelize_workspace_size(n)), dev, stream=stream)
+    _check(L.spc_voxelize(_ptr(points), points.stride(0), _ptr(batch), n, _ptr(n_dev), g, spec, _ptr(feats),
+                          feats.stride(0) if feats is not None else 0, c, _ptr(keys), _ptr(n_vox), _ptr(pv), _ptr(out),
+                          out.stride(0) if out is not None else 0, _DT[out_dtype], _ptr(status), _ptr(bad), _ptr(ws),
+                          ws.numel(), _stream(stream)), "spc_voxelize")
+    _release(ws, stream)
+    return keys, n_vox, pv, out, status, bad
 
 
 # ---------------------------------------------------------------------------------------

@@ -9,7 +9,10 @@
 //                 scatter staged through shared memory (coalesced digit runs)
 // Every kernel reads the element count from device memory (n_dev), so the whole
 // indexing phase runs without host syncs.
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
+
+#include <cmath>
 
 #include "spc_common.cuh"
 
@@ -526,6 +529,138 @@ __global__ void __launch_bounds__(SORT_THREADS) k_unique_write(const uint64_t *_
     }
 }
 
+// ------------------------------------------------------------------------------------
+// NEXT-2 voxelization front-end (§2.1 v = floor(p / g); S:132 averaging):
+// quantise + pack + histograms in one pass, the stable radix sort, then one pass that
+// writes the unique keys, each voxel's first sorted position and the point -> voxel map,
+// and a warp-per-voxel mean of the features in ascending point order
+// ------------------------------------------------------------------------------------
+struct VoxGrid {
+    float g[3];
+};
+
+__global__ void __launch_bounds__(256) k_voxel_pack(const float *__restrict__ pts, int64_t ld,
+                                                    const int32_t *__restrict__ batch, int64_t n_cap,
+                                                    const int64_t *n_dev, VoxGrid vg, PackDev s,
+                                                    uint64_t *__restrict__ keys, uint32_t *status,
+                                                    unsigned long long *bad_point, int passes,
+                                                    unsigned int *__restrict__ ghist, int64_t *total_out) {
+    pdl_wait();   // PDL launch: the predecessor has completed and flushed
+    pdl_trigger();
+    __shared__ unsigned int h[MAX_PASSES][256];
+    for (int i = threadIdx.x; i < passes * 256; i += blockDim.x) h[i / 256][i % 256] = 0;
+    __syncthreads();
+    const int64_t n = dev_count(n_cap, n_dev);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *total_out = n;
+    bool out_of_field = false, non_finite = false;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t v[3];
+        bool fin = true;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            // float32 quotient, IEEE round-to-nearest (reading V1); a non-finite p gives a
+            // non-finite quotient, so checking q covers both
+            const float q = __fdiv_rn(pts[i * ld + d], vg.g[d]);
+            const float f = floorf(q);
+            const bool ok = isfinite(q) && f >= -2147483648.0f && f < 2147483648.0f;
+            fin &= ok;
+            v[d] = ok ? (int64_t)f : 0;
+        }
+        if (!fin) {
+            non_finite = true;
+            if (bad_point) atomicMin(bad_point, (unsigned long long)i);
+        }
+        const int64_t fb = batch ? batch[i] : 0;
+        const int64_t fx = v[0] + (1ll << (s.bx - 1)), fy = v[1] + (1ll << (s.by - 1)), fz = v[2] + (1ll << (s.bz - 1));
+        const bool ok = fb >= 0 && fb < (1ll << s.bb) && fx >= s.lo_room && fx < (1ll << s.bx) - s.hi_room &&
+                        fy >= s.lo_room && fy < (1ll << s.by) - s.hi_room && fz >= s.lo_room &&
+                        fz < (1ll << s.bz) - s.hi_room;
+        out_of_field |= !ok;
+        const uint64_t k = ((uint64_t)fb << (s.bx + s.by + s.bz)) | ((uint64_t)fx << (s.by + s.bz)) |
+                           ((uint64_t)fy << s.bz) | (uint64_t)fz;
+        keys[i] = k;
+        for (int p = 0; p < passes; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 255u], 1u);   // sort histograms
+    }
+    const bool r = __any_sync(0xffffffffu, out_of_field), f = __any_sync(0xffffffffu, non_finite);
+    if (status && (threadIdx.x & 31) == 0 && (r || f))
+        atomicOr(status, (r ? SPC_FLAG_RANGE : 0u) | (f ? SPC_FLAG_NONFINITE : 0u));
+    __syncthreads();
+    for (int i = threadIdx.x; i < passes * 256; i += blockDim.x)
+        if (h[i / 256][i % 256]) atomicAdd(&ghist[i], h[i / 256][i % 256]);
+}
+
+// unique keys, each voxel's first sorted position, and point -> voxel (a voxel's index is
+// the number of run heads before it: the tile prefix from k_unique_scan + a block scan)
+__global__ void __launch_bounds__(SORT_THREADS) k_voxel_segments(const uint64_t *__restrict__ k,
+                                                                 const int32_t *__restrict__ perm,
+                                                                 const int64_t *total_dev,
+                                                                 const int *__restrict__ tile_scan,
+                                                                 uint64_t *__restrict__ keys_out,
+                                                                 int32_t *__restrict__ seg_start,
+                                                                 int32_t *__restrict__ point_voxel) {
+    pdl_wait();   // PDL launch: the predecessor has completed and flushed
+    pdl_trigger();
+    __shared__ int ws[SORT_WARPS];
+    const int64_t total = *total_dev;
+    const int64_t base = (int64_t)blockIdx.x * SORT_TILE;
+    if (base >= total) return;
+    int f[SORT_ITEMS];
+    int c = 0;
+#pragma unroll
+    for (int it = 0; it < SORT_ITEMS; ++it) {
+        const int64_t i = base + threadIdx.x * SORT_ITEMS + it;
+        f[it] = (i < total) && (i == 0 || k[i] != k[i - 1]);
+        c += f[it];
+    }
+    int tot;
+    int pos = block_excl_scan_256(c, ws, tot) + tile_scan[blockIdx.x];
+#pragma unroll
+    for (int it = 0; it < SORT_ITEMS; ++it) {
+        const int64_t i = base + threadIdx.x * SORT_ITEMS + it;
+        if (i >= total) break;
+        if (f[it]) {
+            keys_out[pos] = k[i];
+            seg_start[pos] = (int32_t)i;
+            ++pos;
+        }
+        if (point_voxel) point_voxel[perm[i]] = pos - 1;
+    }
+}
+
+// one warp per voxel, lane = channel: the fp32 sum of the voxel's points in ascending
+// point index (stable sort order), divided by the count, rounded once to the output
+__global__ void __launch_bounds__(256) k_voxel_mean(const float *__restrict__ feats, int64_t ld_f, int c,
+                                                    const int32_t *__restrict__ perm,
+                                                    const int32_t *__restrict__ seg_start, const int64_t *n_vox_dev,
+                                                    const int64_t *total_dev, void *__restrict__ out, int64_t ld_out,
+                                                    int out_dtype, int64_t *bad_point) {
+    pdl_wait();   // PDL launch: the predecessor has completed and flushed
+    pdl_trigger();
+    if (bad_point && blockIdx.x == 0 && threadIdx.x == 0 && *bad_point == INT64_MAX) *bad_point = -1;
+    if (c == 0) return;
+    const int64_t nv = *n_vox_dev, total = *total_dev;
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t v = w0; v < nv; v += nw) {
+        const int64_t s = seg_start[v], e = v + 1 < nv ? seg_start[v + 1] : total;
+        const float cnt = (float)(e - s);
+        for (int ch = lane; ch < c; ch += 32) {
+            float acc = 0.f;
+            for (int64_t j = s; j < e; ++j) acc = __fadd_rn(acc, feats[(int64_t)perm[j] * ld_f + ch]);
+            const float m = __fdiv_rn(acc, cnt);
+            if (out_dtype == SPC_F32) static_cast<float *>(out)[v * ld_out + ch] = m;
+            else static_cast<__nv_bfloat16 *>(out)[v * ld_out + ch] = __float2bfloat16_rn(m);
+        }
+    }
+}
+
+__global__ void k_voxel_init(int64_t *bad_point, int64_t *n_vox, int64_t n_cap) {
+    pdl_wait();
+    pdl_trigger();
+    if (bad_point) *bad_point = n_cap > 0 ? INT64_MAX : -1;
+    if (n_vox && n_cap == 0) *n_vox = 0;
+}
+
 }  // namespace spc
 
 using namespace spc;
@@ -674,5 +809,79 @@ extern "C" spc_status spc_downsample(const uint64_t *keys, int64_t n, const int6
     const uint64_t strip = used >= 64 ? ~0ull : ((1ull << used) - 1);
     SPC_CUDA(launch_pdl(k_unique_write, dim3(nt), dim3(SORT_THREADS), 0, st, sorted, scal, n, n_dev, tile_cnt, scal + 1, strip, level_keys, n));
     SPC_LAUNCH_CHECK("unique");
+    return SPC_OK;
+}
+
+// ------------------------------------------------------------------------------------
+// NEXT-2 voxelization front-end (spc.h)
+// ------------------------------------------------------------------------------------
+extern "C" size_t spc_voxelize_workspace_size(int64_t n) {
+    if (n < 0) n = 0;
+    Sizer z;
+    z.take<uint64_t>((size_t)n);                        // raw keys
+    z.take<uint64_t>((size_t)n);                        // sorted keys
+    z.take<int32_t>((size_t)n);                         // perm
+    z.take<int32_t>((size_t)n);                         // seg_start
+    z.take<int64_t>(4);                                 // total, level_base[2]
+    z.take<int>((size_t)(n / SORT_TILE + 2));           // tile counts
+    return z.used + radix_sort_workspace(n, true) + 512;
+}
+
+extern "C" spc_status spc_voxelize(const float *points, int64_t ld, const int32_t *batch, int64_t n, const int64_t *n_dev,
+                                   const float *grid_host, spc_pack_spec spec, const float *feats, int64_t ld_feats,
+                                   int32_t c, uint64_t *keys_out, int64_t *n_vox_dev, int32_t *point_voxel,
+                                   void *feats_out, int64_t ld_out, int32_t out_dtype, uint32_t *status,
+                                   int64_t *bad_point_dev, void *ws, size_t ws_bytes, void *stream) {
+    SPC_CHECK_ARG(n >= 0 && n < (int64_t)INT32_MAX, "n out of range");
+    SPC_CHECK_ARG(grid_host && n_vox_dev && (keys_out || n == 0), "null grid / keys_out / n_vox_dev");
+    for (int d = 0; d < 3; ++d)
+        SPC_CHECK_ARG(std::isfinite(grid_host[d]) && grid_host[d] > 0.f, "grid sizes must be finite and > 0");
+    SPC_CHECK_ARG(c >= 0 && (c == 0 || (feats && feats_out && ld_feats >= c && ld_out >= c)),
+                  "c < 0, or features without feats / feats_out / row strides >= c");
+    SPC_CHECK_ARG(out_dtype == SPC_F32 || out_dtype == SPC_BF16, "out_dtype must be SPC_F32 or SPC_BF16");
+    const int used = spec.bits_b + spec.bits_x + spec.bits_y + spec.bits_z;
+    SPC_CHECK_ARG(spec.bits_b >= 0 && spec.bits_x >= 2 && spec.bits_y >= 2 && spec.bits_z >= 2 && used <= 62,
+                  "bad pack spec");
+    SPC_CHECK_ARG(spec.reach >= 0 && spec.out_stride >= 1 && (spec.out_stride & (spec.out_stride - 1)) == 0,
+                  "pack spec: reach must be >= 0 and out_stride a power of two >= 1");
+    cudaStream_t st = as_stream(stream);
+    if (n == 0) {
+        SPC_CUDA(launch_pdl(k_voxel_init, dim3(1), dim3(1), 0, st, bad_point_dev, n_vox_dev, (int64_t)0));
+        SPC_LAUNCH_CHECK("k_voxel_init");
+        return SPC_OK;
+    }
+    SPC_CHECK_ARG(points && ld >= 3, "null points or ld < 3");
+    if (ws_bytes < spc_voxelize_workspace_size(n)) return fail(SPC_ERR_WORKSPACE, "spc_voxelize: ws too small");
+    Bump b(ws, ws_bytes);
+    uint64_t *raw = b.take<uint64_t>((size_t)n);
+    uint64_t *sorted = b.take<uint64_t>((size_t)n);
+    int32_t *perm = b.take<int32_t>((size_t)n);
+    int32_t *seg = b.take<int32_t>((size_t)n);
+    int64_t *scal = b.take<int64_t>(4);
+    const int nt = (int)((n + SORT_TILE - 1) / SORT_TILE);
+    int *tile_cnt = b.take<int>((size_t)(n / SORT_TILE + 2));
+    void *rws = b.base + align_up(b.used, 256);
+    const size_t rws_bytes = ws_bytes - align_up(b.used, 256);
+    unsigned int *hist = reinterpret_cast<unsigned int *>(rws);   // == radix_sort's first workspace block
+    SPC_CUDA(cudaMemsetAsync(hist, 0, sizeof(unsigned int) * MAX_PASSES * 256, st));
+    SPC_CUDA(launch_pdl(k_voxel_init, dim3(1), dim3(1), 0, st, bad_point_dev, (int64_t *)nullptr, n));
+    VoxGrid vg{{grid_host[0], grid_host[1], grid_host[2]}};
+    PackDev pd{spec.bits_b, spec.bits_x, spec.bits_y, spec.bits_z, spec.out_stride - 1 + spec.reach, spec.reach};
+    const int grid = (int)imin64((n + 2047) / 2048, 2 * 148);
+    SPC_CUDA(launch_pdl(k_voxel_pack, dim3(grid), dim3(256), 0, st, points, ld, batch, n, n_dev, vg, pd, raw, status,
+                        reinterpret_cast<unsigned long long *>(bad_point_dev), (used + 7) / 8, hist, scal));
+    SPC_LAUNCH_CHECK("k_voxel_pack");
+    spc_status s = radix_sort(raw, nullptr, n, n_dev, used, sorted, perm, rws, rws_bytes, st, true);
+    if (s != SPC_OK) return s;
+    SPC_CUDA(launch_pdl(k_unique_count, dim3(nt), dim3(SORT_THREADS), 0, st, sorted, scal, tile_cnt));
+    SPC_CUDA(launch_pdl(k_unique_scan, dim3(1), dim3(1024), 0, st, tile_cnt, nt, sorted, scal, n, n_dev, 1, scal + 1,
+                        n_vox_dev));
+    SPC_CUDA(launch_pdl(k_voxel_segments, dim3(nt), dim3(SORT_THREADS), 0, st, sorted, perm, scal, tile_cnt, keys_out,
+                        seg, point_voxel));
+    SPC_LAUNCH_CHECK("k_voxel_segments");
+    const int mgrid = (int)imin64((n + 7) / 8, 16 * 148);
+    SPC_CUDA(launch_pdl(k_voxel_mean, dim3(mgrid), dim3(256), 0, st, feats, ld_feats, (int)c, perm, seg, n_vox_dev, scal,
+                        feats_out, ld_out, (int)out_dtype, bad_point_dev));
+    SPC_LAUNCH_CHECK("k_voxel_mean");
     return SPC_OK;
 }

@@ -250,6 +250,12 @@ def make_scan(config: int, scan_index: int = 0, batch: int = 0, calibrate: bool 
     """One synthetic scan for BASELINE config ``config`` (1..5): int32 [N, 4] (b,x,y,z),
     unique rows, random row order.  With ``calibrate`` the azimuth count is rescaled
     once so that N lands within +-10% of the preset target."""
+    _, c = _calibrated_scan(config, scan_index, batch, calibrate)
+    rng = np.random.default_rng(scan_seed(config, scan_index) + 7)
+    return c[rng.permutation(c.shape[0])]
+
+
+def _calibrated_scan(config: int, scan_index: int, batch: int, calibrate: bool):
     preset = PRESETS[CONFIG_PRESET[config]]
     seed = scan_seed(config, scan_index)
     n_az = preset.n_az
@@ -263,8 +269,20 @@ def make_scan(config: int, scan_index: int = 0, batch: int = 0, calibrate: bool 
             n_az = int(round(n_az * min(2.0, max(0.5, ratio ** 1.25))))
             pts = lidar_points(preset, seed, n_az)
             c = voxelize_unique(pts, preset.grid, batch)
-    rng = np.random.default_rng(seed + 7)
-    return c[rng.permutation(c.shape[0])]
+    return pts, c
+
+
+def make_points(config: int, scan_index: int = 0):
+    """The raw points behind make_scan(config, scan_index) for the voxelization front-end
+    (SURVEY NEXT-2): float32 [n, 4] rows (x, y, z, intensity) in a seeded random order,
+    and the preset's grid.  Intensity ~ U[0, 1) stands in for the sensor's return value."""
+    preset = PRESETS[CONFIG_PRESET[config]]
+    pts, _ = _calibrated_scan(config, scan_index, 0, True)
+    rng = np.random.default_rng(scan_seed(config, scan_index) + 11)
+    out = np.empty((pts.shape[0], 4), np.float32)
+    out[:, :3] = pts[rng.permutation(pts.shape[0])]
+    out[:, 3] = rng.random(pts.shape[0], dtype=np.float32)
+    return out, tuple(float(g) for g in np.broadcast_to(np.asarray(preset.grid, dtype=np.float64), (3,)))
 
 
 def make_batch(config: int, n_scans: int, first_scan: int = 0) -> np.ndarray:
