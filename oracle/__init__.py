@@ -15,6 +15,8 @@ arrays through ctypes.  Every function follows a definition in PAPER.md:
 ``kmap``               M[i,k] = j iff p_j = q_i + delta_k, hash-set lookup
 ``conv``               Eq. (2) in fp64, OS or WS loop order
 ``conv_rows``          Eq. (2) for sampled output rows (full-size sampled parity)
+``offsets/kmap/conv``  also over (Kx, Ky, Kz) boxes, even sizes {0..K-1}
+``regular_outputs``    spconv's regular output rule
 ``voxelize``           v = floor(p/g) in float32, unique, mean feature (§2.1)
 =====================  =============================================================
 
@@ -85,6 +87,16 @@ def _L():
         lib.orc_conv.restype = I64
         lib.orc_conv_rows.argtypes = [P, I64, P, P, I64, I, I, I, P, I, P, I, P]
         lib.orc_conv_rows.restype = I64
+        lib.orc_offsets3.argtypes = [I, I, I, I, P, P]
+        lib.orc_offsets3.restype = I
+        lib.orc_kmap3.argtypes = [P, I64, P, I64, I, I, I, I, I, P, I64]
+        lib.orc_kmap3.restype = I64
+        lib.orc_conv3.argtypes = [P, I64, P, I64, I, I, I, I, I, P, I, P, I, P, I]
+        lib.orc_conv3.restype = I64
+        lib.orc_conv_rows3.argtypes = [P, I64, P, P, I64, I, I, I, I, I, P, I, P, I, P]
+        lib.orc_conv_rows3.restype = I64
+        lib.orc_regular_outputs.argtypes = [P, I64, I, I, I, I, I, P]
+        lib.orc_regular_outputs.restype = I64
         lib.orc_voxelize.argtypes = [P, I64, P, I64, P, P, I64, I, P, P, P]
         lib.orc_voxelize.restype = I64
         lib.orc_num_threads.argtypes = []
@@ -134,49 +146,80 @@ def downsample(coords, s: int):
     return out[:m].copy()
 
 
-def offsets(K: int, spacing: int = 1):
-    """-> (int32 [K^3, 3] offsets, int32 [K^3] L1 norm in units of ``spacing``)."""
-    kv = K ** 3
-    off = np.empty((kv, 3), np.int32)
-    l1 = np.empty(kv, np.int32)
-    r = _L().orc_offsets(int(K), int(spacing), _p(off), _p(l1))
-    if r < 0:
-        raise ValueError("even or non-positive K")
+def _box(K):
+    """K (odd, cubic: Delta(K, s_p) of P:111) or a tuple (Kx, Ky, Kz) (the generalised
+    box of SURVEY NEXT-3, even sizes {0..K-1}) -> (kx, ky, kz, generalised?)."""
+    if isinstance(K, (tuple, list)):
+        return int(K[0]), int(K[1]), int(K[2]), True
+    K = int(K)
+    return K, K, K, K % 2 == 0
+
+
+def offsets(K, spacing: int = 1):
+    """-> (int32 [kv, 3] offsets, int32 [kv] L1 norm in units of ``spacing``).  An int K must
+    be odd; a tuple (Kx, Ky, Kz) gives the generalised box (NEXT-3, reading E1)."""
+    if not isinstance(K, (tuple, list)):
+        kv = int(K) ** 3
+        off = np.empty((max(kv, 1), 3), np.int32)
+        l1 = np.empty(max(kv, 1), np.int32)
+        r = _L().orc_offsets(int(K), int(spacing), _p(off), _p(l1))
+        if r < 0:
+            raise ValueError("even or non-positive K")
+        return off, l1
+    kx, ky, kz, _ = _box(K)
+    kv = kx * ky * kz
+    off = np.empty((max(kv, 1), 3), np.int32)
+    l1 = np.empty(max(kv, 1), np.int32)
+    if _L().orc_offsets3(kx, ky, kz, int(spacing), _p(off), _p(l1)) < 0:
+        raise ValueError("non-positive kernel size")
     return off, l1
 
 
-def kmap(in_coords, out_coords, K: int, spacing: int, transposed: bool = False):
-    """-> int32 [nnz, 3] triples (k, out_index, in_index), lexicographically sorted."""
+def kmap(in_coords, out_coords, K, spacing: int, transposed: bool = False):
+    """-> int32 [nnz, 3] triples (k, out_index, in_index), lexicographically sorted.
+    K: odd int or (Kx, Ky, Kz) (NEXT-3)."""
     a = _c(in_coords, np.int32).reshape(-1, 4)
     b = _c(out_coords, np.int32).reshape(-1, 4)
     L = _L()
-    nnz = L.orc_kmap(_p(a), a.shape[0], _p(b), b.shape[0], int(K), int(spacing), int(transposed),
-                     None, 0)
+    kx, ky, kz, gen = _box(K)
+
+    def run(t, cap):
+        if gen:
+            return L.orc_kmap3(_p(a), a.shape[0], _p(b), b.shape[0], kx, ky, kz, int(spacing), int(transposed), t, cap)
+        return L.orc_kmap(_p(a), a.shape[0], _p(b), b.shape[0], kx, int(spacing), int(transposed), t, cap)
+
+    nnz = run(None, 0)
     if nnz < 0:
         raise ValueError("orc_kmap failed")
-    t = np.empty((nnz, 3), np.int32)
-    L.orc_kmap(_p(a), a.shape[0], _p(b), b.shape[0], int(K), int(spacing), int(transposed), _p(t), nnz)
-    return t
+    t = np.empty((max(nnz, 1), 3), np.int32)
+    run(_p(t), nnz)
+    return t[:nnz]
 
 
-def conv(in_coords, out_coords, K: int, spacing: int, F_in, W, transposed: bool = False,
+def conv(in_coords, out_coords, K, spacing: int, F_in, W, transposed: bool = False,
          order: str = "os"):
-    """Eq. (2) in fp64.  F_in [n_in, c_in], W [K^3, c_in, c_out] -> F_out [n_out, c_out]."""
+    """Eq. (2) in fp64.  F_in [n_in, c_in], W [kv, c_in, c_out] -> F_out [n_out, c_out]."""
     a = _c(in_coords, np.int32).reshape(-1, 4)
     b = _c(out_coords, np.int32).reshape(-1, 4)
     F = _c(F_in, np.float64)
     Wd = _c(W, np.float64)
     c_in, c_out = Wd.shape[1], Wd.shape[2]
-    assert F.shape == (a.shape[0], c_in) and Wd.shape[0] == K ** 3
+    kx, ky, kz, gen = _box(K)
+    assert F.shape == (a.shape[0], c_in) and Wd.shape[0] == kx * ky * kz
     out = np.empty((b.shape[0], c_out), np.float64)
-    r = _L().orc_conv(_p(a), a.shape[0], _p(b), b.shape[0], int(K), int(spacing), int(transposed),
-                      _p(F), c_in, _p(Wd), c_out, _p(out), 0 if order == "os" else 1)
+    o = 0 if order == "os" else 1
+    if gen:
+        r = _L().orc_conv3(_p(a), a.shape[0], _p(b), b.shape[0], kx, ky, kz, int(spacing), int(transposed),
+                           _p(F), c_in, _p(Wd), c_out, _p(out), o)
+    else:
+        r = _L().orc_conv(_p(a), a.shape[0], _p(b), b.shape[0], kx, int(spacing), int(transposed),
+                          _p(F), c_in, _p(Wd), c_out, _p(out), o)
     if r < 0:
         raise ValueError("orc_conv failed")
     return out
 
 
-def conv_rows(in_coords, out_coords, rows, K: int, spacing: int, F_in, W, transposed: bool = False):
+def conv_rows(in_coords, out_coords, rows, K, spacing: int, F_in, W, transposed: bool = False):
     """Eq. (2) for output rows ``rows`` only -> [len(rows), c_out] fp64."""
     a = _c(in_coords, np.int32).reshape(-1, 4)
     b = _c(out_coords, np.int32).reshape(-1, 4)
@@ -184,12 +227,29 @@ def conv_rows(in_coords, out_coords, rows, K: int, spacing: int, F_in, W, transp
     F = _c(F_in, np.float64)
     Wd = _c(W, np.float64)
     c_in, c_out = Wd.shape[1], Wd.shape[2]
+    kx, ky, kz, gen = _box(K)
     out = np.empty((rr.shape[0], c_out), np.float64)
-    r = _L().orc_conv_rows(_p(a), a.shape[0], _p(b), _p(rr), rr.shape[0], int(K), int(spacing),
-                           int(transposed), _p(F), c_in, _p(Wd), c_out, _p(out))
+    if gen:
+        r = _L().orc_conv_rows3(_p(a), a.shape[0], _p(b), _p(rr), rr.shape[0], kx, ky, kz, int(spacing),
+                                int(transposed), _p(F), c_in, _p(Wd), c_out, _p(out))
+    else:
+        r = _L().orc_conv_rows(_p(a), a.shape[0], _p(b), _p(rr), rr.shape[0], kx, int(spacing),
+                               int(transposed), _p(F), c_in, _p(Wd), c_out, _p(out))
     if r < 0:
         raise ValueError("orc_conv_rows failed")
     return out
+
+
+def regular_outputs(in_coords, K, spacing: int, out_stride: int):
+    """spconv's regular output rule: sorted unique int32 [m, 4] sites
+    (b, p - delta) on the out_stride lattice, p in in_coords, delta in the offset box."""
+    a = _c(in_coords, np.int32).reshape(-1, 4)
+    kx, ky, kz, _ = _box(K)
+    out = np.empty((max(a.shape[0] * kx * ky * kz, 1), 4), np.int32)
+    m = _L().orc_regular_outputs(_p(a), a.shape[0], kx, ky, kz, int(spacing), int(out_stride), _p(out))
+    if m < 0:
+        raise ValueError("orc_regular_outputs failed")
+    return out[:m].copy()
 
 
 def voxelize(points, grid, batch=None, feats=None):

@@ -131,6 +131,26 @@ int orc_offsets(int K, int spacing, int32_t *off_out, int32_t *l1_units_out) {
     return k;
 }
 
+/* Generalised offset box: per axis K_a offsets; odd K_a centred as in
+ * Delta(K, s_p), even K_a = {0, .., K_a - 1} (reading E1: the K = 2 down/up
+ * layers' {0, s_p}^3); lexicographic (dx, dy, dz), dz fastest. */
+int orc_offsets3(int kx, int ky, int kz, int spacing, int32_t *off_out, int32_t *l1_units_out) {
+    if (kx <= 0 || ky <= 0 || kz <= 0) return -1;
+    const int lx = (kx % 2) ? -(kx - 1) / 2 : 0, ly = (ky % 2) ? -(ky - 1) / 2 : 0, lz = (kz % 2) ? -(kz - 1) / 2 : 0;
+    int k = 0;
+    for (int ex = lx; ex < lx + kx; ++ex)
+        for (int ey = ly; ey < ly + ky; ++ey)
+            for (int ez = lz; ez < lz + kz; ++ez, ++k) {
+                if (off_out) {
+                    off_out[3 * k + 0] = ex * spacing;
+                    off_out[3 * k + 1] = ey * spacing;
+                    off_out[3 * k + 2] = ez * spacing;
+                }
+                if (l1_units_out) l1_units_out[k] = abs(ex) + abs(ey) + abs(ez);
+            }
+    return k;
+}
+
 /* ------------------------------------------------------------------------------------
  * hash set over (b,x,y,z) tuples -> canonical index (open addressing, linear probing)
  * ---------------------------------------------------------------------------------- */
@@ -188,14 +208,10 @@ static void make_query(const int32_t *q, const int32_t *off, int transposed, int
  * kernel map (§2.2): M[i,k] = j if q_i + delta_k matches p_j, else -1
  * ---------------------------------------------------------------------------------- */
 
-int64_t orc_kmap(const int32_t *in_coords, int64_t n_in, const int32_t *out_coords, int64_t n_out,
-                 int K, int spacing, int transposed, int32_t *triples, int64_t cap) {
-    int kv = orc_offsets(K, 1, NULL, NULL);
-    if (kv < 0) return -1;
-    int32_t *off = (int32_t *)malloc(sizeof(int32_t) * 3 * (size_t)kv);
-    orc_offsets(K, spacing, off, NULL);
+static int64_t kmap_impl(const int32_t *in_coords, int64_t n_in, const int32_t *out_coords, int64_t n_out,
+                         const int32_t *off, int kv, int transposed, int32_t *triples, int64_t cap) {
     orc_hash h;
-    if (hash_build(&h, in_coords, n_in)) { free(off); return -1; }
+    if (hash_build(&h, in_coords, n_in)) return -1;
     int64_t nnz = 0;
     int32_t t[4];
     for (int k = 0; k < kv; ++k)
@@ -211,8 +227,37 @@ int64_t orc_kmap(const int32_t *in_coords, int64_t n_in, const int32_t *out_coor
             ++nnz;
         }
     free(h.slot);
-    free(off);
     return nnz;
+}
+
+/* the offset table of Delta(K, s_p) (cubic odd K) or of the generalised box */
+static int32_t *offset_table(int kx, int ky, int kz, int cubic_odd_only, int spacing, int *kv) {
+    *kv = cubic_odd_only ? orc_offsets(kx, 1, NULL, NULL) : orc_offsets3(kx, ky, kz, 1, NULL, NULL);
+    if (*kv < 0) return NULL;
+    int32_t *off = (int32_t *)malloc(sizeof(int32_t) * 3 * (size_t)*kv);
+    if (cubic_odd_only) orc_offsets(kx, spacing, off, NULL);
+    else orc_offsets3(kx, ky, kz, spacing, off, NULL);
+    return off;
+}
+
+int64_t orc_kmap(const int32_t *in_coords, int64_t n_in, const int32_t *out_coords, int64_t n_out,
+                 int K, int spacing, int transposed, int32_t *triples, int64_t cap) {
+    int kv;
+    int32_t *off = offset_table(K, K, K, 1, spacing, &kv);
+    if (!off) return -1;
+    int64_t r = kmap_impl(in_coords, n_in, out_coords, n_out, off, kv, transposed, triples, cap);
+    free(off);
+    return r;
+}
+
+int64_t orc_kmap3(const int32_t *in_coords, int64_t n_in, const int32_t *out_coords, int64_t n_out,
+                  int kx, int ky, int kz, int spacing, int transposed, int32_t *triples, int64_t cap) {
+    int kv;
+    int32_t *off = offset_table(kx, ky, kz, 0, spacing, &kv);
+    if (!off) return -1;
+    int64_t r = kmap_impl(in_coords, n_in, out_coords, n_out, off, kv, transposed, triples, cap);
+    free(off);
+    return r;
 }
 
 /* ------------------------------------------------------------------------------------
@@ -227,15 +272,12 @@ static void axpy_row(const double *f, int c_in, const double *Wk, int c_out, dou
     }
 }
 
-int64_t orc_conv(const int32_t *in_coords, int64_t n_in, const int32_t *out_coords, int64_t n_out,
-                 int K, int spacing, int transposed, const double *F_in, int c_in,
-                 const double *W, int c_out, double *F_out, int order) {
-    int kv = orc_offsets(K, 1, NULL, NULL);
-    if (kv < 0 || c_in <= 0 || c_out <= 0) return -1;
-    int32_t *off = (int32_t *)malloc(sizeof(int32_t) * 3 * (size_t)kv);
-    orc_offsets(K, spacing, off, NULL);
+static int64_t conv_impl(const int32_t *in_coords, int64_t n_in, const int32_t *out_coords, int64_t n_out,
+                         const int32_t *off, int kv, int transposed, const double *F_in, int c_in,
+                         const double *W, int c_out, double *F_out, int order) {
+    if (c_in <= 0 || c_out <= 0) return -1;
     orc_hash h;
-    if (hash_build(&h, in_coords, n_in)) { free(off); return -1; }
+    if (hash_build(&h, in_coords, n_in)) return -1;
     memset(F_out, 0, sizeof(double) * (size_t)n_out * (size_t)c_out);
     int64_t nnz = 0;
     int32_t t[4];
@@ -265,19 +307,36 @@ int64_t orc_conv(const int32_t *in_coords, int64_t n_in, const int32_t *out_coor
             }
     }
     free(h.slot);
-    free(off);
     return nnz;
 }
 
-int64_t orc_conv_rows(const int32_t *in_coords, int64_t n_in, const int32_t *out_coords,
-                      const int64_t *rows, int64_t n_rows, int K, int spacing, int transposed,
-                      const double *F_in, int c_in, const double *W, int c_out, double *F_out) {
-    int kv = orc_offsets(K, 1, NULL, NULL);
-    if (kv < 0) return -1;
-    int32_t *off = (int32_t *)malloc(sizeof(int32_t) * 3 * (size_t)kv);
-    orc_offsets(K, spacing, off, NULL);
+int64_t orc_conv(const int32_t *in_coords, int64_t n_in, const int32_t *out_coords, int64_t n_out,
+                 int K, int spacing, int transposed, const double *F_in, int c_in,
+                 const double *W, int c_out, double *F_out, int order) {
+    int kv;
+    int32_t *off = offset_table(K, K, K, 1, spacing, &kv);
+    if (!off) return -1;
+    int64_t r = conv_impl(in_coords, n_in, out_coords, n_out, off, kv, transposed, F_in, c_in, W, c_out, F_out, order);
+    free(off);
+    return r;
+}
+
+int64_t orc_conv3(const int32_t *in_coords, int64_t n_in, const int32_t *out_coords, int64_t n_out,
+                  int kx, int ky, int kz, int spacing, int transposed, const double *F_in, int c_in,
+                  const double *W, int c_out, double *F_out, int order) {
+    int kv;
+    int32_t *off = offset_table(kx, ky, kz, 0, spacing, &kv);
+    if (!off) return -1;
+    int64_t r = conv_impl(in_coords, n_in, out_coords, n_out, off, kv, transposed, F_in, c_in, W, c_out, F_out, order);
+    free(off);
+    return r;
+}
+
+static int64_t conv_rows_impl(const int32_t *in_coords, int64_t n_in, const int32_t *out_coords,
+                              const int64_t *rows, int64_t n_rows, const int32_t *off, int kv, int transposed,
+                              const double *F_in, int c_in, const double *W, int c_out, double *F_out) {
     orc_hash h;
-    if (hash_build(&h, in_coords, n_in)) { free(off); return -1; }
+    if (hash_build(&h, in_coords, n_in)) return -1;
     memset(F_out, 0, sizeof(double) * (size_t)n_rows * (size_t)c_out);
     int64_t nnz = 0;
 #pragma omp parallel for reduction(+ : nnz) schedule(dynamic, 64)
@@ -292,8 +351,59 @@ int64_t orc_conv_rows(const int32_t *in_coords, int64_t n_in, const int32_t *out
             ++nnz;
         }
     free(h.slot);
-    free(off);
     return nnz;
+}
+
+int64_t orc_conv_rows(const int32_t *in_coords, int64_t n_in, const int32_t *out_coords,
+                      const int64_t *rows, int64_t n_rows, int K, int spacing, int transposed,
+                      const double *F_in, int c_in, const double *W, int c_out, double *F_out) {
+    int kv;
+    int32_t *off = offset_table(K, K, K, 1, spacing, &kv);
+    if (!off) return -1;
+    int64_t r = conv_rows_impl(in_coords, n_in, out_coords, rows, n_rows, off, kv, transposed, F_in, c_in, W, c_out,
+                               F_out);
+    free(off);
+    return r;
+}
+
+int64_t orc_conv_rows3(const int32_t *in_coords, int64_t n_in, const int32_t *out_coords,
+                       const int64_t *rows, int64_t n_rows, int kx, int ky, int kz, int spacing, int transposed,
+                       const double *F_in, int c_in, const double *W, int c_out, double *F_out) {
+    int kv;
+    int32_t *off = offset_table(kx, ky, kz, 0, spacing, &kv);
+    if (!off) return -1;
+    int64_t r = conv_rows_impl(in_coords, n_in, out_coords, rows, n_rows, off, kv, transposed, F_in, c_in, W, c_out,
+                               F_out);
+    free(off);
+    return r;
+}
+
+/* spconv's "regular" output rule (P:476-478 networks' public definitions):
+ * V_out = { (b, p - delta) : p in V_in, delta in the offset box (spacing), every spatial
+ * coordinate of p - delta a multiple of out_stride } -- every output site of stride
+ * out_stride whose kernel footprint touches an input.  Written sorted and unique to out
+ * (room for n * K_x K_y K_z rows).  Returns |V_out| or -1. */
+int64_t orc_regular_outputs(const int32_t *in_coords, int64_t n, int kx, int ky, int kz, int spacing,
+                            int out_stride, int32_t *out) {
+    int kv;
+    int32_t *off = offset_table(kx, ky, kz, 0, spacing, &kv);
+    if (!off || out_stride < 1) { free(off); return -1; }
+    int32_t *cand = (int32_t *)malloc(sizeof(int32_t) * 4 * (size_t)(n * kv > 0 ? n * kv : 1));
+    int64_t m = 0;
+    for (int64_t i = 0; i < n; ++i)
+        for (int k = 0; k < kv; ++k) {
+            int32_t c[4] = {in_coords[4 * i], 0, 0, 0};
+            int on = 1;
+            for (int d = 0; d < 3; ++d) {
+                c[1 + d] = in_coords[4 * i + 1 + d] - off[3 * k + d];
+                on &= orc_round_down(c[1 + d], out_stride) == c[1 + d];
+            }
+            if (on) { memcpy(cand + 4 * m, c, sizeof(c)); ++m; }
+        }
+    int64_t u = orc_downsample(cand, m, 1, out);   /* stride 1: sort + unique */
+    free(cand);
+    free(off);
+    return u;
 }
 
 /* ------------------------------------------------------------------------------------

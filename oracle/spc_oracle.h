@@ -71,6 +71,22 @@ int64_t orc_conv_rows(const int32_t *in_coords, int64_t n_in, const int32_t *out
                       const int64_t *rows, int64_t n_rows, int K, int spacing, int transposed,
                       const double *F_in, int c_in, const double *W, int c_out, double *F_out);
 
+/* the generalised offset box -- K_a offsets per axis, odd K_a centred as
+ * in Delta(K, s_p), even K_a = {0 .. K_a-1} (reading E1) -- and the
+ * kernel map / Eq. (2) over it (same semantics as the cubic odd functions above). */
+int orc_offsets3(int kx, int ky, int kz, int spacing, int32_t *off_out, int32_t *l1_units_out);
+int64_t orc_kmap3(const int32_t *in_coords, int64_t n_in, const int32_t *out_coords, int64_t n_out,
+                  int kx, int ky, int kz, int spacing, int transposed, int32_t *triples, int64_t cap);
+int64_t orc_conv3(const int32_t *in_coords, int64_t n_in, const int32_t *out_coords, int64_t n_out,
+                  int kx, int ky, int kz, int spacing, int transposed, const double *F_in, int c_in,
+                  const double *W, int c_out, double *F_out, int order);
+int64_t orc_conv_rows3(const int32_t *in_coords, int64_t n_in, const int32_t *out_coords,
+                       const int64_t *rows, int64_t n_rows, int kx, int ky, int kz, int spacing, int transposed,
+                       const double *F_in, int c_in, const double *W, int c_out, double *F_out);
+/* spconv "regular" output sites: sorted unique { (b, p - delta) on the out_stride lattice }. */
+int64_t orc_regular_outputs(const int32_t *in_coords, int64_t n, int kx, int ky, int kz, int spacing,
+                            int out_stride, int32_t *out);
+
 /* Voxelization: v = floor(p_raw / g) per axis (§2.1), the
  * quotient taken in float32 (the points are float32; reading V1) and floored
  * toward -infinity.  Point i: coordinates pts[i*ld + 0..2], batch b_i = batch[i] (batch

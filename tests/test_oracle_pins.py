@@ -446,3 +446,97 @@ def test_voxelize_rejects_non_finite():
     P[3, 2] = np.inf
     with pytest.raises(ValueError, match="point 3"):
         oracle.voxelize(P, (0.1, 0.1, 0.1))
+
+
+# ---------------------------------------------------------------------------------------
+# (Kx, Ky, Kz) offset boxes, even sizes {0..K-1} (reading E1), and spconv's
+# regular output rule
+# ---------------------------------------------------------------------------------------
+
+def _box_offsets_py(K, spacing):
+    rng = [range(-(k - 1) // 2, (k - 1) // 2 + 1) if k % 2 else range(0, k) for k in K]
+    return [(ex * spacing, ey * spacing, ez * spacing) for ex in rng[0] for ey in rng[1] for ez in rng[2]]
+
+
+@pytest.mark.parametrize("K,stride,transposed", [((2, 2, 2), 2, False), ((2, 2, 2), 2, True), ((3, 1, 1), 1, False),
+                                                 ((1, 3, 1), 1, False), ((3, 3, 1), 2, False), ((4, 2, 3), 1, False)])
+def test_box_kmap_bruteforce(K, stride, transposed):
+    """orc_kmap3 vs an O(N^2 kv) double loop over explicitly enumerated offsets."""
+    fine = oracle.sort_coords(synth.random_cloud(300, 10, seed=sum(K) + stride, n_batch=2))[0]
+    coarse = oracle.downsample(fine, stride) if stride > 1 else fine
+    inp, out = (coarse, fine) if transposed else (fine, coarse)
+    off = _box_offsets_py(K, 1)
+    ref = []
+    for k, d in enumerate(off):
+        for i, q in enumerate(out.tolist()):
+            t = [q[0]] + [q[1 + a] - d[a] if transposed else q[1 + a] + d[a] for a in range(3)]
+            for j, p in enumerate(inp.tolist()):
+                if p == t:
+                    ref.append((k, i, j))
+    got = oracle.kmap(inp, out, K, 1, transposed=transposed)
+    assert [tuple(r) for r in got.tolist()] == sorted(ref)
+
+
+def test_box_conv_matches_torch_conv3d():
+    """K = 2 stride-2 down (conv3d kernel 2 stride 2), its transposed up
+    (conv_transpose3d), and a non-cubic (3, 1, 1) submanifold layer (conv3d padding
+    (1, 0, 0)) on dense grids in float64, read at the sparse sites."""
+    rng = np.random.default_rng(21)
+    n = 8
+    occ = rng.random((n, n, n)) < 0.4
+    fine = np.array([[0, x, y, z] for x, y, z in zip(*np.nonzero(occ))], np.int32)
+    F = rng.uniform(-1, 1, (len(fine), 3))
+    grid = torch.zeros((1, 3, n, n, n), dtype=torch.float64)
+    for r, (_, x, y, z) in enumerate(fine.tolist()):
+        grid[0, :, x, y, z] = torch.from_numpy(F[r])
+    # down: out sites = Eq. (1) stride-2 sites (= the regular rule for K = 2, s = 2)
+    coarse = oracle.downsample(fine, 2)
+    W = rng.uniform(-1, 1, (8, 3, 4))
+    got = oracle.conv(fine, coarse, (2, 2, 2), 1, F, W)
+    w = torch.from_numpy(W.reshape(2, 2, 2, 3, 4)).permute(4, 3, 0, 1, 2).contiguous()
+    y = torch.nn.functional.conv3d(grid, w, stride=2)
+    ref = np.stack([y[0, :, x // 2, yy // 2, z // 2].numpy() for _, x, yy, z in coarse.tolist()])
+    np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-12)
+    # up (transposed, same weight index): fine outputs from coarse inputs
+    Fc = rng.uniform(-1, 1, (len(coarse), 4))
+    Wt = rng.uniform(-1, 1, (8, 4, 3))
+    got_t = oracle.conv(coarse, fine, (2, 2, 2), 1, Fc, Wt, transposed=True)
+    gc = torch.zeros((1, 4, n // 2, n // 2, n // 2), dtype=torch.float64)
+    for r, (_, x, yy, z) in enumerate(coarse.tolist()):
+        gc[0, :, x // 2, yy // 2, z // 2] = torch.from_numpy(Fc[r])
+    wt = torch.from_numpy(Wt.reshape(2, 2, 2, 4, 3)).permute(3, 4, 0, 1, 2).contiguous()
+    yt = torch.nn.functional.conv_transpose3d(gc, wt, stride=2)
+    ref_t = np.stack([yt[0, :, x, yy, z].numpy() for _, x, yy, z in fine.tolist()])
+    np.testing.assert_allclose(got_t, ref_t, rtol=1e-12, atol=1e-12)
+    # non-cubic submanifold (3, 1, 1)
+    W3 = rng.uniform(-1, 1, (3, 3, 2))
+    got3 = oracle.conv(fine, fine, (3, 1, 1), 1, F, W3)
+    w3 = torch.from_numpy(W3.reshape(3, 1, 1, 3, 2)).permute(4, 3, 0, 1, 2).contiguous()
+    y3 = torch.nn.functional.conv3d(grid, w3, padding=(1, 0, 0))
+    ref3 = np.stack([y3[0, :, x, yy, z].numpy() for _, x, yy, z in fine.tolist()])
+    np.testing.assert_allclose(got3, ref3, rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("K,s", [(3, 2), (3, 1), ((3, 1, 1), 2), (5, 2)])
+def test_regular_outputs_is_conv_support(K, s):
+    """spconv's regular rule = the support of conv3d(occupancy, ones, stride s, padding
+    (K-1)/2): a site is an output iff its kernel footprint touches an input."""
+    rng = np.random.default_rng(4)
+    n = 12
+    occ = np.zeros((n, n, n), bool)
+    occ[2:10, 2:10, 2:10] = rng.random((8, 8, 8)) < 0.05
+    fine = np.array([[0, x, y, z] for x, y, z in zip(*np.nonzero(occ))], np.int32)
+    kx, ky, kz = K if isinstance(K, tuple) else (K, K, K)
+    got = oracle.regular_outputs(fine, K, 1, s)
+    ones = torch.ones((1, 1, kx, ky, kz), dtype=torch.float64)
+    sup = torch.nn.functional.conv3d(torch.from_numpy(occ.astype(np.float64))[None, None], ones, stride=s,
+                                     padding=((kx - 1) // 2, (ky - 1) // 2, (kz - 1) // 2))[0, 0].numpy() > 0
+    ref = sorted((0, int(x) * s, int(y) * s, int(z) * s) for x, y, z in zip(*np.nonzero(sup)))
+    assert [tuple(r) for r in got.tolist()] == ref
+
+
+def test_regular_outputs_k2_s2_equals_eq1_downsample():
+    """K = 2, s = 2 (offsets {0, 1}^3): every point has exactly one lattice site p - delta,
+    its Eq. (1) parent, so the regular rule and Eq. (1) give the same sites."""
+    c = oracle.sort_coords(synth.random_cloud(2000, 40, seed=8, n_batch=3))[0]
+    assert np.array_equal(oracle.regular_outputs(c, (2, 2, 2), 1, 2), oracle.downsample(c, 2))
