@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define SPC_VERSION 2
+#define SPC_VERSION 3
 
 typedef enum {
     SPC_OK = 0,
@@ -235,7 +235,7 @@ spc_status spc_downsample(const uint64_t *keys, int64_t n, const int64_t *n_dev,
  * A4-A8  Kernel maps (§2.2, z-delta search P:253-301 §5.2, layouts P:393-421)
  * ================================================================================ */
 typedef struct {
-    int32_t kernel_size;   /* K, odd                                            */
+    int32_t kernel_size;   /* K (x size of the offset box; odd K: Delta(K, s_p)) */
     int32_t stride;        /* layer stride s_l: 1 = submanifold (V_q = V_p), 2 = down/up */
     int32_t dilation;      /* d >= 1 (offsets delta * d; not in the paper, reading A11)  */
     int32_t tensor_stride; /* stride of the FINE coordinate set (s_p of a normal layer,  */
@@ -244,7 +244,29 @@ typedef struct {
     int32_t transposed;    /* 0: out = V_{ts*stride} (coarse) or V_ts (submanifold), in = V_ts */
                            /* 1: out = V_ts (fine), in = V_{ts*stride} (coarse); triple  */
                            /*    (k,i,j) iff in_j = out_i - delta_k  (reading A8)        */
+    /* a non-cubic box (Kx = kernel_size, Ky, Kz; 0 = kernel_size).  Every
+     * size is in 1..5; per axis the offsets are e*spacing with e in {-(K-1)/2 .. (K-1)/2}
+     * for odd K and e in {0 .. K-1} for even K (reading E1: the K = 2 down/up layers'
+     * {0, s_p}^3).  Weight offsets k are lexicographic (e_x, e_y, e_z), e_z fastest.
+     * SPC_KMAP_HALVE_SYMMETRIC applies to centred boxes (every size odd) only and is
+     * ignored otherwise; the map's reach is max |e| * spacing over the box. */
+    int32_t kernel_size_y;
+    int32_t kernel_size_z;
 } spc_geom;
+
+/* NEXT-3  spconv's "regular" output rule for a forward layer of box `geom` (odd sizes
+ * centred, i.e. spconv padding (K-1)/2; even sizes {0..K-1}): the sorted unique sites
+ *   V_out = { p - delta : p in V_in, delta in the box (spacing tensor_stride*dilation),
+ *             every spatial coordinate a multiple of tensor_stride*stride }
+ * -- every output site whose kernel footprint touches an input (for K = 2, stride 2 this
+ * is Eq. (1)'s V_q).  in_keys: sorted unique keys (n_in_dev nullable).  out_keys: room for
+ * n_in * Kx*Ky*Kz keys; n_out_dev: device int64 count.  The map between V_in and V_out is
+ * then an ordinary spc_build_kmap(in_keys, out_keys, ..., geom).  SPC_ERR_RANGE when the
+ * box reach or the output stride exceeds the spec's planned headroom. */
+size_t spc_regular_outputs_workspace_size(int64_t n_in, spc_geom geom);
+spc_status spc_regular_outputs(const uint64_t *in_keys, int64_t n_in, const int64_t *n_in_dev, spc_pack_spec spec,
+                               spc_geom geom, uint64_t *out_keys, int64_t *n_out_dev, void *ws, size_t ws_bytes,
+                               void *stream);
 
 /* dataflow threshold t: offset k is dense (output-stationary) iff
  * L1(e_k) < t, where e_k in {-r..r}^3 is the offset in units of tensor_stride*dilation

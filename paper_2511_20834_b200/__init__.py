@@ -62,17 +62,33 @@ class PackSpec(ctypes.Structure):
 
 
 class Geom(ctypes.Structure):
+    """spc_geom.  ``kernel_size``: odd int K (Delta(K, s_p)) or a (Kx, Ky, Kz) box,
+    even sizes {0..K-1} (reading E1)."""
     _fields_ = [("kernel_size", ctypes.c_int32), ("stride", ctypes.c_int32), ("dilation", ctypes.c_int32),
-                ("tensor_stride", ctypes.c_int32), ("transposed", ctypes.c_int32)]
+                ("tensor_stride", ctypes.c_int32), ("transposed", ctypes.c_int32),
+                ("kernel_size_y", ctypes.c_int32), ("kernel_size_z", ctypes.c_int32)]
 
     def __init__(self, kernel_size=3, stride=1, dilation=1, tensor_stride=1, transposed=0):
-        super().__init__(kernel_size, stride, dilation, tensor_stride, int(transposed))
+        if isinstance(kernel_size, (tuple, list)):
+            kx, ky, kz = (int(v) for v in kernel_size)
+        else:
+            kx = ky = kz = int(kernel_size)
+        super().__init__(kx, stride, dilation, tensor_stride, int(transposed), ky, kz)
+
+    def box(self):
+        return (self.kernel_size, self.kernel_size_y or self.kernel_size, self.kernel_size_z or self.kernel_size)
+
+    def k_vol(self):
+        kx, ky, kz = self.box()
+        return kx * ky * kz
 
     def key(self):
-        return (self.kernel_size, self.stride, self.dilation, self.tensor_stride, self.transposed)
+        return (self.kernel_size, self.stride, self.dilation, self.tensor_stride, self.transposed) + \
+            ((self.box(),) if len(set(self.box())) > 1 else ())
 
     def __repr__(self):
-        return "Geom(K=%d, s=%d, d=%d, ts=%d, tr=%d)" % self.key()
+        return "Geom(K=%s, s=%d, d=%d, ts=%d, tr=%d)" % ((self.box() if len(set(self.box())) > 1 else self.kernel_size,
+                                                          self.stride, self.dilation, self.tensor_stride, self.transposed))
 
 
 class _Kmap(ctypes.Structure):
@@ -117,6 +133,8 @@ def lib():
             "spc_pack_sort": ([P, I64, P, PackSpec, P, P, P, P, SZ, P], ctypes.c_int),
             "spc_pack_sort32": ([P, I64, P, PackSpec, P, P, P, P, SZ, P], ctypes.c_int),
             "spc_gather_rows": ([P, I64, P, I64, P, I32, P, I64, P], ctypes.c_int),
+            "spc_regular_outputs_workspace_size": ([I64, Geom], SZ),
+            "spc_regular_outputs": ([P, I64, P, PackSpec, Geom, P, P, P, SZ, P], ctypes.c_int),
             "spc_voxelize_workspace_size": ([I64], SZ),
             "spc_voxelize": ([P, I64, P, I64, P, P, PackSpec, P, I64, I32, P, P, P, P, I64, I32, P, P, P, SZ, P],
                              ctypes.c_int),
@@ -280,6 +298,26 @@ def spc_gather_rows(src: torch.Tensor, perm: torch.Tensor, out: torch.Tensor | N
                                  row_bytes, _ptr(out), out.stride(0) * out.element_size(), _stream(stream)),
            "spc_gather_rows")
     return out
+
+
+# ---------------------------------------------------------------------------------------
+# NEXT-3 spconv regular output sites
+# ---------------------------------------------------------------------------------------
+
+def spc_regular_outputs(keys: torch.Tensor, spec: PackSpec, geom: Geom, n_dev=None, stream=None):
+    """Sorted unique output keys of spconv's regular rule for a forward layer of ``geom``
+    (every stride-lattice site whose kernel box touches an input key).  Returns (out_keys
+    int64 [n * k_vol] -- the first n_out valid --, n_out int64 [1] on the device)."""
+    n = keys.shape[0]
+    dev = keys.device
+    out = _alloc(max(n * geom.k_vol(), 1), torch.int64, dev, stream)
+    n_out = _alloc(1, torch.int64, dev, stream)
+    L = lib()
+    ws = _ws(int(L.spc_regular_outputs_workspace_size(n, geom)), dev, stream=stream)
+    _check(L.spc_regular_outputs(_ptr(keys), n, _ptr(n_dev), spec, geom, _ptr(out), _ptr(n_out), _ptr(ws), ws.numel(),
+                                 _stream(stream)), "spc_regular_outputs")
+    _release(ws, stream)
+    return out, n_out
 
 
 # ---------------------------------------------------------------------------------------

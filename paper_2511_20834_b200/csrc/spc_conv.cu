@@ -1489,7 +1489,11 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
     p.split_ok = 0;
     if (!acc) return fail(SPC_ERR_WORKSPACE, "spc_conv_forward: ws too small");
     const int centre = (km->k_vol - 1) / 2;
-    if (!has_os && subm && km->k_vol > 1 && option(SPC_OPT_CONV_DENSE_CENTRE) != 0)
+    // (the zero offset sits at the centre of a centred box only: every size odd)
+    const spc_geom &gm = km->geom;
+    const bool centred = gm.kernel_size % 2 == 1 && (gm.kernel_size_y <= 0 || gm.kernel_size_y % 2 == 1) &&
+                         (gm.kernel_size_z <= 0 || gm.kernel_size_z % 2 == 1);
+    if (!has_os && subm && centred && km->k_vol > 1 && option(SPC_OPT_CONV_DENSE_CENTRE) != 0)
         for (int l = 0; l < km->n_lists; ++l)
             if (km->list_k[l] == centre) p.skip_list = l;
     if (has_os) {

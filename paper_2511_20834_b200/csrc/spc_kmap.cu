@@ -42,10 +42,13 @@ struct KmapDesc {
     int32_t *counts;
     uint32_t *tile_mask;
     unsigned long long *stats;
-    int32_t *bounds;          // [tiles][K^2][2] window bounds (k_kmap_bounds)
+    int32_t *bounds;          // [tiles][Kx*Ky][2] window bounds (k_kmap_bounds)
     int64_t list_stride;
     int32_t spacing;
-    int16_t K, k_dense, tile_words, t_eff;
+    int16_t k_dense, tile_words, t_eff;
+    // offset box: Kx x Ky groups of Kz members along z; per axis the
+    // offsets e = lo .. lo + K - 1 (odd K centred as in Delta(K, s_p); even K from 0)
+    int8_t kx, ky, kz, lox, loy, loz;
     int8_t transposed, halved;
     int8_t ord_idx;                 // density order: index among the ordered maps (-1: none)
     int8_t ord_cls[SPC_MAX_KVOL];   // density-order key bit of each dense column (-1: none)
@@ -118,9 +121,8 @@ __global__ void k_kmap_prep(const __grid_constant__ KmapBatch b) {
 
 // packed query delta of member mm (ascending query order) of offset group g
 __device__ __forceinline__ int64_t group_delta(const KmapDesc &p, int by, int bz, int g, int mm) {
-    const int K = p.K, r = (K - 1) / 2;
-    const int ex = g / K - r, ey = g % K - r;
-    const int ez = p.transposed ? r - mm : mm - r;
+    const int ex = g / p.ky + p.lox, ey = g % p.ky + p.loy;
+    const int ez = p.transposed ? p.loz + p.kz - 1 - mm : p.loz + mm;
     const int64_t d = (int64_t)ex * p.spacing * (1ll << (by + bz)) + (int64_t)ey * p.spacing * (1ll << bz) +
                       (int64_t)ez * p.spacing;
     return p.transposed ? -d : d;
@@ -140,7 +142,7 @@ __global__ void __launch_bounds__(256) k_kmap_bounds(const __grid_constant__ Kma
         for (int m = 0; m < B.n_maps; ++m) {
             s_pre[m] = acc;
             const int64_t n_out = dev_count(B.d[m].n_out_cap, B.d[m].n_out_dev);
-            acc += ((n_out + KM_BM - 1) / KM_BM) * 2 * B.d[m].K * B.d[m].K;
+            acc += ((n_out + KM_BM - 1) / KM_BM) * 2 * B.d[m].kx * B.d[m].ky;
         }
         s_pre[B.n_maps] = acc;
     }
@@ -150,7 +152,7 @@ __global__ void __launch_bounds__(256) k_kmap_bounds(const __grid_constant__ Kma
         int m = 0;
         while (s_pre[m + 1] <= v) ++m;
         const KmapDesc &p = B.d[m];
-        const int G2 = 2 * p.K * p.K;
+        const int G2 = 2 * p.kx * p.ky;
         const int64_t local = v - s_pre[m];
         const int64_t tile = local / G2;
         const int j = (int)(local - tile * G2), g = j >> 1, hi = j & 1;
@@ -161,7 +163,7 @@ __global__ void __launch_bounds__(256) k_kmap_bounds(const __grid_constant__ Kma
         const KeyT *in = static_cast<const KeyT *>(p.in), *out = static_cast<const KeyT *>(p.out);
         // packed(q) + packed(delta) in KeyT arithmetic: the planned headroom keeps the
         // true sum inside the key range, so the wrap-around addition is exact
-        const KeyT q = hi ? (KeyT)(out[row0 + rows - 1] + (KeyT)group_delta(p, B.bits_y, B.bits_z, g, p.K - 1) + (KeyT)1)
+        const KeyT q = hi ? (KeyT)(out[row0 + rows - 1] + (KeyT)group_delta(p, B.bits_y, B.bits_z, g, p.kz - 1) + (KeyT)1)
                           : (KeyT)(out[row0] + (KeyT)group_delta(p, B.bits_y, B.bits_z, g, 0));
         p.bounds[local] = (int32_t)lower_bound_g(in, n_in, q);
     }
@@ -250,6 +252,20 @@ __device__ __forceinline__ int zdelta_chunk(ZTile<KeyT> &zt, int32_t *s_os, int3
     return pos - pos0;   // cursor advances (search-count statistics)
 }
 
+// members per group (Kz) as a compile-time count
+template <typename KeyT, bool SM>
+__device__ __forceinline__ int zdelta_dispatch(int K, ZTile<KeyT> &zt, int32_t *s_os, int32_t *s_ws, int KD,
+                                               const KeyT *wk, int wl, int32_t lo, int g, int ch, int rows, int lane,
+                                               unsigned &n_calls) {
+    switch (K) {
+        case 3: return zdelta_chunk<KeyT, 3, SM>(zt, s_os, s_ws, KD, wk, wl, lo, g, ch, rows, lane, n_calls);
+        case 5: return zdelta_chunk<KeyT, 5, SM>(zt, s_os, s_ws, KD, wk, wl, lo, g, ch, rows, lane, n_calls);
+        case 2: return zdelta_chunk<KeyT, 2, SM>(zt, s_os, s_ws, KD, wk, wl, lo, g, ch, rows, lane, n_calls);
+        case 4: return zdelta_chunk<KeyT, 4, SM>(zt, s_os, s_ws, KD, wk, wl, lo, g, ch, rows, lane, n_calls);
+        default: return zdelta_chunk<KeyT, 1, SM>(zt, s_os, s_ws, KD, wk, wl, lo, g, ch, rows, lane, n_calls);
+    }
+}
+
 constexpr int KM_MIN_BLOCKS = 4;
 // one CTA per (map, tile of KM_BM outputs), grid-strided over every tile of every map of
 // the batch.  Per tile: (1) every warp stages its share of the K^2 group windows
@@ -307,7 +323,7 @@ __global__ void __launch_bounds__(KM_THREADS, KM_MIN_BLOCKS) k_kmap_zdelta(const
         const int64_t tn = vn - s_pre[mn];
         const int rn = (int)imin64(KM_BM, s_nout[mn] - tn * KM_BM);
         if (tid < rn) pf_q = static_cast<const KeyT *>(pn.out)[tn * KM_BM + tid];
-        const int Gn = pn.K * pn.K;
+        const int Gn = pn.kx * pn.ky;
         if (lane < Gn) {
             const int2 b2 = *reinterpret_cast<const int2 *>(pn.bounds + (tn * Gn + lane) * 2);
             pf_lo = b2.x;
@@ -325,7 +341,7 @@ __global__ void __launch_bounds__(KM_THREADS, KM_MIN_BLOCKS) k_kmap_zdelta(const
         const int64_t tile = v - s_pre[m];
         const int64_t row0 = tile * KM_BM;
         const int rows = (int)imin64(KM_BM, s_nout[m] - row0);
-        const int K = p.K, G = K * K, KD = p.k_dense;
+        const int K = p.kz, G = p.kx * p.ky, KD = p.k_dense;   // G groups of K members
         int32_t *s_os = s_tab;
         int32_t *s_ws = s_tab + KM_BM * KD;
         // ---- (1) tile state; group windows (every warp scans the <= 25 group sizes) ----
@@ -335,9 +351,8 @@ __global__ void __launch_bounds__(KM_THREADS, KM_MIN_BLOCKS) k_kmap_zdelta(const
         }
         for (int e = tid; e < G * K; e += KM_THREADS) {
             zt.cnt[e] = 0;
-            const int g = e / K, mm = e - g * K, r = (K - 1) / 2;
-            const int ez = p.transposed ? r - mm : mm - r;
-            const int k = ((g / K) * K + g % K) * K + (ez + r);
+            const int g = e / K, mm = e - g * K;
+            const int k = g * K + (p.transposed ? K - 1 - mm : mm);   // weight offset (dz fastest)
             zt.dq[e] = group_delta(p, B.bits_y, B.bits_z, g, mm);
             const int col = dcol[k], l = lstv[k];
             const int ob = (p.ord_idx >= 0 && col >= 0) ? p.ord_cls[col] : -1;
@@ -411,14 +426,10 @@ __global__ void __launch_bounds__(KM_THREADS, KM_MIN_BLOCKS) k_kmap_zdelta(const
             int adv;
             if (off >= 0) {
                 const KeyT *wk = s_pool + off;
-                if (K == 3) adv = zdelta_chunk<KeyT, 3, true>(zt, s_os, s_ws, KD, wk, wl, lo, g, ch, rows, lane, n_calls);
-                else if (K == 5) adv = zdelta_chunk<KeyT, 5, true>(zt, s_os, s_ws, KD, wk, wl, lo, g, ch, rows, lane, n_calls);
-                else adv = zdelta_chunk<KeyT, 1, true>(zt, s_os, s_ws, KD, wk, wl, lo, g, ch, rows, lane, n_calls);
+                adv = zdelta_dispatch<KeyT, true>(K, zt, s_os, s_ws, KD, wk, wl, lo, g, ch, rows, lane, n_calls);
             } else {
                 const KeyT *wk = static_cast<const KeyT *>(p.in) + lo;
-                if (K == 3) adv = zdelta_chunk<KeyT, 3, false>(zt, s_os, s_ws, KD, wk, wl, lo, g, ch, rows, lane, n_calls);
-                else if (K == 5) adv = zdelta_chunk<KeyT, 5, false>(zt, s_os, s_ws, KD, wk, wl, lo, g, ch, rows, lane, n_calls);
-                else adv = zdelta_chunk<KeyT, 1, false>(zt, s_os, s_ws, KD, wk, wl, lo, g, ch, rows, lane, n_calls);
+                adv = zdelta_dispatch<KeyT, false>(K, zt, s_os, s_ws, KD, wk, wl, lo, g, ch, rows, lane, n_calls);
             }
             n_probe += (unsigned long long)adv;
         }
@@ -494,13 +505,13 @@ __global__ void __launch_bounds__(256) k_kmap_bsearch(const __grid_constant__ Km
     const int64_t n_out = dev_count(p.n_out_cap, p.n_out_dev);
     const int64_t n_in = dev_count(p.n_in_cap, p.n_in_dev);
     const int64_t n_pad = (n_out + 31) & ~int64_t(31);
-    const int K = p.K, r = (K - 1) / 2, kv = K * K * K;
+    const int kv = p.kx * p.ky * p.kz;
     const int lane = threadIdx.x & 31;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < kv * n_pad; e += (int64_t)gridDim.x * blockDim.x) {
         const int k = (int)(e / n_pad);
         const int64_t i = e - k * n_pad;
         const int col = p.dcol[k];
-        const int ex = k / (K * K) - r, ey = (k / K) % K - r, ez = k % K - r;
+        const int ex = k / (p.ky * p.kz) + p.lox, ey = (k / p.kz) % p.ky + p.loy, ez = k % p.kz + p.loz;
         int64_t d = (int64_t)ex * p.spacing * (1ll << (bits_y + bits_z)) + (int64_t)ey * p.spacing * (1ll << bits_z) +
                     (int64_t)ez * p.spacing;
         if (p.transposed) d = -d;
@@ -741,7 +752,10 @@ static spc_status run_orders(const std::vector<OrderJob> &jobs, const OrderScrat
 // host: plan (offset tables, dense/sparse split, lists) and entry points
 // ------------------------------------------------------------------------------------
 struct KmapPlan {
-    int K = 0, r = 0, k_vol = 0, k_dense = 0, n_lists = 0, halved = 0, t_eff = 0, spacing = 1, centre_col = -1;
+    int kk[3] = {0, 0, 0}, lo[3] = {0, 0, 0};   // offset box: sizes and first offset per axis (units)
+    int reach_units = 0;                        // max |e| over the box (the map's reach / spacing)
+    bool symmetric = false;                     // every size odd: centred box, k <-> k_vol-1-k mirrors
+    int k_vol = 0, k_dense = 0, n_lists = 0, halved = 0, t_eff = 0, spacing = 1, centre_col = -1;
     int16_t dense_k[SPC_MAX_KVOL], list_k[SPC_MAX_KVOL];
     int8_t list_mirror[SPC_MAX_KVOL];
     int16_t dense_col[SPC_MAX_KVOL], list_id[SPC_MAX_KVOL];
@@ -750,26 +764,38 @@ struct KmapPlan {
 };
 
 static spc_status make_plan(const spc_geom &g, int32_t t, uint32_t flags, KmapPlan &pl) {
-    if (g.kernel_size < 1 || g.kernel_size % 2 == 0 || g.kernel_size > 5)
-        return fail(SPC_ERR_UNSUPPORTED, "kernel_size must be odd and <= 5 (P:111), got " +
-                                             std::to_string(g.kernel_size));
+    // offset box: Delta(K, s_p) for odd cubic K; per-axis sizes and even sizes
+    // ({0 .. K-1}, reading E1) are the generalisation of SURVEY NEXT-3
+    const int ks[3] = {g.kernel_size, g.kernel_size_y > 0 ? g.kernel_size_y : g.kernel_size,
+                       g.kernel_size_z > 0 ? g.kernel_size_z : g.kernel_size};
+    for (int a = 0; a < 3; ++a)
+        if (ks[a] < 1 || ks[a] > 5)
+            return fail(SPC_ERR_UNSUPPORTED, "kernel sizes must be in 1..5, got " + std::to_string(ks[a]));
     if (g.stride < 1 || g.dilation < 1 || g.tensor_stride < 1)
         return fail(SPC_ERR_INVALID_ARG, "stride, dilation and tensor_stride must be >= 1");
     if (g.transposed && g.stride == 1)
         return fail(SPC_ERR_INVALID_ARG, "a transposed map needs stride > 1");
-    pl.K = g.kernel_size;
-    pl.r = (pl.K - 1) / 2;
-    pl.k_vol = pl.K * pl.K * pl.K;
+    pl.symmetric = true;
+    pl.reach_units = 0;
+    for (int a = 0; a < 3; ++a) {
+        pl.kk[a] = ks[a];
+        pl.lo[a] = ks[a] % 2 ? -(ks[a] - 1) / 2 : 0;
+        pl.symmetric &= ks[a] % 2 == 1;
+        pl.reach_units = std::max(pl.reach_units, std::max(-pl.lo[a], pl.lo[a] + ks[a] - 1));
+    }
+    pl.k_vol = ks[0] * ks[1] * ks[2];
     pl.spacing = g.tensor_stride * g.dilation;
-    const int l1max = 3 * pl.r;
+    int l1max = 0;
+    for (int a = 0; a < 3; ++a) l1max += std::max(-pl.lo[a], pl.lo[a] + ks[a] - 1);
     pl.t_eff = (t < 0 || t > l1max + 1) ? l1max + 1 : t;
     const bool subm = g.stride == 1 && !g.transposed;
-    pl.halved = (flags & SPC_KMAP_HALVE_SYMMETRIC) && subm ? 1 : 0;
-    const int centre = (pl.k_vol - 1) / 2;
+    // halving needs the mirror pairs k <-> k_vol-1-k of a centred box
+    pl.halved = (flags & SPC_KMAP_HALVE_SYMMETRIC) && subm && pl.symmetric ? 1 : 0;
+    const int centre = pl.symmetric ? (pl.k_vol - 1) / 2 : -1;   // the zero offset, if the box has it
     pl.k_dense = pl.n_lists = 0;
     pl.centre_col = -1;
     for (int k = 0; k < pl.k_vol; ++k) {
-        int ex = k / (pl.K * pl.K) - pl.r, ey = (k / pl.K) % pl.K - pl.r, ez = k % pl.K - pl.r;
+        int ex = k / (ks[1] * ks[2]) + pl.lo[0], ey = (k / ks[2]) % ks[1] + pl.lo[1], ez = k % ks[2] + pl.lo[2];
         int l1 = abs(ex) + abs(ey) + abs(ez);
         pl.dense_col[k] = -1;
         pl.list_id[k] = -1;
@@ -801,10 +827,10 @@ static spc_status make_plan(const spc_geom &g, int32_t t, uint32_t flags, KmapPl
             pl.ord_cls[c] = (int8_t)(r < 0 ? -1 : r % 16);
         }
     }
-    for (int gi = 0; gi < pl.K * pl.K; ++gi) {
+    for (int gi = 0; gi < ks[0] * ks[1]; ++gi) {
         bool need = false;
-        for (int m = 0; m < pl.K; ++m) {
-            int k = gi * pl.K + m;
+        for (int m = 0; m < ks[2]; ++m) {
+            int k = gi * ks[2] + m;
             need |= pl.dense_col[k] >= 0 || pl.list_id[k] >= 0;
         }
         pl.group_needed[gi] = need;
@@ -834,7 +860,7 @@ static KmapLayout layout_of(const KmapPlan &pl, int64_t n_out, uint32_t flags, b
     L.counts = take(sizeof(int32_t) * 2 * SPC_MAX_KVOL);
     L.mask = take(sizeof(uint32_t) * (size_t)(L.tiles * L.words));
     L.stats = take(sizeof(unsigned long long) * 2 + 64);   // + a launch work counter
-    L.bounds = take(sizeof(int32_t) * (size_t)L.tiles * 2 * pl.K * pl.K);
+    L.bounds = take(sizeof(int32_t) * (size_t)L.tiles * 2 * pl.kk[0] * pl.kk[1]);
     if (wants_order(pl, flags)) {
         L.rows = take(sizeof(int32_t) * (size_t)n_out);
         L.os_ord = take(sizeof(int32_t) * (size_t)n_out * pl.k_dense);
@@ -878,7 +904,12 @@ static void fill_desc(KmapDesc &d, const spc_kmap &km, const KmapPlan &pl, int32
     d.stats = km.search_stats_dev;
     d.list_stride = km.n_out;
     d.spacing = pl.spacing;
-    d.K = (int16_t)pl.K;
+    d.kx = (int8_t)pl.kk[0];
+    d.ky = (int8_t)pl.kk[1];
+    d.kz = (int8_t)pl.kk[2];
+    d.lox = (int8_t)pl.lo[0];
+    d.loy = (int8_t)pl.lo[1];
+    d.loz = (int8_t)pl.lo[2];
     d.k_dense = (int16_t)pl.k_dense;
     d.tile_words = (int16_t)km.tile_words;
     d.t_eff = (int16_t)pl.t_eff;
@@ -899,7 +930,7 @@ static spc_status launch_kmaps(const KmapBatch &b0, int max_k_dense, int64_t max
     SPC_LAUNCH_CHECK("k_kmap_prep");
     {
         int64_t items = 0;
-        for (int m = 0; m < b.n_maps; ++m) items += ((b.d[m].n_out_cap + KM_BM - 1) / KM_BM) * 2 * b.d[m].K * b.d[m].K;
+        for (int m = 0; m < b.n_maps; ++m) items += ((b.d[m].n_out_cap + KM_BM - 1) / KM_BM) * 2 * b.d[m].kx * b.d[m].ky;
         const int g = (int)std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, 16 * (int64_t)num_sms()));
         if (b.key_bytes == 4) SPC_CUDA(launch_pdl(k_kmap_bounds<uint32_t>, dim3(g), dim3(256), 0, st, b));
         else SPC_CUDA(launch_pdl(k_kmap_bounds<uint64_t>, dim3(g), dim3(256), 0, st, b));
@@ -967,7 +998,7 @@ static spc_status build_kmap(const void *in_keys, int64_t n_in, const int64_t *n
     // reach check (reading A4): spc_pack_sort guarantees every key leaves `spec.reach`
     // (and out_stride - 1 below) of headroom in each field; a map reaching further could
     // carry or borrow into a neighbouring field, so it is refused, never truncated
-    const int64_t reach = (int64_t)pl.r * pl.spacing;
+    const int64_t reach = (int64_t)pl.reach_units * pl.spacing;
     if (reach > spec.reach)
         return fail(SPC_ERR_RANGE, "spc_build_kmap: kernel reach r*tensor_stride*dilation = " + std::to_string(reach) +
                                        " exceeds the planned spec.reach = " + std::to_string(spec.reach));
@@ -1186,12 +1217,21 @@ extern "C" spc_status spc_shard_ranges(const uint64_t *in_keys, int64_t n_in, co
     KmapPlan pl;
     spc_status s = make_plan(geom, SPC_T_ALL_OS, 0, pl);
     if (s != SPC_OK) return s;
-    // packed query offsets of the map: +-delta per axis, delta = e * spacing, e in [-r, r];
-    // the set is symmetric, so a transposed map (negated queries) has the same extremes
-    const int64_t ext = (int64_t)pl.r * pl.spacing;
-    const int64_t d_max = ext * (1ll << (spec.bits_y + spec.bits_z)) + ext * (1ll << spec.bits_z) + ext;
+    // extreme packed query offsets of the map: q + delta per axis with delta = e * spacing,
+    // e in [lo, lo + K - 1] (a transposed map queries q - delta: negated and swapped)
+    const int64_t w[3] = {1ll << (spec.bits_y + spec.bits_z), 1ll << spec.bits_z, 1};
+    int64_t d_lo = 0, d_hi = 0;
+    for (int a = 0; a < 3; ++a) {
+        d_lo += (int64_t)pl.lo[a] * pl.spacing * w[a];
+        d_hi += (int64_t)(pl.lo[a] + pl.kk[a] - 1) * pl.spacing * w[a];
+    }
+    if (geom.transposed) {
+        const int64_t t0 = d_lo;
+        d_lo = -d_hi;
+        d_hi = -t0;
+    }
     SPC_CUDA(launch_pdl(k_shard_ranges, dim3((n_shards + 127) / 128), dim3(128), 0, as_stream(stream), in_keys, n_in,
-                        n_in_dev, out_keys, n_out, n_out_dev, -d_max, d_max, (int)n_shards, bounds_dev));
+                        n_in_dev, out_keys, n_out, n_out_dev, d_lo, d_hi, (int)n_shards, bounds_dev));
     SPC_LAUNCH_CHECK("k_shard_ranges");
     return SPC_OK;
 }

@@ -661,6 +661,45 @@ __global__ void k_voxel_init(int64_t *bad_point, int64_t *n_vox, int64_t n_cap) 
     if (n_vox && n_cap == 0) *n_vox = 0;
 }
 
+// ------------------------------------------------------------------------------------
+// NEXT-3 spconv "regular" output sites: candidates p - delta on the coarse lattice (packed
+// arithmetic; lattice test = the Eq. (1) mask leaves the key unchanged),
+// compacted with one warp reservation, then the stable radix sort + unique
+// ------------------------------------------------------------------------------------
+struct BoxDeltas {
+    int64_t d[SPC_MAX_KVOL];   // packed delta_k
+};
+
+__global__ void __launch_bounds__(256) k_regular_candidates(const uint64_t *__restrict__ in, int64_t n_cap,
+                                                            const int64_t *n_dev, int kv, BoxDeltas bd,
+                                                            uint64_t off_lattice, uint64_t *__restrict__ cand,
+                                                            unsigned long long *count) {
+    pdl_wait();   // PDL launch: the predecessor has completed and flushed
+    pdl_trigger();
+    const int64_t n = dev_count(n_cap, n_dev);
+    const int lane = threadIdx.x & 31;
+    const int64_t total = n * kv;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    // whole warps iterate together (ballot reservation)
+    for (int64_t e0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~int64_t(31); e0 < total;
+         e0 += stride) {
+        const int64_t e = e0 + lane;
+        bool keep = false;
+        uint64_t c = 0;
+        if (e < total) {
+            const int64_t i = e / kv;
+            const int k = (int)(e - i * kv);
+            c = in[i] - (uint64_t)bd.d[k];   // packed(p) - packed(delta) = packed(p - delta)
+            keep = (c & off_lattice) == 0;   // every spatial field a multiple of the out stride
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        unsigned long long base = 0;
+        if (lane == 0 && bal) base = atomicAdd(count, (unsigned long long)__popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (keep) cand[base + __popc(bal & lanemask_lt())] = c;
+    }
+}
+
 }  // namespace spc
 
 using namespace spc;
@@ -883,5 +922,92 @@ extern "C" spc_status spc_voxelize(const float *points, int64_t ld, const int32_
     SPC_CUDA(launch_pdl(k_voxel_mean, dim3(mgrid), dim3(256), 0, st, feats, ld_feats, (int)c, perm, seg, n_vox_dev, scal,
                         feats_out, ld_out, (int)out_dtype, bad_point_dev));
     SPC_LAUNCH_CHECK("k_voxel_mean");
+    return SPC_OK;
+}
+
+// ------------------------------------------------------------------------------------
+// NEXT-3 regular output sites (spc.h)
+// ------------------------------------------------------------------------------------
+static int64_t geom_kvol(const spc_geom &g) {
+    const int ky = g.kernel_size_y > 0 ? g.kernel_size_y : g.kernel_size;
+    const int kz = g.kernel_size_z > 0 ? g.kernel_size_z : g.kernel_size;
+    return (int64_t)g.kernel_size * ky * kz;
+}
+
+extern "C" size_t spc_regular_outputs_workspace_size(int64_t n_in, spc_geom geom) {
+    if (n_in < 0) n_in = 0;
+    const int64_t cap = n_in * std::max<int64_t>(1, geom_kvol(geom));
+    Sizer z;
+    z.take<uint64_t>((size_t)cap);
+    z.take<uint64_t>((size_t)cap);
+    z.take<int64_t>(4);
+    z.take<int>((size_t)(cap / SORT_TILE + 2));
+    return z.used + radix_sort_workspace(cap, false) + 512;
+}
+
+extern "C" spc_status spc_regular_outputs(const uint64_t *in_keys, int64_t n_in, const int64_t *n_in_dev,
+                                          spc_pack_spec spec, spc_geom geom, uint64_t *out_keys, int64_t *n_out_dev,
+                                          void *ws, size_t ws_bytes, void *stream) {
+    SPC_CHECK_ARG(n_in >= 0 && n_out_dev && (n_in == 0 || (in_keys && out_keys)), "null pointer or n_in < 0");
+    const int ks[3] = {geom.kernel_size, geom.kernel_size_y > 0 ? geom.kernel_size_y : geom.kernel_size,
+                       geom.kernel_size_z > 0 ? geom.kernel_size_z : geom.kernel_size};
+    for (int a = 0; a < 3; ++a)
+        SPC_CHECK_ARG(ks[a] >= 1 && ks[a] <= 5, "kernel sizes must be in 1..5");
+    SPC_CHECK_ARG(!geom.transposed && geom.stride >= 1 && geom.dilation >= 1 && geom.tensor_stride >= 1,
+                  "a forward (non-transposed) geometry with stride, dilation, tensor_stride >= 1");
+    const int64_t out_stride = (int64_t)geom.tensor_stride * geom.stride;
+    SPC_CHECK_ARG((out_stride & (out_stride - 1)) == 0, "tensor_stride * stride must be a power of two");
+    const int64_t spacing = (int64_t)geom.tensor_stride * geom.dilation;
+    int lo[3], reach_units = 0;
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = ks[a] % 2 ? -(ks[a] - 1) / 2 : 0;
+        reach_units = std::max(reach_units, std::max(-lo[a], lo[a] + ks[a] - 1));
+    }
+    if (reach_units * spacing > spec.reach)
+        return fail(SPC_ERR_RANGE, "spc_regular_outputs: kernel reach " + std::to_string(reach_units * spacing) +
+                                       " exceeds the planned spec.reach = " + std::to_string(spec.reach));
+    if (out_stride > spec.out_stride)
+        return fail(SPC_ERR_RANGE, "spc_regular_outputs: output stride exceeds the planned spec.out_stride");
+    const int kv = ks[0] * ks[1] * ks[2];
+    if (ws_bytes < spc_regular_outputs_workspace_size(n_in, geom))
+        return fail(SPC_ERR_WORKSPACE, "spc_regular_outputs: ws too small");
+    cudaStream_t st = as_stream(stream);
+    if (n_in == 0) {
+        SPC_CUDA(cudaMemsetAsync(n_out_dev, 0, sizeof(int64_t), st));
+        return SPC_OK;
+    }
+    BoxDeltas bd{};
+    int k = 0;
+    for (int ex = lo[0]; ex < lo[0] + ks[0]; ++ex)
+        for (int ey = lo[1]; ey < lo[1] + ks[1]; ++ey)
+            for (int ez = lo[2]; ez < lo[2] + ks[2]; ++ez)
+                bd.d[k++] = spc_pack_offset(spec, (int32_t)(ex * spacing), (int32_t)(ey * spacing), (int32_t)(ez * spacing));
+    int m = 0;
+    while ((1ll << m) < out_stride) ++m;
+    const int used = spec.bits_b + spec.bits_x + spec.bits_y + spec.bits_z;
+    const uint64_t spatial = ((1ull << (spec.bits_x + spec.bits_y + spec.bits_z)) - 1);
+    const uint64_t off_lattice = spatial & ~spc_downsample_mask(spec, m);   // low m bits of each spatial field
+    const int64_t cap = n_in * kv;
+    Bump b(ws, ws_bytes);
+    uint64_t *cand = b.take<uint64_t>((size_t)cap);
+    uint64_t *sorted = b.take<uint64_t>((size_t)cap);
+    int64_t *scal = b.take<int64_t>(4);   // [0] candidate count, [1..2] unique prefix
+    const int nt = (int)((cap + SORT_TILE - 1) / SORT_TILE);
+    int *tile_cnt = b.take<int>((size_t)(cap / SORT_TILE + 2));
+    void *rws = b.base + align_up(b.used, 256);
+    const size_t rws_bytes = ws_bytes - align_up(b.used, 256);
+    SPC_CUDA(cudaMemsetAsync(scal, 0, sizeof(int64_t), st));
+    const int grid = (int)imin64((cap + 255) / 256, 8 * 148);
+    SPC_CUDA(launch_pdl(k_regular_candidates, dim3(grid), dim3(256), 0, st, in_keys, n_in, n_in_dev, kv, bd, off_lattice,
+                        cand, reinterpret_cast<unsigned long long *>(scal)));
+    SPC_LAUNCH_CHECK("k_regular_candidates");
+    spc_status s = radix_sort(cand, nullptr, cap, scal, used, sorted, nullptr, rws, rws_bytes, st, false);
+    if (s != SPC_OK) return s;
+    SPC_CUDA(launch_pdl(k_unique_count, dim3(nt), dim3(SORT_THREADS), 0, st, sorted, scal, tile_cnt));
+    SPC_CUDA(launch_pdl(k_unique_scan, dim3(1), dim3(1024), 0, st, tile_cnt, nt, sorted, scal, cap, scal, 1, scal + 1,
+                        n_out_dev));
+    SPC_CUDA(launch_pdl(k_unique_write, dim3(nt), dim3(SORT_THREADS), 0, st, sorted, scal, cap, scal, tile_cnt, scal + 1,
+                        ~0ull, out_keys, cap));
+    SPC_LAUNCH_CHECK("regular outputs unique");
     return SPC_OK;
 }

@@ -62,7 +62,11 @@ def test_plan_pack_and_helpers(L):
 def test_kmap_bytes_and_errors(L):
     g = spc.Geom(3, 1, 1, 1, 0)
     assert spc.spc_kmap_bytes(g, -1, 0, 1000, 1000) >= 1000 * 27 * 4
-    assert spc.spc_kmap_bytes(spc.Geom(2, 1, 1, 1, 0), -1, 0, 10, 10) == 0     # even K unsupported
+    # NEXT-3 boxes: K = 2 ({0, 1}^3) and (3, 1, 1) are planned; sizes outside 1..5 are not
+    assert spc.spc_kmap_bytes(spc.Geom(2, 2, 1, 1, 0), -1, 0, 10, 10) >= 10 * 8 * 4
+    assert spc.spc_kmap_bytes(spc.Geom((3, 1, 1), 1, 1, 1, 0), -1, 0, 10, 10) >= 10 * 3 * 4
+    assert spc.spc_kmap_bytes(spc.Geom(6, 1, 1, 1, 0), -1, 0, 10, 10) == 0
+    assert spc.spc_kmap_bytes(spc.Geom((3, 0, 7), 1, 1, 1, 0), -1, 0, 10, 10) == 0
 
 
 def test_plan_records_headroom(L):

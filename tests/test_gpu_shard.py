@@ -22,7 +22,10 @@ def _keys(c, spec):
 
 @pytest.mark.parametrize("R", [2, 3, 4])
 @pytest.mark.parametrize("kind,K,t,flags", [("subm", 3, -1, 8), ("subm", 3, 2, 1), ("subm", 5, 3, 9),
-                                            ("strided", 3, -1, 0), ("transposed", 3, 0, 0), ("subm_d2", 3, -1, 0)])
+                                            ("strided", 3, -1, 0), ("transposed", 3, 0, 0), ("subm_d2", 3, -1, 0),
+                                            # NEXT-3 boxes: the halo extremes of non-centred offsets
+                                            ("strided", (2, 2, 2), -1, 0), ("transposed", (2, 2, 2), -1, 0),
+                                            ("subm", (4, 2, 3), 2, 0), ("subm", (3, 1, 1), -1, 9)])
 def test_range_sharded_map_and_conv(R, kind, K, t, flags):
     coords = synth.make_scan(1, 1)
     spec = spc.spc_plan_pack(coords[:, 1:].min(0), coords[:, 1:].max(0), 1, 16, 16)
@@ -44,7 +47,7 @@ def test_range_sharded_map_and_conv(R, kind, K, t, flags):
     np.testing.assert_array_equal(full, ref)
     c_in, c_out = 32, 48
     F = synth.make_features(len(ic), c_in, seed=9)
-    W = synth.make_weights(K ** 3, c_in, c_out, seed=10, nnz_per_out=10)
+    W = synth.make_weights(g.k_vol(), c_in, c_out, seed=10, nnz_per_out=10)
     Fg = torch.from_numpy(F).to(DEV).bfloat16()
     Wg = spc.spc_prepare_weight(torch.from_numpy(W).to(DEV).bfloat16())
     parts, outs = [], []
