@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--save-t", default=None, help="write the tuned per-map dataflow t to this JSON file")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-order", action="store_true", help="kernel maps without the OS density order (ablation)")
+    ap.add_argument("--net", default=None, choices=["minkunet42_k2"],
+                    help="C2/C4 variant: TorchSparse's MinkUNet layer set with K=2 stride-2 down/up (SURVEY NEXT-3)")
     ap.add_argument("--profile-layers", action="store_true", help="print the per-layer table to stderr")
     return ap.parse_args()
 
@@ -504,6 +506,9 @@ def main():
     spc.lib()
 
     coords_np, feats_np, scans_here, net_name = workload(rank, args.config, world)
+    if args.net:
+        assert net_name == "minkunet42", "--net minkunet42_k2 applies to the MinkUNet configs (2, 4)"
+        net_name = args.net
     n = coords_np.shape[0]
     spec = spec_for(coords_np) if args.config != 4 else spc.spc_plan_pack(
         coords_np[:, 1:].min(0), coords_np[:, 1:].max(0), 8, 16, 16)
@@ -644,13 +649,13 @@ def main():
 
     if rank == 0:
         line = {
-            "metric": METRIC if net_name == "minkunet42" else "SECOND-K5 backbone scans/sec", "value": value,
+            "metric": METRIC if net_name.startswith("minkunet42") else "SECOND-K5 backbone scans/sec", "value": value,
             "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_total / args.steps * 1e3, "higher_is_better": True,
             "scaling": "strong" if args.config == 4 else "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic",
             "config": {"workload": WORKLOADS[args.config],
-                       "model": "MinkUNet-42" if net_name == "minkunet42" else "SECOND/CenterPoint-K5 backbone",
+                       "model": {"minkunet42": "MinkUNet-42", "minkunet42_k2": "MinkUNet-42, K=2 stride-2 down/up (TorchSparse layer set)"}.get(net_name, "SECOND/CenterPoint-K5 backbone"),
                        "global_batch": total_scans, "n_voxels": n, "nccl_gather_ms": gather_ms,
                        "parallelism": f"scan-sharded x{world}", "l2": "flushed (320 MB write) between timed steps",
                        "cuda_graph": graph is not None, "dataflow_t": {str(k): v for k, v in net.t.items()},
@@ -759,7 +764,8 @@ def tune(net, coords, feats, stream):
         K, stride, ts, tr = mk
         if K == 1:
             continue
-        cands = list(range(0, 3 * (K - 1) // 2 + 2))     # 0 (all WS) .. L1max+1 (all OS)
+        l1max = 3 * ((K - 1) // 2 if K % 2 else K - 1)    # odd K centred; even K: offsets {0..K-1}
+        cands = list(range(0, l1max + 2))                  # 0 (all WS) .. L1max+1 (all OS)
         times = {}
         for t in cands:
             net.set_t({mk: t})

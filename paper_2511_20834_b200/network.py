@@ -9,7 +9,8 @@ BN/ReLU are identity (out of scope); weights are seeded random bf16.
 Channel-concatenation skips are free: encoder outputs are written straight into a
 column slice of the decoder's concat buffer (ld_out > c_out).
 
-Layer list (public MinkowskiEngine/TorchSparse MinkUNet with K=3 down/up):
+Layer list (SURVEY §8(d), public MinkowskiEngine/TorchSparse MinkUNet with K=3 down/up;
+``net="minkunet42_k2"``: TorchSparse's K=2 stride-2 down/up):
 cs = [32, 32, 64, 128, 256, 256, 128, 96, 96]; stem 2 x SubM K3; 4 encoder stages
 (Down K3 s2 + 2 ResBlocks); 4 decoder stages (Up K3 s2 transposed + concat + 2
 ResBlocks) = 42 layers with K = 3 plus 7 1x1 projections.
@@ -44,7 +45,9 @@ class ConvSpec:
     c_in_flops: int = 0     # channels counted for algorithmic FLOPs (stem: 4 real channels)
 
 
-def minkunet42_layers():
+def minkunet42_layers(down_k: int = 3):
+    """down_k = 3: the paper's odd-K reading (A10); down_k = 2: TorchSparse's MinkUNet
+    down / up layers (K = 2, stride 2, offsets {0, s_p}^3)."""
     L = []
     lvl_buf = {}
 
@@ -78,7 +81,7 @@ def minkunet42_layers():
     # encoder
     for i in range(1, 5):
         l = i
-        conv(f"enc{i}.down", (3, 2, 2 ** (l - 1), 0), ch, ch, src, sc, f"d{l}", 0, l)
+        conv(f"enc{i}.down", (down_k, 2, 2 ** (l - 1), 0), ch, ch, src, sc, f"d{l}", 0, l)
         dst, dc = (f"cat{l}", up_c[l]) if l < 4 else ("e4", 0)
         resblock(f"enc{i}.rb1", l, f"d{l}", 0, ch, CS[i], f"y{l}", 0)
         resblock(f"enc{i}.rb2", l, f"y{l}", 0, CS[i], CS[i], dst, dc)
@@ -87,7 +90,7 @@ def minkunet42_layers():
     for j in range(1, 5):
         l = 4 - j
         co = CS[4 + j]
-        conv(f"dec{j}.up", (3, 2, 2 ** l, 1), ch, co, src, sc, f"cat{l}", 0, l)
+        conv(f"dec{j}.up", (down_k, 2, 2 ** l, 1), ch, co, src, sc, f"cat{l}", 0, l)
         resblock(f"dec{j}.rb1", l, f"cat{l}", 0, cat_w[l], co, f"y{l}", 0)
         dst = "out" if l == 0 else f"z{l}"
         resblock(f"dec{j}.rb2", l, f"y{l}", 0, co, co, dst, 0)
@@ -151,8 +154,8 @@ class SparseNet:
         self.early_maps = True   # layers >= 1 start their tile decode during the previous layer
         self.spec = spec
         self.n0 = int(n0_cap)
-        if net == "minkunet42":
-            self.layers, widths = minkunet42_layers()
+        if net in ("minkunet42", "minkunet42_k2"):
+            self.layers, widths = minkunet42_layers(2 if net.endswith("_k2") else 3)
             self.out_name, self.n_levels = "out", 5
         elif net.startswith("second"):
             K = 5 if net.endswith("k5") else 3

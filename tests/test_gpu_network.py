@@ -82,6 +82,18 @@ def test_minkunet42_forward_and_layer_local_parity():
         assert _layer_local(net, lv, names.index(name)) <= 0, name
 
 
+def test_minkunet42_k2_forward_and_layer_local_parity():
+    """TorchSparse's MinkUNet layer set: every K = 2 stride-2 down layer
+    (offsets {0, s_p}^3) and K = 2 transposed up layer, plus neighbours."""
+    net, coords, out = _net(1, "minkunet42_k2")
+    assert torch.isfinite(out[: coords.shape[0]].float()).all()
+    lv = _levels(coords, 5)
+    names = [s.name for s in net.layers]
+    for name in [f"enc{i}.down" for i in range(1, 5)] + [f"dec{j}.up" for j in range(1, 5)] + \
+            ["enc1.rb1.conv1", "dec4.rb2.conv2"]:
+        assert _layer_local(net, lv, names.index(name)) <= 0, name
+
+
 def test_second_k5_backbone_forward_and_layer_local_parity():
     net, coords, out = _net(1, "secondk5")
     assert torch.isfinite(out[:1000].float()).all()
