@@ -215,9 +215,14 @@ __device__ __forceinline__ int lb_win(const KeyT *a, int n, KeyT q, unsigned &n_
 // K-1 members -- in the group's window of input keys.  Every stored entry is
 // written to the tile's shared tables (-1 = no match): OS columns [row][K_dense], WS lists
 // [list][row]; counts, mask bits and density-order bits go to shared accumulators.
-template <typename KeyT, int K, bool SM>
+// KT > 0: compile-time member count (unrolled: K = 1, 3, 5); KT = 0: runtime count k_rt
+// (the even / non-cubic boxes of NEXT-3, kept out of line so the hot instantiations keep
+// the kernel body small -- the build is instruction-issue bound)
+template <typename KeyT, int KT, bool SM>
 __device__ __forceinline__ int zdelta_chunk(ZTile<KeyT> &zt, int32_t *s_os, int32_t *s_ws, int KD, const KeyT *wk,
-                                            int wl, int32_t lo, int g, int ch, int rows, int lane, unsigned &n_calls) {
+                                            int wl, int32_t lo, int g, int ch, int rows, int lane, unsigned &n_calls,
+                                            int k_rt = KT) {
+    const int K = KT > 0 ? KT : k_rt;
     const int lr = ch * 32 + lane;
     const bool valid = lr < rows;
     const KeyT q = valid ? zt.q[lr] : (KeyT)0;
@@ -225,7 +230,7 @@ __device__ __forceinline__ int zdelta_chunk(ZTile<KeyT> &zt, int32_t *s_os, int3
     if (valid) pos = lb_win<KeyT, SM>(wk, wl, (KeyT)(q + (KeyT)zt.dq[g * K]), n_calls);
     const int pos0 = pos;
     uint32_t key = 0;
-#pragma unroll
+#pragma unroll (KT > 0 ? KT : 1)
     for (int mm = 0; mm < K; ++mm) {   // members in ascending query order
         const KeyT query = (KeyT)(q + (KeyT)zt.dq[g * K + mm]);
         const int32_t dsc = zt.dsc[g * K + mm];
@@ -252,18 +257,22 @@ __device__ __forceinline__ int zdelta_chunk(ZTile<KeyT> &zt, int32_t *s_os, int3
     return pos - pos0;   // cursor advances (search-count statistics)
 }
 
+template <typename KeyT, bool SM>
+__device__ __noinline__ int zdelta_chunk_rt(ZTile<KeyT> &zt, int32_t *s_os, int32_t *s_ws, int KD, const KeyT *wk,
+                                            int wl, int32_t lo, int g, int ch, int rows, int lane, unsigned &n_calls,
+                                            int K) {
+    return zdelta_chunk<KeyT, 0, SM>(zt, s_os, s_ws, KD, wk, wl, lo, g, ch, rows, lane, n_calls, K);
+}
+
 // members per group (Kz) as a compile-time count
 template <typename KeyT, bool SM>
 __device__ __forceinline__ int zdelta_dispatch(int K, ZTile<KeyT> &zt, int32_t *s_os, int32_t *s_ws, int KD,
                                                const KeyT *wk, int wl, int32_t lo, int g, int ch, int rows, int lane,
                                                unsigned &n_calls) {
-    switch (K) {
-        case 3: return zdelta_chunk<KeyT, 3, SM>(zt, s_os, s_ws, KD, wk, wl, lo, g, ch, rows, lane, n_calls);
-        case 5: return zdelta_chunk<KeyT, 5, SM>(zt, s_os, s_ws, KD, wk, wl, lo, g, ch, rows, lane, n_calls);
-        case 2: return zdelta_chunk<KeyT, 2, SM>(zt, s_os, s_ws, KD, wk, wl, lo, g, ch, rows, lane, n_calls);
-        case 4: return zdelta_chunk<KeyT, 4, SM>(zt, s_os, s_ws, KD, wk, wl, lo, g, ch, rows, lane, n_calls);
-        default: return zdelta_chunk<KeyT, 1, SM>(zt, s_os, s_ws, KD, wk, wl, lo, g, ch, rows, lane, n_calls);
-    }
+    if (K == 3) return zdelta_chunk<KeyT, 3, SM>(zt, s_os, s_ws, KD, wk, wl, lo, g, ch, rows, lane, n_calls);
+    if (K == 5) return zdelta_chunk<KeyT, 5, SM>(zt, s_os, s_ws, KD, wk, wl, lo, g, ch, rows, lane, n_calls);
+    if (K == 1) return zdelta_chunk<KeyT, 1, SM>(zt, s_os, s_ws, KD, wk, wl, lo, g, ch, rows, lane, n_calls);
+    return zdelta_chunk_rt<KeyT, SM>(zt, s_os, s_ws, KD, wk, wl, lo, g, ch, rows, lane, n_calls, K);
 }
 
 constexpr int KM_MIN_BLOCKS = 4;
