@@ -257,11 +257,13 @@ __device__ __forceinline__ int zdelta_chunk(ZTile<KeyT> &zt, int32_t *s_os, int3
     return pos - pos0;   // cursor advances (search-count statistics)
 }
 
+// (its own call counter: a reference into an out-of-line call would put the caller's
+// counter in local memory on every path)
 template <typename KeyT, bool SM>
 __device__ __noinline__ int zdelta_chunk_rt(ZTile<KeyT> &zt, int32_t *s_os, int32_t *s_ws, int KD, const KeyT *wk,
-                                            int wl, int32_t lo, int g, int ch, int rows, int lane, unsigned &n_calls,
-                                            int K) {
-    return zdelta_chunk<KeyT, 0, SM>(zt, s_os, s_ws, KD, wk, wl, lo, g, ch, rows, lane, n_calls, K);
+                                            int wl, int32_t lo, int g, int ch, int rows, int lane, int K) {
+    unsigned calls = 0;
+    return zdelta_chunk<KeyT, 0, SM>(zt, s_os, s_ws, KD, wk, wl, lo, g, ch, rows, lane, calls, K);
 }
 
 // members per group (Kz) as a compile-time count
@@ -272,7 +274,8 @@ __device__ __forceinline__ int zdelta_dispatch(int K, ZTile<KeyT> &zt, int32_t *
     if (K == 3) return zdelta_chunk<KeyT, 3, SM>(zt, s_os, s_ws, KD, wk, wl, lo, g, ch, rows, lane, n_calls);
     if (K == 5) return zdelta_chunk<KeyT, 5, SM>(zt, s_os, s_ws, KD, wk, wl, lo, g, ch, rows, lane, n_calls);
     if (K == 1) return zdelta_chunk<KeyT, 1, SM>(zt, s_os, s_ws, KD, wk, wl, lo, g, ch, rows, lane, n_calls);
-    return zdelta_chunk_rt<KeyT, SM>(zt, s_os, s_ws, KD, wk, wl, lo, g, ch, rows, lane, n_calls, K);
+    n_calls += ch * 32 + lane < rows ? 1u : 0u;   // the one anchor search per valid output
+    return zdelta_chunk_rt<KeyT, SM>(zt, s_os, s_ws, KD, wk, wl, lo, g, ch, rows, lane, K);
 }
 
 constexpr int KM_MIN_BLOCKS = 4;
