@@ -48,7 +48,8 @@ struct KmapDesc {
     int16_t k_dense, tile_words, t_eff;
     // offset box: Kx x Ky groups of Kz members along z; per axis the
     // offsets e = lo .. lo + K - 1 (odd K centred as in Delta(K, s_p); even K from 0)
-    int8_t kx, ky, kz, lox, loy, loz;
+    // (int32: byte-wide fields cost 7% of the build -- sign-extending dynamic param loads)
+    int32_t kx, ky, kz, lox, loy, loz;
     int8_t transposed, halved;
     int8_t ord_idx;                 // density order: index among the ordered maps (-1: none)
     int8_t ord_cls[SPC_MAX_KVOL];   // density-order key bit of each dense column (-1: none)
@@ -916,12 +917,12 @@ static void fill_desc(KmapDesc &d, const spc_kmap &km, const KmapPlan &pl, int32
     d.stats = km.search_stats_dev;
     d.list_stride = km.n_out;
     d.spacing = pl.spacing;
-    d.kx = (int8_t)pl.kk[0];
-    d.ky = (int8_t)pl.kk[1];
-    d.kz = (int8_t)pl.kk[2];
-    d.lox = (int8_t)pl.lo[0];
-    d.loy = (int8_t)pl.lo[1];
-    d.loz = (int8_t)pl.lo[2];
+    d.kx = (int32_t)pl.kk[0];
+    d.ky = (int32_t)pl.kk[1];
+    d.kz = (int32_t)pl.kk[2];
+    d.lox = (int32_t)pl.lo[0];
+    d.loy = (int32_t)pl.lo[1];
+    d.loz = (int32_t)pl.lo[2];
     d.k_dense = (int16_t)pl.k_dense;
     d.tile_words = (int16_t)km.tile_words;
     d.t_eff = (int16_t)pl.t_eff;
