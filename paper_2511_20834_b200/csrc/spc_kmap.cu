@@ -45,13 +45,13 @@ struct KmapDesc {
     int32_t *bounds;          // [tiles][Kx*Ky][2] window bounds (k_kmap_bounds)
     int64_t list_stride;
     int32_t spacing;
-    int16_t k_dense, tile_words, t_eff;
+    int32_t k_dense, tile_words, t_eff;   // (scalars int32: see kx below)
     // offset box: Kx x Ky groups of Kz members along z; per axis the
     // offsets e = lo .. lo + K - 1 (odd K centred as in Delta(K, s_p); even K from 0)
     // (int32: byte-wide fields cost 7% of the build -- sign-extending dynamic param loads)
     int32_t kx, ky, kz, lox, loy, loz;
-    int8_t transposed, halved;
-    int8_t ord_idx;                 // density order: index among the ordered maps (-1: none)
+    int32_t transposed, halved;
+    int32_t ord_idx;                // density order: index among the ordered maps (-1: none)
     int8_t ord_cls[SPC_MAX_KVOL];   // density-order key bit of each dense column (-1: none)
     int8_t dcol[SPC_MAX_KVOL];      // weight offset -> dense column (-1: not dense)
     int8_t lst[SPC_MAX_KVOL];       // weight offset -> stored WS list (-1: none)
@@ -923,11 +923,11 @@ static void fill_desc(KmapDesc &d, const spc_kmap &km, const KmapPlan &pl, int32
     d.lox = (int32_t)pl.lo[0];
     d.loy = (int32_t)pl.lo[1];
     d.loz = (int32_t)pl.lo[2];
-    d.k_dense = (int16_t)pl.k_dense;
-    d.tile_words = (int16_t)km.tile_words;
-    d.t_eff = (int16_t)pl.t_eff;
-    d.transposed = (int8_t)km.geom.transposed;
-    d.halved = (int8_t)pl.halved;
+    d.k_dense = pl.k_dense;
+    d.tile_words = km.tile_words;
+    d.t_eff = pl.t_eff;
+    d.transposed = km.geom.transposed;
+    d.halved = pl.halved;
     d.ord_idx = -1;
     for (int c = 0; c < pl.k_dense; ++c) d.ord_cls[c] = pl.ord_cls[c];
     for (int k = 0; k < SPC_MAX_KVOL; ++k) {
@@ -1096,7 +1096,7 @@ static spc_status build_kmap(const void *in_keys, int64_t n_in, const int64_t *n
         g_defer.max_kd = std::max(g_defer.max_kd, pl.k_dense);
         g_defer.tiles += (int64_t)L.tiles;
         if (order) {
-            d.ord_idx = (int8_t)g_defer.orders.size();
+            d.ord_idx = (int32_t)g_defer.orders.size();
             g_defer.orders.push_back(job);
         }
         return SPC_OK;
