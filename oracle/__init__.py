@@ -99,6 +99,14 @@ def _L():
         lib.orc_regular_outputs.restype = I64
         lib.orc_voxelize.argtypes = [P, I64, P, I64, P, P, I64, I, P, P, P]
         lib.orc_voxelize.restype = I64
+        lib.orc_conv_dgrad3.argtypes = [P, I64, P, I64, I, I, I, I, I, P, I, P, I, P]
+        lib.orc_conv_dgrad3.restype = I64
+        lib.orc_conv_dgrad_rows3.argtypes = [P, I64, P, I64, P, I64, I, I, I, I, I, P, I, P, I, P]
+        lib.orc_conv_dgrad_rows3.restype = I64
+        lib.orc_conv_wgrad3.argtypes = [P, I64, P, I64, I, I, I, I, I, P, I, P, I, P]
+        lib.orc_conv_wgrad3.restype = I64
+        lib.orc_bn_relu.argtypes = [P, I64, I, P, P, P, P, ctypes.c_double, P, I, P]
+        lib.orc_bn_relu.restype = None
         lib.orc_num_threads.argtypes = []
         lib.orc_num_threads.restype = ctypes.c_int
         _lib = lib
@@ -272,3 +280,73 @@ def voxelize(points, grid, batch=None, feats=None):
     if nv < 0:
         raise ValueError(f"voxelize: point {-nv - 1} is not finite (or its quotient leaves int32)")
     return coords[:nv], pv[:n], (mean[:nv, :c] if mean is not None else None)
+
+
+# ---------------------------------------------------------------------------------------
+# training path (gradients of Eq. (2)) and the fused BN / residual / ReLU
+# epilogue -- see spc_oracle.h for the definitions each function writes out.
+# ---------------------------------------------------------------------------------------
+
+def conv_dgrad(in_coords, out_coords, K, spacing: int, dF_out, W, transposed: bool = False):
+    """d(Eq. 2)/d f_in: dF_in [n_in, c_in] fp64 from dF_out [n_out, c_out], W [kv, c_in, c_out]."""
+    a = _c(in_coords, np.int32).reshape(-1, 4)
+    b = _c(out_coords, np.int32).reshape(-1, 4)
+    G = _c(dF_out, np.float64)
+    Wd = _c(W, np.float64)
+    c_in, c_out = Wd.shape[1], Wd.shape[2]
+    kx, ky, kz, _ = _box(K)
+    assert G.shape == (b.shape[0], c_out) and Wd.shape[0] == kx * ky * kz
+    out = np.empty((a.shape[0], c_in), np.float64)
+    r = _L().orc_conv_dgrad3(_p(a), a.shape[0], _p(b), b.shape[0], kx, ky, kz, int(spacing), int(transposed),
+                             _p(G), c_out, _p(Wd), c_in, _p(out))
+    if r < 0:
+        raise ValueError("orc_conv_dgrad3 failed")
+    return out
+
+
+def conv_dgrad_rows(in_coords, out_coords, rows, K, spacing: int, dF_out, W, transposed: bool = False):
+    """dF_in for input rows ``rows`` only, by gathering over the output set -> [len(rows), c_in]."""
+    a = _c(in_coords, np.int32).reshape(-1, 4)
+    b = _c(out_coords, np.int32).reshape(-1, 4)
+    rr = _c(rows, np.int64)
+    G = _c(dF_out, np.float64)
+    Wd = _c(W, np.float64)
+    c_in, c_out = Wd.shape[1], Wd.shape[2]
+    kx, ky, kz, _ = _box(K)
+    out = np.empty((rr.shape[0], c_in), np.float64)
+    r = _L().orc_conv_dgrad_rows3(_p(a), a.shape[0], _p(b), b.shape[0], _p(rr), rr.shape[0], kx, ky, kz,
+                                  int(spacing), int(transposed), _p(G), c_out, _p(Wd), c_in, _p(out))
+    if r < 0:
+        raise ValueError("orc_conv_dgrad_rows3 failed")
+    return out
+
+
+def conv_wgrad(in_coords, out_coords, K, spacing: int, F_in, dF_out, transposed: bool = False):
+    """d(Eq. 2)/d W: dW [kv, c_in, c_out] fp64 from F_in [n_in, c_in] and dF_out [n_out, c_out]."""
+    a = _c(in_coords, np.int32).reshape(-1, 4)
+    b = _c(out_coords, np.int32).reshape(-1, 4)
+    F = _c(F_in, np.float64)
+    G = _c(dF_out, np.float64)
+    c_in, c_out = F.shape[1], G.shape[1]
+    kx, ky, kz, _ = _box(K)
+    assert F.shape[0] == a.shape[0] and G.shape[0] == b.shape[0]
+    out = np.empty((kx * ky * kz, c_in, c_out), np.float64)
+    r = _L().orc_conv_wgrad3(_p(a), a.shape[0], _p(b), b.shape[0], kx, ky, kz, int(spacing), int(transposed),
+                             _p(F), c_in, _p(G), c_out, _p(out))
+    if r < 0:
+        raise ValueError("orc_conv_wgrad3 failed")
+    return out
+
+
+def bn_relu(x, gamma=None, beta=None, mean=None, var=None, eps: float = 1e-5, residual=None, relu: bool = True):
+    """relu(bn(x) + residual) per channel (inference BN), fp64; gamma None: no normalisation."""
+    X = _c(x, np.float64)
+    n, c = X.shape
+    y = np.empty_like(X)
+    prm = [None if v is None else _c(v, np.float64).reshape(c) for v in (gamma, beta, mean, var)]
+    if prm[0] is not None:
+        assert all(v is not None for v in prm)
+    R = None if residual is None else _c(residual, np.float64).reshape(n, c)
+    _L().orc_bn_relu(_p(X), n, c, *[(_p(v) if v is not None else None) for v in prm], float(eps),
+                     _p(R) if R is not None else None, int(bool(relu)), _p(y))
+    return y

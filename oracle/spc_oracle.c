@@ -378,6 +378,120 @@ int64_t orc_conv_rows3(const int32_t *in_coords, int64_t n_in, const int32_t *ou
     return r;
 }
 
+/* ------------------------------------------------------------------------------------
+ * NEXT-4 training path: gradients of Eq. (2) (§2.1; training is beyond the
+ * paper's scope).  Same matches as conv_impl; the gradient of f_out_i w.r.t. f_j is
+ * W_k^T and w.r.t. W_k is f_j^T (x) d f_out_i.
+ * ---------------------------------------------------------------------------------- */
+
+int64_t orc_conv_dgrad3(const int32_t *in_coords, int64_t n_in, const int32_t *out_coords, int64_t n_out,
+                        int kx, int ky, int kz, int spacing, int transposed, const double *dF_out, int c_out,
+                        const double *W, int c_in, double *dF_in) {
+    int kv;
+    int32_t *off = offset_table(kx, ky, kz, 0, spacing, &kv);
+    if (!off || c_in <= 0 || c_out <= 0) { free(off); return -1; }
+    orc_hash h;
+    if (hash_build(&h, in_coords, n_in)) { free(off); return -1; }
+    memset(dF_in, 0, sizeof(double) * (size_t)n_in * (size_t)c_in);
+    int64_t nnz = 0;
+    for (int64_t i = 0; i < n_out; ++i)
+        for (int k = 0; k < kv; ++k) {
+            int32_t t[4];
+            make_query(out_coords + 4 * i, off + 3 * k, transposed, t);
+            int64_t j = hash_find(&h, t);
+            if (j < 0) continue;
+            const double *g = dF_out + (size_t)i * c_out;
+            const double *Wk = W + (size_t)k * c_in * c_out;
+            double *d = dF_in + (size_t)j * c_in;
+            for (int ci = 0; ci < c_in; ++ci) {
+                double s = 0.0;
+                for (int co = 0; co < c_out; ++co) s += g[co] * Wk[(size_t)ci * c_out + co];
+                d[ci] += s;
+            }
+            ++nnz;
+        }
+    free(h.slot);
+    free(off);
+    return nnz;
+}
+
+int64_t orc_conv_dgrad_rows3(const int32_t *in_coords, int64_t n_in, const int32_t *out_coords, int64_t n_out,
+                             const int64_t *rows, int64_t n_rows, int kx, int ky, int kz, int spacing,
+                             int transposed, const double *dF_out, int c_out, const double *W, int c_in,
+                             double *dF_in_rows) {
+    (void)n_in;
+    int kv;
+    int32_t *off = offset_table(kx, ky, kz, 0, spacing, &kv);
+    if (!off || c_in <= 0 || c_out <= 0) { free(off); return -1; }
+    orc_hash h;   /* hash on the OUTPUT set: which outputs reach input row j */
+    if (hash_build(&h, out_coords, n_out)) { free(off); return -1; }
+    memset(dF_in_rows, 0, sizeof(double) * (size_t)n_rows * (size_t)c_in);
+    int64_t nnz = 0;
+#pragma omp parallel for reduction(+ : nnz) schedule(dynamic, 64)
+    for (int64_t r = 0; r < n_rows; ++r)
+        for (int k = 0; k < kv; ++k) {
+            /* p_j = q_i + delta_k  <=>  q_i = p_j - delta_k (transposed: p_j = q_i - delta_k) */
+            int32_t t[4];
+            make_query(in_coords + 4 * rows[r], off + 3 * k, !transposed, t);
+            int64_t i = hash_find(&h, t);
+            if (i < 0) continue;
+            const double *g = dF_out + (size_t)i * c_out;
+            const double *Wk = W + (size_t)k * c_in * c_out;
+            double *d = dF_in_rows + (size_t)r * c_in;
+            for (int ci = 0; ci < c_in; ++ci) {
+                double s = 0.0;
+                for (int co = 0; co < c_out; ++co) s += g[co] * Wk[(size_t)ci * c_out + co];
+                d[ci] += s;
+            }
+            ++nnz;
+        }
+    free(h.slot);
+    free(off);
+    return nnz;
+}
+
+int64_t orc_conv_wgrad3(const int32_t *in_coords, int64_t n_in, const int32_t *out_coords, int64_t n_out,
+                        int kx, int ky, int kz, int spacing, int transposed, const double *F_in, int c_in,
+                        const double *dF_out, int c_out, double *dW) {
+    int kv;
+    int32_t *off = offset_table(kx, ky, kz, 0, spacing, &kv);
+    if (!off || c_in <= 0 || c_out <= 0) { free(off); return -1; }
+    orc_hash h;
+    if (hash_build(&h, in_coords, n_in)) { free(off); return -1; }
+    memset(dW, 0, sizeof(double) * (size_t)kv * (size_t)c_in * (size_t)c_out);
+    int64_t nnz = 0;
+    /* one offset at a time: dW_k is a sum over that offset's matches only */
+#pragma omp parallel for reduction(+ : nnz) schedule(dynamic, 1)
+    for (int k = 0; k < kv; ++k)
+        for (int64_t i = 0; i < n_out; ++i) {
+            int32_t t[4];
+            make_query(out_coords + 4 * i, off + 3 * k, transposed, t);
+            int64_t j = hash_find(&h, t);
+            if (j < 0) continue;
+            const double *f = F_in + (size_t)j * c_in;
+            const double *g = dF_out + (size_t)i * c_out;
+            double *Wk = dW + (size_t)k * c_in * c_out;
+            for (int ci = 0; ci < c_in; ++ci)
+                for (int co = 0; co < c_out; ++co) Wk[(size_t)ci * c_out + co] += f[ci] * g[co];
+            ++nnz;
+        }
+    free(h.slot);
+    free(off);
+    return nnz;
+}
+
+void orc_bn_relu(const double *x, int64_t n, int c, const double *gamma, const double *beta, const double *mean,
+                 const double *var, double eps, const double *residual, int relu, double *y) {
+    for (int64_t i = 0; i < n; ++i)
+        for (int ch = 0; ch < c; ++ch) {
+            double v = x[(size_t)i * c + ch];
+            if (gamma) v = (v - mean[ch]) / sqrt(var[ch] + eps) * gamma[ch] + beta[ch];
+            if (residual) v += residual[(size_t)i * c + ch];
+            if (relu && v < 0.0) v = 0.0;
+            y[(size_t)i * c + ch] = v;
+        }
+}
+
 /* spconv's "regular" output rule (P:476-478 networks' public definitions):
  * V_out = { (b, p - delta) : p in V_in, delta in the offset box (spacing), every spatial
  * coordinate of p - delta a multiple of out_stride } -- every output site of stride

@@ -100,6 +100,35 @@ int64_t orc_voxelize(const float *pts, int64_t ld, const int32_t *batch, int64_t
                      const float *feats, int64_t ld_f, int c, int32_t *coords_out, int32_t *point_voxel,
                      double *feats_out);
 
+/* SURVEY NEXT-4 training path (beyond the paper's inference scope): the gradients of
+ * Eq. (2) (§2.1), f_out_i = sum_k sum_j 1[p_j = q_i + delta_k] f_j W_k, written
+ * as their definitions with the same map semantics (box, spacing, transposed) as orc_conv3:
+ *   dgrad : dF_in[j][c]    = sum over matches (i, j, k) of sum_o dF_out[i][o] * W[k][c][o]
+ *   wgrad : dW[k][c][o]    = sum over matches (i, j, k) of F_in[j][c] * dF_out[i][o]
+ * dgrad loops over outputs and scatters into dF_in (hash on the input set);
+ * dgrad_rows computes chosen input rows by GATHER instead (hash on the output set: output
+ * q_i = p_j - delta_k, or p_j + delta_k for a transposed map) -- the two loop orders meet
+ * only in the definition.  dW / dF_in are overwritten.  Return nnz or -1. */
+int64_t orc_conv_dgrad3(const int32_t *in_coords, int64_t n_in, const int32_t *out_coords, int64_t n_out,
+                        int kx, int ky, int kz, int spacing, int transposed, const double *dF_out, int c_out,
+                        const double *W, int c_in, double *dF_in);
+int64_t orc_conv_dgrad_rows3(const int32_t *in_coords, int64_t n_in, const int32_t *out_coords, int64_t n_out,
+                             const int64_t *rows, int64_t n_rows, int kx, int ky, int kz, int spacing,
+                             int transposed, const double *dF_out, int c_out, const double *W, int c_in,
+                             double *dF_in_rows);
+int64_t orc_conv_wgrad3(const int32_t *in_coords, int64_t n_in, const int32_t *out_coords, int64_t n_out,
+                        int kx, int ky, int kz, int spacing, int transposed, const double *F_in, int c_in,
+                        const double *dF_out, int c_out, double *dW);
+
+/* SURVEY NEXT-4 fused epilogue: inference batch normalisation, residual add and ReLU in
+ * the order of the networks' residual blocks (TorchSparse / MinkowskiEngine
+ * ResidualBlock: relu(bn(conv(x)) + shortcut)):
+ *   y[i][c] = (x[i][c] - mean[c]) / sqrt(var[c] + eps) * gamma[c] + beta[c]
+ *             (+ residual[i][c] if residual != NULL),   then max(y, 0) if relu != 0.
+ * gamma == NULL skips the normalisation (y = x).  x and y may alias. */
+void orc_bn_relu(const double *x, int64_t n, int c, const double *gamma, const double *beta, const double *mean,
+                 const double *var, double eps, const double *residual, int relu, double *y);
+
 /* Threads the Eq. (2) row loops use: 1 in the plain build (liboracle.so), the OpenMP
  * thread count in liboracle_omp.so (same arithmetic per row, rows in parallel). */
 int orc_num_threads(void);
