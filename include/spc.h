@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define SPC_VERSION 3
+#define SPC_VERSION 4
 
 typedef enum {
     SPC_OK = 0,
@@ -409,6 +409,61 @@ spc_status spc_conv_forward(const spc_kmap *kmap, const void *f_in, int64_t ld_i
                             int32_t c_in, const void *weight, int32_t c_out, void *f_out,
                             int64_t ld_out, int32_t out_dtype, const void *residual, int64_t ld_res,
                             void *ws, size_t ws_bytes, void *stream);
+
+/* ================================================================================
+ * fused epilogue, training path (beyond the paper's inference scope,
+ * S:15; the gradients of Eq. (2), §2.1).
+ *
+ * spc_epilogue: applied to every FINAL output element (column c) of spc_conv_forward_ex,
+ * in the order of the networks' residual blocks (relu(bn(conv(x)) + shortcut)):
+ *     y = acc * scale[c] + shift[c];  y += residual (if any);  if (relu) y = max(y, 0).
+ * scale / shift: device fp32 [c_out], 16-byte aligned, each nullable (identity).
+ * spc_conv_forward(...) == spc_conv_forward_ex(..., epi = NULL, ...).
+ *
+ * spc_bn_fold: inference batch norm folded on the device:
+ *     scale = gamma / sqrt(var + eps),  shift = beta - mean * scale   (fp32 [c]).
+ * ================================================================================ */
+typedef struct {
+    const float *scale;
+    const float *shift;
+    int32_t relu;
+} spc_epilogue;
+spc_status spc_conv_forward_ex(const spc_kmap *kmap, const void *f_in, int64_t ld_in, int32_t in_dtype,
+                               int32_t c_in, const void *weight, int32_t c_out, void *f_out,
+                               int64_t ld_out, int32_t out_dtype, const void *residual, int64_t ld_res,
+                               const spc_epilogue *epi, void *ws, size_t ws_bytes, void *stream);
+spc_status spc_bn_fold(const float *gamma, const float *beta, const float *mean, const float *var, float eps,
+                       int32_t c, float *scale, float *shift, void *stream);
+
+/* Weight preparation for the data gradient.  dF_in[j] = sum over the map's matches
+ * (i, j, k) of dF_out[i] W_k^T is Eq. (2) run backwards; it reuses the forward kernels:
+ *  - submanifold layer (centred box): the SAME map (by symmetry (j,i,k) in M <=> (i,j,
+ *    K^3-1-k) in M) with weights W'_k = W_{K^3-1-k}^T  -> SPC_WEIGHT_DGRAD_MIRROR;
+ *  - strided layer: the transposed map (out = the layer's inputs, in = its outputs, same
+ *    k, spc_geom.transposed = 1) with W'_k = W_k^T            -> SPC_WEIGHT_DGRAD;
+ *  - transposed layer: the strided map, W'_k = W_k^T           -> SPC_WEIGHT_DGRAD.
+ * Then spc_conv_forward(dgrad map, dF_out, c_in = layer c_out, prepared W', c_out = layer
+ * c_in, dF_in).  weight: [k_vol][c_in][c_out] of the FORWARD layer; the prepared weight
+ * is that of a (k_vol, c_out -> c_in) layer.  (SPC_WEIGHT_FORWARD = spc_prepare_weight.) */
+typedef enum { SPC_WEIGHT_FORWARD = 0, SPC_WEIGHT_DGRAD = 1, SPC_WEIGHT_DGRAD_MIRROR = 2 } spc_weight_mode;
+spc_status spc_prepare_weight_ex(const void *weight, int32_t k_vol, int32_t c_in, int32_t c_out,
+                                 int32_t in_dtype, int32_t mode, void *prepared, void *stream);
+
+/* spc_conv_wgrad -- dW_k[c][o] += sum over the map's pairs (j, i) at offset k of
+ *                   F_in[j][c] * dF_out[i][o]   for every k (the weight gradient of Eq. (2)).
+ * kmap   : the FORWARD layer's map, any t (dense columns: pairs (os_table[i][c], i),
+ *          sentinel rows contribute nothing, empty 128-row tiles skipped; WS lists;
+ *          halved lists also contribute their mirrored pairs to K^3-1-k).
+ * f_in   : [n_in][ld_in] forward inputs; d_out: [n_out][ld_dout] output gradients (both
+ *          in_dtype, rows 16-byte aligned).
+ * d_weight: device fp32 [k_vol][c_in][c_out], ACCUMULATED (zero it before the first
+ *          call); offsets with no pair are left unchanged.
+ * f16/bf16: tcgen05 per-offset gather-GEMM contracting over the pairs (MN-major operands,
+ *          fp32 accumulation in TMEM, red.global.add into d_weight); c_in, c_out
+ *          multiples of 16.  f32: FFMA.  Reduction order is not fixed (atomics). */
+spc_status spc_conv_wgrad(const spc_kmap *kmap, const void *f_in, int64_t ld_in, int32_t in_dtype,
+                          int32_t c_in, const void *d_out, int64_t ld_dout, int32_t c_out, float *d_weight,
+                          void *stream);
 
 /* ================================================================================
  * A13  spc_network_kmaps -- network-wide voxel indexing (§5.5)

@@ -16,6 +16,7 @@ import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libspc.so")
+_PRODUCT_LIB = LIB_PATH
 
 SPC_OK = 0
 SPC_F32, SPC_F16, SPC_BF16 = 0, 1, 2
@@ -106,6 +107,13 @@ class _Kmap(ctypes.Structure):
                 ("list_mirror", ctypes.c_int8 * SPC_MAX_KVOL)]
 
 
+class Epilogue(ctypes.Structure):
+    """spc_epilogue: y = acc * scale + shift, + residual, then ReLU."""
+    _fields_ = [("scale", ctypes.c_void_p), ("shift", ctypes.c_void_p), ("relu", ctypes.c_int32)]
+
+
+SPC_WEIGHT_FORWARD, SPC_WEIGHT_DGRAD, SPC_WEIGHT_DGRAD_MIRROR = 0, 1, 2
+
 _lib = None
 
 
@@ -151,11 +159,18 @@ def lib():
             "spc_conv_workspace_size": ([ctypes.POINTER(_Kmap), I32, I32], SZ),
             "spc_conv_forward": ([ctypes.POINTER(_Kmap), P, I64, I32, I32, P, I32, P, I64, I32, P, I64, P, SZ, P],
                                  ctypes.c_int),
+            "spc_conv_forward_ex": ([ctypes.POINTER(_Kmap), P, I64, I32, I32, P, I32, P, I64, I32, P, I64,
+                                     ctypes.POINTER(Epilogue), P, SZ, P], ctypes.c_int),
+            "spc_bn_fold": ([P, P, P, P, ctypes.c_float, I32, P, P, P], ctypes.c_int),
+            "spc_prepare_weight_ex": ([P, I32, I32, I32, I32, I32, P, P], ctypes.c_int),
+            "spc_conv_wgrad": ([ctypes.POINTER(_Kmap), P, I64, I32, I32, P, I64, I32, P, P], ctypes.c_int),
             "spc_network_workspace_size": ([I64, I32, P, P, P, I32], SZ),
             "spc_shard_ranges": ([P, I64, P, P, I64, P, PackSpec, Geom, I32, P, P], ctypes.c_int),
             "spc_network_kmaps": ([P, I64, P, PackSpec, I32, P, P, P, I32, P, P, P, P, P, SZ, P], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
+            if LIB_PATH != _PRODUCT_LIB and not hasattr(L, name):
+                continue   # an older experiment build (scripts/ab_lib.py) may predate a symbol
             f = getattr(L, name)
             f.argtypes = args
             f.restype = res
@@ -513,13 +528,46 @@ def spc_prepare_weight(weight: torch.Tensor, stream=None) -> torch.Tensor:
     return out
 
 
+def spc_prepare_weight_ex(weight: torch.Tensor, mode: int, stream=None) -> torch.Tensor:
+    """weight [K^3, C_in, C_out] of a FORWARD layer -> prepared weight of mode SPC_WEIGHT_*
+    (DGRAD: W_k^T, DGRAD_MIRROR: W_{K^3-1-k}^T, i.e. a (K^3, C_out -> C_in) layer)."""
+    kv, ci, co = weight.shape
+    w = weight.contiguous()
+    out = _alloc(w.numel(), w.dtype, w.device, stream)
+    _check(lib().spc_prepare_weight_ex(_ptr(w), kv, ci, co, _DT[w.dtype], int(mode), _ptr(out), _stream(stream)),
+           "spc_prepare_weight_ex")
+    return out
+
+
+def spc_bn_fold(gamma, beta, mean, var, eps: float, stream=None):
+    """Inference batch norm folded on the device -> (scale, shift) fp32 [c]."""
+    c = gamma.numel()
+    scale = _alloc(c, torch.float32, gamma.device, stream)
+    shift = _alloc(c, torch.float32, gamma.device, stream)
+    _check(lib().spc_bn_fold(_ptr(gamma), _ptr(beta), _ptr(mean), _ptr(var), float(eps), c, _ptr(scale), _ptr(shift),
+                             _stream(stream)), "spc_bn_fold")
+    return scale, shift
+
+
+def spc_conv_wgrad(km: KernelMap, f_in: torch.Tensor, d_out: torch.Tensor, c_in: int, c_out: int,
+                   d_weight: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """dW [K^3, c_in, c_out] fp32 += the weight gradient of Eq. (2) over the map's pairs."""
+    if d_weight is None:
+        d_weight = _alloc((km.c.k_vol, c_in, c_out), torch.float32, f_in.device, stream, zero=True)
+    _check(lib().spc_conv_wgrad(ctypes.byref(km.c), _ptr(f_in), f_in.stride(0), _DT[f_in.dtype], int(c_in),
+                                _ptr(d_out), d_out.stride(0), int(c_out), _ptr(d_weight), _stream(stream)),
+           "spc_conv_wgrad")
+    return d_weight
+
+
 def spc_conv_workspace_size(km: KernelMap, c_out: int, out_dtype=torch.float32) -> int:
     return int(lib().spc_conv_workspace_size(ctypes.byref(km.c), int(c_out), _DT[out_dtype]))
 
 
 def spc_conv_forward(km: KernelMap, f_in: torch.Tensor, weight_prepared: torch.Tensor, c_in: int, c_out: int,
                      out: torch.Tensor | None = None, out_dtype=None, residual: torch.Tensor | None = None,
-                     ws: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+                     ws: torch.Tensor | None = None, stream=None, scale: torch.Tensor | None = None,
+                     shift: torch.Tensor | None = None, relu: bool = False) -> torch.Tensor:
     """Eq. (2) for the map ``km``: f_in [n_in, >=c_in] (row stride = f_in.stride(0)) -> out [n_out, c_out].
     ``ws``: byte tensor of >= spc_conv_workspace_size bytes, all-zero before its first use
     (torch.zeros); every call leaves it all-zero again."""
@@ -532,10 +580,19 @@ def spc_conv_forward(km: KernelMap, f_in: torch.Tensor, weight_prepared: torch.T
         ws = _ws(need, f_in.device, zero=True, stream=stream)   # all-zero on first use (spc.h), filled on `stream`
     elif ws.numel() < need:
         raise ValueError(f"spc_conv_forward: ws has {ws.numel()} bytes, needs {need}")
-    _check(lib().spc_conv_forward(ctypes.byref(km.c), _ptr(f_in), f_in.stride(0), _DT[f_in.dtype], int(c_in),
-                                  _ptr(weight_prepared), int(c_out), _ptr(out), out.stride(0), _DT[out.dtype],
-                                  _ptr(residual), residual.stride(0) if residual is not None else 0, _ptr(ws),
-                                  ws.numel(), _stream(stream)), "spc_conv_forward")
+    if scale is None and shift is None and not relu:
+        _check(lib().spc_conv_forward(ctypes.byref(km.c), _ptr(f_in), f_in.stride(0), _DT[f_in.dtype], int(c_in),
+                                      _ptr(weight_prepared), int(c_out), _ptr(out), out.stride(0), _DT[out.dtype],
+                                      _ptr(residual), residual.stride(0) if residual is not None else 0, _ptr(ws),
+                                      ws.numel(), _stream(stream)), "spc_conv_forward")
+    else:
+        epi = Epilogue(scale.data_ptr() if scale is not None else None,
+                       shift.data_ptr() if shift is not None else None, int(bool(relu)))
+        _check(lib().spc_conv_forward_ex(ctypes.byref(km.c), _ptr(f_in), f_in.stride(0), _DT[f_in.dtype], int(c_in),
+                                         _ptr(weight_prepared), int(c_out), _ptr(out), out.stride(0), _DT[out.dtype],
+                                         _ptr(residual), residual.stride(0) if residual is not None else 0,
+                                         ctypes.byref(epi), _ptr(ws), ws.numel(), _stream(stream)),
+               "spc_conv_forward_ex")
     if own_ws:
         _release(ws, stream)
     return out

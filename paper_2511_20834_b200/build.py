@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libspc.so")
-SOURCES = ["spc_host.cu", "spc_sort.cu", "spc_kmap.cu", "spc_conv.cu", "spc_dense.cu"]
+SOURCES = ["spc_host.cu", "spc_sort.cu", "spc_kmap.cu", "spc_conv.cu", "spc_dense.cu", "spc_wgrad.cu"]
 HEADERS = ["spc_common.cuh", "spc_ptx.cuh", "spc_tile.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

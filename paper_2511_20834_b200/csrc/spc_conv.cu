@@ -99,6 +99,7 @@ struct ConvParams {
     int out_dtype;        // for OUT_FINAL
     const void *residual;
     int64_t ld_res;
+    Epi epi;              // fused BN (folded scale / shift) + ReLU of OUT_FINAL stores
     int16_t dense_k[SPC_MAX_KVOL];
     int16_t list_k[SPC_MAX_KVOL];
     int8_t list_mirror[SPC_MAX_KVOL];
@@ -295,6 +296,7 @@ __device__ __noinline__ void os_split_fixup(const ConvParams &p, ConvSmem &cs, c
                     v[4 * q + 3] = __float_as_uint(s4.w);
                     __stcg(ap + q, make_float4(0.f, 0.f, 0.f, 0.f));
                 }
+            if (p.epi.scale || p.epi.shift) epi_affine_u32(p.epi, v, gcol, n);
             store_row(p, orow, gcol, v, n);
         }
     }
@@ -473,6 +475,8 @@ __device__ __forceinline__ void epi_role(const ConvParams &p, ConvSmem &cs, floa
                                     ptx::red_add_v4(op + 4 * q, to_f(vals[4 * q]), to_f(vals[4 * q + 1]),
                                                     to_f(vals[4 * q + 2]), to_f(vals[4 * q + 3]));
                         } else {
+                            if (p.out_kind == OUT_FINAL && (p.epi.scale || p.epi.shift))
+                                epi_affine_u32(p.epi, vals, gcol, n);
                             store_row(p, orow, gcol, vals, n);
                         }
                     }
@@ -497,7 +501,9 @@ __device__ __forceinline__ void epi_role(const ConvParams &p, ConvSmem &cs, floa
 // accumulator is returned to zero (workspace invariant).
 __device__ __forceinline__ void convert_items(float *__restrict__ acc, int64_t ld_acc, int64_t n, int c_out, int out_dtype,
                                               void *__restrict__ out, int64_t ld_out, const void *__restrict__ res,
-                                              int64_t ld_res, int clear, int64_t first, int64_t stride) {
+                                              int64_t ld_res, int clear, int64_t first, int64_t stride,
+                                              const Epi &epi) {
+    const bool ep = epi_on(epi);
     const int g8 = c_out / 8;                 // c_out is a multiple of 16
     const int64_t total = n * g8;
     for (int64_t e = first; e < total; e += stride) {
@@ -510,6 +516,7 @@ __device__ __forceinline__ void convert_items(float *__restrict__ acc, int64_t l
             __stcg(ap + 1, make_float4(0.f, 0.f, 0.f, 0.f));
         }
         float v[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+        if (ep) epi_affine(epi, v, c);
         if (out_dtype == SPC_F32) {
             if (res) {
                 const float4 b0 = *reinterpret_cast<const float4 *>(static_cast<const float *>(res) + r * ld_res + c);
@@ -517,6 +524,7 @@ __device__ __forceinline__ void convert_items(float *__restrict__ acc, int64_t l
                 v[0] += b0.x; v[1] += b0.y; v[2] += b0.z; v[3] += b0.w;
                 v[4] += b1.x; v[5] += b1.y; v[6] += b1.z; v[7] += b1.w;
             }
+            if (ep) epi_relu(epi, v);
             float *o = static_cast<float *>(out) + r * ld_out + c;
             *reinterpret_cast<float4 *>(o) = make_float4(v[0], v[1], v[2], v[3]);
             *reinterpret_cast<float4 *>(o + 4) = make_float4(v[4], v[5], v[6], v[7]);
@@ -531,6 +539,7 @@ __device__ __forceinline__ void convert_items(float *__restrict__ acc, int64_t l
                     v[2 * q + 1] += f.y;
                 }
             }
+            if (ep) epi_relu(epi, v);
             *reinterpret_cast<uint4 *>(static_cast<uint16_t *>(out) + r * ld_out + c) =
                 make_uint4(pack2(v[0], v[1], out_dtype), pack2(v[2], v[3], out_dtype), pack2(v[4], v[5], out_dtype),
                            pack2(v[6], v[7], out_dtype));
@@ -1130,10 +1139,15 @@ __global__ void __launch_bounds__(256) k_conv_simt(const __grid_constant__ ConvP
             const int col = col0 + tx * 4 + j;
             if (col >= c_out) continue;
             float v = acc[i][j];
+            if (p.out_kind == OUT_FINAL) {
+                if (p.epi.scale) v *= p.epi.scale[col];
+                if (p.epi.shift) v += p.epi.shift[col];
+            }
             if (p.out_kind == OUT_F32_RED) {
                 atomicAdd(static_cast<float *>(p.out) + orow * p.ld_out + col, v);
             } else if (p.out_kind == OUT_F32_STORE || p.out_dtype == SPC_F32) {
                 if (p.out_kind == OUT_FINAL && p.residual) v += static_cast<const float *>(p.residual)[orow * p.ld_res + col];
+                if (p.out_kind == OUT_FINAL && p.epi.relu) v = fmaxf(v, 0.f);
                 static_cast<float *>(p.out)[orow * p.ld_out + col] = v;
             } else {
                 if (p.residual) {
@@ -1141,6 +1155,7 @@ __global__ void __launch_bounds__(256) k_conv_simt(const __grid_constant__ ConvP
                     v += p.out_dtype == SPC_BF16 ? __bfloat162float(__ushort_as_bfloat16(h))
                                                  : __half2float(__ushort_as_half(h));
                 }
+                if (p.epi.relu) v = fmaxf(v, 0.f);
                 static_cast<uint16_t *>(p.out)[orow * p.ld_out + col] =
                     p.out_dtype == SPC_BF16 ? __bfloat16_as_ushort(__float2bfloat16_rn(v))
                                             : __half_as_ushort(__float2half_rn(v));
@@ -1154,8 +1169,10 @@ __global__ void __launch_bounds__(256) k_conv_simt(const __grid_constant__ ConvP
 // ------------------------------------------------------------------------------------
 // weights -> per (k, N-tile, C-chunk) blobs laid out exactly as the swizzled K-major smem
 // tile the MMA reads: row n (BK elements = rb bytes), 16-byte chunk j stored at j ^ f(n)
+// mode (spc_weight_mode): 0 = W_k as given; 1 = W_k^T (c_in / c_out are those of the
+// PREPARED weight: the source is [k_vol][c_out][c_in]); 2 = W_{k_vol-1-k}^T
 __global__ void k_prepare_weight_tc(const uint16_t *__restrict__ w, int k_vol, int c_in, int c_out, int BK, int BN,
-                                    uint16_t *__restrict__ out) {
+                                    int mode, uint16_t *__restrict__ out) {
     pdl_wait();   // PDL launch: the predecessor has completed and flushed
     pdl_trigger();
     const int64_t total = (int64_t)k_vol * c_in * c_out;
@@ -1166,12 +1183,14 @@ __global__ void k_prepare_weight_tc(const uint16_t *__restrict__ w, int k_vol, i
         const int64_t t = e / c_out;
         const int ci = (int)(t % c_in);
         const int k = (int)(t / c_in);
+        const int64_t src = mode == 0 ? e
+                                      : ((int64_t)(mode == 2 ? k_vol - 1 - k : k) * c_out + co) * c_in + ci;
         const int nt = co / BN, n = co % BN, cc = ci / BK, c = ci % BK;
         const int64_t blob = ((int64_t)k * n_nt + nt) * n_ch + cc;
         const int f = rb == 128 ? (n & 7) : (rb == 64 ? ((n >> 1) & 3) : ((n >> 2) & 1));
         const int j = (c * 2) / 16, within = (c * 2) % 16;
         const int64_t byte = (int64_t)n * rb + (int64_t)((j ^ f) * 16) + within;
-        out[blob * BN * BK + byte / 2] = w[e];
+        out[blob * BN * BK + byte / 2] = w[src];
     }
 }
 
@@ -1179,12 +1198,12 @@ __global__ void k_prepare_weight_tc(const uint16_t *__restrict__ w, int k_vol, i
 // clear != 0: the accumulator rows are returned to zero after the read (workspace invariant)
 __global__ void k_convert(float *__restrict__ acc, int64_t ld_acc, int64_t n_cap, const int64_t *n_dev, int c_out,
                           int out_dtype, void *__restrict__ out, int64_t ld_out, const void *__restrict__ res,
-                          int64_t ld_res, int clear) {
+                          int64_t ld_res, int clear, Epi epi) {
     pdl_wait();
     pdl_trigger();
     const int64_t n = dev_count(n_cap, n_dev);
     convert_items(acc, ld_acc, n, c_out, out_dtype, out, ld_out, res, ld_res, clear,
-                  blockIdx.x * (int64_t)blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x);
+                  blockIdx.x * (int64_t)blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x, epi);
 }
 
 __global__ void k_zero_rows(float *__restrict__ acc, int64_t ld, int64_t n_cap, const int64_t *n_dev, int c) {
@@ -1215,7 +1234,8 @@ static size_t elem_size(int dt) { return dt == SPC_F32 ? 4 : 2; }
 
 spc_status dense_forward(const void *f_in, int64_t ld_in, int in_dtype, int c_in, const void *wblob, int k, int c_out,
                          int BK, int BN, int64_t n_cap, const int64_t *n_dev, void *out, int64_t ld_out, int out_kind,
-                         int out_dtype, const void *residual, int64_t ld_res, cudaStream_t st);   // spc_dense.cu
+                         int out_dtype, const void *residual, int64_t ld_res, const Epi &epi,
+                         cudaStream_t st);   // spc_dense.cu
 
 }  // namespace spc
 
@@ -1226,13 +1246,65 @@ extern "C" size_t spc_prepared_weight_bytes(int32_t k_vol, int32_t c_in, int32_t
     return (size_t)k_vol * c_in * c_out * elem_size(in_dtype);
 }
 
+__global__ void k_transpose_weight_f32(const float *__restrict__ w, int k_vol, int c_in, int c_out, int mode,
+                                       float *__restrict__ out) {
+    pdl_wait();
+    pdl_trigger();
+    const int64_t total = (int64_t)k_vol * c_in * c_out;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int co = (int)(e % c_out);
+        const int64_t t = e / c_out;
+        const int ci = (int)(t % c_in);
+        const int k = (int)(t / c_in);
+        out[e] = w[((int64_t)(mode == 2 ? k_vol - 1 - k : k) * c_out + co) * c_in + ci];
+    }
+}
+
+__global__ void k_bn_fold(const float *gamma, const float *beta, const float *mean, const float *var, float eps, int c,
+                          float *scale, float *shift) {
+    pdl_wait();
+    pdl_trigger();
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < c; i += gridDim.x * blockDim.x) {
+        const float s = gamma[i] / sqrtf(var[i] + eps);
+        scale[i] = s;
+        shift[i] = beta[i] - mean[i] * s;
+    }
+}
+
+extern "C" spc_status spc_bn_fold(const float *gamma, const float *beta, const float *mean, const float *var,
+                                  float eps, int32_t c, float *scale, float *shift, void *stream) {
+    SPC_CHECK_ARG(gamma && beta && mean && var && scale && shift && c > 0, "bad arguments");
+    SPC_CUDA(launch_pdl(k_bn_fold, dim3((unsigned)((c + 255) / 256)), dim3(256), 0, as_stream(stream), gamma, beta,
+                        mean, var, eps, (int)c, scale, shift));
+    SPC_LAUNCH_CHECK("k_bn_fold");
+    return SPC_OK;
+}
+
 extern "C" spc_status spc_prepare_weight(const void *weight, int32_t k_vol, int32_t c_in, int32_t c_out,
                                          int32_t in_dtype, void *prepared, void *stream) {
+    return spc_prepare_weight_ex(weight, k_vol, c_in, c_out, in_dtype, SPC_WEIGHT_FORWARD, prepared, stream);
+}
+
+extern "C" spc_status spc_prepare_weight_ex(const void *weight, int32_t k_vol, int32_t c_in, int32_t c_out,
+                                            int32_t in_dtype, int32_t mode, void *prepared, void *stream) {
     SPC_CHECK_ARG(weight && prepared, "null pointer");
     SPC_CHECK_ARG(k_vol >= 1 && k_vol <= SPC_MAX_KVOL && c_in > 0 && c_out > 0, "bad shape");
+    SPC_CHECK_ARG(mode >= SPC_WEIGHT_FORWARD && mode <= SPC_WEIGHT_DGRAD_MIRROR, "bad weight mode");
+    SPC_CHECK_ARG(weight != prepared, "weight and prepared must not alias");
     cudaStream_t st = as_stream(stream);
+    // the kernels take the PREPARED layer's channel counts: a dgrad weight is that of a
+    // (c_out -> c_in) layer
+    if (mode != SPC_WEIGHT_FORWARD) std::swap(c_in, c_out);
     if (in_dtype == SPC_F32) {
-        SPC_CUDA(cudaMemcpyAsync(prepared, weight, (size_t)k_vol * c_in * c_out * 4, cudaMemcpyDeviceToDevice, st));
+        if (mode == SPC_WEIGHT_FORWARD) {
+            SPC_CUDA(cudaMemcpyAsync(prepared, weight, (size_t)k_vol * c_in * c_out * 4, cudaMemcpyDeviceToDevice, st));
+        } else {
+            const int64_t total = (int64_t)k_vol * c_in * c_out;
+            SPC_CUDA(launch_pdl(k_transpose_weight_f32, dim3((unsigned)std::min<int64_t>((total + 255) / 256, 4096)),
+                                dim3(256), 0, st, static_cast<const float *>(weight), (int)k_vol, (int)c_in, (int)c_out,
+                                (int)mode, static_cast<float *>(prepared)));
+            SPC_LAUNCH_CHECK("k_transpose_weight_f32");
+        }
         return SPC_OK;
     }
     SPC_CHECK_ARG(in_dtype == SPC_F16 || in_dtype == SPC_BF16, "bad dtype");
@@ -1240,7 +1312,7 @@ extern "C" spc_status spc_prepare_weight(const void *weight, int32_t k_vol, int3
         return fail(SPC_ERR_UNSUPPORTED, "spc_prepare_weight: f16/bf16 needs c_in and c_out multiples of 16");
     const int64_t total = (int64_t)k_vol * c_in * c_out;
     SPC_CUDA(launch_pdl(k_prepare_weight_tc, dim3((unsigned)std::min<int64_t>((total + 255) / 256, 4096)), dim3(256), 0, st, 
-        static_cast<const uint16_t *>(weight), k_vol, c_in, c_out, pick_bk(c_in), pick_bn(c_out),
+        static_cast<const uint16_t *>(weight), k_vol, c_in, c_out, pick_bk(c_in), pick_bn(c_out), (int)mode,
         static_cast<uint16_t *>(prepared)));
     SPC_LAUNCH_CHECK("k_prepare_weight_tc");
     return SPC_OK;
@@ -1345,6 +1417,14 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
                                        int32_t c_in, const void *weight, int32_t c_out, void *f_out, int64_t ld_out,
                                        int32_t out_dtype, const void *residual, int64_t ld_res, void *ws,
                                        size_t ws_bytes, void *stream) {
+    return spc_conv_forward_ex(km, f_in, ld_in, in_dtype, c_in, weight, c_out, f_out, ld_out, out_dtype, residual,
+                               ld_res, nullptr, ws, ws_bytes, stream);
+}
+
+extern "C" spc_status spc_conv_forward_ex(const spc_kmap *km, const void *f_in, int64_t ld_in, int32_t in_dtype,
+                                          int32_t c_in, const void *weight, int32_t c_out, void *f_out,
+                                          int64_t ld_out, int32_t out_dtype, const void *residual, int64_t ld_res,
+                                          const spc_epilogue *epi, void *ws, size_t ws_bytes, void *stream) {
     SPC_CHECK_ARG(km && weight && f_out, "null pointer");
     SPC_CHECK_ARG(in_dtype >= SPC_F32 && in_dtype <= SPC_BF16 && out_dtype >= SPC_F32 && out_dtype <= SPC_BF16,
                   "bad dtype");
@@ -1368,12 +1448,15 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
     p.out_dtype = out_dtype;
     p.residual = residual;
     p.ld_res = ld_res;
+    if (epi) p.epi = Epi{epi->scale, epi->shift, epi->relu};
+    SPC_CHECK_ARG(!epi || ((uintptr_t)epi->scale % 16 == 0 && (uintptr_t)epi->shift % 16 == 0),
+                  "epilogue scale / shift must be 16-byte aligned");
 
     // accumulator of the WS part (fp32)
     float *acc = nullptr;
     int64_t ld_acc = 0;
     if (has_ws) {
-        if (out_dtype == SPC_F32 && !residual) {
+        if (out_dtype == SPC_F32 && !residual && !epi_on(p.epi)) {
             acc = static_cast<float *>(f_out);
             ld_acc = ld_out;
         } else {
@@ -1413,7 +1496,7 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
             if (acc != f_out) {
                 const int64_t work = km->n_out * (c_out / 8);
                 SPC_CUDA(launch_pdl(k_convert, dim3((unsigned)std::min<int64_t>((work + 255) / 256, 8 * 148)), dim3(256), 0, st,
-                    acc, ld_acc, km->n_out, km->n_out_dev, (int)c_out, (int)out_dtype, f_out, ld_out, residual, ld_res, 1));
+                    acc, ld_acc, km->n_out, km->n_out_dev, (int)c_out, (int)out_dtype, f_out, ld_out, residual, ld_res, 1, p.epi));
                 SPC_LAUNCH_CHECK("k_convert");
             }
         }
@@ -1480,7 +1563,7 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
                       km->n_in == km->n_out && km->n_in_dev == km->n_out_dev;
     if (subm && km->k_vol == 1 && km->k_dense == 1)
         return dense_forward(f_in, ld_in, in_dtype, c_in, weight, 0, c_out, p.BK, p.BN, km->n_out, km->n_out_dev, f_out,
-                             ld_out, OUT_FINAL, out_dtype, residual, ld_res, st);
+                             ld_out, OUT_FINAL, out_dtype, residual, ld_res, p.epi, st);
     if (!has_ws) {
         // OS only: one launch; small levels split offsets over CTAs with the in-kernel fixup
         p.split_ok = (p.cg == 1 && wacc && km->k_dense >= 4 && option(SPC_OPT_CONV_OS_SPLIT) != 0) ? 1 : 0;
@@ -1501,7 +1584,7 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
         if (s != SPC_OK) return s;
     } else if (p.skip_list >= 0) {
         spc_status s = dense_forward(f_in, ld_in, in_dtype, c_in, weight, centre, c_out, p.BK, p.BN, km->n_out,
-                                     km->n_out_dev, acc, ld_acc, OUT_F32_STORE, SPC_F32, nullptr, 0, st);
+                                     km->n_out_dev, acc, ld_acc, OUT_F32_STORE, SPC_F32, nullptr, 0, Epi{}, st);
         if (s != SPC_OK) return s;
     } else if (acc == f_out) {
         SPC_CUDA(launch_pdl(k_zero_rows, dim3(1024), dim3(256), 0, st, acc, ld_acc, km->n_out, km->n_out_dev, (int)c_out));
@@ -1514,7 +1597,7 @@ extern "C" spc_status spc_conv_forward(const spc_kmap *km, const void *f_in, int
     if (acc != f_out) {
         const int64_t work = km->n_out * (c_out / 8);
         SPC_CUDA(launch_pdl(k_convert, dim3((unsigned)std::min<int64_t>((work + 255) / 256, 8 * 148)), dim3(256), 0, st,
-            acc, ld_acc, km->n_out, km->n_out_dev, (int)c_out, (int)out_dtype, f_out, ld_out, residual, ld_res, 1));
+            acc, ld_acc, km->n_out, km->n_out_dev, (int)c_out, (int)out_dtype, f_out, ld_out, residual, ld_res, 1, p.epi));
         SPC_LAUNCH_CHECK("k_convert");
     }
     return SPC_OK;

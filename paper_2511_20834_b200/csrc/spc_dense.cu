@@ -47,6 +47,7 @@ struct DenseParams {
     int out_dtype;
     const void *residual;
     int64_t ld_res;
+    Epi epi;                   // fused BN / ReLU of OUT_FINAL stores (spc_tile.cuh)
     Trace trace;
 };
 
@@ -147,7 +148,11 @@ __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_tc(const __grid_constan
                 if (cnt == 32) ptx::tmem_ld32(tbase + col, vals);
                 else ptx::tmem_ld16(tbase + col, vals);
                 ptx::tmem_ld_wait();
-                if (row < n) store_row(p, row, nt * p.BN + col, vals, cnt);
+                if (row < n) {
+                    if (p.out_kind == OUT_FINAL && (p.epi.scale || p.epi.shift))
+                        epi_affine_u32(p.epi, vals, nt * p.BN + col, cnt);
+                    store_row(p, row, nt * p.BN + col, vals, cnt);
+                }
             }
             ptx::tc_fence_before();
             __syncwarp();
@@ -199,7 +204,7 @@ static spc_status encode_rows_tmap(CUtensorMap *tm, const void *base, int64_t n_
 // submanifold centre).  out_kind: OUT_FINAL (dtype + residual) or OUT_F32_STORE.
 spc_status dense_forward(const void *f_in, int64_t ld_in, int in_dtype, int c_in, const void *wblob, int k, int c_out,
                          int BK, int BN, int64_t n_cap, const int64_t *n_dev, void *out, int64_t ld_out, int out_kind,
-                         int out_dtype, const void *residual, int64_t ld_res, cudaStream_t st) {
+                         int out_dtype, const void *residual, int64_t ld_res, const Epi &epi, cudaStream_t st) {
     if (n_cap == 0) return SPC_OK;
     DenseParams p;
     memset(&p, 0, sizeof(p));
@@ -224,6 +229,7 @@ spc_status dense_forward(const void *f_in, int64_t ld_in, int in_dtype, int c_in
     p.out_dtype = out_dtype;
     p.residual = residual;
     p.ld_res = ld_res;
+    p.epi = epi;
     const size_t hdr = align_up(sizeof(DenseSmem), 1024);
     const size_t per = align_up(p.kb_a, 1024) + align_up(p.kb_b, 1024);
     p.stages = (int)std::min<size_t>(DN_MAX_STAGES, (DN_SMEM_BUDGET - 1024 - hdr) / per);
