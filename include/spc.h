@@ -87,7 +87,9 @@ typedef enum {
                                    * kernel drains (programmatic dependent launch) (default 0)  */
     SPC_OPT_CONV_BULK_RED = 11,   /* 1 (default): the weight-stationary scatter reduces 64-column
                                    * row segments with bulk reductions (TMA); 0: red.global.add */
-    SPC_OPT_COUNT = 12
+    SPC_OPT_WGRAD_ITEMS_PER_SM = 12, /* spc_conv_wgrad work items per SM over the map's pair
+                                   * capacity (default 16: smaller items balance better)       */
+    SPC_OPT_COUNT = 13
 } spc_option;
 spc_status spc_set_option(int32_t option, int64_t value);
 int64_t spc_get_option(int32_t option);
@@ -443,7 +445,9 @@ spc_status spc_bn_fold(const float *gamma, const float *beta, const float *mean,
  *    k, spc_geom.transposed = 1) with W'_k = W_k^T            -> SPC_WEIGHT_DGRAD;
  *  - transposed layer: the strided map, W'_k = W_k^T           -> SPC_WEIGHT_DGRAD.
  * Then spc_conv_forward(dgrad map, dF_out, c_in = layer c_out, prepared W', c_out = layer
- * c_in, dF_in).  weight: [k_vol][c_in][c_out] of the FORWARD layer; the prepared weight
+ * c_in, dF_in); gradients of inputs read by several layers accumulate through the
+ * residual operand (residual == f_out is allowed: every element is read, then written, by
+ * the same thread).  weight: [k_vol][c_in][c_out] of the FORWARD layer; the prepared weight
  * is that of a (k_vol, c_out -> c_in) layer.  (SPC_WEIGHT_FORWARD = spc_prepare_weight.) */
 typedef enum { SPC_WEIGHT_FORWARD = 0, SPC_WEIGHT_DGRAD = 1, SPC_WEIGHT_DGRAD_MIRROR = 2 } spc_weight_mode;
 spc_status spc_prepare_weight_ex(const void *weight, int32_t k_vol, int32_t c_in, int32_t c_out,
@@ -461,6 +465,11 @@ spc_status spc_prepare_weight_ex(const void *weight, int32_t k_vol, int32_t c_in
  * f16/bf16: tcgen05 per-offset gather-GEMM contracting over the pairs (MN-major operands,
  *          fp32 accumulation in TMEM, red.global.add into d_weight); c_in, c_out
  *          multiples of 16.  f32: FFMA.  Reduction order is not fixed (atomics). */
+/* dst[r][0..c) += src[r][0..c) for r < *n_dev (or n_cap): the residual branch of a
+ * backward pass (the gradient of out = conv + residual w.r.t. residual).  c % 8 == 0,
+ * rows 16-byte aligned; dst and src must not overlap unless equal. */
+spc_status spc_add_rows(void *dst, int64_t ld_dst, const void *src, int64_t ld_src, int64_t n_cap,
+                        const int64_t *n_dev, int32_t c, int32_t dtype, void *stream);
 spc_status spc_conv_wgrad(const spc_kmap *kmap, const void *f_in, int64_t ld_in, int32_t in_dtype,
                           int32_t c_in, const void *d_out, int64_t ld_dout, int32_t c_out, float *d_weight,
                           void *stream);

@@ -33,6 +33,7 @@ SPC_MAX_KVOL = 125
 SPC_OPT_CONV_TILE_ROWS, SPC_OPT_CONV_STAGE_KB, SPC_OPT_CONV_OS_SPLIT, SPC_OPT_CONV_SPLIT_MIN = 0, 1, 2, 3
 SPC_OPT_CONV_CLAIM_AHEAD, SPC_OPT_CONV_DENSITY_ORDER, SPC_OPT_PDL, SPC_OPT_KMAP_POOL_KEYS = 4, 5, 6, 7
 SPC_OPT_CONV_DENSE_CENTRE, SPC_OPT_CONV_CTA_PAIR, SPC_OPT_CONV_MAPS_READY, SPC_OPT_CONV_BULK_RED = 8, 9, 10, 11
+SPC_OPT_WGRAD_ITEMS_PER_SM = 12
 
 _DT = {torch.float32: SPC_F32, torch.float16: SPC_F16, torch.bfloat16: SPC_BF16}
 _TORCH_DT = {v: k for k, v in _DT.items()}
@@ -163,6 +164,7 @@ def lib():
                                      ctypes.POINTER(Epilogue), P, SZ, P], ctypes.c_int),
             "spc_bn_fold": ([P, P, P, P, ctypes.c_float, I32, P, P, P], ctypes.c_int),
             "spc_prepare_weight_ex": ([P, I32, I32, I32, I32, I32, P, P], ctypes.c_int),
+            "spc_add_rows": ([P, I64, P, I64, I64, P, I32, I32, P], ctypes.c_int),
             "spc_conv_wgrad": ([ctypes.POINTER(_Kmap), P, I64, I32, I32, P, I64, I32, P, P], ctypes.c_int),
             "spc_network_workspace_size": ([I64, I32, P, P, P, I32], SZ),
             "spc_shard_ranges": ([P, I64, P, P, I64, P, PackSpec, Geom, I32, P, P], ctypes.c_int),
@@ -558,6 +560,13 @@ def spc_conv_wgrad(km: KernelMap, f_in: torch.Tensor, d_out: torch.Tensor, c_in:
                                 _ptr(d_out), d_out.stride(0), int(c_out), _ptr(d_weight), _stream(stream)),
            "spc_conv_wgrad")
     return d_weight
+
+
+def spc_add_rows(dst: torch.Tensor, src: torch.Tensor, n_dev=None, stream=None):
+    """dst[:n] += src[:n] (row slices with their own strides; n = *n_dev or dst rows)."""
+    _check(lib().spc_add_rows(_ptr(dst), dst.stride(0), _ptr(src), src.stride(0), dst.shape[0], _ptr(n_dev),
+                              dst.shape[1], _DT[dst.dtype], _stream(stream)), "spc_add_rows")
+    return dst
 
 
 def spc_conv_workspace_size(km: KernelMap, c_out: int, out_dtype=torch.float32) -> int:

@@ -232,6 +232,7 @@ __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: 
 // counter; the part that completes the count reads the sum back, adds the residual,
 // writes the final dtype, and returns the accumulator rows and the counter to zero (so
 // the next launch needs no zero-fill).
+template <bool EPI>
 __device__ __noinline__ void os_split_fixup(const ConvParams &p, ConvSmem &cs, const TileRec &R, uint32_t ti,
                                             int split, int nht, uint32_t tmem_tile, uint32_t tempty_bar, int e,
                                             int lane) {
@@ -296,8 +297,10 @@ __device__ __noinline__ void os_split_fixup(const ConvParams &p, ConvSmem &cs, c
                     v[4 * q + 3] = __float_as_uint(s4.w);
                     __stcg(ap + q, make_float4(0.f, 0.f, 0.f, 0.f));
                 }
-            if (p.epi.scale || p.epi.shift) epi_affine_u32(p.epi, v, gcol, n);
-            store_row(p, orow, gcol, v, n);
+            if constexpr (EPI) {
+                if (p.epi.scale || p.epi.shift) epi_affine_u32(p.epi, v, gcol, n);
+            }
+            store_row<EPI>(p, orow, gcol, v, n);
         }
     }
     if (lead) *reinterpret_cast<volatile int *>(ctr) = 0;
@@ -404,7 +407,7 @@ constexpr int RED_COLS = 64;      // WS scatter: columns per bulk reduction (256
 constexpr int RED_LD = RED_COLS + 4;   // floats per staging row (16-byte aligned, fewer bank conflicts)
 constexpr int RED_STAGE_BYTES = 4 * 32 * RED_LD * 4;
 
-template <bool FIX>
+template <bool FIX, bool EPI>
 __device__ __forceinline__ void epi_role(const ConvParams &p, ConvSmem &cs, float *red_stage, uint32_t tmem_base,
                                          int tr, int nht, int NH, int warp, int lane, int pair_rank) {
     const int e = warp - W_EPI0;   // == warp % 4: the TMEM lane quadrant this warp may access
@@ -425,7 +428,7 @@ __device__ __forceinline__ void epi_role(const ConvParams &p, ConvSmem &cs, floa
         ptx::tc_fence_after();
         const bool fix = FIX && R.nsplit > 1;
         if (fix) {
-            os_split_fixup(p, cs, R, ti, R.nsplit, nht, tmem_base + a * NH * p.tmem_cols, ptx::smem_u32(&cs.tempty[a]),
+            os_split_fixup<EPI>(p, cs, R, ti, R.nsplit, nht, tmem_base + a * NH * p.tmem_cols, ptx::smem_u32(&cs.tempty[a]),
                            e, lane);
         } else {
 #pragma unroll 1
@@ -475,9 +478,11 @@ __device__ __forceinline__ void epi_role(const ConvParams &p, ConvSmem &cs, floa
                                     ptx::red_add_v4(op + 4 * q, to_f(vals[4 * q]), to_f(vals[4 * q + 1]),
                                                     to_f(vals[4 * q + 2]), to_f(vals[4 * q + 3]));
                         } else {
-                            if (p.out_kind == OUT_FINAL && (p.epi.scale || p.epi.shift))
-                                epi_affine_u32(p.epi, vals, gcol, n);
-                            store_row(p, orow, gcol, vals, n);
+                            if constexpr (EPI) {
+                                if (p.out_kind == OUT_FINAL && (p.epi.scale || p.epi.shift))
+                                    epi_affine_u32(p.epi, vals, gcol, n);
+                            }
+                            store_row<EPI>(p, orow, gcol, vals, n);
                         }
                     }
                 }
@@ -547,7 +552,7 @@ __device__ __forceinline__ void convert_items(float *__restrict__ acc, int64_t l
     }
 }
 
-template <int BK, int BM, int CG>
+template <int BK, int BM, int CG, bool EPI = false>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant__ ConvParams p) {
     constexpr int NH = BM / TC_BM;   // 128-row MMA halves per tile (per CTA)
     static_assert(CG == 1 || BM == TC_BM, "a CTA of a pair holds 128 rows");
@@ -1013,9 +1018,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         const int pair_rank = CG == 2 ? (int)rank : -1;
         float *red_stage = p.red_off ? reinterpret_cast<float *>(smem + p.red_off) : nullptr;
         if (wsplit)
-            epi_role<true>(p, cs, red_stage, tmem_base, tr, nht, NH, warp, lane, pair_rank);
+            epi_role<true, EPI>(p, cs, red_stage, tmem_base, tr, nht, NH, warp, lane, pair_rank);
         else
-            epi_role<false>(p, cs, red_stage, tmem_base, tr, nht, NH, warp, lane, pair_rank);
+            epi_role<false, EPI>(p, cs, red_stage, tmem_base, tr, nht, NH, warp, lane, pair_rank);
     }
     ptx::tc_fence_before();
     // a pair frees its TMEM and exits together (the leader's MMAs and commits reach the
@@ -1260,6 +1265,58 @@ __global__ void k_transpose_weight_f32(const float *__restrict__ w, int k_vol, i
     }
 }
 
+// dst[r][0..c) += src[r][0..c) for the live rows (the residual branch of a backward pass);
+// 8 columns per work item, c a multiple of 8, rows 16-byte aligned
+__global__ void k_add_rows(void *__restrict__ dst, int64_t ld_dst, const void *__restrict__ src, int64_t ld_src,
+                           int64_t n_cap, const int64_t *n_dev, int c, int dtype) {
+    pdl_wait();
+    pdl_trigger();
+    const int64_t n = dev_count(n_cap, n_dev);
+    const int g8 = c / 8;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * g8; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = e / g8;
+        const int col = (int)(e - r * g8) * 8;
+        if (dtype == SPC_F32) {
+            float4 *d = reinterpret_cast<float4 *>(static_cast<float *>(dst) + r * ld_dst + col);
+            const float4 *s = reinterpret_cast<const float4 *>(static_cast<const float *>(src) + r * ld_src + col);
+            for (int q = 0; q < 2; ++q) {
+                float4 a = d[q];
+                const float4 b = s[q];
+                a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+                d[q] = a;
+            }
+        } else {
+            uint4 *d = reinterpret_cast<uint4 *>(static_cast<uint16_t *>(dst) + r * ld_dst + col);
+            const uint4 u = *reinterpret_cast<const uint4 *>(static_cast<const uint16_t *>(src) + r * ld_src + col);
+            const uint4 w = *d;
+            const uint32_t a[4] = {w.x, w.y, w.z, w.w}, b[4] = {u.x, u.y, u.z, u.w};
+            uint32_t o[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float2 x = unpack2(a[q], dtype), y = unpack2(b[q], dtype);
+                o[q] = pack2(x.x + y.x, x.y + y.y, dtype);
+            }
+            *d = make_uint4(o[0], o[1], o[2], o[3]);
+        }
+    }
+}
+
+extern "C" spc_status spc_add_rows(void *dst, int64_t ld_dst, const void *src, int64_t ld_src, int64_t n_cap,
+                                   const int64_t *n_dev, int32_t c, int32_t dtype, void *stream) {
+    SPC_CHECK_ARG(dst && src && c > 0 && c % 8 == 0 && ld_dst >= c && ld_src >= c, "bad arguments");
+    SPC_CHECK_ARG(dtype >= SPC_F32 && dtype <= SPC_BF16, "bad dtype");
+    const size_t es = dtype == SPC_F32 ? 4 : 2;
+    SPC_CHECK_ARG((uintptr_t)dst % 16 == 0 && (uintptr_t)src % 16 == 0 && (ld_dst * es) % 16 == 0 &&
+                      (ld_src * es) % 16 == 0,
+                  "rows must be 16-byte aligned");
+    if (n_cap == 0) return SPC_OK;
+    const int64_t work = n_cap * (c / 8);
+    SPC_CUDA(launch_pdl(k_add_rows, dim3((unsigned)std::min<int64_t>((work + 255) / 256, 8 * 148)), dim3(256), 0,
+                        as_stream(stream), dst, ld_dst, src, ld_src, n_cap, n_dev, (int)c, (int)dtype));
+    SPC_LAUNCH_CHECK("k_add_rows");
+    return SPC_OK;
+}
+
 __global__ void k_bn_fold(const float *gamma, const float *beta, const float *mean, const float *var, float eps, int c,
                           float *scale, float *shift) {
     pdl_wait();
@@ -1388,7 +1445,10 @@ static spc_status launch_tc(const ConvParams &p0, int mode, int out_kind, void *
     if (!(configured >> dev & 1)) {
         void (*ks[])(ConvParams) = {k_conv_tc<16, 128, 1>, k_conv_tc<32, 128, 1>, k_conv_tc<64, 128, 1>,
                                     k_conv_tc<16, 256, 1>, k_conv_tc<32, 256, 1>, k_conv_tc<64, 256, 1>,
-                                    k_conv_tc<16, 128, 2>, k_conv_tc<32, 128, 2>, k_conv_tc<64, 128, 2>};
+                                    k_conv_tc<16, 128, 2>, k_conv_tc<32, 128, 2>, k_conv_tc<64, 128, 2>,
+                                    k_conv_tc<16, 128, 1, true>, k_conv_tc<32, 128, 1, true>,
+                                    k_conv_tc<64, 128, 1, true>, k_conv_tc<16, 256, 1, true>,
+                                    k_conv_tc<32, 256, 1, true>, k_conv_tc<64, 256, 1, true>};
         for (auto k : ks) SPC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BUDGET));
         configured |= 1ull << dev;
     }
@@ -1407,8 +1467,17 @@ static spc_status launch_tc(const ConvParams &p0, int mode, int out_kind, void *
         SPC_CUDA(launch_pdl_cluster(k, dim3(grid), dim3(TC_THREADS), smem, st, 2, p));
         return SPC_OK;
     }
-    void (*k)(ConvParams) = p.bm == 256 ? (p.BK == 64 ? k_conv_tc<64, 256, 1> : p.BK == 32 ? k_conv_tc<32, 256, 1> : k_conv_tc<16, 256, 1>)
-                                        : (p.BK == 64 ? k_conv_tc<64, 128, 1> : p.BK == 32 ? k_conv_tc<32, 128, 1> : k_conv_tc<16, 128, 1>);
+    // the fused BN / ReLU epilogue is a separate instantiation: its extra
+    // epilogue registers cost the plain kernel 2% of a C2 step when compiled in (A/B)
+    void (*k)(ConvParams);
+    if (out_kind == OUT_FINAL && epi_on(p.epi))
+        k = p.bm == 256 ? (p.BK == 64 ? k_conv_tc<64, 256, 1, true> : p.BK == 32 ? k_conv_tc<32, 256, 1, true>
+                                                                              : k_conv_tc<16, 256, 1, true>)
+                        : (p.BK == 64 ? k_conv_tc<64, 128, 1, true> : p.BK == 32 ? k_conv_tc<32, 128, 1, true>
+                                                                              : k_conv_tc<16, 128, 1, true>);
+    else
+        k = p.bm == 256 ? (p.BK == 64 ? k_conv_tc<64, 256, 1> : p.BK == 32 ? k_conv_tc<32, 256, 1> : k_conv_tc<16, 256, 1>)
+                        : (p.BK == 64 ? k_conv_tc<64, 128, 1> : p.BK == 32 ? k_conv_tc<32, 128, 1> : k_conv_tc<16, 128, 1>);
     SPC_CUDA(launch_pdl(k, dim3(grid), dim3(TC_THREADS), smem, st, p));
     return SPC_OK;
 }
@@ -1534,7 +1603,7 @@ extern "C" spc_status spc_conv_forward_ex(const spc_kmap *km, const void *f_in, 
         // scatter epilogue dominates there and the pair hand-off adds latency)
         const bool big_os = has_os && !has_ws && !km->n_out_dev &&
                             ((km->n_out + 255) / 256) * p.n_ntiles >= p.num_sms / 2;
-        p.cg = (pair_opt != 0 && wide && (big_os || pair_opt == 2)) ? 2 : 1;
+        p.cg = (pair_opt != 0 && wide && (big_os || pair_opt == 2) && !epi_on(p.epi)) ? 2 : 1;
     }
     p.tbufs = (p.bm == 256 ? 4 : 2) * p.tmem_cols <= 512 ? 2 : 1;
     p.kb_b = (uint32_t)(p.BN * p.BK * 2);

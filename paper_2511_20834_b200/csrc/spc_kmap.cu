@@ -898,8 +898,31 @@ struct DeferState {
     std::vector<OrderJob> orders;
     OrderScratch scratch{};    // density-order scratch of the batch
     int64_t order_rows = 0;    // its row capacity
+    bool flushed = false;      // a full batch was launched early (later maps: no density order)
+    bool batch_orders = false; // the current batch holds ordered maps (it owns the order scratch)
 };
 static thread_local DeferState g_defer;
+static spc_status launch_kmaps(const KmapBatch &b, int max_kd, int64_t tiles, cudaStream_t st);
+
+// a full batch (KM_MAX_MAPS maps, one grid-constant descriptor table) is launched as soon
+// as the next map arrives; the density-order key width is fixed by then, so maps added
+// after an early launch are built without a density order (they stay valid maps)
+static spc_status defer_flush(cudaStream_t st) {
+    KmapBatch &b = g_defer.b;
+    if (g_defer.batch_orders) {
+        if (!g_defer.scratch.ok) return fail(SPC_ERR_WORKSPACE, "network kmaps: density-order scratch too small");
+        b.ord_keys = g_defer.scratch.keys;
+        b.ord_total = g_defer.scratch.total;
+        b.ord_key_bits = ord_key_bits((int)g_defer.orders.size());
+    }
+    spc_status s = launch_kmaps(b, g_defer.max_kd, g_defer.tiles, st);
+    memset(&g_defer.b, 0, sizeof(g_defer.b));
+    g_defer.batch_orders = false;
+    g_defer.max_kd = 0;
+    g_defer.tiles = 0;
+    g_defer.flushed = true;
+    return s;
+}
 
 static void fill_desc(KmapDesc &d, const spc_kmap &km, const KmapPlan &pl, int32_t *bounds) {
     memset(&d, 0, sizeof(d));
@@ -1052,7 +1075,12 @@ static spc_status build_kmap(const void *in_keys, int64_t n_in, const int64_t *n
     OrderJob job;
     memset(&job, 0, sizeof(job));
     // a batch orders at most ORD_MAX maps (one tag each); later ones keep the canonical order
-    const bool order = wants_order(pl, flags) && n_out > 0 && (!g_defer.active || g_defer.orders.size() < ORD_MAX);
+    if (g_defer.active && g_defer.b.n_maps >= KM_MAX_MAPS) {
+        spc_status fs = defer_flush(st);
+        if (fs != SPC_OK) return fs;
+    }
+    const bool order = wants_order(pl, flags) && n_out > 0 &&
+                       (!g_defer.active || (g_defer.orders.size() < ORD_MAX && !g_defer.flushed));
     if (order) {
         km.os_rows = reinterpret_cast<int32_t *>(base + L.rows);
         km.os_table_ord = reinterpret_cast<int32_t *>(base + L.os_ord);
@@ -1082,7 +1110,6 @@ static spc_status build_kmap(const void *in_keys, int64_t n_in, const int64_t *n
         // network-wide phase 2: collect, launch once in kmap_defer_end()
         if (key_bytes != 8) return fail(SPC_ERR_UNSUPPORTED, "network-wide kernel maps use 64-bit keys");
         KmapBatch &b = g_defer.b;
-        if (b.n_maps >= KM_MAX_MAPS) return fail(SPC_ERR_CAPACITY, "too many distinct kernel maps in one batch");
         if (b.n_maps == 0) {
             b.key_bytes = 8;
             b.bits_y = spec.bits_y;
@@ -1098,6 +1125,7 @@ static spc_status build_kmap(const void *in_keys, int64_t n_in, const int64_t *n
         if (order) {
             d.ord_idx = (int32_t)g_defer.orders.size();
             g_defer.orders.push_back(job);
+            g_defer.batch_orders = true;
         }
         return SPC_OK;
     }
@@ -1165,6 +1193,8 @@ void kmap_defer_begin(void *scratch, size_t scratch_bytes, int64_t order_rows) {
     g_defer.tiles = 0;
     g_defer.orders.clear();
     g_defer.order_rows = order_rows;
+    g_defer.flushed = false;
+    g_defer.batch_orders = false;
     g_defer.scratch = order_rows > 0 ? order_scratch(scratch, scratch_bytes, order_rows) : OrderScratch{};
     g_defer.active = true;
 }
@@ -1184,7 +1214,7 @@ spc_status kmap_defer_end(cudaStream_t st) {
     g_defer.active = false;
     if (g_defer.b.n_maps == 0) return SPC_OK;
     KmapBatch &b = g_defer.b;
-    if (!g_defer.orders.empty()) {
+    if (g_defer.batch_orders) {   // (an earlier, flushed batch may own the ordered maps)
         if (!g_defer.scratch.ok) return fail(SPC_ERR_WORKSPACE, "network kmaps: density-order scratch too small");
         b.ord_keys = g_defer.scratch.keys;
         b.ord_total = g_defer.scratch.total;

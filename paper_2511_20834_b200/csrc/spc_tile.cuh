@@ -70,9 +70,9 @@ __device__ __forceinline__ void epi_affine_u32(const Epi &e, uint32_t (&v)[32], 
 
 // store 'n' (16 or 32) fp32 values of one row to the output (fully unrolled: registers only);
 // OUT_FINAL: + residual, then the epilogue's ReLU (its affine part was applied by the caller)
-template <class P>
+template <bool EPI = true, class P>
 __device__ __forceinline__ void store_row(const P &p, int64_t row, int col, const uint32_t (&v)[32], int n) {
-    const bool epi = p.out_kind == OUT_FINAL && p.epi.relu;
+    const bool epi = EPI && p.out_kind == OUT_FINAL && p.epi.relu;
     if (p.out_kind == OUT_FINAL && p.out_dtype != SPC_F32) {
         const uint4 *rp = p.residual
                               ? reinterpret_cast<const uint4 *>(static_cast<const uint16_t *>(p.residual) + row * p.ld_res + col)

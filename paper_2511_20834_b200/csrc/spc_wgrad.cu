@@ -37,7 +37,7 @@ constexpr int WG_PAIRS = 64;                 // pairs per stage (4 K=16 MMAs)
 constexpr int WG_M = 128;                    // c_in channels per item (TMEM lanes)
 constexpr int WG_ATOM = WG_PAIRS * 128;      // bytes of one 64-channel column of a stage
 constexpr int WG_MAX_SRC = 2 * SPC_MAX_KVOL + 1;
-constexpr int WG_MAX_STAGES = 8;
+constexpr int WG_MAX_STAGES = 12;
 constexpr int WG_SMEM_BUDGET = 210 * 1024;
 
 struct WgradParams {
@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_wgrad_tc(const __grid_constan
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < p.stages; ++s) {
-            ptx::mbar_init(ptx::smem_u32(&ws.full[s]), 128);   // one noinc arrival per gather thread
+            ptx::mbar_init(ptx::smem_u32(&ws.full[s]), 32);    // one noinc arrival per lane of the filling warp
             ptx::mbar_init(ptx::smem_u32(&ws.empty[s]), 1);    // MMA commit
         }
         for (int a = 0; a < 2; ++a) {
@@ -166,59 +166,126 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_wgrad_tc(const __grid_constan
     const int64_t n_items = ws.item_start[p.n_src];
 
     if (warp < 4) {
-        // ===================== gather (128 threads) =====================
-        uint32_t it = 0;
-        const int CB = p.NP / 8;   // 16-byte chunks of one B row
-        for (int64_t v = blockIdx.x; v < n_items; v += gridDim.x) {
-            const WItem w = decode_item(p, ws, v);
-            const int kind = p.src_kind[w.src], idx = p.src_idx[w.src];
-            const int m0 = w.mt * WG_M, n0 = w.nt * p.NP;
-            for (int64_t q0 = w.p0; q0 < w.p1; q0 += WG_PAIRS) {
-                if (!stage_active(p, w, q0)) continue;
-                const int s = it % p.stages;
-                ptx::mbar_wait(ptx::smem_u32(&ws.empty[s]), ((it / p.stages) & 1) ^ 1);
-                const uint32_t sA = ring_u32 + s * stage_bytes, sB = sA + p.a_bytes;
-                // this warp's 16 pairs: lane < 16 fetches (j, i) of pair q0 + 16*warp + lane
-                int j = -1, i = -1;
-                const int64_t q = q0 + 16 * warp + lane;
-                if (lane < 16 && q < w.p1) {
+        // ===================== gather (4 warps, one stage each, round-robin) =============
+        // channels past c_in / c_out are the same for every stage when the launch has one
+        // c_in / c_out tile (and the valid chunk count is a power of two): zero them in the
+        // whole ring once instead of zero-filling per stage
+        const bool pre_a = p.n_mt == 1 && p.c_in < WG_M && ((p.c_in / 8) & (p.c_in / 8 - 1)) == 0;
+        const bool pre_b = p.n_nt == 1 && p.c_out < p.NP && ((p.c_out / 8) & (p.c_out / 8 - 1)) == 0;
+        if (pre_a || pre_b) {
+            for (int s = 0; s < p.stages; ++s) {
+                uint4 *a = reinterpret_cast<uint4 *>(ring + s * stage_bytes);
+                for (int e = threadIdx.x; e < (int)(stage_bytes / 16); e += 128) {
+                    const bool in_a = e < (int)(p.a_bytes / 16);
+                    const int off = in_a ? e : e - (int)(p.a_bytes / 16);
+                    const int col = off / (WG_ATOM / 16), r = (off % (WG_ATOM / 16)) / 8, c16 = (off % 8) ^ (r & 7);
+                    const int ch = col * 8 + c16;   // 16-byte chunk (8 channels) of the row
+                    if ((in_a && pre_a && ch * 8 >= p.c_in) || (!in_a && pre_b && ch * 8 >= p.c_out))
+                        a[e] = make_uint4(0, 0, 0, 0);
+                }
+            }
+            ptx::fence_proxy_async();
+            asm volatile("bar.sync 2, 128;" ::: "memory");   // every producer's zeros before any arrival
+        }
+        const int a_sh = __ffs(pre_a ? p.c_in / 8 : 16) - 1;     // log2(chunks issued per A row)
+        const int b_sh = __ffs(pre_b ? p.c_out / 8 : p.NP / 8) - 1;
+        // cursor over the (item, active stage) sequence every role walks; warp w fills the
+        // stages it = w, w + 4, ... and prefetches its next stage's indices before issuing
+        struct Cur {
+            int64_t v, q0;
+            WItem w;
+        };
+        auto settle = [&](Cur &c) {   // move to the first active stage at or after c.q0
+            while (c.v < n_items) {
+                while (c.q0 < c.w.p1 && !stage_active(p, c.w, c.q0)) c.q0 += WG_PAIRS;
+                if (c.q0 < c.w.p1) return;
+                c.v += gridDim.x;
+                if (c.v < n_items) {
+                    c.w = decode_item(p, ws, c.v);
+                    c.q0 = c.w.p0;
+                }
+            }
+        };
+        auto step = [&](Cur &c, int n) {
+            for (int k = 0; k < n && c.v < n_items; ++k) {
+                c.q0 += WG_PAIRS;
+                settle(c);
+            }
+        };
+        // (j, i) of pairs q0 + lane and q0 + 32 + lane of the cursor's stage
+        auto fetch = [&](const Cur &c, int (&j)[2], int (&i)[2]) {
+            const int kind = p.src_kind[c.w.src], idx = p.src_idx[c.w.src];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                j[h] = -1;
+                i[h] = -1;
+                const int64_t q = c.q0 + 32 * h + lane;
+                if (q < c.w.p1) {
                     if (kind == 0) {
-                        j = __ldg(p.os + q * p.k_dense + idx);
-                        i = (int)q;
+                        j[h] = __ldg(p.os + q * p.k_dense + idx);
+                        i[h] = (int)q;
                     } else {
                         const int2 pr = __ldg(p.pairs + idx * p.list_stride + q);
-                        j = kind == 1 ? pr.x : pr.y;
-                        i = kind == 1 ? pr.y : pr.x;
+                        j[h] = kind == 1 ? pr.x : pr.y;
+                        i[h] = kind == 1 ? pr.y : pr.x;
                     }
                 }
-                // A: 16 pairs x 16 chunks (128 channels of F_in row j)
-#pragma unroll 4
-                for (int e = lane; e < 256; e += 32) {
-                    const int pp = e >> 4, ch = e & 15;
-                    const int jj = __shfl_sync(0xffffffffu, j, pp);
-                    const int r = 16 * warp + pp;
-                    const int ci = m0 + ch * 8;
-                    const bool ok = jj >= 0 && ci < p.c_in;
-                    const uint32_t dst = sA + (ch >> 3) * WG_ATOM + r * 128 + (((ch & 7) ^ (r & 7)) << 4);
-                    ptx::cp_async_16(dst, ok ? p.f_in + (int64_t)jj * p.ld_in_bytes + ci * 2 : p.f_in, ok ? 16u : 0u);
-                }
-                // B: 16 pairs x CB chunks (NP channels of dF_out row i); a sentinel pair
-                // contributes nothing, so its B row is zero-filled too (no load)
-                for (int e = lane; e < 16 * CB; e += 32) {
-                    const int pp = e / CB, ch = e - pp * CB;
-                    const int jj = __shfl_sync(0xffffffffu, j, pp);
-                    const int ii = __shfl_sync(0xffffffffu, i, pp);
-                    const int r = 16 * warp + pp;
-                    const int co = n0 + ch * 8;
-                    const bool ok = jj >= 0 && ii >= 0 && co < p.c_out;
-                    const uint32_t dst = sB + (ch >> 3) * WG_ATOM + r * 128 + (((ch & 7) ^ (r & 7)) << 4);
-                    ptx::cp_async_16(dst, ok ? p.d_out + (int64_t)ii * p.ld_dout_bytes + co * 2 : p.d_out,
-                                     ok ? 16u : 0u);
-                }
-                ptx::fence_proxy_async();
-                ptx::cp_async_mbar_arrive(ptx::smem_u32(&ws.full[s]));
-                ++it;
             }
+        };
+        Cur cur;
+        cur.v = blockIdx.x;
+        cur.q0 = 0;
+        if (cur.v < n_items) {
+            cur.w = decode_item(p, ws, cur.v);
+            cur.q0 = cur.w.p0;
+        }
+        settle(cur);
+        step(cur, warp);
+        uint32_t it = warp;
+        // indices of this warp's next two stages are in flight while it fills the current one
+        // (the pair lists / OS columns live in L2 or HBM: one stage of lead hid too little)
+        Cur nxt = cur;
+        step(nxt, 4);
+        int jn[2], in_[2], jn2[2], in2[2];
+        if (cur.v < n_items) fetch(cur, jn, in_);
+        if (nxt.v < n_items) fetch(nxt, jn2, in2);
+        while (cur.v < n_items) {
+            const Cur c = cur;
+            const int j[2] = {jn[0], jn[1]}, i[2] = {in_[0], in_[1]};
+            cur = nxt;
+            jn[0] = jn2[0], jn[1] = jn2[1], in_[0] = in2[0], in_[1] = in2[1];
+            step(nxt, 4);
+            if (nxt.v < n_items) fetch(nxt, jn2, in2);
+            const int s = it % p.stages;
+            ptx::mbar_wait(ptx::smem_u32(&ws.empty[s]), ((it / p.stages) & 1) ^ 1);
+            const uint32_t sA = ring_u32 + s * stage_bytes, sB = sA + p.a_bytes;
+            const int m0 = c.w.mt * WG_M, n0 = c.w.nt * p.NP;
+            // A: 64 pairs x 2^a_sh chunks (channels m0.. of F_in row j), pair-major across lanes
+            for (int e = lane; e < (64 << a_sh); e += 32) {
+                const int pp = e >> a_sh, ch = e & ((1 << a_sh) - 1);
+                const int lo = __shfl_sync(0xffffffffu, j[0], pp & 31), hi = __shfl_sync(0xffffffffu, j[1], pp & 31);
+                const int jj = pp < 32 ? lo : hi;
+                const int ci = m0 + ch * 8;
+                const bool ok = jj >= 0 && ci < p.c_in;
+                const uint32_t dst = sA + (ch >> 3) * WG_ATOM + pp * 128 + (((ch & 7) ^ (pp & 7)) << 4);
+                ptx::cp_async_16(dst, ok ? p.f_in + (int64_t)jj * p.ld_in_bytes + ci * 2 : p.f_in, ok ? 16u : 0u);
+            }
+            // B: 64 pairs x 2^b_sh chunks (channels n0.. of dF_out row i); a sentinel pair
+            // contributes nothing, so its B row is zero-filled too (no load)
+            for (int e = lane; e < (64 << b_sh); e += 32) {
+                const int pp = e >> b_sh, ch = e & ((1 << b_sh) - 1);
+                const int jl = __shfl_sync(0xffffffffu, j[0], pp & 31), jh = __shfl_sync(0xffffffffu, j[1], pp & 31);
+                const int il = __shfl_sync(0xffffffffu, i[0], pp & 31), ih = __shfl_sync(0xffffffffu, i[1], pp & 31);
+                const int jj = pp < 32 ? jl : jh, ii = pp < 32 ? il : ih;
+                const int co = n0 + ch * 8;
+                const bool ok = jj >= 0 && ii >= 0 && co < p.c_out;
+                const uint32_t dst = sB + (ch >> 3) * WG_ATOM + pp * 128 + (((ch & 7) ^ (pp & 7)) << 4);
+                ptx::cp_async_16(dst, ok ? p.d_out + (int64_t)ii * p.ld_dout_bytes + co * 2 : p.d_out,
+                                 ok ? 16u : 0u);
+            }
+            ptx::fence_proxy_async();
+            ptx::cp_async_mbar_arrive(ptx::smem_u32(&ws.full[s]));
+            it += 4;
         }
         ptx::cp_async_wait<0>();
     } else if (warp == 8) {
@@ -436,7 +503,7 @@ extern "C" spc_status spc_conv_wgrad(const spc_kmap *km, const void *f_in, int64
     }
     if (c_in % 16 || c_out % 16)
         return fail(SPC_ERR_UNSUPPORTED, "spc_conv_wgrad: f16/bf16 needs c_in and c_out multiples of 16");
-    p.NP = std::min(256, (c_out + 63) / 64 * 64);
+    p.NP = c_out <= 64 ? 64 : c_out <= 128 ? 128 : 256;   // power-of-two 16-byte chunks per B row
     p.n_nt = (c_out + p.NP - 1) / p.NP;
     p.n_mt = (c_in + WG_M - 1) / WG_M;
     p.a_bytes = 2 * WG_ATOM;
@@ -447,8 +514,9 @@ extern "C" spc_status spc_conv_wgrad(const spc_kmap *km, const void *f_in, int64
     p.idesc = ptx::umma_idesc_f16(in_dtype == SPC_BF16, WG_M, p.NP) | (1u << 15) | (1u << 16);
     // ~4 items per SM over the capacity's pairs (the live counts are smaller or equal)
     const int64_t est = (int64_t)ns * km->n_out * p.n_mt * p.n_nt;
+    const int64_t ipsm = std::max<int64_t>(1, option(SPC_OPT_WGRAD_ITEMS_PER_SM));
     p.range = (int)std::max<int64_t>(4 * WG_PAIRS,
-                                     std::min<int64_t>(64 * WG_PAIRS, est / (4 * sms) / WG_PAIRS * WG_PAIRS));
+                                     std::min<int64_t>(64 * WG_PAIRS, est / (ipsm * sms) / WG_PAIRS * WG_PAIRS));
     const size_t hdr = align_up(sizeof(WgradSmem), 1024);
     const size_t per = p.a_bytes + p.b_bytes;
     p.stages = (int)std::min<size_t>(WG_MAX_STAGES, (WG_SMEM_BUDGET - hdr) / per);

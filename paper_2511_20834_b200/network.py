@@ -132,6 +132,48 @@ def second_backbone_layers(K: int = 5, c_in_raw: int = 5):
     return L, widths, cur
 
 
+def ssa_buffers(layers, widths):
+    """Training: the forward list reuses buffers (h{l}, y{l}, p{l} at every
+    block of a level), but the weight gradient of layer i needs layer i's own input.  Give
+    every write that overlaps an earlier write of the same buffer a fresh version (reads and
+    residuals follow the latest version); disjoint column slices of one buffer -- the
+    decoder's concat of up-sampled features and the encoder skip -- stay one buffer."""
+    ver, written, out, w2 = {}, {}, [], dict(widths)
+
+    def cur(b):
+        return b if ver.get(b, 0) == 0 else f"{b}@{ver[b]}"
+
+    for s in layers:
+        src = cur(s.src)
+        res = (cur(s.residual[0]), s.residual[1]) if s.residual else None
+        d = cur(s.dst)
+        lo, hi = s.dst_col, s.dst_col + s.c_out
+        if any(lo < b and a < hi for a, b in written.get(d, [])):
+            ver[s.dst] = ver.get(s.dst, 0) + 1
+            d = cur(s.dst)
+            w2[d] = widths[s.dst]
+        written.setdefault(d, []).append((lo, hi))
+        out.append(dataclasses.replace(s, src=src, dst=d, residual=res))
+    return out, w2
+
+
+def dgrad_map_key(map_key):
+    """The map the data gradient of a layer runs on (spc.h, spc_prepare_weight_ex): a
+    submanifold layer's own map (mirrored weights), else the map of the opposite
+    direction (strided <-> transposed, same K and fine tensor stride)."""
+    K, stride, ts, tr = map_key
+    return map_key if stride == 1 else (K, stride, ts, 1 - tr)
+
+
+def wgrad_map_key(map_key):
+    """The map the weight gradient runs on: the same geometry with every offset weight-
+    stationary (t = 0; halved for submanifold maps), i.e. compact pair lists -- an OS
+    table would make the pair contraction walk every sentinel row."""
+    if map_key[0] == 1:
+        return map_key   # a K = 1 map has no sentinels (its only offset always matches)
+    return tuple(map_key) + ("ws",)
+
+
 def default_t(map_key):
     """Dataflow threshold per map before tuning (reading: the paper's UNet uses WS in most
     layers).  K=1 maps are always dense."""
@@ -148,7 +190,8 @@ class SparseNet:
     capacity n0 (all levels), so a pass is a fixed launch sequence (CUDA-graph capturable)."""
 
     def __init__(self, n0_cap: int, spec: spc.PackSpec, device="cuda", seed: int = 20834, t_override=None,
-                 nnz_per_out: float = 10.0, net: str = "minkunet42", density_order: bool = True):
+                 nnz_per_out: float = 10.0, net: str = "minkunet42", density_order: bool = True,
+                 train: bool = False):
         self.dev = torch.device(device)
         self.density_order = bool(density_order)
         self.early_maps = True   # layers >= 1 start their tile decode during the previous layer
@@ -163,23 +206,41 @@ class SparseNet:
             self.n_levels = 4
         else:
             raise ValueError(net)
+        self.train = bool(train)
+        if self.train:
+            self.layers, widths = ssa_buffers(self.layers, widths)
+            self.out_name = [s.dst for s in self.layers if s.dst.split("@")[0] == self.out_name][-1]
         self.map_keys = []
-        for s in self.layers:
-            if s.map_key not in self.map_keys:
-                self.map_keys.append(s.map_key)
-        self.t = {mk: (t_override or {}).get(mk, default_t(mk)) for mk in self.map_keys}
+        # forward maps first: a network build orders (SPC_KMAP_DENSITY_ORDER) the maps of its
+        # first grouped launch, and the training maps only add to a second one
+        keys = [s.map_key for s in self.layers]
+        if self.train:
+            keys += [dgrad_map_key(s.map_key) for s in self.layers] + [wgrad_map_key(s.map_key) for s in self.layers]
+        for mk in keys:
+            if mk not in self.map_keys:
+                self.map_keys.append(mk)
+        self.t = {mk: (t_override or {}).get(mk, default_t(mk)) for mk in self.map_keys if len(mk) == 4}
         # weights: seeded, bf16, prepared for the tcgen05 layout
         g = torch.Generator().manual_seed(seed)
-        self.weights = []
+        self.weights, self.raw_weights, self.dgrad_weights = [], [], []
         for s in self.layers:
             kv = s.map_key[0] ** 3
             a = math.sqrt(3.0 / (min(kv, nnz_per_out) * s.c_in_flops))
             w = (torch.rand(kv, s.c_in, s.c_out, generator=g) * 2 - 1) * a
             if s.c_in != s.c_in_flops:
                 w[:, s.c_in_flops:, :] = 0
-            self.weights.append(spc.spc_prepare_weight(w.to(self.dev, torch.bfloat16)))
+            wd = w.to(self.dev, torch.bfloat16)
+            self.weights.append(spc.spc_prepare_weight(wd))
+            if self.train:
+                self.raw_weights.append(wd)
+                self.dgrad_weights.append(spc.spc_prepare_weight_ex(
+                    wd, spc.SPC_WEIGHT_DGRAD_MIRROR if s.map_key[1] == 1 else spc.SPC_WEIGHT_DGRAD))
         # activations (capacity n0 rows for every level)
         self.bufs = {name: torch.zeros(self.n0, w, dtype=torch.bfloat16, device=self.dev) for name, w in widths.items()}
+        if self.train:   # gradient buffers (same layout as the activations) and fp32 dW per layer
+            self.gbufs = {name: torch.zeros_like(b) for name, b in self.bufs.items()}
+            self.dW = [torch.zeros(s.map_key[0] ** 3, s.c_in, s.c_out, dtype=torch.float32, device=self.dev)
+                       for s in self.layers]
         self.coords_ws = None
         self.keys = torch.empty(self.n0, dtype=torch.int64, device=self.dev)
         self.perm = torch.empty(self.n0, dtype=torch.int32, device=self.dev)
@@ -195,12 +256,12 @@ class SparseNet:
     def _geoms(self):
         geoms, ts, flags = [], [], []
         for mk in self.map_keys:
-            K, stride, tsd, tr = mk
+            K, stride, tsd, tr = mk[:4]
             geoms.append(spc.Geom(K, stride, 1, tsd, tr))
-            t = self.t[mk]
+            t = self.t[mk] if len(mk) == 4 else 0   # wgrad maps: all weight-stationary
             ts.append(t)
             f = spc.SPC_KMAP_HALVE_SYMMETRIC if (stride == 1 and K > 1) else 0
-            if self.density_order:
+            if self.density_order and len(mk) == 4:
                 f |= spc.SPC_KMAP_DENSITY_ORDER      # OS part only; ignored when t leaves no OS part
             flags.append(f)
         return geoms, ts, flags
@@ -215,6 +276,9 @@ class SparseNet:
         self.level_keys, self.level_n = self.netidx.level_keys, self.netidx.level_n
         self.maps = dict(zip(self.map_keys, kms))
         need = max(spc.spc_conv_workspace_size(self.maps[s.map_key], s.c_out) for s in self.layers)
+        if self.train:   # the data gradients write n_in x c_in through the dgrad maps
+            need = max([need] + [spc.spc_conv_workspace_size(self.maps[dgrad_map_key(s.map_key)], s.c_in)
+                                 for s in self.layers])
         if self.conv_ws is None or self.conv_ws.numel() < need:
             # zero once (spc.h ws contract), on the stream the convolutions run on
             self.conv_ws = spc._ws(need, self.dev, zero=True, stream=stream)
@@ -264,6 +328,42 @@ class SparseNet:
         finally:
             spc.spc_set_option(spc.SPC_OPT_CONV_MAPS_READY, 0)
         return self.bufs[self.out_name]
+
+    def backward(self, grad_out: torch.Tensor | None = None, stream=None):
+        """Training: the backward pass of the last forward.  grad_out: bf16
+        gradient of the output buffer (None: already in gbufs[out_name]).  Every layer in
+        reverse order: wgrad (spc_conv_wgrad into self.dW[i], zeroed first), the residual
+        branch (spc_add_rows), and the data gradient through the forward kernels on the
+        dgrad map (spc_conv_forward accumulating into the source gradient through its
+        residual operand).  The stem's input gradient is not formed.  Returns self.dW."""
+        if not self.train:
+            raise ValueError("SparseNet(train=True) is required for backward()")
+        st = stream if stream is not None else torch.cuda.current_stream(self.dev)
+        with torch.cuda.stream(st):
+            for name, g in self.gbufs.items():
+                if name != self.out_name or grad_out is not None:
+                    g.zero_()
+            for w in self.dW:
+                w.zero_()
+            if grad_out is not None:
+                self.gbufs[self.out_name][: grad_out.shape[0]].copy_(grad_out)
+        for i in reversed(range(len(self.layers))):
+            self.backward_layer(i, stream)
+        return self.dW
+
+    def backward_layer(self, i, stream=None):
+        s = self.layers[i]
+        g = self.gbufs[s.dst][:, s.dst_col:s.dst_col + s.c_out]
+        src = self.bufs[s.src][:, s.src_col:s.src_col + s.c_in]
+        spc.spc_conv_wgrad(self.maps[wgrad_map_key(s.map_key)], src, g, s.c_in, s.c_out, d_weight=self.dW[i],
+                           stream=stream)
+        if s.residual is not None:
+            rb, rc = s.residual
+            spc.spc_add_rows(self.gbufs[rb][:, rc:rc + s.c_out], g, stream=stream)
+        if i > 0:
+            gsrc = self.gbufs[s.src][:, s.src_col:s.src_col + s.c_in]
+            spc.spc_conv_forward(self.maps[dgrad_map_key(s.map_key)], g, self.dgrad_weights[i], s.c_out, s.c_in,
+                                 out=gsrc, residual=gsrc, ws=self.conv_ws, stream=stream)
 
     # ---------------------------------------------------------------------------------
     def algorithmic_flops(self) -> dict:

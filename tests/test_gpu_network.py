@@ -108,3 +108,57 @@ def test_network_index_levels_match_oracle():
     lv = _levels(coords, 5)
     ln = net.level_n.cpu().tolist()
     assert ln == [len(x) for x in lv]
+
+
+def _map_coords(lv, map_key):
+    K, stride, ts, tr = map_key
+    lf = int(round(math.log2(ts)))
+    if stride == 1:
+        return lv[lf], lv[lf], K, ts, False
+    if tr:
+        return lv[lf + 1], lv[lf], K, ts, True
+    return lv[lf], lv[lf + 1], K, ts, False
+
+
+@pytest.mark.parametrize("net_name", ["minkunet42", "secondk5"])
+def test_training_backward_every_layer(net_name):
+    """one forward + backward of the whole network (SparseNet(train=True):
+    buffers versioned per write, dgrad on the forward / opposite-direction maps, wgrad,
+    residual adds).  Every layer's weight gradient is recomputed by the oracle from the
+    GPU's own forward input and output gradient (fp64, <= 2e-3 max|ref|); every activation
+    gradient equals the sum the layer graph prescribes -- oracle dgrad of each reader plus
+    the residual gradients -- within the bf16 storage of the running sum (1e-2 max|ref|)."""
+    coords = synth.make_scan(1, 0)[:7000]
+    spec = spc.spc_plan_pack(coords[:, 1:].min(0), coords[:, 1:].max(0), 1, 16, 16)
+    net = SparseNet(coords.shape[0], spec, net=net_name, train=True)
+    c_raw = 5 if net_name.startswith("second") else 4
+    feats = torch.zeros(coords.shape[0], C_IN_PAD, dtype=torch.bfloat16, device="cuda")
+    feats[:, :c_raw] = torch.from_numpy(synth.make_features(coords.shape[0], c_raw, seed=3)).cuda().bfloat16()
+    net.forward(torch.from_numpy(coords).cuda(), feats)
+    gout = torch.from_numpy(synth.make_features(coords.shape[0], net.bufs[net.out_name].shape[1], seed=4)).cuda()
+    dW = net.backward(gout.bfloat16())
+    torch.cuda.synchronize()
+    lv = _levels(coords, net.n_levels)
+    host = lambda t, n: t[:n].float().cpu().numpy().astype(np.float64)
+    expect = {}   # (buffer) -> fp64 sum of every gradient contribution
+    for i, s in enumerate(net.layers):
+        inp, out, K, ts, tr = _map_coords(lv, s.map_key)
+        g = host(net.gbufs[s.dst][:, s.dst_col:s.dst_col + s.c_out], len(out))
+        src = host(net.bufs[s.src][:, s.src_col:s.src_col + s.c_in], len(inp))
+        ref_w = oracle.conv_wgrad(inp, out, K, ts, src, g, transposed=tr)
+        got_w = dW[i].cpu().numpy().astype(np.float64)
+        m = np.abs(ref_w).max()
+        assert np.abs(got_w - ref_w).max() <= 2e-3 * (m if m > 0 else 1), s.name
+        if i > 0:
+            W = _unpack_weight(net, i)
+            d = oracle.conv_dgrad(inp, out, K, ts, g, W, transposed=tr)
+            e = expect.setdefault(s.src, np.zeros((len(inp), net.gbufs[s.src].shape[1])))
+            e[:, s.src_col:s.src_col + s.c_in] += d
+        if s.residual is not None:
+            rb, rc = s.residual
+            e = expect.setdefault(rb, np.zeros((len(out), net.gbufs[rb].shape[1])))
+            e[:, rc:rc + s.c_out] += g
+    for name, ref in expect.items():
+        got = host(net.gbufs[name], ref.shape[0])
+        m = np.abs(ref).max()
+        assert np.abs(got - ref).max() <= 1e-2 * m, name

@@ -115,8 +115,8 @@ def test_sharded_stack_halo_exchange_emulated(R, dt):
     one_np = y1.float().cpu().numpy().astype(np.float64)
     # oracle chain (fp64, intermediates rounded like the GPU's stored dtype)
     x, outs = F.astype(np.float64), []
-    for i, (W, (_, _, ic, oc, _, tr)) in enumerate(zip(W64, geo)):
-        y = oracle.conv(ic, oc, 3, 1, x, W, transposed=tr)
+    for i, (W, (_, _, ic, oc, g, tr)) in enumerate(zip(W64, geo)):
+        y = oracle.conv(ic, oc, 3, g.tensor_stride, x, W, transposed=tr)
         if i == 2:
             y = oracle.bn_relu(y * 0.9 + 0.05, residual=outs[0], relu=True)
         y = synth.round_to(y.astype(np.float32), dt).astype(np.float64) if dt == "bf16" else y
