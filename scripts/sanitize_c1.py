@@ -40,4 +40,20 @@ for t, fl, ci, co, dt in ((-1, 0, 64, 256, torch.bfloat16), (2, 9, 32, 64, torch
     W = spc.spc_prepare_weight((torch.randn(K ** 3, ci, co, device=dev) * 0.05).to(dt))
     out = spc.spc_conv_forward(km, F, W, ci, co, out_dtype=torch.float32 if dt == torch.float32 else torch.bfloat16)
 torch.cuda.synchronize()
+# one training step (dgrad through the forward kernels, wgrad, residual adds)
+# and the fused BN / ReLU epilogue
+tnet = SparseNet(n, spec, device=dev, train=True)
+tnet.forward(c, feats)
+tnet.backward(torch.randn(n, tnet.bufs[tnet.out_name].shape[1], device=dev).bfloat16())
+km = spc.spc_build_kmap(keys, keys, spec, spc.Geom(3, 1, 1, 1, 0), 2, 9)
+F = torch.randn(n, 64, device=dev).bfloat16()
+W = spc.spc_prepare_weight((torch.randn(27, 64, 96, device=dev) * 0.05).bfloat16())
+sc, sh = torch.rand(96, device=dev) + 0.5, torch.randn(96, device=dev)
+spc.spc_conv_forward(km, F, W, 64, 96, out_dtype=torch.bfloat16, residual=torch.randn(n, 96, device=dev).bfloat16(),
+                     scale=sc, shift=sh, relu=True)
+for tt in (-1, 0):
+    kw = spc.spc_build_kmap(keys, keys, spec, spc.Geom(3, 1, 1, 1, 0), tt, 1)
+    spc.spc_conv_wgrad(kw, F, torch.randn(n, 96, device=dev).bfloat16(), 64, 96)
+    spc.spc_conv_wgrad(kw, F.float()[:, :32].contiguous(), torch.randn(n, 16, device=dev), 32, 16)
+torch.cuda.synchronize()
 print("sanitize target done", n)

@@ -48,8 +48,10 @@ for (ci, co) in [(16, 16), (16, 32), (32, 32), (64, 64), (128, 128), (256, 256)]
             o = torch.empty(out.shape[0], co, dtype=torch.bfloat16, device="cuda")
             l1max = 3 * (K - 1) // 2
             best = None
-            for t in range(0, l1max + 2):
+            for t, ordered in [(t, o) for t in range(0, l1max + 2) for o in ((False, True) if t > 0 else (False,))]:
                 fl = spc.SPC_KMAP_HALVE_SYMMETRIC if sl == 1 else 0
+                if ordered:   # the density order of the OS part (what the network bench builds)
+                    fl |= spc.SPC_KMAP_DENSITY_ORDER
                 km = spc.spc_build_kmap(inp, out, spec, g, t, fl)
                 nnz = int(km.counts()[:K ** 3].sum().item())
                 if sl == 1 and fl:   # halved maps do not count mirror offsets beyond the centre
@@ -57,7 +59,7 @@ for (ci, co) in [(16, 16), (16, 32), (32, 32), (64, 64), (128, 128), (256, 256)]
                 us_map = med(lambda: spc.spc_build_kmap(inp, out, spec, g, t, fl))
                 us_conv = med(lambda: spc.spc_conv_forward(km, F, W, ci, co, out=o, ws=ws))
                 fl_ = 2.0 * nnz * ci * co
-                kind = "WS" if t == 0 else ("OS" if t == l1max + 1 else f"hybrid t={t}")
+                kind = ("WS" if t == 0 else ("OS" if t == l1max + 1 else f"hybrid t={t}")) + (" +ord" if ordered else "")
                 r = {"c_in": ci, "c_out": co, "K": K, "stride": sl, "t": t, "dataflow": kind, "nnz": nnz,
                      "kmap_us": round(us_map, 1), "conv_us": round(us_conv, 1), "total_us": round(us_map + us_conv, 1),
                      "tflops": round(fl_ / (us_conv * 1e-6) / 1e12, 1), "k_dense": km.k_dense, "n_lists": km.n_lists}
@@ -66,7 +68,7 @@ for (ci, co) in [(16, 16), (16, 32), (32, 32), (64, 64), (128, 128), (256, 256)]
 os.makedirs(os.path.dirname(out_md) or ".", exist_ok=True)
 with open(out_md, "w") as f:
     f.write("# C5 layer sweep (B200, one KITTI-shaped scan, %d voxels; stride-2 outputs: %d)\n\n" % (keys.shape[0], n1))
-    f.write("kmap = spc_build_kmap; conv = spc_conv_forward (bf16 in/out, fp32 accumulate); TFLOP/s = 2 nnz Cin Cout / conv time.\n\n")
+    f.write("kmap = spc_build_kmap; conv = spc_conv_forward (bf16 in/out, fp32 accumulate); TFLOP/s = 2 nnz Cin Cout / conv time; +ord = SPC_KMAP_DENSITY_ORDER (the OS part in density order, as the network builds it; its kmap time includes the order).\n\n")
     f.write("| C_in | C_out | K | s | dataflow | kmap us | conv us | total us | TFLOP/s | best |\n|---|---|---|---|---|---|---|---|---|---|\n")
     groups = {}
     for r in rows:
