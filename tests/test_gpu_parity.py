@@ -98,6 +98,42 @@ def test_downsample_levels_bit_exact(config):
         np.testing.assert_array_equal(lv[l, :ln[l]].cpu().numpy(), _keys_of(ref, spec))
 
 
+@pytest.mark.parametrize("case", ["one_slab", "batched", "tiny", "live_count"])
+def test_downsample_segments_edge_cases(case):
+    """The segmented downsample sorts each (batch, x >> m) group of rows on its own: a group
+    with more distinct keys than the shared hash set holds (one x-slab of 60k voxels: the
+    global-memory path), groups split by the batch field, one- and two-voxel inputs, and a live count
+    below the capacity (rows past it ignored)."""
+    rng = np.random.default_rng(5)
+    if case == "one_slab":
+        yz = rng.choice(400 * 400, 60000, replace=False)   # level 1: ~34k distinct keys in one run
+        coords = np.stack([np.zeros(60000), np.full(60000, 3), yz // 400 - 200, yz % 400 - 200], 1).astype(np.int32)
+    elif case == "batched":
+        coords = np.concatenate([synth.make_scan(1, 0)[:5000] * np.array([0, 1, 1, 1]) + np.array([b, 0, 0, 0])
+                                 for b in range(4)]).astype(np.int32)
+    elif case == "tiny":
+        coords = np.array([[0, -3, 5, 1], [0, -4, 5, 1]], np.int32)
+    else:
+        coords = synth.make_scan(2, 0)
+    spec = _spec_for(coords)
+    keys, _, _ = _pack_sort(coords, spec)
+    n_live = len(keys)
+    if case == "live_count":   # the first 60000 sorted voxels as a live prefix of the capacity
+        n_live = 60000
+        c_sorted = oracle.sort_coords(coords)[0][:n_live]
+        n_dev = torch.tensor([n_live], dtype=torch.int64, device=DEV)
+        lv, ln = spc.spc_downsample(keys, spec, [1, 2, 3, 4], n_dev=n_dev)
+    else:
+        c_sorted = oracle.sort_coords(coords)[0]
+        lv, ln = spc.spc_downsample(keys, spec, [1, 2, 3, 4])
+    torch.cuda.synchronize()
+    ln = ln.cpu().numpy()
+    for l, m in enumerate([1, 2, 3, 4]):
+        ref = oracle.downsample(c_sorted, 2 ** m)
+        assert ln[l] == len(ref)
+        np.testing.assert_array_equal(lv[l, :ln[l]].cpu().numpy(), _keys_of(ref, spec))
+
+
 # ---------------------------------------------------------------------------------------
 # A4-A8 kernel maps
 # ---------------------------------------------------------------------------------------
