@@ -89,7 +89,9 @@ typedef enum {
                                    * row segments with bulk reductions (TMA); 0: red.global.add */
     SPC_OPT_WGRAD_ITEMS_PER_SM = 12, /* spc_conv_wgrad work items per SM over the map's pair
                                    * capacity (default 16: smaller items balance better)       */
-    SPC_OPT_COUNT = 13
+    SPC_OPT_CONV_SPLIT_TILES = 13, /* an OS launch splits its tiles' offsets over CTAs when
+                                   * 2 x (tiles x N-tiles) <= this (default 0: the SM count) */
+    SPC_OPT_COUNT = 14
 } spc_option;
 spc_status spc_set_option(int32_t option, int64_t value);
 int64_t spc_get_option(int32_t option);

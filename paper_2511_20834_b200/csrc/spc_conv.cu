@@ -1585,7 +1585,10 @@ extern "C" spc_status spc_conv_forward_ex(const spc_kmap *km, const void *f_in, 
     p.force_tr = (force_tr == 128 || force_tr == 256) ? (int)force_tr : 0;
     p.split_min_unit = (int)std::max<int64_t>(1, option(SPC_OPT_CONV_SPLIT_MIN));
     p.claim_ahead = (int)std::max<int64_t>(1, std::min<int64_t>(3, option(SPC_OPT_CONV_CLAIM_AHEAD)));
-    p.split_tiles_per_sm2 = p.num_sms;
+    {   // weighted split when 2 * tiles <= this (default: the SM count)
+        const int64_t st_opt = option(SPC_OPT_CONV_SPLIT_TILES);
+        p.split_tiles_per_sm2 = st_opt > 0 ? (int)st_opt : p.num_sms;
+    }
     // 256-row tiles (two MMAs per weight tile) whenever four accumulators fit TMEM; the
     // kernel drops to 128-row tiles on the device when the live row count is small
     p.bm = (4 * p.tmem_cols <= 512) ? 256 : 128;
