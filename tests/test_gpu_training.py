@@ -222,3 +222,37 @@ def test_training_step_full_c2_level0():
     rows = np.random.default_rng(0).choice(len(c), 2048, replace=False)
     ref = oracle.conv_dgrad_rows(c, c, rows, 3, 1, G, W)
     assert _rel(dF.cpu().numpy()[rows].astype(np.float64), ref) <= 2e-3
+
+
+@pytest.mark.parametrize("dt", ["bf16", "f32"])
+def test_add_rows_and_inplace_residual_accumulation(dt):
+    """spc_add_rows (the residual branch of a backward pass) on column slices with a live
+    count, and spc_conv_forward with residual == output (gradient accumulation): every
+    element read, then written, by one thread."""
+    tdt = TDT[dt]
+    rng = np.random.default_rng(1)
+    A = torch.from_numpy(rng.uniform(-1, 1, (500, 48)).astype(np.float32)).to(DEV).to(tdt)
+    B = torch.from_numpy(rng.uniform(-1, 1, (500, 40)).astype(np.float32)).to(DEV).to(tdt)
+    ref = A.float().clone()
+    n_dev = torch.tensor([300], dtype=torch.int64, device=DEV)
+    spc.spc_add_rows(A[:, 8:40], B[:, 0:32], n_dev=n_dev)
+    torch.cuda.synchronize()
+    ref[:300, 8:40] = (ref[:300, 8:40] + B[:300, 0:32].float()).to(tdt).float()
+    assert torch.equal(A.float(), ref)
+    # in-place accumulation through the conv's residual operand (OS, WS and hybrid maps)
+    spec, c, _ = _case(3000, seed=4)
+    k = _keys(c, spec)
+    for t, fl in ((-1, 8), (0, 1), (2, 1)):
+        km = spc.spc_build_kmap(k, k, spec, spc.Geom(3, 1, 1, 1, 0), t, fl)
+        F = synth.make_features(len(c), 32, seed=6, dtype=dt)
+        W = synth.make_weights(27, 32, 32, seed=7, nnz_per_out=8, dtype=dt)
+        G0 = synth.make_features(len(c), 32, seed=8, dtype=dt)
+        G = torch.from_numpy(G0).to(DEV).to(tdt)
+        spc.spc_conv_forward(km, torch.from_numpy(F).to(DEV).to(tdt), spc.spc_prepare_weight(torch.from_numpy(W).to(DEV).to(tdt)),
+                             32, 32, out=G, residual=G)
+        torch.cuda.synchronize()
+        ref = oracle.conv(c, c, 3, 1, F, W) + G0
+        got = G.float().cpu().numpy().astype(np.float64)
+        tol = 1e-5 if dt == "f32" else 2e-3
+        ulp = 0 if dt == "f32" else np.exp2(np.floor(np.log2(np.maximum(np.abs(ref), 1e-30))) - 7)
+        assert (np.abs(got - ref) <= ulp + tol * np.abs(ref).max()).all(), (t, fl)
