@@ -19,10 +19,10 @@
 // device, so no host sync).  Each item accumulates in TMEM and is reduced into the fp32
 // dW with red.global.add.v4.f32 (items of one offset overlap only through those adds).
 //
-//   warps 0-3  gather: cp.async 16-byte row segments (zero-fill for sentinels, pairs past
+//   warps 0-7  gather (one stage each, round-robin): cp.async 16-byte row segments (zero-fill for sentinels, pairs past
 //              the end and channels past c_in / c_out), completion on the stage mbarrier
-//   warps 4-7  epilogue: tcgen05.ld (thread = c_in row) -> red.global.add.v4.f32 into dW
-//   warp 8     TMEM allocation + MMA issue (tcgen05.mma kind::f16, M = 128, N = NP,
+//   warps 8-11 epilogue: tcgen05.ld (thread = c_in row) -> red.global.add.v4.f32 into dW
+//   warp 12    TMEM allocation + MMA issue (tcgen05.mma kind::f16, M = 128, N = NP,
 //              A and B MN-major SWIZZLE_128B), accumulators double-buffered across items
 #include <cuda_runtime.h>
 
@@ -32,7 +32,9 @@
 
 namespace spc {
 
-constexpr int WG_THREADS = 288;
+constexpr int WG_GATHER = 8;              // producer warps
+constexpr int WG_MMA_WARP = WG_GATHER + 4;
+constexpr int WG_THREADS = 32 * (WG_GATHER + 5);
 constexpr int WG_PAIRS = 64;                 // pairs per stage (4 K=16 MMAs)
 constexpr int WG_M = 128;                    // c_in channels per item (TMEM lanes)
 constexpr int WG_ATOM = WG_PAIRS * 128;      // bytes of one 64-channel column of a stage
@@ -144,7 +146,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_wgrad_tc(const __grid_constan
         ptx::fence_mbar_init();
         trace_event(p.trace, 0, 0);
     }
-    if (warp == 8) ptx::tmem_alloc(ptx::smem_u32(ws.tmem_holder), 2 * p.tmem_cols);
+    if (warp == WG_MMA_WARP) ptx::tmem_alloc(ptx::smem_u32(ws.tmem_holder), 2 * p.tmem_cols);
     pdl_wait();   // the map, its counts, F_in and dF_out come from preceding kernels
     pdl_trigger();
     if (threadIdx.x == 0) {
@@ -165,8 +167,8 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_wgrad_tc(const __grid_constan
     const uint32_t tmem_base = ws.tmem_holder[0];
     const int64_t n_items = ws.item_start[p.n_src];
 
-    if (warp < 4) {
-        // ===================== gather (4 warps, one stage each, round-robin) =============
+    if (warp < WG_GATHER) {
+        // ===================== gather (WG_GATHER warps, one stage each, round-robin) =====
         // channels past c_in / c_out are the same for every stage when the launch has one
         // c_in / c_out tile (and the valid chunk count is a power of two): zero them in the
         // whole ring once instead of zero-filling per stage
@@ -175,7 +177,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_wgrad_tc(const __grid_constan
         if (pre_a || pre_b) {
             for (int s = 0; s < p.stages; ++s) {
                 uint4 *a = reinterpret_cast<uint4 *>(ring + s * stage_bytes);
-                for (int e = threadIdx.x; e < (int)(stage_bytes / 16); e += 128) {
+                for (int e = threadIdx.x; e < (int)(stage_bytes / 16); e += 32 * WG_GATHER) {
                     const bool in_a = e < (int)(p.a_bytes / 16);
                     const int off = in_a ? e : e - (int)(p.a_bytes / 16);
                     const int col = off / (WG_ATOM / 16), r = (off % (WG_ATOM / 16)) / 8, c16 = (off % 8) ^ (r & 7);
@@ -185,7 +187,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_wgrad_tc(const __grid_constan
                 }
             }
             ptx::fence_proxy_async();
-            asm volatile("bar.sync 2, 128;" ::: "memory");   // every producer's zeros before any arrival
+            asm volatile("bar.sync 2, %0;" ::"n"(32 * WG_GATHER) : "memory");   // every producer's zeros before any arrival
         }
         const int a_sh = __ffs(pre_a ? p.c_in / 8 : 16) - 1;     // log2(chunks issued per A row)
         const int b_sh = __ffs(pre_b ? p.c_out / 8 : p.NP / 8) - 1;
@@ -240,12 +242,17 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_wgrad_tc(const __grid_constan
             cur.q0 = cur.w.p0;
         }
         settle(cur);
+        // a warp may run at most one ring phase ahead of its slot's previous user: with W
+        // producers filling stages round-robin that needs W <= stages (mbarrier parity waits
+        // cannot tell two phases apart)
+        const int WA = min(WG_GATHER, p.stages);
+        if (warp >= WA) cur.v = n_items;   // idle producer
         step(cur, warp);
         uint32_t it = warp;
         // indices of this warp's next two stages are in flight while it fills the current one
         // (the pair lists / OS columns live in L2 or HBM: one stage of lead hid too little)
         Cur nxt = cur;
-        step(nxt, 4);
+        step(nxt, WA);
         int jn[2], in_[2], jn2[2], in2[2];
         if (cur.v < n_items) fetch(cur, jn, in_);
         if (nxt.v < n_items) fetch(nxt, jn2, in2);
@@ -254,7 +261,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_wgrad_tc(const __grid_constan
             const int j[2] = {jn[0], jn[1]}, i[2] = {in_[0], in_[1]};
             cur = nxt;
             jn[0] = jn2[0], jn[1] = jn2[1], in_[0] = in2[0], in_[1] = in2[1];
-            step(nxt, 4);
+            step(nxt, WA);
             if (nxt.v < n_items) fetch(nxt, jn2, in2);
             const int s = it % p.stages;
             ptx::mbar_wait(ptx::smem_u32(&ws.empty[s]), ((it / p.stages) & 1) ^ 1);
@@ -285,10 +292,10 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_wgrad_tc(const __grid_constan
             }
             ptx::fence_proxy_async();
             ptx::cp_async_mbar_arrive(ptx::smem_u32(&ws.full[s]));
-            it += 4;
+            it += WA;
         }
         ptx::cp_async_wait<0>();
-    } else if (warp == 8) {
+    } else if (warp == WG_MMA_WARP) {
         // ===================== MMA issuer =====================
         uint32_t it = 0, ti = 0;
         const uint32_t tb = __shfl_sync(0xffffffffu, tmem_base, 0);
@@ -355,7 +362,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_wgrad_tc(const __grid_constan
     ptx::tc_fence_before();
     __syncthreads();
     if (threadIdx.x == 0) trace_event(p.trace, 7, 0);
-    if (warp == 8) {
+    if (warp == WG_MMA_WARP) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem_base, 2 * p.tmem_cols);
     }

@@ -219,6 +219,15 @@ def test_training_step_full_c2_level0():
     dF = spc.spc_conv_forward(km, Gg, Wp, 32, 32, out_dtype=torch.float32)
     torch.cuda.synchronize()
     assert _rel(dW.cpu().numpy().astype(np.float64), oracle.conv_wgrad(c, c, 3, 1, F, G)) <= 2e-3
+    # 96 -> 96 on the all-WS halved map the network's backward uses: 32 KB stages, so a
+    # ring of 6 stages for 8 producer warps (only 6 may run: the parity-skew limit)
+    kw = spc.spc_build_kmap(k, k, spec, spc.Geom(3, 1, 1, 1, 0), 0, 1)
+    F9 = synth.make_features(len(c), 96, seed=24)
+    G9 = synth.make_features(len(c), 96, seed=25)
+    dW9 = spc.spc_conv_wgrad(kw, torch.from_numpy(F9).to(DEV).bfloat16(), torch.from_numpy(G9).to(DEV).bfloat16(),
+                             96, 96)
+    torch.cuda.synchronize()
+    assert _rel(dW9.cpu().numpy().astype(np.float64), oracle.conv_wgrad(c, c, 3, 1, F9, G9)) <= 2e-3
     rows = np.random.default_rng(0).choice(len(c), 2048, replace=False)
     ref = oracle.conv_dgrad_rows(c, c, rows, 3, 1, G, W)
     assert _rel(dF.cpu().numpy()[rows].astype(np.float64), ref) <= 2e-3
