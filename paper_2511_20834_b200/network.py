@@ -194,6 +194,7 @@ class SparseNet:
                  train: bool = False):
         self.dev = torch.device(device)
         self.density_order = bool(density_order)
+        self.order_max_ts = 1 << 30   # density-order only maps whose fine tensor stride is <= this
         self.early_maps = True   # layers >= 1 start their tile decode during the previous layer
         self.spec = spec
         self.n0 = int(n0_cap)
@@ -261,7 +262,7 @@ class SparseNet:
             t = self.t[mk] if len(mk) == 4 else 0   # wgrad maps: all weight-stationary
             ts.append(t)
             f = spc.SPC_KMAP_HALVE_SYMMETRIC if (stride == 1 and K > 1) else 0
-            if self.density_order and len(mk) == 4:
+            if self.density_order and len(mk) == 4 and tsd <= self.order_max_ts:
                 f |= spc.SPC_KMAP_DENSITY_ORDER      # OS part only; ignored when t leaves no OS part
             flags.append(f)
         return geoms, ts, flags
