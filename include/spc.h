@@ -467,11 +467,12 @@ spc_status spc_prepare_weight_ex(const void *weight, int32_t k_vol, int32_t c_in
  * f16/bf16: tcgen05 per-offset gather-GEMM contracting over the pairs (MN-major operands,
  *          fp32 accumulation in TMEM, red.global.add into d_weight); c_in, c_out
  *          multiples of 16.  f32: FFMA.  Reduction order is not fixed (atomics). */
-/* dst[r][0..c) += src[r][0..c) for r < *n_dev (or n_cap): the residual branch of a
+/* dst[r][0..c) += src[r][0..c) (accumulate != 0) or = src[r][0..c) (accumulate == 0, the
+ * first contribution to a gradient) for r < *n_dev (or n_cap): the residual branch of a
  * backward pass (the gradient of out = conv + residual w.r.t. residual).  c % 8 == 0,
  * rows 16-byte aligned; dst and src must not overlap unless equal. */
 spc_status spc_add_rows(void *dst, int64_t ld_dst, const void *src, int64_t ld_src, int64_t n_cap,
-                        const int64_t *n_dev, int32_t c, int32_t dtype, void *stream);
+                        const int64_t *n_dev, int32_t c, int32_t dtype, int32_t accumulate, void *stream);
 spc_status spc_conv_wgrad(const spc_kmap *kmap, const void *f_in, int64_t ld_in, int32_t in_dtype,
                           int32_t c_in, const void *d_out, int64_t ld_dout, int32_t c_out, float *d_weight,
                           void *stream);

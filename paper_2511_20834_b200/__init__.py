@@ -164,7 +164,7 @@ def lib():
                                      ctypes.POINTER(Epilogue), P, SZ, P], ctypes.c_int),
             "spc_bn_fold": ([P, P, P, P, ctypes.c_float, I32, P, P, P], ctypes.c_int),
             "spc_prepare_weight_ex": ([P, I32, I32, I32, I32, I32, P, P], ctypes.c_int),
-            "spc_add_rows": ([P, I64, P, I64, I64, P, I32, I32, P], ctypes.c_int),
+            "spc_add_rows": ([P, I64, P, I64, I64, P, I32, I32, I32, P], ctypes.c_int),
             "spc_conv_wgrad": ([ctypes.POINTER(_Kmap), P, I64, I32, I32, P, I64, I32, P, P], ctypes.c_int),
             "spc_network_workspace_size": ([I64, I32, P, P, P, I32], SZ),
             "spc_shard_ranges": ([P, I64, P, P, I64, P, PackSpec, Geom, I32, P, P], ctypes.c_int),
@@ -562,10 +562,11 @@ def spc_conv_wgrad(km: KernelMap, f_in: torch.Tensor, d_out: torch.Tensor, c_in:
     return d_weight
 
 
-def spc_add_rows(dst: torch.Tensor, src: torch.Tensor, n_dev=None, stream=None):
-    """dst[:n] += src[:n] (row slices with their own strides; n = *n_dev or dst rows)."""
+def spc_add_rows(dst: torch.Tensor, src: torch.Tensor, n_dev=None, stream=None, accumulate: bool = True):
+    """dst[:n] += src[:n] (or = src[:n] when not accumulate; row slices with their own
+    strides; n = *n_dev or dst rows)."""
     _check(lib().spc_add_rows(_ptr(dst), dst.stride(0), _ptr(src), src.stride(0), dst.shape[0], _ptr(n_dev),
-                              dst.shape[1], _DT[dst.dtype], _stream(stream)), "spc_add_rows")
+                              dst.shape[1], _DT[dst.dtype], int(bool(accumulate)), _stream(stream)), "spc_add_rows")
     return dst
 
 

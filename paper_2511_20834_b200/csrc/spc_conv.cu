@@ -1268,7 +1268,7 @@ __global__ void k_transpose_weight_f32(const float *__restrict__ w, int k_vol, i
 // dst[r][0..c) += src[r][0..c) for the live rows (the residual branch of a backward pass);
 // 8 columns per work item, c a multiple of 8, rows 16-byte aligned
 __global__ void k_add_rows(void *__restrict__ dst, int64_t ld_dst, const void *__restrict__ src, int64_t ld_src,
-                           int64_t n_cap, const int64_t *n_dev, int c, int dtype) {
+                           int64_t n_cap, const int64_t *n_dev, int c, int dtype, int accumulate) {
     pdl_wait();
     pdl_trigger();
     const int64_t n = dev_count(n_cap, n_dev);
@@ -1280,14 +1280,22 @@ __global__ void k_add_rows(void *__restrict__ dst, int64_t ld_dst, const void *_
             float4 *d = reinterpret_cast<float4 *>(static_cast<float *>(dst) + r * ld_dst + col);
             const float4 *s = reinterpret_cast<const float4 *>(static_cast<const float *>(src) + r * ld_src + col);
             for (int q = 0; q < 2; ++q) {
-                float4 a = d[q];
                 const float4 b = s[q];
-                a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
-                d[q] = a;
+                if (accumulate) {
+                    float4 a = d[q];
+                    a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+                    d[q] = a;
+                } else {
+                    d[q] = b;
+                }
             }
         } else {
             uint4 *d = reinterpret_cast<uint4 *>(static_cast<uint16_t *>(dst) + r * ld_dst + col);
             const uint4 u = *reinterpret_cast<const uint4 *>(static_cast<const uint16_t *>(src) + r * ld_src + col);
+            if (!accumulate) {
+                *d = u;
+                continue;
+            }
             const uint4 w = *d;
             const uint32_t a[4] = {w.x, w.y, w.z, w.w}, b[4] = {u.x, u.y, u.z, u.w};
             uint32_t o[4];
@@ -1302,7 +1310,7 @@ __global__ void k_add_rows(void *__restrict__ dst, int64_t ld_dst, const void *_
 }
 
 extern "C" spc_status spc_add_rows(void *dst, int64_t ld_dst, const void *src, int64_t ld_src, int64_t n_cap,
-                                   const int64_t *n_dev, int32_t c, int32_t dtype, void *stream) {
+                                   const int64_t *n_dev, int32_t c, int32_t dtype, int32_t accumulate, void *stream) {
     SPC_CHECK_ARG(dst && src && c > 0 && c % 8 == 0 && ld_dst >= c && ld_src >= c, "bad arguments");
     SPC_CHECK_ARG(dtype >= SPC_F32 && dtype <= SPC_BF16, "bad dtype");
     const size_t es = dtype == SPC_F32 ? 4 : 2;
@@ -1312,7 +1320,8 @@ extern "C" spc_status spc_add_rows(void *dst, int64_t ld_dst, const void *src, i
     if (n_cap == 0) return SPC_OK;
     const int64_t work = n_cap * (c / 8);
     SPC_CUDA(launch_pdl(k_add_rows, dim3((unsigned)std::min<int64_t>((work + 255) / 256, 8 * 148)), dim3(256), 0,
-                        as_stream(stream), dst, ld_dst, src, ld_src, n_cap, n_dev, (int)c, (int)dtype));
+                        as_stream(stream), dst, ld_dst, src, ld_src, n_cap, n_dev, (int)c, (int)dtype,
+                        accumulate ? 1 : 0));
     SPC_LAUNCH_CHECK("k_add_rows");
     return SPC_OK;
 }

@@ -340,10 +340,11 @@ class SparseNet:
         if not self.train:
             raise ValueError("SparseNet(train=True) is required for backward()")
         st = stream if stream is not None else torch.cuda.current_stream(self.dev)
+        plan = self._first_touch()
         with torch.cuda.stream(st):
-            for name, g in self.gbufs.items():
+            for name in plan["zero"]:
                 if name != self.out_name or grad_out is not None:
-                    g.zero_()
+                    self.gbufs[name].zero_()
             for w in self.dW:
                 w.zero_()
             if grad_out is not None:
@@ -352,19 +353,73 @@ class SparseNet:
             self.backward_layer(i, stream)
         return self.dW
 
+    def _first_touch(self):
+        """Which gradient writes are the first to their region (they overwrite; later ones
+        accumulate), so the gradient buffers need no zero fill: regions are column slices of
+        a buffer; a buffer whose regions are read before fully written, or written partly
+        over an earlier region, is zeroed and accumulated into instead.  Static per layer
+        list (computed once)."""
+        if getattr(self, "_plan", None) is not None:
+            return self._plan
+        zero = set()
+        for attempt in range(2):
+            written = {self.out_name: [(0, self.gbufs[self.out_name].shape[1])]}
+            first_res, first_dgrad = {}, {}
+
+            def covered(name, lo, hi):
+                segs = sorted(written.get(name, []))
+                at = lo
+                for a, b in segs:
+                    if a > at:
+                        break
+                    at = max(at, b)
+                return at >= hi
+
+            def write(name, lo, hi):
+                segs = written.setdefault(name, [])
+                if name in zero:
+                    segs.append((lo, hi))
+                    return False
+                overlap = [s for s in segs if s[0] < hi and lo < s[1]]
+                if not overlap:
+                    segs.append((lo, hi))
+                    return True
+                if not covered(name, lo, hi):
+                    zero.add(name)   # partial overlap: zero the buffer, accumulate everywhere
+                segs.append((lo, hi))
+                return False
+
+            for i in reversed(range(len(self.layers))):
+                s = self.layers[i]
+                if s.dst not in zero and not covered(s.dst, s.dst_col, s.dst_col + s.c_out):
+                    zero.add(s.dst)   # a gradient read before anything wrote all of it
+                if s.residual is not None:
+                    rb, rc = s.residual
+                    first_res[i] = write(rb, rc, rc + s.c_out)
+                if i > 0:
+                    first_dgrad[i] = write(s.src, s.src_col, s.src_col + s.c_in)
+            if attempt == 0 and not zero:
+                break
+        # (the second attempt recomputes with the zeroed buffers forced to accumulate)
+        self._plan = {"zero": sorted(zero), "res": first_res, "dgrad": first_dgrad}
+        return self._plan
+
     def backward_layer(self, i, stream=None):
         s = self.layers[i]
+        plan = self._first_touch()
         g = self.gbufs[s.dst][:, s.dst_col:s.dst_col + s.c_out]
         src = self.bufs[s.src][:, s.src_col:s.src_col + s.c_in]
         spc.spc_conv_wgrad(self.maps[wgrad_map_key(s.map_key)], src, g, s.c_in, s.c_out, d_weight=self.dW[i],
                            stream=stream)
         if s.residual is not None:
             rb, rc = s.residual
-            spc.spc_add_rows(self.gbufs[rb][:, rc:rc + s.c_out], g, stream=stream)
+            spc.spc_add_rows(self.gbufs[rb][:, rc:rc + s.c_out], g, stream=stream, accumulate=not plan["res"][i],
+                             n_dev=self.level_n[s.level_out:s.level_out + 1])
         if i > 0:
             gsrc = self.gbufs[s.src][:, s.src_col:s.src_col + s.c_in]
+            first = plan["dgrad"][i]
             spc.spc_conv_forward(self.maps[dgrad_map_key(s.map_key)], g, self.dgrad_weights[i], s.c_out, s.c_in,
-                                 out=gsrc, residual=gsrc, ws=self.conv_ws, stream=stream)
+                                 out=gsrc, residual=None if first else gsrc, ws=self.conv_ws, stream=stream)
 
     # ---------------------------------------------------------------------------------
     def algorithmic_flops(self) -> dict:
