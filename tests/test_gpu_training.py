@@ -248,6 +248,11 @@ def test_add_rows_and_inplace_residual_accumulation(dt):
     torch.cuda.synchronize()
     ref[:300, 8:40] = (ref[:300, 8:40] + B[:300, 0:32].float()).to(tdt).float()
     assert torch.equal(A.float(), ref)
+    # the first contribution to a gradient overwrites (accumulate = 0)
+    spc.spc_add_rows(A[:, 0:16], B[:, 16:32], n_dev=n_dev, accumulate=False)
+    torch.cuda.synchronize()
+    ref[:300, 0:16] = B[:300, 16:32].float()
+    assert torch.equal(A.float(), ref)
     # in-place accumulation through the conv's residual operand (OS, WS and hybrid maps)
     spec, c, _ = _case(3000, seed=4)
     k = _keys(c, spec)
