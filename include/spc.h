@@ -67,7 +67,7 @@ size_t spc_kmap_struct_bytes(void);        /* sizeof(spc_kmap), for binding layo
  * Returns SPC_ERR_INVALID_ARG for an unknown option. */
 typedef enum {
     SPC_OPT_CONV_TILE_ROWS = 0,   /* 0 = device heuristic (default); 128 / 256 force the OS/WS tile rows */
-    SPC_OPT_CONV_STAGE_KB = 1,    /* pipeline stage size cap in KB (default 72)                   */
+    SPC_OPT_CONV_STAGE_KB = 1,    /* pipeline stage size cap in KB (default 72; 256-wide pairs 48)*/
     SPC_OPT_CONV_OS_SPLIT = 2,    /* 1 (default): small OS launches split a tile's offsets over CTAs */
     SPC_OPT_CONV_SPLIT_MIN = 3,   /* minimum offsets per split part (default 2)                   */
     SPC_OPT_CONV_CLAIM_AHEAD = 4, /* dynamic tile claims ahead of the gather warps, 1..3 (default 1) */

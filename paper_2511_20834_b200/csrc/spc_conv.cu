@@ -1432,7 +1432,12 @@ static spc_status launch_tc(const ConvParams &p0, int mode, int out_kind, void *
     const size_t avail = TC_SMEM_BUDGET - 1024 - header;   // 1024: alignment slack of the dynamic smem base
     // slices (one BK-channel chunk of one offset) per pipeline stage: a stage carries up
     // to ~72 KB so narrow layers pack several offsets into one stage
-    const size_t stage_cap = (size_t)std::max<int64_t>(8, option(SPC_OPT_CONV_STAGE_KB)) * 1024;
+    // default stage cap 72 KB; CTA pairs with 256-wide outputs default to 48 KB stages: a
+    // deeper ring measured 2.7% faster on 256x256 (146 vs 150 us, tensor pipe 48.0% vs 46.5%
+    // of elapsed, 51.4% vs 49.2% of active cycles; profiles/r2_wide_256_256_pair_stage48.txt),
+    // while 192-wide pairs lose 16% with it (110.6 vs 95.0 us)
+    const int64_t skb = option(SPC_OPT_CONV_STAGE_KB);
+    const size_t stage_cap = (size_t)std::max<int64_t>(8, (p.cg == 2 && p.BN == 256 && skb == 72) ? 48 : skb) * 1024;
     size_t ring_bytes = 0;
     for (int g = 0; g < 2; ++g) {
         const int rows = g == 0 ? p.bm : TC_BM;
