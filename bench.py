@@ -64,6 +64,9 @@ def parse():
     ap.add_argument("--net", default=None, choices=["minkunet42_k2"],
                     help="C2/C4 variant: TorchSparse's MinkUNet layer set with K=2 stride-2 down/up (SURVEY NEXT-3)")
     ap.add_argument("--profile-layers", action="store_true", help="print the per-layer table to stderr")
+    ap.add_argument("--no-pipeline", action="store_true",
+                    help="time one scan at a time (default: two scans in flight -- the indexing of scan i+1 "
+                         "on its own stream overlaps the feature computation of scan i)")
     return ap.parse_args()
 
 
@@ -565,16 +568,32 @@ def main():
             graph = None
             torch.cuda.synchronize()
 
-    def step():
-        if graph is not None:
+    # ---- two scans in flight: a second network instance (same weights, maps, t) so that
+    # step i computes the features of scan i on one stream while the voxel indexing of scan
+    # i+1 runs on another; two graphs alternate the instances -------------------------------
+    nets, pgraphs = [net], None
+    if graph is not None and not args.no_pipeline:
+        net2 = SparseNet(n, spec, device=dev, net=net_name, density_order=not args.no_order)
+        net2.set_t(dict(net.t))
+        for _ in range(3):
+            net2.forward(coords, feats, stream=stream)
+        torch.cuda.synchronize()
+        nets = [net, net2]
+        from paper_2511_20834_b200.network import capture_pipeline
+        pgraphs = capture_pipeline(nets, [(coords, feats), (coords, feats)], dev, stream)
+
+    def step(i=0):
+        if pgraphs is not None:
+            pgraphs[i % 2].replay()
+        elif graph is not None:
             graph.replay()
         else:
             net.forward(coords, feats, stream=stream)
 
     # L2 flush buffer (> 126 MB L2) written between timed iterations
     flush = torch.empty(320 * 2 ** 20, dtype=torch.uint8, device=dev)
-    for _ in range(args.warmup):
-        step()
+    for i in range(args.warmup):
+        step(i)
     torch.cuda.synchronize()
 
     # ---- timed region -------------------------------------------------------------------
@@ -587,7 +606,7 @@ def main():
         for i in range(args.steps):
             flush.fill_(i & 0xFF)
             starts[i].record(stream)
-            step()
+            step(i)
             ends[i].record(stream)
         torch.cuda.synchronize()
     if world > 1:
@@ -599,6 +618,21 @@ def main():
         t_total = max_over_ranks(t_total, device=dev)
     total_scans = 8 if args.config == 4 else world
     value = total_scans * args.steps / t_total
+    sequential = None
+    if pgraphs is not None:   # one scan at a time, for reference (same graph, L2 flush, events)
+        ns = min(args.steps, 50)
+        s_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(ns)]
+        for i in range(ns):
+            flush.fill_(i & 0xFF)
+            s_ev[i][0].record(stream)
+            graph.replay()
+            s_ev[i][1].record(stream)
+        torch.cuda.synchronize()
+        seq_s = float(np.sum([a.elapsed_time(b) for a, b in s_ev])) / 1e3
+        if world > 1:
+            from paper_2511_20834_b200.distributed import max_over_ranks
+            seq_s = max_over_ranks(seq_s, device=dev)
+        sequential = {"value": total_scans * ns / seq_s, "ms_per_step": seq_s / ns * 1e3, "steps": ns}
     clocks = clk.summary()
     gather_ms = None
     if args.config == 4 and world > 1:
@@ -639,7 +673,10 @@ def main():
 
     # ---- end to end through the public API: pinned host in -> device -> pinned host out --
     # every rank runs its own pipelined loop; the job's time is the slowest rank's
-    e2e = end_to_end(net, coords_np, feats_np, dev, stream, args.steps, flush, graph, coords, feats)
+    if pgraphs is not None:
+        e2e = end_to_end_pipelined(nets, coords_np, feats_np, dev, stream, args.steps, flush)
+    else:
+        e2e = end_to_end(net, coords_np, feats_np, dev, stream, args.steps, flush, graph, coords, feats)
     e2e_s = e2e["seconds"]
     if world > 1:
         from paper_2511_20834_b200.distributed import max_over_ranks
@@ -660,6 +697,10 @@ def main():
                        "parallelism": f"scan-sharded x{world}",
                        "l2": "flushed (320 MB write) between timed steps; e2e: a 160 MB write before every forward",
                        "cuda_graph": graph is not None, "dataflow_t": {str(k): v for k, v in net.t.items()},
+                       "pipeline": ("two scans in flight: the voxel indexing of scan i+1 (its own stream and "
+                                    "network instance) overlaps the feature computation of scan i; every step "
+                                    "indexes one scan and convolves one scan") if pgraphs is not None else
+                                   "one scan at a time",
                        "pack_spec": list(spec.astuple())},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak,
@@ -675,6 +716,7 @@ def main():
                          "algorithmic_gflop_per_step": total_flop / 1e9, "conv_ms_per_step": conv_ms,
                          "index_ms_per_step": index_ms},
             "clocks": clocks,
+            "sequential": sequential,
             "e2e": {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"],
                     "ms_per_step": e2e["ms"]} if e2e else None,
             "gpu_launches": launches["total"],
@@ -843,6 +885,82 @@ def top_kernel_share(launches):
     tot = sum(dur.values()) or 1.0
     return sorted([{"kernel": k, "launches": launches["by_kernel"][k], "share": v / tot}
                    for k, v in dur.items()], key=lambda r: -r["share"])[:6]
+
+
+def end_to_end_pipelined(nets, coords_np, feats_np, dev, stream, steps, flush):
+    """The public-API serving loop with two scans in flight: every step copies one scan's
+    coords + features from pinned host memory, indexes it (nets[(i+1) % 2].index_stage) while
+    the previous scan's features are computed (nets[i % 2].conv_stage), and reads that scan's
+    output back to pinned host memory.  Copies run on their own streams, double-buffered
+    (landing buffers per instance; each instance's own output buffer is read directly); L2
+    flushed (a 160 MB write) before every step; timed from the first host->device copy to the
+    last device->host copy."""
+    import torch
+    from paper_2511_20834_b200.network import C_IN_PAD
+    n = coords_np.shape[0]
+    h_coords = torch.from_numpy(coords_np).pin_memory()
+    f16 = np.zeros((n, C_IN_PAD), np.float32)
+    f16[:, :feats_np.shape[1]] = feats_np
+    h_feats = torch.from_numpy(f16).to(torch.bfloat16).pin_memory()
+    land = [(torch.empty_like(h_coords, device=dev), torch.empty_like(h_feats, device=dev)) for _ in range(2)]
+    for c, f in land:
+        c.copy_(h_coords)
+        f.copy_(h_feats)
+    outs = [nt.bufs[nt.out_name] for nt in nets]
+    h_out = [torch.empty(outs[0].shape, dtype=outs[0].dtype).pin_memory() for _ in range(2)]
+    from paper_2511_20834_b200.network import capture_pipeline
+    graphs = capture_pipeline(nets, land, dev, stream)
+    fl = flush[:160 * 2 ** 20]
+    cs_in, cs_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    total = steps + 2
+    ev = lambda: torch.cuda.Event()
+    h2d_done = [ev() for _ in range(total + 2)]
+    step_done = [ev() for _ in range(total)]
+    d2h_done = [ev() for _ in range(total)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def h2d(j):   # scan j into land[j % 2] (read by the index stage of step j - 1)
+        with torch.cuda.stream(cs_in):
+            if j >= 3:
+                cs_in.wait_event(step_done[j - 3])   # step j-3 indexed scan j-2 from this buffer
+            elif j == 2:
+                cs_in.wait_event(fill_done)          # the fill indexed scan 0 from this buffer
+            land[j % 2][0].copy_(h_coords, non_blocking=True)
+            land[j % 2][1].copy_(h_feats, non_blocking=True)
+            h2d_done[j].record(cs_in)
+
+    def d2h(i):   # scan i's output, computed by step i in nets[i % 2]
+        with torch.cuda.stream(cs_out):
+            cs_out.wait_event(step_done[i])
+            h_out[i % 2].copy_(outs[i % 2], non_blocking=True)
+            d2h_done[i].record(cs_out)
+
+    torch.cuda.synchronize()
+    # pipeline fill: scan 0 indexed outside the loop (eagerly, from its landing buffer)
+    h2d(0)
+    h2d(1)
+    stream.wait_event(h2d_done[0])
+    nets[0].index_stage(land[0][0], land[0][1], stream)
+    fill_done = ev()
+    fill_done.record(stream)
+    for i in range(total):
+        if i == 2:                                    # two pipeline-fill steps are not timed
+            torch.cuda.synchronize()
+            t0.record(cs_in)
+        h2d(i + 2)
+        stream.wait_event(h2d_done[i + 1])            # the scan this step indexes has landed
+        if i >= 2:
+            stream.wait_event(d2h_done[i - 2])        # this instance's output was read out
+        with torch.cuda.stream(stream):
+            fl.fill_(i & 0xFF)
+            graphs[i % 2].replay()
+            step_done[i].record(stream)
+        d2h(i)
+    t1.record(cs_out)
+    torch.cuda.synchronize()
+    t = t0.elapsed_time(t1) / 1e3
+    return {"value": steps / t, "seconds": t, "ms": t / steps * 1e3, "h2d": int(h_coords.numel() * 4 + h_feats.numel() * 2),
+            "d2h": int(outs[0].numel() * 2)}
 
 
 def end_to_end(net, coords_np, feats_np, dev, stream, steps, flush, graph=None, coords=None, feats=None):

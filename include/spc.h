@@ -91,7 +91,9 @@ typedef enum {
                                    * capacity (default 16: smaller items balance better)       */
     SPC_OPT_CONV_SPLIT_TILES = 13, /* an OS launch splits its tiles' offsets over CTAs when
                                    * 2 x (tiles x N-tiles) <= this (default 0: the SM count) */
-    SPC_OPT_COUNT = 14
+    SPC_OPT_CONV_MAX_CTAS = 14,   /* > 0: the persistent feature kernels use at most this many
+                                   * CTAs (one per SM), leaving SMs to a concurrent stream     */
+    SPC_OPT_COUNT = 15
 } spc_option;
 spc_status spc_set_option(int32_t option, int64_t value);
 int64_t spc_get_option(int32_t option);

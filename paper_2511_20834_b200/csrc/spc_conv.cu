@@ -1471,6 +1471,8 @@ static spc_status launch_tc(const ConvParams &p0, int mode, int out_kind, void *
                                               (p.split_ok ? std::max(1, p.k_dense / 2) : 1)
                                         : (int64_t)num_sms();
     int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles_cap, num_sms()));
+    const int64_t cap = option(SPC_OPT_CONV_MAX_CTAS);   // SMs left to a concurrent stream
+    if (cap > 0) grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid, cap));
     if (p.cg == 2) grid = 2 * std::max(1, std::min(grid, num_sms()) / 2);   // whole CTA pairs
     p.trace = trace_next(std::string("k_conv_tc ") + (mode == 0 ? "os" : "ws") + (p.cg == 2 ? " pair" : "") +
                          " n_out=" + std::to_string(p.n_out_cap) + " c_in=" + std::to_string(p.n_chunks * p.BK) +

@@ -246,7 +246,8 @@ spc_status dense_forward(const void *f_in, int64_t ld_in, int in_dtype, int c_in
         configured |= 1ull << dev;
     }
     const int64_t tiles_cap = ((n_cap + DN_BM - 1) / DN_BM) * p.n_ntiles;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles_cap, num_sms()));
+    int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles_cap, num_sms()));
+    if (option(SPC_OPT_CONV_MAX_CTAS) > 0) grid = (int)std::min<int64_t>(grid, option(SPC_OPT_CONV_MAX_CTAS));
     p.trace = trace_next("k_dense_tc n=" + std::to_string(n_cap) + " c_in=" + std::to_string(c_in) +
                          " c_out=" + std::to_string(c_out) + " k=" + std::to_string(k));
     SPC_CUDA(launch_pdl(k_dense_tc, dim3(grid), dim3(DN_THREADS), smem, st, p));

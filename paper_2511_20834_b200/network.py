@@ -316,10 +316,21 @@ class SparseNet:
             st = stream if stream is not None else torch.cuda.current_stream(self.dev)
             with torch.cuda.stream(st):
                 n_live.fill_(n)
+        self.index_stage(coords, feats, stream, n_live)
+        return self.conv_stage(stream)
+
+    def index_stage(self, coords: torch.Tensor, feats: torch.Tensor, stream=None, n_live=None):
+        """The voxel-indexing half of forward(): pack + sort, feature row gather, every
+        level and every kernel map (n_live: as in forward, already filled)."""
+        n = coords.shape[0]
         spc.spc_pack_sort(coords, self.spec, status=self.status, keys_out=self.keys[:n], perm_out=self.perm[:n],
                           ws=self.sort_ws, stream=stream, n_dev=n_live)
         spc.spc_gather_rows(feats, self.perm[:n], out=self.bufs["x0"][:n], n_dev=n_live, stream=stream)
         self.index(stream, n_dev=n_live)
+
+    def conv_stage(self, stream=None) -> torch.Tensor:
+        """The feature-computation half of forward(): every layer on the maps of the last
+        index_stage()."""
         try:
             for i in range(len(self.layers)):
                 # after the first layer the maps and weights are long complete when the
@@ -473,6 +484,35 @@ class SparseNet:
     def nnz_per_out(self) -> dict:
         """Matches per output voxel of every distinct map (call after algorithmic_flops())."""
         return {mk: self.nnz[mk] / max(1, self.live_n[mk][1]) for mk in self.maps}
+
+
+def capture_pipeline(nets, inputs, dev, stream):
+    """Two CUDA graphs of a pipelined step: graph p runs nets[p].conv_stage (features of the
+    scan nets[p] indexed in the previous step) on one stream and nets[1-p].index_stage on
+    inputs[1-p] (the next scan) on another, forked from and joined into the capture stream."""
+    s0, s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    s0.wait_stream(stream)
+    graphs = []
+    for p in range(2):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s0):
+            fork = torch.cuda.Event()
+            fork.record(s0)
+            s1.wait_event(fork)
+            s2.wait_event(fork)
+            with torch.cuda.stream(s1):
+                nets[p].conv_stage(s1)
+            with torch.cuda.stream(s2):
+                c, f = inputs[1 - p]
+                nets[1 - p].index_stage(c, f, s2)
+            j1, j2 = torch.cuda.Event(), torch.cuda.Event()
+            j1.record(s1)
+            j2.record(s2)
+            s0.wait_event(j1)
+            s0.wait_event(j2)
+        torch.cuda.synchronize()
+        graphs.append(g)
+    return graphs
 
 
 class SparseUNet(SparseNet):

@@ -1,0 +1,98 @@
+"""Two scans in flight (serving pipeline probe): step i runs the feature computation of
+scan i on at most `cap` SMs (SPC_OPT_CONV_MAX_CTAS) while the voxel indexing of scan i+1
+runs on another stream; two SparseNet instances alternate.  Captured as two CUDA graphs
+(one per parity), L2 flushed before every step, CUDA events; compared with the sequential
+forward.  python scripts/pipeline_probe.py [--config 2] [--caps 0 136 128 120]"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import bench  # noqa: E402
+import paper_2511_20834_b200 as spc  # noqa: E402
+from paper_2511_20834_b200.network import SparseNet, C_IN_PAD  # noqa: E402
+
+
+def timed(replays, flush, n=40):
+    ts = []
+    for i in range(n):
+        flush.fill_(i & 0xFF)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        replays[i % len(replays)].replay()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return float(np.median(ts[4:]))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--caps", type=int, nargs="+", default=[0, 144, 140, 136])
+    args = ap.parse_args()
+    dev = torch.device("cuda")
+    coords_np, feats_np, _, net_name = bench.workload(0, args.config)
+    spec = bench.spec_for(coords_np)
+    t_map = bench.load_t(os.path.join(ROOT, "profiles", "r2_tuned_t_c2.json")) if args.config == 2 else None
+    nets = []
+    for _ in range(2):
+        net = SparseNet(coords_np.shape[0], spec, net=net_name)
+        if t_map:
+            net.set_t(t_map)
+        nets.append(net)
+    coords = torch.from_numpy(coords_np).to(dev)
+    feats = torch.zeros(coords_np.shape[0], C_IN_PAD, dtype=torch.bfloat16, device=dev)
+    feats[:, :feats_np.shape[1]] = torch.from_numpy(feats_np).to(dev).bfloat16()
+    for net in nets:
+        for _ in range(2):
+            net.forward(coords, feats)
+    torch.cuda.synchronize()
+    flush = torch.empty(320 * 2 ** 20, dtype=torch.uint8, device=dev)
+    s0, s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    # sequential reference: one graph of the whole forward
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s0):
+        nets[0].forward(coords, feats, stream=s0)
+    torch.cuda.synchronize()
+    res = {"sequential_ms": timed([g], flush)}
+    ref = nets[0].bufs[nets[0].out_name].float().clone()
+    g.replay()
+    torch.cuda.synchronize()
+    # fp32 atomics in the weight-stationary layers: runs agree to rounding, not bit-for-bit
+    res["sequential_run_to_run_maxdiff"] = float((nets[0].bufs[nets[0].out_name].float() - ref).abs().max())
+    for cap in args.caps:
+        graphs = []
+        for p in range(2):
+            gp = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gp, stream=s0):
+                e0 = torch.cuda.Event()
+                e0.record(s0)
+                s1.wait_event(e0)
+                s2.wait_event(e0)
+                spc.spc_set_option(spc.SPC_OPT_CONV_MAX_CTAS, cap)
+                with torch.cuda.stream(s1):
+                    nets[p].conv_stage(s1)
+                spc.spc_set_option(spc.SPC_OPT_CONV_MAX_CTAS, -1)
+                with torch.cuda.stream(s2):
+                    nets[1 - p].index_stage(coords, feats, s2)
+                e1, e2 = torch.cuda.Event(), torch.cuda.Event()
+                e1.record(s1)
+                e2.record(s2)
+                s0.wait_event(e1)
+                s0.wait_event(e2)
+            torch.cuda.synchronize()
+            graphs.append(gp)
+        res[f"pipelined_ms_cap{cap}"] = timed(graphs, flush)
+        d = max(float((nets[q].bufs[nets[q].out_name].float() - ref).abs().max()) for q in range(2))
+        res[f"maxdiff_cap{cap}"] = d
+    print(json.dumps({"config": args.config, "n": int(coords_np.shape[0]), **res}))
+
+
+if __name__ == "__main__":
+    main()

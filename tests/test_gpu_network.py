@@ -162,3 +162,40 @@ def test_training_backward_every_layer(net_name):
         got = host(net.gbufs[name], ref.shape[0])
         m = np.abs(ref).max()
         assert np.abs(got - ref).max() <= 1e-2 * m, name
+
+
+def test_two_scans_in_flight_match_sequential():
+    """capture_pipeline (the serving loop with two scans in flight: indexing of scan i+1
+    on its own stream beside the convolutions of scan i, two network instances): with a
+    deterministic configuration (all-OS maps, no split-K atomics) every output equals the
+    sequential forward of the same scan bit for bit, for two different scans alternating."""
+    from paper_2511_20834_b200.network import capture_pipeline
+    scans = [synth.make_scan(1, 0)[:9000], synth.make_scan(1, 1)[:9000]]
+    allc = np.concatenate(scans)
+    spec = spc.spc_plan_pack(allc[:, 1:].min(0), allc[:, 1:].max(0), 1, 16, 16)
+    spc.spc_set_option(spc.SPC_OPT_CONV_OS_SPLIT, 0)
+    try:
+        mk = lambda: SparseNet(9000, spec, t_override={k: spc.SPC_T_ALL_OS for k in
+                                                       SparseNet(16, spec).map_keys})
+        nets = [mk(), mk()]
+        ins = []
+        for s in scans:
+            f = torch.zeros(s.shape[0], C_IN_PAD, dtype=torch.bfloat16, device="cuda")
+            f[:, :4] = torch.from_numpy(synth.make_features(s.shape[0], 4, seed=s.shape[0])).cuda().bfloat16()
+            ins.append((torch.from_numpy(s).cuda(), f))
+        refs = []
+        for c, f in ins:   # sequential reference, one scan at a time
+            refs.append(nets[0].forward(c, f).clone())
+        torch.cuda.synchronize()
+        for q in range(2):
+            nets[q].forward(*ins[q])
+        nets[0].forward(*ins[0])   # scan 0 indexed in instance 0 (the pipeline's fill)
+        torch.cuda.synchronize()
+        graphs = capture_pipeline(nets, ins, torch.device("cuda"), torch.cuda.current_stream())
+        nets[0].index_stage(*ins[0])
+        for i in range(4):           # step i: features of scan i % 2 in nets[i % 2]
+            graphs[i % 2].replay()
+            torch.cuda.synchronize()
+            assert torch.equal(nets[i % 2].bufs[nets[i % 2].out_name], refs[i % 2]), i
+    finally:
+        spc.spc_set_option(spc.SPC_OPT_CONV_OS_SPLIT, -1)
