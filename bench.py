@@ -579,8 +579,9 @@ def main():
             net2.forward(coords, feats, stream=stream)
         torch.cuda.synchronize()
         nets = [net, net2]
-        from paper_2511_20834_b200.network import capture_pipeline
-        pgraphs = capture_pipeline(nets, [(coords, feats), (coords, feats)], dev, stream)
+        from paper_2511_20834_b200.network import capture_pipeline, pipeline_index_after
+        pgraphs = capture_pipeline(nets, [(coords, feats), (coords, feats)], dev, stream,
+                                   index_after_layer=pipeline_index_after(net))
 
     def step(i=0):
         if pgraphs is not None:
@@ -698,8 +699,9 @@ def main():
                        "l2": "flushed (320 MB write) between timed steps; e2e: a 160 MB write before every forward",
                        "cuda_graph": graph is not None, "dataflow_t": {str(k): v for k, v in net.t.items()},
                        "pipeline": ("two scans in flight: the voxel indexing of scan i+1 (its own stream and "
-                                    "network instance) overlaps the feature computation of scan i; every step "
-                                    "indexes one scan and convolves one scan") if pgraphs is not None else
+                                    "network instance) overlaps the feature computation of scan i, starting when "
+                                    "the convolutions reach the deepest level; every step indexes one scan and "
+                                    "convolves one scan") if pgraphs is not None else
                                    "one scan at a time",
                        "pack_spec": list(spec.astuple())},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -908,8 +910,8 @@ def end_to_end_pipelined(nets, coords_np, feats_np, dev, stream, steps, flush):
         f.copy_(h_feats)
     outs = [nt.bufs[nt.out_name] for nt in nets]
     h_out = [torch.empty(outs[0].shape, dtype=outs[0].dtype).pin_memory() for _ in range(2)]
-    from paper_2511_20834_b200.network import capture_pipeline
-    graphs = capture_pipeline(nets, land, dev, stream)
+    from paper_2511_20834_b200.network import capture_pipeline, pipeline_index_after
+    graphs = capture_pipeline(nets, land, dev, stream, index_after_layer=pipeline_index_after(nets[0]))
     fl = flush[:160 * 2 ** 20]
     cs_in, cs_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
     total = steps + 2

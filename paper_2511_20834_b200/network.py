@@ -328,15 +328,17 @@ class SparseNet:
         spc.spc_gather_rows(feats, self.perm[:n], out=self.bufs["x0"][:n], n_dev=n_live, stream=stream)
         self.index(stream, n_dev=n_live)
 
-    def conv_stage(self, stream=None) -> torch.Tensor:
+    def conv_stage(self, stream=None, marks=None) -> torch.Tensor:
         """The feature-computation half of forward(): every layer on the maps of the last
-        index_stage()."""
+        index_stage().  marks: {layer index: event} recorded on `stream` after that layer."""
         try:
             for i in range(len(self.layers)):
                 # after the first layer the maps and weights are long complete when the
                 # preceding kernel starts: let each layer decode tiles early (PDL)
                 spc.spc_set_option(spc.SPC_OPT_CONV_MAPS_READY, 1 if (i > 0 and self.early_maps) else 0)
                 self.conv(i, stream)
+                if marks and i in marks:
+                    marks[i].record(stream)
         finally:
             spc.spc_set_option(spc.SPC_OPT_CONV_MAPS_READY, 0)
         return self.bufs[self.out_name]
@@ -486,11 +488,28 @@ class SparseNet:
         return {mk: self.nnz[mk] / max(1, self.live_n[mk][1]) for mk in self.maps}
 
 
-def capture_pipeline(nets, inputs, dev, stream):
+def pipeline_index_after(net) -> int:
+    """The layer after which a pipelined step starts indexing the next scan: the first layer
+    writing the deepest level, so the latency-bound indexing kernels overlap the small
+    levels' latency-bound convolutions instead of the large levels' saturating ones (C2
+    sweep of the start layer: 1.366 ms from the step start, 1.335 ms after the first
+    deepest-level layer, 1.397 ms six layers later; scripts/pipeline_probe.py)."""
+    deepest = max(s.level_out for s in net.layers)
+    first = next(i for i, s in enumerate(net.layers) if s.level_out == deepest)
+    # ... unless the deepest level is the network's tail (SECOND: 5 of 21 layers), where the
+    # indexing would outlast the convolutions left (C3: 944 scans/s from the step start vs
+    # 870 from its deepest level)
+    return first if len(net.layers) - first >= 0.4 * len(net.layers) else -1
+
+
+def capture_pipeline(nets, inputs, dev, stream, index_priority: int = 0, conv_priority: int = 0,
+                     index_after_layer: int = -1):
     """Two CUDA graphs of a pipelined step: graph p runs nets[p].conv_stage (features of the
     scan nets[p] indexed in the previous step) on one stream and nets[1-p].index_stage on
     inputs[1-p] (the next scan) on another, forked from and joined into the capture stream."""
-    s0, s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    s0 = torch.cuda.Stream(dev)
+    s1 = torch.cuda.Stream(dev, priority=conv_priority)    # (< 0: higher scheduling priority)
+    s2 = torch.cuda.Stream(dev, priority=index_priority)
     s0.wait_stream(stream)
     graphs = []
     for p in range(2):
@@ -500,8 +519,11 @@ def capture_pipeline(nets, inputs, dev, stream):
             fork.record(s0)
             s1.wait_event(fork)
             s2.wait_event(fork)
+            mark = torch.cuda.Event() if index_after_layer >= 0 else None
             with torch.cuda.stream(s1):
-                nets[p].conv_stage(s1)
+                nets[p].conv_stage(s1, marks={index_after_layer: mark} if mark is not None else None)
+            if mark is not None:   # start the indexing once the convolutions reach the small levels
+                s2.wait_event(mark)
             with torch.cuda.stream(s2):
                 c, f = inputs[1 - p]
                 nets[1 - p].index_stage(c, f, s2)

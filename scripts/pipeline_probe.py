@@ -34,7 +34,10 @@ def timed(replays, flush, n=40):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=2)
-    ap.add_argument("--caps", type=int, nargs="+", default=[0, 144, 140, 136])
+    ap.add_argument("--caps", type=int, nargs="+", default=[0])
+    ap.add_argument("--prios", type=int, nargs="+", default=[0],
+                    help="conv-stream priorities (< 0 = higher); the indexing stream stays at 0")
+    ap.add_argument("--afters", type=int, nargs="+", default=[-1, 5, 9, 13, 19, 25])
     args = ap.parse_args()
     dev = torch.device("cuda")
     coords_np, feats_np, _, net_name = bench.workload(0, args.config)
@@ -66,31 +69,18 @@ def main():
     torch.cuda.synchronize()
     # fp32 atomics in the weight-stationary layers: runs agree to rounding, not bit-for-bit
     res["sequential_run_to_run_maxdiff"] = float((nets[0].bufs[nets[0].out_name].float() - ref).abs().max())
+    from paper_2511_20834_b200.network import capture_pipeline  # noqa: F811
     for cap in args.caps:
-        graphs = []
-        for p in range(2):
-            gp = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(gp, stream=s0):
-                e0 = torch.cuda.Event()
-                e0.record(s0)
-                s1.wait_event(e0)
-                s2.wait_event(e0)
+        for prio in args.prios:
+            for after in args.afters:
                 spc.spc_set_option(spc.SPC_OPT_CONV_MAX_CTAS, cap)
-                with torch.cuda.stream(s1):
-                    nets[p].conv_stage(s1)
+                graphs = capture_pipeline(nets, [(coords, feats), (coords, feats)], dev, torch.cuda.current_stream(),
+                                          conv_priority=prio, index_after_layer=after)
                 spc.spc_set_option(spc.SPC_OPT_CONV_MAX_CTAS, -1)
-                with torch.cuda.stream(s2):
-                    nets[1 - p].index_stage(coords, feats, s2)
-                e1, e2 = torch.cuda.Event(), torch.cuda.Event()
-                e1.record(s1)
-                e2.record(s2)
-                s0.wait_event(e1)
-                s0.wait_event(e2)
-            torch.cuda.synchronize()
-            graphs.append(gp)
-        res[f"pipelined_ms_cap{cap}"] = timed(graphs, flush)
-        d = max(float((nets[q].bufs[nets[q].out_name].float() - ref).abs().max()) for q in range(2))
-        res[f"maxdiff_cap{cap}"] = d
+                key = f"cap{cap}_prio{prio}_after{after}"
+                res["ms_" + key] = timed(graphs, flush)
+                res["maxdiff_" + key] = max(float((nets[q].bufs[nets[q].out_name].float() - ref).abs().max())
+                                            for q in range(2))
     print(json.dumps({"config": args.config, "n": int(coords_np.shape[0]), **res}))
 
 
