@@ -196,6 +196,7 @@ class SparseNet:
         self.density_order = bool(density_order)
         self.order_max_ts = 1 << 30   # density-order only maps whose fine tensor stride is <= this
         self.early_maps = True   # layers >= 1 start their tile decode during the previous layer
+        self.overlap_proj = True   # ResBlock 1x1 projections on a side stream beside conv1 (+1.7% C2)
         self.spec = spec
         self.n0 = int(n0_cap)
         if net in ("minkunet42", "minkunet42_k2"):
@@ -319,6 +320,11 @@ class SparseNet:
         self.index_stage(coords, feats, stream, n_live)
         return self.conv_stage(stream)
 
+    def _side_stream(self):
+        if getattr(self, "_side", None) is None:
+            self._side = torch.cuda.Stream(self.dev)
+        return self._side
+
     def index_stage(self, coords: torch.Tensor, feats: torch.Tensor, stream=None, n_live=None):
         """The voxel-indexing half of forward(): pack + sort, feature row gather, every
         level and every kernel map (n_live: as in forward, already filled)."""
@@ -331,8 +337,32 @@ class SparseNet:
     def conv_stage(self, stream=None, marks=None) -> torch.Tensor:
         """The feature-computation half of forward(): every layer on the maps of the last
         index_stage().  marks: {layer index: event} recorded on `stream` after that layer."""
+        side = self._side_stream() if self.overlap_proj else None
+        st = stream if stream is not None else torch.cuda.current_stream(self.dev)
+        pending = {}    # layer index -> event of a 1x1 projection running on the side stream
+        issued = set()  # projections already issued on the side stream
         try:
             for i in range(len(self.layers)):
+                s = self.layers[i]
+                if i in issued:
+                    continue
+                if side is not None and i + 1 < len(self.layers):
+                    nx = self.layers[i + 1]
+                    if nx.map_key[0] == 1 and nx.src == s.src and nx.src_col == s.src_col:
+                        # a ResBlock's 1x1 projection reads the block input like conv1: run it on
+                        # the side stream beside conv1; conv2 (its residual reader) waits for it
+                        fork = torch.cuda.Event()
+                        fork.record(st)
+                        side.wait_event(fork)
+                        with torch.cuda.stream(side):
+                            spc.spc_set_option(spc.SPC_OPT_CONV_MAPS_READY, 0)
+                            self.conv(i + 1, side)
+                        done = torch.cuda.Event()
+                        done.record(side)
+                        pending[i + 2] = done
+                        issued.add(i + 1)
+                if i in pending:
+                    st.wait_event(pending.pop(i))
                 # after the first layer the maps and weights are long complete when the
                 # preceding kernel starts: let each layer decode tiles early (PDL)
                 spc.spc_set_option(spc.SPC_OPT_CONV_MAPS_READY, 1 if (i > 0 and self.early_maps) else 0)

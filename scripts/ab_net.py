@@ -28,6 +28,8 @@ for rnd in range(3):
         net.set_t(t_map)
         if k == "early_maps":
             net.early_maps = bool(int(v))
+        elif k == "overlap_proj":
+            net.overlap_proj = bool(int(v))
         elif k == "order_max_ts":
             net.order_max_ts = int(v)
             net.density_order = int(v) > 0
@@ -52,7 +54,7 @@ for rnd in range(3):
             torch.cuda.synchronize()
             ts.append(a.elapsed_time(b))
         results.setdefault(arg, []).append(float(np.median(ts[5:])))
-        if k not in ("early_maps", "order_max_ts"):
+        if k not in ("early_maps", "order_max_ts", "overlap_proj"):
             spc.spc_set_option(getattr(spc, "SPC_OPT_" + k), -1)
         del g, net
 for k, v in results.items():
