@@ -197,6 +197,7 @@ class SparseNet:
         self.order_max_ts = 1 << 30   # density-order only maps whose fine tensor stride is <= this
         self.early_maps = True   # layers >= 1 start their tile decode during the previous layer
         self.overlap_proj = True   # ResBlock 1x1 projections on a side stream beside conv1 (+1.7% C2)
+        self.overlap_wgrad = True  # backward: weight gradients on a side stream beside the data gradients
         self.spec = spec
         self.n0 = int(n0_cap)
         if net in ("minkunet42", "minkunet42_k2"):
@@ -392,8 +393,24 @@ class SparseNet:
                 w.zero_()
             if grad_out is not None:
                 self.gbufs[self.out_name][: grad_out.shape[0]].copy_(grad_out)
+        side = self._side_stream() if self.overlap_wgrad else None
         for i in reversed(range(len(self.layers))):
-            self.backward_layer(i, stream)
+            if side is not None:
+                # layer i's output gradient is final here (every reader came later in the
+                # forward, so earlier here) and nothing in the backward writes it again: its
+                # weight gradient runs on the side stream beside the data gradients
+                ready = torch.cuda.Event()
+                ready.record(st)
+                side.wait_event(ready)
+                with torch.cuda.stream(side):
+                    self.backward_layer(i, side, parts=("wgrad",))
+                self.backward_layer(i, stream, parts=("residual", "dgrad"))
+            else:
+                self.backward_layer(i, stream)
+        if side is not None:
+            done = torch.cuda.Event()
+            done.record(side)
+            st.wait_event(done)
         return self.dW
 
     def _first_touch(self):
@@ -447,18 +464,19 @@ class SparseNet:
         self._plan = {"zero": sorted(zero), "res": first_res, "dgrad": first_dgrad}
         return self._plan
 
-    def backward_layer(self, i, stream=None):
+    def backward_layer(self, i, stream=None, parts=("wgrad", "residual", "dgrad")):
         s = self.layers[i]
         plan = self._first_touch()
         g = self.gbufs[s.dst][:, s.dst_col:s.dst_col + s.c_out]
         src = self.bufs[s.src][:, s.src_col:s.src_col + s.c_in]
-        spc.spc_conv_wgrad(self.maps[wgrad_map_key(s.map_key)], src, g, s.c_in, s.c_out, d_weight=self.dW[i],
-                           stream=stream)
-        if s.residual is not None:
+        if "wgrad" in parts:
+            spc.spc_conv_wgrad(self.maps[wgrad_map_key(s.map_key)], src, g, s.c_in, s.c_out, d_weight=self.dW[i],
+                               stream=stream)
+        if "residual" in parts and s.residual is not None:
             rb, rc = s.residual
             spc.spc_add_rows(self.gbufs[rb][:, rc:rc + s.c_out], g, stream=stream, accumulate=not plan["res"][i],
                              n_dev=self.level_n[s.level_out:s.level_out + 1])
-        if i > 0:
+        if "dgrad" in parts and i > 0:
             gsrc = self.gbufs[s.src][:, s.src_col:s.src_col + s.c_in]
             first = plan["dgrad"][i]
             spc.spc_conv_forward(self.maps[dgrad_map_key(s.map_key)], g, self.dgrad_weights[i], s.c_out, s.c_in,
