@@ -103,6 +103,13 @@ def workload(rank: int, config: int = CONFIG_ID, world: int = 1, scan_offset: in
     return coords, feats, 1, ("secondk5" if config == 3 else "minkunet42")
 
 
+def pipeline_split(net) -> int:
+    """Layer at which a three-deep pipeline splits a scan's convolutions: 45% of the layer
+    list (C2 sweep: split 19 / 22 / 25 / 28 / 31 -> 1.256 / 1.227 / 1.241 / 1.232 / 1.267 ms,
+    scripts/pipeline_probe.py)."""
+    return max(1, int(round(0.45 * len(net.layers))))
+
+
 def spec_for(coords):
     import paper_2511_20834_b200 as spc
     return spc.spc_plan_pack(coords[:, 1:].min(0), coords[:, 1:].max(0), int(coords[:, 0].max()) + 1, 16, 16)
@@ -571,21 +578,42 @@ def main():
     # ---- two scans in flight: a second network instance (same weights, maps, t) so that
     # step i computes the features of scan i on one stream while the voxel indexing of scan
     # i+1 runs on another; two graphs alternate the instances -------------------------------
-    nets, pgraphs = [net], None
+    nets, pgraphs, depth, split = [net], None, 1, None
+    pipe_trials = {}
     if graph is not None and not args.no_pipeline:
-        net2 = SparseNet(n, spec, device=dev, net=net_name, density_order=not args.no_order)
-        net2.set_t(dict(net.t))
-        for _ in range(3):
-            net2.forward(coords, feats, stream=stream)
+        from paper_2511_20834_b200.network import capture_pipeline, capture_pipeline3, pipeline_index_after
+        for _ in range(2):
+            nt = SparseNet(n, spec, device=dev, net=net_name, density_order=not args.no_order)
+            nt.set_t(dict(net.t))
+            for _ in range(3):
+                nt.forward(coords, feats, stream=stream)
+            nets.append(nt)
         torch.cuda.synchronize()
-        nets = [net, net2]
-        from paper_2511_20834_b200.network import capture_pipeline, pipeline_index_after
-        pgraphs = capture_pipeline(nets, [(coords, feats), (coords, feats)], dev, stream,
-                                   index_after_layer=pipeline_index_after(net))
+        split = pipeline_split(net)
+        cand = {2: capture_pipeline(nets[:2], [(coords, feats)] * 2, dev, stream,
+                                    index_after_layer=pipeline_index_after(net)),
+                3: capture_pipeline3(nets, [(coords, feats)] * 3, dev, stream, split)}
+        # one-time choice of the pipeline depth (like the dataflow t): 30 flushed steps each
+        probe_flush = torch.empty(320 * 2 ** 20, dtype=torch.uint8, device=dev)
+        for d, gs in cand.items():
+            ts = []
+            for i in range(30):
+                probe_flush.fill_(i & 0xFF)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                gs[i % d].replay()
+                b.record(stream)
+                torch.cuda.synchronize()
+                ts.append(a.elapsed_time(b))
+            pipe_trials[d] = float(np.median(ts[3:]))
+        del probe_flush
+        depth = min(pipe_trials, key=pipe_trials.get)
+        pgraphs = cand[depth]
+        nets = nets[:depth]
 
     def step(i=0):
         if pgraphs is not None:
-            pgraphs[i % 2].replay()
+            pgraphs[i % depth].replay()
         elif graph is not None:
             graph.replay()
         else:
@@ -675,7 +703,7 @@ def main():
     # ---- end to end through the public API: pinned host in -> device -> pinned host out --
     # every rank runs its own pipelined loop; the job's time is the slowest rank's
     if pgraphs is not None:
-        e2e = end_to_end_pipelined(nets, coords_np, feats_np, dev, stream, args.steps, flush)
+        e2e = end_to_end_pipelined(nets, coords_np, feats_np, dev, stream, args.steps, flush, split)
     else:
         e2e = end_to_end(net, coords_np, feats_np, dev, stream, args.steps, flush, graph, coords, feats)
     e2e_s = e2e["seconds"]
@@ -698,11 +726,14 @@ def main():
                        "parallelism": f"scan-sharded x{world}",
                        "l2": "flushed (320 MB write) between timed steps; e2e: a 160 MB write before every forward",
                        "cuda_graph": graph is not None, "dataflow_t": {str(k): v for k, v in net.t.items()},
-                       "pipeline": ("two scans in flight: the voxel indexing of scan i+1 (its own stream and "
-                                    "network instance) overlaps the feature computation of scan i, starting when "
-                                    "the convolutions reach the deepest level; every step indexes one scan and "
-                                    "convolves one scan") if pgraphs is not None else
-                                   "one scan at a time",
+                       "pipeline": ({2: "two scans in flight: the voxel indexing of scan i+1 (its own stream "
+                                        "and network instance) beside the feature computation of scan i",
+                                     3: f"three scans in flight: layers [{split}, end) of scan i, layers "
+                                        f"[0, {split}) of scan i+1 and the voxel indexing of scan i+2, each on its "
+                                        "own stream and network instance"}[depth] +
+                                    "; every step indexes one scan and convolves one scan; depth chosen once "
+                                    f"from 30 flushed steps each (ms/step {pipe_trials})") if pgraphs is not None
+                                   else "one scan at a time",
                        "pack_spec": list(spec.astuple())},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak,
@@ -889,73 +920,79 @@ def top_kernel_share(launches):
                    for k, v in dur.items()], key=lambda r: -r["share"])[:6]
 
 
-def end_to_end_pipelined(nets, coords_np, feats_np, dev, stream, steps, flush):
-    """The public-API serving loop with two scans in flight: every step copies one scan's
-    coords + features from pinned host memory, indexes it (nets[(i+1) % 2].index_stage) while
-    the previous scan's features are computed (nets[i % 2].conv_stage), and reads that scan's
-    output back to pinned host memory.  Copies run on their own streams, double-buffered
-    (landing buffers per instance; each instance's own output buffer is read directly); L2
-    flushed (a 160 MB write) before every step; timed from the first host->device copy to the
-    last device->host copy."""
+def end_to_end_pipelined(nets, coords_np, feats_np, dev, stream, steps, flush, split=None):
+    """The public-API serving loop with len(nets) = D scans in flight (D = 2: the next scan's
+    indexing beside this scan's features; D = 3: this scan's layers [split, end), the next
+    scan's layers [0, split) and the indexing of the one after, network.capture_pipeline /
+    capture_pipeline3): every step copies one scan's coords + features from pinned host
+    memory (landing buffers per instance), indexes it, and reads one finished scan's output
+    (each instance's own output buffer) back to pinned host memory.  Copies on their own
+    streams; L2 flushed (a 160 MB write) before every step; timed from the first
+    host->device copy to the last device->host copy, after D pipeline-fill steps."""
     import torch
-    from paper_2511_20834_b200.network import C_IN_PAD
+    from paper_2511_20834_b200.network import C_IN_PAD, capture_pipeline, capture_pipeline3, pipeline_index_after
+    D = len(nets)
     n = coords_np.shape[0]
     h_coords = torch.from_numpy(coords_np).pin_memory()
     f16 = np.zeros((n, C_IN_PAD), np.float32)
     f16[:, :feats_np.shape[1]] = feats_np
     h_feats = torch.from_numpy(f16).to(torch.bfloat16).pin_memory()
-    land = [(torch.empty_like(h_coords, device=dev), torch.empty_like(h_feats, device=dev)) for _ in range(2)]
+    land = [(torch.empty_like(h_coords, device=dev), torch.empty_like(h_feats, device=dev)) for _ in range(D)]
     for c, f in land:
         c.copy_(h_coords)
         f.copy_(h_feats)
     outs = [nt.bufs[nt.out_name] for nt in nets]
-    h_out = [torch.empty(outs[0].shape, dtype=outs[0].dtype).pin_memory() for _ in range(2)]
-    from paper_2511_20834_b200.network import capture_pipeline, pipeline_index_after
-    graphs = capture_pipeline(nets, land, dev, stream, index_after_layer=pipeline_index_after(nets[0]))
+    h_out = [torch.empty(outs[0].shape, dtype=outs[0].dtype).pin_memory() for _ in range(D)]
+    graphs = (capture_pipeline(nets, land, dev, stream, index_after_layer=pipeline_index_after(nets[0])) if D == 2
+              else capture_pipeline3(nets, land, dev, stream, split))
     fl = flush[:160 * 2 ** 20]
     cs_in, cs_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-    total = steps + 2
+    total = steps + D
     ev = lambda: torch.cuda.Event()
-    h2d_done = [ev() for _ in range(total + 2)]
+    h2d_done = [ev() for _ in range(total + D)]
     step_done = [ev() for _ in range(total)]
     d2h_done = [ev() for _ in range(total)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    fill_done = ev()
 
-    def h2d(j):   # scan j into land[j % 2] (read by the index stage of step j - 1)
+    def h2d(j):   # scan j into land[j % D]; it is indexed by step j - (D - 1)
         with torch.cuda.stream(cs_in):
-            if j >= 3:
-                cs_in.wait_event(step_done[j - 3])   # step j-3 indexed scan j-2 from this buffer
-            elif j == 2:
-                cs_in.wait_event(fill_done)          # the fill indexed scan 0 from this buffer
-            land[j % 2][0].copy_(h_coords, non_blocking=True)
-            land[j % 2][1].copy_(h_feats, non_blocking=True)
+            prev = j - 2 * D + 1                     # the step that indexed scan j - D from this buffer
+            if prev >= 0:
+                cs_in.wait_event(step_done[prev])
+            elif j >= D:
+                cs_in.wait_event(fill_done)
+            land[j % D][0].copy_(h_coords, non_blocking=True)
+            land[j % D][1].copy_(h_feats, non_blocking=True)
             h2d_done[j].record(cs_in)
 
-    def d2h(i):   # scan i's output, computed by step i in nets[i % 2]
+    def d2h(i):   # scan i finishes in step i, in nets[i % D]
         with torch.cuda.stream(cs_out):
             cs_out.wait_event(step_done[i])
-            h_out[i % 2].copy_(outs[i % 2], non_blocking=True)
+            h_out[i % D].copy_(outs[i % D], non_blocking=True)
             d2h_done[i].record(cs_out)
 
     torch.cuda.synchronize()
-    # pipeline fill: scan 0 indexed outside the loop (eagerly, from its landing buffer)
-    h2d(0)
-    h2d(1)
-    stream.wait_event(h2d_done[0])
-    nets[0].index_stage(land[0][0], land[0][1], stream)
-    fill_done = ev()
+    # pipeline fill: scans 0 .. D-2 indexed (and, for D = 3, scan 0's first layers) eagerly
+    for j in range(D):
+        h2d(j)
+    for j in range(D - 1):
+        stream.wait_event(h2d_done[j])
+        nets[j].index_stage(land[j][0], land[j][1], stream)
+    if D == 3:
+        nets[0].conv_stage(stream, stop=split)
     fill_done.record(stream)
     for i in range(total):
-        if i == 2:                                    # two pipeline-fill steps are not timed
+        if i == D:                                    # D pipeline-fill steps are not timed
             torch.cuda.synchronize()
             t0.record(cs_in)
-        h2d(i + 2)
-        stream.wait_event(h2d_done[i + 1])            # the scan this step indexes has landed
-        if i >= 2:
-            stream.wait_event(d2h_done[i - 2])        # this instance's output was read out
+        h2d(i + D)
+        stream.wait_event(h2d_done[i + D - 1])        # the scan this step indexes has landed
+        if i >= D:
+            stream.wait_event(d2h_done[i - D])        # this instance's output was read out
         with torch.cuda.stream(stream):
             fl.fill_(i & 0xFF)
-            graphs[i % 2].replay()
+            graphs[i % D].replay()
             step_done[i].record(stream)
         d2h(i)
     t1.record(cs_out)

@@ -335,19 +335,21 @@ class SparseNet:
         spc.spc_gather_rows(feats, self.perm[:n], out=self.bufs["x0"][:n], n_dev=n_live, stream=stream)
         self.index(stream, n_dev=n_live)
 
-    def conv_stage(self, stream=None, marks=None) -> torch.Tensor:
-        """The feature-computation half of forward(): every layer on the maps of the last
-        index_stage().  marks: {layer index: event} recorded on `stream` after that layer."""
+    def conv_stage(self, stream=None, marks=None, start: int = 0, stop: int | None = None) -> torch.Tensor:
+        """The feature-computation half of forward(): layers [start, stop) (default all) on
+        the maps of the last index_stage().  marks: {layer index: event} recorded on
+        `stream` after that layer."""
         side = self._side_stream() if self.overlap_proj else None
         st = stream if stream is not None else torch.cuda.current_stream(self.dev)
         pending = {}    # layer index -> event of a 1x1 projection running on the side stream
         issued = set()  # projections already issued on the side stream
+        stop = len(self.layers) if stop is None else stop
         try:
-            for i in range(len(self.layers)):
+            for i in range(start, stop):
                 s = self.layers[i]
                 if i in issued:
                     continue
-                if side is not None and i + 1 < len(self.layers):
+                if side is not None and i + 2 < stop:
                     nx = self.layers[i + 1]
                     if nx.map_key[0] == 1 and nx.src == s.src and nx.src_col == s.src_col:
                         # a ResBlock's 1x1 projection reads the block input like conv1: run it on
@@ -366,7 +368,7 @@ class SparseNet:
                     st.wait_event(pending.pop(i))
                 # after the first layer the maps and weights are long complete when the
                 # preceding kernel starts: let each layer decode tiles early (PDL)
-                spc.spc_set_option(spc.SPC_OPT_CONV_MAPS_READY, 1 if (i > 0 and self.early_maps) else 0)
+                spc.spc_set_option(spc.SPC_OPT_CONV_MAPS_READY, 1 if (i > start and self.early_maps) else 0)
                 self.conv(i, stream)
                 if marks and i in marks:
                     marks[i].record(stream)
@@ -580,6 +582,37 @@ def capture_pipeline(nets, inputs, dev, stream, index_priority: int = 0, conv_pr
             j2.record(s2)
             s0.wait_event(j1)
             s0.wait_event(j2)
+        torch.cuda.synchronize()
+        graphs.append(g)
+    return graphs
+
+
+def capture_pipeline3(nets, inputs, dev, stream, split: int):
+    """Three scans in flight: graph p runs the layers [split, end) of nets[p] (scan i), the
+    layers [0, split) of nets[p+1] (scan i+1) and the voxel indexing of nets[p+2] on
+    inputs[p+2] (scan i+2), each on its own stream (three graphs, one per rotation)."""
+    s0 = torch.cuda.Stream(dev)
+    ss = [torch.cuda.Stream(dev) for _ in range(3)]
+    s0.wait_stream(stream)
+    graphs = []
+    for p in range(3):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s0):
+            fork = torch.cuda.Event()
+            fork.record(s0)
+            for s in ss:
+                s.wait_event(fork)
+            with torch.cuda.stream(ss[0]):
+                nets[p].conv_stage(ss[0], start=split)
+            with torch.cuda.stream(ss[1]):
+                nets[(p + 1) % 3].conv_stage(ss[1], stop=split)
+            with torch.cuda.stream(ss[2]):
+                c, f = inputs[(p + 2) % 3]
+                nets[(p + 2) % 3].index_stage(c, f, ss[2])
+            for s in ss:
+                j = torch.cuda.Event()
+                j.record(s)
+                s0.wait_event(j)
         torch.cuda.synchronize()
         graphs.append(g)
     return graphs

@@ -199,3 +199,40 @@ def test_two_scans_in_flight_match_sequential():
             assert torch.equal(nets[i % 2].bufs[nets[i % 2].out_name], refs[i % 2]), i
     finally:
         spc.spc_set_option(spc.SPC_OPT_CONV_OS_SPLIT, -1)
+
+
+def test_three_scans_in_flight_match_sequential():
+    """capture_pipeline3 (a scan's convolutions split at a layer: tail of scan i, head of
+    scan i+1 and indexing of scan i+2 on three streams, three instances): with the
+    deterministic configuration every output equals the sequential forward bit for bit."""
+    from paper_2511_20834_b200.network import capture_pipeline3
+    scans = [synth.make_scan(1, s)[:9000] for s in range(3)]
+    allc = np.concatenate(scans)
+    spec = spc.spc_plan_pack(allc[:, 1:].min(0), allc[:, 1:].max(0), 1, 16, 16)
+    spc.spc_set_option(spc.SPC_OPT_CONV_OS_SPLIT, 0)
+    try:
+        mk = lambda: SparseNet(9000, spec, t_override={k: spc.SPC_T_ALL_OS for k in
+                                                       SparseNet(16, spec).map_keys})
+        nets = [mk(), mk(), mk()]
+        ins = []
+        for s in scans:
+            f = torch.zeros(s.shape[0], C_IN_PAD, dtype=torch.bfloat16, device="cuda")
+            f[:, :4] = torch.from_numpy(synth.make_features(s.shape[0], 4, seed=s.shape[0])).cuda().bfloat16()
+            ins.append((torch.from_numpy(s).cuda(), f))
+        refs = [nets[0].forward(c, f).clone() for c, f in ins]
+        torch.cuda.synchronize()
+        for q in range(3):
+            nets[q].forward(*ins[q])
+        torch.cuda.synchronize()
+        split = 22
+        graphs = capture_pipeline3(nets, ins, torch.device("cuda"), torch.cuda.current_stream(), split)
+        # fill: scans 0 and 1 indexed, scan 0's first layers done
+        nets[0].index_stage(*ins[0])
+        nets[1].index_stage(*ins[1])
+        nets[0].conv_stage(stop=split)
+        for i in range(6):           # step i finishes scan i % 3 in nets[i % 3]
+            graphs[i % 3].replay()
+            torch.cuda.synchronize()
+            assert torch.equal(nets[i % 3].bufs[nets[i % 3].out_name], refs[i % 3]), i
+    finally:
+        spc.spc_set_option(spc.SPC_OPT_CONV_OS_SPLIT, -1)
