@@ -591,24 +591,36 @@ def capture_pipeline3(nets, inputs, dev, stream, split: int):
     """Three scans in flight: graph p runs the layers [split, end) of nets[p] (scan i), the
     layers [0, split) of nets[p+1] (scan i+1) and the voxel indexing of nets[p+2] on
     inputs[p+2] (scan i+2), each on its own stream (three graphs, one per rotation)."""
+    return capture_pipeline_n(nets, inputs, dev, stream, [split])
+
+
+def capture_pipeline_n(nets, inputs, dev, stream, splits):
+    """len(splits) + 2 scans in flight: a scan's convolutions are cut at `splits` into
+    S = len(splits) + 1 segments; graph p runs segment S-1-k of nets[(p+k) % D] for k < S
+    and the voxel indexing of nets[(p+S) % D] on inputs[(p+S) % D] (D = S + 1 instances),
+    each on its own stream: every step finishes one scan and indexes one."""
+    S = len(splits) + 1
+    D = S + 1
+    assert len(nets) == D and len(inputs) == D
+    bounds = [0] + list(splits) + [None]
     s0 = torch.cuda.Stream(dev)
-    ss = [torch.cuda.Stream(dev) for _ in range(3)]
+    ss = [torch.cuda.Stream(dev) for _ in range(D)]
     s0.wait_stream(stream)
     graphs = []
-    for p in range(3):
+    for p in range(D):
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=s0):
             fork = torch.cuda.Event()
             fork.record(s0)
             for s in ss:
                 s.wait_event(fork)
-            with torch.cuda.stream(ss[0]):
-                nets[p].conv_stage(ss[0], start=split)
-            with torch.cuda.stream(ss[1]):
-                nets[(p + 1) % 3].conv_stage(ss[1], stop=split)
-            with torch.cuda.stream(ss[2]):
-                c, f = inputs[(p + 2) % 3]
-                nets[(p + 2) % 3].index_stage(c, f, ss[2])
+            for k in range(S):
+                seg = S - 1 - k
+                with torch.cuda.stream(ss[k]):
+                    nets[(p + k) % D].conv_stage(ss[k], start=bounds[seg], stop=bounds[seg + 1])
+            with torch.cuda.stream(ss[S]):
+                c, f = inputs[(p + S) % D]
+                nets[(p + S) % D].index_stage(c, f, ss[S])
             for s in ss:
                 j = torch.cuda.Event()
                 j.record(s)

@@ -38,8 +38,8 @@ def main():
     ap.add_argument("--prios", type=int, nargs="+", default=[0],
                     help="conv-stream priorities (< 0 = higher); the indexing stream stays at 0")
     ap.add_argument("--afters", type=int, nargs="+", default=[19])
-    ap.add_argument("--splits", type=int, nargs="+", default=[7, 13, 19, 25],
-                    help="three scans in flight: layer where a scan's convolutions are split")
+    ap.add_argument("--splitsets", nargs="+", default=["22", "15,30", "13,26", "19,34", "10,25", "22,36"],
+                    help="comma-separated split layers (one: three scans in flight, two: four)")
     args = ap.parse_args()
     dev = torch.device("cuda")
     coords_np, feats_np, _, net_name = bench.workload(0, args.config)
@@ -83,20 +83,23 @@ def main():
                 res["ms_" + key] = timed(graphs, flush)
                 res["maxdiff_" + key] = max(float((nets[q].bufs[nets[q].out_name].float() - ref).abs().max())
                                             for q in range(2))
-    # three scans in flight
-    from paper_2511_20834_b200.network import capture_pipeline3
-    net3 = SparseNet(coords_np.shape[0], spec, net=net_name)
-    if t_map:
-        net3.set_t(t_map)
+    # three and four scans in flight
+    from paper_2511_20834_b200.network import capture_pipeline_n
+    extra = []
     for _ in range(2):
-        net3.forward(coords, feats)
+        nt = SparseNet(coords_np.shape[0], spec, net=net_name)
+        if t_map:
+            nt.set_t(t_map)
+        for _ in range(2):
+            nt.forward(coords, feats)
+        extra.append(nt)
     torch.cuda.synchronize()
-    nets3 = nets + [net3]
-    for split in args.splits:
-        graphs = capture_pipeline3(nets3, [(coords, feats)] * 3, dev, torch.cuda.current_stream(), split)
-        res[f"ms3_split{split}"] = timed(graphs, flush, n=60)
-        res[f"maxdiff3_split{split}"] = max(float((nets3[q].bufs[nets3[q].out_name].float() - ref).abs().max())
-                                             for q in range(3))
+    for sp in args.splitsets:
+        splits = [int(v) for v in sp.split(",")]
+        D = len(splits) + 2
+        nn = (nets + extra)[:D]
+        graphs = capture_pipeline_n(nn, [(coords, feats)] * D, dev, torch.cuda.current_stream(), splits)
+        res[f"ms_split{sp}"] = timed(graphs, flush, n=60)
     print(json.dumps({"config": args.config, "n": int(coords_np.shape[0]), **res}))
 
 
