@@ -38,6 +38,8 @@ def main():
     ap.add_argument("--prios", type=int, nargs="+", default=[0],
                     help="conv-stream priorities (< 0 = higher); the indexing stream stays at 0")
     ap.add_argument("--afters", type=int, nargs="+", default=[19])
+    ap.add_argument("--t-set", action="append", default=[],
+                    help="K,stride,ts,tr=t overrides on top of the tuned t (e.g. 3,1,8,0=4)")
     ap.add_argument("--splitsets", nargs="+", default=["22", "15,30", "13,26", "19,34", "10,25", "22,36"],
                     help="comma-separated split layers (one: three scans in flight, two: four)")
     args = ap.parse_args()
@@ -45,6 +47,10 @@ def main():
     coords_np, feats_np, _, net_name = bench.workload(0, args.config)
     spec = bench.spec_for(coords_np)
     t_map = bench.load_t(os.path.join(ROOT, "profiles", "r2_tuned_t_c2.json")) if args.config == 2 else None
+    for o in args.t_set:
+        k, v = o.split("=")
+        t_map = dict(t_map or {})
+        t_map[tuple(int(x) for x in k.split(","))] = int(v)
     nets = []
     for _ in range(2):
         net = SparseNet(coords_np.shape[0], spec, net=net_name)
