@@ -594,7 +594,7 @@ def capture_pipeline3(nets, inputs, dev, stream, split: int):
     return capture_pipeline_n(nets, inputs, dev, stream, [split])
 
 
-def capture_pipeline_n(nets, inputs, dev, stream, splits):
+def capture_pipeline_n(nets, inputs, dev, stream, splits, index_after_layer: int = -1):
     """len(splits) + 2 scans in flight: a scan's convolutions are cut at `splits` into
     S = len(splits) + 1 segments; graph p runs segment S-1-k of nets[(p+k) % D] for k < S
     and the voxel indexing of nets[(p+S) % D] on inputs[(p+S) % D] (D = S + 1 instances),
@@ -614,10 +614,18 @@ def capture_pipeline_n(nets, inputs, dev, stream, splits):
             fork.record(s0)
             for s in ss:
                 s.wait_event(fork)
+            mark = None
             for k in range(S):
                 seg = S - 1 - k
+                lo_, hi_ = bounds[seg], bounds[seg + 1]
+                marks = None
+                if index_after_layer >= lo_ and (hi_ is None or index_after_layer < hi_):
+                    mark = torch.cuda.Event()   # the indexing starts once this layer is done
+                    marks = {index_after_layer: mark}
                 with torch.cuda.stream(ss[k]):
-                    nets[(p + k) % D].conv_stage(ss[k], start=bounds[seg], stop=bounds[seg + 1])
+                    nets[(p + k) % D].conv_stage(ss[k], marks=marks, start=lo_, stop=hi_)
+            if mark is not None:
+                ss[S].wait_event(mark)
             with torch.cuda.stream(ss[S]):
                 c, f = inputs[(p + S) % D]
                 nets[(p + S) % D].index_stage(c, f, ss[S])

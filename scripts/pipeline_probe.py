@@ -38,6 +38,7 @@ def main():
     ap.add_argument("--prios", type=int, nargs="+", default=[0],
                     help="conv-stream priorities (< 0 = higher); the indexing stream stays at 0")
     ap.add_argument("--afters", type=int, nargs="+", default=[19])
+    ap.add_argument("--index-afters", type=int, nargs="+", default=[-1])
     ap.add_argument("--t-set", action="append", default=[],
                     help="K,stride,ts,tr=t overrides on top of the tuned t (e.g. 3,1,8,0=4)")
     ap.add_argument("--splitsets", nargs="+", default=["22", "15,30", "13,26", "19,34", "10,25", "22,36"],
@@ -104,8 +105,10 @@ def main():
         splits = [int(v) for v in sp.split(",")]
         D = len(splits) + 2
         nn = (nets + extra)[:D]
-        graphs = capture_pipeline_n(nn, [(coords, feats)] * D, dev, torch.cuda.current_stream(), splits)
-        res[f"ms_split{sp}"] = timed(graphs, flush, n=60)
+        for ia in args.index_afters:
+            graphs = capture_pipeline_n(nn, [(coords, feats)] * D, dev, torch.cuda.current_stream(), splits,
+                                        index_after_layer=ia)
+            res[f"ms_split{sp}_ia{ia}"] = timed(graphs, flush, n=60)
     print(json.dumps({"config": args.config, "n": int(coords_np.shape[0]), **res}))
 
 
