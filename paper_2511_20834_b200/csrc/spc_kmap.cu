@@ -560,7 +560,7 @@ __global__ void __launch_bounds__(256) k_kmap_bsearch(const __grid_constant__ Km
 // matched, to none), folded onto <= 16 bits.  All ordered maps of a build are sorted
 // together: key = map tag above the mask bits, rows concatenated by live counts.
 // ------------------------------------------------------------------------------------
-constexpr int ORD_MAX = 8;
+constexpr int ORD_MAX = 16;   // ordered maps per network build (tag bits: ceil(log2 n))
 struct OrderJob {
     const int32_t *os;
     int32_t *os_ord;
