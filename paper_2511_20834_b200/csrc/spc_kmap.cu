@@ -836,8 +836,19 @@ static spc_status make_plan(const spc_geom &g, int32_t t, uint32_t flags, KmapPl
             rank[k] = rank[m] = ncls++;
         }
         for (int c = 0; c < pl.k_dense; ++c) {
-            const int r = rank[pl.dense_k[c]];
-            pl.ord_cls[c] = (int8_t)(r < 0 ? -1 : r % 16);
+            const int k = pl.dense_k[c];
+            const int r = rank[k];
+            if (r < 0 || ncls <= 16) {
+                pl.ord_cls[c] = (int8_t)r;   // every direction pair its own bit (K = 3: 13)
+                continue;
+            }
+            // more pairs than bits (K = 5: 62): fold by geometry, not by index -- the axes
+            // the offset moves along (7 patterns) x inner / outer ring (|e|_inf 1 or 2): rows
+            // of one surface orientation share bits (r % 16 merged unrelated directions)
+            const int ex = k / (ks[1] * ks[2]) + pl.lo[0], ey = (k / ks[2]) % ks[1] + pl.lo[1], ez = k % ks[2] + pl.lo[2];
+            const int mask = (ex != 0) << 2 | (ey != 0) << 1 | (ez != 0);
+            const int linf = std::max(std::abs(ex), std::max(std::abs(ey), std::abs(ez)));
+            pl.ord_cls[c] = (int8_t)(mask == 0 ? -1 : (mask - 1) + 7 * (linf >= 2 ? 1 : 0));
         }
     }
     for (int gi = 0; gi < ks[0] * ks[1]; ++gi) {
