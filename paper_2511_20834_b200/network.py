@@ -546,7 +546,7 @@ def pipeline_index_after(net) -> int:
     deepest-level layer, 1.397 ms six layers later; scripts/pipeline_probe.py)."""
     deepest = max(s.level_out for s in net.layers)
     first = next(i for i, s in enumerate(net.layers) if s.level_out == deepest)
-    # ... unless the deepest level is the network's tail (SECOND: 5 of 21 layers), where the
+    # ... unless the deepest level is the network's tail (SECOND: 5 of 20 layers), where the
     # indexing would outlast the convolutions left (C3: 944 scans/s from the step start vs
     # 870 from its deepest level)
     return first if len(net.layers) - first >= 0.4 * len(net.layers) else -1
