@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--no-tune", action="store_true")
     ap.add_argument("--t-from", default=None, help="take the per-map dataflow t from a previous bench JSON line "
                                                    "(config.dataflow_t) instead of tuning")
+    ap.add_argument("--order-min-ts", type=int, default=0,
+                    help="density-order only maps whose fine tensor stride is >= this (default: all)")
     ap.add_argument("--save-t", default=None, help="write the tuned per-map dataflow t to this JSON file")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-order", action="store_true", help="kernel maps without the OS density order (ablation)")
@@ -523,6 +525,7 @@ def main():
     spec = spec_for(coords_np) if args.config != 4 else spc.spc_plan_pack(
         coords_np[:, 1:].min(0), coords_np[:, 1:].max(0), 8, 16, 16)
     net = SparseNet(n, spec, device=dev, net=net_name, density_order=not args.no_order)
+    net.order_min_ts = args.order_min_ts
     coords = torch.from_numpy(coords_np).to(dev)
     feats = torch.zeros(n, C_IN_PAD, dtype=torch.bfloat16, device=dev)
     feats[:, :feats_np.shape[1]] = torch.from_numpy(feats_np).to(dev, torch.bfloat16)
@@ -538,6 +541,7 @@ def main():
         tnet = SparseNet(tc_np.shape[0], spec_for(tc_np) if args.config != 4 else spc.spc_plan_pack(
             tc_np[:, 1:].min(0), tc_np[:, 1:].max(0), 8, 16, 16), device=dev, net=net_name,
             density_order=not args.no_order)
+        tnet.order_min_ts = args.order_min_ts
         tfeats = torch.zeros(tc_np.shape[0], C_IN_PAD, dtype=torch.bfloat16, device=dev)
         tfeats[:, :tf_np.shape[1]] = torch.from_numpy(tf_np).to(dev, torch.bfloat16)
         tuned = tune(tnet, torch.from_numpy(tc_np).to(dev), tfeats, stream)
@@ -584,6 +588,7 @@ def main():
         from paper_2511_20834_b200.network import capture_pipeline, capture_pipeline3, pipeline_index_after
         for _ in range(2):
             nt = SparseNet(n, spec, device=dev, net=net_name, density_order=not args.no_order)
+            nt.order_min_ts = args.order_min_ts
             nt.set_t(dict(net.t))
             for _ in range(3):
                 nt.forward(coords, feats, stream=stream)

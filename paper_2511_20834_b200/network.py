@@ -195,6 +195,7 @@ class SparseNet:
         self.dev = torch.device(device)
         self.density_order = bool(density_order)
         self.order_max_ts = 1 << 30   # density-order only maps whose fine tensor stride is <= this
+        self.order_min_ts = 0         # ... and >= this
         self.early_maps = True   # layers >= 1 start their tile decode during the previous layer
         self.overlap_proj = True   # ResBlock 1x1 projections on a side stream beside conv1 (+1.7% C2)
         self.overlap_wgrad = True  # backward: weight gradients on a side stream beside the data gradients
@@ -264,7 +265,7 @@ class SparseNet:
             t = self.t[mk] if len(mk) == 4 else 0   # wgrad maps: all weight-stationary
             ts.append(t)
             f = spc.SPC_KMAP_HALVE_SYMMETRIC if (stride == 1 and K > 1) else 0
-            if self.density_order and len(mk) == 4 and tsd <= self.order_max_ts:
+            if self.density_order and len(mk) == 4 and self.order_min_ts <= tsd <= self.order_max_ts:
                 f |= spc.SPC_KMAP_DENSITY_ORDER      # OS part only; ignored when t leaves no OS part
             flags.append(f)
         return geoms, ts, flags
