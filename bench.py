@@ -748,7 +748,7 @@ def main():
                                           f"({traffic['file']}; serialised, cold-cache)") if traffic else
                                          "no ncu capture for this config",
                          "algorithmic_bytes_per_step": alg_bytes,
-                         "kernel": "feature computation (k_conv_tc OS+WS launches, 49 layers)",
+                         "kernel": f"feature computation (k_conv_tc OS+WS launches, {len(net.layers)} layers)",
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst, measured)" if "bf16_tflops" in peaks
                          else "fallback 1.59 PFLOP/s (B200_PROFILING.md)",
                          "algorithmic_gflop_per_step": total_flop / 1e9, "conv_ms_per_step": conv_ms,
@@ -899,13 +899,23 @@ def per_layer_times(net, coords, feats, stream, flush, reps=5):
 
 
 def count_launches(net, coords, feats, stream):
-    """Kernels launched by one step (CUPTI via torch.profiler; names from libspc)."""
+    """Kernels launched by one step (CUPTI via torch.profiler; names from libspc).  The
+    profiled forward runs without programmatic dependent launches, so a kernel's duration
+    does not include the time its CTAs spent waiting for the predecessor (with PDL they start
+    early and a short kernel after a long one would show the long one's tail)."""
     import torch
     from torch.profiler import profile, ProfilerActivity
+    import paper_2511_20834_b200 as spc
     torch.cuda.synchronize()
-    with profile(activities=[ProfilerActivity.CUDA]) as prof:
-        net.forward(coords, feats, stream=stream)
+    spc.spc_set_option(spc.SPC_OPT_PDL, 0)
+    try:
+        net.forward(coords, feats, stream=stream)   # (maps of this pass: built without PDL too)
         torch.cuda.synchronize()
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            net.forward(coords, feats, stream=stream)
+            torch.cuda.synchronize()
+    finally:
+        spc.spc_set_option(spc.SPC_OPT_PDL, -1)
     by = {}
     dur = {}
     for e in prof.events():
