@@ -93,7 +93,10 @@ typedef enum {
                                    * 2 x (tiles x N-tiles) <= this (default 0: the SM count) */
     SPC_OPT_CONV_MAX_CTAS = 14,   /* > 0: the persistent feature kernels use at most this many
                                    * CTAs (one per SM), leaving SMs to a concurrent stream     */
-    SPC_OPT_COUNT = 15
+    SPC_OPT_CONV_BLK_KB = 15,     /* OS gather-index blocks: two in flight (the next tile's loads
+                                   * while this tile gathers) up to this many KB for both, beside
+                                   * a ring of >= 2 stages (default 128; 64: K = 5 keeps one)    */
+    SPC_OPT_COUNT = 16
 } spc_option;
 spc_status spc_set_option(int32_t option, int64_t value);
 int64_t spc_get_option(int32_t option);

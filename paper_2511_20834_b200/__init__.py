@@ -34,6 +34,7 @@ SPC_OPT_CONV_TILE_ROWS, SPC_OPT_CONV_STAGE_KB, SPC_OPT_CONV_OS_SPLIT, SPC_OPT_CO
 SPC_OPT_CONV_CLAIM_AHEAD, SPC_OPT_CONV_DENSITY_ORDER, SPC_OPT_PDL, SPC_OPT_KMAP_POOL_KEYS = 4, 5, 6, 7
 SPC_OPT_CONV_DENSE_CENTRE, SPC_OPT_CONV_CTA_PAIR, SPC_OPT_CONV_MAPS_READY, SPC_OPT_CONV_BULK_RED = 8, 9, 10, 11
 SPC_OPT_WGRAD_ITEMS_PER_SM, SPC_OPT_CONV_SPLIT_TILES, SPC_OPT_CONV_MAX_CTAS = 12, 13, 14
+SPC_OPT_CONV_BLK_KB = 15
 
 _DT = {torch.float32: SPC_F32, torch.float16: SPC_F16, torch.bfloat16: SPC_BF16}
 _TORCH_DT = {v: k for k, v in _DT.items()}

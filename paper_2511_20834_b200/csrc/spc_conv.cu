@@ -1425,11 +1425,7 @@ static spc_status launch_tc(const ConvParams &p0, int mode, int out_kind, void *
     p.ld_out = ld_out;
     const int kd = mode == 0 ? p.k_dense : 1;
     const size_t blk_bytes = (size_t)((p.bm * kd + 3) & ~3) * 4;
-    p.blk_slots = 2 * blk_bytes <= 64 * 1024 ? 2 : 1;
     const bool bulk_red = out_kind == OUT_F32_RED && p.BN % RED_COLS == 0 && option(SPC_OPT_CONV_BULK_RED) != 0;
-    const size_t header = align_up(sizeof(ConvSmem), 128) + (size_t)p.blk_slots * blk_bytes +
-                          (bulk_red ? RED_STAGE_BYTES : 0);
-    const size_t avail = TC_SMEM_BUDGET - 1024 - header;   // 1024: alignment slack of the dynamic smem base
     // slices (one BK-channel chunk of one offset) per pipeline stage: a stage carries up
     // to ~72 KB so narrow layers pack several offsets into one stage
     // default stage cap 72 KB; CTA pairs with 256-wide outputs default to 48 KB stages: a
@@ -1437,20 +1433,37 @@ static spc_status launch_tc(const ConvParams &p0, int mode, int out_kind, void *
     // of elapsed, 51.4% vs 49.2% of active cycles; profiles/r2_wide_256_256_pair_stage48.txt),
     // while 192-wide pairs lose 16% with it (110.6 vs 95.0 us)
     const int64_t skb = option(SPC_OPT_CONV_STAGE_KB);
-    const size_t stage_cap = (size_t)std::max<int64_t>(8, (p.cg == 2 && p.BN == 256 && skb == 72) ? 48 : skb) * 1024;
-    size_t ring_bytes = 0;
-    for (int g = 0; g < 2; ++g) {
-        const int rows = g == 0 ? p.bm : TC_BM;
-        ConvParams::Ring &R = p.ring[g];
-        const uint32_t kb_bl = p.kb_b / p.cg;   // this CTA's share of a weight tile
-        R.kb_a = (uint32_t)(rows * p.BK * 2);
-        R.nkb = (int)std::max<size_t>(1, std::min<size_t>(8, stage_cap / (R.kb_a + kb_bl)));
-        R.a_bytes = R.nkb * R.kb_a;
-        R.b_bytes = R.nkb * kb_bl;
-        R.stages = (int)std::min<size_t>(16, avail / (R.a_bytes + R.b_bytes));
-        if (R.stages < 2) return fail(SPC_ERR_UNSUPPORTED, "spc_conv_forward: tile does not fit shared memory");
-        ring_bytes = std::max(ring_bytes, (size_t)R.stages * (R.a_bytes + R.b_bytes));
-    }
+    const size_t stage_cap0 = (size_t)std::max<int64_t>(8, (p.cg == 2 && p.BN == 256 && skb == 72) ? 48 : skb) * 1024;
+    // carve the ring for `slots` index blocks; false when it gets fewer than min_stages
+    size_t ring_bytes = 0, header = 0;
+    auto carve = [&](int slots, size_t stage_cap, int min_stages) {
+        header = align_up(sizeof(ConvSmem), 128) + (size_t)slots * blk_bytes + (bulk_red ? RED_STAGE_BYTES : 0);
+        if (header + 1024 + 8 * 1024 > TC_SMEM_BUDGET) return false;
+        const size_t avail = TC_SMEM_BUDGET - 1024 - header;   // 1024: alignment slack of the dynamic smem base
+        ring_bytes = 0;
+        for (int g = 0; g < 2; ++g) {
+            const int rows = g == 0 ? p.bm : TC_BM;
+            ConvParams::Ring &R = p.ring[g];
+            const uint32_t kb_bl = p.kb_b / p.cg;   // this CTA's share of a weight tile
+            R.kb_a = (uint32_t)(rows * p.BK * 2);
+            R.nkb = (int)std::max<size_t>(1, std::min<size_t>(8, stage_cap / (R.kb_a + kb_bl)));
+            R.a_bytes = R.nkb * R.kb_a;
+            R.b_bytes = R.nkb * kb_bl;
+            R.stages = (int)std::min<size_t>(16, avail / (R.a_bytes + R.b_bytes));
+            if (R.stages < min_stages) return false;
+            ring_bytes = std::max(ring_bytes, (size_t)R.stages * (R.a_bytes + R.b_bytes));
+        }
+        p.blk_slots = slots;
+        return true;
+    };
+    // two index blocks (the next tile's indices load while this tile gathers) whenever they
+    // fit beside an unshrunk ring of >= 2 stages: large ones (K = 5 OS, 64 KB per 128-row
+    // tile) only on narrow layers (C3 level 0, 16 -> 16: 52.8 -> 48.9 us); shrinking the
+    // stages to make room loses (32 / 64 / 128 channels: +15% / +28% / +22%)
+    const size_t blk_cap = (size_t)std::max<int64_t>(0, option(SPC_OPT_CONV_BLK_KB)) * 1024;
+    bool ok = 2 * blk_bytes <= std::max<size_t>(blk_cap, 64 * 1024) && carve(2, stage_cap0, 2);
+    if (!ok) ok = carve(1, stage_cap0, 2);
+    if (!ok) return fail(SPC_ERR_UNSUPPORTED, "spc_conv_forward: tile does not fit shared memory");
     p.hdr_off = (uint32_t)align_up(ring_bytes, 128);
     p.red_off = bulk_red ? (uint32_t)(p.hdr_off + align_up(sizeof(ConvSmem), 128) + (size_t)p.blk_slots * blk_bytes) : 0u;
     const size_t smem = 1024 + p.hdr_off + header;

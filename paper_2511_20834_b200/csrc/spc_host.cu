@@ -25,8 +25,8 @@ spc_status cuda_fail(cudaError_t e, const char *what) {
 }
 
 // process-wide tuning options (spc_set_option); performance only
-static const int64_t kOptDefault[SPC_OPT_COUNT] = {0, 72, 1, 2, 1, 1, 1, 4096, 0, 1, 0, 1, 16, 0, 0};
-static int64_t g_opt[SPC_OPT_COUNT] = {0, 72, 1, 2, 1, 1, 1, 4096, 0, 1, 0, 1, 16, 0, 0};
+static const int64_t kOptDefault[SPC_OPT_COUNT] = {0, 72, 1, 2, 1, 1, 1, 4096, 0, 1, 0, 1, 16, 0, 0, 128};
+static int64_t g_opt[SPC_OPT_COUNT] = {0, 72, 1, 2, 1, 1, 1, 4096, 0, 1, 0, 1, 16, 0, 0, 128};
 
 static unsigned long long *g_trace_buf = nullptr;
 static int64_t g_trace_cap = 0;
