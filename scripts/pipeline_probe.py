@@ -41,13 +41,15 @@ def main():
     ap.add_argument("--index-afters", type=int, nargs="+", default=[-1])
     ap.add_argument("--t-set", action="append", default=[],
                     help="K,stride,ts,tr=t overrides on top of the tuned t (e.g. 3,1,8,0=4)")
+    ap.add_argument("--t-from", default=None, help="tuned t file (bench.py --save-t); default: C2's committed one")
     ap.add_argument("--splitsets", nargs="+", default=["22", "15,30", "13,26", "19,34", "10,25", "22,36"],
                     help="comma-separated split layers (one: three scans in flight, two: four)")
     args = ap.parse_args()
     dev = torch.device("cuda")
     coords_np, feats_np, _, net_name = bench.workload(0, args.config)
     spec = bench.spec_for(coords_np)
-    t_map = bench.load_t(os.path.join(ROOT, "profiles", "r2_tuned_t_c2.json")) if args.config == 2 else None
+    t_map = bench.load_t(args.t_from) if args.t_from else \
+        (bench.load_t(os.path.join(ROOT, "profiles", "r2_tuned_t_c2.json")) if args.config == 2 else None)
     for o in args.t_set:
         k, v = o.split("=")
         t_map = dict(t_map or {})
