@@ -28,7 +28,11 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--t-from", default=os.path.join(ROOT, "profiles", "r2_tuned_t_c2.json"))
+    ap.add_argument("--opt", action="append", default=[], help="NAME=VALUE spc_set_option (A/B runs)")
     args = ap.parse_args()
+    for o in args.opt:
+        k, v = o.split("=")
+        spc.spc_set_option(getattr(spc, "SPC_OPT_" + k), int(v))
     dev = torch.device("cuda:0")
     coords_np, feats_np, _, net_name = bench.workload(0, args.config)
     spec = bench.spec_for(coords_np)
