@@ -97,3 +97,23 @@ def test_pipeline_split_points():
     net2 = _Net(L2, {}, "out")
     assert nw.pipeline_index_after(net2) == -1   # the deepest level is the network's tail
     assert bench.pipeline_split(net2) == 9
+
+
+class _GeomNet:
+    def __init__(self, keys, lo, hi):
+        self.map_keys, self.t = keys, {k: 4 for k in keys}
+        self.density_order, self.order_min_ts, self.order_max_ts = True, lo, hi
+
+
+@pytest.mark.parametrize("lo,hi", [(0, 1 << 30), (2, 1 << 30), (0, 2), (4, 8)])
+def test_map_flags_follow_the_order_window(lo, hi):
+    """Per-map build flags: halving on submanifold K > 1 maps, the density order exactly on
+    the forward maps whose fine tensor stride lies in [order_min_ts, order_max_ts]."""
+    from paper_2511_20834_b200 import SPC_KMAP_DENSITY_ORDER, SPC_KMAP_HALVE_SYMMETRIC
+    L, _ = nw.minkunet42_layers(3)
+    keys = list(dict.fromkeys(s.map_key for s in L))
+    _, _, flags = nw.SparseNet._geoms(_GeomNet(keys, lo, hi))
+    for mk, f in zip(keys, flags):
+        K, stride, tsd, tr = mk
+        assert bool(f & SPC_KMAP_HALVE_SYMMETRIC) == (stride == 1 and K > 1), mk
+        assert bool(f & SPC_KMAP_DENSITY_ORDER) == (lo <= tsd <= hi), mk
