@@ -595,11 +595,26 @@ def capture_pipeline3(nets, inputs, dev, stream, split: int):
     return capture_pipeline_n(nets, inputs, dev, stream, [split])
 
 
-def capture_pipeline_n(nets, inputs, dev, stream, splits, index_after_layer: int = -1):
+def capture_pipeline_n(nets, inputs, dev, stream, splits, index_after_layer: int = -1,
+                       conv_max_ctas: int | None = None):
     """len(splits) + 2 scans in flight: a scan's convolutions are cut at `splits` into
     S = len(splits) + 1 segments; graph p runs segment S-1-k of nets[(p+k) % D] for k < S
     and the voxel indexing of nets[(p+S) % D] on inputs[(p+S) % D] (D = S + 1 instances),
-    each on its own stream: every step finishes one scan and indexes one."""
+    each on its own stream: every step finishes one scan and indexes one.
+    conv_max_ctas: CTAs of the persistent feature kernels (SPC_OPT_CONV_MAX_CTAS) while
+    capturing; None = SMs - 4, leaving a few SMs to the other streams' launches (C2 three in
+    flight: 1.231 -> 1.202 ms at 142-146; 140: 1.207, 128: 1.209, uncapped 1.231); 0 = all."""
+    if conv_max_ctas is None:
+        conv_max_ctas = torch.cuda.get_device_properties(dev).multi_processor_count - 4
+    prev = spc.spc_get_option(spc.SPC_OPT_CONV_MAX_CTAS)
+    spc.spc_set_option(spc.SPC_OPT_CONV_MAX_CTAS, max(0, int(conv_max_ctas)))
+    try:
+        return _capture_pipeline_n(nets, inputs, dev, stream, splits, index_after_layer)
+    finally:
+        spc.spc_set_option(spc.SPC_OPT_CONV_MAX_CTAS, prev)
+
+
+def _capture_pipeline_n(nets, inputs, dev, stream, splits, index_after_layer):
     S = len(splits) + 1
     D = S + 1
     assert len(nets) == D and len(inputs) == D
