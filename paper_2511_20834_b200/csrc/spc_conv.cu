@@ -1485,7 +1485,13 @@ static spc_status launch_tc(const ConvParams &p0, int mode, int out_kind, void *
                                         : (int64_t)num_sms();
     int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles_cap, num_sms()));
     const int64_t cap = option(SPC_OPT_CONV_MAX_CTAS);   // SMs left to a concurrent stream
-    if (cap > 0) grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid, cap));
+    if (cap > 0) {
+        grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid, cap));
+        // the device-side tile heuristics (split-K parts, 128 / 256-row tiles) count the CTAs
+        // that actually run: parts sized for 148 on a 140-CTA grid left a second wave
+        // (C2 three in flight with the tail capped at 140: 1.352 vs 1.203 ms)
+        p.num_sms = std::min(p.num_sms, grid);
+    }
     if (p.cg == 2) grid = 2 * std::max(1, std::min(grid, num_sms()) / 2);   // whole CTA pairs
     p.trace = trace_next(std::string("k_conv_tc ") + (mode == 0 ? "os" : "ws") + (p.cg == 2 ? " pair" : "") +
                          " n_out=" + std::to_string(p.n_out_cap) + " c_in=" + std::to_string(p.n_chunks * p.BK) +

@@ -606,15 +606,15 @@ def capture_pipeline_n(nets, inputs, dev, stream, splits, index_after_layer: int
     flight: 1.231 -> 1.202 ms at 142-146; 140: 1.207, 128: 1.209, uncapped 1.231); 0 = all."""
     if conv_max_ctas is None:
         conv_max_ctas = torch.cuda.get_device_properties(dev).multi_processor_count - 4
+    caps = list(conv_max_ctas) if isinstance(conv_max_ctas, (list, tuple)) else [conv_max_ctas] * (len(splits) + 1)
     prev = spc.spc_get_option(spc.SPC_OPT_CONV_MAX_CTAS)
-    spc.spc_set_option(spc.SPC_OPT_CONV_MAX_CTAS, max(0, int(conv_max_ctas)))
     try:
-        return _capture_pipeline_n(nets, inputs, dev, stream, splits, index_after_layer)
+        return _capture_pipeline_n(nets, inputs, dev, stream, splits, index_after_layer, caps)
     finally:
         spc.spc_set_option(spc.SPC_OPT_CONV_MAX_CTAS, prev)
 
 
-def _capture_pipeline_n(nets, inputs, dev, stream, splits, index_after_layer):
+def _capture_pipeline_n(nets, inputs, dev, stream, splits, index_after_layer, caps):
     S = len(splits) + 1
     D = S + 1
     assert len(nets) == D and len(inputs) == D
@@ -638,6 +638,7 @@ def _capture_pipeline_n(nets, inputs, dev, stream, splits, index_after_layer):
                 if index_after_layer >= lo_ and (hi_ is None or index_after_layer < hi_):
                     mark = torch.cuda.Event()   # the indexing starts once this layer is done
                     marks = {index_after_layer: mark}
+                spc.spc_set_option(spc.SPC_OPT_CONV_MAX_CTAS, max(0, int(caps[seg])))   # (segment seg's cap)
                 with torch.cuda.stream(ss[k]):
                     nets[(p + k) % D].conv_stage(ss[k], marks=marks, start=lo_, stop=hi_)
             if mark is not None:

@@ -41,8 +41,9 @@ def main():
     ap.add_argument("--index-afters", type=int, nargs="+", default=[-1])
     ap.add_argument("--t-set", action="append", default=[],
                     help="K,stride,ts,tr=t overrides on top of the tuned t (e.g. 3,1,8,0=4)")
-    ap.add_argument("--caps3", type=int, nargs="+", default=[0],
-                    help="SPC_OPT_CONV_MAX_CTAS while capturing the three- / four-deep pipelines")
+    ap.add_argument("--caps3", nargs="+", default=["0"],
+                    help="SPC_OPT_CONV_MAX_CTAS while capturing the three- / four-deep pipelines "
+                         "(one value, or comma-separated per segment)")
     ap.add_argument("--t-from", default=None, help="tuned t file (bench.py --save-t); default: C2's committed one")
     ap.add_argument("--splitsets", nargs="+", default=["22", "15,30", "13,26", "19,34", "10,25", "22,36"],
                     help="comma-separated split layers (one: three scans in flight, two: four)")
@@ -111,11 +112,10 @@ def main():
         nn = (nets + extra)[:D]
         for ia in args.index_afters:
             for cap in args.caps3:
-                spc.spc_set_option(spc.SPC_OPT_CONV_MAX_CTAS, cap)
+                cv = [int(x) for x in cap.split(",")]
                 graphs = capture_pipeline_n(nn, [(coords, feats)] * D, dev, torch.cuda.current_stream(), splits,
-                                            index_after_layer=ia)
-                spc.spc_set_option(spc.SPC_OPT_CONV_MAX_CTAS, -1)
-                res[f"ms_split{sp}_ia{ia}" + (f"_cap{cap}" if cap else "")] = timed(graphs, flush, n=60)
+                                            index_after_layer=ia, conv_max_ctas=cv if len(cv) > 1 else cv[0])
+                res[f"ms_split{sp}_ia{ia}_cap{cap}"] = timed(graphs, flush, n=60)
     print(json.dumps({"config": args.config, "n": int(coords_np.shape[0]), **res}))
 
 
