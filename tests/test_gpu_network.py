@@ -201,11 +201,13 @@ def test_two_scans_in_flight_match_sequential():
         spc.spc_set_option(spc.SPC_OPT_CONV_OS_SPLIT, -1)
 
 
-def test_three_scans_in_flight_match_sequential():
+@pytest.mark.parametrize("caps", [None, 0, 140, [144, 136]])
+def test_three_scans_in_flight_match_sequential(caps):
     """capture_pipeline3 (a scan's convolutions split at a layer: tail of scan i, head of
     scan i+1 and indexing of scan i+2 on three streams, three instances): with the
-    deterministic configuration every output equals the sequential forward bit for bit."""
-    from paper_2511_20834_b200.network import capture_pipeline3
+    deterministic configuration every output equals the sequential forward bit for bit,
+    with the default CTA cap (SMs - 4), none, and per-segment caps."""
+    from paper_2511_20834_b200.network import capture_pipeline_n
     scans = [synth.make_scan(1, s)[:9000] for s in range(3)]
     allc = np.concatenate(scans)
     spec = spc.spc_plan_pack(allc[:, 1:].min(0), allc[:, 1:].max(0), 1, 16, 16)
@@ -225,7 +227,9 @@ def test_three_scans_in_flight_match_sequential():
             nets[q].forward(*ins[q])
         torch.cuda.synchronize()
         split = 22
-        graphs = capture_pipeline3(nets, ins, torch.device("cuda"), torch.cuda.current_stream(), split)
+        graphs = capture_pipeline_n(nets, ins, torch.device("cuda"), torch.cuda.current_stream(), [split],
+                                    conv_max_ctas=caps)
+        assert spc.spc_get_option(spc.SPC_OPT_CONV_MAX_CTAS) == 0   # restored after the capture
         # fill: scans 0 and 1 indexed, scan 0's first layers done
         nets[0].index_stage(*ins[0])
         nets[1].index_stage(*ins[1])
